@@ -1,0 +1,426 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 generalized-ECDF / Laplacian-KDE hot path (BASELINE.json metric:
+"ECDF/Laplacian-KDE points/sec at 1/2/4/8 B200; % of HBM roofline").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg5|cfg5a|cfg5b|cfg3|cfg1|cfg2|cfg4]
+
+Default workload: BASELINE config 5 (the largest configuration that fits one GPU): N = 1e8
+points iid U[0,1]^4 on a 128^4 grid; one step = the 4-D grid ECDF (y == 1) followed by the
+Laplacian KDE (y ~ Exp(1), h = 0.05) on the same resident points.  Prints ONE JSON line on
+rank 0.  `value` is device throughput (points/s, inputs resident in HBM, CUDA events, max over
+ranks); `e2e` is the same metric through the public API from pinned host buffers with the H2D
+input copies and the D2H of the full result grids inside the timed region.
+
+--impl reference times the CPU restatement of the reference algorithm (oracle/, the reference
+itself is pure Python and cannot travel to the GPU box) on the host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import workloads as wl  # noqa: E402
+
+METRIC = "ECDF/Laplacian-KDE points/sec at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "points/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", default="cfg5")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------------------------------
+# clocks during the timed region
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.gpu)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["active", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names[1:], parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        med = float(np.median(sm)) if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+# workloads: algorithmic bytes per kernel launch (pass-structured)
+
+def grid_ecdf_bytes(n, d, m, unit=True):
+    L = int(np.prod(m))  # dead layers elided: lattice = output extents
+    e = 4 if unit else 8
+    return {
+        "lattice_zero": e * L,
+        "bin_scatter_count" if unit else "bin_scatter_w": 8 * n * d + (0 if unit else 8 * n) + 2 * e * n,
+        "scan_rows": 2 * e * L,
+        "scan_lines": 2 * e * L,
+        "scan_lines_final": e * L + 8 * L,
+    }
+
+
+def grid_kde_bytes(n, d, m, unit_w):
+    L = int(np.prod(m))
+    return {
+        "lattice_zero": 8 * L,
+        "bin_scatter_psi": 8 * n * d + (0 if unit_w else 8 * n) + 16 * n,
+        "scan_rows": 16 * L,
+        "scan_lines": 16 * L,
+        # first term only writes the accumulator; the other 2^d - 1 read and write it
+        "scan_lines_final": 8 * L + (8 * L + 16 * L * ((1 << d) - 1)) // (1 << d),
+        "kde_zfac": 16 * int(np.sum(m)),
+        "minmax": 8 * n * d,
+    }
+
+
+class GridWorkload:
+    """Grid configs (1, 3, 5a, 5b, 5): device-resident sample + public API calls."""
+
+    def __init__(self, name):
+        import paper_2005_03246_b200 as fcb
+
+        self.fcb = fcb
+        self.name = name
+        base = name[:4]
+        gen = {"cfg1": wl.cfg1, "cfg3": wl.cfg3, "cfg5": wl.cfg5}[base]
+        self.w = gen()
+        self.do_ecdf = name in ("cfg1", "cfg3", "cfg5", "cfg5a")
+        self.do_kde = name in ("cfg5", "cfg5b")
+        self.grid = fcb.RectilinearGrid.from_knots(self.w.knots)
+        self.n, self.d = self.w.n, self.w.d
+        self.m = self.grid.shape
+        self.delta = fcb.DeltaVector(self.w.delta)
+        self.bw = fcb.Bandwidth.diag(self.w.h) if self.w.h is not None else None
+        self.y = self.w.extra.get("y")
+
+    def describe(self):
+        parts = []
+        if self.do_ecdf:
+            parts.append(f"{self.d}-D grid ECDF y==1 delta={self.w.delta}")
+        if self.do_kde:
+            parts.append(f"{self.d}-D grid Laplacian KDE y~Exp(1) h={float(self.w.h[0])}")
+        return {
+            "workload": self.name,
+            "what": " + ".join(parts),
+            "n_points": self.n, "dims": self.d, "grid": "x".join(str(v) for v in self.m),
+            "lattice_cells": int(np.prod(self.m)),
+            "l2": f"inputs larger than L2 ({self.n * self.d * 8 / 1e9:.2f} GB points)"
+            if self.n * self.d * 8 > 126e6 else "L2-resident (launch-bound config)",
+        }
+
+    def to_device(self):
+        import torch
+
+        fcb = self.fcb
+        x = torch.from_numpy(self.w.points).cuda()
+        self.s_unit = fcb.Sample(x, torch.ones(self.n, dtype=torch.float64, device=x.device),
+                                 None, True)
+        if self.do_kde:
+            y = torch.from_numpy(self.y).cuda()
+            self.s_y = fcb.Sample(x, y, None, False)
+
+    def to_pinned(self):
+        import torch
+
+        fcb = self.fcb
+        xp = torch.from_numpy(self.w.points).pin_memory()
+        self.p_unit = fcb.Sample(xp, torch.ones(1), None, True)
+        self.out_pinned = torch.empty(int(np.prod(self.m)), dtype=torch.float64).pin_memory()
+        if self.do_kde:
+            yp = torch.from_numpy(self.y).pin_memory()
+            self.p_y = fcb.Sample(xp, yp, None, False)
+            self.out2_pinned = torch.empty(int(np.prod(self.m)), dtype=torch.float64).pin_memory()
+        self.h2d_bytes = self.w.points.nbytes + (self.y.nbytes if self.do_kde else 0)
+        self.d2h_bytes = self.out_pinned.numel() * 8 * (int(self.do_ecdf) + int(self.do_kde))
+
+    def step(self):
+        fcb = self.fcb
+        if self.do_ecdf:
+            fcb.ecdf_fastsum(self.s_unit, self.grid, self.delta)
+        if self.do_kde:
+            fcb.kde_fastsum(self.s_y, self.grid, fcb.laplacian(), self.bw)
+
+    def step_e2e(self):
+        fcb = self.fcb
+        if self.do_ecdf:
+            v = fcb.ecdf_fastsum(self.p_unit, self.grid, self.delta).values
+            self.out_pinned.copy_(v, non_blocking=True)
+        if self.do_kde:
+            v = fcb.kde_fastsum(self.p_y, self.grid, fcb.laplacian(), self.bw).values
+            self.out2_pinned.copy_(v, non_blocking=True)
+
+    def bytes_per_launch(self):
+        b = {}
+        if self.do_kde:
+            b.update(grid_kde_bytes(self.n, self.d, self.m, False))
+        if self.do_ecdf:
+            e = grid_ecdf_bytes(self.n, self.d, self.m, True)
+            for k, v in e.items():
+                if k in b:  # shared label between ECDF and KDE: keep them apart
+                    b[k + "@ecdf"] = v
+                else:
+                    b[k] = v
+        return b
+
+    # ---- CPU baseline: the oracle (restated reference algorithm) on a bounded sample ----
+    def cpu_sample(self, threads):
+        import oracle
+
+        used = oracle.set_threads(threads)
+        t_total = 0.0
+        desc = []
+        if self.do_ecdf:
+            t0 = time.perf_counter()
+            oracle.ecdf_fastsum(self.w.points, None, self.w.knots, self.w.delta, scaled=True)
+            t_total += time.perf_counter() - t0
+            desc.append("full grid ECDF")
+        if self.do_kde:
+            t0 = time.perf_counter()
+            oracle.kde_fastsum_laplacian(self.w.points, self.y, self.w.knots, self.w.h, codes=[0])
+            dt = time.perf_counter() - t0
+            t_total += dt * (1 << self.d)
+            desc.append(f"KDE: 1 of {1 << self.d} delta-terms timed on the full data, x{1 << self.d}")
+        return self.n / t_total, used, "; ".join(desc), t_total
+
+
+def dominant(prof: dict, bytes_map: dict):
+    """Kernel label with the largest device time; its algorithmic bytes per launch."""
+    best = None
+    for name, (cnt, ms) in prof.items():
+        if name == "lattice_zero":
+            continue
+        if best is None or ms > best[2]:
+            best = (name, cnt, ms)
+    if best is None:
+        return None
+    name, cnt, ms = best
+    return name, cnt, ms, bytes_map.get(name)
+
+
+def make_workload(name):
+    if name in ("cfg1", "cfg3", "cfg5", "cfg5a", "cfg5b"):
+        return GridWorkload(name)
+    raise SystemExit(f"unknown workload {name!r}")
+
+
+# ------------------------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    """--impl reference: the oracle port on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    import oracle
+
+    w = make_workload(args.workload)
+    threads = oracle.set_threads(0)
+    vals = []
+    for _ in range(max(args.warmup, 0)):
+        small = wl.cfg1(n=4096, m=16)
+        oracle.ecdf_fastsum(small.points, None, small.knots, small.delta)
+    sample = ""
+    for _ in range(args.steps):
+        v, used, sample, _ = w.cpu_sample(threads)
+        vals.append(v)
+    value = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": w.n / value * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded numpy, SURVEY §8d)",
+        "config": w.describe(),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "oracle/ = C restatement of the reference fastcdf algorithm (pure-Python "
+                "reference cannot travel to the GPU box); warm-up steps run a tiny instance",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2005_03246_b200 import _lib
+
+    _lib.load_library()
+    w = make_workload(args.workload)
+    w.to_device()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        w.step()
+    barrier()
+
+    # ---- timed region: device-resident inputs -------------------------------------------
+    clocks = ClockSampler(local)
+    clocks.start()
+    _lib.profile_enable(True)
+    _lib.profile_report()  # clear
+    stream = torch.cuda.current_stream()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        w.step()
+    ev1.record(stream)
+    barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    prof = _lib.profile_report()
+    _lib.profile_enable(False)
+    clk = clocks.stop()
+    t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    value = world * w.n / (ms_step / 1e3)
+
+    launches = sum(c for k, (c, _) in prof.items() if k != "lattice_zero")
+    peak, peak_src = peaks()
+    dom = dominant(prof, w.bytes_per_launch())
+    roof = None
+    if dom is not None:
+        name, cnt, ms, nbytes = dom
+        avg_s = ms / cnt / 1e3
+        ach = (nbytes / avg_s / 1e9) if nbytes else None
+        roof = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": (ach / peak) if ach else None, "traffic": None,
+                "bytes_per_launch": nbytes, "avg_launch_ms": avg_s * 1e3,
+                "share_of_step": ms / ms_total, "peak_source": peak_src}
+    breakdown = {k: {"launches": c, "ms_total": round(ms, 4),
+                     "share": round(ms / ms_total, 4)} for k, (c, ms) in prof.items()}
+
+    # ---- e2e: public API from pinned host buffers, H2D + D2H inside the timed region ------
+    e2e = None
+    if not args.no_e2e:
+        w.to_pinned()
+        w.step_e2e()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            w.step_e2e()
+        e1.record(stream)
+        barrier()
+        wall = (time.perf_counter() - t0) * 1e3
+        ems = torch.tensor([max(e0.elapsed_time(e1), wall)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e_step = float(ems.item()) / args.e2e_steps
+        e2e = {"value": world * w.n / (e_step / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": w.h2d_bytes, "d2h_bytes_per_step": w.d2h_bytes,
+               "ms_per_step": e_step, "steps": args.e2e_steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, used, sample, secs = w.cpu_sample(0)
+        cpu = {"value": v, "unit": UNIT, "cores": used, "kind": "port", "sample": sample,
+               "seconds": secs}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded numpy, SURVEY §8d shapes)",
+            "config": {**w.describe(), "parallelism": f"replicas x{world}" if world > 1 else "single"},
+            "e2e": e2e, "gpu_launches": int(launches), "roofline": roof,
+            "cpu_baseline": cpu, "clocks": clk, "kernels": breakdown,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

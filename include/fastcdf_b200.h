@@ -1,0 +1,162 @@
+/*
+ * fastcdf_b200.h — C-ABI of the B200-native generalized-ECDF / Laplacian-KDE hot path.
+ *
+ * The reference (`fastcdf`, arXiv 2005.03246, /root/reference/pkg/src/fastcdf) is a pure
+ * Python/numba package with no FFI of its own.  Each entry point below is the native body of
+ * one public reference function; the Python package `paper_2005_03246_b200` binds them with
+ * ctypes and keeps the reference's Python signatures on top.
+ *
+ * Conventions (all entry points):
+ *   - Array arguments named x, w, knots, out, lattice, ... are DEVICE pointers (cudaMalloc'd or
+ *     torch CUDA storage).  Small per-dimension parameter arrays (m, delta, dims, h, centre) are
+ *     HOST pointers of length d.
+ *   - x is row-major (n, d) fp64, exactly the reference's `Sample.points` layout (core.py:49-74).
+ *   - w == NULL means unit weights y == 1 (core.py:270-271).  Unit-weight grid paths accumulate
+ *     in int32 lattices (exact; n < 2^31) and are bit-exact with the reference.
+ *   - Grids are rectilinear: knots = the d knot vectors concatenated (dim 0 first), m[k] knots in
+ *     dim k, each strictly increasing (core.py:77-141).  Output grid order is lexicographic with
+ *     the last dimension fastest (core.py:137-141).
+ *   - delta[k] = +1 selects "<=" and -1 selects "<" (core.py:144-172).
+ *   - Every call only enqueues work on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *     Calls documented as "syncs" read a device scalar back and block on the stream.
+ *   - Workspace protocol (CUB style): call with ws == NULL to receive the byte count in
+ *     *ws_bytes; then call again with a device buffer of at least that size.  The library never
+ *     allocates device memory itself and keeps no state between calls (reentrant).
+ *   - Return value: FCG_OK or an error code; fcg_last_error() gives a thread-local message.
+ *     No C++ exception crosses this boundary.
+ */
+#ifndef FASTCDF_B200_H
+#define FASTCDF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FCG_ABI_VERSION 1
+#define FCG_MAX_DIM 8
+
+/* status codes */
+#define FCG_OK 0
+#define FCG_EINVAL 22      /* bad argument (maps to ParameterError / ShapeError host-side) */
+#define FCG_EUNSUPPORTED 95 /* shape outside what the kernels implement (e.g. d > FCG_MAX_DIM) */
+#define FCG_ECUDA 100      /* a CUDA launch or copy failed */
+#define FCG_EWORKSPACE 101 /* ws too small */
+
+/* lattice element kinds */
+#define FCG_LAT_I32 0      /* exact unit-weight counts */
+#define FCG_LAT_F64 1      /* weighted sums */
+
+int fcg_abi_version(void);
+const char *fcg_last_error(void);
+/* Number of SMs of the current device (for host-side sizing / reporting). */
+int fcg_device_sm_count(void);
+
+/* Launch profiler (the B200 stand-in for the reference's runtime_seconds metadata,
+ * fastsum.py:79,89-92): when enabled, every kernel launch of this library is bracketed by CUDA
+ * events recorded on its own stream.  fcg_profile_report() synchronises those events and
+ * writes "name count total_ms launches\n" lines (one per kernel label) into buf, then clears
+ * the records.  Returns the number of bytes written (truncated to cap-1), or -1 on error.
+ * fcg_profile_launches() returns the number of launches recorded since the last report. */
+int fcg_profile_enable(int on);
+int fcg_profile_report(char *buf, size_t cap);
+int64_t fcg_profile_launches(void);
+
+/* ---------------------------------------------------------------------------------------
+ * Grid path (Algorithm 1, lexicographic sweep)
+ * ------------------------------------------------------------------------------------- */
+
+/* Generalized local sums, Eq. (4): lattice[(M_1+1) x ... x (M_d+1)] = per-cell sums of w
+ * (or counts when w == NULL) with the delta-dependent bin rule b_k = #knots < x (delta=+1) or
+ * #knots <= x (delta=-1).
+ * Replaces: histogram.py:191-217 local_sums / local_sums_sorted / local_sums_uniform
+ *           (= flat_bin_indices histogram.py:153-174 + scatter_flat histogram.py:177-181). */
+int fcg_local_sums(const double *x, int64_t n, int32_t d, const double *w,
+                   const double *knots, const int64_t *m, const int32_t *delta,
+                   int32_t lat_kind, void *lattice,
+                   void *ws, size_t *ws_bytes, void *stream);
+
+/* In-place directional sweep of a dense lattice: inclusive prefix sums along every axis,
+ * forward where delta=+1 and suffix (reverse) where delta=-1.
+ * Replaces: fastsum.py:60-66 directional_sweep (_cumsum_directional fastsum.py:45-57). */
+int fcg_directional_sweep(void *lattice, int32_t lat_kind, int32_t d, const int64_t *dims,
+                          const int32_t *delta, void *ws, size_t *ws_bytes, void *stream);
+
+/* Generalized ECDF on the grid, Eq. (3) at every grid node (survival == 0) — replaces
+ * fastsum.py:69-92 ecdf_fastsum — or the survival function Eq. (2) (survival == 1, delta is
+ * ignored; all comparisons strict ">") — replaces fastsum.py:95-111 esf_fastsum.
+ * out: prod(m) values.  out_kind 0: fp64 (count or sum, divided by n when scaled);
+ *                       out_kind 1: int64 raw counts (requires w == NULL). */
+int fcg_ecdf_grid(const double *x, int64_t n, int32_t d, const double *w,
+                  const double *knots, const int64_t *m, const int32_t *delta,
+                  int32_t survival, int32_t scaled, int32_t out_kind, void *out,
+                  void *ws, size_t *ws_bytes, void *stream);
+
+/* Per-dimension min / max of x: out_minmax[0:d] = min, out_minmax[d:2d] = max (device).
+ * Feeds the centring / overflow guard of fastsum.py:114-129 and dnc.py:598-605,656. */
+int fcg_minmax(const double *x, int64_t n, int32_t d, double *out_minmax,
+               void *ws, size_t *ws_bytes, void *stream);
+
+/* Laplacian KDE on the grid by the 2^d-term CDF decomposition, Eq. (12).
+ * h: host (d,) diagonal bandwidth; centre: host (d,) centring point c (the caller computes the
+ * reference's hull midrange and overflow guard).  out: prod(m) fp64 densities.
+ * Replaces: fastsum.py:204-233 kde_fastsum for family "laplacian"
+ *           (_kde_exponential_fastsum fastsum.py:139-169,179-182). */
+int fcg_kde_grid_laplacian(const double *x, int64_t n, int32_t d, const double *w,
+                           const double *knots, const int64_t *m, const double *h,
+                           const double *centre, double *out,
+                           void *ws, size_t *ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Ranking (subsystem 1): device LSD radix sort of fp64 keys.
+ * keys: device, element i at keys[i*stride].  Outputs (device int32, any may be NULL):
+ *   order[p]  = index of the element at sorted position p (stable)
+ *   pos[i]    = sorted position of element i
+ *   lower[i]  = #keys <  keys[i]      upper[i] = #keys <= keys[i]
+ *   dense[i]  = #distinct keys < keys[i]
+ * n must be < 2^31.  -0.0 and +0.0 rank equal.  Replaces the np.argsort(kind="stable") calls
+ * at histogram.py:131 and dnc.py:517,527,544 and the tie scan of core.py:278-281. */
+int fcg_rank_f64(const double *keys, int64_t n, int64_t stride,
+                 int32_t *order, int32_t *pos, int32_t *lower, int32_t *upper, int32_t *dense,
+                 void *ws, size_t *ws_bytes, void *stream);
+
+/* Distinct-per-dimension flags (core.py:278-281): flags[k] = 1 when the n coordinates of
+ * dimension k are pairwise distinct.  flags: host (d,).  Syncs. */
+int fcg_distinct(const double *x, int64_t n, int32_t d, int32_t *flags,
+                 void *ws, size_t *ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * At-points path (subsystem 4)
+ * ------------------------------------------------------------------------------------- */
+
+/* Generalized ECDF at the sample points with ties allowed, Eq. (3) exactly as naive.py:90-114
+ * implements it (i == j included): out[j] = sum_i w_i prod_k [x_ik <= x_jk] (delta=+1) or
+ * [x_ik < x_jk] (delta=-1); survival == 1 gives Eq. (2), sum_i w_i prod_k [x_ik > x_jk].
+ * Divided by n when scaled.  Syncs (reads the distinct-level counts to pick the rank lattice
+ * or the dominance kernel). */
+int fcg_ecdf_points(const double *x, int64_t n, int32_t d, const double *w,
+                    const int32_t *delta, int32_t survival, int32_t scaled, double *out,
+                    void *ws, size_t *ws_bytes, void *stream);
+
+/* Strict-dominance ECDF at the sample points (requires pairwise-distinct coordinates per
+ * dimension, checked by the caller): out[j] = sum_{i != j, x_i < x_j in every dim} w_i,
+ * + w_j when include_self, / n when scaled.  Replaces dnc.py:531-561 ecdf_dnc. */
+int fcg_dnc_ecdf(const double *x, int64_t n, int32_t d, const double *w,
+                 int32_t include_self, int32_t scaled, double *out,
+                 void *ws, size_t *ws_bytes, void *stream);
+
+/* Laplacian KDE at the sample points via 2^d all-delta strict-dominance sums
+ * (dnc.py:635-690 kde_dnc, _run_all_delta dnc.py:564-585).  Requires distinct coordinates.
+ * h, centre: host (d,).  nw weight vectors w[v*n + i] (v < nw) are evaluated in one pass;
+ * out[v*n + j] receives the density numerator of weight vector v (self term and
+ * 1/(2^d n prod h) included, exactly the reference's kde_dnc output). */
+int fcg_kde_points_laplacian(const double *x, int64_t n, int32_t d, const double *w,
+                             int32_t nw, const double *h, const double *centre, double *out,
+                             void *ws, size_t *ws_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTCDF_B200_H */

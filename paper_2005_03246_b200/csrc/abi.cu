@@ -1,0 +1,123 @@
+// Error plumbing and small ABI queries.
+#include "common.cuh"
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+namespace fcg {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+int fail(int code, const std::string &msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int sm_count() {
+  static thread_local int cached = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  static thread_local int cached_dev = -1;
+  if (cached < 0 || cached_dev != dev) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    cached = v;
+    cached_dev = dev;
+  }
+  return cached;
+}
+
+// ---- launch profiler ----
+struct ProfRec {
+  const char *name;
+  cudaEvent_t a, b;
+};
+static std::mutex g_prof_mu;
+static std::vector<ProfRec> g_prof;
+static std::vector<cudaEvent_t> g_event_pool;
+static std::atomic<bool> g_prof_on{false};
+
+bool prof_enabled() { return g_prof_on.load(std::memory_order_relaxed); }
+
+cudaEvent_t prof_event() {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void prof_record(const char *name, cudaEvent_t a, cudaEvent_t b) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof.push_back({name, a, b});
+}
+
+}  // namespace fcg
+
+extern "C" int fcg_profile_enable(int on) {
+  fcg::g_prof_on.store(on != 0);
+  return FCG_OK;
+}
+
+extern "C" int64_t fcg_profile_launches(void) {
+  std::lock_guard<std::mutex> lk(fcg::g_prof_mu);
+  return (int64_t)fcg::g_prof.size();
+}
+
+extern "C" int fcg_profile_report(char *buf, size_t cap) {
+  std::vector<fcg::ProfRec> recs;
+  {
+    std::lock_guard<std::mutex> lk(fcg::g_prof_mu);
+    recs.swap(fcg::g_prof);
+  }
+  std::map<std::string, std::pair<int64_t, double>> agg;
+  std::vector<std::string> order;
+  for (auto &r : recs) {
+    if (cudaEventSynchronize(r.b) != cudaSuccess) return -1;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    auto it = agg.find(r.name);
+    if (it == agg.end()) {
+      order.push_back(r.name);
+      agg[r.name] = {1, ms};
+    } else {
+      it->second.first += 1;
+      it->second.second += ms;
+    }
+  }
+  {
+    std::lock_guard<std::mutex> lk(fcg::g_prof_mu);
+    for (auto &r : recs) {
+      fcg::g_event_pool.push_back(r.a);
+      fcg::g_event_pool.push_back(r.b);
+    }
+  }
+  std::string out;
+  for (auto &nm : order) {
+    char line[256];
+    snprintf(line, sizeof(line), "%s %lld %.6f\n", nm.c_str(), (long long)agg[nm].first,
+             agg[nm].second);
+    out += line;
+  }
+  if (cap == 0 || buf == nullptr) return (int)out.size();
+  size_t nb = out.size() < cap - 1 ? out.size() : cap - 1;
+  memcpy(buf, out.data(), nb);
+  buf[nb] = 0;
+  return (int)nb;
+}
+
+extern "C" int fcg_abi_version(void) { return FCG_ABI_VERSION; }
+
+extern "C" const char *fcg_last_error(void) { return fcg::g_last_error.c_str(); }
+
+extern "C" int fcg_device_sm_count(void) { return fcg::sm_count(); }

@@ -1,0 +1,489 @@
+// Grid path: fused per-point binning + scatter-add (subsystems 1-2 on a rectilinear grid),
+// directional sweeps (subsystem 3) and the grid ECDF / ESF / Laplacian-KDE pipelines.
+//
+// Reference semantics followed:
+//   * bin rule, histogram.py:3-15 and _flat_bins_uniform histogram.py:60-92: in dimension k a
+//     point lands in bin b = #knots < x (delta_k = +1) or #knots <= x (delta_k = -1), b in
+//     [0, M_k].  The device computes exactly that count from the uploaded knot values (a mesh
+//     guess verified against the knots, binary search when the guess is off), never from
+//     z0 + j*dz, so it is exact for any rectilinear grid and for points sitting on knots.
+//   * ecdf_fastsum (fastsum.py:69-92): forward prefix sums over delta-binned local sums, the
+//     j_k = M_k overflow layer is dropped, one division by N at the end.
+//   * esf_fastsum (fastsum.py:95-111): equals "strictly above" = delta=+1 binning, suffix sums,
+//     read one bin later (the reflection identity).
+//   * _kde_exponential_fastsum Laplacian branch (fastsum.py:139-169,179-182).
+//
+// Dead-layer elision: for a forward axis the j = M_k layer never reaches an output, for a
+// reverse axis the j = 0 layer never does (_delta_term_slices fastsum.py:132-136).  The fast
+// pipelines therefore scatter into an exactly prod(M_k)-cell lattice (cell = b - shift_k,
+// points falling in the dead layer are skipped) and the final scan pass writes the output in
+// place of the reference's slice + copy.
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace fcg {
+
+namespace {
+
+constexpr int kSmemKnots = 4096;  // up to 32 KB of knots staged in (dynamic) shared memory
+
+struct BinGrid {
+  int d;
+  int64_t m[FCG_MAX_DIM];
+  int64_t koff[FCG_MAX_DIM];
+  int le[FCG_MAX_DIM];       // 1: count knots <= x (delta=-1); 0: count knots < x (delta=+1)
+  int64_t shift[FCG_MAX_DIM];  // lattice cell = b - shift
+  int64_t dims[FCG_MAX_DIM];   // lattice extents
+  int64_t stride[FCG_MAX_DIM];
+  int64_t total_knots;
+};
+
+enum WeightKind { W_UNIT = 0, W_F64 = 1, W_PSI = 2 };
+
+struct PsiParams {  // psi_i = w_i * exp(sum_k (x_ik - c_k) * a_k), a_k = delta_k / h_k
+  double c[FCG_MAX_DIM];
+  double a[FCG_MAX_DIM];
+};
+
+// #knots < x (le = 0) or #knots <= x (le = 1) for a strictly increasing knot vector.
+__device__ __forceinline__ int64_t knot_count(double x, const double *kn, int64_t m, int le,
+                                              double z0, double inv_dz) {
+  double t = (x - z0) * inv_dz;
+  t = fmin(fmax(t, -1.0), (double)m + 1.0);
+  int64_t g = le ? (int64_t)floor(t) + 1 : (int64_t)ceil(t);
+  g = g < 0 ? 0 : (g > m ? m : g);
+#pragma unroll 1
+  for (int it = 0; it < 4; ++it) {
+    const bool lo_ok = (g == 0) || (le ? (kn[g - 1] <= x) : (kn[g - 1] < x));
+    const bool hi_ok = (g == m) || (le ? (x < kn[g]) : (x <= kn[g]));
+    if (lo_ok && hi_ok) return g;
+    g += lo_ok ? 1 : -1;
+  }
+  int64_t lo = 0, hi = m;  // first index whose knot fails the predicate
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const bool pred = le ? (kn[mid] <= x) : (kn[mid] < x);
+    if (pred) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+template <int D, int WK, typename T>
+__global__ void __launch_bounds__(256) bin_scatter_kernel(const double *__restrict__ x,
+                                                          int64_t n, int drt,
+                                                          const double *__restrict__ w,
+                                                          const double *__restrict__ knots,
+                                                          BinGrid g, PsiParams pp,
+                                                          T *__restrict__ lat) {
+  extern __shared__ double s_knots[];
+  __shared__ double s_z0[FCG_MAX_DIM], s_idz[FCG_MAX_DIM];
+  const int d = D > 0 ? D : drt;
+  const bool use_smem = g.total_knots <= kSmemKnots;
+  if (use_smem)
+    for (int64_t i = threadIdx.x; i < g.total_knots; i += blockDim.x) s_knots[i] = knots[i];
+  if (threadIdx.x < d) {
+    const int k = threadIdx.x;
+    const double *kn = knots + g.koff[k];
+    const int64_t m = g.m[k];
+    s_z0[k] = kn[0];
+    s_idz[k] = (m > 1) ? (double)(m - 1) / (kn[m - 1] - kn[0]) : 0.0;
+  }
+  __syncthreads();
+  const double *kb = use_smem ? s_knots : knots;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double xi[D > 0 ? D : FCG_MAX_DIM];
+    if constexpr (D == 2) {
+      const double2 v = reinterpret_cast<const double2 *>(x)[i];
+      xi[0] = v.x;
+      xi[1] = v.y;
+    } else if constexpr (D == 4) {
+      const double2 v0 = reinterpret_cast<const double2 *>(x)[2 * i];
+      const double2 v1 = reinterpret_cast<const double2 *>(x)[2 * i + 1];
+      xi[0] = v0.x; xi[1] = v0.y; xi[2] = v1.x; xi[3] = v1.y;
+    } else {
+#pragma unroll
+      for (int k = 0; k < (D > 0 ? D : FCG_MAX_DIM); ++k)
+        if (k < d) xi[k] = x[i * d + k];
+    }
+    int64_t flat = 0;
+    bool live = true;
+#pragma unroll
+    for (int k = 0; k < (D > 0 ? D : FCG_MAX_DIM); ++k) {
+      if (k < d) {
+        const int64_t b = knot_count(xi[k], kb + g.koff[k], g.m[k], g.le[k], s_z0[k], s_idz[k]);
+        const int64_t cell = b - g.shift[k];
+        live = live && (cell >= 0) && (cell < g.dims[k]);
+        flat += cell * g.stride[k];
+      }
+    }
+    if (!live) continue;
+    if constexpr (WK == W_UNIT) {
+      atomicAdd(reinterpret_cast<int *>(lat) + flat, 1);
+    } else if constexpr (WK == W_F64) {
+      atomicAdd(reinterpret_cast<double *>(lat) + flat, w[i]);
+    } else {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < (D > 0 ? D : FCG_MAX_DIM); ++k)
+        if (k < d) s += (xi[k] - pp.c[k]) * pp.a[k];
+      const double wi = w ? w[i] : 1.0;
+      atomicAdd(reinterpret_cast<double *>(lat) + flat, wi * exp(s));
+    }
+  }
+}
+
+template <int WK, typename T>
+int launch_bin_scatter(const double *x, int64_t n, int d, const double *w, const double *knots,
+                       const BinGrid &g, const PsiParams &pp, T *lat, cudaStream_t st) {
+  if (n == 0) return FCG_OK;
+  const int grid = grid_for(n, 256, 8);
+  const size_t smem = g.total_knots <= kSmemKnots ? (size_t)g.total_knots * sizeof(double) : 0;
+  const bool vec_ok = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  FCG_PROF(WK == W_UNIT ? "bin_scatter_count" : (WK == W_F64 ? "bin_scatter_w" : "bin_scatter_psi"), st);
+  switch (d) {
+    case 1: bin_scatter_kernel<1, WK, T><<<grid, 256, smem, st>>>(x, n, d, w, knots, g, pp, lat); break;
+    case 2:
+      if (vec_ok) bin_scatter_kernel<2, WK, T><<<grid, 256, smem, st>>>(x, n, d, w, knots, g, pp, lat);
+      else bin_scatter_kernel<0, WK, T><<<grid, 256, smem, st>>>(x, n, d, w, knots, g, pp, lat);
+      break;
+    case 3: bin_scatter_kernel<3, WK, T><<<grid, 256, smem, st>>>(x, n, d, w, knots, g, pp, lat); break;
+    case 4:
+      if (vec_ok) bin_scatter_kernel<4, WK, T><<<grid, 256, smem, st>>>(x, n, d, w, knots, g, pp, lat);
+      else bin_scatter_kernel<0, WK, T><<<grid, 256, smem, st>>>(x, n, d, w, knots, g, pp, lat);
+      break;
+    default: bin_scatter_kernel<0, WK, T><<<grid, 256, smem, st>>>(x, n, d, w, knots, g, pp, lat); break;
+  }
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}
+
+int check_common(int64_t n, int32_t d, const int64_t *m) {
+  if (d < 1 || d > FCG_MAX_DIM)
+    return fail(FCG_EUNSUPPORTED, "dimension d must be in [1, " + std::to_string(FCG_MAX_DIM) + "]");
+  if (n < 0) return fail(FCG_EINVAL, "n must be >= 0");
+  if (n >= (int64_t(1) << 31)) return fail(FCG_EUNSUPPORTED, "n must be < 2^31");
+  for (int k = 0; k < d; ++k)
+    if (m[k] < 1) return fail(FCG_EINVAL, "every dimension needs at least one knot");
+  return FCG_OK;
+}
+
+// Bin grid for a lattice whose extents are `dims` and where cell = b - shift.
+BinGrid make_bin_grid(int d, const int64_t *m, const int *le, const int64_t *shift,
+                      const int64_t *dims) {
+  BinGrid g{};
+  g.d = d;
+  int64_t off = 0;
+  for (int k = 0; k < d; ++k) {
+    g.m[k] = m[k];
+    g.koff[k] = off;
+    off += m[k];
+    g.le[k] = le[k];
+    g.shift[k] = shift[k];
+    g.dims[k] = dims[k];
+  }
+  g.total_knots = off;
+  int64_t s = 1;
+  for (int k = d - 1; k >= 0; --k) {
+    g.stride[k] = s;
+    s *= dims[k];
+  }
+  return g;
+}
+
+// ---- KDE helpers -------------------------------------------------------------------------
+
+// zf[koff_k + j] = exp(-delta_k * (knot_kj - c_k) / h_k)   (fastsum.py:162-166)
+struct ZfParams {
+  int d;
+  int64_t m[FCG_MAX_DIM], koff[FCG_MAX_DIM];
+  double c[FCG_MAX_DIM], h[FCG_MAX_DIM], s[FCG_MAX_DIM];
+};
+
+__global__ void zf_kernel(const double *__restrict__ knots, ZfParams p, double *__restrict__ zf,
+                          int64_t total) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int k = 0;
+    while (k + 1 < p.d && i >= p.koff[k + 1]) ++k;
+    const double zc = knots[i] - p.c[k];
+    zf[i] = exp((-p.s[k] * zc) / p.h[k]);
+  }
+}
+
+// ---- min / max ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t ord_key(double v) { return f64_key(v); }
+__device__ __forceinline__ double ord_val(uint64_t k) {
+  uint64_t u = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)u);
+}
+
+__global__ void minmax_init(unsigned long long *mm, int d) {
+  int k = threadIdx.x;
+  if (k < d) {
+    mm[k] = ~0ull;
+    mm[d + k] = 0ull;
+  }
+}
+
+__global__ void __launch_bounds__(256) minmax_kernel(const double *__restrict__ x, int64_t n,
+                                                     int d, unsigned long long *mm) {
+  uint64_t lo[FCG_MAX_DIM], hi[FCG_MAX_DIM];
+  for (int k = 0; k < d; ++k) {
+    lo[k] = ~0ull;
+    hi[k] = 0ull;
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    for (int k = 0; k < d; ++k) {
+      const uint64_t key = ord_key(x[i * d + k]);
+      lo[k] = key < lo[k] ? key : lo[k];
+      hi[k] = key > hi[k] ? key : hi[k];
+    }
+  }
+  for (int k = 0; k < d; ++k) {
+    uint64_t a = lo[k], b = hi[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t ao = __shfl_xor_sync(0xffffffffu, a, o);
+      const uint64_t bo = __shfl_xor_sync(0xffffffffu, b, o);
+      a = ao < a ? ao : a;
+      b = bo > b ? bo : b;
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(mm + k, (unsigned long long)a);
+      atomicMax(mm + d + k, (unsigned long long)b);
+    }
+  }
+}
+
+__global__ void minmax_finish(const unsigned long long *mm, int d, double *out) {
+  int k = threadIdx.x;
+  if (k < 2 * d) out[k] = ord_val(mm[k]);
+}
+
+}  // namespace
+
+// ============================================================================================
+// C-ABI entry points
+// ============================================================================================
+
+}  // namespace fcg
+
+using namespace fcg;
+
+extern "C" int fcg_local_sums(const double *x, int64_t n, int32_t d, const double *w,
+                              const double *knots, const int64_t *m, const int32_t *delta,
+                              int32_t lat_kind, void *lattice, void *ws, size_t *ws_bytes,
+                              void *stream) {
+  FCG_TRY(check_common(n, d, m));
+  if (lat_kind == FCG_LAT_I32 && w != nullptr)
+    return fail(FCG_EINVAL, "int32 lattices hold unit-weight counts only (pass w = NULL)");
+  if (ws == nullptr) {
+    *ws_bytes = 256;
+    return FCG_OK;
+  }
+  cudaStream_t st = as_stream(stream);
+  int le[FCG_MAX_DIM];
+  int64_t shift[FCG_MAX_DIM], dims[FCG_MAX_DIM];
+  int64_t L = 1;
+  for (int k = 0; k < d; ++k) {
+    if (delta[k] != 1 && delta[k] != -1) return fail(FCG_EINVAL, "delta entries must be -1 or +1");
+    le[k] = delta[k] < 0;
+    shift[k] = 0;
+    dims[k] = m[k] + 1;  // full (M_k+1) lattice incl. the overflow layer (histogram.py:27-31)
+    L *= dims[k];
+  }
+  BinGrid g = make_bin_grid(d, m, le, shift, dims);
+  PsiParams pp{};
+  const size_t esz = lat_kind == FCG_LAT_I32 ? 4 : 8;
+  FCG_CUDA_TRY(cudaMemsetAsync(lattice, 0, (size_t)L * esz, st));
+  if (lat_kind == FCG_LAT_I32)
+    return launch_bin_scatter<W_UNIT>(x, n, d, w, knots, g, pp, static_cast<int32_t *>(lattice), st);
+  return launch_bin_scatter<W_F64>(x, n, d, w, knots, g, pp, static_cast<double *>(lattice), st);
+}
+
+extern "C" int fcg_directional_sweep(void *lattice, int32_t lat_kind, int32_t d,
+                                     const int64_t *dims, const int32_t *delta, void *ws,
+                                     size_t *ws_bytes, void *stream) {
+  if (d < 1 || d > FCG_MAX_DIM) return fail(FCG_EUNSUPPORTED, "dimension out of range");
+  LatShape s;
+  s.d = d;
+  for (int k = 0; k < d; ++k) {
+    if (dims[k] < 1) return fail(FCG_EINVAL, "lattice extents must be >= 1");
+    s.dims[k] = dims[k];
+  }
+  const size_t esz = lat_kind == FCG_LAT_I32 ? 4 : 8;
+  Workspace W(ws);
+  void *scratch = W.take<char>((size_t)scan_scratch_elems(s) * esz);
+  if (ws == nullptr) {
+    *ws_bytes = W.bytes();
+    return FCG_OK;
+  }
+  bool rev[FCG_MAX_DIM];
+  for (int k = 0; k < d; ++k) {
+    if (delta[k] != 1 && delta[k] != -1) return fail(FCG_EINVAL, "delta entries must be -1 or +1");
+    rev[k] = delta[k] < 0;
+  }
+  Epi e;  // in place
+  cudaStream_t st = as_stream(stream);
+  if (lat_kind == FCG_LAT_I32)
+    return scan_lattice<int32_t>(static_cast<int32_t *>(lattice), s, rev, e,
+                                 static_cast<int32_t *>(scratch), st);
+  return scan_lattice<double>(static_cast<double *>(lattice), s, rev, e,
+                              static_cast<double *>(scratch), st);
+}
+
+extern "C" int fcg_ecdf_grid(const double *x, int64_t n, int32_t d, const double *w,
+                             const double *knots, const int64_t *m, const int32_t *delta,
+                             int32_t survival, int32_t scaled, int32_t out_kind, void *out,
+                             void *ws, size_t *ws_bytes, void *stream) {
+  FCG_TRY(check_common(n, d, m));
+  if (out_kind == 1 && w != nullptr)
+    return fail(FCG_EINVAL, "int64 count output requires unit weights (w = NULL)");
+  LatShape s;
+  s.d = d;
+  for (int k = 0; k < d; ++k) s.dims[k] = m[k];
+  const int64_t L = s.size();
+  const bool unit = (w == nullptr);
+  const size_t esz = unit ? 4 : 8;
+  Workspace W(ws);
+  void *lat = W.take<char>((size_t)L * esz);
+  void *scratch = W.take<char>((size_t)scan_scratch_elems(s) * esz);
+  if (ws == nullptr) {
+    *ws_bytes = W.bytes();
+    return FCG_OK;
+  }
+  int le[FCG_MAX_DIM];
+  int64_t shift[FCG_MAX_DIM];
+  bool rev[FCG_MAX_DIM];
+  for (int k = 0; k < d; ++k) {
+    if (!survival && delta[k] != 1 && delta[k] != -1)
+      return fail(FCG_EINVAL, "delta entries must be -1 or +1");
+    if (survival) {  // strictly above: #knots < x binning, suffix sums read one bin later
+      le[k] = 0;
+      shift[k] = 1;
+      rev[k] = true;
+    } else {
+      le[k] = delta[k] < 0;
+      shift[k] = 0;
+      rev[k] = false;
+    }
+  }
+  BinGrid g = make_bin_grid(d, m, le, shift, s.dims);
+  PsiParams pp{};
+  cudaStream_t st = as_stream(stream);
+  {
+    FCG_PROF("lattice_zero", st);
+    FCG_CUDA_TRY(cudaMemsetAsync(lat, 0, (size_t)L * esz, st));
+  }
+  Epi e;
+  e.kind = out_kind == 1 ? EPI_I64 : EPI_F64;
+  e.out = out;
+  e.div = scaled ? (double)n : 0.0;
+  if (unit) {
+    FCG_TRY(launch_bin_scatter<W_UNIT>(x, n, d, w, knots, g, pp, static_cast<int32_t *>(lat), st));
+    return scan_lattice<int32_t>(static_cast<int32_t *>(lat), s, rev, e,
+                                 static_cast<int32_t *>(scratch), st);
+  }
+  FCG_TRY(launch_bin_scatter<W_F64>(x, n, d, w, knots, g, pp, static_cast<double *>(lat), st));
+  return scan_lattice<double>(static_cast<double *>(lat), s, rev, e,
+                              static_cast<double *>(scratch), st);
+}
+
+extern "C" int fcg_minmax(const double *x, int64_t n, int32_t d, double *out_minmax, void *ws,
+                          size_t *ws_bytes, void *stream) {
+  if (d < 1 || d > FCG_MAX_DIM) return fail(FCG_EUNSUPPORTED, "dimension out of range");
+  Workspace W(ws);
+  unsigned long long *mm = W.take<unsigned long long>(2 * d);
+  if (ws == nullptr) {
+    *ws_bytes = W.bytes();
+    return FCG_OK;
+  }
+  cudaStream_t st = as_stream(stream);
+  FCG_PROF("minmax", st);
+  minmax_init<<<1, 32, 0, st>>>(mm, d);
+  FCG_LAUNCH_CHECK();
+  if (n > 0) {
+    minmax_kernel<<<grid_for(n, 256, 4), 256, 0, st>>>(x, n, d, mm);
+    FCG_LAUNCH_CHECK();
+  }
+  minmax_finish<<<1, 32, 0, st>>>(mm, d, out_minmax);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}
+
+extern "C" int fcg_kde_grid_laplacian(const double *x, int64_t n, int32_t d, const double *w,
+                                      const double *knots, const int64_t *m, const double *h,
+                                      const double *centre, double *out, void *ws,
+                                      size_t *ws_bytes, void *stream) {
+  FCG_TRY(check_common(n, d, m));
+  LatShape s;
+  s.d = d;
+  int64_t total_knots = 0;
+  for (int k = 0; k < d; ++k) {
+    s.dims[k] = m[k];
+    total_knots += m[k];
+  }
+  const int64_t L = s.size();
+  Workspace W(ws);
+  double *lat = W.take<double>((size_t)L);
+  double *scratch = W.take<double>((size_t)scan_scratch_elems(s));
+  double *zf = W.take<double>((size_t)total_knots);
+  if (ws == nullptr) {
+    *ws_bytes = W.bytes();
+    return FCG_OK;
+  }
+  for (int k = 0; k < d; ++k)
+    if (!(h[k] > 0.0)) return fail(FCG_EINVAL, "bandwidth must be > 0");
+  cudaStream_t st = as_stream(stream);
+  double prod_h = 1.0;
+  for (int k = 0; k < d; ++k) prod_h *= h[k];
+  const double scale = 1.0 / (std::ldexp(1.0, d) * (double)n * prod_h);
+  const int ncodes = 1 << d;
+  for (int code = 0; code < ncodes; ++code) {
+    int le[FCG_MAX_DIM];
+    int64_t shift[FCG_MAX_DIM];
+    bool rev[FCG_MAX_DIM];
+    PsiParams pp{};
+    ZfParams zp{};
+    zp.d = d;
+    int64_t off = 0;
+    for (int k = 0; k < d; ++k) {
+      const double sgn = ((code >> k) & 1) ? -1.0 : 1.0;  // DeltaVector.from_code, core.py:165-168
+      le[k] = 0;                                       // one delta=+1 binning for every term
+      shift[k] = sgn < 0 ? 1 : 0;                      // -1 axes read [1:M+1]
+      rev[k] = sgn < 0;
+      pp.c[k] = centre[k];
+      pp.a[k] = sgn / h[k];
+      zp.m[k] = m[k];
+      zp.koff[k] = off;
+      off += m[k];
+      zp.c[k] = centre[k];
+      zp.h[k] = h[k];
+      zp.s[k] = sgn;
+    }
+    BinGrid g = make_bin_grid(d, m, le, shift, s.dims);
+    {
+      FCG_PROF("kde_zfac", st);
+      zf_kernel<<<grid_for(total_knots, 256, 1), 256, 0, st>>>(knots, zp, zf, total_knots);
+    }
+    FCG_LAUNCH_CHECK();
+    {
+      FCG_PROF("lattice_zero", st);
+      FCG_CUDA_TRY(cudaMemsetAsync(lat, 0, (size_t)L * sizeof(double), st));
+    }
+    FCG_TRY(launch_bin_scatter<W_PSI>(x, n, d, w, knots, g, pp, lat, st));
+    Epi e;
+    e.kind = EPI_KDE;
+    e.out = out;
+    e.zf = zf;
+    for (int k = 0; k < d; ++k) e.zoff[k] = zp.koff[k];
+    e.accumulate = code > 0;
+    e.apply_scale = code == ncodes - 1;
+    e.scale = scale;
+    FCG_TRY(scan_lattice<double>(lat, s, rev, e, scratch, st));
+  }
+  return FCG_OK;
+}

@@ -1,0 +1,327 @@
+// Directional prefix-sum engine; see scan.cuh.
+#include "scan.cuh"
+
+namespace fcg {
+
+namespace {
+
+constexpr int kUnroll = 8;
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  return v;
+}
+
+// Product over the axes other than e.ax of zf_k[i_k] for the multi-index of flat line origin
+// (a over axes < ax, b over axes > ax).
+__device__ __forceinline__ double zprod_other(const Epi &e, int64_t a, int64_t b) {
+  double z = 1.0;
+  // decompose b over axes d-1 .. ax+1 (last axis fastest)
+  for (int k = e.d - 1; k > e.ax; --k) {
+    int64_t i = b % e.dims[k];
+    b /= e.dims[k];
+    z *= e.zf[e.zoff[k] + i];
+  }
+  for (int k = e.ax - 1; k >= 0; --k) {
+    int64_t i = a % e.dims[k];
+    a /= e.dims[k];
+    z *= e.zf[e.zoff[k] + i];
+  }
+  return z;
+}
+
+template <typename T, int EK>
+__device__ __forceinline__ void emit(T *lat, const Epi &e, int64_t f, int64_t j, double zo, T v) {
+  if constexpr (EK == EPI_INPLACE) {
+    lat[f] = v;
+  } else if constexpr (EK == EPI_F64) {
+    double r = (double)v;
+    if (e.div > 0.0) r = r / e.div;
+    static_cast<double *>(e.out)[f] = r;
+  } else if constexpr (EK == EPI_I64) {
+    static_cast<int64_t *>(e.out)[f] = (int64_t)v;
+  } else {
+    double *o = static_cast<double *>(e.out);
+    double r = (zo * e.zf[e.zoff[e.ax] + j]) * (double)v;
+    if (e.accumulate) r = o[f] + r;
+    if (e.apply_scale) r = r * e.scale;
+    o[f] = r;
+  }
+}
+
+// ---- lines: thread per (a, chunk c, b) ----------------------------------------------------
+template <typename T, bool REV, int EK>
+__global__ void __launch_bounds__(256) lines_kernel(T *__restrict__ lat, int64_t A, int64_t D,
+                                                    int64_t B, int64_t Dc, int64_t C,
+                                                    const T *__restrict__ carry_in, Epi e) {
+  const int64_t total = A * C * B;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t % B;
+    const int64_t r = t / B;
+    const int64_t c = r % C;
+    const int64_t a = r / C;
+    T carry = carry_in ? carry_in[(a * C + c) * B + b] : T(0);
+    const int64_t j0 = c * Dc;
+    const int64_t j1 = (j0 + Dc < D) ? j0 + Dc : D;
+    T *base = lat + a * D * B + b;
+    double zo = 1.0;
+    if constexpr (EK == EPI_KDE) zo = zprod_other(e, a, b);
+    int64_t jj = j0;
+    for (; jj + kUnroll <= j1; jj += kUnroll) {
+      T v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t j = REV ? (D - 1 - (jj + u)) : (jj + u);
+        v[u] = base[j * B];
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t j = REV ? (D - 1 - (jj + u)) : (jj + u);
+        carry += v[u];
+        emit<T, EK>(lat, e, a * D * B + j * B + b, j, zo, carry);
+      }
+    }
+    for (; jj < j1; ++jj) {
+      const int64_t j = REV ? (D - 1 - jj) : jj;
+      carry += base[j * B];
+      emit<T, EK>(lat, e, a * D * B + j * B + b, j, zo, carry);
+    }
+  }
+}
+
+// chunk totals for lines: sums[(a*C + c)*B + b]
+template <typename T, bool REV>
+__global__ void __launch_bounds__(256) lines_chunk_sums(const T *__restrict__ lat, int64_t A,
+                                                        int64_t D, int64_t B, int64_t Dc,
+                                                        int64_t C, T *__restrict__ sums) {
+  const int64_t total = A * C * B;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t % B;
+    const int64_t r = t / B;
+    const int64_t c = r % C;
+    const int64_t a = r / C;
+    const int64_t j0 = c * Dc;
+    const int64_t j1 = (j0 + Dc < D) ? j0 + Dc : D;
+    const T *base = lat + a * D * B + b;
+    T s = T(0);
+    int64_t jj = j0;
+    for (; jj + kUnroll <= j1; jj += kUnroll) {
+      T v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t j = REV ? (D - 1 - (jj + u)) : (jj + u);
+        v[u] = base[j * B];
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) s += v[u];
+    }
+    for (; jj < j1; ++jj) s += base[(REV ? (D - 1 - jj) : jj) * B];
+    sums[t] = s;
+  }
+}
+
+// exclusive scan over c of sums[a][c][b] (in place), thread per (a, b)
+template <typename T>
+__global__ void chunk_excl_scan(T *__restrict__ sums, int64_t A, int64_t C, int64_t B) {
+  const int64_t total = A * B;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t % B;
+    const int64_t a = t / B;
+    T run = T(0);
+    for (int64_t c = 0; c < C; ++c) {
+      T *p = sums + (a * C + c) * B + b;
+      T v = *p;
+      *p = run;
+      run += v;
+    }
+  }
+}
+
+// ---- rows (B == 1): warp per (row a, chunk c) ---------------------------------------------
+template <typename T, bool REV, int EK>
+__global__ void __launch_bounds__(256) rows_kernel(T *__restrict__ lat, int64_t A, int64_t D,
+                                                   int64_t Dc, int64_t C,
+                                                   const T *__restrict__ carry_in, Epi e) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < A * C;
+       w += warps) {
+    const int64_t a = w / C;
+    const int64_t c = w % C;
+    T carry = carry_in ? carry_in[w] : T(0);
+    const int64_t j0 = c * Dc;
+    const int64_t j1 = (j0 + Dc < D) ? j0 + Dc : D;
+    T *row = lat + a * D;
+    double zo = 1.0;
+    if constexpr (EK == EPI_KDE) zo = zprod_other(e, a, 0);
+    constexpr int U = 4;
+    for (int64_t jb = j0; jb < j1; jb += 32 * U) {
+      T v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t jj = jb + u * 32 + lane;
+        v[u] = (jj < j1) ? row[REV ? (D - 1 - jj) : jj] : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        T s = warp_incl_scan(v[u], lane) + carry;
+        carry = __shfl_sync(0xffffffffu, s, 31);
+        const int64_t jj = jb + u * 32 + lane;
+        if (jj < j1) {
+          const int64_t j = REV ? (D - 1 - jj) : jj;
+          emit<T, EK>(lat, e, a * D + j, j, zo, s);
+        }
+      }
+    }
+  }
+}
+
+template <typename T, bool REV>
+__global__ void __launch_bounds__(256) rows_chunk_sums(const T *__restrict__ lat, int64_t A,
+                                                       int64_t D, int64_t Dc, int64_t C,
+                                                       T *__restrict__ sums) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < A * C;
+       w += warps) {
+    const int64_t a = w / C;
+    const int64_t c = w % C;
+    const int64_t j0 = c * Dc;
+    const int64_t j1 = (j0 + Dc < D) ? j0 + Dc : D;
+    const T *row = lat + a * D;
+    T s = T(0);
+    for (int64_t jj = j0 + lane; jj < j1; jj += 32) s += row[REV ? (D - 1 - jj) : jj];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) sums[w] = s;
+  }
+}
+
+struct PassPlan {
+  int64_t A, D, B, C, Dc;
+};
+
+PassPlan plan_pass(const LatShape &s, int ax) {
+  PassPlan p;
+  p.A = 1;
+  for (int k = 0; k < ax; ++k) p.A *= s.dims[k];
+  p.D = s.dims[ax];
+  p.B = 1;
+  for (int k = ax + 1; k < s.d; ++k) p.B *= s.dims[k];
+  const int64_t target = (int64_t)sm_count() * 1536;  // resident threads worth filling
+  const int64_t units = (p.B == 1) ? p.A * 32 : p.A * p.B;
+  int64_t C = 1;
+  if (units < target && p.D >= 128) {
+    C = ceil_div(target, units);
+    int64_t cmax = p.D / 32;
+    if (C > cmax) C = cmax;
+    if (C > 512) C = 512;
+    if (C < 1) C = 1;
+  }
+  p.C = C;
+  p.Dc = ceil_div(p.D, C);
+  p.C = ceil_div(p.D, p.Dc);
+  return p;
+}
+
+template <typename T, bool REV, int EK>
+int launch_pass(T *lat, const PassPlan &p, const Epi &e, T *scratch, cudaStream_t st) {
+  const T *carry = nullptr;
+  if (p.C > 1) {
+    FCG_PROF("scan_chunk_carry", st);
+    if (p.B == 1) {
+      const int64_t warps = p.A * p.C;
+      rows_chunk_sums<T, REV><<<grid_for(warps * 32, 256), 256, 0, st>>>(lat, p.A, p.D, p.Dc,
+                                                                       p.C, scratch);
+      FCG_LAUNCH_CHECK();
+      chunk_excl_scan<T><<<grid_for(p.A, 256), 256, 0, st>>>(scratch, p.A, p.C, 1);
+    } else {
+      lines_chunk_sums<T, REV><<<grid_for(p.A * p.C * p.B, 256), 256, 0, st>>>(
+          lat, p.A, p.D, p.B, p.Dc, p.C, scratch);
+      FCG_LAUNCH_CHECK();
+      chunk_excl_scan<T><<<grid_for(p.A * p.B, 256), 256, 0, st>>>(scratch, p.A, p.C, p.B);
+    }
+    FCG_LAUNCH_CHECK();
+    carry = scratch;
+  }
+  const bool fin = EK != EPI_INPLACE;
+  if (p.B == 1) {
+    FCG_PROF(fin ? "scan_rows_final" : "scan_rows", st);
+    rows_kernel<T, REV, EK><<<grid_for(p.A * p.C * 32, 256), 256, 0, st>>>(lat, p.A, p.D, p.Dc,
+                                                                          p.C, carry, e);
+  } else {
+    FCG_PROF(fin ? "scan_lines_final" : "scan_lines", st);
+    lines_kernel<T, REV, EK><<<grid_for(p.A * p.C * p.B, 256), 256, 0, st>>>(
+        lat, p.A, p.D, p.B, p.Dc, p.C, carry, e);
+  }
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}
+
+template <typename T, int EK>
+int launch_dir(T *lat, const PassPlan &p, bool rev, const Epi &e, T *scratch, cudaStream_t st) {
+  return rev ? launch_pass<T, true, EK>(lat, p, e, scratch, st)
+             : launch_pass<T, false, EK>(lat, p, e, scratch, st);
+}
+
+}  // namespace
+
+int64_t scan_scratch_elems(const LatShape &s) {
+  int64_t mx = 0;
+  for (int ax = 0; ax < s.d; ++ax) {
+    PassPlan p = plan_pass(s, ax);
+    if (p.C > 1) {
+      int64_t need = p.A * p.C * p.B;
+      if (need > mx) mx = need;
+    }
+  }
+  return mx;
+}
+
+template <typename T>
+int scan_axis(T *lat, const LatShape &s, int ax, bool rev, const Epi &epi, T *scratch,
+              cudaStream_t st) {
+  PassPlan p = plan_pass(s, ax);
+  Epi e = epi;
+  e.ax = ax;
+  e.d = s.d;
+  for (int k = 0; k < s.d; ++k) e.dims[k] = s.dims[k];
+  switch (e.kind) {
+    case EPI_INPLACE: return launch_dir<T, EPI_INPLACE>(lat, p, rev, e, scratch, st);
+    case EPI_F64: return launch_dir<T, EPI_F64>(lat, p, rev, e, scratch, st);
+    case EPI_I64: return launch_dir<T, EPI_I64>(lat, p, rev, e, scratch, st);
+    case EPI_KDE: return launch_dir<T, EPI_KDE>(lat, p, rev, e, scratch, st);
+  }
+  return fail(FCG_EINVAL, "unknown epilogue kind");
+}
+
+template <typename T>
+int scan_lattice(T *lat, const LatShape &s, const bool *rev, const Epi &epi, T *scratch,
+                 cudaStream_t st) {
+  // last (contiguous) axis first, axis 0 last so that its coalesced line walk carries the
+  // epilogue.
+  Epi inplace;
+  for (int ax = s.d - 1; ax >= 0; --ax) {
+    FCG_TRY(scan_axis<T>(lat, s, ax, rev[ax], ax == 0 ? epi : inplace, scratch, st));
+  }
+  return FCG_OK;
+}
+
+template int scan_lattice<int32_t>(int32_t *, const LatShape &, const bool *, const Epi &,
+                                   int32_t *, cudaStream_t);
+template int scan_lattice<double>(double *, const LatShape &, const bool *, const Epi &, double *,
+                                  cudaStream_t);
+template int scan_axis<int32_t>(int32_t *, const LatShape &, int, bool, const Epi &, int32_t *,
+                                cudaStream_t);
+template int scan_axis<double>(double *, const LatShape &, int, bool, const Epi &, double *,
+                               cudaStream_t);
+
+}  // namespace fcg

@@ -1,0 +1,348 @@
+// Subsystem 1 (ranking): stable LSD radix sort of order-preserving fp64 keys, device-wide
+// scans and the rank outputs of fcg_rank_f64.  Replaces np.argsort(kind="stable")
+// (histogram.py:131, dnc.py:517,527,544) and the tie scan of core.py:278-281.
+//
+// One radix pass (8-bit digit) = digit histogram per 4096-item tile (warp-aggregated shared
+// atomics) -> exclusive scan of the digit-major histogram -> stable scatter: every warp ranks
+// its 512 items with __match_any_sync peers and per-warp digit counters, so equal digits keep
+// their input order (stability across tiles comes from the digit-major global offsets).
+#include "sort.cuh"
+
+namespace fcg {
+
+namespace {
+
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Block-wide exclusive scan of one int per thread (blockDim = 1024); returns the exclusive
+// prefix, *total receives the block total.
+__device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t *s_warp, int32_t *total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int32_t t = (lane < (int)(blockDim.x >> 5)) ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int32_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    s_warp[lane] = t;  // inclusive warp-total prefix
+  }
+  __syncthreads();
+  const int32_t warp_excl = warp ? s_warp[warp - 1] : 0;
+  *total = s_warp[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return warp_excl + x - v;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const int32_t *__restrict__ in,
+                                                                   int64_t n,
+                                                                   int32_t *__restrict__ partial) {
+  __shared__ int32_t s_warp[32];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j)
+    if (base + j < n) s += in[base + j];
+  int32_t tot;
+  block_excl_scan(s, s_warp, &tot);
+  if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+}
+
+// single CTA: exclusive scan of partial[0..np) in place
+__global__ void __launch_bounds__(kScanThreads) scan_partials_kernel(int32_t *partial, int64_t np) {
+  __shared__ int32_t s_warp[32];
+  int32_t carry = 0;
+  for (int64_t b0 = 0; b0 < np; b0 += kScanTile) {
+    const int64_t base = b0 + (int64_t)threadIdx.x * kScanItems;
+    int32_t v[kScanItems];
+    int32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      v[j] = (base + j < np) ? partial[base + j] : 0;
+      s += v[j];
+    }
+    int32_t tot;
+    int32_t run = block_excl_scan(s, s_warp, &tot) + carry;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      if (base + j < np) partial[base + j] = run;
+      run += v[j];
+    }
+    carry += tot;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const int32_t *in, int32_t *out,
+                                                                  int64_t n,
+                                                                  const int32_t *__restrict__ partial,
+                                                                  int inclusive) {
+  __shared__ int32_t s_warp[32];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int32_t v[kScanItems];
+  int32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    v[j] = (base + j < n) ? in[base + j] : 0;
+    s += v[j];
+  }
+  int32_t tot;
+  int32_t run = block_excl_scan(s, s_warp, &tot) + partial[blockIdx.x];
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    if (base + j < n) out[base + j] = inclusive ? run + v[j] : run;
+    run += v[j];
+  }
+}
+
+__global__ void radix_init_kernel(const double *__restrict__ x, int64_t n, int64_t stride,
+                                  uint64_t *__restrict__ keys, int32_t *__restrict__ vals) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = f64_key(x[i * stride]);
+    vals[i] = (int32_t)i;
+  }
+}
+
+__global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint64_t *__restrict__ keys,
+                                                                  int64_t n, int shift,
+                                                                  int32_t *__restrict__ hist,
+                                                                  int64_t tiles) {
+  __shared__ int32_t s_hist[256];
+  s_hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kSortTile;
+  const int lane = threadIdx.x & 31;
+#pragma unroll 4
+  for (int j = 0; j < kSortItems; ++j) {
+    const int64_t i = base + (int64_t)j * kSortThreads + threadIdx.x;
+    const bool ok = i < n;
+    const unsigned dig = ok ? (unsigned)((keys[i] >> shift) & 0xFF) : 256u + lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, dig);
+    if (ok && lane == __ffs(peers) - 1) atomicAdd(&s_hist[dig], __popc(peers));
+  }
+  __syncthreads();
+  hist[(int64_t)threadIdx.x * tiles + blockIdx.x] = s_hist[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
+    const uint64_t *__restrict__ kin, const int32_t *__restrict__ vin, uint64_t *__restrict__ kout,
+    int32_t *__restrict__ vout, int64_t n, int shift, const int32_t *__restrict__ offs,
+    int64_t tiles) {
+  __shared__ int32_t s_cnt[kSortThreads / 32][256];
+  __shared__ int32_t s_goff[256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int d = lane; d < 256; d += 32) s_cnt[warp][d] = 0;
+  s_goff[threadIdx.x] = offs[(int64_t)threadIdx.x * tiles + blockIdx.x];
+  __syncwarp();
+  const int64_t base = (int64_t)blockIdx.x * kSortTile + (int64_t)warp * (kSortTile / 8);
+  uint64_t k[kSortItems];
+  int32_t v[kSortItems];
+  int32_t r[kSortItems];
+  const unsigned lt = lanemask_lt();
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const int64_t i = base + (int64_t)j * 32 + lane;
+    const bool ok = i < n;
+    k[j] = ok ? kin[i] : 0ull;
+    v[j] = ok ? vin[i] : 0;
+    const unsigned dig = ok ? (unsigned)((k[j] >> shift) & 0xFF) : 256u + lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, dig);
+    int32_t before = 0;
+    if (ok) before = s_cnt[warp][dig];
+    __syncwarp();
+    if (ok && lane == __ffs(peers) - 1) s_cnt[warp][dig] = before + __popc(peers);
+    __syncwarp();
+    r[j] = before + __popc(peers & lt);
+  }
+  __syncthreads();
+  {
+    const int d = threadIdx.x;  // 256 threads, one digit each
+    int32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kSortThreads / 32; ++w) {
+      const int32_t t = s_cnt[w][d];
+      s_cnt[w][d] = run;
+      run += t;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const int64_t i = base + (int64_t)j * 32 + lane;
+    if (i < n) {
+      const unsigned dig = (unsigned)((k[j] >> shift) & 0xFF);
+      const int64_t dst = (int64_t)s_goff[dig] + s_cnt[warp][dig] + r[j];
+      kout[dst] = k[j];
+      vout[dst] = v[j];
+    }
+  }
+}
+
+__global__ void rank_heads_kernel(const uint64_t *__restrict__ keys,
+                                  const int32_t *__restrict__ order, int64_t n,
+                                  int32_t *__restrict__ heads, int32_t *__restrict__ pos) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    heads[p] = (p == 0 || keys[p] != keys[p - 1]) ? 1 : 0;
+    if (pos) pos[order[p]] = (int32_t)p;
+  }
+}
+
+// heads now holds the inclusive scan (dense rank + 1) of the head flags
+__global__ void rank_start_kernel(const uint64_t *__restrict__ keys, const int32_t *__restrict__ incl,
+                                  int64_t n, int32_t *__restrict__ start, int32_t *n_distinct) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t dr = incl[p] - 1;
+    if (p == 0 || keys[p] != keys[p - 1]) start[dr] = (int32_t)p;
+    if (p == n - 1) {
+      start[dr + 1] = (int32_t)n;
+      if (n_distinct) *n_distinct = dr + 1;
+    }
+  }
+}
+
+__global__ void rank_scatter_kernel(const int32_t *__restrict__ order,
+                                    const int32_t *__restrict__ incl,
+                                    const int32_t *__restrict__ start, int64_t n,
+                                    int32_t *lower, int32_t *upper, int32_t *dense) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = order[p];
+    const int32_t dr = incl[p] - 1;
+    if (dense) dense[i] = dr;
+    if (lower) lower[i] = start[dr];
+    if (upper) upper[i] = start[dr + 1];
+  }
+}
+
+}  // namespace
+
+size_t radix_ws_hist_elems(int64_t n) { return (size_t)256 * (size_t)ceil_div(n, kSortTile) + 1; }
+
+size_t scan_ws_partial_elems(int64_t n) { return (size_t)ceil_div(n, kScanTile) + 1; }
+
+int scan_i32(const int32_t *in, int32_t *out, int64_t n, bool inclusive, int32_t *partial,
+             cudaStream_t st) {
+  if (n <= 0) return FCG_OK;
+  const int64_t blocks = ceil_div(n, kScanTile);
+  FCG_PROF("scan_i32", st);
+  scan_reduce_kernel<<<(unsigned)blocks, kScanThreads, 0, st>>>(in, n, partial);
+  FCG_LAUNCH_CHECK();
+  scan_partials_kernel<<<1, kScanThreads, 0, st>>>(partial, blocks);
+  FCG_LAUNCH_CHECK();
+  scan_apply_kernel<<<(unsigned)blocks, kScanThreads, 0, st>>>(in, out, n, partial, inclusive);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}
+
+int radix_init_f64(const double *x, int64_t n, int64_t stride, uint64_t *keys, int32_t *vals,
+                   cudaStream_t st) {
+  if (n <= 0) return FCG_OK;
+  FCG_PROF("radix_init", st);
+  radix_init_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(x, n, stride, keys, vals);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}
+
+int radix_sort_pairs(uint64_t *keys, int32_t *vals, int64_t n, int begin_bit, int end_bit,
+                     const RadixWs &ws, cudaStream_t st) {
+  if (n <= 1) return FCG_OK;
+  const int64_t tiles = ceil_div(n, kSortTile);
+  uint64_t *ka = keys, *kb = ws.keys_alt;
+  int32_t *va = vals, *vb = ws.vals_alt;
+  int passes = 0;
+  for (int shift = begin_bit; shift < end_bit; shift += 8) {
+    {
+      FCG_PROF("radix_hist", st);
+      radix_hist_kernel<<<(unsigned)tiles, kSortThreads, 0, st>>>(ka, n, shift, ws.hist, tiles);
+      FCG_LAUNCH_CHECK();
+    }
+    FCG_TRY(scan_i32(ws.hist, ws.hist, 256 * tiles, false, ws.partial, st));
+    {
+      FCG_PROF("radix_scatter", st);
+      radix_scatter_kernel<<<(unsigned)tiles, kSortThreads, 0, st>>>(ka, va, kb, vb, n, shift,
+                                                                     ws.hist, tiles);
+      FCG_LAUNCH_CHECK();
+    }
+    std::swap(ka, kb);
+    std::swap(va, vb);
+    ++passes;
+  }
+  if (passes & 1) {
+    FCG_CUDA_TRY(cudaMemcpyAsync(keys, ka, (size_t)n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+    FCG_CUDA_TRY(cudaMemcpyAsync(vals, va, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  }
+  return FCG_OK;
+}
+
+int rank_outputs(const uint64_t *sorted_keys, const int32_t *order, int64_t n, int32_t *pos,
+                 int32_t *lower, int32_t *upper, int32_t *dense, int32_t *heads, int32_t *start,
+                 int32_t *partial, int32_t *n_distinct_dev, cudaStream_t st) {
+  if (n <= 0) return FCG_OK;
+  const int g = grid_for(n, 256, 8);
+  {
+    FCG_PROF("rank_heads", st);
+    rank_heads_kernel<<<g, 256, 0, st>>>(sorted_keys, order, n, heads, pos);
+    FCG_LAUNCH_CHECK();
+  }
+  FCG_TRY(scan_i32(heads, heads, n, true, partial, st));
+  FCG_PROF("rank_scatter", st);
+  rank_start_kernel<<<g, 256, 0, st>>>(sorted_keys, heads, n, start, n_distinct_dev);
+  FCG_LAUNCH_CHECK();
+  if (lower || upper || dense) {
+    rank_scatter_kernel<<<g, 256, 0, st>>>(order, heads, start, n, lower, upper, dense);
+    FCG_LAUNCH_CHECK();
+  }
+  return FCG_OK;
+}
+
+}  // namespace fcg
+
+using namespace fcg;
+
+extern "C" int fcg_rank_f64(const double *keys, int64_t n, int64_t stride, int32_t *order,
+                            int32_t *pos, int32_t *lower, int32_t *upper, int32_t *dense, void *ws,
+                            size_t *ws_bytes, void *stream) {
+  if (n < 0) return fail(FCG_EINVAL, "n must be >= 0");
+  if (n >= (int64_t(1) << 31) - 1) return fail(FCG_EUNSUPPORTED, "n must be < 2^31 - 1");
+  if (stride < 1) return fail(FCG_EINVAL, "stride must be >= 1");
+  Workspace W(ws);
+  uint64_t *k = W.take<uint64_t>(n);
+  int32_t *v = W.take<int32_t>(n);
+  RadixWs rw;
+  rw.keys_alt = W.take<uint64_t>(n);
+  rw.vals_alt = W.take<int32_t>(n);
+  rw.hist = W.take<int32_t>(radix_ws_hist_elems(n));
+  rw.partial = W.take<int32_t>(scan_ws_partial_elems(256 * (n / kSortTile + 1) + n));
+  int32_t *heads = W.take<int32_t>(n);
+  int32_t *start = W.take<int32_t>(n + 1);
+  if (ws == nullptr) {
+    *ws_bytes = W.bytes();
+    return FCG_OK;
+  }
+  if (n == 0) return FCG_OK;
+  cudaStream_t st = as_stream(stream);
+  FCG_TRY(radix_init_f64(keys, n, stride, k, v, st));
+  FCG_TRY(radix_sort_pairs(k, v, n, 0, 64, rw, st));
+  if (order)
+    FCG_CUDA_TRY(cudaMemcpyAsync(order, v, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  return rank_outputs(k, v, n, pos, lower, upper, dense, heads, start, rw.partial, nullptr, st);
+}

@@ -1,0 +1,40 @@
+// Device building blocks for subsystem 1 (ranking): a stable LSD radix sort of 64-bit keys
+// with int32 payloads, device-wide int32 scans, and small-key bucketing.
+#pragma once
+#include "common.cuh"
+
+namespace fcg {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;                       // per thread
+constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 items per CTA
+
+// Workspace elements needed by radix_sort_pairs for n items.
+struct RadixWs {
+  uint64_t *keys_alt;
+  int32_t *vals_alt;
+  int32_t *hist;     // 256 * tiles
+  int32_t *partial;  // scan partials
+};
+size_t radix_ws_hist_elems(int64_t n);
+size_t scan_ws_partial_elems(int64_t n);
+
+// Stable sort of (keys, vals) by bits [begin_bit, end_bit) of keys; in place (result in
+// keys/vals), ping-ponging through ws.keys_alt / ws.vals_alt.
+int radix_sort_pairs(uint64_t *keys, int32_t *vals, int64_t n, int begin_bit, int end_bit,
+                     const RadixWs &ws, cudaStream_t st);
+
+// Exclusive (or inclusive) prefix sum of int32 (in and out may alias). partial: scan ws.
+int scan_i32(const int32_t *in, int32_t *out, int64_t n, bool inclusive, int32_t *partial,
+             cudaStream_t st);
+
+// fp64 keys (strided) -> order-preserving uint64 keys, vals = 0..n-1
+int radix_init_f64(const double *x, int64_t n, int64_t stride, uint64_t *keys, int32_t *vals,
+                   cudaStream_t st);
+
+// Rank outputs from a sorted key sequence (see fcg_rank_f64). start: n+1 ints scratch.
+int rank_outputs(const uint64_t *sorted_keys, const int32_t *order, int64_t n, int32_t *pos,
+                 int32_t *lower, int32_t *upper, int32_t *dense, int32_t *heads, int32_t *start,
+                 int32_t *partial, int32_t *n_distinct_dev, cudaStream_t st);
+
+}  // namespace fcg

@@ -1,0 +1,114 @@
+"""CPU-only checks: the C-ABI library loads and exports every symbol the header declares, and
+the host-side domain types / guards behave like the reference's (core.py, histogram.py)."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2005_03246_b200 as fcb
+from paper_2005_03246_b200 import _lib
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def header_functions():
+    txt = (ROOT / "include" / "fastcdf_b200.h").read_text()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(fcg_\w+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load_library()
+    names = header_functions()
+    assert len(names) >= 15
+    for name in names:
+        assert hasattr(lib, name), name
+        assert name in _lib.EXPORTED, f"{name} has no ctypes signature"
+    assert lib.fcg_abi_version() == 1
+
+
+def test_workspace_query_needs_no_gpu():
+    """Size queries are pure host arithmetic (no device touched)."""
+    import ctypes as C
+
+    lib = _lib.load_library()
+    nbytes = C.c_size_t(0)
+    rc = lib.fcg_ecdf_grid(None, 1000, 3, None, None, _lib.i64_array([512, 512, 512]),
+                           _lib.i32_array([1, 1, 1]), 0, 1, 0, None, None, C.byref(nbytes), None)
+    assert rc == 0
+    assert nbytes.value >= 512 ** 3 * 4  # int32 lattice of the exact output extents
+    rc = lib.fcg_ecdf_grid(None, 10, 9, None, None, _lib.i64_array([2] * 9),
+                           _lib.i32_array([1] * 9), 0, 1, 0, None, None, C.byref(nbytes), None)
+    assert rc == _lib.FCG_EUNSUPPORTED
+    assert b"dimension" in lib.fcg_last_error()
+
+
+def test_no_cpu_fallback_without_cuda():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present")
+    s = fcb.validate_sample([[0.1, 0.2], [0.3, 0.4]])
+    g = fcb.RectilinearGrid.from_knots([[0.5], [0.5]])
+    with pytest.raises(RuntimeError, match="CUDA"):
+        fcb.ecdf_fastsum(s, g)
+
+
+def test_validate_sample_contracts():
+    s = fcb.validate_sample([[0.2, 0.7], [0.5, 0.1], [0.9, 0.9]], [1.0, 1.0, 1.0])
+    assert s.count == 3 and s.dim == 2 and s.distinct and s.unit_weights
+    with pytest.raises(fcb.ValidationError):
+        fcb.validate_sample([[0.0, np.nan]])
+    with pytest.raises(fcb.ValidationError):
+        fcb.validate_sample([[0.0]], [np.inf])
+    with pytest.raises(fcb.ShapeError):
+        fcb.validate_sample(np.empty((0, 2)))
+    with pytest.raises(fcb.ShapeError):
+        fcb.validate_sample([[1.0, 2.0]], [1.0, 2.0])
+    assert fcb.validate_sample([[1.0, 3.0], [1.0, 4.0]]).distinct_by_dim == (False, True)
+    assert not fcb.validate_sample([[1.0], [2.0]], [1.0, 2.0]).unit_weights
+    np.testing.assert_array_equal(fcb.validate_sample([[1.0], [2.0]]).weights, [1.0, 1.0])
+
+
+def test_grid_and_delta_contracts():
+    with pytest.raises(fcb.ValidationError):
+        fcb.RectilinearGrid.from_knots([np.array([0.0, 0.0, 1.0])])
+    with pytest.raises(fcb.ValidationError):
+        fcb.RectilinearGrid.from_knots([np.array([1.0, 0.5])])
+    g = fcb.RectilinearGrid.from_knots([np.array([0.0, 0.5, 1.0]), np.array([0.0, 0.3, 1.0])])
+    assert g.uniform == (True, False) and g.shape == (3, 3) and g.size == 9
+    lat = fcb.RectilinearGrid.from_knots([[0.0, 1.0], [10.0, 20.0, 30.0]]).lattice()
+    np.testing.assert_array_equal(lat[:3, 1], [10.0, 20.0, 30.0])
+    with pytest.raises(fcb.ParameterError):
+        fcb.DeltaVector((0, 1))
+    dv = fcb.DeltaVector((-1, 1, -1))
+    assert dv.parity == 1 and fcb.DeltaVector.from_code(dv.code, 3) == dv
+    assert [d.code for d in fcb.all_deltas(3)] == list(range(8))
+    s = fcb.validate_sample([[0.0, 1.0], [1.0, 1.0]])
+    with pytest.raises(fcb.ParameterError):
+        fcb.build_grid_auto(s, [1, 4])
+    with pytest.raises(fcb.DegenerateRangeError):
+        fcb.build_grid_auto(s, [4, 4])
+    with pytest.raises(fcb.ParameterError):
+        fcb.Bandwidth.diag([0.1, -0.2])
+
+
+def test_generator_bit_exact_vs_reference(small_golden):
+    np.testing.assert_array_equal(fcb.generate_gaussian_sample(4, 2, 7).points,
+                                  small_golden["gen.4x2s7"])
+    np.testing.assert_array_equal(fcb.generate_gaussian_sample(1001, 3, 3).points,
+                                  small_golden["gen.1001x3s3"])
+
+
+def test_dimension_mismatch_raises_before_device_work():
+    s = fcb.validate_sample([[0.1, 0.2]])
+    g = fcb.RectilinearGrid.from_knots([[0.5]])
+    with pytest.raises(fcb.ParameterError, match="dimension mismatch"):
+        fcb.local_sums_sorted(s, g)
+    with pytest.raises(fcb.ParameterError):
+        fcb.ecdf_fastsum(s, g)
+    with pytest.raises(fcb.ParameterError):
+        fcb.kde_fastsum(s, fcb.RectilinearGrid.from_knots([[0.5], [0.5]]), fcb.laplacian(),
+                        fcb.Bandwidth.full(np.eye(2)))

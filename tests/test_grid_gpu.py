@@ -1,0 +1,241 @@
+"""GPU parity of the grid path (local sums, directional sweep, grid ECDF / ESF / KDE) against the
+golden fixtures produced by the reference and against the pinned oracle."""
+
+import numpy as np
+import pytest
+
+import paper_2005_03246_b200 as fcb
+from conftest import cfg_golden
+
+pytestmark = pytest.mark.gpu
+
+THREE = [[0.2, 0.7], [0.5, 0.1], [0.9, 0.9]]
+REL_F64 = 1e-12   # north_star: weighted fp64 ECDF tolerance
+REL_KDE = 1e-9    # north_star: KDE tolerance
+
+
+def _grid(knots):
+    return fcb.RectilinearGrid.from_knots([np.asarray(z, float) for z in knots])
+
+
+def assert_rel(got, ref, rel):
+    got, ref = np.asarray(got), np.asarray(ref)
+    assert got.shape == ref.shape
+    scale = np.maximum(np.abs(ref), np.finfo(float).tiny)
+    err = np.max(np.abs(got - ref) / scale) if ref.size else 0.0
+    assert err <= rel, f"max relative error {err:.3e} > {rel:.1e}"
+
+
+# ---- hand KATs (reference tests test_histogram.py:18-40, test_fastsum.py:52-85) ----------
+
+def test_kat_local_sums(small_golden):
+    s = fcb.validate_sample(THREE)
+    g = _grid([[0.5], [0.5]])
+    np.testing.assert_array_equal(fcb.local_sums_sorted(s, g, fcb.DeltaVector((1, 1))).data,
+                                  small_golden["kat.ls_pp"])
+    np.testing.assert_array_equal(fcb.local_sums_sorted(s, g, fcb.DeltaVector((-1, 1))).data,
+                                  small_golden["kat.ls_mp"])
+    t = fcb.local_sums_sorted(s, _grid([[5.0], [0.5]]))
+    assert t.data[1].sum() == 0
+    np.testing.assert_array_equal(t.data[0], [1.0, 2.0])
+
+
+def test_kat_ecdf_esf(small_golden):
+    s = fcb.validate_sample(THREE)
+    g = _grid([[0.5, 0.9], [0.5, 0.9]])
+    np.testing.assert_array_equal(fcb.ecdf_fastsum(s, g).values, small_golden["kat.ecdf"])
+    np.testing.assert_array_equal(fcb.ecdf_fastsum(s, g, fcb.DeltaVector((-1, -1))).values,
+                                  small_golden["kat.ecdf_mm"])
+    assert fcb.ecdf_fastsum(s, g, fcb.DeltaVector((-1, -1))).values[0] == 0.0
+    np.testing.assert_array_equal(fcb.ecdf_fastsum(s, _grid([[-2, -1], [-2, -1]])).values,
+                                  np.zeros(4))
+    np.testing.assert_array_equal(fcb.esf_fastsum(s, _grid([[0.4], [0.4]])).values,
+                                  small_golden["kat.esf04"])
+    assert fcb.esf_fastsum(s, _grid([[2.0], [2.0]])).values[0] == 0.0
+    assert fcb.esf_fastsum(s, _grid([[-1.0], [-1.0]])).values[0] == 1.0
+
+
+def test_uniform_formula_knot_hits():
+    # x = 0.5 on knots (0, .5, 1): bin 1 under <=, bin 2 under <; x = -3 -> bin 0
+    s = fcb.validate_sample([[0.5], [-3.0]])
+    g = _grid([[0.0, 0.5, 1.0]])
+    np.testing.assert_array_equal(fcb.local_sums(s, g, fcb.DeltaVector((1,))).data, [1, 1, 0, 0])
+    np.testing.assert_array_equal(fcb.local_sums(s, g, fcb.DeltaVector((-1,))).data, [1, 0, 1, 0])
+
+
+# ---- seeded fixtures ---------------------------------------------------------------------
+
+def test_local_sums_golden_bit_exact(small_golden):
+    g = small_golden
+    seeds = g.keys("ls.")
+    assert len(seeds) == 40
+    for seed in seeds:
+        key = f"ls.{seed}"
+        s = fcb.validate_sample(g[key + ".x"], g[key + ".w"])
+        grid = _grid(g.knots(key))
+        delta = fcb.DeltaVector(tuple(int(v) for v in g[key + ".delta"]))
+        np.testing.assert_array_equal(fcb.local_sums(s, grid, delta).data, g[key + ".out"])
+        su = fcb.validate_sample(g[key + ".x"])
+        cnt = np.bincount(g[key + ".flat"], minlength=int(np.prod([len(z) + 1 for z in g.knots(key)])))
+        np.testing.assert_array_equal(fcb.local_sums(su, grid, delta).data.reshape(-1), cnt)
+
+
+def test_ecdf_fastsum_golden(small_golden):
+    g = small_golden
+    for d in range(1, 6):
+        for seed in range(6):
+            key = f"ecdf.{d}.{seed}"
+            x, grid = g[key + ".x"], _grid(g.knots(key))
+            delta = fcb.DeltaVector(tuple(int(v) for v in g[key + ".delta"]))
+            # integer weights: exact
+            got = fcb.ecdf_fastsum(fcb.validate_sample(x, g[key + ".w"]), grid, delta, scaled=False)
+            np.testing.assert_array_equal(got.values, g[key + ".out"])
+            # unit weights: int32 lattice, count / N bitwise
+            got = fcb.ecdf_fastsum(fcb.validate_sample(x), grid, delta)
+            np.testing.assert_array_equal(got.values, g[key + ".unit"])
+            # float weights: tolerance
+            sw = fcb.validate_sample(x, g[key + ".wf"])
+            assert_rel(fcb.ecdf_fastsum(sw, grid, delta).values, g[key + ".outf"], REL_F64)
+            assert_rel(fcb.esf_fastsum(sw, grid).values, g[key + ".esf"], REL_F64)
+
+
+def test_directional_sweep_golden(small_golden):
+    g = small_golden
+    for d in range(1, 5):
+        t = g[f"sweep.{d}.in"]
+        for code in range(1 << d):
+            out = fcb.directional_sweep(fcb.LocalSumTensor(t.copy()), fcb.DeltaVector.from_code(code, d))
+            assert_rel(out.data, g[f"sweep.{d}.{code}"], 1e-13)
+    data = np.arange(6.0).reshape(2, 3)
+    t = fcb.LocalSumTensor(data.copy())
+    fcb.directional_sweep(t, fcb.DeltaVector((1, 1)))
+    np.testing.assert_array_equal(t.data, data)  # input not mutated
+
+
+def test_kde_fastsum_golden(small_golden):
+    g = small_golden
+    for d in (1, 2, 3):
+        key = f"kde.{d}"
+        s = fcb.validate_sample(g[key + ".x"], g[key + ".w"])
+        grid = _grid(g.knots(key))
+        bw = fcb.Bandwidth.diag(g[key + ".h"])
+        got = fcb.kde_fastsum(s, grid, fcb.laplacian(), bw).values
+        assert_rel(got, g[key + ".fast"], REL_KDE)
+        assert np.max(np.abs(got - g[key + ".naive"])) <= 1e-13  # reference bound
+        assert_rel(fcb.kde_fastsum(s, grid, fcb.uniform(), bw).values, g[key + ".unif"], 1e-12)
+    s = fcb.validate_sample(g["kdeknots.x"], g["kdeknots.w"])
+    got = fcb.kde_fastsum(s, _grid(g.knots("kdeknots")), fcb.laplacian(),
+                          fcb.Bandwidth.diag([0.25, 0.4])).values
+    assert_rel(got, g["kdeknots.fast"], REL_KDE)
+
+
+def test_kde_single_point_kats():
+    s = fcb.validate_sample([[0.0]])
+    v = fcb.kde_fastsum(s, _grid([[-1.0, 1.0]]), fcb.laplacian(), fcb.Bandwidth.diag([1.0])).values
+    np.testing.assert_allclose(v, 0.5 * np.exp(-1.0), rtol=1e-15)
+    s = fcb.validate_sample([[0.0, 0.0]])
+    v = fcb.kde_fastsum(s, _grid([[0.0, 1.0], [0.0, 1.0]]), fcb.laplacian(),
+                        fcb.Bandwidth.diag([1.0, 1.0])).values
+    assert np.isclose(v[-1], 0.25 * np.exp(-2.0)) and np.isclose(v[0], 0.25)
+
+
+# ---- errors (reference error contracts) --------------------------------------------------
+
+def test_error_contracts():
+    s = fcb.validate_sample([[0.1, 0.2]])
+    with pytest.raises(fcb.ParameterError):
+        fcb.local_sums_sorted(s, _grid([[0.5]]))
+    with pytest.raises(fcb.ParameterError):
+        fcb.local_sums_uniform(fcb.validate_sample([[0.5]]), _grid([[0.0, 0.4, 1.0]]))
+    rng = np.random.default_rng(3)
+    s = fcb.validate_sample(np.column_stack([rng.uniform(0, 1, 50), rng.uniform(0, 700, 50)]))
+    g = fcb.build_grid_auto(s, [4, 4])
+    with pytest.raises(fcb.OverflowGuardError, match="dimension 1"):
+        fcb.kde_fastsum(s, g, fcb.laplacian(), fcb.Bandwidth.diag([1.0, 1.0]))
+    with pytest.raises(fcb.ParameterError):
+        fcb.kde_fastsum(fcb.validate_sample([[0.0], [1.0]]), _grid([[0.0, 1.0]]), fcb.gaussian(),
+                        fcb.Bandwidth.diag([1.0]))
+    with pytest.raises(fcb.ParameterError):
+        fcb.kde_fastsum(fcb.validate_sample([[0.0, 0.0], [1.0, 1.0]]), _grid([[0, 1], [0, 1]]),
+                        fcb.laplacian(), fcb.Bandwidth.full(np.eye(2)))
+
+
+# ---- random properties vs the oracle -----------------------------------------------------
+
+@pytest.mark.parametrize("d", [1, 2, 3, 4, 5, 6])
+def test_ecdf_vs_oracle_random(d, oracle):
+    for seed in range(5):
+        rng = np.random.default_rng(7000 + 10 * d + seed)
+        n = int(rng.integers(1, 3000))
+        x = rng.standard_normal((n, d))
+        m = [int(v) for v in rng.integers(1, 40 if d <= 3 else 9, d)]
+        knots = [np.sort(rng.uniform(-2.5, 2.5, mk)) for mk in m]
+        knots = [np.unique(np.concatenate([z, x[rng.integers(0, n, 2), k]])) for k, z in enumerate(knots)]
+        delta = tuple(int(v) for v in rng.choice([-1, 1], d))
+        grid = _grid(knots)
+        got = fcb.ecdf_fastsum_counts(fcb.validate_sample(x), grid, fcb.DeltaVector(delta))
+        ref = oracle.ecdf_fastsum(x, None, knots, delta, scaled=False)
+        np.testing.assert_array_equal(got, ref.astype(np.int64))
+        got = fcb.esf_fastsum(fcb.validate_sample(x), grid, scaled=False).values
+        np.testing.assert_array_equal(got, oracle.esf_fastsum(x, None, knots, scaled=False))
+
+
+def test_long_axis_chunked_scan(oracle):
+    """1-D grid with 200k knots forces the chunked 3-phase scan path."""
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((300_000, 1))
+    knots = [np.linspace(-3, 3, 200_000)]
+    w = rng.uniform(0, 1, x.shape[0])
+    got = fcb.ecdf_fastsum(fcb.validate_sample(x), _grid(knots), scaled=False).values
+    np.testing.assert_array_equal(got, oracle.ecdf_fastsum(x, None, knots, scaled=False))
+    got = fcb.ecdf_fastsum(fcb.validate_sample(x, w), _grid(knots)).values
+    assert_rel(got, oracle.ecdf_fastsum(x, w, knots), REL_F64)
+
+
+def test_device_tensor_roundtrip(oracle):
+    import torch
+
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((5000, 3))
+    knots = [np.linspace(-2, 2, 17)] * 3
+    s_dev = fcb.validate_sample(torch.from_numpy(x).cuda())
+    res = fcb.ecdf_fastsum(s_dev, _grid(knots), scaled=False)
+    assert isinstance(res.values, torch.Tensor) and res.values.is_cuda
+    np.testing.assert_array_equal(res.values.cpu().numpy(),
+                                  oracle.ecdf_fastsum(x, None, knots, scaled=False))
+
+
+# ---- full-size configurations ------------------------------------------------------------
+
+def test_cfg1_full_bit_exact(oracle):
+    import workloads as wl
+
+    gold = cfg_golden("cfg1")
+    w = wl.cfg1()
+    s = fcb.validate_sample(w.points)
+    grid = _grid(w.knots)
+    counts = fcb.ecdf_fastsum_counts(s, grid, fcb.DeltaVector(w.delta))
+    ref = oracle.ecdf_fastsum(w.points, None, w.knots, w.delta, scaled=False)
+    np.testing.assert_array_equal(counts, ref.astype(np.int64))
+    vals = fcb.ecdf_fastsum(s, grid, fcb.DeltaVector(w.delta)).values
+    np.testing.assert_array_equal(vals, oracle.ecdf_fastsum(w.points, None, w.knots, w.delta))
+    if gold is not None:
+        np.testing.assert_array_equal(counts, gold["counts"].astype(np.int64))
+
+
+@pytest.mark.slow
+def test_cfg3_full_bit_exact(oracle, cfg_meta):
+    import workloads as wl
+
+    oracle.set_threads(0)
+    w = wl.cfg3()
+    s = fcb.validate_sample(w.points)
+    counts = fcb.ecdf_fastsum_counts(s, _grid(w.knots), fcb.DeltaVector(w.delta))
+    meta = cfg_meta.get("cfg3", {})
+    if meta.get("input_sha") == wl.digest(w.points):
+        assert wl.digest(counts) == meta["out_sha_i64"]  # the reference's own output digest
+    ref = oracle.ecdf_fastsum(w.points, None, w.knots, w.delta, scaled=False)
+    np.testing.assert_array_equal(counts, ref.astype(np.int64))
+    # size-independent property: last corner == number of points inside the grid box
+    inside = np.all(w.points <= 4.0, axis=1).sum()
+    assert counts[-1] == inside
