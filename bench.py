@@ -269,9 +269,111 @@ def dominant(prof: dict, bytes_map: dict):
     return name, cnt, ms, bytes_map.get(name)
 
 
+def radix_bytes(n):
+    # per radix pass: histogram reads 8-byte keys; scatter reads and writes key + int32 payload
+    return {"radix_hist": 8 * n, "radix_scatter": 24 * n, "radix_init": 8 * n + 12 * n}
+
+
+class PointsWorkload:
+    """At-points configs: cfg2 (ECDF delta=(1,-1) + ESF with ties, N = 1e6) and cfg4 (Laplacian
+    KDE density + regression numerators, N = 1e7, one device pass)."""
+
+    def __init__(self, name):
+        import paper_2005_03246_b200 as fcb
+
+        self.fcb = fcb
+        self.name = name
+        self.w = wl.cfg2() if name == "cfg2" else wl.cfg4()
+        self.n, self.d = self.w.n, self.w.d
+
+    def describe(self):
+        if self.name == "cfg2":
+            what = "2-D ECDF at the points, ties (1024 levels), y~U(0,1), delta=(1,-1) + ESF"
+        else:
+            what = "2-D Laplacian KDE density + kernel-regression numerators at the points, h=0.1"
+        return {"workload": self.name, "what": what, "n_points": self.n, "dims": self.d,
+                "l2": "inputs fit in L2 (launch/latency-bound config)" if self.n * 16 < 126e6
+                else f"inputs larger than L2 ({self.n * 16 / 1e9:.2f} GB points)"}
+
+    def _sample(self, x, y):
+        fcb = self.fcb
+        if self.name == "cfg2":
+            return fcb.Sample(x, y, None, False)
+        return fcb.Sample(x, None, (True, True), True)
+
+    def to_device(self):
+        import torch
+
+        x = torch.from_numpy(self.w.points).cuda()
+        yv = self.w.weights if self.name == "cfg2" else self.w.extra["y"]
+        self.y_dev = torch.from_numpy(yv).cuda()
+        self.s_dev = self._sample(x, self.y_dev)
+
+    def to_pinned(self):
+        import torch
+
+        xp = torch.from_numpy(self.w.points).pin_memory()
+        yv = self.w.weights if self.name == "cfg2" else self.w.extra["y"]
+        self.y_pin = torch.from_numpy(yv).pin_memory()
+        self.s_pin = self._sample(xp, self.y_pin)
+        nout = 2 * self.n
+        self.out_pinned = torch.empty(nout, dtype=torch.float64).pin_memory()
+        self.h2d_bytes = self.w.points.nbytes + yv.nbytes
+        self.d2h_bytes = nout * 8
+
+    def _run(self, s, y):
+        fcb = self.fcb
+        if self.name == "cfg2":
+            a = fcb.ecdf_at_points(s, fcb.DeltaVector(self.w.delta)).values
+            b = fcb.esf_at_points(s).values
+            return a, b
+        num = fcb.kde_numerators(s, [None, y], fcb.Bandwidth.diag(self.w.h))
+        return num[0], num[1]
+
+    def step(self):
+        self._run(self.s_dev, self.y_dev)
+
+    def step_e2e(self):
+        a, b = self._run(self.s_pin, self.y_pin)
+        self.out_pinned[: self.n].copy_(a, non_blocking=True)
+        self.out_pinned[self.n:].copy_(b, non_blocking=True)
+
+    def bytes_per_launch(self):
+        n = self.n
+        b = radix_bytes(n)
+        if self.name == "cfg2":
+            b.update({"pts_rank_scatter": (8 + 8 + 8) * n, "pts_gather": (8 + 8 + 8) * n})
+        else:
+            # level-2 solvers: per source (id + 2 positions + 2 psi) and per query (threshold
+            # pair + list entry + 2-channel output read-modify-write)
+            b.update({"pts_level2_chunk": (4 + 8 + 16) * n + (8 + 4 + 32) * n,
+                      "pts_level2_block": (4 + 8 + 16) * n + (8 + 4 + 32) * n,
+                      "pts_psi": (16 + 8 + 8 + 16) * n, "pts_kde_accum": (8 + 16 + 32) * n})
+        return b
+
+    def cpu_sample(self, threads):
+        import oracle
+
+        used = oracle.set_threads(threads)
+        if self.name == "cfg2":
+            t0 = time.perf_counter()
+            oracle.ecdf_at_points(self.w.points, self.w.weights, self.w.delta)
+            oracle.esf_at_points(self.w.points, self.w.weights)
+            dt = time.perf_counter() - t0
+            return self.n / dt, used, "full config (ECDF + ESF via the exact rank lattice)", dt
+        m = 1_000_000
+        t0 = time.perf_counter()
+        oracle.kde_dnc_laplacian(self.w.points[:m], None, self.w.h)
+        oracle.kde_dnc_laplacian(self.w.points[:m], self.w.extra["y"][:m], self.w.h)
+        dt = time.perf_counter() - t0
+        return m / dt, 1, f"first {m} points, both numerators (the C recursion is single-threaded)", dt
+
+
 def make_workload(name):
     if name in ("cfg1", "cfg3", "cfg5", "cfg5a", "cfg5b"):
         return GridWorkload(name)
+    if name in ("cfg2", "cfg4"):
+        return PointsWorkload(name)
     raise SystemExit(f"unknown workload {name!r}")
 
 

@@ -45,10 +45,7 @@ from .kernels import (
     uniform,
 )
 
-try:  # at-points path (ranking + dominance kernels)
-    from .dnc import ecdf_dnc, kde_dnc
-    from .points import ecdf_at_points, esf_at_points, kernel_regression
-except ImportError:  # pragma: no cover - modules land incrementally
-    pass
+from .dnc import ecdf_dnc, kde_dnc
+from .points import ecdf_at_points, esf_at_points, kde_numerators, kernel_regression
 
 __version__ = "0.1.0"

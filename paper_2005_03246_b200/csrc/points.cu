@@ -1,25 +1,1032 @@
-// At-points path entry points (placeholder until the ranking / dominance kernels land).
+// At-points path (subsystem 4): generalized ECDF / ESF at the sample points with ties
+// (Eq. 3 as naive.py:90-114 implements it), the strict-dominance ECDF of ecdf_dnc
+// (dnc.py:531-561) and the all-delta Laplacian KDE of kde_dnc (dnc.py:635-690).
+//
+// Routes:
+//  * rank lattice (any d, few distinct levels — BASELINE config 2): dense ranks per dimension
+//    are bin indices on the grid of distinct values, so the grid engine (scatter -> directional
+//    scans) computes every orthant sum and a gather reads each point's own node.  This is the
+//    reference's own exact route for tied data.
+//  * rank-space dominance, d = 2 (continuous data — config 4): after ranking, the points are a
+//    permutation in [0,n)^2.  A 3-level decomposition answers every lower-left query
+//    F(t) = sum_i psi_i [p0_i < Q0_t][p1_i < Q1_t]:
+//      level 1: chunks of S = 4096 consecutive p1 positions x blocks of S p0 positions form a
+//               coarse (n/S)^2 grid; a 2-D inclusive prefix gives all fully-dominated cells;
+//      level 2: the query's own chunk and own block are solved inside one CTA each: the
+//               <= 4096 sources are laid out in shared memory by local slot / local rank, a
+//               64x64 sub-grid prefix covers full sub-cells, and <= 2 x 63 direct checks finish.
+//    The four sign codes of the KDE (dnc.py:459-468) are the four orientations of the same
+//    problem (flip p0 and/or p1), sharing one ranking and one chunk/block grouping.
+//  * brute force O(n^2) tiles (d >= 3 without a feasible rank lattice; SURVEY §8f #3 widens
+//    this later).
 #include "common.cuh"
+#include "scan.cuh"
+#include "sort.cuh"
+
+namespace fcg {
+
+namespace {
+
+constexpr int LS = 12;
+constexpr int S = 1 << LS;    // level-1 block / chunk size
+constexpr int SUBL = 6;
+constexpr int SUB = 1 << SUBL;  // level-2 sub-block size
+constexpr int NSUB = S / SUB;   // 64
+constexpr int kSolverThreads = 512;
+constexpr int64_t kMaxDominanceN = int64_t(1) << 26;  // coarse grid (n/S)^2 must fit in HBM
+
+// ------------------------------------------------------------------------------------------
+// helpers
+__global__ void fill_f64(double *p, int64_t n, double v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void gather_sorted_w(const int32_t *__restrict__ order, const double *__restrict__ w,
+                                int64_t n, double *__restrict__ ws) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    ws[p] = w ? w[order[p]] : 1.0;
+}
+
+// ------------------------------------------------------------------------------------------
+// rank lattice route
+struct RankLat {
+  int d;
+  const int32_t *dense[FCG_MAX_DIM];
+  int shift[FCG_MAX_DIM];      // cell = dense - shift (ECDF delta=-1: -1, ESF: +1)
+  int64_t dims[FCG_MAX_DIM];
+  int64_t stride[FCG_MAX_DIM];
+};
+
+template <bool UNIT>
+__global__ void rank_scatter_kernel(RankLat r, int64_t n, const double *__restrict__ w,
+                                    void *lat) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t flat = 0;
+    bool live = true;
+    for (int k = 0; k < r.d; ++k) {
+      const int64_t c = (int64_t)r.dense[k][i] - r.shift[k];
+      live = live && c >= 0 && c < r.dims[k];
+      flat += c * r.stride[k];
+    }
+    if (!live) continue;
+    if (UNIT) atomicAdd(static_cast<int *>(lat) + flat, 1);
+    else atomicAdd(static_cast<double *>(lat) + flat, w[i]);
+  }
+}
+
+template <typename T>
+__global__ void rank_gather_kernel(RankLat r, int64_t n, const T *__restrict__ lat, double div,
+                                   double *__restrict__ out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t flat = 0;
+    for (int k = 0; k < r.d; ++k) flat += (int64_t)r.dense[k][t] * r.stride[k];
+    double v = (double)lat[flat];
+    if (div > 0.0) v = v / div;
+    out[t] = v;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// dominance, d = 2
+struct Dom2 {
+  int64_t n, nq, P, npad;
+  int nch;
+  int f0, f1;
+  const int32_t *pos0, *pos1;     // unflipped source positions (permutations of [0, n))
+  const int32_t *bychunk;         // sources sorted by (p1 >> LS, p0)
+  const int32_t *byblock;         // sources sorted by (p0 >> LS, p1)
+  const double *psi;              // [nch][n]
+  const int32_t *Q0f, *Q1f;       // query thresholds in the flipped frame, in [0, npad]
+  double *out;                    // [nch][nq]
+  double *G;                      // [P][P][nch] coarse grid
+  const int32_t *qc_list, *qc_start;  // queries bucketed by chunk(Q1f) (P + 1 buckets)
+  const int32_t *qb_list, *qb_start;  // queries bucketed by block(Q0f)
+};
+
+__device__ __forceinline__ int32_t flipp(int32_t p, int f, int64_t npad) {
+  return f ? (int32_t)(npad - 1 - p) : p;
+}
+
+// coarse rows: CTA per flipped chunk c; row[b][ch] accumulated in shared memory
+__global__ void __launch_bounds__(512) coarse_rows_smem(Dom2 D) {
+  extern __shared__ double s_row[];  // [P][nch]
+  const int64_t c = blockIdx.x;
+  const int64_t g = D.f1 ? D.P - 1 - c : c;
+  const int64_t P = D.P;
+  for (int64_t i = threadIdx.x; i < P * D.nch; i += blockDim.x) s_row[i] = 0.0;
+  __syncthreads();
+  const int64_t lo = g * S, hi = (g + 1) * S < D.n ? (g + 1) * S : D.n;
+  for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) {
+    const int32_t src = D.bychunk[k];
+    const int64_t b = flipp(D.pos0[src], D.f0, D.npad) >> LS;
+    for (int ch = 0; ch < D.nch; ++ch) atomicAdd(&s_row[b * D.nch + ch], D.psi[ch * D.n + src]);
+  }
+  __syncthreads();
+  double *row = D.G + c * P * D.nch;
+  for (int64_t i = threadIdx.x; i < P * D.nch; i += blockDim.x) row[i] = s_row[i];
+}
+
+__global__ void coarse_atomic(Dom2 D) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < D.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = flipp(D.pos1[i], D.f1, D.npad) >> LS;
+    const int64_t b = flipp(D.pos0[i], D.f0, D.npad) >> LS;
+    for (int ch = 0; ch < D.nch; ++ch)
+      atomicAdd(&D.G[(c * D.P + b) * D.nch + ch], D.psi[ch * D.n + i]);
+  }
+}
+
+// out = inclusive-prefix coarse grid at (chunk(Q1f) - 1, block(Q0f) - 1)
+__global__ void coarse_query(Dom2 D) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < D.nq;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c = D.Q1f[t] >> LS, b = D.Q0f[t] >> LS;
+    c = c > D.P ? D.P : c;
+    b = b > D.P ? D.P : b;
+    for (int ch = 0; ch < D.nch; ++ch) {
+      double v = 0.0;
+      if (c > 0 && b > 0) v = D.G[((c - 1) * D.P + (b - 1)) * D.nch + ch];
+      D.out[ch * D.nq + t] = v;
+    }
+  }
+}
+
+// keys for query bucketing: chunk(Q1f) or block(Q0f), clamped to P
+__global__ void query_keys(Dom2 D, int32_t *kc, int32_t *kb) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < D.nq;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c = D.Q1f[t] >> LS, b = D.Q0f[t] >> LS;
+    kc[t] = (int32_t)(c > D.P ? D.P : c);
+    kb[t] = (int32_t)(b > D.P ? D.P : b);
+  }
+}
+
+__global__ void bucket_count(const int32_t *__restrict__ key, int64_t n, int32_t *cnt) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[key[t]], 1);
+}
+
+__global__ void bucket_fill(const int32_t *__restrict__ key, int64_t n, int32_t *cursor,
+                            int32_t *list) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    list[atomicAdd(&cursor[key[t]], 1)] = (int32_t)t;
+}
+
+// Level-2 solver.  CHUNK: CTA per flipped chunk c, sources of that chunk; slot X = local p1f,
+// rank Y = rank of p0f within the chunk; query (qx = Q1f - cS, qy = #sources with p0f < Q0f).
+// BLOCK: CTA per flipped block b; slot X = local p0f, rank Y = rank of p1f within the block;
+// query (qx = Q0f - bS, qy = #sources with p1f < chunk(Q1f) * S).
+template <bool CHUNK, int NCH>
+__global__ void __launch_bounds__(kSolverThreads) level2_solver(Dom2 D) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double *s_sub = reinterpret_cast<double *>(smem);             // [NCH][NSUB][NSUB]
+  double *s_psi = s_sub + NCH * NSUB * NSUB;                    // [NCH][S] by slot X
+  int32_t *s_key = reinterpret_cast<int32_t *>(s_psi + NCH * S);  // [S] sorted keys by rank Y
+  int16_t *s_yofx = reinterpret_cast<int16_t *>(s_key + S);     // [S]
+  int16_t *s_xofy = s_yofx + S;                                 // [S]
+
+  const int64_t cb = blockIdx.x;  // flipped chunk (CHUNK) or flipped block (BLOCK)
+  const int fslot = CHUNK ? D.f1 : D.f0;
+  const int frank = CHUNK ? D.f0 : D.f1;
+  const int64_t g = fslot ? D.P - 1 - cb : cb;  // unflipped group index
+  const int64_t lo = g * S;
+  const int64_t Sg = (lo + S < D.n ? S : D.n - lo);
+  const int32_t *grp = (CHUNK ? D.bychunk : D.byblock) + lo;
+  const int32_t *slotpos = CHUNK ? D.pos1 : D.pos0;
+  const int32_t *rankpos = CHUNK ? D.pos0 : D.pos1;
+
+  for (int i = threadIdx.x; i < NCH * NSUB * NSUB; i += blockDim.x) s_sub[i] = 0.0;
+  for (int i = threadIdx.x; i < S; i += blockDim.x) {
+    s_yofx[i] = -1;
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) s_psi[ch * S + i] = 0.0;
+  }
+  __syncthreads();
+  for (int64_t k = threadIdx.x; k < Sg; k += blockDim.x) {
+    const int32_t src = grp[k];
+    const int y = frank ? (int)(Sg - 1 - k) : (int)k;
+    int x = slotpos[src] - (int32_t)lo;
+    if (fslot) x = S - 1 - x;
+    s_yofx[x] = (int16_t)y;
+    s_xofy[y] = (int16_t)x;
+    s_key[y] = flipp(rankpos[src], frank, D.npad);
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) s_psi[ch * S + x] = D.psi[ch * D.n + src];
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < S; x += blockDim.x) {
+    const int y = s_yofx[x];
+    if (y >= 0) {
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch)
+        atomicAdd(&s_sub[(ch * NSUB + (x >> SUBL)) * NSUB + (y >> SUBL)], s_psi[ch * S + x]);
+    }
+  }
+  __syncthreads();
+  // inclusive 2-D prefix of the sub-grid: rows (over y-sub index), then columns
+  for (int r = threadIdx.x; r < NCH * NSUB; r += blockDim.x) {
+    double *row = s_sub + r * NSUB;
+    double run = 0.0;
+    for (int v = 0; v < NSUB; ++v) { run += row[v]; row[v] = run; }
+  }
+  __syncthreads();
+  for (int cidx = threadIdx.x; cidx < NCH * NSUB; cidx += blockDim.x) {
+    const int ch = cidx / NSUB, v = cidx % NSUB;
+    double run = 0.0;
+    for (int u = 0; u < NSUB; ++u) {
+      double *p = s_sub + (ch * NSUB + u) * NSUB + v;
+      run += *p;
+      *p = run;
+    }
+  }
+  __syncthreads();
+
+  const int32_t *qlist = CHUNK ? D.qc_list : D.qb_list;
+  const int32_t q0 = (CHUNK ? D.qc_start : D.qb_start)[cb];
+  const int32_t q1 = (CHUNK ? D.qc_start : D.qb_start)[cb + 1];
+  for (int32_t qi = q0 + threadIdx.x; qi < q1; qi += blockDim.x) {
+    const int32_t t = qlist[qi];
+    int qx, qy;
+    int32_t ythr;
+    if (CHUNK) {
+      qx = (int)(D.Q1f[t] - cb * S);
+      ythr = D.Q0f[t];
+    } else {
+      qx = (int)(D.Q0f[t] - cb * S);
+      int64_t c = D.Q1f[t] >> LS;
+      ythr = (int32_t)((c > D.P ? D.P : c) * S);
+    }
+    // qy = #keys < ythr among the Sg sorted keys
+    int a = 0, bnd = (int)Sg;
+    while (a < bnd) {
+      const int mid = (a + bnd) >> 1;
+      if (s_key[mid] < ythr) a = mid + 1;
+      else bnd = mid;
+    }
+    qy = a;
+    const int u = qx >> SUBL, v = qy >> SUBL;
+    double acc[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch)
+      acc[ch] = (u > 0 && v > 0) ? s_sub[(ch * NSUB + (u - 1)) * NSUB + (v - 1)] : 0.0;
+    for (int x = u << SUBL; x < qx; ++x) {  // partial slot sub-range, any rank < qy
+      const int y = s_yofx[x];
+      if (y >= 0 && y < qy) {
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) acc[ch] += s_psi[ch * S + x];
+      }
+    }
+    const int xfull = u << SUBL;
+    for (int y = v << SUBL; y < qy; ++y) {  // partial rank sub-range, full slot sub-blocks
+      const int x = s_xofy[y];
+      if (x < xfull) {
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) acc[ch] += s_psi[ch * S + x];
+      }
+    }
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) D.out[ch * D.nq + t] += acc[ch];
+  }
+}
+
+size_t level2_smem(int nch) {
+  return (size_t)nch * NSUB * NSUB * 8 + (size_t)nch * S * 8 + (size_t)S * 4 + (size_t)S * 4;
+}
+
+// grouping keys: key[p] = pos_other[order[p]] >> LS, val[p] = order[p]
+__global__ void group_keys(const int32_t *__restrict__ order, const int32_t *__restrict__ pos_other,
+                           int64_t n, uint64_t *keys, int32_t *vals) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = order[p];
+    keys[p] = (uint64_t)(pos_other[i] >> LS);
+    vals[p] = i;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// brute force (d >= 3): CTA = 256 queries, source tiles staged in shared memory
+enum BruteMode { BR_ECDF = 0, BR_KDE = 1 };
+
+struct Brute {
+  int64_t n;
+  int d;
+  const double *x;
+  const double *w;   // [nw][n] or NULL
+  int nw;
+  int sign[FCG_MAX_DIM];  // ECDF: +1 <=, -1 <, 2 = strictly greater (survival)
+  double inv_h[FCG_MAX_DIM];
+  double *out;       // [nw][n]
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(256) brute_kernel(Brute B) {
+  __shared__ double s_x[256 * FCG_MAX_DIM];
+  __shared__ double s_w[2][256];
+  const int64_t t = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const bool live = t < B.n;
+  double xt[FCG_MAX_DIM];
+  for (int k = 0; k < B.d; ++k) xt[k] = live ? B.x[t * B.d + k] : 0.0;
+  double acc[2] = {0.0, 0.0};
+  for (int64_t base = 0; base < B.n; base += 256) {
+    const int64_t i = base + threadIdx.x;
+    __syncthreads();
+    if (i < B.n) {
+      for (int k = 0; k < B.d; ++k) s_x[threadIdx.x * B.d + k] = B.x[i * B.d + k];
+      for (int v = 0; v < B.nw; ++v) s_w[v][threadIdx.x] = B.w ? B.w[v * B.n + i] : 1.0;
+    }
+    __syncthreads();
+    const int cnt = (int)((B.n - base) < 256 ? (B.n - base) : 256);
+    for (int j = 0; j < cnt; ++j) {
+      const double *xs = s_x + j * B.d;
+      if (MODE == BR_ECDF) {
+        bool ok = true;
+        for (int k = 0; k < B.d; ++k) {
+          const double a = xs[k], z = xt[k];
+          const int s = B.sign[k];
+          ok = ok && (s == 1 ? a <= z : (s == -1 ? a < z : a > z));
+        }
+        if (ok)
+          for (int v = 0; v < B.nw; ++v) acc[v] += s_w[v][j];
+      } else {
+        if (base + j == t) continue;  // self term added in closed form by the caller
+        double e = 0.0;
+        for (int k = 0; k < B.d; ++k) e += fabs(xs[k] - xt[k]) * B.inv_h[k];
+        const double kv = exp(-e);
+        for (int v = 0; v < B.nw; ++v) acc[v] += s_w[v][j] * kv;
+      }
+    }
+  }
+  if (live)
+    for (int v = 0; v < B.nw; ++v) B.out[v * B.n + t] = acc[v];
+}
+
+// ------------------------------------------------------------------------------------------
+// KDE epilogue pieces (dnc.py:661-686)
+struct KdeP {
+  int d;
+  double c[FCG_MAX_DIM], a[FCG_MAX_DIM];  // a_k = s_k / h_k
+};
+
+// expo[i] = sum_k (x_ik - c_k) * a_k ; psi[v][i] = w[v][i] * exp(expo[i])
+__global__ void kde_psi_kernel(const double *__restrict__ x, int64_t n, KdeP p,
+                               const double *__restrict__ w, int nw, double *__restrict__ expo,
+                               double *__restrict__ psi) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < p.d; ++k) s += (x[i * p.d + k] - p.c[k]) * p.a[k];
+    expo[i] = s;
+    const double e = exp(s);
+    for (int v = 0; v < nw; ++v) psi[v * n + i] = (w ? w[v * n + i] : 1.0) * e;
+  }
+}
+
+// out[v][t] (+)= exp(-expo[t]) * F[v][t]
+__global__ void kde_accum_kernel(int64_t n, int nw, const double *__restrict__ expo,
+                                 const double *__restrict__ F, double *__restrict__ out, int first) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const double z = exp(-expo[t]);
+    for (int v = 0; v < nw; ++v) {
+      const double r = z * F[v * n + t];
+      out[v * n + t] = first ? r : out[v * n + t] + r;
+    }
+  }
+}
+
+// out[v][t] = (out[v][t] + w[v][t]) * scale   (self term, then the shared normalisation)
+__global__ void kde_finish_kernel(int64_t n, int nw, const double *__restrict__ w, double scale,
+                                  double *__restrict__ out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    for (int v = 0; v < nw; ++v) {
+      double r = out[v * n + t] + (w ? w[v * n + t] : 1.0);
+      out[v * n + t] = r * scale;
+    }
+}
+
+// final: out[t] = (out[t] + (self ? w[t] : 0)) / div
+__global__ void finish_ecdf_kernel(double *__restrict__ out, int64_t n,
+                                   const double *__restrict__ w, int include_self, double div) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    double r = out[t];
+    if (include_self) r = r + (w ? w[t] : 1.0);
+    if (div > 0.0) r = r / div;
+    out[t] = r;
+  }
+}
+
+// d == 1 gather from an inclusive sorted prefix (forward) or suffix (reverse) scan
+// mode 0: out[t] = q > 0 ? incl[q-1] : 0   (sources at sorted positions < q)
+// mode 1: out[t] = q < n ? suf[q] : 0      (sources at sorted positions >= q)
+__global__ void gather1d_kernel(const double *__restrict__ scan, const int32_t *__restrict__ q,
+                                int64_t n, int mode, double *__restrict__ out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t qq = q[t];
+    out[t] = mode == 0 ? (qq > 0 ? scan[qq - 1] : 0.0) : (qq < n ? scan[qq] : 0.0);
+  }
+}
+
+// srt[p] = vals[order[p]] (vals == NULL: ones); cpy = copy for the in-place scan
+__global__ void permute_kernel(const double *__restrict__ vals, const int32_t *__restrict__ order,
+                               int64_t n, double *__restrict__ srt, double *__restrict__ cpy) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const double v = vals ? vals[order[p]] : 1.0;
+    srt[p] = v;
+    cpy[p] = v;
+  }
+}
+
+// dst[order[p]] = incl[p] - srt[p]: "cumsum - self" of dnc.py:543-547 and dnc.py:572-579
+__global__ void excl_scatter_kernel(const double *__restrict__ incl, const double *__restrict__ srt,
+                                    const int32_t *__restrict__ order, int64_t n,
+                                    double *__restrict__ dst) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    dst[order[p]] = incl[p] - srt[p];
+}
+
+// flipped-frame thresholds: Q0f = f(base0) etc.  kind: 0 = copy, 1 = npad-1-pos (self, flipped),
+// 2 = npad - q (count-type threshold, flipped)
+__global__ void make_q_kernel(const int32_t *__restrict__ a, int64_t n, int kind, int64_t npad,
+                              int32_t *__restrict__ out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = a[t];
+    out[t] = kind == 0 ? v : (kind == 1 ? (int32_t)(npad - 1 - v) : (int32_t)(npad - v));
+  }
+}
+
+__global__ void adjacent_equal_kernel(const uint64_t *__restrict__ keys, int64_t n, int32_t *flag) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + 1; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    if (keys[p] == keys[p - 1]) *flag = 1;
+}
+
+// ------------------------------------------------------------------------------------------
+// host-side composition
+
+struct Ranked {        // per-dimension ranking results (device)
+  int32_t *order, *pos, *lower, *upper, *dense;
+};
+
+struct PtsWs {
+  // ranking
+  uint64_t *k;
+  int32_t *v;
+  RadixWs rw;
+  int32_t *heads, *start, *ndist;
+  Ranked r[FCG_MAX_DIM];
+  // d = 2 dominance
+  int32_t *bychunk, *byblock, *Q0f, *Q1f, *kc, *kb, *qc_list, *qc_start, *qb_list, *qb_start,
+      *cursor;
+  double *G, *psi, *expo, *F, *lat, *scratch;
+  int64_t P, npad, lat_cells;
+};
+
+int64_t pad_of(int64_t n) { return ceil_div(n, S) * S; }
+
+void carve(Workspace &W, PtsWs &p, int64_t n, int d, int nch, bool need_dom, bool need_kde,
+           int64_t lat_cells) {
+  p.k = W.take<uint64_t>(n);
+  p.v = W.take<int32_t>(n);
+  p.rw.keys_alt = W.take<uint64_t>(n);
+  p.rw.vals_alt = W.take<int32_t>(n);
+  p.rw.hist = W.take<int32_t>(radix_ws_hist_elems(n));
+  p.rw.partial = W.take<int32_t>(scan_ws_partial_elems(256 * (n / kSortTile + 1) + n + 2));
+  p.heads = W.take<int32_t>(n);
+  p.start = W.take<int32_t>(n + 1);
+  p.ndist = W.take<int32_t>(FCG_MAX_DIM);
+  for (int k = 0; k < d; ++k) {
+    p.r[k].order = W.take<int32_t>(n);
+    p.r[k].pos = W.take<int32_t>(n);
+    p.r[k].lower = W.take<int32_t>(n);
+    p.r[k].upper = W.take<int32_t>(n);
+    p.r[k].dense = W.take<int32_t>(n);
+  }
+  p.P = ceil_div(n, S);
+  p.npad = p.P * S;
+  p.lat_cells = lat_cells;
+  if (lat_cells > 0) {
+    p.lat = W.take<double>(lat_cells);
+  } else {
+    p.lat = nullptr;
+  }
+  p.scratch = W.take<double>(scan_scratch_bound());
+  if (need_dom) {
+    p.bychunk = W.take<int32_t>(n);
+    p.byblock = W.take<int32_t>(n);
+    p.Q0f = W.take<int32_t>(n);
+    p.Q1f = W.take<int32_t>(n);
+    p.kc = W.take<int32_t>(n);
+    p.kb = W.take<int32_t>(n);
+    p.qc_list = W.take<int32_t>(n);
+    p.qb_list = W.take<int32_t>(n);
+    p.qc_start = W.take<int32_t>(p.P + 2);
+    p.qb_start = W.take<int32_t>(p.P + 2);
+    p.cursor = W.take<int32_t>(p.P + 2);
+    p.G = W.take<double>(p.P * p.P * nch);
+    p.psi = W.take<double>((size_t)n * nch);
+    p.F = W.take<double>((size_t)n * nch);
+  }
+  if (need_kde) p.expo = W.take<double>(n);
+}
+
+int rank_dim(const double *x, int64_t n, int d, int k, PtsWs &p, cudaStream_t st) {
+  FCG_TRY(radix_init_f64(x + k, n, d, p.k, p.v, st));
+  FCG_TRY(radix_sort_pairs(p.k, p.v, n, 0, 64, p.rw, st));
+  FCG_CUDA_TRY(cudaMemcpyAsync(p.r[k].order, p.v, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+  return rank_outputs(p.k, p.v, n, p.r[k].pos, p.r[k].lower, p.r[k].upper, p.r[k].dense, p.heads,
+                      p.start, p.rw.partial, p.ndist + k, st);
+}
+
+int group_by(const int32_t *order, const int32_t *pos_other, int64_t n, int64_t P, int32_t *out,
+             PtsWs &p, cudaStream_t st) {
+  {
+    FCG_PROF("pts_group_keys", st);
+    group_keys<<<grid_for(n, 256), 256, 0, st>>>(order, pos_other, n, p.k, p.v);
+    FCG_LAUNCH_CHECK();
+  }
+  int bits = 0;
+  while ((int64_t(1) << bits) < P) ++bits;
+  FCG_TRY(radix_sort_pairs(p.k, p.v, n, 0, bits < 1 ? 8 : ((bits + 7) / 8) * 8, p.rw, st));
+  FCG_CUDA_TRY(cudaMemcpyAsync(out, p.v, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+  return FCG_OK;
+}
+
+int bucket(const int32_t *keys, int64_t n, int64_t nb, int32_t *list, int32_t *start,
+           int32_t *cursor, PtsWs &p, cudaStream_t st) {
+  FCG_CUDA_TRY(cudaMemsetAsync(start, 0, (size_t)(nb + 1) * 4, st));
+  {
+    FCG_PROF("pts_bucket", st);
+    bucket_count<<<grid_for(n, 256), 256, 0, st>>>(keys, n, start);
+    FCG_LAUNCH_CHECK();
+  }
+  FCG_TRY(scan_i32(start, start, nb + 1, false, p.rw.partial, st));
+  FCG_CUDA_TRY(cudaMemcpyAsync(cursor, start, (size_t)(nb + 1) * 4, cudaMemcpyDeviceToDevice, st));
+  FCG_PROF("pts_bucket", st);
+  bucket_fill<<<grid_for(n, 256), 256, 0, st>>>(keys, n, cursor, list);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}
+
+// Lower-left dominance sums in one orientation (f0, f1) of the shared ranking.
+// psi: [nch][n] (nch <= 2), thresholds already in p.Q0f / p.Q1f; out: [nch][n].
+int dom2d(PtsWs &p, int64_t n, int nch, int f0, int f1, const double *psi, double *out,
+          cudaStream_t st) {
+  Dom2 D;
+  D.n = n;
+  D.nq = n;
+  D.P = p.P;
+  D.npad = p.npad;
+  D.nch = nch;
+  D.f0 = f0;
+  D.f1 = f1;
+  D.pos0 = p.r[0].pos;
+  D.pos1 = p.r[1].pos;
+  D.bychunk = p.bychunk;
+  D.byblock = p.byblock;
+  D.psi = psi;
+  D.Q0f = p.Q0f;
+  D.Q1f = p.Q1f;
+  D.out = out;
+  D.G = p.G;
+  D.qc_list = p.qc_list;
+  D.qc_start = p.qc_start;
+  D.qb_list = p.qb_list;
+  D.qb_start = p.qb_start;
+  const int64_t P = p.P;
+  {
+    FCG_PROF("pts_query_keys", st);
+    query_keys<<<grid_for(n, 256), 256, 0, st>>>(D, p.kc, p.kb);
+    FCG_LAUNCH_CHECK();
+  }
+  FCG_TRY(bucket(p.kc, n, P + 1, p.qc_list, p.qc_start, p.cursor, p, st));
+  FCG_TRY(bucket(p.kb, n, P + 1, p.qb_list, p.qb_start, p.cursor, p, st));
+  // level 1: coarse grid
+  const size_t row_smem = (size_t)P * nch * sizeof(double);
+  if (row_smem <= 96 * 1024) {
+    FCG_PROF("pts_coarse_hist", st);
+    FCG_CUDA_TRY(cudaFuncSetAttribute(coarse_rows_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(96 * 1024)));
+    coarse_rows_smem<<<(unsigned)P, 512, row_smem, st>>>(D);
+    FCG_LAUNCH_CHECK();
+  } else {
+    FCG_PROF("pts_coarse_hist", st);
+    FCG_CUDA_TRY(cudaMemsetAsync(p.G, 0, (size_t)P * P * nch * sizeof(double), st));
+    coarse_atomic<<<grid_for(n, 256), 256, 0, st>>>(D);
+    FCG_LAUNCH_CHECK();
+  }
+  LatShape gs;
+  gs.d = 3;
+  gs.dims[0] = P;
+  gs.dims[1] = P;
+  gs.dims[2] = nch;
+  Epi inplace;
+  FCG_TRY(scan_axis<double>(p.G, gs, 1, false, inplace, p.scratch, st));
+  FCG_TRY(scan_axis<double>(p.G, gs, 0, false, inplace, p.scratch, st));
+  {
+    FCG_PROF("pts_coarse_query", st);
+    coarse_query<<<grid_for(n, 256), 256, 0, st>>>(D);
+    FCG_LAUNCH_CHECK();
+  }
+  // level 2: own chunk, own block
+  const size_t sm = level2_smem(nch);
+  if (nch == 1) {
+    FCG_CUDA_TRY(cudaFuncSetAttribute(level2_solver<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    FCG_CUDA_TRY(cudaFuncSetAttribute(level2_solver<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    {
+      FCG_PROF("pts_level2_chunk", st);
+      level2_solver<true, 1><<<(unsigned)P, kSolverThreads, sm, st>>>(D);
+      FCG_LAUNCH_CHECK();
+    }
+    FCG_PROF("pts_level2_block", st);
+    level2_solver<false, 1><<<(unsigned)P, kSolverThreads, sm, st>>>(D);
+    FCG_LAUNCH_CHECK();
+  } else {
+    FCG_CUDA_TRY(cudaFuncSetAttribute(level2_solver<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    FCG_CUDA_TRY(cudaFuncSetAttribute(level2_solver<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    {
+      FCG_PROF("pts_level2_chunk", st);
+      level2_solver<true, 2><<<(unsigned)P, kSolverThreads, sm, st>>>(D);
+      FCG_LAUNCH_CHECK();
+    }
+    FCG_PROF("pts_level2_block", st);
+    level2_solver<false, 2><<<(unsigned)P, kSolverThreads, sm, st>>>(D);
+    FCG_LAUNCH_CHECK();
+  }
+  return FCG_OK;
+}
+
+int prep2d(const double *x, int64_t n, PtsWs &p, cudaStream_t st) {
+  FCG_TRY(rank_dim(x, n, 2, 0, p, st));
+  FCG_TRY(rank_dim(x, n, 2, 1, p, st));
+  FCG_TRY(group_by(p.r[0].order, p.r[1].pos, n, p.P, p.bychunk, p, st));
+  FCG_TRY(group_by(p.r[1].order, p.r[0].pos, n, p.P, p.byblock, p, st));
+  return FCG_OK;
+}
+
+// d == 1 dominance: dst[i] = sum over sorted positions before (rev: after) i of vals, as the
+// reference computes it (inclusive cumsum minus self).  lat: 2n doubles of scratch.
+int sorted_exclusive(const double *vals, const int32_t *order, int64_t n, bool rev, double *lat,
+                     double *scratch, double *dst, cudaStream_t st) {
+  {
+    FCG_PROF("pts_sorted_w", st);
+    permute_kernel<<<grid_for(n, 256), 256, 0, st>>>(vals, order, n, lat, lat + n);
+    FCG_LAUNCH_CHECK();
+  }
+  LatShape s1;
+  s1.d = 1;
+  s1.dims[0] = n;
+  Epi inplace;
+  FCG_TRY(scan_axis<double>(lat + n, s1, 0, rev, inplace, scratch, st));
+  FCG_PROF("pts_gather", st);
+  excl_scatter_kernel<<<grid_for(n, 256), 256, 0, st>>>(lat + n, lat, order, n, dst);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}
+
+int make_q(const int32_t *a, int64_t n, int kind, int64_t npad, int32_t *out, cudaStream_t st) {
+  FCG_PROF("pts_make_q", st);
+  make_q_kernel<<<grid_for(n, 256), 256, 0, st>>>(a, n, kind, npad, out);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}
+
+int check_pts(int64_t n, int32_t d) {
+  if (d < 1 || d > FCG_MAX_DIM) return fail(FCG_EUNSUPPORTED, "dimension out of range");
+  if (n < 0) return fail(FCG_EINVAL, "n must be >= 0");
+  if (n >= (int64_t(1) << 31) - 1) return fail(FCG_EUNSUPPORTED, "n must be < 2^31 - 1");
+  return FCG_OK;
+}
+
+// lattice budget for the rank-lattice route
+int64_t lattice_budget(int64_t n) {
+  int64_t b = 4 * n;
+  if (b < (int64_t(1) << 22)) b = int64_t(1) << 22;
+  if (b > (int64_t(1) << 30)) b = int64_t(1) << 30;
+  return b;
+}
+
+}  // namespace
+
+}  // namespace fcg
 
 using namespace fcg;
 
-extern "C" int fcg_rank_f64(const double *, int64_t, int64_t, int32_t *, int32_t *, int32_t *,
-                            int32_t *, int32_t *, void *, size_t *, void *) {
-  return fail(FCG_EUNSUPPORTED, "fcg_rank_f64: not built yet");
+extern "C" int fcg_distinct(const double *x, int64_t n, int32_t d, int32_t *flags, void *ws,
+                            size_t *ws_bytes, void *stream) {
+  FCG_TRY(check_pts(n, d));
+  Workspace W(ws);
+  uint64_t *k = W.take<uint64_t>(n);
+  int32_t *v = W.take<int32_t>(n);
+  RadixWs rw;
+  rw.keys_alt = W.take<uint64_t>(n);
+  rw.vals_alt = W.take<int32_t>(n);
+  rw.hist = W.take<int32_t>(radix_ws_hist_elems(n));
+  rw.partial = W.take<int32_t>(scan_ws_partial_elems(256 * (n / kSortTile + 1) + 2));
+  int32_t *dflag = W.take<int32_t>(FCG_MAX_DIM);
+  if (ws == nullptr) {
+    *ws_bytes = W.bytes();
+    return FCG_OK;
+  }
+  cudaStream_t st = as_stream(stream);
+  FCG_CUDA_TRY(cudaMemsetAsync(dflag, 0, FCG_MAX_DIM * 4, st));
+  for (int kd = 0; kd < d; ++kd) {
+    FCG_TRY(radix_init_f64(x + kd, n, d, k, v, st));
+    FCG_TRY(radix_sort_pairs(k, v, n, 0, 64, rw, st));
+    if (n > 1) {
+      FCG_PROF("pts_distinct", st);
+      adjacent_equal_kernel<<<grid_for(n, 256), 256, 0, st>>>(k, n, dflag + kd);
+      FCG_LAUNCH_CHECK();
+    }
+  }
+  int32_t h[FCG_MAX_DIM];
+  FCG_CUDA_TRY(cudaMemcpyAsync(h, dflag, FCG_MAX_DIM * 4, cudaMemcpyDeviceToHost, st));
+  FCG_CUDA_TRY(cudaStreamSynchronize(st));
+  for (int kd = 0; kd < d; ++kd) flags[kd] = h[kd] ? 0 : 1;
+  return FCG_OK;
 }
-extern "C" int fcg_distinct(const double *, int64_t, int32_t, int32_t *, void *, size_t *, void *) {
-  return fail(FCG_EUNSUPPORTED, "fcg_distinct: not built yet");
+
+extern "C" int fcg_ecdf_points(const double *x, int64_t n, int32_t d, const double *w,
+                               const int32_t *delta, int32_t survival, int32_t scaled,
+                               double *out, void *ws, size_t *ws_bytes, void *stream) {
+  FCG_TRY(check_pts(n, d));
+  if (!survival)
+    for (int k = 0; k < d; ++k)
+      if (delta[k] != 1 && delta[k] != -1) return fail(FCG_EINVAL, "delta entries must be -1 or +1");
+  // Workspace is sized for the worst case of the routes chosen at run time.
+  const bool dom_ok = (d == 2 && n <= kMaxDominanceN);
+  const int64_t budget = lattice_budget(n);
+  Workspace W(ws);
+  PtsWs p;
+  carve(W, p, n, d, 1, dom_ok, false, d == 1 ? n : budget);
+  if (ws == nullptr) {
+    *ws_bytes = W.bytes();
+    return FCG_OK;
+  }
+  if (n == 0) return FCG_OK;
+  cudaStream_t st = as_stream(stream);
+  const double div = scaled ? (double)n : 0.0;
+
+  if (d == 1) {  // sort, prefix (or suffix) scan of sorted weights, gather
+    FCG_TRY(rank_dim(x, n, 1, 0, p, st));
+    {
+      FCG_PROF("pts_sorted_w", st);
+      gather_sorted_w<<<grid_for(n, 256), 256, 0, st>>>(p.r[0].order, w, n, p.lat);
+      FCG_LAUNCH_CHECK();
+    }
+    LatShape s1;
+    s1.d = 1;
+    s1.dims[0] = n;
+    Epi inplace;
+    const bool rev = survival != 0;
+    FCG_TRY(scan_axis<double>(p.lat, s1, 0, rev, inplace, p.scratch, st));
+    const int32_t *q = survival ? p.r[0].upper : (delta[0] > 0 ? p.r[0].upper : p.r[0].lower);
+    {
+      FCG_PROF("pts_gather", st);
+      gather1d_kernel<<<grid_for(n, 256), 256, 0, st>>>(p.lat, q, n, survival ? 1 : 0, out);
+      FCG_LAUNCH_CHECK();
+    }
+    {
+      FCG_PROF("pts_finish", st);
+      finish_ecdf_kernel<<<grid_for(n, 256), 256, 0, st>>>(out, n, w, 0, div);
+      FCG_LAUNCH_CHECK();
+    }
+    return FCG_OK;
+  }
+
+  // rank every dimension; the distinct counts decide the route (host sync)
+  for (int k = 0; k < d; ++k) FCG_TRY(rank_dim(x, n, d, k, p, st));
+  int32_t nd[FCG_MAX_DIM];
+  FCG_CUDA_TRY(cudaMemcpyAsync(nd, p.ndist, d * 4, cudaMemcpyDeviceToHost, st));
+  FCG_CUDA_TRY(cudaStreamSynchronize(st));
+  double cells = 1.0;
+  for (int k = 0; k < d; ++k) cells *= (double)nd[k];
+
+  if (cells <= (double)budget) {  // rank lattice route
+    RankLat r;
+    LatShape s;
+    r.d = s.d = d;
+    bool rev[FCG_MAX_DIM];
+    int64_t stride = 1;
+    for (int k = d - 1; k >= 0; --k) {
+      r.dense[k] = p.r[k].dense;
+      r.shift[k] = survival ? 1 : (delta[k] > 0 ? 0 : -1);
+      r.dims[k] = s.dims[k] = nd[k];
+      r.stride[k] = stride;
+      stride *= nd[k];
+      rev[k] = survival != 0;
+    }
+    const bool unit = (w == nullptr);
+    {
+      FCG_PROF("lattice_zero", st);
+      FCG_CUDA_TRY(cudaMemsetAsync(p.lat, 0, (size_t)stride * (unit ? 4 : 8), st));
+    }
+    {
+      FCG_PROF("pts_rank_scatter", st);
+      if (unit) rank_scatter_kernel<true><<<grid_for(n, 256), 256, 0, st>>>(r, n, w, p.lat);
+      else rank_scatter_kernel<false><<<grid_for(n, 256), 256, 0, st>>>(r, n, w, p.lat);
+      FCG_LAUNCH_CHECK();
+    }
+    Epi inplace;
+    if (unit) {
+      FCG_TRY(scan_lattice<int32_t>(reinterpret_cast<int32_t *>(p.lat), s, rev, inplace,
+                                    reinterpret_cast<int32_t *>(p.scratch), st));
+      FCG_PROF("pts_gather", st);
+      rank_gather_kernel<int32_t><<<grid_for(n, 256), 256, 0, st>>>(
+          r, n, reinterpret_cast<const int32_t *>(p.lat), div, out);
+    } else {
+      FCG_TRY(scan_lattice<double>(p.lat, s, rev, inplace, p.scratch, st));
+      FCG_PROF("pts_gather", st);
+      rank_gather_kernel<double><<<grid_for(n, 256), 256, 0, st>>>(r, n, p.lat, div, out);
+    }
+    FCG_LAUNCH_CHECK();
+    return FCG_OK;
+  }
+
+  if (dom_ok) {  // d == 2 rank-space dominance
+    FCG_TRY(group_by(p.r[0].order, p.r[1].pos, n, p.P, p.bychunk, p, st));
+    FCG_TRY(group_by(p.r[1].order, p.r[0].pos, n, p.P, p.byblock, p, st));
+    if (survival) {  // [x_i > x_t] <=> flipped p_i < npad - upper_t
+      FCG_TRY(make_q(p.r[0].upper, n, 2, p.npad, p.Q0f, st));
+      FCG_TRY(make_q(p.r[1].upper, n, 2, p.npad, p.Q1f, st));
+    } else {
+      FCG_TRY(make_q(delta[0] > 0 ? p.r[0].upper : p.r[0].lower, n, 0, p.npad, p.Q0f, st));
+      FCG_TRY(make_q(delta[1] > 0 ? p.r[1].upper : p.r[1].lower, n, 0, p.npad, p.Q1f, st));
+    }
+    {
+      FCG_PROF("pts_psi", st);
+      if (w) FCG_CUDA_TRY(cudaMemcpyAsync(p.psi, w, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
+      else fill_f64<<<grid_for(n, 256), 256, 0, st>>>(p.psi, n, 1.0);
+      FCG_LAUNCH_CHECK();
+    }
+    FCG_TRY(dom2d(p, n, 1, survival, survival, p.psi, out, st));
+    FCG_PROF("pts_finish", st);
+    finish_ecdf_kernel<<<grid_for(n, 256), 256, 0, st>>>(out, n, w, 0, div);
+    FCG_LAUNCH_CHECK();
+    return FCG_OK;
+  }
+
+  // brute force
+  Brute B;
+  B.n = n;
+  B.d = d;
+  B.x = x;
+  B.w = w;
+  B.nw = 1;
+  B.out = out;
+  for (int k = 0; k < d; ++k) B.sign[k] = survival ? 2 : delta[k];
+  {
+    FCG_PROF("pts_brute", st);
+    brute_kernel<BR_ECDF><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(B);
+    FCG_LAUNCH_CHECK();
+  }
+  FCG_PROF("pts_finish", st);
+  finish_ecdf_kernel<<<grid_for(n, 256), 256, 0, st>>>(out, n, w, 0, div);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
 }
-extern "C" int fcg_ecdf_points(const double *, int64_t, int32_t, const double *, const int32_t *,
-                               int32_t, int32_t, double *, void *, size_t *, void *) {
-  return fail(FCG_EUNSUPPORTED, "fcg_ecdf_points: not built yet");
+
+extern "C" int fcg_dnc_ecdf(const double *x, int64_t n, int32_t d, const double *w,
+                            int32_t include_self, int32_t scaled, double *out, void *ws,
+                            size_t *ws_bytes, void *stream) {
+  FCG_TRY(check_pts(n, d));
+  const bool dom_ok = (d == 2 && n <= kMaxDominanceN);
+  Workspace W(ws);
+  PtsWs p;
+  carve(W, p, n, d < 2 ? d : 2, 1, dom_ok, false, d == 1 ? 2 * n : 0);
+  if (ws == nullptr) {
+    *ws_bytes = W.bytes();
+    return FCG_OK;
+  }
+  if (n == 0) return FCG_OK;
+  cudaStream_t st = as_stream(stream);
+  const double div = scaled ? (double)n : 0.0;
+  if (d == 1) {  // argsort, cumsum - self (dnc.py:543-547)
+    FCG_TRY(rank_dim(x, n, 1, 0, p, st));
+    FCG_TRY(sorted_exclusive(w, p.r[0].order, n, false, p.lat, p.scratch, out, st));
+  } else if (dom_ok) {
+    FCG_TRY(prep2d(x, n, p, st));
+    FCG_TRY(make_q(p.r[0].pos, n, 0, p.npad, p.Q0f, st));
+    FCG_TRY(make_q(p.r[1].pos, n, 0, p.npad, p.Q1f, st));
+    {
+      FCG_PROF("pts_psi", st);
+      if (w) FCG_CUDA_TRY(cudaMemcpyAsync(p.psi, w, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
+      else fill_f64<<<grid_for(n, 256), 256, 0, st>>>(p.psi, n, 1.0);
+      FCG_LAUNCH_CHECK();
+    }
+    FCG_TRY(dom2d(p, n, 1, 0, 0, p.psi, out, st));
+  } else {
+    Brute B;
+    B.n = n;
+    B.d = d;
+    B.x = x;
+    B.w = w;
+    B.nw = 1;
+    B.out = out;
+    for (int k = 0; k < d; ++k) B.sign[k] = -1;
+    FCG_PROF("pts_brute", st);
+    brute_kernel<BR_ECDF><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(B);
+    FCG_LAUNCH_CHECK();
+  }
+  FCG_PROF("pts_finish", st);
+  finish_ecdf_kernel<<<grid_for(n, 256), 256, 0, st>>>(out, n, w, include_self, div);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
 }
-extern "C" int fcg_dnc_ecdf(const double *, int64_t, int32_t, const double *, int32_t, int32_t,
-                            double *, void *, size_t *, void *) {
-  return fail(FCG_EUNSUPPORTED, "fcg_dnc_ecdf: not built yet");
-}
-extern "C" int fcg_kde_points_laplacian(const double *, int64_t, int32_t, const double *, int32_t,
-                                        const double *, const double *, double *, void *, size_t *,
-                                        void *) {
-  return fail(FCG_EUNSUPPORTED, "fcg_kde_points_laplacian: not built yet");
+
+extern "C" int fcg_kde_points_laplacian(const double *x, int64_t n, int32_t d, const double *w,
+                                        int32_t nw, const double *h, const double *centre,
+                                        double *out, void *ws, size_t *ws_bytes, void *stream) {
+  FCG_TRY(check_pts(n, d));
+  if (nw < 1 || nw > 2) return fail(FCG_EUNSUPPORTED, "nw must be 1 or 2 weight vectors per call");
+  const bool dom_ok = (d == 2 && n <= kMaxDominanceN);
+  Workspace W(ws);
+  PtsWs p;
+  carve(W, p, n, d < 2 ? d : 2, nw, dom_ok, true, d == 1 ? n * 2 : 0);
+  double *psi1 = nullptr, *F1 = nullptr;
+  if (d == 1) {
+    psi1 = W.take<double>((size_t)n * nw);
+    F1 = W.take<double>((size_t)n * nw);
+  }
+  if (ws == nullptr) {
+    *ws_bytes = W.bytes();
+    return FCG_OK;
+  }
+  if (n == 0) return FCG_OK;
+  for (int k = 0; k < d; ++k)
+    if (!(h[k] > 0.0)) return fail(FCG_EINVAL, "bandwidth must be > 0");
+  cudaStream_t st = as_stream(stream);
+  double prod_h = 1.0;
+  for (int k = 0; k < d; ++k) prod_h *= h[k];
+  const double scale = 1.0 / (std::ldexp(1.0, d) * (double)n * prod_h);
+
+  if (d >= 3 || !(d == 1 || dom_ok)) {
+    Brute B;
+    B.n = n;
+    B.d = d;
+    B.x = x;
+    B.w = w;
+    B.nw = nw;
+    B.out = out;
+    for (int k = 0; k < d; ++k) B.inv_h[k] = 1.0 / h[k];
+    {
+      FCG_PROF("pts_brute", st);
+      brute_kernel<BR_KDE><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(B);
+      FCG_LAUNCH_CHECK();
+    }
+    FCG_PROF("pts_finish", st);
+    kde_finish_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, nw, w, scale, out);
+    FCG_LAUNCH_CHECK();
+    return FCG_OK;
+  }
+
+  const int ncodes = 1 << d;
+  if (d == 2) FCG_TRY(prep2d(x, n, p, st));
+  else FCG_TRY(rank_dim(x, n, 1, 0, p, st));
+  for (int code = 0; code < ncodes; ++code) {
+    KdeP kp;
+    kp.d = d;
+    for (int k = 0; k < d; ++k) {
+      const double sgn = ((code >> k) & 1) ? -1.0 : 1.0;  // DeltaVector.from_code
+      kp.c[k] = centre[k];
+      kp.a[k] = sgn / h[k];
+    }
+    {
+      FCG_PROF("pts_psi", st);
+      kde_psi_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, kp, w, nw, p.expo,
+                                                       d == 2 ? p.psi : psi1);
+      FCG_LAUNCH_CHECK();
+    }
+    if (d == 2) {
+      const int f0 = code & 1, f1 = (code >> 1) & 1;
+      FCG_TRY(make_q(p.r[0].pos, n, f0, p.npad, p.Q0f, st));
+      FCG_TRY(make_q(p.r[1].pos, n, f1, p.npad, p.Q1f, st));
+      FCG_TRY(dom2d(p, n, nw, f0, f1, p.psi, p.F, st));
+    } else {  // d == 1: code 0 = strictly below (prefix), code 1 = strictly above (suffix)
+      for (int v = 0; v < nw; ++v)
+        FCG_TRY(sorted_exclusive(psi1 + (size_t)v * n, p.r[0].order, n, code == 1, p.lat,
+                                 p.scratch, F1 + (size_t)v * n, st));
+    }
+    FCG_PROF("pts_kde_accum", st);
+    kde_accum_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, nw, p.expo, d == 2 ? p.F : F1, out,
+                                                       code == 0);
+    FCG_LAUNCH_CHECK();
+  }
+  FCG_PROF("pts_finish", st);
+  kde_finish_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, nw, w, scale, out);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
 }

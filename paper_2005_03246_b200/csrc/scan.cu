@@ -286,6 +286,8 @@ int64_t scan_scratch_elems(const LatShape &s) {
   return mx;
 }
 
+int64_t scan_scratch_bound() { return (int64_t)sm_count() * 1536 * 3 + 4096; }
+
 template <typename T>
 int scan_axis(T *lat, const LatShape &s, int ax, bool rev, const Epi &epi, T *scratch,
               cudaStream_t st) {

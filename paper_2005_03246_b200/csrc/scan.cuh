@@ -47,6 +47,9 @@ struct LatShape {
 
 // Size (elements of T) of the chunk-carry scratch the engine may need for one pass.
 int64_t scan_scratch_elems(const LatShape &s);
+// Upper bound of scan_scratch_elems over every lattice shape (chunking only happens when a
+// pass has fewer parallel units than ~3 x resident threads).
+int64_t scan_scratch_bound();
 
 // Scan every axis of `lat` (in place) with direction rev[k] (true = suffix sums).  The last
 // processed axis (axis 0) applies `epi`.  T = int32_t or double.

@@ -1,0 +1,123 @@
+"""Dominance sums at the sample points — drop-in for the reference's ``fastcdf.dnc`` public
+functions ``ecdf_dnc`` (dnc.py:531-561) and ``kde_dnc`` (dnc.py:635-690).
+
+The reference computes them with an O(N log N) divide-and-conquer recursion; here the same sums
+come from the rank-space dominance kernel of ``fcg_dnc_ecdf`` / ``fcg_kde_points_laplacian``
+(device radix ranking + a 3-level coarse-grid / shared-memory decomposition, d = 2; sort + scan
+for d = 1; tiled direct sums for d >= 3).  Semantics, guards and exceptions follow the
+reference: distinct coordinates are required (TieError), strict comparisons on raw coordinates,
+exponentials on midrange-centred coordinates, the self term w_j added before the shared
+1/(2^d N prod h) normalisation.
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+
+from . import _lib
+from .core import (
+    EXP_OVERFLOW_GUARD,
+    POINT_ALIGNED,
+    Bandwidth,
+    EvalResult,
+    OverflowGuardError,
+    ParameterError,
+    Sample,
+    TieError,
+)
+from .kernels import KernelSpec
+
+
+def _require_distinct(sample: Sample):
+    """TieError when a dimension has duplicates (dnc.py:491-499)."""
+    if not sample.distinct:
+        bad = [k for k, ok in enumerate(sample.distinct_by_dim) if not ok]
+        raise TieError(
+            f"duplicate coordinates in dimension(s) {bad}; the recursion requires distinct "
+            f"values per dimension - jitter the data, deduplicate with merged weights, or use "
+            f"rank_tiebreak() for pure ECDF counting")
+
+
+def _diag_bandwidth(sample: Sample, bandwidth: Bandwidth) -> np.ndarray:
+    """dnc.py:588-595."""
+    if not bandwidth.is_diagonal:
+        raise ParameterError("divide-and-conquer KDE requires a diagonal bandwidth; rotate "
+                             "matrix bandwidths first")
+    h = np.ascontiguousarray(bandwidth.diagonal, dtype=np.float64)
+    if h.size != sample.dim:
+        raise ParameterError("bandwidth dimension does not match sample")
+    return h
+
+
+def _span_guard_and_centre(sample: Sample, h: np.ndarray) -> np.ndarray:
+    """Overflow guard (dnc.py:598-605) and data midrange (dnc.py:656)."""
+    lo, hi = _lib.minmax(sample.points)
+    span = hi - lo
+    for k in range(sample.dim):
+        if span[k] / h[k] > EXP_OVERFLOW_GUARD:
+            raise OverflowGuardError(
+                f"dimension {k}: span/bandwidth = {span[k] / h[k]:.1f} exceeds "
+                f"{EXP_OVERFLOW_GUARD:.0f}; enlarge the bandwidth or rescale")
+    return 0.5 * (lo + hi)
+
+
+def _out(sample: Sample, t):
+    return t if sample.on_device else t.cpu().numpy()
+
+
+def ecdf_dnc(sample: Sample, include_self: bool = False, scaled: bool = True) -> EvalResult:
+    """Weight sum over the points strictly below each point in every dimension
+    (dnc.py:531-561); + own weight when ``include_self``; / N when ``scaled``."""
+    import torch
+
+    t0 = time.perf_counter()
+    _require_distinct(sample)
+    x = _lib.to_device_f64(sample.points)
+    n, d = x.shape
+    w = None if sample.unit_weights else _lib.to_device_f64(sample.weights)
+    out = torch.empty(n, dtype=torch.float64, device=x.device)
+    _lib.call_ws("fcg_dnc_ecdf", _lib.ptr(x), n, d, _lib.ptr(w), int(include_self),
+                 int(scaled), _lib.ptr(out))
+    return EvalResult(_out(sample, out), POINT_ALIGNED, {
+        "method": "dnc", "scaled": scaled, "include_self": include_self,
+        "runtime_seconds": time.perf_counter() - t0})
+
+
+def _kde_points(sample: Sample, weights_list, h: np.ndarray):
+    """Laplacian KDE numerators at the sample points for up to two weight vectors in one
+    pass; returns a (nw, n) device tensor."""
+    import torch
+
+    c = _span_guard_and_centre(sample, h)
+    x = _lib.to_device_f64(sample.points)
+    n, d = x.shape
+    ws = [None if w is None else _lib.to_device_f64(w) for w in weights_list]
+    nw = len(ws)
+    if any(w is None for w in ws):
+        ws = [torch.ones(n, dtype=torch.float64, device=x.device) if w is None else w for w in ws]
+    wmat = torch.stack(ws).contiguous()
+    out = torch.empty((nw, n), dtype=torch.float64, device=x.device)
+    _lib.call_ws("fcg_kde_points_laplacian", _lib.ptr(x), n, d, _lib.ptr(wmat), nw,
+                 _lib.f64_array(h), _lib.f64_array(c), _lib.ptr(out))
+    return out
+
+
+def kde_dnc(sample: Sample, kernel: KernelSpec, bandwidth: Bandwidth) -> EvalResult:
+    """Kernel density estimate at the sample points (dnc.py:635-690), Laplacian family."""
+    t0 = time.perf_counter()
+    _require_distinct(sample)
+    fam = kernel.family
+    if fam == "matern32-additive":
+        raise ParameterError("matern32-additive is not implemented on the B200 path yet "
+                             "(SURVEY §8f #1)")
+    if fam != "laplacian":
+        raise ParameterError(f"kde_dnc supports laplacian and matern32-additive kernels, "
+                             f"got {fam!r}")
+    h = _diag_bandwidth(sample, bandwidth)
+    w = None if sample.unit_weights else sample.weights
+    vals = _kde_points(sample, [w], h)[0]
+    return EvalResult(_out(sample, vals), POINT_ALIGNED, {
+        "method": "dnc", "kernel": str(kernel),
+        "runtime_seconds": time.perf_counter() - t0})

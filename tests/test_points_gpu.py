@@ -1,0 +1,216 @@
+"""GPU parity of the at-points path: ranking, generalized ECDF / ESF at the points with ties
+(rank lattice and rank-space dominance routes), ecdf_dnc, kde_dnc, kernel regression."""
+
+import numpy as np
+import pytest
+
+import paper_2005_03246_b200 as fcb
+from conftest import cfg_golden
+
+pytestmark = pytest.mark.gpu
+
+THREE = [[0.2, 0.7], [0.5, 0.1], [0.9, 0.9]]
+
+
+def rel_err(got, ref, scale=None):
+    got, ref = np.asarray(got), np.asarray(ref)
+    s = np.abs(ref) if scale is None else np.asarray(scale)
+    s = np.maximum(s, np.finfo(float).tiny)
+    return float(np.max(np.abs(got - ref) / s)) if ref.size else 0.0
+
+
+# ---- ecdf_dnc (dnc.py:531-561; reference tests test_dnc.py:23-72) -----------------------
+
+def test_ecdf_dnc_kats(small_golden):
+    s = fcb.validate_sample(THREE)
+    np.testing.assert_array_equal(fcb.ecdf_dnc(s).values, small_golden["kat.dnc"])
+    np.testing.assert_array_equal(fcb.ecdf_dnc(s, include_self=True).values,
+                                  small_golden["kat.dnc_self"])
+    s1 = fcb.validate_sample([[0.3, 0.4]])
+    assert fcb.ecdf_dnc(s1).values[0] == 0.0
+    assert fcb.ecdf_dnc(s1, include_self=True).values[0] == 1.0
+    with pytest.raises(fcb.TieError, match="dimension"):
+        fcb.ecdf_dnc(fcb.validate_sample([[1.0, 2.0], [1.0, 3.0]]))
+
+
+def test_ecdf_dnc_golden_bit_exact(small_golden):
+    g = small_golden
+    for d in (1, 2, 3):
+        for seed in range(4):
+            key = f"dnc.{d}.{seed}"
+            s = fcb.validate_sample(g[key + ".x"], g[key + ".w"])
+            np.testing.assert_array_equal(fcb.ecdf_dnc(s, scaled=False).values, g[key + ".out"])
+            np.testing.assert_array_equal(fcb.ecdf_dnc(s, include_self=True).values,
+                                          g[key + ".self"])
+
+
+@pytest.mark.parametrize("n", [1, 2, 33, 4095, 4097, 20_000, 300_001])
+def test_ecdf_dnc_vs_oracle_2d(n, oracle):
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((n, 2))
+    w = rng.integers(1, 5, n).astype(float)
+    got = fcb.ecdf_dnc(fcb.validate_sample(x, w), scaled=False).values
+    np.testing.assert_array_equal(got, oracle.ecdf_dnc(x, w, scaled=False))
+    got = fcb.ecdf_dnc(fcb.validate_sample(x)).values
+    np.testing.assert_array_equal(got, oracle.ecdf_dnc(x, None))
+
+
+def test_ecdf_dnc_permutation_invariance():
+    rng = np.random.default_rng(17)
+    pts = rng.standard_normal((2000, 2))
+    w = rng.uniform(0.5, 2.0, 2000)
+    perm = rng.permutation(2000)
+    a = fcb.ecdf_dnc(fcb.validate_sample(pts, w)).values
+    b = fcb.ecdf_dnc(fcb.validate_sample(pts[perm], w[perm])).values
+    assert rel_err(a[perm], b) <= 1e-12
+
+
+# ---- generalized ECDF / ESF at the points with ties -------------------------------------
+
+def test_points_with_ties_golden(small_golden):
+    g = small_golden
+    for d in (1, 2, 3):
+        for seed in range(3):
+            key = f"pts.{d}.{seed}"
+            s = fcb.validate_sample(g[key + ".x"], g[key + ".w"])
+            for code in range(1 << d):
+                dv = fcb.DeltaVector.from_code(code, d)
+                got = fcb.ecdf_at_points(s, dv).values
+                assert rel_err(got, g[f"{key}.ecdf.{code}"]) <= 1e-12
+            assert rel_err(fcb.esf_at_points(s).values, g[key + ".esf"]) <= 1e-12
+
+
+def test_points_dominance_route_with_ties(oracle):
+    """Distinct-level product above the lattice budget forces the rank-space dominance kernel
+    with tie-aware thresholds."""
+    oracle.set_threads(0)
+    rng = np.random.default_rng(42)
+    n = 1_500_000
+    x = np.floor(rng.random((n, 2)) * 6000) / 6000  # ties in both dims, 3.6e7 level pairs
+    y = rng.random(n)
+    s = fcb.validate_sample(x, y)
+    q = rng.integers(0, n, 1500)
+    for delta in [(1, 1), (1, -1), (-1, 1), (-1, -1)]:
+        got = fcb.ecdf_at_points(s, fcb.DeltaVector(delta)).values[q]
+        ref = oracle.ecdf_naive(x, y, x[q], delta)
+        assert rel_err(got, ref) <= 1e-12, delta
+    got = fcb.esf_at_points(s).values[q]
+    assert rel_err(got, oracle.esf_naive(x, y, x[q])) <= 1e-12
+    cnt = fcb.ecdf_at_points(fcb.validate_sample(x), fcb.DeltaVector((1, -1)), scaled=False).values[q]
+    np.testing.assert_array_equal(cnt, oracle.ecdf_naive(x, None, x[q], (1, -1), scaled=False))
+
+
+def test_cfg2_full(oracle, cfg_meta):
+    import workloads as wl
+
+    w = wl.cfg2()
+    s = fcb.validate_sample(w.points, w.weights)
+    ecdf = fcb.ecdf_at_points(s, fcb.DeltaVector(w.delta)).values
+    esf = fcb.esf_at_points(s).values
+    ref = oracle.ecdf_at_points(w.points, w.weights, w.delta)
+    assert rel_err(ecdf, ref) <= 1e-12
+    assert rel_err(esf, oracle.esf_at_points(w.points, w.weights)) <= 1e-12
+    gold = cfg_golden("cfg2")
+    meta = cfg_meta.get("cfg2", {})
+    if gold is not None and meta.get("input_sha") == wl.digest(w.points):
+        idx = gold["idx"]
+        assert rel_err(ecdf[idx], gold["ecdf"]) <= 1e-12
+        assert rel_err(esf[idx], gold["esf"]) <= 1e-12
+        assert rel_err(ecdf[idx[:1000]], gold["naive_ecdf"]) <= 1e-12
+        assert rel_err(esf[idx[:1000]], gold["naive_esf"]) <= 1e-12
+    # unit weights: exact integer counts
+    cnt = fcb.ecdf_at_points(fcb.validate_sample(w.points), fcb.DeltaVector(w.delta), scaled=False).values
+    np.testing.assert_array_equal(cnt, oracle.ecdf_at_points(w.points, None, w.delta, scaled=False))
+
+
+# ---- kde_dnc (dnc.py:635-690; reference tests test_dnc.py:163-189) ---------------------
+
+def test_kde_dnc_kats():
+    s = fcb.validate_sample([[0.0], [1.0]])
+    v = fcb.kde_dnc(s, fcb.laplacian(), fcb.Bandwidth.diag([1.0])).values
+    np.testing.assert_allclose(v, 0.25 * (1 + np.exp(-1.0)), rtol=1e-15)
+    s = fcb.validate_sample([[0.4, -0.2]], [3.0])
+    v = fcb.kde_dnc(s, fcb.laplacian(), fcb.Bandwidth.diag([0.5, 0.5])).values
+    np.testing.assert_allclose(v[0], 3.0 * 0.25 / 0.25, rtol=1e-15)
+    with pytest.raises(fcb.ParameterError):
+        fcb.kde_dnc(fcb.validate_sample([[0.0], [1.0]]), fcb.uniform(), fcb.Bandwidth.diag([1.0]))
+    with pytest.raises(fcb.OverflowGuardError, match="dimension 0"):
+        fcb.kde_dnc(fcb.validate_sample([[0.0], [700.0]]), fcb.laplacian(), fcb.Bandwidth.diag([1.0]))
+    with pytest.raises(fcb.TieError):
+        fcb.kde_dnc(fcb.validate_sample([[0.0, 1.0], [0.0, 2.0]]), fcb.laplacian(),
+                    fcb.Bandwidth.diag([1.0, 1.0]))
+
+
+def test_kde_dnc_golden(small_golden):
+    g = small_golden
+    for d in (1, 2, 3):
+        key = f"kdednc.{d}"
+        s = fcb.validate_sample(g[key + ".x"], g[key + ".w"])
+        got = fcb.kde_dnc(s, fcb.laplacian(), fcb.Bandwidth.diag(g[key + ".h"])).values
+        assert rel_err(got, g[key + ".out"]) <= 1e-9
+        assert np.max(np.abs(got - g[key + ".naive"])) <= 1e-13  # reference bound
+
+
+@pytest.mark.parametrize("n", [5, 4096, 9000, 250_000])
+def test_kde_dnc_vs_oracle_signed(n, oracle):
+    rng = np.random.default_rng(1000 + n)
+    x = rng.standard_normal((n, 2))
+    w = rng.standard_normal(n)  # signed weights: compare on the |w| KDE scale
+    h = [0.3, 0.2]
+    s = fcb.validate_sample(x, w)
+    got = fcb.kde_dnc(s, fcb.laplacian(), fcb.Bandwidth.diag(h)).values
+    ref = oracle.kde_dnc_laplacian(x, w, h)
+    absk = oracle.kde_dnc_laplacian(x, np.abs(w), h)
+    assert rel_err(got, ref, absk) <= 1e-9
+
+
+def test_cfg4_1e6_and_regression(oracle, cfg_meta):
+    import workloads as wl
+
+    w = wl.cfg4(1_000_000)
+    s = fcb.validate_sample(w.points)
+    y = w.extra["y"]
+    bw = fcb.Bandwidth.diag(w.h)
+    num = fcb.kde_numerators(s, [None, y], bw)
+    dens = fcb.kde_dnc(s, fcb.laplacian(), bw).values
+    assert rel_err(num[0], dens) <= 1e-12
+    gold = cfg_golden("cfg4_1e6")
+    meta = cfg_meta.get("cfg4_1e6", {})
+    if gold is not None and meta.get("input_sha") == wl.digest(w.points) \
+            and meta.get("y_sha") == wl.digest(y):
+        idx = gold["idx"]
+        assert rel_err(num[0][idx], gold["density"]) <= 1e-9
+        assert rel_err(num[1][idx], gold["regression"], gold["abs_regression"]) <= 1e-9
+    else:
+        ref = oracle.kde_dnc_laplacian(w.points, None, w.h)
+        assert rel_err(num[0], ref) <= 1e-9
+    nw = fcb.kernel_regression(s, y, fcb.laplacian(), bw).values
+    num_abs = fcb.kde_numerators(s, [np.abs(y)], bw)[0]
+    # fp64 atomics make runs differ in the last bits; judge on the |y|-weighted scale
+    assert rel_err(nw * num[0], num[1], num_abs) <= 1e-9
+
+
+def test_d3_brute_paths(oracle):
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((3000, 3))
+    w = rng.uniform(0.5, 2, 3000)
+    s = fcb.validate_sample(x, w)
+    got = fcb.ecdf_dnc(s, scaled=False).values
+    ref = oracle.ecdf_naive(x, w, x, (-1, -1, -1), scaled=False)
+    assert rel_err(got, ref) <= 1e-12
+    got = fcb.kde_dnc(s, fcb.laplacian(), fcb.Bandwidth.diag([0.4, 0.5, 0.6])).values
+    ref = oracle.kde_naive_laplacian(x, w, x, [0.4, 0.5, 0.6])
+    assert rel_err(got, ref) <= 1e-9
+    xt = np.floor(rng.random((50_000, 3)) * 300) / 300  # 2.7e7 level triples > budget -> brute
+    got = fcb.ecdf_at_points(fcb.validate_sample(xt), fcb.DeltaVector((1, -1, 1)), scaled=False).values
+    q = rng.integers(0, 50_000, 500)
+    np.testing.assert_array_equal(got[q], oracle.ecdf_naive(xt, None, xt[q], (1, -1, 1), scaled=False))
+
+
+def test_distinct_flags_device():
+    import torch
+
+    x = torch.tensor([[1.0, 3.0], [1.0, 4.0], [2.0, -0.0], [5.0, 0.0]], device="cuda")
+    assert fcb.validate_sample(x).distinct_by_dim == (False, False)  # -0.0 == +0.0
+    x = torch.tensor([[1.0, 3.0], [2.0, 4.0]], device="cuda")
+    assert fcb.validate_sample(x).distinct_by_dim == (True, True)
