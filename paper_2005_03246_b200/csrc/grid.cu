@@ -20,57 +20,15 @@
 // place of the reference's slice + copy.
 #include "common.cuh"
 #include "scan.cuh"
+#include "bin.cuh"
+#include "grid_part.cuh"
 
 namespace fcg {
 
 namespace {
 
-constexpr int kSmemKnots = 4096;  // up to 32 KB of knots staged in (dynamic) shared memory
-
-struct BinGrid {
-  int d;
-  int64_t m[FCG_MAX_DIM];
-  int64_t koff[FCG_MAX_DIM];
-  int le[FCG_MAX_DIM];       // 1: count knots <= x (delta=-1); 0: count knots < x (delta=+1)
-  int64_t shift[FCG_MAX_DIM];  // lattice cell = b - shift
-  int64_t dims[FCG_MAX_DIM];   // lattice extents
-  int64_t stride[FCG_MAX_DIM];
-  int64_t total_knots;
-};
-
-enum WeightKind { W_UNIT = 0, W_F64 = 1, W_PSI = 2 };
-
-struct PsiParams {  // psi_i = w_i * exp(sum_k (x_ik - c_k) * a_k), a_k = delta_k / h_k
-  double c[FCG_MAX_DIM];
-  double a[FCG_MAX_DIM];
-};
-
-// #knots < x (le = 0) or #knots <= x (le = 1) for a strictly increasing knot vector.
-__device__ __forceinline__ int64_t knot_count(double x, const double *kn, int64_t m, int le,
-                                              double z0, double inv_dz) {
-  double t = (x - z0) * inv_dz;
-  t = fmin(fmax(t, -1.0), (double)m + 1.0);
-  int64_t g = le ? (int64_t)floor(t) + 1 : (int64_t)ceil(t);
-  g = g < 0 ? 0 : (g > m ? m : g);
-#pragma unroll 1
-  for (int it = 0; it < 4; ++it) {
-    const bool lo_ok = (g == 0) || (le ? (kn[g - 1] <= x) : (kn[g - 1] < x));
-    const bool hi_ok = (g == m) || (le ? (x < kn[g]) : (x <= kn[g]));
-    if (lo_ok && hi_ok) return g;
-    g += lo_ok ? 1 : -1;
-  }
-  int64_t lo = 0, hi = m;  // first index whose knot fails the predicate
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    const bool pred = le ? (kn[mid] <= x) : (kn[mid] < x);
-    if (pred) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
-
 template <int D, int WK, typename T>
-__global__ void __launch_bounds__(256) bin_scatter_kernel(const double *__restrict__ x,
+__global__ void __launch_bounds__(256, 4) bin_scatter_kernel(const double *__restrict__ x,
                                                           int64_t n, int drt,
                                                           const double *__restrict__ w,
                                                           const double *__restrict__ knots,
@@ -112,7 +70,7 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(const double *__restri
 #pragma unroll
     for (int k = 0; k < (D > 0 ? D : FCG_MAX_DIM); ++k) {
       if (k < d) {
-        const int64_t b = knot_count(xi[k], kb + g.koff[k], g.m[k], g.le[k], s_z0[k], s_idz[k]);
+        const int64_t b = knot_count(xi[k], kb + g.koff[k], (int)g.m[k], g.le[k], s_z0[k], s_idz[k]);
         const int64_t cell = b - g.shift[k];
         live = live && (cell >= 0) && (cell < g.dims[k]);
         flat += cell * g.stride[k];
@@ -167,29 +125,6 @@ int check_common(int64_t n, int32_t d, const int64_t *m) {
   for (int k = 0; k < d; ++k)
     if (m[k] < 1) return fail(FCG_EINVAL, "every dimension needs at least one knot");
   return FCG_OK;
-}
-
-// Bin grid for a lattice whose extents are `dims` and where cell = b - shift.
-BinGrid make_bin_grid(int d, const int64_t *m, const int *le, const int64_t *shift,
-                      const int64_t *dims) {
-  BinGrid g{};
-  g.d = d;
-  int64_t off = 0;
-  for (int k = 0; k < d; ++k) {
-    g.m[k] = m[k];
-    g.koff[k] = off;
-    off += m[k];
-    g.le[k] = le[k];
-    g.shift[k] = shift[k];
-    g.dims[k] = dims[k];
-  }
-  g.total_knots = off;
-  int64_t s = 1;
-  for (int k = d - 1; k >= 0; --k) {
-    g.stride[k] = s;
-    s *= dims[k];
-  }
-  return g;
 }
 
 // ---- KDE helpers -------------------------------------------------------------------------
@@ -264,6 +199,25 @@ __global__ void minmax_finish(const unsigned long long *mm, int d, double *out) 
 }
 
 }  // namespace
+
+int launch_kde_zf(const double *knots, int d, const int64_t *m, const double *c, const double *h,
+                  int code, double *zf, cudaStream_t st) {
+  ZfParams zp{};
+  zp.d = d;
+  int64_t off = 0;
+  for (int k = 0; k < d; ++k) {
+    zp.m[k] = m[k];
+    zp.koff[k] = off;
+    off += m[k];
+    zp.c[k] = c[k];
+    zp.h[k] = h[k];
+    zp.s[k] = ((code >> k) & 1) ? -1.0 : 1.0;
+  }
+  FCG_PROF("kde_zfac", st);
+  zf_kernel<<<grid_for(off, 256, 1), 256, 0, st>>>(knots, zp, zf, off);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}
 
 // ============================================================================================
 // C-ABI entry points
@@ -348,13 +302,6 @@ extern "C" int fcg_ecdf_grid(const double *x, int64_t n, int32_t d, const double
   const int64_t L = s.size();
   const bool unit = (w == nullptr);
   const size_t esz = unit ? 4 : 8;
-  Workspace W(ws);
-  void *lat = W.take<char>((size_t)L * esz);
-  void *scratch = W.take<char>((size_t)scan_scratch_elems(s) * esz);
-  if (ws == nullptr) {
-    *ws_bytes = W.bytes();
-    return FCG_OK;
-  }
   int le[FCG_MAX_DIM];
   int64_t shift[FCG_MAX_DIM];
   bool rev[FCG_MAX_DIM];
@@ -372,16 +319,30 @@ extern "C" int fcg_ecdf_grid(const double *x, int64_t n, int32_t d, const double
     }
   }
   BinGrid g = make_bin_grid(d, m, le, shift, s.dims);
-  PsiParams pp{};
-  cudaStream_t st = as_stream(stream);
-  {
-    FCG_PROF("lattice_zero", st);
-    FCG_CUDA_TRY(cudaMemsetAsync(lat, 0, (size_t)L * esz, st));
-  }
   Epi e;
   e.kind = out_kind == 1 ? EPI_I64 : EPI_F64;
   e.out = out;
   e.div = scaled ? (double)n : 0.0;
+  cudaStream_t st = as_stream(stream);
+  Workspace W(ws);
+  // unit weights at scale: plane-partitioned pipeline (grid_part.cu)
+  const PartPlan plan = unit ? plan_ecdf_partition(g, n) : PartPlan{};
+  if (plan.ok) {
+    FCG_TRY(ecdf_partitioned(x, n, knots, g, rev, plan, e, W, ws != nullptr, st));
+    if (ws == nullptr) *ws_bytes = W.bytes();
+    return FCG_OK;
+  }
+  void *lat = W.take<char>((size_t)L * esz);
+  void *scratch = W.take<char>((size_t)scan_scratch_elems(s) * esz);
+  if (ws == nullptr) {
+    *ws_bytes = W.bytes();
+    return FCG_OK;
+  }
+  PsiParams pp{};
+  {
+    FCG_PROF("lattice_zero", st);
+    FCG_CUDA_TRY(cudaMemsetAsync(lat, 0, (size_t)L * esz, st));
+  }
   if (unit) {
     FCG_TRY(launch_bin_scatter<W_UNIT>(x, n, d, w, knots, g, pp, static_cast<int32_t *>(lat), st));
     return scan_lattice<int32_t>(static_cast<int32_t *>(lat), s, rev, e,
@@ -427,7 +388,16 @@ extern "C" int fcg_kde_grid_laplacian(const double *x, int64_t n, int32_t d, con
     total_knots += m[k];
   }
   const int64_t L = s.size();
+  for (int k = 0; k < d; ++k)
+    if (!(h[k] > 0.0)) return fail(FCG_EINVAL, "bandwidth must be > 0");
+  cudaStream_t st = as_stream(stream);
   Workspace W(ws);
+  const PartPlan plan = plan_kde_partition(d, m, n);
+  if (plan.ok) {
+    FCG_TRY(kde_partitioned(x, n, w, knots, m, d, h, centre, plan, out, W, ws != nullptr, st));
+    if (ws == nullptr) *ws_bytes = W.bytes();
+    return FCG_OK;
+  }
   double *lat = W.take<double>((size_t)L);
   double *scratch = W.take<double>((size_t)scan_scratch_elems(s));
   double *zf = W.take<double>((size_t)total_knots);
@@ -435,9 +405,6 @@ extern "C" int fcg_kde_grid_laplacian(const double *x, int64_t n, int32_t d, con
     *ws_bytes = W.bytes();
     return FCG_OK;
   }
-  for (int k = 0; k < d; ++k)
-    if (!(h[k] > 0.0)) return fail(FCG_EINVAL, "bandwidth must be > 0");
-  cudaStream_t st = as_stream(stream);
   double prod_h = 1.0;
   for (int k = 0; k < d; ++k) prod_h *= h[k];
   const double scale = 1.0 / (std::ldexp(1.0, d) * (double)n * prod_h);

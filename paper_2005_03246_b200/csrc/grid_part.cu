@@ -1,0 +1,565 @@
+// Partitioned grid pipeline; see grid_part.cuh.
+//
+// Why: scattering 1e8 points with global atomics into a 1-2 GB lattice is random
+// read-modify-write traffic (two 32-byte sectors per point, ~10x the useful bytes, measured at
+// 12-16% of HBM peak).  Bucketing by plane first turns it into streaming: each CTA reads its
+// bucket's records contiguously, accumulates in shared memory and writes its plane once, with
+// the two in-plane scan passes (Algorithm 1's sweeps along axes d-2, d-1) fused in.
+#include "grid_part.cuh"
+#include "sort.cuh"
+
+namespace fcg {
+
+int launch_kde_zf(const double *knots, int d, const int64_t *m, const double *c, const double *h,
+                  int code, double *zf, cudaStream_t st);
+
+namespace {
+
+constexpr uint32_t kDead = 0xFFFFFFFFu;
+constexpr int kPlaneThreads = 512;
+constexpr size_t kEcdfTileBytes = 96 * 1024;   // int32 tile budget (2 CTAs per SM)
+constexpr size_t kKdeTileBytes = 72 * 1024;    // fp64 row-block budget (3 CTAs per SM)
+constexpr int64_t kMinPartitionN = int64_t(1) << 20;
+
+struct PartGeo {
+  int d;
+  int64_t E[FCG_MAX_DIM];      // extents of the bucketed space
+  int64_t shift[FCG_MAX_DIM];  // bucket-space index = b - shift
+  int64_t W, R, nrb, H;
+  int ecdf;                    // 1: val = in-block cell offset; 0: val = point index
+};
+
+template <int D>
+__global__ void __launch_bounds__(256, 4) part_bin_kernel(const double *__restrict__ x, int64_t n,
+                                                       int drt, const double *__restrict__ knots,
+                                                       BinGrid g, PartGeo p,
+                                                       uint32_t *__restrict__ keys,
+                                                       int32_t *__restrict__ vals) {
+  extern __shared__ double s_knots[];
+  __shared__ double s_z0[FCG_MAX_DIM], s_idz[FCG_MAX_DIM];
+  const int d = D > 0 ? D : drt;
+  const double *kb = stage_knots(g, knots, s_knots, s_z0, s_idz);
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double xi[D > 0 ? D : FCG_MAX_DIM];
+    if constexpr (D == 4) {
+      const double2 v0 = reinterpret_cast<const double2 *>(x)[2 * i];
+      const double2 v1 = reinterpret_cast<const double2 *>(x)[2 * i + 1];
+      xi[0] = v0.x; xi[1] = v0.y; xi[2] = v1.x; xi[3] = v1.y;
+    } else {
+#pragma unroll
+      for (int k = 0; k < (D > 0 ? D : FCG_MAX_DIM); ++k)
+        if (k < d) xi[k] = x[i * d + k];
+    }
+    uint32_t plane = 0;
+    int row = 0, col = 0;
+    bool live = true;
+#pragma unroll
+    for (int k = 0; k < (D > 0 ? D : FCG_MAX_DIM); ++k) {
+      if (k < d) {
+        const int c = knot_count(xi[k], kb + g.koff[k], (int)g.m[k], g.le[k], s_z0[k], s_idz[k]) -
+                      (int)p.shift[k];
+        live = live && c >= 0 && c < (int)p.E[k];
+        if (k < d - 2) plane = plane * (uint32_t)p.E[k] + (uint32_t)c;
+        else if (k == d - 2) row = c;
+        else col = c;
+      }
+    }
+    uint32_t key = kDead;
+    int32_t val = (int32_t)i;
+    if (live) {
+      const int rb = row / (int)p.R;
+      key = plane * (uint32_t)p.nrb + (uint32_t)rb;
+      if (p.ecdf) val = (row - rb * (int)p.R) * (int)p.W + col;
+    }
+    keys[i] = key;
+    vals[i] = val;
+  }
+}
+
+// start[b] = first sorted position whose key >= b, for b in [0, NB]
+__global__ void bucket_start_kernel(const uint32_t *__restrict__ keys, int64_t n, int64_t NB,
+                                    int32_t *__restrict__ start) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= NB;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((int64_t)keys[mid] < b) lo = mid + 1;
+      else hi = mid;
+    }
+    start[b] = (int32_t)lo;
+  }
+}
+
+// In-shared-memory scans of an nr x W tile: rows along the last axis (warp per row), then
+// columns along axis d-2 (segmented: G threads per column) continuing the carry row.
+template <typename T>
+__device__ __forceinline__ void tile_scan(T *tile, int nr, int W, bool rev_r, bool rev_c, T *carry,
+                                          T *seg) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  // warp per row, 32 consecutive elements per step (conflict-free), shuffle scans + carry
+  for (int r = warp; r < nr; r += nwarps) {
+    T *row = tile + (size_t)r * W;
+    T run = T(0);
+    for (int jb = 0; jb < W; jb += 32) {
+      const int jj = jb + lane;
+      const int j = rev_c ? W - 1 - jj : jj;
+      T v = jj < W ? row[j] : T(0);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const T u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+      }
+      v += run;
+      if (jj < W) row[j] = v;
+      run = __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncthreads();
+  const int G = (int)blockDim.x >= W ? (int)blockDim.x / W : 1;
+  const int Rg = (nr + G - 1) / G;
+  // phase A: segment totals
+  for (int cc = threadIdx.x; cc < W * G; cc += blockDim.x) {
+    const int c = cc % W, g = cc / W;
+    T s = T(0);
+    for (int q = g * Rg; q < nr && q < (g + 1) * Rg; ++q) {
+      const int r = rev_r ? nr - 1 - q : q;
+      s += tile[(size_t)r * W + c];
+    }
+    seg[(size_t)g * W + c] = s;
+  }
+  __syncthreads();
+  // phase B: rescan with carry-in
+  for (int cc = threadIdx.x; cc < W * G; cc += blockDim.x) {
+    const int c = cc % W, g = cc / W;
+    T run = carry[c];
+    for (int gg = 0; gg < g; ++gg) run += seg[(size_t)gg * W + c];
+    for (int q = g * Rg; q < nr && q < (g + 1) * Rg; ++q) {
+      const int r = rev_r ? nr - 1 - q : q;
+      run += tile[(size_t)r * W + c];
+      tile[(size_t)r * W + c] = run;
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < W; c += blockDim.x) {
+    T s = carry[c];
+    for (int g = 0; g < G; ++g) s += seg[(size_t)g * W + c];
+    carry[c] = s;
+  }
+  __syncthreads();
+}
+
+template <typename T>
+__device__ __forceinline__ void tile_store(T *__restrict__ dst, const T *tile, int64_t count) {
+  // 16-byte vector stores when both sides are aligned (they are for whole planes)
+  constexpr int V = 16 / sizeof(T);
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0 && count % V == 0) {
+    const int4 *src4 = reinterpret_cast<const int4 *>(tile);
+    int4 *dst4 = reinterpret_cast<int4 *>(dst);
+    for (int64_t i = threadIdx.x; i < count / V; i += blockDim.x) dst4[i] = src4[i];
+  } else {
+    for (int64_t i = threadIdx.x; i < count; i += blockDim.x) dst[i] = tile[i];
+  }
+}
+
+// ECDF / ESF counts: CTA per plane, row blocks in scan order.
+__global__ void __launch_bounds__(kPlaneThreads) plane_count_kernel(
+    PartGeo p, const int32_t *__restrict__ start, const int32_t *__restrict__ vals, int rev_r,
+    int rev_c, int32_t *__restrict__ lat) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int W = (int)p.W, R = (int)p.R;
+  const int G = (int)blockDim.x >= W ? (int)blockDim.x / W : 1;
+  int32_t *tile = reinterpret_cast<int32_t *>(smem);
+  int32_t *carry = tile + (size_t)R * W;
+  int32_t *seg = carry + W;
+  const int64_t plane = blockIdx.x;
+  for (int c = threadIdx.x; c < W; c += blockDim.x) carry[c] = 0;
+  for (int64_t rbi = 0; rbi < p.nrb; ++rbi) {
+    const int64_t rb = rev_r ? p.nrb - 1 - rbi : rbi;
+    const int64_t r0 = rb * R;
+    const int nr = (int)((r0 + R <= p.H) ? R : p.H - r0);
+    for (int i = threadIdx.x; i < nr * W; i += blockDim.x) tile[i] = 0;
+    __syncthreads();
+    const int64_t b = plane * p.nrb + rb;
+    const int32_t q0 = start[b], q1 = start[b + 1];
+    constexpr int KB = 8;
+    for (int32_t qb = q0 + threadIdx.x; qb < q1; qb += KB * blockDim.x) {
+      int32_t v[KB];
+#pragma unroll
+      for (int u = 0; u < KB; ++u) {
+        const int32_t q = qb + u * (int32_t)blockDim.x;
+        v[u] = q < q1 ? vals[q] : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < KB; ++u)
+        if (v[u] >= 0) atomicAdd(&tile[v[u]], 1);
+    }
+    __syncthreads();
+    tile_scan<int32_t>(tile, nr, W, rev_r, rev_c, carry, seg);
+    tile_store<int32_t>(lat + (plane * p.H + r0) * W, tile, (int64_t)nr * W);
+    __syncthreads();
+  }
+  (void)G;
+}
+
+// KDE term: CTA per cell-space plane.  Records are bucketed by full-space (M+1) row block; a
+// term with row shift s reads full block rb as cell rows [rb*Rf - s, (rb+1)*Rf - s), so every
+// cell row block comes from exactly one bucket.  Blocks are visited in the term's row scan
+// direction with a carry row, like the ECDF plane kernel.
+struct KdeTerm {
+  int d;
+  int64_t Mr, Mc;                    // cell extents of axes d-2, d-1
+  int64_t sr, sc;                    // shifts (1 where delta = -1)
+  int64_t Rf, nrb;                   // full-space rows per bucket block, blocks per plane
+  int64_t lead_m[FCG_MAX_DIM];       // cell extents of leading axes
+  int64_t lead_s[FCG_MAX_DIM];       // their shifts
+  int64_t lead_full[FCG_MAX_DIM];    // full (M+1) extents of leading axes
+  double c[FCG_MAX_DIM], a[FCG_MAX_DIM];
+};
+
+__global__ void __launch_bounds__(kPlaneThreads) plane_kde_kernel(
+    KdeTerm t, const int32_t *__restrict__ start, const double *__restrict__ xs,
+    const double *__restrict__ ws, const uint32_t *__restrict__ loc, int rev_r, int rev_c,
+    double *__restrict__ lat) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int W = (int)t.Mc, H = (int)t.Mr, Rf = (int)t.Rf;
+  double *tile = reinterpret_cast<double *>(smem);
+  double *carry = tile + (size_t)Rf * W;
+  double *seg = carry + W;
+  const int d = t.d;
+  int64_t rem = blockIdx.x, fplane = 0, mul = 1;
+  for (int k = d - 3; k >= 0; --k) {
+    const int64_t i = rem % t.lead_m[k];
+    rem /= t.lead_m[k];
+    fplane += (i + t.lead_s[k]) * mul;
+    mul *= t.lead_full[k];
+  }
+  for (int c = threadIdx.x; c < W; c += blockDim.x) carry[c] = 0.0;
+  double *plane_out = lat + (int64_t)blockIdx.x * H * W;
+  for (int64_t rbi = 0; rbi < t.nrb; ++rbi) {
+    const int64_t rb = rev_r ? t.nrb - 1 - rbi : rbi;
+    // cell rows of this block, clipped to [0, H)
+    int lo = (int)(rb * Rf - t.sr), hi = lo + Rf;
+    const int clo = lo < 0 ? 0 : lo, chi = hi > H ? H : hi;
+    if (chi <= clo) continue;
+    const int nr = chi - clo;
+    for (int i = threadIdx.x; i < nr * W; i += blockDim.x) tile[i] = 0.0;
+    __syncthreads();
+    const int64_t b = fplane * t.nrb + rb;
+    const int32_t q0 = start[b], q1 = start[b + 1];
+    // batches of KB records per thread: all loads issued before any exp / atomic so the
+    // memory latency overlaps (the fp64 shared atomic is a CAS loop the compiler will not
+    // hoist loads across)
+    constexpr int KB = 4;
+    for (int32_t qb = q0 + threadIdx.x; qb < q1; qb += KB * blockDim.x) {
+      uint32_t l[KB];
+      double wv[KB], s[KB];
+#pragma unroll
+      for (int u = 0; u < KB; ++u) {
+        const int32_t q = qb + u * (int32_t)blockDim.x;
+        const bool ok = q < q1;
+        l[u] = ok ? loc[q] : 0xFFFFFFFFu;
+        wv[u] = ok ? ws[q] : 0.0;
+        s[u] = 0.0;
+        for (int k = 0; k < d; ++k) s[u] += ((ok ? xs[(int64_t)q * d + k] : 0.0) - t.c[k]) * t.a[k];
+      }
+#pragma unroll
+      for (int u = 0; u < KB; ++u) {
+        const int cr = (int)(l[u] >> 16) - (int)t.sr - clo;
+        const int cc = (int)(l[u] & 0xFFFFu) - (int)t.sc;
+        if (l[u] == 0xFFFFFFFFu || cr < 0 || cr >= nr || cc < 0 || cc >= W) continue;
+        atomicAdd(&tile[cr * W + cc], wv[u] * exp(s[u]));
+      }
+    }
+    __syncthreads();
+    tile_scan<double>(tile, nr, W, rev_r, rev_c, carry, seg);
+    tile_store<double>(plane_out + (int64_t)clo * W, tile, (int64_t)nr * W);
+    __syncthreads();
+  }
+}
+
+// gather the sorted records the KDE terms stream: x row, weight, in-plane full-space offset
+__global__ void kde_materialize_kernel(const double *__restrict__ x, const double *__restrict__ w,
+                                       int64_t n, int d, const int32_t *__restrict__ order,
+                                       const double *__restrict__ knots, BinGrid g,
+                                       double *__restrict__ xs, double *__restrict__ ws,
+                                       uint32_t *__restrict__ loc) {
+  extern __shared__ double s_knots[];
+  __shared__ double s_z0[FCG_MAX_DIM], s_idz[FCG_MAX_DIM];
+  const double *kb = stage_knots(g, knots, s_knots, s_z0, s_idz);
+  __syncthreads();
+  const int kr = d - 2, kc = d - 1;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = order[q];
+    for (int k = 0; k < d; ++k) xs[q * d + k] = x[i * d + k];
+    ws[q] = w ? w[i] : 1.0;
+    const int64_t br = knot_count(x[i * d + kr], kb + g.koff[kr], (int)g.m[kr], 0, s_z0[kr], s_idz[kr]);
+    const int64_t bc = knot_count(x[i * d + kc], kb + g.koff[kc], (int)g.m[kc], 0, s_z0[kc], s_idz[kc]);
+    loc[q] = ((uint32_t)br << 16) | (uint32_t)bc;
+  }
+}
+
+int bits_for(int64_t v) {  // smallest b with v < 2^b
+  int b = 0;
+  while (b < 32 && (int64_t(1) << b) <= v) ++b;
+  return b;
+}
+
+int launch_part_bin(const double *x, int64_t n, int d, const double *knots, const BinGrid &g,
+                    const PartGeo &p, uint32_t *keys, int32_t *vals, cudaStream_t st) {
+  const size_t smem = g.total_knots <= kSmemKnots ? (size_t)g.total_knots * sizeof(double) : 0;
+  const int grid = grid_for(n, 256, 8);
+  FCG_PROF("part_bin", st);
+  switch (d) {
+    case 3: part_bin_kernel<3><<<grid, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals); break;
+    case 4:
+      if ((reinterpret_cast<uintptr_t>(x) & 15) == 0)
+        part_bin_kernel<4><<<grid, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals);
+      else
+        part_bin_kernel<0><<<grid, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals);
+      break;
+    default: part_bin_kernel<0><<<grid, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals); break;
+  }
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}
+
+struct PartBufs {
+  uint32_t *keys;
+  int32_t *vals;
+  RadixWs rw;
+  int32_t *start;
+};
+
+void carve_part(Workspace &W, PartBufs &b, int64_t n, int64_t NB) {
+  b.keys = W.take<uint32_t>(n);
+  b.vals = W.take<int32_t>(n);
+  b.rw.keys_alt = reinterpret_cast<uint64_t *>(W.take<uint32_t>(n));
+  b.rw.vals_alt = W.take<int32_t>(n);
+  b.rw.hist = W.take<int32_t>(radix_ws_hist_elems(n));
+  b.rw.partial = W.take<int32_t>(scan_ws_partial_elems(256 * (n / kSortTile + 1) + 2));
+  b.start = W.take<int32_t>(NB + 1);
+}
+
+int partition(const double *x, int64_t n, int d, const double *knots, const BinGrid &g,
+              const PartGeo &p, int64_t NB, int nbits, PartBufs &b, cudaStream_t st) {
+  FCG_TRY(launch_part_bin(x, n, d, knots, g, p, b.keys, b.vals, st));
+  FCG_TRY(radix_sort_pairs<uint32_t>(b.keys, b.vals, n, 0, ((nbits + 7) / 8) * 8, b.rw, st));
+  FCG_PROF("part_bucket_start", st);
+  bucket_start_kernel<<<grid_for(NB + 1, 256, 4), 256, 0, st>>>(b.keys, n, NB, b.start);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}
+
+}  // namespace
+
+PartPlan plan_ecdf_partition(const BinGrid &g, int64_t n) {
+  PartPlan pl;
+  const int d = g.d;
+  if (d < 3 || n < kMinPartitionN) return pl;
+  // Sparse lattices (well under one point per 4 cells, e.g. config 3 at 0.07) keep the atomic
+  // scatter: its random updates mostly hit L2 and the partition would cost more than it saves.
+  int64_t cells = 1;
+  for (int k = 0; k < d; ++k) cells *= g.dims[k];
+  if (4 * n < cells) return pl;
+  pl.W = g.dims[d - 1];
+  pl.H = g.dims[d - 2];
+  pl.NP = 1;
+  for (int k = 0; k < d - 2; ++k) pl.NP *= g.dims[k];
+  if (pl.W > 8192 || pl.NP < 2 * (int64_t)sm_count()) return pl;
+  const int64_t G = kPlaneThreads >= pl.W ? kPlaneThreads / pl.W : 1;
+  // tile + carry + segment totals
+  int64_t R = (int64_t)(kEcdfTileBytes / 4 - pl.W - G * pl.W) / pl.W;
+  if (R < 1) return pl;
+  if (R > pl.H) R = pl.H;
+  pl.R = R;
+  pl.nrb = ceil_div(pl.H, R);
+  pl.NB = pl.NP * pl.nrb;
+  if (pl.NB >= (int64_t(1) << 31) - 2 || n >= (int64_t(1) << 31) - 1) return pl;
+  pl.nbits = bits_for(pl.NB);  // kDead's low nbits are all ones > NB - 1
+  pl.ok = true;
+  return pl;
+}
+
+int ecdf_partitioned(const double *x, int64_t n, const double *knots, const BinGrid &g,
+                     const bool *rev, const PartPlan &pl, const Epi &epi, Workspace &W, bool run,
+                     cudaStream_t st) {
+  const int d = g.d;
+  PartBufs b;
+  carve_part(W, b, n, pl.NB);
+  LatShape s;
+  s.d = d;
+  for (int k = 0; k < d; ++k) s.dims[k] = g.dims[k];
+  int32_t *lat = W.take<int32_t>(s.size());
+  int32_t *scratch = W.take<int32_t>(scan_scratch_bound());
+  if (!run) return FCG_OK;
+  PartGeo p{};
+  p.d = d;
+  for (int k = 0; k < d; ++k) {
+    p.E[k] = g.dims[k];
+    p.shift[k] = g.shift[k];
+  }
+  p.W = pl.W;
+  p.R = pl.R;
+  p.nrb = pl.nrb;
+  p.H = pl.H;
+  p.ecdf = 1;
+  FCG_TRY(partition(x, n, d, knots, g, p, pl.NB, pl.nbits, b, st));
+  const int64_t G = kPlaneThreads >= pl.W ? kPlaneThreads / pl.W : 1;
+  const size_t smem = (size_t)(pl.R * pl.W + pl.W + G * pl.W) * sizeof(int32_t);
+  {
+    FCG_PROF("plane_count", st);
+    FCG_CUDA_TRY(cudaFuncSetAttribute(plane_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    plane_count_kernel<<<(unsigned)pl.NP, kPlaneThreads, smem, st>>>(p, b.start, b.vals,
+                                                                    rev[d - 2], rev[d - 1], lat);
+    FCG_LAUNCH_CHECK();
+  }
+  Epi inplace;
+  for (int ax = d - 3; ax >= 1; --ax) FCG_TRY(scan_axis<int32_t>(lat, s, ax, rev[ax], inplace, scratch, st));
+  return scan_axis<int32_t>(lat, s, 0, rev[0], epi, scratch, st);
+}
+
+PartPlan plan_kde_partition(int d, const int64_t *m, int64_t n) {
+  PartPlan pl;
+  if (d < 3 || n < kMinPartitionN) return pl;
+  pl.W = m[d - 1];
+  pl.H = m[d - 2];
+  if (pl.W + 1 > 65535 || pl.H + 1 > 65535) return pl;  // packed 16-bit (row, col) offsets
+  const int64_t G = kPlaneThreads >= pl.W ? kPlaneThreads / pl.W : 1;
+  const int64_t Hf = pl.H + 1;
+  // fewest full-space row blocks whose tile fits the budget
+  int64_t nrb = 1, Rf = Hf;
+  while (true) {
+    Rf = ceil_div(Hf, nrb);
+    const size_t bytes = (size_t)(Rf * pl.W + pl.W + G * pl.W) * sizeof(double);
+    if (bytes <= kKdeTileBytes) break;
+    if (Rf == 1) return pl;
+    ++nrb;
+  }
+  pl.NP = 1;
+  int64_t np_full = 1;
+  for (int k = 0; k < d - 2; ++k) {
+    pl.NP *= m[k];
+    np_full *= m[k] + 1;
+  }
+  if (pl.NP < 2 * (int64_t)sm_count()) return pl;
+  pl.R = Rf;
+  pl.nrb = nrb;
+  pl.NB = np_full * nrb;
+  if (pl.NB >= (int64_t(1) << 31) - 2 || n >= (int64_t(1) << 31) - 1) return pl;
+  pl.nbits = bits_for(pl.NB);
+  pl.ok = true;
+  return pl;
+}
+
+int kde_partitioned(const double *x, int64_t n, const double *w, const double *knots,
+                    const int64_t *m, int d, const double *h, const double *centre,
+                    const PartPlan &pl, double *out, Workspace &W, bool run, cudaStream_t st) {
+  PartBufs b;
+  carve_part(W, b, n, pl.NB);
+  double *xs = W.take<double>((size_t)n * d);
+  double *wsorted = W.take<double>(n);
+  uint32_t *loc = W.take<uint32_t>(n);
+  LatShape s;
+  s.d = d;
+  int64_t total_knots = 0;
+  for (int k = 0; k < d; ++k) {
+    s.dims[k] = m[k];
+    total_knots += m[k];
+  }
+  double *lat = W.take<double>(s.size());
+  double *scratch = W.take<double>(scan_scratch_bound());
+  double *zf = W.take<double>(total_knots);
+  if (!run) return FCG_OK;
+
+  // one delta=+1 binning in the full (M+1)^d space serves every term (fastsum.py:146-149)
+  int le[FCG_MAX_DIM];
+  int64_t zero[FCG_MAX_DIM], full[FCG_MAX_DIM];
+  for (int k = 0; k < d; ++k) {
+    le[k] = 0;
+    zero[k] = 0;
+    full[k] = m[k] + 1;
+  }
+  BinGrid g = make_bin_grid(d, m, le, zero, full);
+  PartGeo p{};
+  p.d = d;
+  for (int k = 0; k < d; ++k) {
+    p.E[k] = full[k];
+    p.shift[k] = 0;
+  }
+  p.W = full[d - 1];
+  p.H = full[d - 2];
+  p.R = pl.R;
+  p.nrb = pl.nrb;
+  p.ecdf = 0;
+  FCG_TRY(partition(x, n, d, knots, g, p, pl.NB, pl.nbits, b, st));
+  {
+    const size_t smem = g.total_knots <= kSmemKnots ? (size_t)g.total_knots * sizeof(double) : 0;
+    FCG_PROF("kde_materialize", st);
+    kde_materialize_kernel<<<grid_for(n, 256, 8), 256, smem, st>>>(x, w, n, d, b.vals, knots, g, xs,
+                                                                  wsorted, loc);
+    FCG_LAUNCH_CHECK();
+  }
+  double prod_h = 1.0;
+  for (int k = 0; k < d; ++k) prod_h *= h[k];
+  const double scale = 1.0 / (std::ldexp(1.0, d) * (double)n * prod_h);
+  const int64_t G = kPlaneThreads >= pl.W ? kPlaneThreads / pl.W : 1;
+  const size_t smem = (size_t)(pl.R * pl.W + pl.W + G * pl.W) * sizeof(double);
+  FCG_CUDA_TRY(cudaFuncSetAttribute(plane_kde_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+  const int ncodes = 1 << d;
+  for (int code = 0; code < ncodes; ++code) {
+    KdeTerm t{};
+    t.d = d;
+    bool rev[FCG_MAX_DIM];
+    int64_t sh[FCG_MAX_DIM];
+    for (int k = 0; k < d; ++k) {
+      const double sgn = ((code >> k) & 1) ? -1.0 : 1.0;
+      rev[k] = sgn < 0;
+      sh[k] = sgn < 0 ? 1 : 0;
+      t.c[k] = centre[k];
+      t.a[k] = sgn / h[k];
+    }
+    t.Mr = m[d - 2];
+    t.Mc = m[d - 1];
+    t.sr = sh[d - 2];
+    t.sc = sh[d - 1];
+    t.Rf = pl.R;
+    t.nrb = pl.nrb;
+    for (int k = 0; k < d - 2; ++k) {
+      t.lead_m[k] = m[k];
+      t.lead_s[k] = sh[k];
+      t.lead_full[k] = m[k] + 1;
+    }
+    FCG_TRY(launch_kde_zf(knots, d, m, centre, h, code, zf, st));
+    {
+      FCG_PROF("plane_kde", st);
+      plane_kde_kernel<<<(unsigned)pl.NP, kPlaneThreads, smem, st>>>(t, b.start, xs, wsorted, loc,
+                                                                    rev[d - 2], rev[d - 1], lat);
+      FCG_LAUNCH_CHECK();
+    }
+    Epi inplace;
+    for (int ax = d - 3; ax >= 1; --ax)
+      FCG_TRY(scan_axis<double>(lat, s, ax, rev[ax], inplace, scratch, st));
+    Epi e;
+    e.kind = EPI_KDE;
+    e.out = out;
+    e.zf = zf;
+    int64_t off = 0;
+    for (int k = 0; k < d; ++k) {
+      e.zoff[k] = off;
+      off += m[k];
+    }
+    e.accumulate = code > 0;
+    e.apply_scale = code == ncodes - 1;
+    e.scale = scale;
+    FCG_TRY(scan_axis<double>(lat, s, 0, rev[0], e, scratch, st));
+  }
+  return FCG_OK;
+}
+
+}  // namespace fcg

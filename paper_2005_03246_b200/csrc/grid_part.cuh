@@ -1,0 +1,36 @@
+// Partitioned grid pipeline (d >= 3): points are bucketed once by lattice plane (the last two
+// axes) with a 2-pass radix partition on 32-bit bucket keys; one CTA per plane then builds the
+// plane histogram in shared memory (no memset, no global atomics), scans both in-plane axes
+// there and writes the plane once.  The remaining leading axes are walked by the scan engine,
+// whose last pass carries the output epilogue.
+#pragma once
+#include "bin.cuh"
+#include "scan.cuh"
+
+namespace fcg {
+
+struct PartPlan {
+  bool ok = false;
+  int64_t NP = 0;   // planes (product of the leading d-2 extents)
+  int64_t H = 0;    // rows per plane (extent of axis d-2)
+  int64_t W = 0;    // row length (extent of axis d-1)
+  int64_t R = 0;    // rows per shared-memory block
+  int64_t nrb = 0;  // row blocks per plane
+  int64_t NB = 0;   // buckets
+  int nbits = 0;    // radix key bits
+};
+
+// Unit-weight ECDF / ESF over the cell-space lattice `g` (dims = output extents).
+PartPlan plan_ecdf_partition(const BinGrid &g, int64_t n);
+// Carve (ws == nullptr: size only) and run.  epi: the final epilogue (axis 0).
+int ecdf_partitioned(const double *x, int64_t n, const double *knots, const BinGrid &g,
+                     const bool *rev, const PartPlan &plan, const Epi &epi, Workspace &W,
+                     bool run, cudaStream_t st);
+
+// Laplacian KDE: full-space binning (dims M_k + 1) shared by all 2^d terms.
+PartPlan plan_kde_partition(int d, const int64_t *m, int64_t n);
+int kde_partitioned(const double *x, int64_t n, const double *w, const double *knots,
+                    const int64_t *m, int d, const double *h, const double *centre,
+                    const PartPlan &plan, double *out, Workspace &W, bool run, cudaStream_t st);
+
+}  // namespace fcg

@@ -75,16 +75,28 @@ __global__ void __launch_bounds__(256) lines_kernel(T *__restrict__ lat, int64_t
     int64_t jj = j0;
     for (; jj + kUnroll <= j1; jj += kUnroll) {
       T v[kUnroll];
+      double ov[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         const int64_t j = REV ? (D - 1 - (jj + u)) : (jj + u);
         v[u] = base[j * B];
+        // the KDE accumulator is read-modify-written: issue its loads with the lattice loads
+        // (the compiler cannot hoist them past the stores on its own)
+        if constexpr (EK == EPI_KDE)
+          ov[u] = e.accumulate ? static_cast<const double *>(e.out)[a * D * B + j * B + b] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         const int64_t j = REV ? (D - 1 - (jj + u)) : (jj + u);
         carry += v[u];
-        emit<T, EK>(lat, e, a * D * B + j * B + b, j, zo, carry);
+        if constexpr (EK == EPI_KDE) {
+          double r = (zo * e.zf[e.zoff[e.ax] + j]) * (double)carry;
+          if (e.accumulate) r = ov[u] + r;
+          if (e.apply_scale) r = r * e.scale;
+          static_cast<double *>(e.out)[a * D * B + j * B + b] = r;
+        } else {
+          emit<T, EK>(lat, e, a * D * B + j * B + b, j, zo, carry);
+        }
       }
     }
     for (; jj < j1; ++jj) {

@@ -120,39 +120,52 @@ __global__ void radix_init_kernel(const double *__restrict__ x, int64_t n, int64
   }
 }
 
-__global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint64_t *__restrict__ keys,
+template <typename KeyT>
+__global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const KeyT *__restrict__ keys,
                                                                   int64_t n, int shift,
                                                                   int32_t *__restrict__ hist,
                                                                   int64_t tiles) {
-  __shared__ int32_t s_hist[256];
-  s_hist[threadIdx.x] = 0;
-  __syncthreads();
+  __shared__ int32_t s_hist[kSortThreads / 32][256];
+  const int warp = threadIdx.x >> 5;
+  for (int d = threadIdx.x & 31; d < 256; d += 32) s_hist[warp][d] = 0;
+  __syncwarp();
   const int64_t base = (int64_t)blockIdx.x * kSortTile;
-  const int lane = threadIdx.x & 31;
 #pragma unroll 4
   for (int j = 0; j < kSortItems; ++j) {
     const int64_t i = base + (int64_t)j * kSortThreads + threadIdx.x;
-    const bool ok = i < n;
-    const unsigned dig = ok ? (unsigned)((keys[i] >> shift) & 0xFF) : 256u + lane;
-    const unsigned peers = __match_any_sync(0xffffffffu, dig);
-    if (ok && lane == __ffs(peers) - 1) atomicAdd(&s_hist[dig], __popc(peers));
+    if (i < n) atomicAdd(&s_hist[warp][(unsigned)((keys[i] >> shift) & 0xFF)], 1);
   }
   __syncthreads();
-  hist[(int64_t)threadIdx.x * tiles + blockIdx.x] = s_hist[threadIdx.x];
+  int32_t tot = 0;
+#pragma unroll
+  for (int w = 0; w < kSortThreads / 32; ++w) tot += s_hist[w][threadIdx.x];
+  hist[(int64_t)threadIdx.x * tiles + blockIdx.x] = tot;
 }
 
-__global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
-    const uint64_t *__restrict__ kin, const int32_t *__restrict__ vin, uint64_t *__restrict__ kout,
+// Stable scatter of one tile (4096 items) by one 8-bit digit.  Items are first ranked inside
+// the tile (warp peers via __match_any_sync + per-warp digit counters), staged in shared memory
+// in digit order, then written out so that consecutive threads write consecutive addresses of
+// each digit's run (coalesced) instead of 32 scattered 4-byte stores per warp.
+template <typename KeyT>
+__global__ void __launch_bounds__(kSortThreads, 3) radix_scatter_kernel(
+    const KeyT *__restrict__ kin, const int32_t *__restrict__ vin, KeyT *__restrict__ kout,
     int32_t *__restrict__ vout, int64_t n, int shift, const int32_t *__restrict__ offs,
     int64_t tiles) {
-  __shared__ int32_t s_cnt[kSortThreads / 32][256];
-  __shared__ int32_t s_goff[256];
+  extern __shared__ __align__(16) unsigned char rs_smem[];
+  KeyT *s_key = reinterpret_cast<KeyT *>(rs_smem);                       // [kSortTile]
+  int32_t *s_val = reinterpret_cast<int32_t *>(s_key + kSortTile);        // [kSortTile]
+  int32_t *s_cnt = s_val + kSortTile;                                     // [8][256]
+  int32_t *s_goff = s_cnt + (kSortThreads / 32) * 256;                    // [256]
+  int32_t *s_tstart = s_goff + 256;                                       // [256]
+  int32_t *s_wsum = s_tstart + 256;                                       // [8]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int d = lane; d < 256; d += 32) s_cnt[warp][d] = 0;
+  for (int d = lane; d < 256; d += 32) s_cnt[warp * 256 + d] = 0;
   s_goff[threadIdx.x] = offs[(int64_t)threadIdx.x * tiles + blockIdx.x];
   __syncwarp();
-  const int64_t base = (int64_t)blockIdx.x * kSortTile + (int64_t)warp * (kSortTile / 8);
-  uint64_t k[kSortItems];
+  const int64_t tile0 = (int64_t)blockIdx.x * kSortTile;
+  const int64_t base = tile0 + (int64_t)warp * (kSortTile / 8);
+  const int tile_n = (int)((n - tile0) < kSortTile ? (n - tile0) : kSortTile);
+  KeyT k[kSortItems];
   int32_t v[kSortItems];
   int32_t r[kSortItems];
   const unsigned lt = lanemask_lt();
@@ -160,27 +173,40 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
   for (int j = 0; j < kSortItems; ++j) {
     const int64_t i = base + (int64_t)j * 32 + lane;
     const bool ok = i < n;
-    k[j] = ok ? kin[i] : 0ull;
+    k[j] = ok ? kin[i] : KeyT(0);
     v[j] = ok ? vin[i] : 0;
     const unsigned dig = ok ? (unsigned)((k[j] >> shift) & 0xFF) : 256u + lane;
     const unsigned peers = __match_any_sync(0xffffffffu, dig);
     int32_t before = 0;
-    if (ok) before = s_cnt[warp][dig];
+    if (ok) before = s_cnt[warp * 256 + dig];
     __syncwarp();
-    if (ok && lane == __ffs(peers) - 1) s_cnt[warp][dig] = before + __popc(peers);
+    if (ok && lane == __ffs(peers) - 1) s_cnt[warp * 256 + dig] = before + __popc(peers);
     __syncwarp();
     r[j] = before + __popc(peers & lt);
   }
   __syncthreads();
   {
-    const int d = threadIdx.x;  // 256 threads, one digit each
+    // per digit: exclusive prefix over warps, and the digit's total for the tile-level scan
+    const int d = threadIdx.x;
     int32_t run = 0;
 #pragma unroll
     for (int w = 0; w < kSortThreads / 32; ++w) {
-      const int32_t t = s_cnt[w][d];
-      s_cnt[w][d] = run;
+      const int32_t t = s_cnt[w * 256 + d];
+      s_cnt[w * 256 + d] = run;
       run += t;
     }
+    // exclusive scan of the 256 digit totals -> tile start of every digit run
+    int32_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[warp] = x;
+    __syncthreads();
+    int32_t wpre = 0;
+    for (int w = 0; w < warp; ++w) wpre += s_wsum[w];
+    s_tstart[d] = wpre + x - run;
   }
   __syncthreads();
 #pragma unroll
@@ -188,11 +214,24 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     const int64_t i = base + (int64_t)j * 32 + lane;
     if (i < n) {
       const unsigned dig = (unsigned)((k[j] >> shift) & 0xFF);
-      const int64_t dst = (int64_t)s_goff[dig] + s_cnt[warp][dig] + r[j];
-      kout[dst] = k[j];
-      vout[dst] = v[j];
+      const int pos = s_tstart[dig] + s_cnt[warp * 256 + dig] + r[j];
+      s_key[pos] = k[j];
+      s_val[pos] = v[j];
     }
   }
+  __syncthreads();
+  for (int pos = threadIdx.x; pos < tile_n; pos += kSortThreads) {
+    const KeyT key = s_key[pos];
+    const unsigned dig = (unsigned)((key >> shift) & 0xFF);
+    const int64_t dst = (int64_t)s_goff[dig] + (pos - s_tstart[dig]);
+    kout[dst] = key;
+    vout[dst] = s_val[pos];
+  }
+}
+
+template <typename KeyT>
+constexpr size_t radix_scatter_smem() {
+  return (size_t)kSortTile * (sizeof(KeyT) + 4) + ((kSortThreads / 32) * 256 + 256 + 256 + 8) * 4;
 }
 
 __global__ void rank_heads_kernel(const uint64_t *__restrict__ keys,
@@ -262,24 +301,28 @@ int radix_init_f64(const double *x, int64_t n, int64_t stride, uint64_t *keys, i
   return FCG_OK;
 }
 
-int radix_sort_pairs(uint64_t *keys, int32_t *vals, int64_t n, int begin_bit, int end_bit,
+template <typename KeyT>
+int radix_sort_pairs(KeyT *keys, int32_t *vals, int64_t n, int begin_bit, int end_bit,
                      const RadixWs &ws, cudaStream_t st) {
   if (n <= 1) return FCG_OK;
   const int64_t tiles = ceil_div(n, kSortTile);
-  uint64_t *ka = keys, *kb = ws.keys_alt;
+  KeyT *ka = keys, *kb = reinterpret_cast<KeyT *>(ws.keys_alt);
   int32_t *va = vals, *vb = ws.vals_alt;
   int passes = 0;
   for (int shift = begin_bit; shift < end_bit; shift += 8) {
     {
       FCG_PROF("radix_hist", st);
-      radix_hist_kernel<<<(unsigned)tiles, kSortThreads, 0, st>>>(ka, n, shift, ws.hist, tiles);
+      radix_hist_kernel<KeyT><<<(unsigned)tiles, kSortThreads, 0, st>>>(ka, n, shift, ws.hist, tiles);
       FCG_LAUNCH_CHECK();
     }
     FCG_TRY(scan_i32(ws.hist, ws.hist, 256 * tiles, false, ws.partial, st));
     {
       FCG_PROF("radix_scatter", st);
-      radix_scatter_kernel<<<(unsigned)tiles, kSortThreads, 0, st>>>(ka, va, kb, vb, n, shift,
-                                                                     ws.hist, tiles);
+      constexpr size_t sm = radix_scatter_smem<KeyT>();
+      FCG_CUDA_TRY(cudaFuncSetAttribute(radix_scatter_kernel<KeyT>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      radix_scatter_kernel<KeyT><<<(unsigned)tiles, kSortThreads, sm, st>>>(ka, va, kb, vb, n, shift,
+                                                                            ws.hist, tiles);
       FCG_LAUNCH_CHECK();
     }
     std::swap(ka, kb);
@@ -287,11 +330,16 @@ int radix_sort_pairs(uint64_t *keys, int32_t *vals, int64_t n, int begin_bit, in
     ++passes;
   }
   if (passes & 1) {
-    FCG_CUDA_TRY(cudaMemcpyAsync(keys, ka, (size_t)n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+    FCG_CUDA_TRY(cudaMemcpyAsync(keys, ka, (size_t)n * sizeof(KeyT), cudaMemcpyDeviceToDevice, st));
     FCG_CUDA_TRY(cudaMemcpyAsync(vals, va, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
   }
   return FCG_OK;
 }
+
+template int radix_sort_pairs<uint64_t>(uint64_t *, int32_t *, int64_t, int, int, const RadixWs &,
+                                        cudaStream_t);
+template int radix_sort_pairs<uint32_t>(uint32_t *, int32_t *, int64_t, int, int, const RadixWs &,
+                                        cudaStream_t);
 
 int rank_outputs(const uint64_t *sorted_keys, const int32_t *order, int64_t n, int32_t *pos,
                  int32_t *lower, int32_t *upper, int32_t *dense, int32_t *heads, int32_t *start,

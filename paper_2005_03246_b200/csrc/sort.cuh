@@ -11,7 +11,7 @@ constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 items per CTA
 
 // Workspace elements needed by radix_sort_pairs for n items.
 struct RadixWs {
-  uint64_t *keys_alt;
+  uint64_t *keys_alt;  // n elements of the key type (u64 or u32 sorts reuse the same buffer)
   int32_t *vals_alt;
   int32_t *hist;     // 256 * tiles
   int32_t *partial;  // scan partials
@@ -21,7 +21,8 @@ size_t scan_ws_partial_elems(int64_t n);
 
 // Stable sort of (keys, vals) by bits [begin_bit, end_bit) of keys; in place (result in
 // keys/vals), ping-ponging through ws.keys_alt / ws.vals_alt.
-int radix_sort_pairs(uint64_t *keys, int32_t *vals, int64_t n, int begin_bit, int end_bit,
+template <typename KeyT>
+int radix_sort_pairs(KeyT *keys, int32_t *vals, int64_t n, int begin_bit, int end_bit,
                      const RadixWs &ws, cudaStream_t st);
 
 // Exclusive (or inclusive) prefix sum of int32 (in and out may alias). partial: scan ws.

@@ -243,3 +243,70 @@ def test_cfg3_full_bit_exact(oracle, cfg_meta):
     # size-independent property: last corner == number of points inside the grid box
     inside = np.all(w.points <= 4.0, axis=1).sum()
     assert counts[-1] == inside
+
+
+# ---- plane-partitioned pipeline (d >= 3, n >= 2^20) ----------------------------------------
+
+# planes >= 2 x 148 SMs so the partitioned route is taken; (300, 700, 300) needs 9 row blocks
+@pytest.mark.parametrize("dims,delta", [((300, 53, 61), (1, -1, 1)), ((40, 9, 150, 77), (-1, 1, 1, -1)),
+                                        ((300, 700, 300), (1, 1, -1)), ((12, 10, 5, 7, 9), (1, 1, 1, 1, 1))])
+def test_partitioned_ecdf_esf_vs_oracle(dims, delta, oracle):
+    oracle.set_threads(0)
+    d = len(dims)
+    rng = np.random.default_rng(sum(dims))
+    n = 1_200_000
+    x = rng.standard_normal((n, d))
+    knots = [np.sort(rng.uniform(-2.2, 2.2, m)) for m in dims]
+    knots = [np.unique(np.concatenate([z[:-2], x[:2, k]])) for k, z in enumerate(knots)]
+    grid = _grid(knots)
+    got = fcb.ecdf_fastsum_counts(fcb.validate_sample(x), grid, fcb.DeltaVector(delta))
+    ref = oracle.ecdf_fastsum(x, None, knots, delta, scaled=False)
+    np.testing.assert_array_equal(got, ref.astype(np.int64))
+    got = fcb.esf_fastsum(fcb.validate_sample(x), grid).values
+    np.testing.assert_array_equal(got, oracle.esf_fastsum(x, None, knots))
+
+
+@pytest.mark.parametrize("dims", [(320, 17, 40), (20, 16, 33, 21)])
+def test_partitioned_kde_vs_oracle(dims, oracle):
+    oracle.set_threads(0)
+    d = len(dims)
+    rng = np.random.default_rng(7 * sum(dims))
+    n = 1_100_000
+    x = rng.uniform(-1, 1, (n, d))
+    w = rng.exponential(1.0, n)
+    knots = [np.linspace(-1.1, 0.9, m) for m in dims]
+    knots[0] = np.unique(np.concatenate([knots[0], x[:3, 0]]))  # knot hits
+    h = rng.uniform(0.05, 0.3, d)
+    got = fcb.kde_fastsum(fcb.validate_sample(x, w), _grid(knots), fcb.laplacian(),
+                          fcb.Bandwidth.diag(h)).values
+    ref = oracle.kde_fastsum_laplacian(x, w, knots, h)
+    assert_rel(got, ref, REL_KDE)
+
+
+@pytest.mark.slow
+def test_cfg5_full(oracle, cfg_meta):
+    """Config 5 at full size (N = 1e8, 128^4): the ECDF's int64 counts must equal the digest of
+    the reference's own output; the KDE is checked on the reference's seeded subset."""
+    import workloads as wl
+
+    w = wl.cfg5()
+    grid = _grid(w.knots)
+    meta_a, meta_b = cfg_meta.get("cfg5a", {}), cfg_meta.get("cfg5b", {})
+    same_input = meta_a.get("input_sha") == wl.digest(w.points)
+    counts = fcb.ecdf_fastsum_counts(fcb.validate_sample(w.points), grid, fcb.DeltaVector(w.delta))
+    # size-independent properties: monotone along the last axis, corner = N (all points inside)
+    c4 = counts.reshape(128, 128, 128, 128)
+    assert counts[-1] == w.n
+    assert np.all(np.diff(c4[::17, ::13, ::11, :], axis=-1) >= 0)
+    if same_input:
+        assert wl.digest(counts) == meta_a["out_sha_i64"]
+    gold_a = cfg_golden("cfg5a")
+    if gold_a is not None and same_input:
+        np.testing.assert_array_equal(counts[gold_a["idx"]], gold_a["vals"].astype(np.int64))
+    del counts, c4
+    vals = fcb.kde_fastsum(fcb.Sample(w.points, w.extra["y"], None, False), grid, fcb.laplacian(),
+                           fcb.Bandwidth.diag(w.h)).values
+    gold_b = cfg_golden("cfg5b")
+    if gold_b is not None and meta_b.get("input_sha") == wl.digest(w.points):
+        assert_rel(vals[gold_b["idx"]], gold_b["vals"], REL_KDE)
+    assert np.all(vals > 0)
