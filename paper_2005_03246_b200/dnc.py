@@ -18,6 +18,7 @@ import numpy as np
 
 from . import _lib
 from .core import (
+    as_sample,
     EXP_OVERFLOW_GUARD,
     POINT_ALIGNED,
     Bandwidth,
@@ -70,6 +71,7 @@ def _out(sample: Sample, t):
 def ecdf_dnc(sample: Sample, include_self: bool = False, scaled: bool = True) -> EvalResult:
     """Weight sum over the points strictly below each point in every dimension
     (dnc.py:531-561); + own weight when ``include_self``; / N when ``scaled``."""
+    sample = as_sample(sample)
     import torch
 
     t0 = time.perf_counter()
@@ -106,6 +108,7 @@ def _kde_points(sample: Sample, weights_list, h: np.ndarray):
 
 def kde_dnc(sample: Sample, kernel: KernelSpec, bandwidth: Bandwidth) -> EvalResult:
     """Kernel density estimate at the sample points (dnc.py:635-690), Laplacian family."""
+    sample = as_sample(sample)
     t0 = time.perf_counter()
     _require_distinct(sample)
     fam = kernel.family

@@ -15,6 +15,7 @@ import numpy as np
 
 from . import _lib
 from .core import (
+    as_sample,
     EXP_OVERFLOW_GUARD,
     GRID_ALIGNED,
     Bandwidth,
@@ -83,6 +84,7 @@ def ecdf_fastsum(sample: Sample, grid: RectilinearGrid, delta: DeltaVector | Non
                  scaled: bool = True) -> EvalResult:
     """Generalized ECDF F_N(z, delta; x, y) at every grid node, exactly (fastsum.py:69-92).
     Unit weights give exact integer counts before the single division by N."""
+    sample = as_sample(sample)
     t0 = time.perf_counter()
     vals = _ecdf_grid_device(sample, grid, delta, False, scaled)
     return EvalResult(_out(sample, vals), GRID_ALIGNED, {
@@ -93,12 +95,14 @@ def ecdf_fastsum(sample: Sample, grid: RectilinearGrid, delta: DeltaVector | Non
 def ecdf_fastsum_counts(sample: Sample, grid: RectilinearGrid,
                         delta: DeltaVector | None = None):
     """Unit-weight grid ECDF as exact int64 counts (device tensor or numpy)."""
+    sample = as_sample(sample)
     return _out(sample, _ecdf_grid_device(sample, grid, delta, False, False, counts=True))
 
 
 def esf_fastsum(sample: Sample, grid: RectilinearGrid, scaled: bool = True) -> EvalResult:
     """Empirical survival function sum_i y_i prod_k [x_ik > z_k] on the grid
     (fastsum.py:95-111), computed directly as suffix sums of strictly-above bins."""
+    sample = as_sample(sample)
     t0 = time.perf_counter()
     vals = _ecdf_grid_device(sample, grid, None, True, scaled)
     return EvalResult(_out(sample, vals), GRID_ALIGNED, {
@@ -155,6 +159,7 @@ def _kde_uniform_grid(sample: Sample, grid: RectilinearGrid, h: np.ndarray):
 def kde_fastsum(sample: Sample, grid: RectilinearGrid, kernel: KernelSpec,
                 bandwidth: Bandwidth) -> EvalResult:
     """Kernel density estimate at every grid node by CDF decomposition (fastsum.py:204-233)."""
+    sample = as_sample(sample)
     t0 = time.perf_counter()
     if not bandwidth.is_diagonal:
         raise ParameterError("kde_fastsum requires a diagonal bandwidth")

@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .core import DeltaVector, ParameterError, RectilinearGrid, Sample
+from .core import as_sample, DeltaVector, ParameterError, RectilinearGrid, Sample
 
 
 @dataclass(frozen=True)
@@ -64,6 +64,7 @@ def _wrap(sample: Sample, t):
 def local_sums(sample: Sample, grid: RectilinearGrid,
                delta: DeltaVector | None = None) -> LocalSumTensor:
     """Local sums with the delta bin convention (histogram.py:210-217)."""
+    sample = as_sample(sample)
     delta = delta or DeltaVector.ones(sample.dim)
     return LocalSumTensor(_wrap(sample, _local_sums_device(sample, grid, delta)))
 

@@ -19,7 +19,7 @@ import time
 import numpy as np
 
 from . import _lib
-from .core import POINT_ALIGNED, Bandwidth, DeltaVector, EvalResult, ParameterError, Sample
+from .core import as_sample, POINT_ALIGNED, Bandwidth, DeltaVector, EvalResult, ParameterError, Sample
 from .dnc import _diag_bandwidth, _kde_points, _out, _require_distinct
 from .kernels import KernelSpec
 
@@ -41,6 +41,7 @@ def _points_device(sample: Sample, delta: DeltaVector | None, survival: bool, sc
 
 def ecdf_at_points(sample: Sample, delta: DeltaVector | None = None,
                    scaled: bool = True) -> EvalResult:
+    sample = as_sample(sample)
     t0 = time.perf_counter()
     vals = _points_device(sample, delta, False, scaled)
     return EvalResult(_out(sample, vals), POINT_ALIGNED, {
@@ -49,6 +50,7 @@ def ecdf_at_points(sample: Sample, delta: DeltaVector | None = None,
 
 
 def esf_at_points(sample: Sample, scaled: bool = True) -> EvalResult:
+    sample = as_sample(sample)
     t0 = time.perf_counter()
     vals = _points_device(sample, None, True, scaled)
     return EvalResult(_out(sample, vals), POINT_ALIGNED, {
@@ -59,6 +61,7 @@ def esf_at_points(sample: Sample, scaled: bool = True) -> EvalResult:
 def kde_numerators(sample: Sample, weights_list, bandwidth: Bandwidth):
     """Laplacian KDE numerators at the points for one or two weight vectors (None = unit) in a
     single device pass; (nw, n) tensor (device sample) or array."""
+    sample = as_sample(sample)
     _require_distinct(sample)
     h = _diag_bandwidth(sample, bandwidth)
     if not 1 <= len(weights_list) <= 2:
@@ -68,6 +71,7 @@ def kde_numerators(sample: Sample, weights_list, bandwidth: Bandwidth):
 
 def kernel_regression(sample: Sample, y, kernel: KernelSpec, bandwidth: Bandwidth) -> EvalResult:
     """Nadaraya-Watson regression at the sample points with a Laplacian kernel."""
+    sample = as_sample(sample)
     t0 = time.perf_counter()
     if kernel.family != "laplacian":
         raise ParameterError(f"kernel_regression supports the laplacian kernel, got {kernel.family!r}")

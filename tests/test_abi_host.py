@@ -112,3 +112,18 @@ def test_dimension_mismatch_raises_before_device_work():
     with pytest.raises(fcb.ParameterError):
         fcb.kde_fastsum(s, fcb.RectilinearGrid.from_knots([[0.5], [0.5]]), fcb.laplacian(),
                         fcb.Bandwidth.full(np.eye(2)))
+
+
+def test_reference_style_objects_are_accepted():
+    """Duck typing: an object shaped like the reference's fastcdf.Sample works."""
+    from types import SimpleNamespace
+
+    ref_like = SimpleNamespace(points=np.zeros((3, 2)), weights=np.ones(3),
+                               distinct_by_dim=(False, False))
+    s = fcb.core.as_sample(ref_like)
+    assert s.count == 3 and s.distinct_by_dim == (False, False) and s.unit_weights
+    g = fcb.RectilinearGrid.from_knots([[0.5]])
+    with pytest.raises(fcb.ParameterError, match="dimension mismatch"):
+        fcb.local_sums(ref_like, g)
+    with pytest.raises(fcb.TieError):
+        fcb.ecdf_dnc(ref_like)
