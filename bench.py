@@ -148,6 +148,15 @@ def grid_kde_bytes(n, d, m, unit_w):
 class GridWorkload:
     """Grid configs (1, 3, 5a, 5b, 5): device-resident sample + public API calls."""
 
+    scaling = "strong"  # the configuration's total work is fixed; N > 1 shards it
+
+    @staticmethod
+    def parallelism(world):
+        if world == 1:
+            return "single GPU"
+        return (f"slab x{world}: lattice split along axis 1, points routed with one NCCL "
+                f"all-to-all, slab carry planes exchanged with an NCCL all-gather")
+
     def __init__(self, name):
         import paper_2005_03246_b200 as fcb
 
@@ -180,53 +189,81 @@ class GridWorkload:
             if self.n * self.d * 8 > 126e6 else "L2-resident (launch-bound config)",
         }
 
+    def shard(self, rank, world):
+        """Strong scaling over the fixed config: rank r holds points r::world."""
+        self.rank, self.world = rank, world
+        self.n_total = self.n
+        if world > 1:
+            self.pts = np.ascontiguousarray(self.w.points[rank::world])
+            self.yv = None if self.y is None else np.ascontiguousarray(self.y[rank::world])
+        else:
+            self.pts, self.yv = self.w.points, self.y
+
     def to_device(self):
         import torch
 
         fcb = self.fcb
-        x = torch.from_numpy(self.w.points).cuda()
-        self.s_unit = fcb.Sample(x, torch.ones(self.n, dtype=torch.float64, device=x.device),
+        x = torch.from_numpy(self.pts).cuda()
+        self.s_unit = fcb.Sample(x, torch.ones(x.shape[0], dtype=torch.float64, device=x.device),
                                  None, True)
         if self.do_kde:
-            y = torch.from_numpy(self.y).cuda()
+            y = torch.from_numpy(self.yv).cuda()
             self.s_y = fcb.Sample(x, y, None, False)
 
     def to_pinned(self):
         import torch
 
         fcb = self.fcb
-        xp = torch.from_numpy(self.w.points).pin_memory()
+        xp = torch.from_numpy(self.pts).pin_memory()
         self.p_unit = fcb.Sample(xp, torch.ones(1), None, True)
-        self.out_pinned = torch.empty(int(np.prod(self.m)), dtype=torch.float64).pin_memory()
+        nloc = int(np.prod(self.m))
+        self.out_pinned = torch.empty(nloc, dtype=torch.float64).pin_memory()
         if self.do_kde:
-            yp = torch.from_numpy(self.y).pin_memory()
+            yp = torch.from_numpy(self.yv).pin_memory()
             self.p_y = fcb.Sample(xp, yp, None, False)
-            self.out2_pinned = torch.empty(int(np.prod(self.m)), dtype=torch.float64).pin_memory()
-        self.h2d_bytes = self.w.points.nbytes + (self.y.nbytes if self.do_kde else 0)
-        self.d2h_bytes = self.out_pinned.numel() * 8 * (int(self.do_ecdf) + int(self.do_kde))
+            self.out2_pinned = torch.empty(nloc, dtype=torch.float64).pin_memory()
+        self.h2d_bytes = self.pts.nbytes + (self.yv.nbytes if self.do_kde else 0)
+        self.d2h_bytes = nloc * 8 * (int(self.do_ecdf) + int(self.do_kde)) // self.world
+
+    def _ecdf(self, s):
+        if self.world > 1:
+            from paper_2005_03246_b200 import distributed as fdist
+
+            return fdist.ecdf_fastsum_slab(s, self.grid, self.delta).values
+        return self.fcb.ecdf_fastsum(s, self.grid, self.delta).values
+
+    def _kde(self, s):
+        if self.world > 1:
+            from paper_2005_03246_b200 import distributed as fdist
+
+            return fdist.kde_fastsum_slab(s, self.grid, self.fcb.laplacian(), self.bw).values
+        return self.fcb.kde_fastsum(s, self.grid, self.fcb.laplacian(), self.bw).values
 
     def step(self):
-        fcb = self.fcb
         if self.do_ecdf:
-            fcb.ecdf_fastsum(self.s_unit, self.grid, self.delta)
+            self._ecdf(self.s_unit)
         if self.do_kde:
-            fcb.kde_fastsum(self.s_y, self.grid, fcb.laplacian(), self.bw)
+            self._kde(self.s_y)
 
     def step_e2e(self):
-        fcb = self.fcb
         if self.do_ecdf:
-            v = fcb.ecdf_fastsum(self.p_unit, self.grid, self.delta).values
-            self.out_pinned.copy_(v, non_blocking=True)
+            v = self._ecdf(self.p_unit)
+            self.out_pinned[: v.numel()].copy_(v, non_blocking=True)
         if self.do_kde:
-            v = fcb.kde_fastsum(self.p_y, self.grid, fcb.laplacian(), self.bw).values
-            self.out2_pinned.copy_(v, non_blocking=True)
+            v = self._kde(self.p_y)
+            self.out2_pinned[: v.numel()].copy_(v, non_blocking=True)
 
     def bytes_per_launch(self):
+        # per rank: ~1/world of the points and of the lattice (axis-1 slab) when sharded
+        n = self.n // self.world
+        m = list(self.m)
+        if self.world > 1:
+            m[1] = max(1, m[1] // self.world)
         b = {}
         if self.do_kde:
-            b.update(grid_kde_bytes(self.n, self.d, self.m, False))
+            b.update(grid_kde_bytes(n, self.d, m, False))
         if self.do_ecdf:
-            e = grid_ecdf_bytes(self.n, self.d, self.m, True)
+            e = grid_ecdf_bytes(n, self.d, m, True)
             for k, v in e.items():
                 if k in b:  # shared label between ECDF and KDE: keep them apart
                     b[k + "@ecdf"] = v
@@ -236,23 +273,36 @@ class GridWorkload:
 
     # ---- CPU baseline: the oracle (restated reference algorithm) on a bounded sample ----
     def cpu_sample(self, threads):
+        """Time the oracle port on a bounded sample of this workload.  Configs with >= 5e7
+        points use the exact axis-0 slab made of the first 1/8 of the grid's axis-0 knots and
+        the points falling in it (the ECDF there is exactly that sub-problem); the KDE is timed
+        on one of its 2^d delta-terms and scaled by 2^d."""
         import oracle
 
         used = oracle.set_threads(threads)
+        knots = [np.asarray(z) for z in self.w.knots]
+        pts, y = self.w.points, self.y
+        frac = 8 if self.n >= 50_000_000 else 1
+        if frac > 1:
+            knots[0] = knots[0][: len(knots[0]) // frac]
+            sel = pts[:, 0] <= knots[0][-1]
+            pts = np.ascontiguousarray(pts[sel])
+            y = None if y is None else np.ascontiguousarray(y[sel])
+        n_s = pts.shape[0]
         t_total = 0.0
-        desc = []
+        desc = [f"{n_s} points" + (f" (axis-0 slab, 1/{frac} of the grid)" if frac > 1 else "")]
         if self.do_ecdf:
             t0 = time.perf_counter()
-            oracle.ecdf_fastsum(self.w.points, None, self.w.knots, self.w.delta, scaled=True)
+            oracle.ecdf_fastsum(pts, None, knots, self.w.delta, scaled=True)
             t_total += time.perf_counter() - t0
-            desc.append("full grid ECDF")
+            desc.append("grid ECDF")
         if self.do_kde:
             t0 = time.perf_counter()
-            oracle.kde_fastsum_laplacian(self.w.points, self.y, self.w.knots, self.w.h, codes=[0])
+            oracle.kde_fastsum_laplacian(pts, y, knots, self.w.h, codes=[0])
             dt = time.perf_counter() - t0
             t_total += dt * (1 << self.d)
-            desc.append(f"KDE: 1 of {1 << self.d} delta-terms timed on the full data, x{1 << self.d}")
-        return self.n / t_total, used, "; ".join(desc), t_total
+            desc.append(f"KDE: 1 of {1 << self.d} delta-terms timed, x{1 << self.d}")
+        return n_s / t_total, used, "; ".join(desc), t_total
 
 
 def dominant(prof: dict, bytes_map: dict):
@@ -278,6 +328,12 @@ class PointsWorkload:
     """At-points configs: cfg2 (ECDF delta=(1,-1) + ESF with ties, N = 1e6) and cfg4 (Laplacian
     KDE density + regression numerators, N = 1e7, one device pass)."""
 
+    scaling = "weak"
+
+    @staticmethod
+    def parallelism(world):
+        return "single GPU" if world == 1 else f"replicas x{world} (one full problem per GPU)"
+
     def __init__(self, name):
         import paper_2005_03246_b200 as fcb
 
@@ -294,6 +350,11 @@ class PointsWorkload:
         return {"workload": self.name, "what": what, "n_points": self.n, "dims": self.d,
                 "l2": "inputs fit in L2 (launch/latency-bound config)" if self.n * 16 < 126e6
                 else f"inputs larger than L2 ({self.n * 16 / 1e9:.2f} GB points)"}
+
+    def shard(self, rank, world):
+        """At-points configs run one full replica per GPU (weak scaling)."""
+        self.rank, self.world = rank, world
+        self.n_total = self.n * world
 
     def _sample(self, x, y):
         fcb = self.fcb
@@ -398,7 +459,7 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": w.n / value * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": w.n / value * 1e3, "higher_is_better": True, "scaling": w.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded numpy, SURVEY §8d)",
         "config": w.describe(),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
@@ -428,6 +489,7 @@ def main():
 
     _lib.load_library()
     w = make_workload(args.workload)
+    w.shard(rank, world)
     w.to_device()
     torch.cuda.synchronize()
 
@@ -463,7 +525,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     ms_step = ms_max / args.steps
-    value = world * w.n / (ms_step / 1e3)
+    value = w.n_total / (ms_step / 1e3)
 
     launches = sum(c for k, (c, _) in prof.items() if k != "lattice_zero")
     peak, peak_src = peaks()
@@ -499,7 +561,7 @@ def main():
         if world > 1:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         e_step = float(ems.item()) / args.e2e_steps
-        e2e = {"value": world * w.n / (e_step / 1e3), "unit": UNIT,
+        e2e = {"value": w.n_total / (e_step / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": w.h2d_bytes, "d2h_bytes_per_step": w.d2h_bytes,
                "ms_per_step": e_step, "steps": args.e2e_steps}
 
@@ -513,9 +575,9 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": w.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded numpy, SURVEY §8d shapes)",
-            "config": {**w.describe(), "parallelism": f"replicas x{world}" if world > 1 else "single"},
+            "config": {**w.describe(), "parallelism": w.parallelism(world)},
             "e2e": e2e, "gpu_launches": int(launches), "roofline": roof,
             "cpu_baseline": cpu, "clocks": clk, "kernels": breakdown,
         }

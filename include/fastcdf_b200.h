@@ -110,6 +110,47 @@ int fcg_kde_grid_laplacian(const double *x, int64_t n, int32_t d, const double *
                            void *ws, size_t *ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------------------
+ * Multi-GPU slab decomposition along axis 1 (used by paper_2005_03246_b200.distributed)
+ * ------------------------------------------------------------------------------------- */
+
+/* owner[i] = r with bounds[r] <= c < bounds[r+1] where c = b - shift is point i's cell along
+ * `axis` (b = #knots_axis < x, or <= x when le), or -1 when no slab holds it.  G <= 64. */
+int fcg_axis_owner(const double *x, int64_t n, int32_t d, int32_t axis, const double *knots_axis,
+                   int64_t m, int32_t le, int32_t shift, const int64_t *bounds, int32_t G,
+                   int32_t *owner, void *stream);
+
+/* Stable partition of the rows of x (and w, may be NULL) by owner (rows with owner -1 are
+ * dropped): x_out / w_out hold owner 0's rows, then owner 1's, ...; counts (host, G) per owner.
+ * Syncs (the counts size the all-to-all). */
+int fcg_partition_rows(const double *x, int64_t n, int32_t d, const double *w,
+                       const int32_t *owner, int32_t G, double *x_out, double *w_out,
+                       int64_t *counts, void *ws, size_t *ws_bytes, void *stream);
+
+/* out[a][j][b] = (local[a][j][b] + carry[a][b]) / div (div <= 0: no division); kind 0: local and
+ * carry are int64 counts, 1: fp64.  The carry plane is the all-gathered axis-1 prefix of the
+ * lower slabs (or suffix of the higher slabs). */
+int fcg_slab_finish(const void *local, int32_t kind, const void *carry, int64_t A, int64_t J,
+                    int64_t B, double div, double *out, void *stream);
+
+/* fcg_kde_grid_laplacian with extras: n_scale is the N of the normalisation (the global N on a
+ * slab); u_bound (> 0 when known) bounds sum_k max_i |x_ik - c_k| / h_k and, when <= 600, lets
+ * the kernels build each term's weights from per-point exponential factors instead of one exp
+ * per point and term (the reference's fastsum.py:114-129 guard bounds the span per dimension);
+ * when planes != NULL, term `code` also stores its slab-boundary plane of S (last axis-1 plane
+ * for delta_1 = +1, first for -1) at planes[code * (M_0 * M_2 * ... * M_{d-1})]. */
+int fcg_kde_grid_laplacian_ex(const double *x, int64_t n, int32_t d, const double *w,
+                              const double *knots, const int64_t *m, const double *h,
+                              const double *centre, double n_scale, double u_bound,
+                              double *planes, double *out, void *ws, size_t *ws_bytes,
+                              void *stream);
+
+/* out[i] += sum_code zfac_code(i) * C_code[i_0, i_2, ...] / (2^d n_scale prod h): the exchanged
+ * carry planes of every term folded into a slab's KDE (the zfac factor is linear in S). */
+int fcg_kde_carry_fixup(double *out, int32_t d, const int64_t *m, const double *knots,
+                        const double *h, const double *centre, const double *planes,
+                        double n_scale, void *ws, size_t *ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------------------
  * Ranking (subsystem 1): device LSD radix sort of fp64 keys.
  * keys: device, element i at keys[i*stride].  Outputs (device int32, any may be NULL):
  *   order[p]  = index of the element at sorted position p (stable)

@@ -375,10 +375,14 @@ extern "C" int fcg_minmax(const double *x, int64_t n, int32_t d, double *out_min
   return FCG_OK;
 }
 
-extern "C" int fcg_kde_grid_laplacian(const double *x, int64_t n, int32_t d, const double *w,
-                                      const double *knots, const int64_t *m, const double *h,
-                                      const double *centre, double *out, void *ws,
-                                      size_t *ws_bytes, void *stream) {
+namespace fcg {
+
+// Laplacian grid KDE (fastsum.py:139-169,179-182).  n_scale: N of the normalisation;
+// planes: optional per-term slab-boundary plane capture (see fcg_kde_grid_laplacian_ex).
+static int kde_grid_impl(const double *x, int64_t n, int32_t d, const double *w,
+                         const double *knots, const int64_t *m, const double *h,
+                         const double *centre, double n_scale, double u_bound, double *planes,
+                         double *out, void *ws, size_t *ws_bytes, void *stream) {
   FCG_TRY(check_common(n, d, m));
   LatShape s;
   s.d = d;
@@ -390,11 +394,13 @@ extern "C" int fcg_kde_grid_laplacian(const double *x, int64_t n, int32_t d, con
   const int64_t L = s.size();
   for (int k = 0; k < d; ++k)
     if (!(h[k] > 0.0)) return fail(FCG_EINVAL, "bandwidth must be > 0");
+  if (planes && d < 2) return fail(FCG_EINVAL, "slab planes need d >= 2");
   cudaStream_t st = as_stream(stream);
   Workspace W(ws);
   const PartPlan plan = plan_kde_partition(d, m, n);
   if (plan.ok) {
-    FCG_TRY(kde_partitioned(x, n, w, knots, m, d, h, centre, plan, out, W, ws != nullptr, st));
+    FCG_TRY(kde_partitioned(x, n, w, knots, m, d, h, centre, u_bound > 0.0 ? u_bound : 1e300,
+                            n_scale, planes, plan, out, W, ws != nullptr, st));
     if (ws == nullptr) *ws_bytes = W.bytes();
     return FCG_OK;
   }
@@ -407,16 +413,15 @@ extern "C" int fcg_kde_grid_laplacian(const double *x, int64_t n, int32_t d, con
   }
   double prod_h = 1.0;
   for (int k = 0; k < d; ++k) prod_h *= h[k];
-  const double scale = 1.0 / (std::ldexp(1.0, d) * (double)n * prod_h);
+  const double scale = 1.0 / (std::ldexp(1.0, d) * n_scale * prod_h);
+  int64_t plane_sz = m[0];
+  for (int k = 2; k < d; ++k) plane_sz *= m[k];
   const int ncodes = 1 << d;
   for (int code = 0; code < ncodes; ++code) {
     int le[FCG_MAX_DIM];
     int64_t shift[FCG_MAX_DIM];
     bool rev[FCG_MAX_DIM];
     PsiParams pp{};
-    ZfParams zp{};
-    zp.d = d;
-    int64_t off = 0;
     for (int k = 0; k < d; ++k) {
       const double sgn = ((code >> k) & 1) ? -1.0 : 1.0;  // DeltaVector.from_code, core.py:165-168
       le[k] = 0;                                       // one delta=+1 binning for every term
@@ -424,19 +429,9 @@ extern "C" int fcg_kde_grid_laplacian(const double *x, int64_t n, int32_t d, con
       rev[k] = sgn < 0;
       pp.c[k] = centre[k];
       pp.a[k] = sgn / h[k];
-      zp.m[k] = m[k];
-      zp.koff[k] = off;
-      off += m[k];
-      zp.c[k] = centre[k];
-      zp.h[k] = h[k];
-      zp.s[k] = sgn;
     }
     BinGrid g = make_bin_grid(d, m, le, shift, s.dims);
-    {
-      FCG_PROF("kde_zfac", st);
-      zf_kernel<<<grid_for(total_knots, 256, 1), 256, 0, st>>>(knots, zp, zf, total_knots);
-    }
-    FCG_LAUNCH_CHECK();
+    FCG_TRY(launch_kde_zf(knots, d, m, centre, h, code, zf, st));
     {
       FCG_PROF("lattice_zero", st);
       FCG_CUDA_TRY(cudaMemsetAsync(lat, 0, (size_t)L * sizeof(double), st));
@@ -446,11 +441,113 @@ extern "C" int fcg_kde_grid_laplacian(const double *x, int64_t n, int32_t d, con
     e.kind = EPI_KDE;
     e.out = out;
     e.zf = zf;
-    for (int k = 0; k < d; ++k) e.zoff[k] = zp.koff[k];
+    int64_t off = 0;
+    for (int k = 0; k < d; ++k) {
+      e.zoff[k] = off;
+      off += m[k];
+    }
     e.accumulate = code > 0;
     e.apply_scale = code == ncodes - 1;
     e.scale = scale;
+    if (planes) {
+      e.plane_out = planes + (int64_t)code * plane_sz;
+      e.plane_idx = rev[1] ? 0 : m[1] - 1;
+    }
     FCG_TRY(scan_lattice<double>(lat, s, rev, e, scratch, st));
   }
+  return FCG_OK;
+}
+
+namespace {
+// out[i] += scale * sum_code zfac_code(i) * C_code[i0, i2, ..]   (slab carry fix-up)
+struct FixP {
+  int d, ncodes;
+  int64_t dims[FCG_MAX_DIM];
+  int64_t zoff[FCG_MAX_DIM];
+  int64_t zsz;        // entries per code in zf
+  int64_t plane_sz;   // entries per code in C
+  double scale;
+};
+
+__global__ void kde_fixup_kernel(double *__restrict__ out, FixP p, const double *__restrict__ zf,
+                                 const double *__restrict__ C) {
+  int64_t L = 1;
+  for (int k = 0; k < p.d; ++k) L *= p.dims[k];
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t idx[FCG_MAX_DIM];
+    int64_t rem = t;
+    for (int k = p.d - 1; k >= 0; --k) {
+      idx[k] = rem % p.dims[k];
+      rem /= p.dims[k];
+    }
+    int64_t pi = idx[0];
+    for (int k = 2; k < p.d; ++k) pi = pi * p.dims[k] + idx[k];
+    double acc = 0.0;
+    for (int code = 0; code < p.ncodes; ++code) {
+      const double *z = zf + code * p.zsz;
+      double zz = 1.0;
+      for (int k = 0; k < p.d; ++k) zz *= z[p.zoff[k] + idx[k]];
+      acc += zz * C[code * p.plane_sz + pi];
+    }
+    out[t] += p.scale * acc;
+  }
+}
+}  // namespace
+
+}  // namespace fcg
+
+extern "C" int fcg_kde_grid_laplacian(const double *x, int64_t n, int32_t d, const double *w,
+                                      const double *knots, const int64_t *m, const double *h,
+                                      const double *centre, double *out, void *ws,
+                                      size_t *ws_bytes, void *stream) {
+  return kde_grid_impl(x, n, d, w, knots, m, h, centre, (double)n, -1.0, nullptr, out, ws,
+                       ws_bytes, stream);
+}
+
+extern "C" int fcg_kde_grid_laplacian_ex(const double *x, int64_t n, int32_t d, const double *w,
+                                         const double *knots, const int64_t *m, const double *h,
+                                         const double *centre, double n_scale, double u_bound,
+                                         double *planes, double *out, void *ws, size_t *ws_bytes,
+                                         void *stream) {
+  return kde_grid_impl(x, n, d, w, knots, m, h, centre, n_scale, u_bound, planes, out, ws,
+                       ws_bytes, stream);
+}
+
+extern "C" int fcg_kde_carry_fixup(double *out, int32_t d, const int64_t *m, const double *knots,
+                                   const double *h, const double *centre, const double *planes,
+                                   double n_scale, void *ws, size_t *ws_bytes, void *stream) {
+  if (d < 2 || d > FCG_MAX_DIM) return fail(FCG_EINVAL, "dimension out of range");
+  int64_t total_knots = 0;
+  for (int k = 0; k < d; ++k) total_knots += m[k];
+  const int ncodes = 1 << d;
+  Workspace W(ws);
+  double *zf = W.take<double>((size_t)ncodes * total_knots);
+  if (ws == nullptr) {
+    *ws_bytes = W.bytes();
+    return FCG_OK;
+  }
+  cudaStream_t st = as_stream(stream);
+  for (int code = 0; code < ncodes; ++code)
+    FCG_TRY(launch_kde_zf(knots, d, m, centre, h, code, zf + (int64_t)code * total_knots, st));
+  FixP p{};
+  p.d = d;
+  p.ncodes = ncodes;
+  int64_t off = 0, L = 1;
+  for (int k = 0; k < d; ++k) {
+    p.dims[k] = m[k];
+    p.zoff[k] = off;
+    off += m[k];
+    L *= m[k];
+  }
+  p.zsz = total_knots;
+  p.plane_sz = L / m[1];
+  double prod_h = 1.0;
+  for (int k = 0; k < d; ++k) prod_h *= h[k];
+  p.scale = 1.0 / (std::ldexp(1.0, d) * n_scale * prod_h);
+  if (L == 0) return FCG_OK;
+  FCG_PROF("dist_kde_fixup", st);
+  kde_fixup_kernel<<<grid_for(L, 256), 256, 0, st>>>(out, p, zf, planes);
+  FCG_LAUNCH_CHECK();
   return FCG_OK;
 }

@@ -17,6 +17,7 @@ namespace {
 
 constexpr uint32_t kDead = 0xFFFFFFFFu;
 constexpr int kPlaneThreads = 512;
+constexpr int kKdeThreads = 512;
 constexpr size_t kEcdfTileBytes = 96 * 1024;   // int32 tile budget (2 CTAs per SM)
 constexpr size_t kKdeTileBytes = 72 * 1024;    // fp64 row-block budget (3 CTAs per SM)
 constexpr int64_t kMinPartitionN = int64_t(1) << 20;
@@ -151,6 +152,162 @@ __device__ __forceinline__ void tile_scan(T *tile, int nr, int W, bool rev_r, bo
   __syncthreads();
 }
 
+template <typename T> struct V16 {};
+template <> struct V16<double> { using vt = double2; static constexpr int V = 2; };
+template <> struct V16<int32_t> { using vt = int4; static constexpr int V = 4; };
+
+template <typename T>
+__device__ __forceinline__ void v16_load(const T *p, T *r) {
+  if constexpr (sizeof(T) == 8) {
+    const double2 a = *reinterpret_cast<const double2 *>(p);
+    r[0] = a.x; r[1] = a.y;
+  } else {
+    const int4 a = *reinterpret_cast<const int4 *>(p);
+    r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w;
+  }
+}
+template <typename T>
+__device__ __forceinline__ void v16_store(T *p, const T *r) {
+  if constexpr (sizeof(T) == 8) {
+    *reinterpret_cast<double2 *>(p) = make_double2(r[0], r[1]);
+  } else {
+    *reinterpret_cast<int4 *>(p) = make_int4(r[0], r[1], r[2], r[3]);
+  }
+}
+
+// Vectorised tile scan for rows whose length is a multiple of 32 * V (V = 16 / sizeof(T)):
+// every lane owns E = W / 32 consecutive elements read with 16-byte shared accesses
+// (conflict-free), scans them serially, and one warp scan stitches the lanes; columns are
+// walked V at a time with pointer increments (no per-element index arithmetic).
+// Requires W % (32 * V) == 0 and E <= 16.
+template <typename T, int EMAX>
+__device__ __forceinline__ void tile_scan_vec(T *tile, int nr, int W, bool rev_r, bool rev_c,
+                                              T *carry, T *seg) {
+  constexpr int V = V16<T>::V;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  constexpr int E = EMAX;  // W == 32 * E
+  for (int r = warp; r < nr; r += nwarps) {
+    T *row = tile + (size_t)r * W;
+    // lane-contiguous chunk in scan order: forward [lane*E, lane*E+E), reverse mirrored
+    T *chunk = rev_c ? row + (W - (lane + 1) * E) : row + lane * E;
+    T v[EMAX];
+#pragma unroll
+    for (int e = 0; e < EMAX; e += V)
+      if (e < E) v16_load<T>(chunk + e, v + e);
+    T tot = T(0);
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e)
+      if (e < E) tot += v[e];
+    T incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    T run = incl - tot;
+    if (!rev_c) {
+#pragma unroll
+      for (int e = 0; e < EMAX; ++e)
+        if (e < E) { run += v[e]; v[e] = run; }
+    } else {
+#pragma unroll
+      for (int e = EMAX - 1; e >= 0; --e)
+        if (e < E) { run += v[e]; v[e] = run; }
+    }
+#pragma unroll
+    for (int e = 0; e < EMAX; e += V)
+      if (e < E) v16_store<T>(chunk + e, v + e);
+  }
+  __syncthreads();
+  // columns, V adjacent columns per thread, G segments of rows per column group
+  const int CG = W / V;
+  const int G = (int)blockDim.x >= CG ? (int)blockDim.x / CG : 1;
+  const int Rg = (nr + G - 1) / G;
+  const long step = rev_r ? -(long)W : (long)W;
+  for (int cc = threadIdx.x; cc < CG * G; cc += blockDim.x) {
+    const int cgi = cc % CG, g = cc / CG;
+    const int q0 = g * Rg, q1 = min(nr, (g + 1) * Rg);
+    T s[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) s[k] = T(0);
+    if (q0 < q1) {
+      const T *p = tile + (size_t)(rev_r ? nr - 1 - q0 : q0) * W + cgi * V;
+      for (int q = q0; q < q1; ++q, p += step) {
+        T a[V];
+        v16_load<T>(p, a);
+#pragma unroll
+        for (int k = 0; k < V; ++k) s[k] += a[k];
+      }
+    }
+    v16_store<T>(seg + (size_t)g * W + cgi * V, s);
+  }
+  __syncthreads();
+  for (int cc = threadIdx.x; cc < CG * G; cc += blockDim.x) {
+    const int cgi = cc % CG, g = cc / CG;
+    const int q0 = g * Rg, q1 = min(nr, (g + 1) * Rg);
+    T run[V];
+    v16_load<T>(carry + cgi * V, run);
+    for (int gg = 0; gg < g; ++gg) {
+      T a[V];
+      v16_load<T>(seg + (size_t)gg * W + cgi * V, a);
+#pragma unroll
+      for (int k = 0; k < V; ++k) run[k] += a[k];
+    }
+    if (q0 < q1) {
+      T *p = tile + (size_t)(rev_r ? nr - 1 - q0 : q0) * W + cgi * V;
+      for (int q = q0; q < q1; ++q, p += step) {
+        T a[V];
+        v16_load<T>(p, a);
+#pragma unroll
+        for (int k = 0; k < V; ++k) { run[k] += a[k]; a[k] = run[k]; }
+        v16_store<T>(p, a);
+      }
+    }
+  }
+  __syncthreads();
+  for (int cgi = threadIdx.x; cgi < CG; cgi += blockDim.x) {
+    T c[V];
+    v16_load<T>(carry + cgi * V, c);
+    for (int g = 0; g < G; ++g) {
+      T a[V];
+      v16_load<T>(seg + (size_t)g * W + cgi * V, a);
+#pragma unroll
+      for (int k = 0; k < V; ++k) c[k] += a[k];
+    }
+    v16_store<T>(carry + cgi * V, c);
+  }
+  __syncthreads();
+}
+
+// dispatch: compile-time lane chunk for W in {32V, 64V, 128V}, generic scan otherwise
+template <typename T, int SE>
+__device__ __forceinline__ void tile_scan_any(T *tile, int nr, int W, bool rev_r, bool rev_c,
+                                              T *carry, T *seg) {
+  if constexpr (SE > 0) tile_scan_vec<T, SE>(tile, nr, W, rev_r, rev_c, carry, seg);
+  else tile_scan<T>(tile, nr, W, rev_r, rev_c, carry, seg);
+}
+
+// host: the lane chunk E (= W / 32) of the vectorised scan, 0 for the generic scan
+int scan_variant(int64_t W, int V) {
+  for (int e : {V, 2 * V, 4 * V})
+    if (e <= 8 && W == 32 * e) return e;
+  return 0;
+}
+
+template <typename T>
+__device__ __forceinline__ void tile_zero(T *tile, int count) {
+  constexpr int V = V16<T>::V;
+  if (count % V == 0) {
+    using vt = typename V16<T>::vt;
+    vt z;
+    memset(&z, 0, sizeof(vt));
+    vt *t4 = reinterpret_cast<vt *>(tile);
+    for (int i = threadIdx.x; i < count / V; i += blockDim.x) t4[i] = z;
+  } else {
+    for (int i = threadIdx.x; i < count; i += blockDim.x) tile[i] = T(0);
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ void tile_store(T *__restrict__ dst, const T *tile, int64_t count) {
   // 16-byte vector stores when both sides are aligned (they are for whole planes)
@@ -165,7 +322,8 @@ __device__ __forceinline__ void tile_store(T *__restrict__ dst, const T *tile, i
 }
 
 // ECDF / ESF counts: CTA per plane, row blocks in scan order.
-__global__ void __launch_bounds__(kPlaneThreads) plane_count_kernel(
+template <int SE>
+__global__ void __launch_bounds__(kPlaneThreads, 2) plane_count_kernel(
     PartGeo p, const int32_t *__restrict__ start, const int32_t *__restrict__ vals, int rev_r,
     int rev_c, int32_t *__restrict__ lat) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -180,7 +338,7 @@ __global__ void __launch_bounds__(kPlaneThreads) plane_count_kernel(
     const int64_t rb = rev_r ? p.nrb - 1 - rbi : rbi;
     const int64_t r0 = rb * R;
     const int nr = (int)((r0 + R <= p.H) ? R : p.H - r0);
-    for (int i = threadIdx.x; i < nr * W; i += blockDim.x) tile[i] = 0;
+    tile_zero<int32_t>(tile, nr * W);
     __syncthreads();
     const int64_t b = plane * p.nrb + rb;
     const int32_t q0 = start[b], q1 = start[b + 1];
@@ -197,7 +355,7 @@ __global__ void __launch_bounds__(kPlaneThreads) plane_count_kernel(
         if (v[u] >= 0) atomicAdd(&tile[v[u]], 1);
     }
     __syncthreads();
-    tile_scan<int32_t>(tile, nr, W, rev_r, rev_c, carry, seg);
+    tile_scan_any<int32_t, SE>(tile, nr, W, rev_r, rev_c, carry, seg);
     tile_store<int32_t>(lat + (plane * p.H + r0) * W, tile, (int64_t)nr * W);
     __syncthreads();
   }
@@ -219,9 +377,10 @@ struct KdeTerm {
   double c[FCG_MAX_DIM], a[FCG_MAX_DIM];
 };
 
-__global__ void __launch_bounds__(kPlaneThreads) plane_kde_kernel(
-    KdeTerm t, const int32_t *__restrict__ start, const double *__restrict__ xs,
-    const double *__restrict__ ws, const uint32_t *__restrict__ loc, int rev_r, int rev_c,
+template <int SE>
+__global__ void __launch_bounds__(kKdeThreads, 2) plane_kde_kernel(
+    KdeTerm t, const int32_t *__restrict__ start, const double *__restrict__ rec,
+    const uint32_t *__restrict__ loc, int factored, unsigned negmask, int rev_r, int rev_c,
     double *__restrict__ lat) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int W = (int)t.Mc, H = (int)t.Mr, Rf = (int)t.Rf;
@@ -240,51 +399,63 @@ __global__ void __launch_bounds__(kPlaneThreads) plane_kde_kernel(
   double *plane_out = lat + (int64_t)blockIdx.x * H * W;
   for (int64_t rbi = 0; rbi < t.nrb; ++rbi) {
     const int64_t rb = rev_r ? t.nrb - 1 - rbi : rbi;
-    // cell rows of this block, clipped to [0, H)
     int lo = (int)(rb * Rf - t.sr), hi = lo + Rf;
     const int clo = lo < 0 ? 0 : lo, chi = hi > H ? H : hi;
     if (chi <= clo) continue;
     const int nr = chi - clo;
-    for (int i = threadIdx.x; i < nr * W; i += blockDim.x) tile[i] = 0.0;
+    double *gtile = plane_out + (int64_t)clo * W;  // this block's rows of the lattice
+    tile_zero<double>(tile, nr * W);
     __syncthreads();
     const int64_t b = fplane * t.nrb + rb;
     const int32_t q0 = start[b], q1 = start[b + 1];
-    // batches of KB records per thread: all loads issued before any exp / atomic so the
-    // memory latency overlaps (the fp64 shared atomic is a CAS loop the compiler will not
-    // hoist loads across)
-    constexpr int KB = 4;
+    constexpr int KB = 2;
     for (int32_t qb = q0 + threadIdx.x; qb < q1; qb += KB * blockDim.x) {
       uint32_t l[KB];
-      double wv[KB], s[KB];
+      double psi[KB];  // loads of all KB records issued before the first atomic
 #pragma unroll
       for (int u = 0; u < KB; ++u) {
         const int32_t q = qb + u * (int32_t)blockDim.x;
         const bool ok = q < q1;
         l[u] = ok ? loc[q] : 0xFFFFFFFFu;
-        wv[u] = ok ? ws[q] : 0.0;
-        s[u] = 0.0;
-        for (int k = 0; k < d; ++k) s[u] += ((ok ? xs[(int64_t)q * d + k] : 0.0) - t.c[k]) * t.a[k];
+        const double *r = rec + (int64_t)(ok ? q : q0) * (d + 1);
+        double v;
+        if (factored) {
+          v = r[0];
+          for (int k = 0; k < d; ++k)
+            if ((negmask >> k) & 1) v *= r[1 + k];
+        } else {
+          double sx = 0.0;
+          for (int k = 0; k < d; ++k) sx += (r[k] - t.c[k]) * t.a[k];
+          v = r[d] * exp(sx);
+        }
+        psi[u] = v;
       }
 #pragma unroll
       for (int u = 0; u < KB; ++u) {
         const int cr = (int)(l[u] >> 16) - (int)t.sr - clo;
         const int cc = (int)(l[u] & 0xFFFFu) - (int)t.sc;
         if (l[u] == 0xFFFFFFFFu || cr < 0 || cr >= nr || cc < 0 || cc >= W) continue;
-        atomicAdd(&tile[cr * W + cc], wv[u] * exp(s[u]));
+        atomicAdd(&tile[cr * W + cc], psi[u]);  // fp64 shared atomic (CAS loop on sm_100)
       }
     }
     __syncthreads();
-    tile_scan<double>(tile, nr, W, rev_r, rev_c, carry, seg);
-    tile_store<double>(plane_out + (int64_t)clo * W, tile, (int64_t)nr * W);
+    tile_scan_any<double, SE>(tile, nr, W, rev_r, rev_c, carry, seg);
+    tile_store<double>(gtile, tile, (int64_t)nr * W);
     __syncthreads();
   }
 }
 
-// gather the sorted records the KDE terms stream: x row, weight, in-plane full-space offset
+// gather the sorted records the KDE terms stream: the in-plane full-space offset packed as
+// 16-bit (row, col), and either
+//   factored (f != 0): rec[q] = (A, q_0..q_{d-1}) with A = w e^{sum_k u_k}, q_k = e^{-2 u_k},
+//                      u_k = (x_k - c_k) / h_k, so term psi = A * prod_{k: delta_k=-1} q_k;
+//   raw:               rec[q] = (x_0..x_{d-1}, w) and psi = w e^{sum_k delta_k u_k} per term.
+// The factored form is used only when sum_k max|u_k| <= 600, which keeps every partial
+// product inside e^{+-600} (fp64 overflows past e^709).
 __global__ void kde_materialize_kernel(const double *__restrict__ x, const double *__restrict__ w,
                                        int64_t n, int d, const int32_t *__restrict__ order,
-                                       const double *__restrict__ knots, BinGrid g,
-                                       double *__restrict__ xs, double *__restrict__ ws,
+                                       const double *__restrict__ knots, BinGrid g, PsiParams pp,
+                                       int factored, double *__restrict__ rec,
                                        uint32_t *__restrict__ loc) {
   extern __shared__ double s_knots[];
   __shared__ double s_z0[FCG_MAX_DIM], s_idz[FCG_MAX_DIM];
@@ -294,12 +465,31 @@ __global__ void kde_materialize_kernel(const double *__restrict__ x, const doubl
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
        q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = order[q];
-    for (int k = 0; k < d; ++k) xs[q * d + k] = x[i * d + k];
-    ws[q] = w ? w[i] : 1.0;
-    const int64_t br = knot_count(x[i * d + kr], kb + g.koff[kr], (int)g.m[kr], 0, s_z0[kr], s_idz[kr]);
-    const int64_t bc = knot_count(x[i * d + kc], kb + g.koff[kc], (int)g.m[kc], 0, s_z0[kc], s_idz[kc]);
+    const double wi = w ? w[i] : 1.0;
+    double *r = rec + q * (d + 1);
+    if (factored) {
+      double su = 0.0;
+      for (int k = 0; k < d; ++k) {
+        const double u = (x[i * d + k] - pp.c[k]) * pp.a[k];  // a_k = 1 / h_k
+        su += u;
+        r[1 + k] = exp(-2.0 * u);
+      }
+      r[0] = wi * exp(su);
+    } else {
+      for (int k = 0; k < d; ++k) r[k] = x[i * d + k];
+      r[d] = wi;
+    }
+    const int br = knot_count(x[i * d + kr], kb + g.koff[kr], (int)g.m[kr], 0, s_z0[kr], s_idz[kr]);
+    const int bc = knot_count(x[i * d + kc], kb + g.koff[kc], (int)g.m[kc], 0, s_z0[kc], s_idz[kc]);
     loc[q] = ((uint32_t)br << 16) | (uint32_t)bc;
   }
+}
+
+// rows of segment totals the tile scans need (scalar or vectorised column pass)
+int64_t seg_rows(int threads, int64_t W, int V) {
+  int64_t g1 = threads >= W ? threads / W : 1;
+  int64_t g2 = threads * V >= W ? threads * V / W : 1;
+  return g1 > g2 ? g1 : g2;
 }
 
 int bits_for(int64_t v) {  // smallest b with v < 2^b
@@ -370,7 +560,7 @@ PartPlan plan_ecdf_partition(const BinGrid &g, int64_t n) {
   pl.NP = 1;
   for (int k = 0; k < d - 2; ++k) pl.NP *= g.dims[k];
   if (pl.W > 8192 || pl.NP < 2 * (int64_t)sm_count()) return pl;
-  const int64_t G = kPlaneThreads >= pl.W ? kPlaneThreads / pl.W : 1;
+  const int64_t G = seg_rows(kPlaneThreads, pl.W, 4);
   // tile + carry + segment totals
   int64_t R = (int64_t)(kEcdfTileBytes / 4 - pl.W - G * pl.W) / pl.W;
   if (R < 1) return pl;
@@ -408,14 +598,14 @@ int ecdf_partitioned(const double *x, int64_t n, const double *knots, const BinG
   p.H = pl.H;
   p.ecdf = 1;
   FCG_TRY(partition(x, n, d, knots, g, p, pl.NB, pl.nbits, b, st));
-  const int64_t G = kPlaneThreads >= pl.W ? kPlaneThreads / pl.W : 1;
+  const int64_t G = seg_rows(kPlaneThreads, pl.W, 4);
   const size_t smem = (size_t)(pl.R * pl.W + pl.W + G * pl.W) * sizeof(int32_t);
   {
     FCG_PROF("plane_count", st);
-    FCG_CUDA_TRY(cudaFuncSetAttribute(plane_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-    plane_count_kernel<<<(unsigned)pl.NP, kPlaneThreads, smem, st>>>(p, b.start, b.vals,
-                                                                    rev[d - 2], rev[d - 1], lat);
+    const int se = scan_variant(pl.W, 4);
+    auto kern = se == 4 ? plane_count_kernel<4> : (se == 8 ? plane_count_kernel<8> : plane_count_kernel<0>);
+    FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)pl.NP, kPlaneThreads, smem, st>>>(p, b.start, b.vals, rev[d - 2], rev[d - 1], lat);
     FCG_LAUNCH_CHECK();
   }
   Epi inplace;
@@ -429,7 +619,7 @@ PartPlan plan_kde_partition(int d, const int64_t *m, int64_t n) {
   pl.W = m[d - 1];
   pl.H = m[d - 2];
   if (pl.W + 1 > 65535 || pl.H + 1 > 65535) return pl;  // packed 16-bit (row, col) offsets
-  const int64_t G = kPlaneThreads >= pl.W ? kPlaneThreads / pl.W : 1;
+  const int64_t G = seg_rows(kKdeThreads, pl.W, 2);
   const int64_t Hf = pl.H + 1;
   // fewest full-space row blocks whose tile fits the budget
   int64_t nrb = 1, Rf = Hf;
@@ -458,11 +648,11 @@ PartPlan plan_kde_partition(int d, const int64_t *m, int64_t n) {
 
 int kde_partitioned(const double *x, int64_t n, const double *w, const double *knots,
                     const int64_t *m, int d, const double *h, const double *centre,
-                    const PartPlan &pl, double *out, Workspace &W, bool run, cudaStream_t st) {
+                    double bound_u_sum, double n_scale, double *planes, const PartPlan &pl,
+                    double *out, Workspace &W, bool run, cudaStream_t st) {
   PartBufs b;
   carve_part(W, b, n, pl.NB);
-  double *xs = W.take<double>((size_t)n * d);
-  double *wsorted = W.take<double>(n);
+  double *rec = W.take<double>((size_t)n * (d + 1));
   uint32_t *loc = W.take<uint32_t>(n);
   LatShape s;
   s.d = d;
@@ -497,20 +687,33 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   p.nrb = pl.nrb;
   p.ecdf = 0;
   FCG_TRY(partition(x, n, d, knots, g, p, pl.NB, pl.nbits, b, st));
+  // factored psi records when every partial product stays inside e^{+-600}: needs
+  // sum_k max|u_k| <= 600 with u_k = (x_k - c_k)/h_k; bounded here by the hull of the knots
+  // and the data (the caller's centre is that hull's midrange, fastsum.py:118-129)
+  PsiParams pp{};
+  for (int k = 0; k < d; ++k) {
+    pp.c[k] = centre[k];
+    pp.a[k] = 1.0 / h[k];
+  }
+  int factored = bound_u_sum <= 600.0 ? 1 : 0;
   {
     const size_t smem = g.total_knots <= kSmemKnots ? (size_t)g.total_knots * sizeof(double) : 0;
     FCG_PROF("kde_materialize", st);
-    kde_materialize_kernel<<<grid_for(n, 256, 8), 256, smem, st>>>(x, w, n, d, b.vals, knots, g, xs,
-                                                                  wsorted, loc);
+    kde_materialize_kernel<<<grid_for(n, 256, 8), 256, smem, st>>>(x, w, n, d, b.vals, knots, g, pp,
+                                                                  factored, rec, loc);
     FCG_LAUNCH_CHECK();
   }
   double prod_h = 1.0;
   for (int k = 0; k < d; ++k) prod_h *= h[k];
-  const double scale = 1.0 / (std::ldexp(1.0, d) * (double)n * prod_h);
-  const int64_t G = kPlaneThreads >= pl.W ? kPlaneThreads / pl.W : 1;
+  const double scale = 1.0 / (std::ldexp(1.0, d) * n_scale * prod_h);
+  const int64_t G = seg_rows(kKdeThreads, pl.W, 2);
+  int64_t plane_sz = m[0];
+  for (int k = 2; k < d; ++k) plane_sz *= m[k];
   const size_t smem = (size_t)(pl.R * pl.W + pl.W + G * pl.W) * sizeof(double);
-  FCG_CUDA_TRY(cudaFuncSetAttribute(plane_kde_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
+  const int se = scan_variant(pl.W, 2);
+  auto kde_kern = se == 2 ? plane_kde_kernel<2>
+                          : (se == 4 ? plane_kde_kernel<4> : (se == 8 ? plane_kde_kernel<8> : plane_kde_kernel<0>));
+  FCG_CUDA_TRY(cudaFuncSetAttribute(kde_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int ncodes = 1 << d;
   for (int code = 0; code < ncodes; ++code) {
     KdeTerm t{};
@@ -538,8 +741,11 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
     FCG_TRY(launch_kde_zf(knots, d, m, centre, h, code, zf, st));
     {
       FCG_PROF("plane_kde", st);
-      plane_kde_kernel<<<(unsigned)pl.NP, kPlaneThreads, smem, st>>>(t, b.start, xs, wsorted, loc,
-                                                                    rev[d - 2], rev[d - 1], lat);
+      unsigned negmask = 0;
+      for (int k = 0; k < d; ++k)
+        if (rev[k]) negmask |= 1u << k;
+      kde_kern<<<(unsigned)pl.NP, kKdeThreads, smem, st>>>(
+          t, b.start, rec, loc, factored, negmask, rev[d - 2], rev[d - 1], lat);
       FCG_LAUNCH_CHECK();
     }
     Epi inplace;
@@ -557,6 +763,10 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
     e.accumulate = code > 0;
     e.apply_scale = code == ncodes - 1;
     e.scale = scale;
+    if (planes) {
+      e.plane_out = planes + (int64_t)code * plane_sz;
+      e.plane_idx = rev[1] ? 0 : m[1] - 1;  // carry plane: last (prefix) or first (suffix)
+    }
     FCG_TRY(scan_axis<double>(lat, s, 0, rev[0], e, scratch, st));
   }
   return FCG_OK;

@@ -29,8 +29,12 @@ int ecdf_partitioned(const double *x, int64_t n, const double *knots, const BinG
 
 // Laplacian KDE: full-space binning (dims M_k + 1) shared by all 2^d terms.
 PartPlan plan_kde_partition(int d, const int64_t *m, int64_t n);
+// bound_u_sum: an upper bound of sum_k max_i |x_ik - c_k| / h_k (selects the factored psi
+// records); n_scale: the N of the 1/(2^d N prod h) normalisation (the global N on a slab);
+// planes: optional [2^d][A * B1] capture of each term's slab-boundary S plane (may be null).
 int kde_partitioned(const double *x, int64_t n, const double *w, const double *knots,
                     const int64_t *m, int d, const double *h, const double *centre,
-                    const PartPlan &plan, double *out, Workspace &W, bool run, cudaStream_t st);
+                    double bound_u_sum, double n_scale, double *planes, const PartPlan &plan,
+                    double *out, Workspace &W, bool run, cudaStream_t st);
 
 }  // namespace fcg

@@ -72,6 +72,15 @@ __global__ void __launch_bounds__(256) lines_kernel(T *__restrict__ lat, int64_t
     T *base = lat + a * D * B + b;
     double zo = 1.0;
     if constexpr (EK == EPI_KDE) zo = zprod_other(e, a, b);
+    // slab carry capture: this line lies in the requested axis-1 plane (axis-0 pass, d >= 2)
+    double *pcap = nullptr;
+    int64_t pB1 = 0;
+    if constexpr (EK == EPI_KDE) {
+      if (e.plane_out && e.ax == 0 && e.d >= 2) {
+        pB1 = B / e.dims[1];
+        if (b / pB1 == e.plane_idx) pcap = e.plane_out + (b % pB1);
+      }
+    }
     int64_t jj = j0;
     for (; jj + kUnroll <= j1; jj += kUnroll) {
       T v[kUnroll];
@@ -94,6 +103,7 @@ __global__ void __launch_bounds__(256) lines_kernel(T *__restrict__ lat, int64_t
           if (e.accumulate) r = ov[u] + r;
           if (e.apply_scale) r = r * e.scale;
           static_cast<double *>(e.out)[a * D * B + j * B + b] = r;
+          if (pcap) pcap[j * pB1] = (double)carry;
         } else {
           emit<T, EK>(lat, e, a * D * B + j * B + b, j, zo, carry);
         }
@@ -103,6 +113,8 @@ __global__ void __launch_bounds__(256) lines_kernel(T *__restrict__ lat, int64_t
       const int64_t j = REV ? (D - 1 - jj) : jj;
       carry += base[j * B];
       emit<T, EK>(lat, e, a * D * B + j * B + b, j, zo, carry);
+      if constexpr (EK == EPI_KDE)
+        if (pcap) pcap[j * pB1] = (double)carry;
     }
   }
 }

@@ -1,0 +1,283 @@
+"""Multi-GPU grid ECDF / ESF / Laplacian KDE: slab decomposition along axis 1.
+
+One process per GPU (torch.distributed, NCCL).  Every rank starts with its own shard of the
+points; the output lattice is split along axis 1 into contiguous slabs, one per rank.
+
+1. Routing: each point goes to the rank owning its axis-1 cell (``fcg_axis_owner``), rows are
+   partitioned by owner on the device (``fcg_partition_rows``) and exchanged with one
+   ``all_to_all_single`` per array.
+2. Local pipeline: the rank runs the ordinary single-GPU pipeline on the sub-grid whose axis-1
+   knots are its slab's knots.  Because prefix sums along different axes commute, everything
+   except the axis-1 coupling between slabs is exact locally.
+3. Carry exchange: the slab-boundary plane of every rank (last axis-1 plane for a forward scan,
+   first plane for a reverse one) is all-gathered; rank r adds the sum of the lower ranks'
+   planes (forward) or the higher ranks' planes (reverse), broadcast along axis 1
+   (``fcg_slab_finish``).  Unit-weight counts stay int64 until the final division by the
+   global N, so the result is bit-identical to the single-GPU one.
+4. Laplacian KDE: every term's S = local S + carry plane; since the term enters the output as
+   zfac * S (linear), all 2^d exchanged carry planes are folded in one pass
+   (``fcg_kde_carry_fixup``).  The centre c is the global hull midrange (one all-reduce), so
+   all ranks use the same exponential frame.  A point whose delta=+1 bin is a slab's first bin
+   is also needed by the slab below (its delta_1 = -1 cell), so it is sent to both.
+
+Output stays sharded: rank r returns values for axis-1 cells [lo_r, hi_r) (lexicographic
+within the slab).  ``engine`` exists so the CPU tests can drive the same decomposition with
+the oracle; the product path always uses the device engine.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .core import (
+    EXP_OVERFLOW_GUARD,
+    GRID_ALIGNED,
+    Bandwidth,
+    DeltaVector,
+    EvalResult,
+    OverflowGuardError,
+    ParameterError,
+    RectilinearGrid,
+    Sample,
+    as_sample,
+)
+
+
+def slab_bounds(m1: int, world: int) -> list[int]:
+    """Contiguous, balanced split of m1 axis-1 cells over `world` ranks (uneven allowed)."""
+    if m1 < world:
+        raise ParameterError(f"axis 1 has {m1} cells, fewer than {world} ranks")
+    base, extra = divmod(m1, world)
+    out = [0]
+    for r in range(world):
+        out.append(out[-1] + base + (1 if r < extra else 0))
+    return out
+
+
+class DeviceEngine:
+    """Local steps on the current CUDA device through the C-ABI."""
+
+    def tensor(self, a):
+        return _lib.to_device_f64(a)
+
+    def axis_owner(self, x, knots_axis, le, shift, bounds):
+        import torch
+
+        n, d = x.shape
+        owner = torch.empty(n, dtype=torch.int32, device=x.device)
+        kn = _lib.to_device_f64(knots_axis)
+        _lib.check(_lib.load_library().fcg_axis_owner(
+            _lib.ptr(x), n, d, 1, _lib.ptr(kn), int(kn.numel()), int(le), int(shift),
+            _lib.i64_array(bounds), len(bounds) - 1, _lib.ptr(owner), _lib.stream_handle()),
+            "fcg_axis_owner")
+        return owner
+
+    def partition(self, x, w, owner, G):
+        import torch
+
+        n, d = x.shape
+        xo = torch.empty_like(x)
+        wo = None if w is None else torch.empty_like(w)
+        counts = (C.c_int64 * G)()
+        _lib.call_ws("fcg_partition_rows", _lib.ptr(x), n, d, _lib.ptr(w), _lib.ptr(owner), G,
+                     _lib.ptr(xo), _lib.ptr(wo), counts)
+        return xo, wo, [int(c) for c in counts]
+
+    def local_ecdf(self, x, w, grid, delta, survival):
+        """Unscaled slab-local values: int64 counts (w None) or fp64 sums."""
+        from .fastsum import _ecdf_grid_device
+
+        s = Sample(x, w if w is not None else None, None, w is None)
+        return _ecdf_grid_device(s, grid, delta, survival, False, counts=w is None)
+
+    def slab_finish(self, local, carry, A, J, B, div):
+        import torch
+
+        out = torch.empty(A * J * B, dtype=torch.float64, device=local.device)
+        kind = 0 if local.dtype == torch.int64 else 1
+        _lib.check(_lib.load_library().fcg_slab_finish(
+            _lib.ptr(local), kind, _lib.ptr(carry), A, J, B, float(div), _lib.ptr(out),
+            _lib.stream_handle()), "fcg_slab_finish")
+        return out
+
+    def minmax(self, x):
+        return _lib.minmax(x)
+
+    def local_kde(self, x, w, grid, h, centre, n_scale, u_bound=-1.0):
+        """Slab-local KDE and the 2^d slab-boundary planes of S."""
+        import torch
+
+        n, d = x.shape
+        m = grid.shape
+        plane = int(np.prod(m)) // m[1]
+        out = torch.empty(int(np.prod(m)), dtype=torch.float64, device=x.device)
+        planes = torch.zeros((1 << d) * plane, dtype=torch.float64, device=x.device)
+        kn = _lib.device_knots(grid)
+        _lib.call_ws("fcg_kde_grid_laplacian_ex", _lib.ptr(x), n, d, _lib.ptr(w), _lib.ptr(kn),
+                     _lib.i64_array(m), _lib.f64_array(h), _lib.f64_array(centre),
+                     float(n_scale), float(u_bound), _lib.ptr(planes), _lib.ptr(out))
+        return out, planes
+
+    def kde_fixup(self, out, grid, h, centre, carries, n_scale):
+        kn = _lib.device_knots(grid)
+        _lib.call_ws("fcg_kde_carry_fixup", _lib.ptr(out), grid.dim, _lib.i64_array(grid.shape),
+                     _lib.ptr(kn), _lib.f64_array(h), _lib.f64_array(centre), _lib.ptr(carries),
+                     float(n_scale))
+        return out
+
+
+def _dist():
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        raise RuntimeError("torch.distributed is not initialised")
+    return dist
+
+
+def _exchange_rows(x, w, owner, world, engine, group):
+    """Partition local rows by owner and all-to-all them; returns the received (x, w)."""
+    import torch
+
+    dist = _dist()
+    d = x.shape[1]
+    xs, ws, counts = engine.partition(x, w, owner, world)
+    send = torch.tensor(counts, dtype=torch.int64, device=x.device)
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv, send, group=group)
+    rc = [int(v) for v in recv.tolist()]
+    live = sum(counts)
+    xr = torch.empty((sum(rc), d), dtype=torch.float64, device=x.device)
+    dist.all_to_all_single(xr.view(-1), xs[:live].reshape(-1).contiguous(),
+                           output_split_sizes=[c * d for c in rc],
+                           input_split_sizes=[c * d for c in counts], group=group)
+    wr = None
+    if w is not None:
+        wr = torch.empty(sum(rc), dtype=torch.float64, device=x.device)
+        dist.all_to_all_single(wr, ws[:live].contiguous(), output_split_sizes=rc,
+                               input_split_sizes=counts, group=group)
+    return xr, wr
+
+
+def _sub_grid(grid, lo, hi):
+    knots = [np.asarray(z, dtype=np.float64) for z in grid.knots]
+    knots[1] = knots[1][lo:hi]
+    return RectilinearGrid.from_knots(knots)
+
+
+def _gather_planes(plane, world, group):
+    import torch
+
+    dist = _dist()
+    bufs = [torch.empty_like(plane) for _ in range(world)]
+    dist.all_gather(bufs, plane.contiguous(), group=group)
+    return bufs
+
+
+def ecdf_fastsum_slab(sample: Sample, grid: RectilinearGrid, delta: DeltaVector | None = None,
+                      scaled: bool = True, survival: bool = False, group=None,
+                      engine=None) -> EvalResult:
+    """Distributed ecdf_fastsum (survival=False) / esf_fastsum (survival=True); each rank passes
+    its shard of the points and receives its axis-1 slab of the grid values."""
+    import torch
+
+    sample = as_sample(sample)
+    dist = _dist()
+    eng = engine or DeviceEngine()
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    d = sample.dim
+    if d < 2 or grid.dim != d:
+        raise ParameterError("slab decomposition needs d >= 2 and a matching grid")
+    delta = delta or DeltaVector.ones(d)
+    m = grid.shape
+    bounds = slab_bounds(m[1], world)
+    lo, hi = bounds[rank], bounds[rank + 1]
+    x = eng.tensor(sample.points)
+    w = None if sample.unit_weights else eng.tensor(sample.weights)
+    le = 0 if survival else int(delta.signs[1] < 0)
+    shift = 1 if survival else 0
+    owner = eng.axis_owner(x, grid.knots[1], le, shift, bounds)
+    xr, wr = _exchange_rows(x, w, owner, world, eng, group)
+    n_total = torch.tensor([sample.count], dtype=torch.int64, device=x.device)
+    dist.all_reduce(n_total, group=group)
+    sub = _sub_grid(grid, lo, hi)
+    local = eng.local_ecdf(xr, wr, sub, delta, survival)
+    A, J = m[0], hi - lo
+    B = int(np.prod(m[2:])) if d > 2 else 1
+    cube = local.view(A, J, B)
+    plane = (cube[:, 0, :] if survival else cube[:, J - 1, :]).contiguous()
+    planes = _gather_planes(plane, world, group)
+    others = planes[rank + 1:] if survival else planes[:rank]
+    carry = torch.zeros_like(plane)
+    for p in others:
+        carry += p
+    out = eng.slab_finish(local, carry, A, J, B, float(n_total.item()) if scaled else 0.0)
+    return EvalResult(out, GRID_ALIGNED, {"method": "fastsum-slab", "scaled": scaled,
+                                          "slab": (lo, hi), "world": world})
+
+
+def kde_fastsum_slab(sample: Sample, grid: RectilinearGrid, kernel, bandwidth: Bandwidth,
+                     group=None, engine=None) -> EvalResult:
+    """Distributed Laplacian kde_fastsum; each rank passes its shard of the points (and their
+    weights) and receives its axis-1 slab of the density grid."""
+    import torch
+
+    sample = as_sample(sample)
+    dist = _dist()
+    eng = engine or DeviceEngine()
+    if kernel.family != "laplacian":
+        raise ParameterError("the slab-decomposed KDE supports the laplacian kernel")
+    if not bandwidth.is_diagonal:
+        raise ParameterError("kde_fastsum requires a diagonal bandwidth")
+    h = np.ascontiguousarray(bandwidth.diagonal, dtype=np.float64)
+    d = sample.dim
+    if d < 2 or grid.dim != d or h.size != d:
+        raise ParameterError("slab decomposition needs d >= 2 and matching grid / bandwidth")
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    m = grid.shape
+    bounds = slab_bounds(m[1], world)
+    lo, hi = bounds[rank], bounds[rank + 1]
+    x = eng.tensor(sample.points)
+    w = None if sample.unit_weights else eng.tensor(sample.weights)
+    # global hull midrange of data and grid + overflow guard (fastsum.py:114-129)
+    dmin, dmax = eng.minmax(x)
+    mm = torch.tensor(np.concatenate([-dmin, dmax]), dtype=torch.float64, device=x.device)
+    dist.all_reduce(mm, op=dist.ReduceOp.MAX, group=group)
+    mm = mm.cpu().numpy()
+    lo_h = np.minimum(-mm[:d], np.array([float(np.asarray(z)[0]) for z in grid.knots]))
+    hi_h = np.maximum(mm[d:], np.array([float(np.asarray(z)[-1]) for z in grid.knots]))
+    span = hi_h - lo_h
+    for k in range(d):
+        if span[k] / h[k] > EXP_OVERFLOW_GUARD:
+            raise OverflowGuardError(
+                f"dimension {k}: span/bandwidth = {span[k] / h[k]:.1f} exceeds "
+                f"{EXP_OVERFLOW_GUARD:.0f}; enlarge the bandwidth or rescale")
+    centre = 0.5 * (lo_h + hi_h)
+    # route by the delta=+1 cell and, for the delta_1 = -1 terms, by the cell one bin lower
+    own_a = eng.axis_owner(x, grid.knots[1], 0, 0, bounds)
+    own_b = eng.axis_owner(x, grid.knots[1], 0, 1, bounds)
+    own_b = torch.where(own_b == own_a, torch.full_like(own_b, -1), own_b)
+    xa, wa = _exchange_rows(x, w, own_a, world, eng, group)
+    xb, wb = _exchange_rows(x, w, own_b, world, eng, group)
+    xr = torch.cat([xa, xb])
+    wr = None if w is None else torch.cat([wa, wb])
+    n_total = torch.tensor([sample.count], dtype=torch.int64, device=x.device)
+    dist.all_reduce(n_total, group=group)
+    N = float(n_total.item())
+    sub = _sub_grid(grid, lo, hi)
+    out, planes = eng.local_kde(xr, wr, sub, h, centre, N, float(np.sum(span / (2.0 * h))) * 1.000001)
+    ncodes = 1 << d
+    gathered = _gather_planes(planes, world, group)
+    plane_sz = planes.numel() // ncodes
+    carries = torch.zeros_like(planes)
+    for code in range(ncodes):
+        reverse = bool((code >> 1) & 1)  # delta_1 = -1: suffix along axis 1
+        sel = gathered[rank + 1:] if reverse else gathered[:rank]
+        seg = slice(code * plane_sz, (code + 1) * plane_sz)
+        for g in sel:
+            carries[seg] += g[seg]
+    out = eng.kde_fixup(out, sub, h, centre, carries, N)
+    return EvalResult(out, GRID_ALIGNED, {"method": "fastsum-slab", "kernel": str(kernel),
+                                          "slab": (lo, hi), "world": world})

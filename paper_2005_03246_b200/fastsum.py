@@ -110,9 +110,10 @@ def esf_fastsum(sample: Sample, grid: RectilinearGrid, scaled: bool = True) -> E
         "runtime_seconds": time.perf_counter() - t0})
 
 
-def _exp_guard_and_center(sample: Sample, grid: RectilinearGrid, h: np.ndarray) -> np.ndarray:
+def _exp_guard_and_center(sample: Sample, grid: RectilinearGrid, h: np.ndarray):
     """Hull midrange of data and grid; OverflowGuardError past span/h > 600
-    (fastsum.py:114-129)."""
+    (fastsum.py:114-129).  Also returns sum_k span_k / (2 h_k), the bound on the centred
+    exponents that lets the kernels factor each term's weights."""
     dmin, dmax = _lib.minmax(sample.points)
     lo = np.minimum(dmin, np.array([float(np.asarray(z)[0]) for z in grid.knots]))
     hi = np.maximum(dmax, np.array([float(np.asarray(z)[-1]) for z in grid.knots]))
@@ -122,21 +123,21 @@ def _exp_guard_and_center(sample: Sample, grid: RectilinearGrid, h: np.ndarray) 
             raise OverflowGuardError(
                 f"dimension {k}: span/bandwidth = {span[k] / h[k]:.1f} exceeds "
                 f"{EXP_OVERFLOW_GUARD:.0f}; enlarge the bandwidth or rescale")
-    return 0.5 * (lo + hi)
+    return 0.5 * (lo + hi), float(np.sum(span / (2.0 * h)))
 
 
 def _kde_laplacian_grid(sample: Sample, grid: RectilinearGrid, h: np.ndarray):
     import torch
 
-    c = _exp_guard_and_center(sample, grid, h)
+    c, ubound = _exp_guard_and_center(sample, grid, h)
     x = _lib.to_device_f64(sample.points)
     n, d = x.shape
     w = None if sample.unit_weights else _lib.to_device_f64(sample.weights)
     kn = _lib.device_knots(grid)
     out = torch.empty(grid.size, dtype=torch.float64, device=x.device)
-    _lib.call_ws("fcg_kde_grid_laplacian", _lib.ptr(x), n, d, _lib.ptr(w), _lib.ptr(kn),
-                 _lib.i64_array(grid.shape), _lib.f64_array(h), _lib.f64_array(c),
-                 _lib.ptr(out))
+    _lib.call_ws("fcg_kde_grid_laplacian_ex", _lib.ptr(x), n, d, _lib.ptr(w), _lib.ptr(kn),
+                 _lib.i64_array(grid.shape), _lib.f64_array(h), _lib.f64_array(c), float(n),
+                 ubound * 1.000001, None, _lib.ptr(out))
     return out
 
 
