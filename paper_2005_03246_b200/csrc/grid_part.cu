@@ -388,7 +388,8 @@ __global__ void __launch_bounds__(kKdeThreads, 2) plane_kde_kernel(
   double *carry = tile + (size_t)Rf * W;
   double *seg = carry + W;
   const int d = t.d;
-  int64_t rem = blockIdx.x, fplane = 0, mul = 1;
+  const int64_t cplane = blockIdx.x;
+  int64_t rem = cplane, fplane = 0, mul = 1;
   for (int k = d - 3; k >= 0; --k) {
     const int64_t i = rem % t.lead_m[k];
     rem /= t.lead_m[k];
@@ -396,7 +397,7 @@ __global__ void __launch_bounds__(kKdeThreads, 2) plane_kde_kernel(
     mul *= t.lead_full[k];
   }
   for (int c = threadIdx.x; c < W; c += blockDim.x) carry[c] = 0.0;
-  double *plane_out = lat + (int64_t)blockIdx.x * H * W;
+  double *plane_out = lat + cplane * H * W;
   for (int64_t rbi = 0; rbi < t.nrb; ++rbi) {
     const int64_t rb = rev_r ? t.nrb - 1 - rbi : rbi;
     int lo = (int)(rb * Rf - t.sr), hi = lo + Rf;
@@ -483,6 +484,103 @@ __global__ void kde_materialize_kernel(const double *__restrict__ x, const doubl
     const int bc = knot_count(x[i * d + kc], kb + g.koff[kc], (int)g.m[kc], 0, s_z0[kc], s_idz[kc]);
     loc[q] = ((uint32_t)br << 16) | (uint32_t)bc;
   }
+}
+
+// Final axis-0 pass for a group of KDE terms sharing (delta_0, delta_1): each term's lattice is
+// scanned along axis 0 (same direction for the whole group) and
+//   out (+)= sum_t zfac_t(i) * S_t(i)      (x scale after the last group)
+// so the accumulator is read-modify-written once per group instead of once per term
+// (fastsum.py:162-168, summed over terms in group order).
+constexpr int kMaxGroup = 8;
+struct MultiFinal {
+  int nt, d;
+  const double *lat[kMaxGroup];
+  const double *zf[kMaxGroup];
+  double *plane[kMaxGroup];   // slab carry capture per term (or null)
+  int64_t zoff[FCG_MAX_DIM];
+  int64_t dims[FCG_MAX_DIM];
+  int64_t plane_idx;          // axis-1 index captured (-1: none)
+  int accumulate, apply_scale;
+  double scale;
+  double *out;
+};
+
+template <int NT, bool REV>
+__global__ void __launch_bounds__(256) kde_final_multi(MultiFinal f) {
+  const int64_t D0 = f.dims[0];
+  int64_t B = 1;
+  for (int k = 1; k < f.d; ++k) B *= f.dims[k];
+  const int64_t B1 = B / f.dims[1];
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < B;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    double zo[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) zo[t] = 1.0;
+    {
+      int64_t rem = b;
+      for (int k = f.d - 1; k >= 1; --k) {
+        const int64_t i = rem % f.dims[k];
+        rem /= f.dims[k];
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+          if (t < f.nt) zo[t] *= f.zf[t][f.zoff[k] + i];
+      }
+    }
+    const int64_t cap = (f.plane_idx >= 0 && b / B1 == f.plane_idx) ? b % B1 : -1;
+    double carry[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) carry[t] = 0.0;
+    constexpr int U = 4;
+    for (int64_t jj0 = 0; jj0 < D0; jj0 += U) {
+      double v[U][NT], o[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t jj = jj0 + u;
+        const int64_t j = REV ? D0 - 1 - jj : jj;
+        const bool ok = jj < D0;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) v[u][t] = (ok && t < f.nt) ? f.lat[t][j * B + b] : 0.0;
+        o[u] = (ok && f.accumulate) ? f.out[j * B + b] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t jj = jj0 + u;
+        if (jj >= D0) break;
+        const int64_t j = REV ? D0 - 1 - jj : jj;
+        double val = 0.0;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          if (t < f.nt) {
+            carry[t] += v[u][t];
+            val += (zo[t] * f.zf[t][f.zoff[0] + j]) * carry[t];
+            if (cap >= 0) f.plane[t][j * B1 + cap] = carry[t];
+          }
+        }
+        double r = o[u] + val;
+        if (f.apply_scale) r = r * f.scale;
+        f.out[j * B + b] = r;
+      }
+    }
+  }
+}
+
+int launch_final_multi(const MultiFinal &f, bool rev, cudaStream_t st) {
+  int64_t B = 1;
+  for (int k = 1; k < f.d; ++k) B *= f.dims[k];
+  const int grid = grid_for(B, 256, 8);
+  FCG_PROF("kde_final_group", st);
+if (f.nt <= 2) {
+    if (rev) kde_final_multi<2, true><<<grid, 256, 0, st>>>(f);
+    else kde_final_multi<2, false><<<grid, 256, 0, st>>>(f);
+  } else if (f.nt <= 4) {
+    if (rev) kde_final_multi<4, true><<<grid, 256, 0, st>>>(f);
+    else kde_final_multi<4, false><<<grid, 256, 0, st>>>(f);
+  } else {
+    if (rev) kde_final_multi<8, true><<<grid, 256, 0, st>>>(f);
+    else kde_final_multi<8, false><<<grid, 256, 0, st>>>(f);
+  }
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
 }
 
 // rows of segment totals the tile scans need (scalar or vectorised column pass)
@@ -605,11 +703,13 @@ int ecdf_partitioned(const double *x, int64_t n, const double *knots, const BinG
     const int se = scan_variant(pl.W, 4);
     auto kern = se == 4 ? plane_count_kernel<4> : (se == 8 ? plane_count_kernel<8> : plane_count_kernel<0>);
     FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)pl.NP, kPlaneThreads, smem, st>>>(p, b.start, b.vals, rev[d - 2], rev[d - 1], lat);
+    kern<<<(unsigned)pl.NP, kPlaneThreads, smem, st>>>(p, b.start, b.vals, rev[d - 2], rev[d - 1],
+                                                      lat);
     FCG_LAUNCH_CHECK();
   }
   Epi inplace;
-  for (int ax = d - 3; ax >= 1; --ax) FCG_TRY(scan_axis<int32_t>(lat, s, ax, rev[ax], inplace, scratch, st));
+  for (int ax = d - 3; ax >= 1; --ax)
+    FCG_TRY(scan_axis<int32_t>(lat, s, ax, rev[ax], inplace, scratch, st));
   return scan_axis<int32_t>(lat, s, 0, rev[0], epi, scratch, st);
 }
 
@@ -661,9 +761,12 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
     s.dims[k] = m[k];
     total_knots += m[k];
   }
-  double *lat = W.take<double>(s.size());
+  // terms are processed in groups sharing (delta_0, delta_1); one lattice + zf table per member
+  const int ntg = 1 << (d - 2);
+  const int nbatch = ntg < kMaxGroup ? ntg : kMaxGroup;
+  double *lats = W.take<double>((size_t)s.size() * nbatch);
   double *scratch = W.take<double>(scan_scratch_bound());
-  double *zf = W.take<double>(total_knots);
+  double *zfs = W.take<double>((size_t)total_knots * nbatch);
   if (!run) return FCG_OK;
 
   // one delta=+1 binning in the full (M+1)^d space serves every term (fastsum.py:146-149)
@@ -714,60 +817,76 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   auto kde_kern = se == 2 ? plane_kde_kernel<2>
                           : (se == 4 ? plane_kde_kernel<4> : (se == 8 ? plane_kde_kernel<8> : plane_kde_kernel<0>));
   FCG_CUDA_TRY(cudaFuncSetAttribute(kde_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int ncodes = 1 << d;
-  for (int code = 0; code < ncodes; ++code) {
-    KdeTerm t{};
-    t.d = d;
-    bool rev[FCG_MAX_DIM];
-    int64_t sh[FCG_MAX_DIM];
-    for (int k = 0; k < d; ++k) {
-      const double sgn = ((code >> k) & 1) ? -1.0 : 1.0;
-      rev[k] = sgn < 0;
-      sh[k] = sgn < 0 ? 1 : 0;
-      t.c[k] = centre[k];
-      t.a[k] = sgn / h[k];
-    }
-    t.Mr = m[d - 2];
-    t.Mc = m[d - 1];
-    t.sr = sh[d - 2];
-    t.sc = sh[d - 1];
-    t.Rf = pl.R;
-    t.nrb = pl.nrb;
-    for (int k = 0; k < d - 2; ++k) {
-      t.lead_m[k] = m[k];
-      t.lead_s[k] = sh[k];
-      t.lead_full[k] = m[k] + 1;
-    }
-    FCG_TRY(launch_kde_zf(knots, d, m, centre, h, code, zf, st));
-    {
-      FCG_PROF("plane_kde", st);
-      unsigned negmask = 0;
-      for (int k = 0; k < d; ++k)
-        if (rev[k]) negmask |= 1u << k;
-      kde_kern<<<(unsigned)pl.NP, kKdeThreads, smem, st>>>(
-          t, b.start, rec, loc, factored, negmask, rev[d - 2], rev[d - 1], lat);
-      FCG_LAUNCH_CHECK();
-    }
-    Epi inplace;
-    for (int ax = d - 3; ax >= 1; --ax)
-      FCG_TRY(scan_axis<double>(lat, s, ax, rev[ax], inplace, scratch, st));
-    Epi e;
-    e.kind = EPI_KDE;
-    e.out = out;
-    e.zf = zf;
+  const int64_t L = s.size();
+  int64_t zoff[FCG_MAX_DIM];
+  {
     int64_t off = 0;
     for (int k = 0; k < d; ++k) {
-      e.zoff[k] = off;
+      zoff[k] = off;
       off += m[k];
     }
-    e.accumulate = code > 0;
-    e.apply_scale = code == ncodes - 1;
-    e.scale = scale;
-    if (planes) {
-      e.plane_out = planes + (int64_t)code * plane_sz;
-      e.plane_idx = rev[1] ? 0 : m[1] - 1;  // carry plane: last (prefix) or first (suffix)
+  }
+  for (int grp = 0; grp < 4; ++grp) {
+    for (int b0 = 0; b0 < ntg; b0 += nbatch) {
+      const int nt = (ntg - b0) < nbatch ? (ntg - b0) : nbatch;
+      MultiFinal f{};
+      f.nt = nt;
+      f.d = d;
+      for (int k = 0; k < d; ++k) {
+        f.zoff[k] = zoff[k];
+        f.dims[k] = m[k];
+      }
+      const bool rev0 = grp & 1, rev1 = (grp >> 1) & 1;
+      f.plane_idx = planes ? (rev1 ? 0 : m[1] - 1) : -1;
+      for (int tt = 0; tt < nt; ++tt) {
+        const int code = grp | ((b0 + tt) << 2);
+        double *lat = lats + (size_t)tt * L;
+        double *zf = zfs + (size_t)tt * total_knots;
+        KdeTerm t{};
+        t.d = d;
+        bool rev[FCG_MAX_DIM];
+        int64_t sh[FCG_MAX_DIM];
+        for (int k = 0; k < d; ++k) {
+          const double sgn = ((code >> k) & 1) ? -1.0 : 1.0;
+          rev[k] = sgn < 0;
+          sh[k] = sgn < 0 ? 1 : 0;
+          t.c[k] = centre[k];
+          t.a[k] = sgn / h[k];
+        }
+        t.Mr = m[d - 2];
+        t.Mc = m[d - 1];
+        t.sr = sh[d - 2];
+        t.sc = sh[d - 1];
+        t.Rf = pl.R;
+        t.nrb = pl.nrb;
+        for (int k = 0; k < d - 2; ++k) {
+          t.lead_m[k] = m[k];
+          t.lead_s[k] = sh[k];
+          t.lead_full[k] = m[k] + 1;
+        }
+        FCG_TRY(launch_kde_zf(knots, d, m, centre, h, code, zf, st));
+        {
+          FCG_PROF("plane_kde", st);
+          unsigned negmask = 0;
+          for (int k = 0; k < d; ++k)
+            if (rev[k]) negmask |= 1u << k;
+          kde_kern<<<(unsigned)pl.NP, kKdeThreads, smem, st>>>(
+              t, b.start, rec, loc, factored, negmask, rev[d - 2], rev[d - 1], lat);
+          FCG_LAUNCH_CHECK();
+        }
+        Epi inplace;
+        for (int ax = d - 3; ax >= 1; --ax)
+          FCG_TRY(scan_axis<double>(lat, s, ax, rev[ax], inplace, scratch, st));
+        f.lat[tt] = lat;
+        f.zf[tt] = zf;
+        f.plane[tt] = planes ? planes + (int64_t)code * plane_sz : nullptr;
+      }
+      f.accumulate = (grp > 0 || b0 > 0) ? 1 : 0;
+      f.apply_scale = (grp == 3 && b0 + nt >= ntg) ? 1 : 0;
+      f.scale = scale;
+      f.out = out;
+      FCG_TRY(launch_final_multi(f, rev0, st));
     }
-    FCG_TRY(scan_axis<double>(lat, s, 0, rev[0], e, scratch, st));
   }
   return FCG_OK;
 }
