@@ -123,26 +123,56 @@ def grid_ecdf_bytes(n, d, m, unit=True):
     L = int(np.prod(m))  # dead layers elided: lattice = output extents
     e = 4 if unit else 8
     return {
+        # atomic path (sparse lattices)
         "lattice_zero": e * L,
         "bin_scatter_count" if unit else "bin_scatter_w": 8 * n * d + (0 if unit else 8 * n) + 2 * e * n,
         "scan_rows": 2 * e * L,
         "scan_lines": 2 * e * L,
         "scan_lines_final": e * L + 8 * L,
+        # plane-partitioned path: bucket keys + payloads (u32 each), one 8-bit radix pass each
+        "part_bin": 8 * n * d + 8 * n,
+        "radix_hist": 4 * n,
+        "radix_scatter": 16 * n,
+        "plane_count": 4 * n + e * L,
     }
 
 
 def grid_kde_bytes(n, d, m, unit_w):
     L = int(np.prod(m))
+    terms = 1 << d
+    group = 1 << (d - 2) if d >= 3 else 1
     return {
         "lattice_zero": 8 * L,
         "bin_scatter_psi": 8 * n * d + (0 if unit_w else 8 * n) + 16 * n,
         "scan_rows": 16 * L,
         "scan_lines": 16 * L,
         # first term only writes the accumulator; the other 2^d - 1 read and write it
-        "scan_lines_final": 8 * L + (8 * L + 16 * L * ((1 << d) - 1)) // (1 << d),
+        "scan_lines_final": 8 * L + (8 * L + 16 * L * (terms - 1)) // terms,
         "kde_zfac": 16 * int(np.sum(m)),
         "minmax": 8 * n * d,
+        "part_bin": 8 * n * d + 8 * n,
+        "radix_hist": 4 * n,
+        "radix_scatter": 16 * n,
+        # sorted records: (d+1) doubles + packed offset per point; reads x, w, order
+        "kde_materialize": 8 * n * d + 8 * n + 4 * n + 8 * n * (d + 1) + 4 * n,
+        # one term: stream the sorted records, write the plane-scanned lattice once
+        "plane_kde": (8 * (d + 1) + 4) * n + 8 * L,
+        # one group of 2^(d-2) terms: read each term's lattice, accumulator RMW once
+        # (the first group only writes it)
+        "kde_final_group": group * 8 * L + (8 * L + 16 * L * 3) // 4,
     }
+
+
+def traffic_lookup(workload, kernel):
+    """DRAM bytes per launch of `kernel` from a committed ncu --set full capture
+    (profiles/traffic.json, written from dram__bytes_read.sum + dram__bytes_write.sum)."""
+    p = ROOT / "profiles" / "traffic.json"
+    if not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text()).get(workload, {}).get(kernel)
+    except ValueError:
+        return None
 
 
 class GridWorkload:
@@ -407,9 +437,13 @@ class PointsWorkload:
         else:
             # level-2 solvers: per source (id + 2 positions + 2 psi) and per query (threshold
             # pair + list entry + 2-channel output read-modify-write)
-            b.update({"pts_level2_chunk": (4 + 8 + 16) * n + (8 + 4 + 32) * n,
-                      "pts_level2_block": (4 + 8 + 16) * n + (8 + 4 + 32) * n,
-                      "pts_psi": (16 + 8 + 8 + 16) * n, "pts_kde_accum": (8 + 16 + 32) * n})
+            # group-ordered self dominance, per launch and per point: slot + rank positions,
+            # 2-channel psi, the z factor, and two read-modify-writes of the 2-channel
+            # accumulator (slot-order pass, rank-order pass)
+            b.update({"pts_level2_chunk": (4 + 4 + 16 + 8 + 2 * 32) * n,
+                      "pts_level2_block": (4 + 4 + 16 + 8 + 2 * 32) * n,
+                      "pts_group_gather": (4 + 8 + 16 + 16) * n + (4 + 4 + 16 + 16 + 4) * n,
+                      "pts_psi": (16 + 16 + 16 + 8) * n})
         return b
 
     def cpu_sample(self, threads):
@@ -536,7 +570,8 @@ def main():
         avg_s = ms / cnt / 1e3
         ach = (nbytes / avg_s / 1e9) if nbytes else None
         roof = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": (ach / peak) if ach else None, "traffic": None,
+                "frac": (ach / peak) if ach else None,
+                "traffic": traffic_lookup(w.name, name),
                 "bytes_per_launch": nbytes, "avg_launch_ms": avg_s * 1e3,
                 "share_of_step": ms / ms_total, "peak_source": peak_src}
     breakdown = {k: {"launches": c, "ms_total": round(ms, 4),

@@ -32,7 +32,7 @@ constexpr int S = 1 << LS;    // level-1 block / chunk size
 constexpr int SUBL = 6;
 constexpr int SUB = 1 << SUBL;  // level-2 sub-block size
 constexpr int NSUB = S / SUB;   // 64
-constexpr int kSolverThreads = 512;
+constexpr int kSolverThreads = 1024;
 constexpr int64_t kMaxDominanceN = int64_t(1) << 26;  // coarse grid (n/S)^2 must fit in HBM
 
 // ------------------------------------------------------------------------------------------
@@ -166,17 +166,40 @@ __global__ void query_keys(Dom2 D, int32_t *kc, int32_t *kb) {
   }
 }
 
+// Query bucketing with warp-aggregated atomics: sorted or clustered keys would otherwise
+// serialise thousands of threads on one counter.
+__device__ __forceinline__ unsigned lane_lt_mask() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
 __global__ void bucket_count(const int32_t *__restrict__ key, int64_t n, int32_t *cnt) {
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
-       t += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(&cnt[key[t]], 1);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t t = base + threadIdx.x;
+    const bool ok = t < n;
+    const int k = ok ? key[t] : -1 - (int)(threadIdx.x & 31);
+    const unsigned peers = __match_any_sync(0xffffffffu, k);
+    if (ok && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&cnt[k], __popc(peers));
+  }
 }
 
 __global__ void bucket_fill(const int32_t *__restrict__ key, int64_t n, int32_t *cursor,
                             int32_t *list) {
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
-       t += (int64_t)gridDim.x * blockDim.x)
-    list[atomicAdd(&cursor[key[t]], 1)] = (int32_t)t;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t t = base + threadIdx.x;
+    const bool ok = t < n;
+    const int k = ok ? key[t] : -1 - lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, k);
+    const int leader = __ffs(peers) - 1;
+    int pos = 0;
+    if (ok && lane == leader) pos = atomicAdd(&cursor[k], __popc(peers));
+    pos = __shfl_sync(0xffffffffu, pos, leader);
+    if (ok) list[pos + __popc(peers & lane_lt_mask())] = (int32_t)t;
+  }
 }
 
 // Level-2 solver.  CHUNK: CTA per flipped chunk c, sources of that chunk; slot X = local p1f,
@@ -209,24 +232,48 @@ __global__ void __launch_bounds__(kSolverThreads) level2_solver(Dom2 D) {
     for (int ch = 0; ch < NCH; ++ch) s_psi[ch * S + i] = 0.0;
   }
   __syncthreads();
-  for (int64_t k = threadIdx.x; k < Sg; k += blockDim.x) {
-    const int32_t src = grp[k];
-    const int y = frank ? (int)(Sg - 1 - k) : (int)k;
-    int x = slotpos[src] - (int32_t)lo;
-    if (fslot) x = S - 1 - x;
-    s_yofx[x] = (int16_t)y;
-    s_xofy[y] = (int16_t)x;
-    s_key[y] = flipp(rankpos[src], frank, D.npad);
+  // gather the group's sources: batches of KG per thread with every global load of a batch
+  // issued before the shared-memory stores (the gathers are random, latency-bound)
+  constexpr int KG = 4;
+  for (int64_t k0 = threadIdx.x; k0 < Sg; k0 += KG * blockDim.x) {
+    int32_t src[KG], sp[KG], rp[KG];
+    double ps[KG][NCH];
 #pragma unroll
-    for (int ch = 0; ch < NCH; ++ch) s_psi[ch * S + x] = D.psi[ch * D.n + src];
+    for (int u = 0; u < KG; ++u) {
+      const int64_t k = k0 + u * (int64_t)blockDim.x;
+      src[u] = k < Sg ? grp[k] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < KG; ++u) {
+      const int32_t sr = src[u] < 0 ? grp[0] : src[u];
+      sp[u] = slotpos[sr];
+      rp[u] = rankpos[sr];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) ps[u][ch] = D.psi[ch * D.n + sr];
+    }
+#pragma unroll
+    for (int u = 0; u < KG; ++u) {
+      if (src[u] < 0) continue;
+      const int64_t k = k0 + u * (int64_t)blockDim.x;
+      const int y = frank ? (int)(Sg - 1 - k) : (int)k;
+      int x = sp[u] - (int32_t)lo;
+      if (fslot) x = S - 1 - x;
+      s_yofx[x] = (int16_t)y;
+      s_xofy[y] = (int16_t)x;
+      s_key[y] = flipp(rp[u], frank, D.npad);
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) s_psi[ch * S + x] = ps[u][ch];
+    }
   }
   __syncthreads();
-  for (int x = threadIdx.x; x < S; x += blockDim.x) {
-    const int y = s_yofx[x];
-    if (y >= 0) {
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch)
-        atomicAdd(&s_sub[(ch * NSUB + (x >> SUBL)) * NSUB + (y >> SUBL)], s_psi[ch * S + x]);
+  // sub-grid cell sums: thread (channel, sub-row u) owns row u and walks its SUB slots (no
+  // fp64 shared atomics, which are CAS loops on sm_100)
+  for (int r = threadIdx.x; r < NCH * NSUB; r += blockDim.x) {
+    const int ch = r / NSUB, u = r % NSUB;
+    double *row = s_sub + (ch * NSUB + u) * NSUB;
+    for (int x = u << SUBL; x < (u + 1) << SUBL; ++x) {
+      const int y = s_yofx[x];
+      if (y >= 0) row[y >> SUBL] += s_psi[ch * S + x];
     }
   }
   __syncthreads();
@@ -254,23 +301,25 @@ __global__ void __launch_bounds__(kSolverThreads) level2_solver(Dom2 D) {
   for (int32_t qi = q0 + threadIdx.x; qi < q1; qi += blockDim.x) {
     const int32_t t = qlist[qi];
     int qx, qy;
-    int32_t ythr;
-    if (CHUNK) {
-      qx = (int)(D.Q1f[t] - cb * S);
-      ythr = D.Q0f[t];
-    } else {
-      qx = (int)(D.Q0f[t] - cb * S);
-      int64_t c = D.Q1f[t] >> LS;
-      ythr = (int32_t)((c > D.P ? D.P : c) * S);
+    {
+      int32_t ythr;
+      if (CHUNK) {
+        qx = (int)(D.Q1f[t] - cb * S);
+        ythr = D.Q0f[t];
+      } else {
+        qx = (int)(D.Q0f[t] - cb * S);
+        int64_t c = D.Q1f[t] >> LS;
+        ythr = (int32_t)((c > D.P ? D.P : c) * S);
+      }
+      // qy = #keys < ythr among the Sg sorted keys
+      int a = 0, bnd = (int)Sg;
+      while (a < bnd) {
+        const int mid = (a + bnd) >> 1;
+        if (s_key[mid] < ythr) a = mid + 1;
+        else bnd = mid;
+      }
+      qy = a;
     }
-    // qy = #keys < ythr among the Sg sorted keys
-    int a = 0, bnd = (int)Sg;
-    while (a < bnd) {
-      const int mid = (a + bnd) >> 1;
-      if (s_key[mid] < ythr) a = mid + 1;
-      else bnd = mid;
-    }
-    qy = a;
     const int u = qx >> SUBL, v = qy >> SUBL;
     double acc[NCH];
 #pragma unroll
@@ -475,6 +524,260 @@ __global__ void adjacent_equal_kernel(const uint64_t *__restrict__ keys, int64_t
 }
 
 // ------------------------------------------------------------------------------------------
+// Self-query dominance in group order (kde_dnc / ecdf_dnc, d = 2).  All per-source data is
+// laid out in the order of the chunk grouping (sources sorted by (p1 >> LS, p0)) and of the
+// block grouping ((p0 >> LS, p1)), so the level-2 CTAs read and accumulate contiguous ranges;
+// the three partial results (coarse grid in query order, chunk part, block part) are combined
+// once at the end with two gathers per point.
+struct GrpArrays {
+  int32_t *slot;     // unflipped slot-dimension position (p1 for chunks, p0 for blocks)
+  int32_t *rankpos;  // unflipped rank-dimension position (p0 for chunks, p1 for blocks)
+  double *x;         // [n][2] points
+  double *w;         // [nw][n] weights
+  double *psi;       // [nch][n] current code's psi
+  double *z;         // [n] current code's exp(-expo) (KDE) or unused
+  double *acc;       // [nch][n] accumulated z * partial dominance sums
+  int32_t *inv;      // source id -> group-order index
+};
+
+__global__ void group_gather_kernel(const int32_t *__restrict__ order,
+                                    const int32_t *__restrict__ pos_slot,
+                                    const int32_t *__restrict__ pos_rank,
+                                    const double *__restrict__ x, const double *__restrict__ w,
+                                    int nw, int64_t n, GrpArrays g) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = order[k];
+    g.slot[k] = pos_slot[i];
+    g.rankpos[k] = pos_rank[i];
+    g.x[2 * k] = x[2 * (int64_t)i];
+    g.x[2 * k + 1] = x[2 * (int64_t)i + 1];
+    for (int v = 0; v < nw; ++v) g.w[v * n + k] = w ? w[v * n + i] : 1.0;
+    g.inv[i] = (int32_t)k;
+  }
+}
+
+// psi[v][k] = w[v][k] e^{s}, z[k] = e^{-s}, s = sum_j (x_kj - c_j) a_j  (dnc.py:661-669,673)
+// kde == 0: psi = w (plain strict-dominance ECDF)
+__global__ void group_psi_kernel(GrpArrays g, int64_t n, KdeP kp, int nw, int kde) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    double e = 1.0;
+    if (kde) {
+      const double s = (g.x[2 * k] - kp.c[0]) * kp.a[0] + (g.x[2 * k + 1] - kp.c[1]) * kp.a[1];
+      e = exp(s);
+      g.z[k] = exp(-s);
+    }
+    for (int v = 0; v < nw; ++v) g.psi[v * n + k] = g.w[v * n + k] * e;
+  }
+}
+
+struct Dom2S {
+  int64_t n, P, npad;
+  int nch, f0, f1, kde;
+  GrpArrays gc, gb;  // chunk and block groupings
+  double *G;         // coarse grid [P][P][nch]
+};
+
+__global__ void __launch_bounds__(512) coarse_rows_group(Dom2S D) {
+  extern __shared__ double s_row[];  // [P][nch]
+  const int64_t c = blockIdx.x;
+  const int64_t g = D.f1 ? D.P - 1 - c : c;
+  const int64_t P = D.P;
+  for (int64_t i = threadIdx.x; i < P * D.nch; i += blockDim.x) s_row[i] = 0.0;
+  __syncthreads();
+  const int64_t lo = g * S, hi = (g + 1) * S < D.n ? (g + 1) * S : D.n;
+  for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) {
+    const int64_t b = flipp(D.gc.rankpos[k], D.f0, D.npad) >> LS;
+    for (int ch = 0; ch < D.nch; ++ch) atomicAdd(&s_row[b * D.nch + ch], D.gc.psi[ch * D.n + k]);
+  }
+  __syncthreads();
+  double *row = D.G + c * P * D.nch;
+  for (int64_t i = threadIdx.x; i < P * D.nch; i += blockDim.x) row[i] = s_row[i];
+}
+
+// acc_q[ch][t] += z_t * G[chunk(t) - 1][block(t) - 1]   (query order, self thresholds)
+__global__ void coarse_query_self(Dom2S D, const int32_t *__restrict__ pos0,
+                                  const int32_t *__restrict__ pos1, const double *__restrict__ x,
+                                  KdeP kp, double *__restrict__ accq) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < D.n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = flipp(pos1[t], D.f1, D.npad) >> LS, b = flipp(pos0[t], D.f0, D.npad) >> LS;
+    if (c == 0 || b == 0) continue;
+    double z = 1.0;
+    if (D.kde)
+      z = exp(-((x[2 * t] - kp.c[0]) * kp.a[0] + (x[2 * t + 1] - kp.c[1]) * kp.a[1]));
+    for (int ch = 0; ch < D.nch; ++ch)
+      accq[ch * D.n + t] += z * D.G[((c - 1) * D.P + (b - 1)) * D.nch + ch];
+  }
+}
+
+template <bool CHUNK, int NCH>
+__global__ void __launch_bounds__(kSolverThreads) level2_self(Dom2S D) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double *s_sub = reinterpret_cast<double *>(smem);               // [NCH][NSUB][NSUB]
+  double *s_psi = s_sub + NCH * NSUB * NSUB;                      // [NCH][S] by slot
+  int32_t *s_key = reinterpret_cast<int32_t *>(s_psi + NCH * S);  // [S] rank-dim positions by rank
+  int16_t *s_yofx = reinterpret_cast<int16_t *>(s_key + S);       // [S]
+  int16_t *s_xofy = s_yofx + S;                                   // [S]
+  int16_t *s_kofx = s_xofy + S;                                   // [S] group index by slot
+  int16_t *s_qy = s_kofx + S;                                     // [S] rank threshold by slot
+
+  const GrpArrays &A = CHUNK ? D.gc : D.gb;
+  const int64_t cb = blockIdx.x;
+  const int fslot = CHUNK ? D.f1 : D.f0;
+  const int frank = CHUNK ? D.f0 : D.f1;
+  const int64_t g = fslot ? D.P - 1 - cb : cb;
+  const int64_t lo = g * S;
+  const int Sg = (int)(lo + S < D.n ? S : D.n - lo);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+
+  for (int i = threadIdx.x; i < NCH * NSUB * NSUB; i += blockDim.x) s_sub[i] = 0.0;
+  for (int i = threadIdx.x; i < S; i += blockDim.x) {
+    s_yofx[i] = -1;
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) s_psi[ch * S + i] = 0.0;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < Sg; k += blockDim.x) {  // contiguous, coalesced
+    const int y = frank ? Sg - 1 - k : k;
+    int x = A.slot[lo + k] - (int32_t)lo;
+    if (fslot) x = S - 1 - x;
+    s_yofx[x] = (int16_t)y;
+    s_xofy[y] = (int16_t)x;
+    s_kofx[x] = (int16_t)k;
+    s_key[y] = flipp(A.rankpos[lo + k], frank, D.npad);
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) s_psi[ch * S + x] = A.psi[ch * D.n + lo + k];
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < NCH * NSUB; r += blockDim.x) {  // sub-grid cell sums, row-owned
+    const int ch = r / NSUB, u = r % NSUB;
+    double *row = s_sub + (ch * NSUB + u) * NSUB;
+    for (int x = u << SUBL; x < (u + 1) << SUBL; ++x) {
+      const int y = s_yofx[x];
+      if (y >= 0) row[y >> SUBL] += s_psi[ch * S + x];
+    }
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < NCH * NSUB; r += blockDim.x) {
+    double *row = s_sub + r * NSUB;
+    double run = 0.0;
+    for (int v = 0; v < NSUB; ++v) { run += row[v]; row[v] = run; }
+  }
+  __syncthreads();
+  for (int cidx = threadIdx.x; cidx < NCH * NSUB; cidx += blockDim.x) {
+    const int ch = cidx / NSUB, v = cidx % NSUB;
+    double run = 0.0;
+    for (int u = 0; u < NSUB; ++u) {
+      double *pp = s_sub + (ch * NSUB + u) * NSUB + v;
+      run += *pp;
+      *pp = run;
+    }
+  }
+  __syncthreads();
+
+  // pass A, slot order: full sub-cells + the query's partial slot sub-range
+  for (int xb = warp * 32; xb < S; xb += nwarps * 32) {
+    const int x = xb + lane;
+    const int y = s_yofx[x];
+    const bool occ = y >= 0;
+    int qy = 0, k = 0;
+    if (occ) {
+      k = s_kofx[x];
+      if (CHUNK) {
+        qy = y;
+      } else {
+        const int64_t c = s_key[y] >> LS;  // own chunk (self threshold)
+        const int32_t ythr = (int32_t)((c > D.P ? D.P : c) * S);
+        int a = 0, bnd = Sg;
+        while (a < bnd) {
+          const int mid = (a + bnd) >> 1;
+          if (s_key[mid] < ythr) a = mid + 1;
+          else bnd = mid;
+        }
+        qy = a;
+      }
+      s_qy[x] = (int16_t)qy;
+    }
+    const int u = xb >> SUBL, v = qy >> SUBL;
+    double acc[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch)
+      acc[ch] = (occ && u > 0 && v > 0) ? s_sub[(ch * NSUB + (u - 1)) * NSUB + (v - 1)] : 0.0;
+    const int cend = (int)__reduce_max_sync(0xffffffffu, occ ? (unsigned)x : 0u);
+    for (int c = u << SUBL; c < cend; ++c) {
+      const int yc = s_yofx[c];
+      const bool hit = occ && c < x && yc >= 0 && yc < qy;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const double pc = s_psi[ch * S + c];
+        if (hit) acc[ch] += pc;
+      }
+    }
+    if (occ) {
+      const double z = D.kde ? A.z[lo + k] : 1.0;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) A.acc[ch * D.n + lo + k] += z * acc[ch];
+    }
+  }
+  __syncthreads();
+  // pass B, rank order (coalesced accumulators): the partial rank sub-range, full slot rows
+  for (int yb = warp * 32; yb < Sg; yb += nwarps * 32) {
+    const int y = yb + lane;
+    const bool ok = y < Sg;
+    const int x = ok ? s_xofy[y] : 0;
+    const int qy = ok ? (int)s_qy[x] : 0;
+    const int xfull = (x >> SUBL) << SUBL;
+    const int cbeg = ok ? (qy >> SUBL) << SUBL : S;
+    const int cstart = (int)__reduce_min_sync(0xffffffffu, (unsigned)cbeg);
+    const int cend = (int)__reduce_max_sync(0xffffffffu, ok ? (unsigned)qy : 0u);
+    double acc[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) acc[ch] = 0.0;
+    for (int c = cstart; c < cend; ++c) {
+      const int xc = s_xofy[c];
+      const bool hit = ok && c >= cbeg && c < qy && xc < xfull;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const double pc = s_psi[ch * S + xc];
+        if (hit) acc[ch] += pc;
+      }
+    }
+    if (ok) {
+      const int k = frank ? Sg - 1 - y : y;
+      const double z = D.kde ? A.z[lo + k] : 1.0;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) A.acc[ch * D.n + lo + k] += z * acc[ch];
+    }
+  }
+}
+
+size_t level2_self_smem(int nch) {
+  return (size_t)nch * NSUB * NSUB * 8 + (size_t)nch * S * 8 + (size_t)S * 4 + (size_t)S * 2 * 4;
+}
+
+// out[v][t] = (acc_q[v][t] + acc_c[v][inv_c[t]] + acc_b[v][inv_b[t]] + (add_w ? w[v][t] : 0))
+//             * mult / div      (mult == 0: none, div == 0: none)
+__global__ void self_finish_kernel(int64_t n, int nw, const double *__restrict__ accq,
+                                   const double *__restrict__ accc, const int32_t *__restrict__ invc,
+                                   const double *__restrict__ accb, const int32_t *__restrict__ invb,
+                                   const double *__restrict__ w, int add_w, double mult, double div,
+                                   double *__restrict__ out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t kc = invc[t], kb = invb[t];
+    for (int v = 0; v < nw; ++v) {
+      double r = accq[v * n + t] + accc[v * n + kc] + accb[v * n + kb];
+      if (add_w) r = r + (w ? w[v * n + t] : 1.0);
+      if (mult != 0.0) r = r * mult;
+      if (div != 0.0) r = r / div;
+      out[v * n + t] = r;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // host-side composition
 
 struct Ranked {        // per-dimension ranking results (device)
@@ -607,13 +910,15 @@ int dom2d(PtsWs &p, int64_t n, int nch, int f0, int f1, const double *psi, doubl
   D.qb_list = p.qb_list;
   D.qb_start = p.qb_start;
   const int64_t P = p.P;
-  {
-    FCG_PROF("pts_query_keys", st);
-    query_keys<<<grid_for(n, 256), 256, 0, st>>>(D, p.kc, p.kb);
-    FCG_LAUNCH_CHECK();
+  {  // general thresholds: bucket the queries by chunk and by block
+    {
+      FCG_PROF("pts_query_keys", st);
+      query_keys<<<grid_for(n, 256), 256, 0, st>>>(D, p.kc, p.kb);
+      FCG_LAUNCH_CHECK();
+    }
+    FCG_TRY(bucket(p.kc, n, P + 1, p.qc_list, p.qc_start, p.cursor, p, st));
+    FCG_TRY(bucket(p.kb, n, P + 1, p.qb_list, p.qb_start, p.cursor, p, st));
   }
-  FCG_TRY(bucket(p.kc, n, P + 1, p.qc_list, p.qc_start, p.cursor, p, st));
-  FCG_TRY(bucket(p.kb, n, P + 1, p.qb_list, p.qb_start, p.cursor, p, st));
   // level 1: coarse grid
   const size_t row_smem = (size_t)P * nch * sizeof(double);
   if (row_smem <= 96 * 1024) {
@@ -693,6 +998,124 @@ int sorted_exclusive(const double *vals, const int32_t *order, int64_t n, bool r
   FCG_TRY(scan_axis<double>(lat + n, s1, 0, rev, inplace, scratch, st));
   FCG_PROF("pts_gather", st);
   excl_scatter_kernel<<<grid_for(n, 256), 256, 0, st>>>(lat + n, lat, order, n, dst);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}
+
+struct SelfWs {
+  GrpArrays gc, gb;
+  double *accq;
+};
+
+void carve_self(Workspace &W, SelfWs &q, int64_t n, int nw) {
+  for (GrpArrays *g : {&q.gc, &q.gb}) {
+    g->slot = W.take<int32_t>(n);
+    g->rankpos = W.take<int32_t>(n);
+    g->x = W.take<double>((size_t)n * 2);
+    g->w = W.take<double>((size_t)n * nw);
+    g->psi = W.take<double>((size_t)n * nw);
+    g->z = W.take<double>(n);
+    g->acc = W.take<double>((size_t)n * nw);
+    g->inv = W.take<int32_t>(n);
+  }
+  q.accq = W.take<double>((size_t)n * nw);
+}
+
+// Strict-dominance sums at the points for d = 2 in group order: the plain ECDF (kde = 0, one
+// orientation, psi = w) or the 2^2 Laplacian orientations (kde = 1, psi = w e^{s}, each term
+// weighted by e^{-s} at the query).  out[v][t] = (sum + (add_w ? w : 0)) * mult / div.
+int self_dom2d(const double *x, const double *w, int64_t n, int nw, int kde, const double *h,
+               const double *centre, int add_w, double mult, double div, PtsWs &p, SelfWs &q,
+               double *out, cudaStream_t st) {
+  FCG_TRY(prep2d(x, n, p, st));
+  const int g = grid_for(n, 256);
+  {
+    FCG_PROF("pts_group_gather", st);
+    group_gather_kernel<<<g, 256, 0, st>>>(p.bychunk, p.r[1].pos, p.r[0].pos, x, w, nw, n, q.gc);
+    group_gather_kernel<<<g, 256, 0, st>>>(p.byblock, p.r[0].pos, p.r[1].pos, x, w, nw, n, q.gb);
+    FCG_LAUNCH_CHECK();
+  }
+  FCG_CUDA_TRY(cudaMemsetAsync(q.gc.acc, 0, (size_t)n * nw * 8, st));
+  FCG_CUDA_TRY(cudaMemsetAsync(q.gb.acc, 0, (size_t)n * nw * 8, st));
+  FCG_CUDA_TRY(cudaMemsetAsync(q.accq, 0, (size_t)n * nw * 8, st));
+  Dom2S D{};
+  D.n = n;
+  D.P = p.P;
+  D.npad = p.npad;
+  D.nch = nw;
+  D.kde = kde;
+  D.gc = q.gc;
+  D.gb = q.gb;
+  D.G = p.G;
+  const int64_t P = p.P;
+  const size_t sm = level2_self_smem(nw);
+  if (nw == 1) {
+    FCG_CUDA_TRY(cudaFuncSetAttribute(level2_self<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    FCG_CUDA_TRY(cudaFuncSetAttribute(level2_self<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  } else {
+    FCG_CUDA_TRY(cudaFuncSetAttribute(level2_self<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    FCG_CUDA_TRY(cudaFuncSetAttribute(level2_self<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  }
+  const size_t row_smem = (size_t)P * nw * sizeof(double);
+  const bool smem_rows = row_smem <= 96 * 1024;
+  if (smem_rows)
+    FCG_CUDA_TRY(cudaFuncSetAttribute(coarse_rows_group, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(96 * 1024)));
+  const int ncodes = kde ? 4 : 1;
+  for (int code = 0; code < ncodes; ++code) {
+    KdeP kp{};
+    kp.d = 2;
+    for (int k = 0; k < 2; ++k) {
+      const double sgn = ((code >> k) & 1) ? -1.0 : 1.0;  // DeltaVector.from_code
+      kp.c[k] = kde ? centre[k] : 0.0;
+      kp.a[k] = kde ? sgn / h[k] : 0.0;
+    }
+    D.f0 = code & 1;
+    D.f1 = (code >> 1) & 1;
+    {
+      FCG_PROF("pts_psi", st);
+      group_psi_kernel<<<g, 256, 0, st>>>(q.gc, n, kp, nw, kde);
+      group_psi_kernel<<<g, 256, 0, st>>>(q.gb, n, kp, nw, kde);
+      FCG_LAUNCH_CHECK();
+    }
+    {
+      FCG_PROF("pts_coarse_hist", st);
+      if (smem_rows) {
+        coarse_rows_group<<<(unsigned)P, 512, row_smem, st>>>(D);
+      } else {
+        return fail(FCG_EUNSUPPORTED, "coarse grid row exceeds shared memory (n too large)");
+      }
+      FCG_LAUNCH_CHECK();
+    }
+    LatShape gs;
+    gs.d = 3;
+    gs.dims[0] = P;
+    gs.dims[1] = P;
+    gs.dims[2] = nw;
+    Epi inplace;
+    FCG_TRY(scan_axis<double>(p.G, gs, 1, false, inplace, p.scratch, st));
+    FCG_TRY(scan_axis<double>(p.G, gs, 0, false, inplace, p.scratch, st));
+    {
+      FCG_PROF("pts_coarse_query", st);
+      coarse_query_self<<<g, 256, 0, st>>>(D, p.r[0].pos, p.r[1].pos, x, kp, q.accq);
+      FCG_LAUNCH_CHECK();
+    }
+    {
+      FCG_PROF("pts_level2_chunk", st);
+      if (nw == 1) level2_self<true, 1><<<(unsigned)P, kSolverThreads, sm, st>>>(D);
+      else level2_self<true, 2><<<(unsigned)P, kSolverThreads, sm, st>>>(D);
+      FCG_LAUNCH_CHECK();
+    }
+    {
+      FCG_PROF("pts_level2_block", st);
+      if (nw == 1) level2_self<false, 1><<<(unsigned)P, kSolverThreads, sm, st>>>(D);
+      else level2_self<false, 2><<<(unsigned)P, kSolverThreads, sm, st>>>(D);
+      FCG_LAUNCH_CHECK();
+    }
+  }
+  FCG_PROF("pts_finish", st);
+  self_finish_kernel<<<g, 256, 0, st>>>(n, nw, q.accq, q.gc.acc, q.gc.inv, q.gb.acc, q.gb.inv, w,
+                                       add_w, mult, div, out);
   FCG_LAUNCH_CHECK();
   return FCG_OK;
 }
@@ -907,6 +1330,8 @@ extern "C" int fcg_dnc_ecdf(const double *x, int64_t n, int32_t d, const double 
   Workspace W(ws);
   PtsWs p;
   carve(W, p, n, d < 2 ? d : 2, 1, dom_ok, false, d == 1 ? 2 * n : 0);
+  SelfWs q{};
+  if (dom_ok) carve_self(W, q, n, 1);
   if (ws == nullptr) {
     *ws_bytes = W.bytes();
     return FCG_OK;
@@ -918,16 +1343,7 @@ extern "C" int fcg_dnc_ecdf(const double *x, int64_t n, int32_t d, const double 
     FCG_TRY(rank_dim(x, n, 1, 0, p, st));
     FCG_TRY(sorted_exclusive(w, p.r[0].order, n, false, p.lat, p.scratch, out, st));
   } else if (dom_ok) {
-    FCG_TRY(prep2d(x, n, p, st));
-    FCG_TRY(make_q(p.r[0].pos, n, 0, p.npad, p.Q0f, st));
-    FCG_TRY(make_q(p.r[1].pos, n, 0, p.npad, p.Q1f, st));
-    {
-      FCG_PROF("pts_psi", st);
-      if (w) FCG_CUDA_TRY(cudaMemcpyAsync(p.psi, w, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
-      else fill_f64<<<grid_for(n, 256), 256, 0, st>>>(p.psi, n, 1.0);
-      FCG_LAUNCH_CHECK();
-    }
-    FCG_TRY(dom2d(p, n, 1, 0, 0, p.psi, out, st));
+    return self_dom2d(x, w, n, 1, 0, nullptr, nullptr, include_self, 0.0, div, p, q, out, st);
   } else {
     Brute B;
     B.n = n;
@@ -956,6 +1372,8 @@ extern "C" int fcg_kde_points_laplacian(const double *x, int64_t n, int32_t d, c
   Workspace W(ws);
   PtsWs p;
   carve(W, p, n, d < 2 ? d : 2, nw, dom_ok, true, d == 1 ? n * 2 : 0);
+  SelfWs q{};
+  if (dom_ok) carve_self(W, q, n, nw);
   double *psi1 = nullptr, *F1 = nullptr;
   if (d == 1) {
     psi1 = W.take<double>((size_t)n * nw);
@@ -993,9 +1411,10 @@ extern "C" int fcg_kde_points_laplacian(const double *x, int64_t n, int32_t d, c
     return FCG_OK;
   }
 
+  if (d == 2)  // group-ordered self dominance over the 4 orientations (dnc.py:459-468)
+    return self_dom2d(x, w, n, nw, 1, h, centre, 1, scale, 0.0, p, q, out, st);
   const int ncodes = 1 << d;
-  if (d == 2) FCG_TRY(prep2d(x, n, p, st));
-  else FCG_TRY(rank_dim(x, n, 1, 0, p, st));
+  FCG_TRY(rank_dim(x, n, 1, 0, p, st));
   for (int code = 0; code < ncodes; ++code) {
     KdeP kp;
     kp.d = d;
@@ -1006,23 +1425,16 @@ extern "C" int fcg_kde_points_laplacian(const double *x, int64_t n, int32_t d, c
     }
     {
       FCG_PROF("pts_psi", st);
-      kde_psi_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, kp, w, nw, p.expo,
-                                                       d == 2 ? p.psi : psi1);
+      kde_psi_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, kp, w, nw, p.expo, psi1);
       FCG_LAUNCH_CHECK();
     }
-    if (d == 2) {
-      const int f0 = code & 1, f1 = (code >> 1) & 1;
-      FCG_TRY(make_q(p.r[0].pos, n, f0, p.npad, p.Q0f, st));
-      FCG_TRY(make_q(p.r[1].pos, n, f1, p.npad, p.Q1f, st));
-      FCG_TRY(dom2d(p, n, nw, f0, f1, p.psi, p.F, st));
-    } else {  // d == 1: code 0 = strictly below (prefix), code 1 = strictly above (suffix)
+    {  // d == 1: code 0 = strictly below (prefix), code 1 = strictly above (suffix)
       for (int v = 0; v < nw; ++v)
         FCG_TRY(sorted_exclusive(psi1 + (size_t)v * n, p.r[0].order, n, code == 1, p.lat,
                                  p.scratch, F1 + (size_t)v * n, st));
     }
     FCG_PROF("pts_kde_accum", st);
-    kde_accum_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, nw, p.expo, d == 2 ? p.F : F1, out,
-                                                       code == 0);
+    kde_accum_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, nw, p.expo, F1, out, code == 0);
     FCG_LAUNCH_CHECK();
   }
   FCG_PROF("pts_finish", st);
