@@ -136,16 +136,20 @@ int fcg_slab_finish(const void *local, int32_t kind, const void *carry, int64_t 
  * slab); u_bound (> 0 when known) bounds sum_k max_i |x_ik - c_k| / h_k and, when <= 600, lets
  * the kernels build each term's weights from per-point exponential factors instead of one exp
  * per point and term (the reference's fastsum.py:114-129 guard bounds the span per dimension);
- * when planes != NULL, term `code` also stores its slab-boundary plane of S (last axis-1 plane
- * for delta_1 = +1, first for -1) at planes[code * (M_0 * M_2 * ... * M_{d-1})]. */
+ * when planes != NULL, slot `code` of planes[code * (M_0 * M_2 * ... * M_{d-1})] receives the
+ * slab-boundary plane of S (last axis-1 plane for delta_1 = +1, first for -1) weighted by the
+ * term's factors zf_k(i_k) = exp(-delta_k (z_k - c_k) / h_k) of the axes k >= kw, kw =
+ * max(2, d - 2); terms that differ only in the signs of those axes may be summed into the slot
+ * of the lowest such code (the other slots are then zero).  Linear, so the exchange is a sum. */
 int fcg_kde_grid_laplacian_ex(const double *x, int64_t n, int32_t d, const double *w,
                               const double *knots, const int64_t *m, const double *h,
                               const double *centre, double n_scale, double u_bound,
                               double *planes, double *out, void *ws, size_t *ws_bytes,
                               void *stream);
 
-/* out[i] += sum_code zfac_code(i) * C_code[i_0, i_2, ...] / (2^d n_scale prod h): the exchanged
- * carry planes of every term folded into a slab's KDE (the zfac factor is linear in S). */
+/* out[i] += sum_code prod_{k<kw} zf_code,k(i_k) * C_code[i_0, i_2, ...] / (2^d n_scale prod h):
+ * the exchanged carry planes (weighted as fcg_kde_grid_laplacian_ex stores them) folded into a
+ * slab's KDE (zfac is linear in S). */
 int fcg_kde_carry_fixup(double *out, int32_t d, const int64_t *m, const double *knots,
                         const double *h, const double *centre, const double *planes,
                         double n_scale, void *ws, size_t *ws_bytes, void *stream);

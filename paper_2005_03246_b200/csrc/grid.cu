@@ -162,34 +162,50 @@ __global__ void minmax_init(unsigned long long *mm, int d) {
   }
 }
 
-__global__ void __launch_bounds__(256) minmax_kernel(const double *__restrict__ x, int64_t n,
+// x is read as a flat stream of n*d doubles, VEC per load; the grid's total stride is a
+// multiple of d, so each thread's VEC lanes always hold the same components k0..k0+VEC-1
+// (mod d) and it keeps one (lo, hi) pair per lane -- coalesced, no per-point component loop.
+template <int VEC>
+__global__ void __launch_bounds__(256) minmax_kernel(const double *__restrict__ x, int64_t total,
                                                      int d, unsigned long long *mm) {
-  uint64_t lo[FCG_MAX_DIM], hi[FCG_MAX_DIM];
-  for (int k = 0; k < d; ++k) {
-    lo[k] = ~0ull;
-    hi[k] = 0ull;
+  __shared__ unsigned long long s_lo[FCG_MAX_DIM], s_hi[FCG_MAX_DIM];
+  if (threadIdx.x < FCG_MAX_DIM) {
+    s_lo[threadIdx.x] = ~0ull;
+    s_hi[threadIdx.x] = 0ull;
   }
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    for (int k = 0; k < d; ++k) {
-      const uint64_t key = ord_key(x[i * d + k]);
-      lo[k] = key < lo[k] ? key : lo[k];
-      hi[k] = key > hi[k] ? key : hi[k];
-    }
-  }
-  for (int k = 0; k < d; ++k) {
-    uint64_t a = lo[k], b = hi[k];
+  __syncthreads();
+  uint64_t lo[VEC], hi[VEC];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t ao = __shfl_xor_sync(0xffffffffu, a, o);
-      const uint64_t bo = __shfl_xor_sync(0xffffffffu, b, o);
-      a = ao < a ? ao : a;
-      b = bo > b ? bo : b;
+  for (int v = 0; v < VEC; ++v) {
+    lo[v] = ~0ull;
+    hi[v] = 0ull;
+  }
+  const int64_t t0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * VEC;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * VEC;
+  for (int64_t j = t0; j < total; j += stride) {
+    if (VEC == 2 && j + 1 < total) {
+      const double2 p = __ldcs(reinterpret_cast<const double2 *>(x + j));
+      const uint64_t a = ord_key(p.x), b = ord_key(p.y);
+      lo[0] = a < lo[0] ? a : lo[0];
+      hi[0] = a > hi[0] ? a : hi[0];
+      lo[VEC - 1] = b < lo[VEC - 1] ? b : lo[VEC - 1];
+      hi[VEC - 1] = b > hi[VEC - 1] ? b : hi[VEC - 1];
+    } else {
+      const uint64_t a = ord_key(x[j]);
+      lo[0] = a < lo[0] ? a : lo[0];
+      hi[0] = a > hi[0] ? a : hi[0];
     }
-    if ((threadIdx.x & 31) == 0) {
-      atomicMin(mm + k, (unsigned long long)a);
-      atomicMax(mm + d + k, (unsigned long long)b);
-    }
+  }
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    const int k = (int)((t0 + v) % d);
+    atomicMin(s_lo + k, (unsigned long long)lo[v]);  // idle lanes hold the identities
+    atomicMax(s_hi + k, (unsigned long long)hi[v]);
+  }
+  __syncthreads();
+  if (threadIdx.x < d) {
+    atomicMin(mm + threadIdx.x, s_lo[threadIdx.x]);
+    atomicMax(mm + d + threadIdx.x, s_hi[threadIdx.x]);
   }
 }
 
@@ -367,7 +383,16 @@ extern "C" int fcg_minmax(const double *x, int64_t n, int32_t d, double *out_min
   minmax_init<<<1, 32, 0, st>>>(mm, d);
   FCG_LAUNCH_CHECK();
   if (n > 0) {
-    minmax_kernel<<<grid_for(n, 256, 4), 256, 0, st>>>(x, n, d, mm);
+    // grid: a multiple of d blocks (so the flat stride is a multiple of d), ~4 per SM
+    const int64_t total = n * d;
+    const bool vec = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    const int64_t per = vec ? 512 : 256;
+    int64_t blocks = std::min<int64_t>(ceil_div(total, per), 4 * (int64_t)sm_count());
+    blocks = ceil_div(blocks, d) * d;
+    if (vec)
+      minmax_kernel<2><<<(unsigned)blocks, 256, 0, st>>>(x, total, d, mm);
+    else
+      minmax_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(x, total, d, mm);
     FCG_LAUNCH_CHECK();
   }
   minmax_finish<<<1, 32, 0, st>>>(mm, d, out_minmax);
@@ -452,6 +477,7 @@ static int kde_grid_impl(const double *x, int64_t n, int32_t d, const double *w,
     if (planes) {
       e.plane_out = planes + (int64_t)code * plane_sz;
       e.plane_idx = rev[1] ? 0 : m[1] - 1;
+      e.cap_kw = kde_cap_kw(d);
     }
     FCG_TRY(scan_lattice<double>(lat, s, rev, e, scratch, st));
   }
@@ -461,7 +487,7 @@ static int kde_grid_impl(const double *x, int64_t n, int32_t d, const double *w,
 namespace {
 // out[i] += scale * sum_code zfac_code(i) * C_code[i0, i2, ..]   (slab carry fix-up)
 struct FixP {
-  int d, ncodes;
+  int d, ncodes, kw;  // zf of axes k < kw (the captured planes carry the rest)
   int64_t dims[FCG_MAX_DIM];
   int64_t zoff[FCG_MAX_DIM];
   int64_t zsz;        // entries per code in zf
@@ -487,7 +513,7 @@ __global__ void kde_fixup_kernel(double *__restrict__ out, FixP p, const double 
     for (int code = 0; code < p.ncodes; ++code) {
       const double *z = zf + code * p.zsz;
       double zz = 1.0;
-      for (int k = 0; k < p.d; ++k) zz *= z[p.zoff[k] + idx[k]];
+      for (int k = 0; k < p.kw; ++k) zz *= z[p.zoff[k] + idx[k]];
       acc += zz * C[code * p.plane_sz + pi];
     }
     out[t] += p.scale * acc;
@@ -533,6 +559,7 @@ extern "C" int fcg_kde_carry_fixup(double *out, int32_t d, const int64_t *m, con
   FixP p{};
   p.d = d;
   p.ncodes = ncodes;
+  p.kw = kde_cap_kw(d);
   int64_t off = 0, L = 1;
   for (int k = 0; k < d; ++k) {
     p.dims[k] = m[k];

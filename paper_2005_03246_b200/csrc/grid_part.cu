@@ -17,9 +17,9 @@ namespace {
 
 constexpr uint32_t kDead = 0xFFFFFFFFu;
 constexpr int kPlaneThreads = 512;
-constexpr int kKdeThreads = 512;
+constexpr int kKdeThreads = 256;
 constexpr size_t kEcdfTileBytes = 96 * 1024;   // int32 tile budget (2 CTAs per SM)
-constexpr size_t kKdeTileBytes = 72 * 1024;    // fp64 row-block budget (3 CTAs per SM)
+constexpr size_t kKdeTileBytes = 110 * 1024;   // two fp64 row-block tiles (2 CTAs per SM)
 constexpr int64_t kMinPartitionN = int64_t(1) << 20;
 
 struct PartGeo {
@@ -28,6 +28,8 @@ struct PartGeo {
   int64_t shift[FCG_MAX_DIM];  // bucket-space index = b - shift
   int64_t W, R, nrb, H;
   int ecdf;                    // 1: val = in-block cell offset; 0: val = point index
+  int cell_bits;               // > 0: key = bucket << cell_bits | r_in << col_bits | col
+  int col_bits;
 };
 
 template <int D>
@@ -73,21 +75,24 @@ __global__ void __launch_bounds__(256, 4) part_bin_kernel(const double *__restri
       const int rb = row / (int)p.R;
       key = plane * (uint32_t)p.nrb + (uint32_t)rb;
       if (p.ecdf) val = (row - rb * (int)p.R) * (int)p.W + col;
+      if (p.cell_bits > 0)
+        key = (key << p.cell_bits) | ((uint32_t)(row - rb * (int)p.R) << p.col_bits) | (uint32_t)col;
     }
     keys[i] = key;
     vals[i] = val;
   }
 }
 
-// start[b] = first sorted position whose key >= b, for b in [0, NB]
+// start[b] = first sorted position whose key >= b << shift, for b in [0, NB]
 __global__ void bucket_start_kernel(const uint32_t *__restrict__ keys, int64_t n, int64_t NB,
-                                    int32_t *__restrict__ start) {
+                                    int shift, int32_t *__restrict__ start) {
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= NB;
        b += (int64_t)gridDim.x * blockDim.x) {
     int64_t lo = 0, hi = n;
+    const int64_t bk = b << shift;
     while (lo < hi) {
       const int64_t mid = (lo + hi) >> 1;
-      if ((int64_t)keys[mid] < b) lo = mid + 1;
+      if ((int64_t)keys[mid] < bk) lo = mid + 1;
       else hi = mid;
     }
     start[b] = (int32_t)lo;
@@ -362,32 +367,364 @@ __global__ void __launch_bounds__(kPlaneThreads, 2) plane_count_kernel(
   (void)G;
 }
 
-// KDE term: CTA per cell-space plane.  Records are bucketed by full-space (M+1) row block; a
-// term with row shift s reads full block rb as cell rows [rb*Rf - s, (rb+1)*Rf - s), so every
-// cell row block comes from exactly one bucket.  Blocks are visited in the term's row scan
-// direction with a carry row, like the ECDF plane kernel.
-struct KdeTerm {
+// KDE term group: CTA per cell-space plane.  The 2^d terms are folded in groups that share
+// the signs of the leading axes (k < kz); inside a group only the in-plane factors differ, so
+//   sum_t zfac_t S_t = prod_{k<kz} zf_k  x  S_lead( sum_t zf_r,t(i_r) zf_c,t(i_c) P_t )
+// with P_t the term's in-plane 2-D scan (the leading-axis scans are linear and commute with
+// multiplication by functions of the in-plane indices).  The CTA builds, per row direction
+// (phase), the two column-direction tiles from ONE pass over its bucket's records, scans them,
+// weights them by the in-plane factors and writes (phase 0) or adds (phase 1) the plane.
+// Records are bucketed by full-space (M+1) row block; a phase with row shift s reads full block
+// rb as cell rows [rb*Rf - s, (rb+1)*Rf - s), so every cell row block comes from one bucket.
+struct KdeGroup {
   int d;
   int64_t Mr, Mc;                    // cell extents of axes d-2, d-1
-  int64_t sr, sc;                    // shifts (1 where delta = -1)
   int64_t Rf, nrb;                   // full-space rows per bucket block, blocks per plane
   int64_t lead_m[FCG_MAX_DIM];       // cell extents of leading axes
-  int64_t lead_s[FCG_MAX_DIM];       // their shifts
+  int64_t lead_s[FCG_MAX_DIM];       // their shifts (1 where delta = -1)
   int64_t lead_full[FCG_MAX_DIM];    // full (M+1) extents of leading axes
-  double c[FCG_MAX_DIM], a[FCG_MAX_DIM];
+  unsigned lead_neg;                 // leading axes with delta = -1 (bit k)
+  int nphase;                        // 1: row sign fixed (rneg[0]); 2: both row signs
+  int rneg[2];
+  double c[FCG_MAX_DIM], a[FCG_MAX_DIM];  // raw records: centre and 1/h
+  const double *zr[2];               // row-axis factor table of each phase (cell index)
+  const double *zcp, *zcm;           // column-axis factor tables, delta_c = +1 / -1
+  int cell_bits, col_bits;           // sorted key layout: bucket << cell_bits | r_in << col_bits | col
+  unsigned fmask[2];                 // factored record fields multiplied into psi per phase
+  int nf[2];                         // ... as a list (fast path)
+  int fidx[2][FCG_MAX_DIM + 1];
+  int exp;                           // profiling experiments (FCG_KDE_EXP): 1 no records, 2 no walk
 };
 
+// ---- accumulation of cell-sorted records into the two row-block tiles -------------------
+// Each warp owns a contiguous share of the bucket and walks it in windows of 32 consecutive
+// records.  Runs of equal keys are summed with shuffles; a run strictly inside the warp's
+// share holds every record of its cell (the bucket is sorted), so it is written with a plain
+// shared store, and a run reaching lane 31 is carried into the next window in registers.  Only
+// the first and last run of a share may meet another warp's records and use atomics (fp64
+// shared atomics are CAS loops on sm_100).
+struct TileTarget {
+  double *tp, *tm;
+  int W, nr, rowoff, col_bits;
+  uint32_t cmask, rmask;
+  int swz;  // tiles use the swizzled row layout of kde_tiles_walk
+};
+
+// Row layout of the vectorised walk: 16-byte chunk ch of a row is stored at ch ^ ((ch>>3)&7),
+// so the lanes' strided 16-byte accesses (E/2 chunks per lane) hit distinct banks.
+__device__ __forceinline__ int swz_col(int c) { return c ^ (((c >> 4) & 7) << 1); }
+
+__device__ __forceinline__ void tile_put(const TileTarget &T, uint32_t key, double vp, double vm,
+                                         bool atomic) {
+  const int cr = (int)((key >> T.col_bits) & T.rmask) + T.rowoff;
+  const int col = (int)(key & T.cmask);
+  if (cr < 0 || cr >= T.nr) return;
+  if (col < T.W) {
+    double *p = T.tp + cr * T.W + (T.swz ? swz_col(col) : col);
+    if (atomic) atomicAdd(p, vp);
+    else *p = vp;
+  }
+  if (col >= 1) {
+    double *m = T.tm + cr * T.W + (T.swz ? swz_col(col - 1) : col - 1);
+    if (atomic) atomicAdd(m, vm);
+    else *m = vm;
+  }
+}
+
+struct KdeRec {
+  uint32_t key;
+  double pp, pm;
+};
+
+// psi of the delta_c = +1 / -1 terms of the phase for sorted record q
+__device__ __forceinline__ KdeRec kde_load(const uint32_t *__restrict__ keys,
+                                           const double *__restrict__ rec, int64_t nrec,
+                                           int32_t q, bool in, int factored, unsigned fmask,
+                                           int mfield, int d, const double *c, const double *a,
+                                           unsigned negmask) {
+  KdeRec r;
+  r.key = in ? keys[q] : 0xFFFFFFFFu;
+  r.pp = 0.0;
+  r.pm = 0.0;
+  if (!in) return r;
+  if (factored) {
+    double f[FCG_MAX_DIM + 1];
+#pragma unroll
+    for (int k = 0; k <= FCG_MAX_DIM; ++k)  // all loads issued before the product
+      f[k] = ((fmask >> k) & 1) ? rec[(int64_t)k * nrec + q] : 1.0;
+    const double qc = rec[(int64_t)mfield * nrec + q];
+    double v = f[0];
+#pragma unroll
+    for (int k = 1; k <= FCG_MAX_DIM; ++k) v *= f[k];
+    r.pp = v;
+    r.pm = v * qc;
+  } else {
+    double sx = 0.0;
+    for (int k = 0; k < d - 1; ++k)
+      sx += (rec[(int64_t)k * nrec + q] - c[k]) * (((negmask >> k) & 1) ? -a[k] : a[k]);
+    const double uc = (rec[(int64_t)(d - 1) * nrec + q] - c[d - 1]) * a[d - 1];
+    const double wq = rec[(int64_t)d * nrec + q];
+    r.pp = wq * exp(sx + uc);
+    r.pm = wq * exp(sx - uc);
+  }
+  return r;
+}
+
+// Factored records: psi_+ = prod of NF fields, psi_- = psi_+ * q_c.  Raw fields of the next
+// two windows are loaded ahead of the reduction of the current one (the product would
+// otherwise wait on each window's loads in turn).
+template <int NF>
+struct RawWin {
+  uint32_t key;
+  double f[NF > 0 ? NF : 1];
+  double qc;
+};
+
+template <int NF>
+__device__ __forceinline__ void raw_load(RawWin<NF> &r, const uint32_t *__restrict__ keys,
+                                         const double *const *fp, const double *fq, int32_t q,
+                                         bool in) {
+  r.key = in ? keys[q] : 0xFFFFFFFFu;
+  const int32_t qq = in ? q : 0;
+#pragma unroll
+  for (int j = 0; j < NF; ++j) r.f[j] = fp[j][qq];
+  r.qc = fq[qq];
+}
+
+struct AccParams {
+  const uint32_t *keys;
+  const double *fp[FCG_MAX_DIM + 1];
+  const double *fq;
+  int32_t q0, q1;
+};
+
+// one window: segmented run sums, carry handling, tile writes (see the comment above)
+struct RunCarry {
+  uint32_t key = 0xFFFFFFFFu;
+  double p = 0.0, m = 0.0;
+  bool first = false;
+};
+
+__device__ __forceinline__ void window_reduce(const TileTarget &T, uint32_t key, double pp,
+                                              double pm, bool share_first, RunCarry &c,
+                                              int lane) {
+  const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+  const bool head = lane == 0 || key != prev;
+  const unsigned heads = __ballot_sync(0xffffffffu, head);
+  const int hl = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+  const int span = lane - hl;
+  const int maxspan = __reduce_max_sync(0xffffffffu, span);
+  double sp = pp, sm = pm;
+  for (int o = 1; o <= maxspan; ++o) {
+    const double up = __shfl_up_sync(0xffffffffu, pp, o);
+    const double um = __shfl_up_sync(0xffffffffu, pm, o);
+    if (o <= span) {
+      sp += up;
+      sm += um;
+    }
+  }
+  const uint32_t key0 = __shfl_sync(0xffffffffu, key, 0);
+  const bool cont = key0 == c.key;
+  if (cont && hl == 0) {
+    sp += c.p;
+    sm += c.m;
+  }
+  if (!cont && c.key != 0xFFFFFFFFu && lane == 0) tile_put(T, c.key, c.p, c.m, c.first);
+  const bool ffirst = share_first || (cont && c.first);  // window's first run = share's first
+  const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1);
+  if (tail && lane != 31 && key != 0xFFFFFFFFu) tile_put(T, key, sp, sm, hl == 0 && ffirst);
+  c.key = __shfl_sync(0xffffffffu, key, 31);
+  c.p = __shfl_sync(0xffffffffu, sp, 31);
+  c.m = __shfl_sync(0xffffffffu, sm, 31);
+  const int hl31 = __shfl_sync(0xffffffffu, hl, 31);
+  c.first = hl31 == 0 && ffirst;
+}
+
+template <int NF, int DEPTH = (NF <= 2 ? 2 : 1)>
+__device__ __forceinline__ void accumulate_factored(const TileTarget &T, const AccParams &P,
+                                                    int wb, int we, int lane) {
+  RunCarry c;
+  RawWin<NF> n1, n2;
+  const double *fp[NF > 0 ? NF : 1];
+#pragma unroll
+  for (int j = 0; j < NF; ++j) fp[j] = P.fp[j];
+  auto ld = [&](RawWin<NF> &r, int win) {
+    const int32_t q = P.q0 + win * 32 + lane;
+    raw_load<NF>(r, P.keys, fp, P.fq, q, q < P.q1);
+  };
+  if (wb < we) ld(n1, wb);
+  if (DEPTH > 1 && wb + 1 < we) ld(n2, wb + 1);
+  for (int win = wb; win < we; ++win) {
+    const RawWin<NF> cur = n1;
+    if (DEPTH > 1) {
+      n1 = n2;
+      if (win + 2 < we) ld(n2, win + 2);
+    } else if (win + 1 < we) {
+      ld(n1, win + 1);
+    }
+    double pp = 1.0;
+#pragma unroll
+    for (int j = 0; j < NF; ++j) pp *= cur.f[j];
+    if (cur.key == 0xFFFFFFFFu) pp = 0.0;
+    window_reduce(T, cur.key, pp, pp * cur.qc, win == wb, c, lane);
+  }
+  if (c.key != 0xFFFFFFFFu && lane == 0) tile_put(T, c.key, c.p, c.m, true);
+}
+
+// In-plane 2-D scan of the two row-block tiles fused with the factor weighting and the plane
+// write, for W == 32 * E: warp g walks row segment g (in scan order) with each lane owning E
+// consecutive columns of both tiles in registers.  U accumulates raw column sums (carry of the
+// previous row blocks + earlier segments + rows so far), so each row's 2-D scan value is the
+// row-direction scan of U (serial over the lane's E columns, one warp scan across lanes):
+//   delta_c = +1 tile: prefix over columns, delta_c = -1 tile: suffix.
+// Every tile element is read twice (segment sums, walk) and zeroed on the walk, ready for the
+// next row block.
+template <int E>
+__device__ __forceinline__ void kde_tiles_walk(double *tp, double *tm, double *cp, double *cm,
+                                               double *segp, double *segm, int nr, int rneg,
+                                               const double *zr, const double *zcp_r,
+                                               const double *zcm_r, double *g, int ph) {
+  constexpr int W = 32 * E, C = E / 2;  // C 16-byte chunks per lane
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int c0 = lane * E;
+  int pc[C];  // physical (swizzled) double offsets of the lane's chunks
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    const int ch = lane * C + j;
+    pc[j] = (ch ^ ((ch >> 3) & 7)) * 2;
+  }
+  const int Rg = (nr + nw - 1) / nw;
+  const int q0 = warp * Rg, q1 = min(nr, q0 + Rg);
+  // pass 1: raw column sums of this warp's segment
+  {
+    double sp[E], sm[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) sp[e] = sm[e] = 0.0;
+    for (int q = q0; q < q1; ++q) {
+      const int r = rneg ? nr - 1 - q : q;
+#pragma unroll
+      for (int j = 0; j < C; ++j) {
+        const double2 u = *reinterpret_cast<const double2 *>(tp + r * W + pc[j]);
+        const double2 v = *reinterpret_cast<const double2 *>(tm + r * W + pc[j]);
+        sp[2 * j] += u.x; sp[2 * j + 1] += u.y;
+        sm[2 * j] += v.x; sm[2 * j + 1] += v.y;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      *reinterpret_cast<double2 *>(segp + warp * W + pc[j]) = make_double2(sp[2 * j], sp[2 * j + 1]);
+      *reinterpret_cast<double2 *>(segm + warp * W + pc[j]) = make_double2(sm[2 * j], sm[2 * j + 1]);
+    }
+  }
+  __syncthreads();
+  // pass 2: walk the segment with the column sums of everything before it
+  double up[E], um[E];
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    const double2 a = *reinterpret_cast<const double2 *>(cp + pc[j]);
+    const double2 b = *reinterpret_cast<const double2 *>(cm + pc[j]);
+    up[2 * j] = a.x; up[2 * j + 1] = a.y;
+    um[2 * j] = b.x; um[2 * j + 1] = b.y;
+  }
+  for (int w = 0; w < warp; ++w) {
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const double2 a = *reinterpret_cast<const double2 *>(segp + w * W + pc[j]);
+      const double2 b = *reinterpret_cast<const double2 *>(segm + w * W + pc[j]);
+      up[2 * j] += a.x; up[2 * j + 1] += a.y;
+      um[2 * j] += b.x; um[2 * j + 1] += b.y;
+    }
+  }
+  double zp[E], zm[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    zp[e] = zcp_r[c0 + e];
+    zm[e] = zcm_r[c0 + e];
+  }
+  const double2 zero2 = make_double2(0.0, 0.0);
+  for (int q = q0; q < q1; ++q) {
+    const int r = rneg ? nr - 1 - q : q;
+    double2 *o = reinterpret_cast<double2 *>(g + (int64_t)r * W + c0);
+    const double zrv = __ldg(zr + r);
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      double2 *a = reinterpret_cast<double2 *>(tp + r * W + pc[j]);
+      double2 *b = reinterpret_cast<double2 *>(tm + r * W + pc[j]);
+      const double2 u = *a, v = *b;
+      *a = zero2;
+      *b = zero2;
+      up[2 * j] += u.x; up[2 * j + 1] += u.y;
+      um[2 * j] += v.x; um[2 * j + 1] += v.y;
+    }
+    double tsp = 0.0, tsm = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      tsp += up[e];
+      tsm += um[e];
+    }
+    double ip = tsp, im = tsm;  // inclusive prefix (p) / suffix (m) of the lane totals
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const double xp = __shfl_up_sync(0xffffffffu, ip, off);
+      const double xm = __shfl_down_sync(0xffffffffu, im, off);
+      if (lane >= off) ip += xp;
+      if (lane + off < 32) im += xm;
+    }
+    double sp[E], sm[E];
+    double run = ip - tsp;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      run += up[e];
+      sp[e] = run;
+    }
+    run = im - tsm;
+#pragma unroll
+    for (int e = E - 1; e >= 0; --e) {
+      run += um[e];
+      sm[e] = run;
+    }
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const int e = 2 * j;
+      double2 v;
+      v.x = zrv * (zp[e] * sp[e] + zm[e] * sm[e]);
+      v.y = zrv * (zp[e + 1] * sp[e + 1] + zm[e + 1] * sm[e + 1]);
+      if (ph > 0) {
+        const double2 old = o[j];
+        v.x += old.x;
+        v.y += old.y;
+      }
+      o[j] = v;
+    }
+  }
+  __syncthreads();
+  // carry for the next row block: column sums through this block (same swizzled layout)
+  for (int c = threadIdx.x; c < W; c += blockDim.x) {
+    double a = cp[c], b = cm[c];
+    for (int w = 0; w < nw; ++w) {
+      a += segp[w * W + c];
+      b += segm[w * W + c];
+    }
+    cp[c] = a;
+    cm[c] = b;
+  }
+  __syncthreads();
+}
+
 template <int SE>
-__global__ void __launch_bounds__(kKdeThreads, 2) plane_kde_kernel(
-    KdeTerm t, const int32_t *__restrict__ start, const double *__restrict__ rec,
-    const uint32_t *__restrict__ loc, int factored, unsigned negmask, int rev_r, int rev_c,
-    double *__restrict__ lat) {
+__global__ void __launch_bounds__(kKdeThreads, 2) plane_kde_group_kernel(
+    KdeGroup t, const int32_t *__restrict__ start, const double *__restrict__ rec, int64_t nrec,
+    const uint32_t *__restrict__ keys, int factored, double *__restrict__ lat) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int W = (int)t.Mc, H = (int)t.Mr, Rf = (int)t.Rf;
-  double *tile = reinterpret_cast<double *>(smem);
-  double *carry = tile + (size_t)Rf * W;
-  double *seg = carry + W;
+  double *tp = reinterpret_cast<double *>(smem);  // delta_c = +1 tile
+  double *tm = tp + (size_t)Rf * W;               // delta_c = -1 tile
+  double *cp = tm + (size_t)Rf * W;
+  double *cm = cp + W;
+  double *zc = cm + W;                            // interleaved (zcp, zcm) per column (SE == 0)
+  double *seg = zc + 2 * W;                       // SE > 0: [2][nwarps][W]; else scan segments
   const int d = t.d;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int64_t cplane = blockIdx.x;
   int64_t rem = cplane, fplane = 0, mul = 1;
   for (int k = d - 3; k >= 0; --k) {
@@ -396,93 +733,125 @@ __global__ void __launch_bounds__(kKdeThreads, 2) plane_kde_kernel(
     fplane += (i + t.lead_s[k]) * mul;
     mul *= t.lead_full[k];
   }
-  for (int c = threadIdx.x; c < W; c += blockDim.x) carry[c] = 0.0;
+  for (int c = threadIdx.x; c < W; c += blockDim.x) {
+    zc[2 * c] = t.zcp[c];
+    zc[2 * c + 1] = t.zcm[c];
+  }
+  if (SE > 0) {  // the walk re-zeroes the tiles as it reads them
+    tile_zero<double>(tp, 2 * Rf * W);
+  }
   double *plane_out = lat + cplane * H * W;
-  for (int64_t rbi = 0; rbi < t.nrb; ++rbi) {
-    const int64_t rb = rev_r ? t.nrb - 1 - rbi : rbi;
-    int lo = (int)(rb * Rf - t.sr), hi = lo + Rf;
-    const int clo = lo < 0 ? 0 : lo, chi = hi > H ? H : hi;
-    if (chi <= clo) continue;
-    const int nr = chi - clo;
-    double *gtile = plane_out + (int64_t)clo * W;  // this block's rows of the lattice
-    tile_zero<double>(tile, nr * W);
-    __syncthreads();
-    const int64_t b = fplane * t.nrb + rb;
-    const int32_t q0 = start[b], q1 = start[b + 1];
-    constexpr int KB = 2;
-    for (int32_t qb = q0 + threadIdx.x; qb < q1; qb += KB * blockDim.x) {
-      uint32_t l[KB];
-      double psi[KB];  // loads of all KB records issued before the first atomic
-#pragma unroll
-      for (int u = 0; u < KB; ++u) {
-        const int32_t q = qb + u * (int32_t)blockDim.x;
-        const bool ok = q < q1;
-        l[u] = ok ? loc[q] : 0xFFFFFFFFu;
-        const double *r = rec + (int64_t)(ok ? q : q0) * (d + 1);
-        double v;
-        if (factored) {
-          v = r[0];
-          for (int k = 0; k < d; ++k)
-            if ((negmask >> k) & 1) v *= r[1 + k];
-        } else {
-          double sx = 0.0;
-          for (int k = 0; k < d; ++k) sx += (r[k] - t.c[k]) * t.a[k];
-          v = r[d] * exp(sx);
-        }
-        psi[u] = v;
+  const int kr = d - 2, kcol = d - 1;
+  const uint32_t cmask = (1u << t.col_bits) - 1u, rmask = (1u << (t.cell_bits - t.col_bits)) - 1u;
+  for (int ph = 0; ph < t.nphase; ++ph) {
+    const int rneg = t.rneg[ph];
+    const int sr = rneg;
+    const double *zr = t.zr[ph];
+    for (int c = threadIdx.x; c < W; c += blockDim.x) {
+      cp[c] = 0.0;
+      cm[c] = 0.0;
+    }
+    for (int64_t rbi = 0; rbi < t.nrb; ++rbi) {
+      const int64_t rb = rneg ? t.nrb - 1 - rbi : rbi;
+      const int lo = (int)(rb * Rf - sr), hi = lo + Rf;
+      const int clo = lo < 0 ? 0 : lo, chi = hi > H ? H : hi;
+      if (chi <= clo) continue;
+      const int nr = chi - clo;
+      if (SE == 0) {
+        tile_zero<double>(tp, nr * W);
+        tile_zero<double>(tm, nr * W);
       }
-#pragma unroll
-      for (int u = 0; u < KB; ++u) {
-        const int cr = (int)(l[u] >> 16) - (int)t.sr - clo;
-        const int cc = (int)(l[u] & 0xFFFFu) - (int)t.sc;
-        if (l[u] == 0xFFFFFFFFu || cr < 0 || cr >= nr || cc < 0 || cc >= W) continue;
-        atomicAdd(&tile[cr * W + cc], psi[u]);  // fp64 shared atomic (CAS loop on sm_100)
+      __syncthreads();
+      const int64_t b = fplane * t.nrb + rb;
+      const int32_t q0 = start[b], q1 = start[b + 1];
+      const int rowoff = (int)(rb * Rf) - sr - clo;  // tile row = r_in + rowoff
+      TileTarget T;
+      T.tp = tp;
+      T.tm = tm;
+      T.W = W;
+      T.nr = nr;
+      T.rowoff = rowoff;
+      T.col_bits = t.col_bits;
+      T.cmask = cmask;
+      T.rmask = rmask;
+      T.swz = SE > 0;
+      const int nwin = (q1 - q0 + 31) >> 5;
+      const int per = (nwin + nw - 1) / nw;
+      const int wb = warp * per, we = (t.exp & 1) ? wb : min(nwin, wb + per);
+      const int nf = factored ? t.nf[ph] : 0;
+      if (nf >= 1 && nf <= 5) {
+        AccParams P;
+        P.keys = keys;
+        for (int j = 0; j < nf; ++j) P.fp[j] = rec + (int64_t)t.fidx[ph][j] * nrec;
+        P.fq = rec + (int64_t)(1 + kcol) * nrec;
+        P.q0 = q0;
+        P.q1 = q1;
+        switch (nf) {
+          case 1: accumulate_factored<1>(T, P, wb, we, lane); break;
+          case 2: accumulate_factored<2>(T, P, wb, we, lane); break;
+          case 3: accumulate_factored<3>(T, P, wb, we, lane); break;
+          case 4: accumulate_factored<4>(T, P, wb, we, lane); break;
+          default: accumulate_factored<5>(T, P, wb, we, lane); break;
+        }
+      } else {  // raw records (or many factors): product / exp at load time
+        const unsigned negmask = t.lead_neg | (rneg ? 1u << kr : 0u);
+        RunCarry c;
+        for (int win = wb; win < we; ++win) {
+          const int32_t q = q0 + win * 32 + lane;
+          const KdeRec cur = kde_load(keys, rec, nrec, q, q < q1, factored, t.fmask[ph], 1 + kcol,
+                                      d, t.c, t.a, negmask);
+          window_reduce(T, cur.key, cur.pp, cur.pm, win == wb, c, lane);
+        }
+        if (c.key != 0xFFFFFFFFu && lane == 0) tile_put(T, c.key, c.p, c.m, true);
+      }
+      __syncthreads();
+      double *g = plane_out + (int64_t)clo * W;
+      if (t.exp & 2) {
+      } else if constexpr (SE > 0) {
+        kde_tiles_walk<SE>(tp, tm, cp, cm, seg, seg + nw * W, nr, rneg, zr + clo, t.zcp, t.zcm, g,
+                           ph);
+      } else {
+        tile_scan<double>(tp, nr, W, rneg, false, cp, seg);
+        tile_scan<double>(tm, nr, W, rneg, true, cm, seg);
+        // weight by the in-plane factors and write / accumulate this block's rows of the plane
+        for (int i = threadIdx.x; i < nr * W; i += blockDim.x) {
+          const int r = i / W, c = i - r * W;
+          double v = __ldg(zr + clo + r) * (zc[2 * c] * tp[i] + zc[2 * c + 1] * tm[i]);
+          if (ph > 0) v += g[i];
+          g[i] = v;
+        }
+        __syncthreads();
       }
     }
-    __syncthreads();
-    tile_scan_any<double, SE>(tile, nr, W, rev_r, rev_c, carry, seg);
-    tile_store<double>(gtile, tile, (int64_t)nr * W);
-    __syncthreads();
   }
 }
 
-// gather the sorted records the KDE terms stream: the in-plane full-space offset packed as
-// 16-bit (row, col), and either
-//   factored (f != 0): rec[q] = (A, q_0..q_{d-1}) with A = w e^{sum_k u_k}, q_k = e^{-2 u_k},
-//                      u_k = (x_k - c_k) / h_k, so term psi = A * prod_{k: delta_k=-1} q_k;
-//   raw:               rec[q] = (x_0..x_{d-1}, w) and psi = w e^{sum_k delta_k u_k} per term.
+// gather the sorted records the KDE groups stream, field-major (rec[f * n + q], so a warp's
+// loads of one field are coalesced and a phase loads only the fields it multiplies):
+//   factored (f != 0): fields (A, q_0..q_{d-1}) with A = w e^{sum_k u_k}, q_k = e^{-2 u_k},
+//                      u_k = (x_k - c_k) / h_k, so a term's psi = A * prod_{k: delta_k=-1} q_k;
+//   raw:               fields (x_0..x_{d-1}, w) and psi = w e^{sum_k delta_k u_k}.
 // The factored form is used only when sum_k max|u_k| <= 600, which keeps every partial
 // product inside e^{+-600} (fp64 overflows past e^709).
 __global__ void kde_materialize_kernel(const double *__restrict__ x, const double *__restrict__ w,
                                        int64_t n, int d, const int32_t *__restrict__ order,
-                                       const double *__restrict__ knots, BinGrid g, PsiParams pp,
-                                       int factored, double *__restrict__ rec,
-                                       uint32_t *__restrict__ loc) {
-  extern __shared__ double s_knots[];
-  __shared__ double s_z0[FCG_MAX_DIM], s_idz[FCG_MAX_DIM];
-  const double *kb = stage_knots(g, knots, s_knots, s_z0, s_idz);
-  __syncthreads();
-  const int kr = d - 2, kc = d - 1;
+                                       PsiParams pp, int factored, double *__restrict__ rec) {
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
        q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = order[q];
     const double wi = w ? w[i] : 1.0;
-    double *r = rec + q * (d + 1);
     if (factored) {
       double su = 0.0;
       for (int k = 0; k < d; ++k) {
         const double u = (x[i * d + k] - pp.c[k]) * pp.a[k];  // a_k = 1 / h_k
         su += u;
-        r[1 + k] = exp(-2.0 * u);
+        rec[(int64_t)(1 + k) * n + q] = exp(-2.0 * u);
       }
-      r[0] = wi * exp(su);
+      rec[q] = wi * exp(su);
     } else {
-      for (int k = 0; k < d; ++k) r[k] = x[i * d + k];
-      r[d] = wi;
+      for (int k = 0; k < d; ++k) rec[(int64_t)k * n + q] = x[i * d + k];
+      rec[(int64_t)d * n + q] = wi;
     }
-    const int br = knot_count(x[i * d + kr], kb + g.koff[kr], (int)g.m[kr], 0, s_z0[kr], s_idz[kr]);
-    const int bc = knot_count(x[i * d + kc], kb + g.koff[kc], (int)g.m[kc], 0, s_z0[kc], s_idz[kc]);
-    loc[q] = ((uint32_t)br << 16) | (uint32_t)bc;
   }
 }
 
@@ -499,7 +868,8 @@ struct MultiFinal {
   double *plane[kMaxGroup];   // slab carry capture per term (or null)
   int64_t zoff[FCG_MAX_DIM];
   int64_t dims[FCG_MAX_DIM];
-  int64_t plane_idx;          // axis-1 index captured (-1: none)
+  int64_t plane_idx[kMaxGroup];  // axis-1 index each member captures (-1: none)
+  int kz;                     // zf applies on axes k < kz (the in-plane factors are folded in)
   int accumulate, apply_scale;
   double scale;
   double *out;
@@ -521,12 +891,16 @@ __global__ void __launch_bounds__(256) kde_final_multi(MultiFinal f) {
       for (int k = f.d - 1; k >= 1; --k) {
         const int64_t i = rem % f.dims[k];
         rem /= f.dims[k];
+        if (k >= f.kz) continue;
 #pragma unroll
         for (int t = 0; t < NT; ++t)
           if (t < f.nt) zo[t] *= f.zf[t][f.zoff[k] + i];
       }
     }
-    const int64_t cap = (f.plane_idx >= 0 && b / B1 == f.plane_idx) ? b % B1 : -1;
+    int64_t cap[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+      cap[t] = (t < f.nt && f.plane_idx[t] >= 0 && b / B1 == f.plane_idx[t]) ? b % B1 : -1;
     double carry[NT];
 #pragma unroll
     for (int t = 0; t < NT; ++t) carry[t] = 0.0;
@@ -553,7 +927,7 @@ __global__ void __launch_bounds__(256) kde_final_multi(MultiFinal f) {
           if (t < f.nt) {
             carry[t] += v[u][t];
             val += (zo[t] * f.zf[t][f.zoff[0] + j]) * carry[t];
-            if (cap >= 0) f.plane[t][j * B1 + cap] = carry[t];
+            if (cap[t] >= 0) f.plane[t][j * B1 + cap[t]] = carry[t];
           }
         }
         double r = o[u] + val;
@@ -588,6 +962,13 @@ int64_t seg_rows(int threads, int64_t W, int V) {
   int64_t g1 = threads >= W ? threads / W : 1;
   int64_t g2 = threads * V >= W ? threads * V / W : 1;
   return g1 > g2 ? g1 : g2;
+}
+
+// plane_kde_group_kernel: two tiles, two carry rows, the column factor pairs, segment totals
+// (vectorised walk: [2][warps][W]; generic scan: G rows)
+size_t kde_group_smem(int64_t Rf, int64_t W, int64_t G) {
+  const int64_t segs = std::max<int64_t>(G, 2 * (kKdeThreads / 32));
+  return (size_t)(2 * Rf * W + 2 * W + 2 * W + segs * W) * sizeof(double);
 }
 
 int bits_for(int64_t v) {  // smallest b with v < 2^b
@@ -637,7 +1018,8 @@ int partition(const double *x, int64_t n, int d, const double *knots, const BinG
   FCG_TRY(launch_part_bin(x, n, d, knots, g, p, b.keys, b.vals, st));
   FCG_TRY(radix_sort_pairs<uint32_t>(b.keys, b.vals, n, 0, ((nbits + 7) / 8) * 8, b.rw, st));
   FCG_PROF("part_bucket_start", st);
-  bucket_start_kernel<<<grid_for(NB + 1, 256, 4), 256, 0, st>>>(b.keys, n, NB, b.start);
+  bucket_start_kernel<<<grid_for(NB + 1, 256, 4), 256, 0, st>>>(b.keys, n, NB, p.cell_bits,
+                                                                 b.start);
   FCG_LAUNCH_CHECK();
   return FCG_OK;
 }
@@ -725,7 +1107,7 @@ PartPlan plan_kde_partition(int d, const int64_t *m, int64_t n) {
   int64_t nrb = 1, Rf = Hf;
   while (true) {
     Rf = ceil_div(Hf, nrb);
-    const size_t bytes = (size_t)(Rf * pl.W + pl.W + G * pl.W) * sizeof(double);
+    const size_t bytes = kde_group_smem(Rf, pl.W, G);
     if (bytes <= kKdeTileBytes) break;
     if (Rf == 1) return pl;
     ++nrb;
@@ -741,7 +1123,12 @@ PartPlan plan_kde_partition(int d, const int64_t *m, int64_t n) {
   pl.nrb = nrb;
   pl.NB = np_full * nrb;
   if (pl.NB >= (int64_t(1) << 31) - 2 || n >= (int64_t(1) << 31) - 1) return pl;
-  pl.nbits = bits_for(pl.NB);
+  // records sorted by full cell: key = bucket << cell_bits | r_in << col_bits | col (< 2^31,
+  // so the dead key 0xFFFFFFFF sorts last)
+  pl.col_bits = bits_for(pl.W);      // full-space columns 0..W
+  pl.cell_bits = pl.col_bits + bits_for(Rf - 1);
+  pl.nbits = bits_for(pl.NB - 1) + pl.cell_bits;
+  if (pl.nbits > 31) return pl;
   pl.ok = true;
   return pl;
 }
@@ -753,7 +1140,6 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   PartBufs b;
   carve_part(W, b, n, pl.NB);
   double *rec = W.take<double>((size_t)n * (d + 1));
-  uint32_t *loc = W.take<uint32_t>(n);
   LatShape s;
   s.d = d;
   int64_t total_knots = 0;
@@ -761,12 +1147,17 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
     s.dims[k] = m[k];
     total_knots += m[k];
   }
-  // terms are processed in groups sharing (delta_0, delta_1); one lattice + zf table per member
-  const int ntg = 1 << (d - 2);
-  const int nbatch = ntg < kMaxGroup ? ntg : kMaxGroup;
+  // Terms are folded in groups sharing the signs of axes k < kz (see plane_kde_group_kernel):
+  // kz = d - 2 folds all four in-plane sign pairs; with slab planes requested the folded axes
+  // must all be >= 2 (the slab axis 1 factor has to stay outside the captured plane), so d = 3
+  // then folds only the column axis.  Groups sharing delta_0 share one final axis-0 pass.
+  const int kz = planes ? kde_cap_kw(d) : d - 2;
+  const int ngroups = 1 << kz;
+  const int per0 = ngroups / 2;  // groups per delta_0 sign
+  const int nbatch = per0 < kMaxGroup ? per0 : kMaxGroup;
   double *lats = W.take<double>((size_t)s.size() * nbatch);
   double *scratch = W.take<double>(scan_scratch_bound());
-  double *zfs = W.take<double>((size_t)total_knots * nbatch);
+  double *zfs = W.take<double>((size_t)total_knots * (nbatch + 2));
   if (!run) return FCG_OK;
 
   // one delta=+1 binning in the full (M+1)^d space serves every term (fastsum.py:146-149)
@@ -789,6 +1180,8 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   p.R = pl.R;
   p.nrb = pl.nrb;
   p.ecdf = 0;
+  p.cell_bits = pl.cell_bits;
+  p.col_bits = pl.col_bits;
   FCG_TRY(partition(x, n, d, knots, g, p, pl.NB, pl.nbits, b, st));
   // factored psi records when every partial product stays inside e^{+-600}: needs
   // sum_k max|u_k| <= 600 with u_k = (x_k - c_k)/h_k; bounded here by the hull of the knots
@@ -800,10 +1193,9 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   }
   int factored = bound_u_sum <= 600.0 ? 1 : 0;
   {
-    const size_t smem = g.total_knots <= kSmemKnots ? (size_t)g.total_knots * sizeof(double) : 0;
     FCG_PROF("kde_materialize", st);
-    kde_materialize_kernel<<<grid_for(n, 256, 8), 256, smem, st>>>(x, w, n, d, b.vals, knots, g, pp,
-                                                                  factored, rec, loc);
+    kde_materialize_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(x, w, n, d, b.vals, pp, factored,
+                                                               rec);
     FCG_LAUNCH_CHECK();
   }
   double prod_h = 1.0;
@@ -812,10 +1204,13 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   const int64_t G = seg_rows(kKdeThreads, pl.W, 2);
   int64_t plane_sz = m[0];
   for (int k = 2; k < d; ++k) plane_sz *= m[k];
-  const size_t smem = (size_t)(pl.R * pl.W + pl.W + G * pl.W) * sizeof(double);
+  if (planes)  // slots of codes that are folded into a lower code stay zero
+    FCG_CUDA_TRY(cudaMemsetAsync(planes, 0, (size_t)plane_sz * (size_t(1) << d) * sizeof(double), st));
+  const size_t smem = kde_group_smem(pl.R, pl.W, G);
   const int se = scan_variant(pl.W, 2);
-  auto kde_kern = se == 2 ? plane_kde_kernel<2>
-                          : (se == 4 ? plane_kde_kernel<4> : (se == 8 ? plane_kde_kernel<8> : plane_kde_kernel<0>));
+  auto kde_kern = se == 2 ? plane_kde_group_kernel<2>
+                          : (se == 4 ? plane_kde_group_kernel<4>
+                                     : (se == 8 ? plane_kde_group_kernel<8> : plane_kde_group_kernel<0>));
   FCG_CUDA_TRY(cudaFuncSetAttribute(kde_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t L = s.size();
   int64_t zoff[FCG_MAX_DIM];
@@ -826,52 +1221,70 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
       off += m[k];
     }
   }
-  for (int grp = 0; grp < 4; ++grp) {
-    for (int b0 = 0; b0 < ntg; b0 += nbatch) {
-      const int nt = (ntg - b0) < nbatch ? (ntg - b0) : nbatch;
+  // factor tables of the all-(+1) and all-(-1) sign vectors: the in-plane factors of any term
+  double *zpos = zfs + (size_t)nbatch * total_knots, *zneg = zpos + total_knots;
+  FCG_TRY(launch_kde_zf(knots, d, m, centre, h, 0, zpos, st));
+  FCG_TRY(launch_kde_zf(knots, d, m, centre, h, (1 << d) - 1, zneg, st));
+  const int kr = d - 2, kc = d - 1;
+  for (int s0 = 0; s0 < 2; ++s0) {
+    for (int b0 = 0; b0 < per0; b0 += nbatch) {
+      const int nt = (per0 - b0) < nbatch ? (per0 - b0) : nbatch;
       MultiFinal f{};
       f.nt = nt;
       f.d = d;
+      f.kz = kz;
       for (int k = 0; k < d; ++k) {
         f.zoff[k] = zoff[k];
         f.dims[k] = m[k];
       }
-      const bool rev0 = grp & 1, rev1 = (grp >> 1) & 1;
-      f.plane_idx = planes ? (rev1 ? 0 : m[1] - 1) : -1;
       for (int tt = 0; tt < nt; ++tt) {
-        const int code = grp | ((b0 + tt) << 2);
+        const int gl = s0 | ((b0 + tt) << 1);  // signs of axes < kz (bit k: delta_k = -1)
         double *lat = lats + (size_t)tt * L;
         double *zf = zfs + (size_t)tt * total_knots;
-        KdeTerm t{};
+        KdeGroup t{};
         t.d = d;
         bool rev[FCG_MAX_DIM];
-        int64_t sh[FCG_MAX_DIM];
         for (int k = 0; k < d; ++k) {
-          const double sgn = ((code >> k) & 1) ? -1.0 : 1.0;
-          rev[k] = sgn < 0;
-          sh[k] = sgn < 0 ? 1 : 0;
+          rev[k] = k < kz && ((gl >> k) & 1);
           t.c[k] = centre[k];
-          t.a[k] = sgn / h[k];
+          t.a[k] = 1.0 / h[k];
         }
-        t.Mr = m[d - 2];
-        t.Mc = m[d - 1];
-        t.sr = sh[d - 2];
-        t.sc = sh[d - 1];
+        t.Mr = m[kr];
+        t.Mc = m[kc];
         t.Rf = pl.R;
         t.nrb = pl.nrb;
-        for (int k = 0; k < d - 2; ++k) {
+        t.lead_neg = 0;
+        for (int k = 0; k < kr; ++k) {
           t.lead_m[k] = m[k];
-          t.lead_s[k] = sh[k];
+          t.lead_s[k] = rev[k] ? 1 : 0;
           t.lead_full[k] = m[k] + 1;
+          if (rev[k]) t.lead_neg |= 1u << k;
         }
-        FCG_TRY(launch_kde_zf(knots, d, m, centre, h, code, zf, st));
+        if (kz > kr) {  // row sign fixed by the group
+          t.nphase = 1;
+          t.rneg[0] = rev[kr] ? 1 : 0;
+        } else {
+          t.nphase = 2;
+          t.rneg[0] = 0;
+          t.rneg[1] = 1;
+        }
+        for (int ph = 0; ph < t.nphase; ++ph) {
+          t.zr[ph] = (t.rneg[ph] ? zneg : zpos) + zoff[kr];
+          t.fmask[ph] = 1u | (t.lead_neg << 1) | (t.rneg[ph] ? 1u << (1 + kr) : 0u);
+          t.nf[ph] = 0;
+          for (int f = 0; f <= d; ++f)
+            if ((t.fmask[ph] >> f) & 1) t.fidx[ph][t.nf[ph]++] = f;
+        }
+        t.zcp = zpos + zoff[kc];
+        t.zcm = zneg + zoff[kc];
+        t.cell_bits = pl.cell_bits;
+        t.col_bits = pl.col_bits;
+        t.exp = getenv("FCG_KDE_EXP") ? atoi(getenv("FCG_KDE_EXP")) : 0;
+        FCG_TRY(launch_kde_zf(knots, d, m, centre, h, gl, zf, st));
         {
           FCG_PROF("plane_kde", st);
-          unsigned negmask = 0;
-          for (int k = 0; k < d; ++k)
-            if (rev[k]) negmask |= 1u << k;
-          kde_kern<<<(unsigned)pl.NP, kKdeThreads, smem, st>>>(
-              t, b.start, rec, loc, factored, negmask, rev[d - 2], rev[d - 1], lat);
+          kde_kern<<<(unsigned)pl.NP, kKdeThreads, smem, st>>>(t, b.start, rec, n, b.keys,
+                                                               factored, lat);
           FCG_LAUNCH_CHECK();
         }
         Epi inplace;
@@ -879,13 +1292,14 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
           FCG_TRY(scan_axis<double>(lat, s, ax, rev[ax], inplace, scratch, st));
         f.lat[tt] = lat;
         f.zf[tt] = zf;
-        f.plane[tt] = planes ? planes + (int64_t)code * plane_sz : nullptr;
+        f.plane[tt] = planes ? planes + (int64_t)gl * plane_sz : nullptr;
+        f.plane_idx[tt] = planes ? (rev[1] ? 0 : m[1] - 1) : -1;
       }
-      f.accumulate = (grp > 0 || b0 > 0) ? 1 : 0;
-      f.apply_scale = (grp == 3 && b0 + nt >= ntg) ? 1 : 0;
+      f.accumulate = (s0 > 0 || b0 > 0) ? 1 : 0;
+      f.apply_scale = (s0 == 1 && b0 + nt >= per0) ? 1 : 0;
       f.scale = scale;
       f.out = out;
-      FCG_TRY(launch_final_multi(f, rev0, st));
+      FCG_TRY(launch_final_multi(f, s0 == 1, st));
     }
   }
   return FCG_OK;

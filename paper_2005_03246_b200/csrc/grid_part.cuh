@@ -18,6 +18,8 @@ struct PartPlan {
   int64_t nrb = 0;  // row blocks per plane
   int64_t NB = 0;   // buckets
   int nbits = 0;    // radix key bits
+  int cell_bits = 0;  // KDE: in-bucket cell bits of the sorted key (0: bucket-only keys)
+  int col_bits = 0;
 };
 
 // Unit-weight ECDF / ESF over the cell-space lattice `g` (dims = output extents).
@@ -26,6 +28,11 @@ PartPlan plan_ecdf_partition(const BinGrid &g, int64_t n);
 int ecdf_partitioned(const double *x, int64_t n, const double *knots, const BinGrid &g,
                      const bool *rev, const PartPlan &plan, const Epi &epi, Workspace &W,
                      bool run, cudaStream_t st);
+
+// Slab carry planes of the KDE: a captured plane is weighted by the factors zf_k of the axes
+// k >= kde_cap_kw(d) (the in-plane axes the partitioned path folds, never the slab axis 1);
+// the carry fix-up applies the factors of the axes below it.
+inline int kde_cap_kw(int d) { return d - 2 > 2 ? d - 2 : 2; }
 
 // Laplacian KDE: full-space binning (dims M_k + 1) shared by all 2^d terms.
 PartPlan plan_kde_partition(int d, const int64_t *m, int64_t n);

@@ -75,10 +75,19 @@ __global__ void __launch_bounds__(256) lines_kernel(T *__restrict__ lat, int64_t
     // slab carry capture: this line lies in the requested axis-1 plane (axis-0 pass, d >= 2)
     double *pcap = nullptr;
     int64_t pB1 = 0;
+    double pw = 1.0;
     if constexpr (EK == EPI_KDE) {
       if (e.plane_out && e.ax == 0 && e.d >= 2) {
         pB1 = B / e.dims[1];
-        if (b / pB1 == e.plane_idx) pcap = e.plane_out + (b % pB1);
+        if (b / pB1 == e.plane_idx) {
+          pcap = e.plane_out + (b % pB1);
+          int64_t r = b;  // capture weight: zf of the axes >= cap_kw (b spans axes 1..d-1)
+          for (int k = e.d - 1; k >= 1; --k) {
+            const int64_t i = r % e.dims[k];
+            r /= e.dims[k];
+            if (k >= e.cap_kw) pw *= e.zf[e.zoff[k] + i];
+          }
+        }
       }
     }
     int64_t jj = j0;
@@ -103,7 +112,7 @@ __global__ void __launch_bounds__(256) lines_kernel(T *__restrict__ lat, int64_t
           if (e.accumulate) r = ov[u] + r;
           if (e.apply_scale) r = r * e.scale;
           static_cast<double *>(e.out)[a * D * B + j * B + b] = r;
-          if (pcap) pcap[j * pB1] = (double)carry;
+          if (pcap) pcap[j * pB1] = pw * (double)carry;
         } else {
           emit<T, EK>(lat, e, a * D * B + j * B + b, j, zo, carry);
         }
@@ -114,7 +123,7 @@ __global__ void __launch_bounds__(256) lines_kernel(T *__restrict__ lat, int64_t
       carry += base[j * B];
       emit<T, EK>(lat, e, a * D * B + j * B + b, j, zo, carry);
       if constexpr (EK == EPI_KDE)
-        if (pcap) pcap[j * pB1] = (double)carry;
+        if (pcap) pcap[j * pB1] = pw * (double)carry;
     }
   }
 }

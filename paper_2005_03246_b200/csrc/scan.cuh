@@ -34,9 +34,11 @@ struct Epi {
   int apply_scale = 0;
   double scale = 1.0;
   // optional side output (axis-0 pass only): the S values of the axis-1 plane plane_idx,
-  // stored as plane_out[i0 * (dims[2] * ... * dims[d-1]) + rest] (slab carry exchange)
+  // weighted by zf_k(i_k) of the axes k >= cap_kw, stored as
+  // plane_out[i0 * (dims[2] * ... * dims[d-1]) + rest] (slab carry exchange)
   double *plane_out = nullptr;
   int64_t plane_idx = -1;
+  int cap_kw = FCG_MAX_DIM;
 };
 
 struct LatShape {

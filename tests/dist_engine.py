@@ -58,10 +58,18 @@ class OracleEngine:
         pts = x.numpy().reshape(-1, grid.dim)
         out, terms, _ = oracle.kde_fastsum_laplacian_terms(
             pts, None if w is None else w.numpy(), grid.knots, h, centre, n_scale)
+        d = grid.dim
+        kw = max(2, d - 2)  # slot weights: zf of axes >= kw (fastcdf_b200.h)
+        knots = [np.asarray(z, dtype=np.float64) for z in grid.knots]
         planes = []
         for code, (_, s0) in enumerate(terms):
             rev = (code >> 1) & 1
             p = s0[:, 0] if rev else s0[:, -1]
+            for k in range(kw, d):
+                sgn = -1.0 if (code >> k) & 1 else 1.0
+                sh = [1] * (d - 1)
+                sh[k - 1] = len(knots[k])
+                p = p * np.exp(-sgn * (knots[k] - centre[k]) / h[k]).reshape(sh)
             planes.append(np.ascontiguousarray(p).reshape(-1))
         return torch.as_tensor(out), torch.as_tensor(np.concatenate(planes))
 
@@ -76,7 +84,7 @@ class OracleEngine:
         for code in range(1 << d):
             signs = [-1.0 if (code >> k) & 1 else 1.0 for k in range(d)]
             zfac = np.ones(shape)
-            for k in range(d):
+            for k in range(min(d, max(2, d - 2))):
                 sh = [1] * d
                 sh[k] = shape[k]
                 zfac = zfac * np.exp(-signs[k] * (knots[k] - centre[k]) / h[k]).reshape(sh)
