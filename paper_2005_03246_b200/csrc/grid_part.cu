@@ -387,7 +387,7 @@ struct KdeGroup {
   int nphase;                        // 1: row sign fixed (rneg[0]); 2: both row signs
   int rneg[2];
   double c[FCG_MAX_DIM], a[FCG_MAX_DIM];  // raw records: centre and 1/h
-  const double *zr[2];               // row-axis factor table of each phase (cell index)
+  const double *zr[2];               // row-axis factor table of each phase (null: factor 1)
   const double *zcp, *zcm;           // column-axis factor tables, delta_c = +1 / -1
   int cell_bits, col_bits;           // sorted key layout: bucket << cell_bits | r_in << col_bits | col
   unsigned fmask[2];                 // factored record fields multiplied into psi per phase
@@ -645,7 +645,7 @@ __device__ __forceinline__ void kde_tiles_walk(double *tp, double *tm, double *c
   for (int q = q0; q < q1; ++q) {
     const int r = rneg ? nr - 1 - q : q;
     double2 *o = reinterpret_cast<double2 *>(g + (int64_t)r * W + c0);
-    const double zrv = __ldg(zr + r);
+    const double zrv = zr ? __ldg(zr + r) : 1.0;
 #pragma unroll
     for (int j = 0; j < C; ++j) {
       double2 *a = reinterpret_cast<double2 *>(tp + r * W + pc[j]);
@@ -808,7 +808,7 @@ __global__ void __launch_bounds__(kKdeThreads, 2) plane_kde_group_kernel(
       double *g = plane_out + (int64_t)clo * W;
       if (t.exp & 2) {
       } else if constexpr (SE > 0) {
-        kde_tiles_walk<SE>(tp, tm, cp, cm, seg, seg + nw * W, nr, rneg, zr + clo, t.zcp, t.zcm, g,
+        kde_tiles_walk<SE>(tp, tm, cp, cm, seg, seg + nw * W, nr, rneg, zr ? zr + clo : nullptr, t.zcp, t.zcm, g,
                            ph);
       } else {
         tile_scan<double>(tp, nr, W, rneg, false, cp, seg);
@@ -816,7 +816,7 @@ __global__ void __launch_bounds__(kKdeThreads, 2) plane_kde_group_kernel(
         // weight by the in-plane factors and write / accumulate this block's rows of the plane
         for (int i = threadIdx.x; i < nr * W; i += blockDim.x) {
           const int r = i / W, c = i - r * W;
-          double v = __ldg(zr + clo + r) * (zc[2 * c] * tp[i] + zc[2 * c + 1] * tm[i]);
+          double v = (zr ? __ldg(zr + clo + r) : 1.0) * (zc[2 * c] * tp[i] + zc[2 * c + 1] * tm[i]);
           if (ph > 0) v += g[i];
           g[i] = v;
         }
@@ -1269,7 +1269,8 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
           t.rneg[1] = 1;
         }
         for (int ph = 0; ph < t.nphase; ++ph) {
-          t.zr[ph] = (t.rneg[ph] ? zneg : zpos) + zoff[kr];
+          // a row sign fixed by the group leaves the row factor to the final pass (k < kz)
+          t.zr[ph] = kz > kr ? nullptr : (t.rneg[ph] ? zneg : zpos) + zoff[kr];
           t.fmask[ph] = 1u | (t.lead_neg << 1) | (t.rneg[ph] ? 1u << (1 + kr) : 0u);
           t.nf[ph] = 0;
           for (int f = 0; f <= d; ++f)
