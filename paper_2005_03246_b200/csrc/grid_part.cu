@@ -6,6 +6,7 @@
 // bucket's records contiguously, accumulates in shared memory and writes its plane once, with
 // the two in-plane scan passes (Algorithm 1's sweeps along axes d-2, d-1) fused in.
 #include "grid_part.cuh"
+#include "partition.cuh"
 #include "sort.cuh"
 
 namespace fcg {
@@ -480,6 +481,13 @@ struct RawWin {
   double qc;
 };
 
+struct AccParams {
+  const uint32_t *keys;
+  const double *fp[FCG_MAX_DIM + 1];  // field arrays of the sorted records (field-major)
+  const double *fq;
+  int32_t q0, q1;
+};
+
 template <int NF>
 __device__ __forceinline__ void raw_load(RawWin<NF> &r, const uint32_t *__restrict__ keys,
                                          const double *const *fp, const double *fq, int32_t q,
@@ -490,13 +498,6 @@ __device__ __forceinline__ void raw_load(RawWin<NF> &r, const uint32_t *__restri
   for (int j = 0; j < NF; ++j) r.f[j] = fp[j][qq];
   r.qc = fq[qq];
 }
-
-struct AccParams {
-  const uint32_t *keys;
-  const double *fp[FCG_MAX_DIM + 1];
-  const double *fq;
-  int32_t q0, q1;
-};
 
 // one window: segmented run sums, carry handling, tile writes (see the comment above)
 struct RunCarry {
@@ -826,31 +827,68 @@ __global__ void __launch_bounds__(kKdeThreads, 2) plane_kde_group_kernel(
   }
 }
 
-// gather the sorted records the KDE groups stream, field-major (rec[f * n + q], so a warp's
-// loads of one field are coalesced and a phase loads only the fields it multiplies):
+// KDE records, built in the coarse partition pass (partition.cuh) from coalesced reads of x, w:
 //   factored (f != 0): fields (A, q_0..q_{d-1}) with A = w e^{sum_k u_k}, q_k = e^{-2 u_k},
 //                      u_k = (x_k - c_k) / h_k, so a term's psi = A * prod_{k: delta_k=-1} q_k;
 //   raw:               fields (x_0..x_{d-1}, w) and psi = w e^{sum_k delta_k u_k}.
 // The factored form is used only when sum_k max|u_k| <= 600, which keeps every partial
-// product inside e^{+-600} (fp64 overflows past e^709).
-__global__ void kde_materialize_kernel(const double *__restrict__ x, const double *__restrict__ w,
-                                       int64_t n, int d, const int32_t *__restrict__ order,
-                                       PsiParams pp, int factored, double *__restrict__ rec) {
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = order[q];
+// product inside e^{+-600} (fp64 overflows past e^709).  The pass groups the records by the
+// top 8 bits of the sorted key (256 coarse buckets of ~n/256 records) and writes them
+// record-major next to their keys; the full sort then only moves (key, slot) pairs and the
+// final gather reads each coarse bucket from L2 (sorted order walks the buckets in turn)
+// instead of paying a DRAM line per random record.
+struct KdeBuild {
+  const double *x, *w;
+  int d, factored;
+  PsiParams pp;
+  __device__ __forceinline__ void operator()(int64_t i, double *r) const {
     const double wi = w ? w[i] : 1.0;
     if (factored) {
       double su = 0.0;
       for (int k = 0; k < d; ++k) {
         const double u = (x[i * d + k] - pp.c[k]) * pp.a[k];  // a_k = 1 / h_k
         su += u;
-        rec[(int64_t)(1 + k) * n + q] = exp(-2.0 * u);
+        r[1 + k] = exp(-2.0 * u);
       }
-      rec[q] = wi * exp(su);
+      r[0] = wi * exp(su);
     } else {
-      for (int k = 0; k < d; ++k) rec[(int64_t)k * n + q] = x[i * d + k];
-      rec[(int64_t)d * n + q] = wi;
+      for (int k = 0; k < d; ++k) r[k] = x[i * d + k];
+      r[d] = wi;
+    }
+  }
+};
+
+// sorted records, field-major (rec[f * n + q], so a warp's loads of one field are coalesced and
+// a phase loads only the fields it multiplies), from the coarse-bucketed record-major array
+__global__ void __launch_bounds__(256) kde_gather_kernel(const double *__restrict__ rec_c,
+                                                        const int32_t *__restrict__ slot,
+                                                        int64_t n, int d,
+                                                        double *__restrict__ rec) {
+  constexpr int U = 4;  // records in flight per thread (slot loads, then all field loads)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < n; q0 += U * stride) {
+    int32_t sl[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = q0 + u * stride;
+      sl[u] = q < n ? __ldcs(slot + q) : 0;
+    }
+    double v[U][FCG_MAX_DIM + 1];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double *r = rec_c + (int64_t)sl[u] * (d + 1);
+#pragma unroll
+      for (int f = 0; f <= FCG_MAX_DIM; ++f)
+        if (f <= d) v[u][f] = r[f];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = q0 + u * stride;
+      if (q < n) {
+#pragma unroll
+        for (int f = 0; f <= FCG_MAX_DIM; ++f)
+          if (f <= d) __stcs(rec + (int64_t)f * n + q, v[u][f]);  // streaming: keep L2 for rec_c
+      }
     }
   }
 }
@@ -1008,8 +1046,10 @@ void carve_part(Workspace &W, PartBufs &b, int64_t n, int64_t NB) {
   b.vals = W.take<int32_t>(n);
   b.rw.keys_alt = reinterpret_cast<uint64_t *>(W.take<uint32_t>(n));
   b.rw.vals_alt = W.take<int32_t>(n);
-  b.rw.hist = W.take<int32_t>(radix_ws_hist_elems(n));
-  b.rw.partial = W.take<int32_t>(scan_ws_partial_elems(256 * (n / kSortTile + 1) + 2));
+  // histograms of the radix passes (4096-item tiles) and of the record partition (2048)
+  const size_t hist = std::max(radix_ws_hist_elems(n), digit_hist_elems(n));
+  b.rw.hist = W.take<int32_t>(hist);
+  b.rw.partial = W.take<int32_t>(scan_ws_partial_elems((int64_t)hist + 2));
   b.start = W.take<int32_t>(NB + 1);
 }
 
@@ -1140,6 +1180,8 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   PartBufs b;
   carve_part(W, b, n, pl.NB);
   double *rec = W.take<double>((size_t)n * (d + 1));
+  double *rec_c = W.take<double>((size_t)n * (d + 1));
+  uint32_t *keys_c = W.take<uint32_t>(n);
   LatShape s;
   s.d = d;
   int64_t total_knots = 0;
@@ -1182,7 +1224,6 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   p.ecdf = 0;
   p.cell_bits = pl.cell_bits;
   p.col_bits = pl.col_bits;
-  FCG_TRY(partition(x, n, d, knots, g, p, pl.NB, pl.nbits, b, st));
   // factored psi records when every partial product stays inside e^{+-600}: needs
   // sum_k max|u_k| <= 600 with u_k = (x_k - c_k)/h_k; bounded here by the hull of the knots
   // and the data (the caller's centre is that hull's midrange, fastsum.py:118-129)
@@ -1191,11 +1232,23 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
     pp.c[k] = centre[k];
     pp.a[k] = 1.0 / h[k];
   }
-  int factored = bound_u_sum <= 600.0 ? 1 : 0;
+  const int factored = bound_u_sum <= 600.0 ? 1 : 0;
+  // keys -> records grouped by the key's top 8 bits -> sort (key, slot) -> L2-local gather
+  const int sort_bits = ((pl.nbits + 7) / 8) * 8;
+  FCG_TRY(launch_part_bin(x, n, d, knots, g, p, b.keys, b.vals, st));
+  KdeBuild kb{x, w, d, factored, pp};
+  FCG_TRY(digit_partition_build(b.keys, n, pl.nbits > 8 ? pl.nbits - 8 : 0, d + 1, kb, rec_c, keys_c,
+                                b.vals, b.rw.hist, b.rw.partial, st));
+  FCG_TRY(radix_sort_pairs<uint32_t>(keys_c, b.vals, n, 0, sort_bits, b.rw, st));
+  {
+    FCG_PROF("part_bucket_start", st);
+    bucket_start_kernel<<<grid_for(pl.NB + 1, 256, 4), 256, 0, st>>>(keys_c, n, pl.NB, p.cell_bits,
+                                                                      b.start);
+    FCG_LAUNCH_CHECK();
+  }
   {
     FCG_PROF("kde_materialize", st);
-    kde_materialize_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(x, w, n, d, b.vals, pp, factored,
-                                                               rec);
+    kde_gather_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(rec_c, b.vals, n, d, rec);
     FCG_LAUNCH_CHECK();
   }
   double prod_h = 1.0;
@@ -1284,7 +1337,7 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
         FCG_TRY(launch_kde_zf(knots, d, m, centre, h, gl, zf, st));
         {
           FCG_PROF("plane_kde", st);
-          kde_kern<<<(unsigned)pl.NP, kKdeThreads, smem, st>>>(t, b.start, rec, n, b.keys,
+          kde_kern<<<(unsigned)pl.NP, kKdeThreads, smem, st>>>(t, b.start, rec, n, keys_c,
                                                                factored, lat);
           FCG_LAUNCH_CHECK();
         }

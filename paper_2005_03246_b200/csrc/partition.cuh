@@ -1,0 +1,164 @@
+// Stable partition of n items by one 8-bit digit of a 32-bit key that builds a record of
+// `words` doubles per item on the way (build(i, out) writes item i's record): the pass that
+// groups the items also writes their records, record-major, next to their keys and slots.
+// A tile (kPartTile items) is ranked exactly like the radix sort's scatter (match_any peers +
+// per-warp digit counters, digit-major global offsets, so items of one digit keep their input
+// order), built into shared memory in digit order, and written out with consecutive threads on
+// consecutive doubles of each digit's run.
+#pragma once
+#include "sort.cuh"
+
+namespace fcg {
+
+constexpr int kPartThreads = 256;
+constexpr int kPartItems = 8;
+constexpr int kPartTile = kPartThreads * kPartItems;  // 2048 items per CTA
+
+namespace part_detail {
+
+__device__ __forceinline__ unsigned lane_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__global__ void __launch_bounds__(kPartThreads) digit_hist_kernel(const uint32_t *__restrict__ keys,
+                                                                  int64_t n, int shift,
+                                                                  int32_t *__restrict__ hist,
+                                                                  int64_t tiles) {
+  __shared__ int32_t s_hist[kPartThreads / 32][256];
+  const int warp = threadIdx.x >> 5;
+  for (int d = threadIdx.x & 31; d < 256; d += 32) s_hist[warp][d] = 0;
+  __syncwarp();
+  const int64_t base = (int64_t)blockIdx.x * kPartTile;
+#pragma unroll 4
+  for (int j = 0; j < kPartItems; ++j) {
+    const int64_t i = base + (int64_t)j * kPartThreads + threadIdx.x;
+    if (i < n) atomicAdd(&s_hist[warp][(keys[i] >> shift) & 0xFFu], 1);
+  }
+  __syncthreads();
+  int32_t tot = 0;
+#pragma unroll
+  for (int w = 0; w < kPartThreads / 32; ++w) tot += s_hist[w][threadIdx.x];
+  hist[(int64_t)threadIdx.x * tiles + blockIdx.x] = tot;
+}
+
+template <class Build>
+__global__ void __launch_bounds__(kPartThreads) digit_stage_kernel(
+    const uint32_t *__restrict__ keys, int64_t n, int shift, const int32_t *__restrict__ offs,
+    int64_t tiles, int words, Build build, double *__restrict__ rec_out,
+    uint32_t *__restrict__ keys_out, int32_t *__restrict__ slot_out) {
+  extern __shared__ __align__(16) unsigned char ps_smem[];
+  double *s_rec = reinterpret_cast<double *>(ps_smem);                       // [tile][words]
+  uint32_t *s_key = reinterpret_cast<uint32_t *>(s_rec + (size_t)kPartTile * words);
+  int32_t *s_cnt = reinterpret_cast<int32_t *>(s_key + kPartTile);            // [8][256]
+  int32_t *s_goff = s_cnt + (kPartThreads / 32) * 256;
+  int32_t *s_tstart = s_goff + 256;
+  int32_t *s_wsum = s_tstart + 256;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int d = lane; d < 256; d += 32) s_cnt[warp * 256 + d] = 0;
+  s_goff[threadIdx.x] = offs[(int64_t)threadIdx.x * tiles + blockIdx.x];
+  __syncwarp();
+  const int64_t tile0 = (int64_t)blockIdx.x * kPartTile;
+  const int64_t base = tile0 + (int64_t)warp * (kPartTile / 8);
+  const int tile_n = (int)((n - tile0) < kPartTile ? (n - tile0) : kPartTile);
+  uint32_t k[kPartItems];
+  int32_t r[kPartItems];
+  const unsigned lt = lane_lt();
+#pragma unroll
+  for (int j = 0; j < kPartItems; ++j) {
+    const int64_t i = base + (int64_t)j * 32 + lane;
+    const bool ok = i < n;
+    k[j] = ok ? keys[i] : 0u;
+    const unsigned dig = ok ? ((k[j] >> shift) & 0xFFu) : 256u + lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, dig);
+    int32_t before = 0;
+    if (ok) before = s_cnt[warp * 256 + dig];
+    __syncwarp();
+    if (ok && lane == __ffs(peers) - 1) s_cnt[warp * 256 + dig] = before + __popc(peers);
+    __syncwarp();
+    r[j] = before + __popc(peers & lt);
+  }
+  __syncthreads();
+  {
+    const int d = threadIdx.x;
+    int32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kPartThreads / 32; ++w) {
+      const int32_t t = s_cnt[w * 256 + d];
+      s_cnt[w * 256 + d] = run;
+      run += t;
+    }
+    int32_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[warp] = x;
+    __syncthreads();
+    int32_t wpre = 0;
+    for (int w = 0; w < warp; ++w) wpre += s_wsum[w];
+    s_tstart[d] = wpre + x - run;
+  }
+  __syncthreads();
+  for (int j = 0; j < kPartItems; ++j) {
+    const int64_t i = base + (int64_t)j * 32 + lane;
+    if (i < n) {
+      const unsigned dig = (k[j] >> shift) & 0xFFu;
+      const int pos = s_tstart[dig] + s_cnt[warp * 256 + dig] + r[j];
+      s_key[pos] = k[j];
+      build(i, s_rec + (size_t)pos * words);
+    }
+  }
+  __syncthreads();
+  for (int pos = threadIdx.x; pos < tile_n; pos += kPartThreads) {
+    const uint32_t key = s_key[pos];
+    const unsigned dig = (key >> shift) & 0xFFu;
+    const int64_t dst = (int64_t)s_goff[dig] + (pos - s_tstart[dig]);
+    keys_out[dst] = key;
+    slot_out[dst] = (int32_t)dst;
+  }
+  const int tw = tile_n * words;
+  for (int idx = threadIdx.x; idx < tw; idx += kPartThreads) {
+    const int pos = idx / words;
+    const unsigned dig = (s_key[pos] >> shift) & 0xFFu;
+    const int64_t dst = (int64_t)s_goff[dig] + (pos - s_tstart[dig]);
+    rec_out[dst * words + (idx - pos * words)] = s_rec[idx];
+  }
+}
+
+}  // namespace part_detail
+
+inline size_t digit_stage_smem(int words) {
+  return (size_t)kPartTile * (words * sizeof(double) + sizeof(uint32_t)) +
+         ((kPartThreads / 32) * 256 + 256 + 256 + 8) * sizeof(int32_t);
+}
+
+inline size_t digit_hist_elems(int64_t n) { return (size_t)256 * (size_t)ceil_div(n, kPartTile) + 1; }
+
+// Workspace: hist = digit_hist_elems(n) ints, partial = scan_ws_partial_elems(hist elems).
+template <class Build>
+int digit_partition_build(const uint32_t *keys, int64_t n, int shift, int words, const Build &build,
+                          double *rec_out, uint32_t *keys_out, int32_t *slot_out, int32_t *hist,
+                          int32_t *partial, cudaStream_t st) {
+  if (n <= 0) return FCG_OK;
+  const int64_t tiles = ceil_div(n, kPartTile);
+  {
+    FCG_PROF("part_hist", st);
+    part_detail::digit_hist_kernel<<<(unsigned)tiles, kPartThreads, 0, st>>>(keys, n, shift, hist,
+                                                                            tiles);
+    FCG_LAUNCH_CHECK();
+  }
+  FCG_TRY(scan_i32(hist, hist, 256 * tiles, false, partial, st));
+  FCG_PROF("part_emit", st);
+  const size_t sm = digit_stage_smem(words);
+  FCG_CUDA_TRY(cudaFuncSetAttribute(part_detail::digit_stage_kernel<Build>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  part_detail::digit_stage_kernel<Build><<<(unsigned)tiles, kPartThreads, sm, st>>>(
+      keys, n, shift, hist, tiles, words, build, rec_out, keys_out, slot_out);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}
+
+}  // namespace fcg
