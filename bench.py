@@ -138,28 +138,36 @@ def grid_ecdf_bytes(n, d, m, unit=True):
 
 
 def grid_kde_bytes(n, d, m, unit_w):
+    """Algorithmic bytes per launch of the partitioned Laplacian KDE (d >= 3) and of the
+    per-term pipeline (smaller problems)."""
     L = int(np.prod(m))
     terms = 1 << d
-    group = 1 << (d - 2) if d >= 3 else 1
+    wb = 0 if unit_w else 8 * n
+    per0 = max(1, (1 << max(d - 2, 1)) // 2)  # group lattices per final axis-0 pass
     return {
         "lattice_zero": 8 * L,
-        "bin_scatter_psi": 8 * n * d + (0 if unit_w else 8 * n) + 16 * n,
+        "bin_scatter_psi": 8 * n * d + wb + 16 * n,
         "scan_rows": 16 * L,
         "scan_lines": 16 * L,
         # first term only writes the accumulator; the other 2^d - 1 read and write it
         "scan_lines_final": 8 * L + (8 * L + 16 * L * (terms - 1)) // terms,
         "kde_zfac": 16 * int(np.sum(m)),
         "minmax": 8 * n * d,
+        # keys + slots of every point from its coordinates
         "part_bin": 8 * n * d + 8 * n,
+        "part_hist": 4 * n,
+        # records built from x, w (coalesced) and written grouped by the key's top 8 bits
+        "part_emit": 4 * n + 8 * n * d + wb + 8 * n * (d + 1) + 8 * n,
         "radix_hist": 4 * n,
         "radix_scatter": 16 * n,
-        # sorted records: (d+1) doubles + packed offset per point; reads x, w, order
-        "kde_materialize": 8 * n * d + 8 * n + 4 * n + 8 * n * (d + 1) + 4 * n,
-        # one term: stream the sorted records, write the plane-scanned lattice once
-        "plane_kde": (8 * (d + 1) + 4) * n + 8 * L,
-        # one group of 2^(d-2) terms: read each term's lattice, accumulator RMW once
-        # (the first group only writes it)
-        "kde_final_group": group * 8 * L + (8 * L + 16 * L * 3) // 4,
+        # sorted field-major records from the grouped record-major ones
+        "kde_materialize": 4 * n + 16 * n * (d + 1),
+        # one group: per row-sign phase the keys and the fields it multiplies (on average
+        # d + 3 fields over both phases), the weighted plane lattice written once
+        "plane_kde": 8 * n + 8 * n * (d + 3) + 8 * L,
+        # one axis-0 pass over the group lattices sharing delta_0; accumulator written by the
+        # first pass, read + written by the second
+        "kde_final_group": per0 * 8 * L + (8 * L + 16 * L) // 2,
     }
 
 
@@ -170,9 +178,14 @@ def traffic_lookup(workload, kernel):
     if not p.exists():
         return None
     try:
-        return json.loads(p.read_text()).get(workload, {}).get(kernel)
+        tab = json.loads(p.read_text())
     except ValueError:
         return None
+    for wl_name in (workload, workload + "b", workload + "a"):  # cfg5 = cfg5a + cfg5b
+        v = tab.get(wl_name, {}).get(kernel)
+        if v is not None:
+            return v
+    return None
 
 
 class GridWorkload:

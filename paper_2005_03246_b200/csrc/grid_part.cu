@@ -545,7 +545,7 @@ template <int NF, int DEPTH = (NF <= 2 ? 2 : 1)>
 __device__ __forceinline__ void accumulate_factored(const TileTarget &T, const AccParams &P,
                                                     int wb, int we, int lane) {
   RunCarry c;
-  RawWin<NF> n1, n2;
+  RawWin<NF> buf[DEPTH];  // ring of windows in flight (static indices: k is unrolled)
   const double *fp[NF > 0 ? NF : 1];
 #pragma unroll
   for (int j = 0; j < NF; ++j) fp[j] = P.fp[j];
@@ -553,21 +553,22 @@ __device__ __forceinline__ void accumulate_factored(const TileTarget &T, const A
     const int32_t q = P.q0 + win * 32 + lane;
     raw_load<NF>(r, P.keys, fp, P.fq, q, q < P.q1);
   };
-  if (wb < we) ld(n1, wb);
-  if (DEPTH > 1 && wb + 1 < we) ld(n2, wb + 1);
-  for (int win = wb; win < we; ++win) {
-    const RawWin<NF> cur = n1;
-    if (DEPTH > 1) {
-      n1 = n2;
-      if (win + 2 < we) ld(n2, win + 2);
-    } else if (win + 1 < we) {
-      ld(n1, win + 1);
-    }
-    double pp = 1.0;
 #pragma unroll
-    for (int j = 0; j < NF; ++j) pp *= cur.f[j];
-    if (cur.key == 0xFFFFFFFFu) pp = 0.0;
-    window_reduce(T, cur.key, pp, pp * cur.qc, win == wb, c, lane);
+  for (int k = 0; k < DEPTH; ++k)
+    if (wb + k < we) ld(buf[k], wb + k);
+  for (int win = wb; win < we; win += DEPTH) {
+#pragma unroll
+    for (int k = 0; k < DEPTH; ++k) {
+      if (win + k < we) {  // warp-uniform
+        const RawWin<NF> cur = buf[k];
+        if (win + k + DEPTH < we) ld(buf[k], win + k + DEPTH);
+        double pp = 1.0;
+#pragma unroll
+        for (int j = 0; j < NF; ++j) pp *= cur.f[j];
+        if (cur.key == 0xFFFFFFFFu) pp = 0.0;
+        window_reduce(T, cur.key, pp, pp * cur.qc, win + k == wb, c, lane);
+      }
+    }
   }
   if (c.key != 0xFFFFFFFFu && lane == 0) tile_put(T, c.key, c.p, c.m, true);
 }

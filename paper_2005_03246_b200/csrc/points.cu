@@ -848,7 +848,7 @@ void carve(Workspace &W, PtsWs &p, int64_t n, int d, int nch, bool need_dom, boo
 
 int rank_dim(const double *x, int64_t n, int d, int k, PtsWs &p, cudaStream_t st) {
   FCG_TRY(radix_init_f64(x + k, n, d, p.k, p.v, st));
-  FCG_TRY(radix_sort_pairs(p.k, p.v, n, 0, 64, p.rw, st));
+  FCG_TRY(radix_sort_pairs_pruned(p.k, p.v, n, p.rw, st));
   FCG_CUDA_TRY(cudaMemcpyAsync(p.r[k].order, p.v, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
   return rank_outputs(p.k, p.v, n, p.r[k].pos, p.r[k].lower, p.r[k].upper, p.r[k].dense, p.heads,
                       p.start, p.rw.partial, p.ndist + k, st);
@@ -1168,7 +1168,7 @@ extern "C" int fcg_distinct(const double *x, int64_t n, int32_t d, int32_t *flag
   FCG_CUDA_TRY(cudaMemsetAsync(dflag, 0, FCG_MAX_DIM * 4, st));
   for (int kd = 0; kd < d; ++kd) {
     FCG_TRY(radix_init_f64(x + kd, n, d, k, v, st));
-    FCG_TRY(radix_sort_pairs(k, v, n, 0, 64, rw, st));
+    FCG_TRY(radix_sort_pairs_pruned(k, v, n, rw, st));
     if (n > 1) {
       FCG_PROF("pts_distinct", st);
       adjacent_equal_kernel<<<grid_for(n, 256), 256, 0, st>>>(k, n, dflag + kd);

@@ -89,6 +89,32 @@ __global__ void __launch_bounds__(kScanThreads) scan_partials_kernel(int32_t *pa
   }
 }
 
+// single CTA, whole array (small scans: one launch instead of three)
+__global__ void __launch_bounds__(kScanThreads) scan_single_kernel(const int32_t *in, int32_t *out,
+                                                                   int64_t n, int inclusive) {
+  __shared__ int32_t s_warp[32];
+  int32_t carry = 0;
+  for (int64_t b0 = 0; b0 < n; b0 += kScanTile) {
+    const int64_t base = b0 + (int64_t)threadIdx.x * kScanItems;
+    int32_t v[kScanItems];
+    int32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      v[j] = (base + j < n) ? in[base + j] : 0;
+      s += v[j];
+    }
+    int32_t tot;
+    int32_t run = block_excl_scan(s, s_warp, &tot) + carry;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      if (base + j < n) out[base + j] = inclusive ? run + v[j] : run;
+      run += v[j];
+    }
+    carry += tot;
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const int32_t *in, int32_t *out,
                                                                   int64_t n,
                                                                   const int32_t *__restrict__ partial,
@@ -272,6 +298,33 @@ __global__ void rank_scatter_kernel(const int32_t *__restrict__ order,
   }
 }
 
+// AND / OR of all keys: digits where they agree are the same for every key, so the radix
+// passes on them are identities and can be skipped.
+__global__ void key_andor_kernel(const uint64_t *__restrict__ keys, int64_t n,
+                                 unsigned long long *__restrict__ out) {
+  uint64_t a = ~0ull, o = 0ull;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+    a &= k;
+    o |= k;
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    a &= __shfl_xor_sync(0xffffffffu, a, s);
+    o |= __shfl_xor_sync(0xffffffffu, o, s);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAnd(out, (unsigned long long)a);
+    atomicOr(out + 1, (unsigned long long)o);
+  }
+}
+
+__global__ void key_andor_init(unsigned long long *out) {
+  out[0] = ~0ull;
+  out[1] = 0ull;
+}
+
 }  // namespace
 
 size_t radix_ws_hist_elems(int64_t n) { return (size_t)256 * (size_t)ceil_div(n, kSortTile) + 1; }
@@ -283,6 +336,11 @@ int scan_i32(const int32_t *in, int32_t *out, int64_t n, bool inclusive, int32_t
   if (n <= 0) return FCG_OK;
   const int64_t blocks = ceil_div(n, kScanTile);
   FCG_PROF("scan_i32", st);
+  if (blocks <= 2) {
+    scan_single_kernel<<<1, kScanThreads, 0, st>>>(in, out, n, inclusive ? 1 : 0);
+    FCG_LAUNCH_CHECK();
+    return FCG_OK;
+  }
   scan_reduce_kernel<<<(unsigned)blocks, kScanThreads, 0, st>>>(in, n, partial);
   FCG_LAUNCH_CHECK();
   scan_partials_kernel<<<1, kScanThreads, 0, st>>>(partial, blocks);
@@ -302,14 +360,16 @@ int radix_init_f64(const double *x, int64_t n, int64_t stride, uint64_t *keys, i
 }
 
 template <typename KeyT>
-int radix_sort_pairs(KeyT *keys, int32_t *vals, int64_t n, int begin_bit, int end_bit,
-                     const RadixWs &ws, cudaStream_t st) {
+static int radix_sort_digits(KeyT *keys, int32_t *vals, int64_t n, uint32_t digit_mask,
+                             const RadixWs &ws, cudaStream_t st) {
   if (n <= 1) return FCG_OK;
   const int64_t tiles = ceil_div(n, kSortTile);
   KeyT *ka = keys, *kb = reinterpret_cast<KeyT *>(ws.keys_alt);
   int32_t *va = vals, *vb = ws.vals_alt;
   int passes = 0;
-  for (int shift = begin_bit; shift < end_bit; shift += 8) {
+  for (int dg = 0; dg < (int)sizeof(KeyT); ++dg) {
+    if (!((digit_mask >> dg) & 1u)) continue;
+    const int shift = 8 * dg;
     {
       FCG_PROF("radix_hist", st);
       radix_hist_kernel<KeyT><<<(unsigned)tiles, kSortThreads, 0, st>>>(ka, n, shift, ws.hist, tiles);
@@ -334,6 +394,36 @@ int radix_sort_pairs(KeyT *keys, int32_t *vals, int64_t n, int begin_bit, int en
     FCG_CUDA_TRY(cudaMemcpyAsync(vals, va, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
   }
   return FCG_OK;
+}
+
+template <typename KeyT>
+int radix_sort_pairs(KeyT *keys, int32_t *vals, int64_t n, int begin_bit, int end_bit,
+                     const RadixWs &ws, cudaStream_t st) {
+  uint32_t mask = 0;
+  for (int shift = begin_bit; shift < end_bit; shift += 8) mask |= 1u << (shift / 8);
+  return radix_sort_digits<KeyT>(keys, vals, n, mask, ws, st);
+}
+
+int radix_sort_pairs_pruned(uint64_t *keys, int32_t *vals, int64_t n, const RadixWs &ws,
+                            cudaStream_t st) {
+  if (n <= 1) return FCG_OK;
+  // the AND / OR pair lives in the histogram buffer until the first pass overwrites it
+  unsigned long long *ao = reinterpret_cast<unsigned long long *>(ws.hist);
+  {
+    FCG_PROF("radix_prune", st);
+    key_andor_init<<<1, 1, 0, st>>>(ao);
+    FCG_LAUNCH_CHECK();
+    key_andor_kernel<<<grid_for(n, 256, 4), 256, 0, st>>>(keys, n, ao);
+    FCG_LAUNCH_CHECK();
+  }
+  unsigned long long h[2];
+  FCG_CUDA_TRY(cudaMemcpyAsync(h, ao, sizeof(h), cudaMemcpyDeviceToHost, st));
+  FCG_CUDA_TRY(cudaStreamSynchronize(st));
+  const uint64_t diff = h[0] ^ h[1];
+  uint32_t mask = 0;
+  for (int dg = 0; dg < 8; ++dg)
+    if ((diff >> (8 * dg)) & 0xFFull) mask |= 1u << dg;
+  return radix_sort_digits<uint64_t>(keys, vals, n, mask, ws, st);
 }
 
 template int radix_sort_pairs<uint64_t>(uint64_t *, int32_t *, int64_t, int, int, const RadixWs &,
@@ -389,7 +479,7 @@ extern "C" int fcg_rank_f64(const double *keys, int64_t n, int64_t stride, int32
   if (n == 0) return FCG_OK;
   cudaStream_t st = as_stream(stream);
   FCG_TRY(radix_init_f64(keys, n, stride, k, v, st));
-  FCG_TRY(radix_sort_pairs(k, v, n, 0, 64, rw, st));
+  FCG_TRY(radix_sort_pairs_pruned(k, v, n, rw, st));
   if (order)
     FCG_CUDA_TRY(cudaMemcpyAsync(order, v, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
   return rank_outputs(k, v, n, pos, lower, upper, dense, heads, start, rw.partial, nullptr, st);

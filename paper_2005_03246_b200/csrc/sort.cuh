@@ -25,6 +25,11 @@ template <typename KeyT>
 int radix_sort_pairs(KeyT *keys, int32_t *vals, int64_t n, int begin_bit, int end_bit,
                      const RadixWs &ws, cudaStream_t st);
 
+// Stable sort of 64-bit keys over the digits where they differ (one AND/OR reduction and a
+// 16-byte device-to-host read decide which 8-bit passes are identities).  Synchronises `st`.
+int radix_sort_pairs_pruned(uint64_t *keys, int32_t *vals, int64_t n, const RadixWs &ws,
+                            cudaStream_t st);
+
 // Exclusive (or inclusive) prefix sum of int32 (in and out may alias). partial: scan ws.
 int scan_i32(const int32_t *in, int32_t *out, int64_t n, bool inclusive, int32_t *partial,
              cudaStream_t st);
