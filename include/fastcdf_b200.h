@@ -109,6 +109,17 @@ int fcg_kde_grid_laplacian(const double *x, int64_t n, int32_t d, const double *
                            const double *centre, double *out,
                            void *ws, size_t *ws_bytes, void *stream);
 
+/* matern32-additive KDE on the grid through the same 2^d terms, Eq. (29): per term the d + 1
+ * channels w e and w e (x_l - c_l) are binned and swept like the Laplacian term and combined as
+ * zfac * (coef * S_0 - sum_l (delta_l / h_l) S_l), coef = 1 + sum_k delta_k (z_k - c_k) / h_k,
+ * scaled by 1 / (2^d N prod h (1 + d)).  Arguments as fcg_kde_grid_laplacian.
+ * Replaces: fastsum.py:204-233 kde_fastsum for family "matern32-additive"
+ *           (_kde_exponential_fastsum fastsum.py:139-181 with additive_matern). */
+int fcg_kde_grid_matern32(const double *x, int64_t n, int32_t d, const double *w,
+                          const double *knots, const int64_t *m, const double *h,
+                          const double *centre, double *out,
+                          void *ws, size_t *ws_bytes, void *stream);
+
 /* ---------------------------------------------------------------------------------------
  * Multi-GPU slab decomposition along axis 1 (used by paper_2005_03246_b200.distributed)
  * ------------------------------------------------------------------------------------- */

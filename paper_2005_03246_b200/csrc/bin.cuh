@@ -23,6 +23,7 @@ enum WeightKind { W_UNIT = 0, W_F64 = 1, W_PSI = 2 };
 struct PsiParams {  // psi_i = w_i * exp(sum_k (x_ik - c_k) * a_k), a_k = delta_k / h_k
   double c[FCG_MAX_DIM];
   double a[FCG_MAX_DIM];
+  int poly1;  // l + 1: psi_i also times (x_il - c_l) (matern32 channels); 0: no factor
 };
 
 // #knots < x (le = 0) or #knots <= x (le = 1) for a strictly increasing knot vector.

@@ -87,7 +87,9 @@ __global__ void __launch_bounds__(256, 4) bin_scatter_kernel(const double *__res
       for (int k = 0; k < (D > 0 ? D : FCG_MAX_DIM); ++k)
         if (k < d) s += (xi[k] - pp.c[k]) * pp.a[k];
       const double wi = w ? w[i] : 1.0;
-      atomicAdd(reinterpret_cast<double *>(lat) + flat, wi * exp(s));
+      double v = wi * exp(s);
+      if (pp.poly1 > 0) v = v * (xi[pp.poly1 - 1] - pp.c[pp.poly1 - 1]);  // w e xc_l
+      atomicAdd(reinterpret_cast<double *>(lat) + flat, v);
     }
   }
 }
@@ -485,6 +487,42 @@ static int kde_grid_impl(const double *x, int64_t n, int32_t d, const double *w,
 }
 
 namespace {
+// matern32-additive term (fastsum.py:170-178): with S_0 the sweep of w e and S_l that of
+// w e xc_l,  acc = coef * S_0 - sum_l (delta_l / h_l) S_l,  coef = 1 + sum_k delta_k zc_k / h_k,
+// out (+)= zfac * acc, times the final scale after the last term.
+struct MaternP {
+  int d;
+  int64_t dims[FCG_MAX_DIM], zoff[FCG_MAX_DIM];
+  double sgn[FCG_MAX_DIM], c[FCG_MAX_DIM], h[FCG_MAX_DIM];
+  int accumulate, apply_scale;
+  double scale;
+};
+
+__global__ void matern_combine_kernel(double *__restrict__ out, const double *__restrict__ S,
+                                      int64_t L, const double *__restrict__ zf,
+                                      const double *__restrict__ knots, MaternP p) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t idx[FCG_MAX_DIM];
+    int64_t rem = t;
+    for (int k = p.d - 1; k >= 0; --k) {
+      idx[k] = rem % p.dims[k];
+      rem /= p.dims[k];
+    }
+    double zfac = 1.0, coef = 1.0;
+    for (int k = 0; k < p.d; ++k) {
+      zfac = zfac * zf[p.zoff[k] + idx[k]];
+      coef = coef + (p.sgn[k] * (knots[p.zoff[k] + idx[k]] - p.c[k])) / p.h[k];
+    }
+    double acc = coef * S[t];
+    for (int l = 0; l < p.d; ++l) acc -= (p.sgn[l] / p.h[l]) * S[(int64_t)(l + 1) * L + t];
+    double r = zfac * acc;
+    if (p.accumulate) r = out[t] + r;
+    if (p.apply_scale) r = r * p.scale;
+    out[t] = r;
+  }
+}
+
 // out[i] += scale * sum_code zfac_code(i) * C_code[i0, i2, ..]   (slab carry fix-up)
 struct FixP {
   int d, ncodes, kw;  // zf of axes k < kw (the captured planes carry the rest)
@@ -538,6 +576,82 @@ extern "C" int fcg_kde_grid_laplacian_ex(const double *x, int64_t n, int32_t d, 
                                          void *stream) {
   return kde_grid_impl(x, n, d, w, knots, m, h, centre, n_scale, u_bound, planes, out, ws,
                        ws_bytes, stream);
+}
+
+extern "C" int fcg_kde_grid_matern32(const double *x, int64_t n, int32_t d, const double *w,
+                                     const double *knots, const int64_t *m, const double *h,
+                                     const double *centre, double *out, void *ws,
+                                     size_t *ws_bytes, void *stream) {
+  FCG_TRY(check_common(n, d, m));
+  for (int k = 0; k < d; ++k)
+    if (!(h[k] > 0.0)) return fail(FCG_EINVAL, "bandwidth must be > 0");
+  LatShape s;
+  s.d = d;
+  int64_t total_knots = 0;
+  for (int k = 0; k < d; ++k) {
+    s.dims[k] = m[k];
+    total_knots += m[k];
+  }
+  const int64_t L = s.size();
+  Workspace W(ws);
+  double *S = W.take<double>((size_t)L * (d + 1));  // S_0 .. S_d of the current term
+  double *scratch = W.take<double>((size_t)scan_scratch_elems(s));
+  double *zf = W.take<double>((size_t)total_knots);
+  if (ws == nullptr) {
+    *ws_bytes = W.bytes();
+    return FCG_OK;
+  }
+  if (L == 0) return FCG_OK;
+  cudaStream_t st = as_stream(stream);
+  // scale = 1 / (2^d n prod h), then / (1 + d)   (fastsum.py:179-181)
+  double prod_h = 1.0;
+  for (int k = 0; k < d; ++k) prod_h *= h[k];
+  double scale = 1.0 / (std::ldexp(1.0, d) * (double)n * prod_h);
+  scale /= 1.0 + d;
+  const int ncodes = 1 << d;
+  for (int code = 0; code < ncodes; ++code) {
+    int le[FCG_MAX_DIM];
+    int64_t shift[FCG_MAX_DIM];
+    bool rev[FCG_MAX_DIM];
+    PsiParams pp{};
+    MaternP mp{};
+    mp.d = d;
+    int64_t off = 0;
+    for (int k = 0; k < d; ++k) {
+      const double sgn = ((code >> k) & 1) ? -1.0 : 1.0;  // DeltaVector.from_code
+      le[k] = 0;
+      shift[k] = sgn < 0 ? 1 : 0;
+      rev[k] = sgn < 0;
+      pp.c[k] = centre[k];
+      pp.a[k] = sgn / h[k];
+      mp.dims[k] = m[k];
+      mp.zoff[k] = off;
+      off += m[k];
+      mp.sgn[k] = sgn;
+      mp.c[k] = centre[k];
+      mp.h[k] = h[k];
+    }
+    BinGrid g = make_bin_grid(d, m, le, shift, s.dims);
+    FCG_TRY(launch_kde_zf(knots, d, m, centre, h, code, zf, st));
+    Epi inplace;
+    for (int ch = 0; ch <= d; ++ch) {  // channel 0: w e; channel l: w e xc_{l-1}
+      double *lat = S + (int64_t)ch * L;
+      {
+        FCG_PROF("lattice_zero", st);
+        FCG_CUDA_TRY(cudaMemsetAsync(lat, 0, (size_t)L * sizeof(double), st));
+      }
+      pp.poly1 = ch;
+      if (n > 0) FCG_TRY(launch_bin_scatter<W_PSI>(x, n, d, w, knots, g, pp, lat, st));
+      FCG_TRY(scan_lattice<double>(lat, s, rev, inplace, scratch, st));
+    }
+    mp.accumulate = code > 0;
+    mp.apply_scale = code == ncodes - 1;
+    mp.scale = scale;
+    FCG_PROF("kde_matern_combine", st);
+    matern_combine_kernel<<<grid_for(L, 256), 256, 0, st>>>(out, S, L, zf, knots, mp);
+    FCG_LAUNCH_CHECK();
+  }
+  return FCG_OK;
 }
 
 extern "C" int fcg_kde_carry_fixup(double *out, int32_t d, const int64_t *m, const double *knots,

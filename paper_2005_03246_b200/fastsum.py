@@ -141,6 +141,21 @@ def _kde_laplacian_grid(sample: Sample, grid: RectilinearGrid, h: np.ndarray):
     return out
 
 
+def _kde_matern32_grid(sample: Sample, grid: RectilinearGrid, h: np.ndarray):
+    """matern32-additive: the Laplacian terms with d + 1 channels each (fastsum.py:139-181)."""
+    import torch
+
+    c, _ = _exp_guard_and_center(sample, grid, h)
+    x = _lib.to_device_f64(sample.points)
+    n, d = x.shape
+    w = None if sample.unit_weights else _lib.to_device_f64(sample.weights)
+    kn = _lib.device_knots(grid)
+    out = torch.empty(grid.size, dtype=torch.float64, device=x.device)
+    _lib.call_ws("fcg_kde_grid_matern32", _lib.ptr(x), n, d, _lib.ptr(w), _lib.ptr(kn),
+                 _lib.i64_array(grid.shape), _lib.f64_array(h), _lib.f64_array(c), _lib.ptr(out))
+    return out
+
+
 def _kde_uniform_grid(sample: Sample, grid: RectilinearGrid, h: np.ndarray):
     """Uniform kernel as 2^d shifted-grid generalized ECDFs with parity signs
     (fastsum.py:185-201, Eq. 15)."""
@@ -173,8 +188,7 @@ def kde_fastsum(sample: Sample, grid: RectilinearGrid, kernel: KernelSpec,
     elif fam == "uniform":
         vals = _kde_uniform_grid(sample, grid, h)
     elif fam == "matern32-additive":
-        raise ParameterError("matern32-additive is not implemented on the B200 path yet "
-                             "(SURVEY §8f #1)")
+        vals = _kde_matern32_grid(sample, grid, h)
     else:
         raise ParameterError(f"kde_fastsum supports laplacian, uniform and matern32-additive "
                              f"kernels, got {fam!r}")

@@ -144,6 +144,11 @@ def small():
                                            fc.Bandwidth.diag(h)).values)
         b.put(key + ".unif", fc.kde_fastsum(s, grid, fc.uniform(), fc.Bandwidth.diag(h)).values)
         b.put(key + ".dnc", fc.kde_dnc(s, fc.laplacian(), fc.Bandwidth.diag(h)).values)
+        # matern32-additive through the same terms (fastsum.py:170-181)
+        b.put(key + ".mat", fc.kde_fastsum(s, grid, fc.matern32_additive(),
+                                           fc.Bandwidth.diag(h)).values)
+        b.put(key + ".matnaive", fc.kde_naive(s, grid.lattice(), fc.matern32_additive(),
+                                              fc.Bandwidth.diag(h)).values)
     rng = np.random.default_rng(8)  # points on knots (test_fastsum.py:152-164)
     lat = np.linspace(-1.0, 1.0, 11)
     pts = np.column_stack([rng.choice(lat, 300), rng.choice(lat, 300)])
@@ -195,6 +200,9 @@ def small():
         b.put(key + ".h", h)
         b.put(key + ".out", fc.kde_dnc(s, fc.laplacian(), fc.Bandwidth.diag(h)).values)
         b.put(key + ".naive", fc.kde_naive(s, pts, fc.laplacian(), fc.Bandwidth.diag(h)).values)
+        b.put(key + ".mat", fc.kde_dnc(s, fc.matern32_additive(), fc.Bandwidth.diag(h)).values)
+        b.put(key + ".matnaive", fc.kde_naive(s, pts, fc.matern32_additive(),
+                                              fc.Bandwidth.diag(h)).values)
         if d == 2:
             tt = fc.kde_terms_dnc(s, fc.Bandwidth.diag(h))
             b.put(key + ".psi", tt.psi)

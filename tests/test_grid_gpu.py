@@ -266,6 +266,33 @@ def test_partitioned_ecdf_esf_vs_oracle(dims, delta, oracle):
     np.testing.assert_array_equal(got, oracle.esf_fastsum(x, None, knots))
 
 
+def test_kde_matern32_golden(small_golden):
+    """matern32-additive grid KDE (fastsum.py:170-181) against the reference's own output."""
+    g = small_golden
+    for d in (1, 2, 3):
+        key = f"kde.{d}"
+        s = fcb.validate_sample(g[key + ".x"], g[key + ".w"])
+        got = fcb.kde_fastsum(s, _grid(g.knots(key)), fcb.matern32_additive(),
+                              fcb.Bandwidth.diag(g[key + ".h"])).values
+        assert_rel(got, g[key + ".mat"], REL_KDE)
+        assert np.max(np.abs(got - g[key + ".matnaive"])) <= 1e-13
+
+
+@pytest.mark.parametrize("d", [2, 4])
+def test_kde_matern32_vs_oracle(d, oracle):
+    rng = np.random.default_rng(40 + d)
+    n = 30000
+    x = rng.standard_normal((n, d))
+    w = rng.exponential(1.0, n)
+    m = {2: (61, 47), 4: (9, 12, 7, 10)}[d]
+    knots = [np.linspace(-2.5, 2.2, k) for k in m]
+    knots[0] = np.unique(np.concatenate([knots[0], x[:2, 0]]))  # knot hits
+    h = rng.uniform(0.15, 0.5, d)
+    got = fcb.kde_fastsum(fcb.validate_sample(x, w), _grid(knots), fcb.matern32_additive(),
+                          fcb.Bandwidth.diag(h)).values
+    assert_rel(got, oracle.kde_fastsum_matern32(x, w, knots, h), REL_KDE)
+
+
 @pytest.mark.parametrize("dims", [(320, 17, 40), (20, 16, 33, 21)])
 def test_partitioned_kde_vs_oracle(dims, oracle):
     oracle.set_threads(0)

@@ -116,3 +116,19 @@ def test_cfg1_full(oracle):
     w = wl.cfg1()
     got = oracle.ecdf_fastsum(w.points, None, w.knots, w.delta, scaled=False)
     np.testing.assert_array_equal(got, gold["counts"].astype(np.float64))
+
+
+def test_matern32_additive(small_golden, oracle):
+    """matern32-additive through the Laplacian terms (fastsum.py:170-181, dnc.py:659-685),
+    pinned to the reference's own fast and naive outputs."""
+    g = small_golden
+    for d in (1, 2, 3):
+        key = f"kde.{d}"
+        got = oracle.kde_fastsum_matern32(g[key + ".x"], g[key + ".w"], g.knots(key), g[key + ".h"])
+        np.testing.assert_allclose(got, g[key + ".mat"], rtol=1e-13, atol=0)
+        np.testing.assert_allclose(got, g[key + ".matnaive"], rtol=1e-12, atol=0)
+    for d in (1, 2):
+        key = f"kdednc.{d}"
+        got = oracle.kde_dnc_matern32(g[key + ".x"], g[key + ".w"], g[key + ".h"])
+        np.testing.assert_allclose(got, g[key + ".mat"], rtol=1e-13, atol=0)
+        np.testing.assert_allclose(got, g[key + ".matnaive"], rtol=1e-12, atol=0)
