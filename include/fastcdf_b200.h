@@ -212,6 +212,15 @@ int fcg_kde_points_laplacian(const double *x, int64_t n, int32_t d, const double
                              int32_t nw, const double *h, const double *centre, double *out,
                              void *ws, size_t *ws_bytes, void *stream);
 
+/* matern32-additive KDE at the sample points (dnc.py:635-690 with family "matern32-additive"):
+ * the d + 1 channels of dnc.py:661-669 are run as 2d + 1 Laplacian dominance channels whose
+ * weights only change sign with the term (A = w e, B_k = s_k w e, C_l = s_l w xc_l e / h_l),
+ * combined as A + sum_k (xc_k / h_k) B_k - sum_l C_l, + w, * 1 / (2^d n prod h (1 + d)).
+ * One weight vector (or NULL); requires distinct coordinates; h, centre host (d,). */
+int fcg_kde_points_matern32(const double *x, int64_t n, int32_t d, const double *w,
+                            const double *h, const double *centre, double *out,
+                            void *ws, size_t *ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -51,6 +51,7 @@ _SIGS = {
     "fcg_ecdf_points": ([_P, _I64, _I32, _P, _P, _I32, _I32, _P, _P, _SZP, _P], C.c_int),
     "fcg_dnc_ecdf": ([_P, _I64, _I32, _P, _I32, _I32, _P, _P, _SZP, _P], C.c_int),
     "fcg_kde_points_laplacian": ([_P, _I64, _I32, _P, _I32, _P, _P, _P, _P, _SZP, _P], C.c_int),
+    "fcg_kde_points_matern32": ([_P, _I64, _I32, _P, _P, _P, _P, _P, _SZP, _P], C.c_int),
     "fcg_axis_owner": ([_P, _I64, _I32, _I32, _P, _I64, _I32, _I32, _P, _I32, _P, _P], C.c_int),
     "fcg_partition_rows": ([_P, _I64, _I32, _P, _P, _I32, _P, _P, _P, _P, _SZP, _P], C.c_int),
     "fcg_slab_finish": ([_P, _I32, _P, _I64, _I64, _I64, C.c_double, _P, _P], C.c_int),

@@ -362,7 +362,7 @@ __global__ void group_keys(const int32_t *__restrict__ order, const int32_t *__r
 
 // ------------------------------------------------------------------------------------------
 // brute force (d >= 3): CTA = 256 queries, source tiles staged in shared memory
-enum BruteMode { BR_ECDF = 0, BR_KDE = 1 };
+enum BruteMode { BR_ECDF = 0, BR_KDE = 1, BR_MATERN = 2 };
 
 struct Brute {
   int64_t n;
@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(256) brute_kernel(Brute B) {
         if (base + j == t) continue;  // self term added in closed form by the caller
         double e = 0.0;
         for (int k = 0; k < B.d; ++k) e += fabs(xs[k] - xt[k]) * B.inv_h[k];
-        const double kv = exp(-e);
+        const double kv = MODE == BR_MATERN ? (1.0 + e) * exp(-e) : exp(-e);
         for (int v = 0; v < B.nw; ++v) acc[v] += s_w[v][j] * kv;
       }
     }
@@ -422,7 +422,13 @@ __global__ void __launch_bounds__(256) brute_kernel(Brute B) {
 struct KdeP {
   int d;
   double c[FCG_MAX_DIM], a[FCG_MAX_DIM];  // a_k = s_k / h_k
+  int code;                                // the term's sign code (bit k: s_k = -1)
+  unsigned smask[2];                       // channel v's psi carries prod_{k in smask} s_k
 };
+
+__device__ __forceinline__ double chan_sign(const KdeP &p, int v) {
+  return (__popc(p.smask[v] & (unsigned)p.code) & 1) ? -1.0 : 1.0;
+}
 
 // expo[i] = sum_k (x_ik - c_k) * a_k ; psi[v][i] = w[v][i] * exp(expo[i])
 __global__ void kde_psi_kernel(const double *__restrict__ x, int64_t n, KdeP p,
@@ -434,7 +440,7 @@ __global__ void kde_psi_kernel(const double *__restrict__ x, int64_t n, KdeP p,
     for (int k = 0; k < p.d; ++k) s += (x[i * p.d + k] - p.c[k]) * p.a[k];
     expo[i] = s;
     const double e = exp(s);
-    for (int v = 0; v < nw; ++v) psi[v * n + i] = (w ? w[v * n + i] : 1.0) * e;
+    for (int v = 0; v < nw; ++v) psi[v * n + i] = (w ? w[v * n + i] : 1.0) * e * chan_sign(p, v);
   }
 }
 
@@ -568,7 +574,7 @@ __global__ void group_psi_kernel(GrpArrays g, int64_t n, KdeP kp, int nw, int kd
       e = exp(s);
       g.z[k] = exp(-s);
     }
-    for (int v = 0; v < nw; ++v) g.psi[v * n + k] = g.w[v * n + k] * e;
+    for (int v = 0; v < nw; ++v) g.psi[v * n + k] = g.w[v * n + k] * e * (kde ? chan_sign(kp, v) : 1.0);
   }
 }
 
@@ -1026,7 +1032,7 @@ void carve_self(Workspace &W, SelfWs &q, int64_t n, int nw) {
 // weighted by e^{-s} at the query).  out[v][t] = (sum + (add_w ? w : 0)) * mult / div.
 int self_dom2d(const double *x, const double *w, int64_t n, int nw, int kde, const double *h,
                const double *centre, int add_w, double mult, double div, PtsWs &p, SelfWs &q,
-               double *out, cudaStream_t st) {
+               double *out, cudaStream_t st, const unsigned *smask = nullptr) {
   FCG_TRY(prep2d(x, n, p, st));
   const int g = grid_for(n, 256);
   {
@@ -1065,6 +1071,8 @@ int self_dom2d(const double *x, const double *w, int64_t n, int nw, int kde, con
   for (int code = 0; code < ncodes; ++code) {
     KdeP kp{};
     kp.d = 2;
+    kp.code = code;
+    for (int v = 0; v < nw; ++v) kp.smask[v] = smask ? smask[v] : 0u;
     for (int k = 0; k < 2; ++k) {
       const double sgn = ((code >> k) & 1) ? -1.0 : 1.0;  // DeltaVector.from_code
       kp.c[k] = kde ? centre[k] : 0.0;
@@ -1439,6 +1447,154 @@ extern "C" int fcg_kde_points_laplacian(const double *x, int64_t n, int32_t d, c
   }
   FCG_PROF("pts_finish", st);
   kde_finish_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, nw, w, scale, out);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}
+
+namespace fcg {
+namespace {
+// matern32-additive at the points as signed Laplacian channels.  With s the term's signs,
+//   sum_code z_code [(1 + expo_code) F_0 - sum_l (s_l / h_l) F_l]
+//     = A + sum_k (xc_k / h_k) B_k - sum_l C_l,
+// A = sum_code z F(w e), B_k = sum_code z F(s_k w e), C_l = sum_code z F(s_l w xc_l e / h_l):
+// 2d + 1 channels of the Laplacian dominance engine whose psi only changes sign with the code.
+__global__ void matern_channels_kernel(const double *__restrict__ x, int64_t n, int d,
+                                       const double *__restrict__ w, const double *c,
+                                       const double *hinv, double *__restrict__ wv) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double wi = w ? w[i] : 1.0;
+    wv[i] = wi;
+    for (int k = 0; k < d; ++k) {
+      wv[(int64_t)(1 + k) * n + i] = wi;
+      wv[(int64_t)(1 + d + k) * n + i] = wi * (x[i * d + k] - c[k]) * hinv[k];
+    }
+  }
+}
+
+struct MatFin {
+  int d;
+  double c[FCG_MAX_DIM], hinv[FCG_MAX_DIM];
+  double scale;
+};
+
+// out = (A + sum_k (xc_k / h_k) B_k - sum_l C_l + w) * scale   (self term, dnc.py:682-686)
+__global__ void matern_finish_kernel(const double *__restrict__ acc, const double *__restrict__ x,
+                                     int64_t n, const double *__restrict__ w, MatFin f,
+                                     double *__restrict__ out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    double r = acc[t];
+    for (int k = 0; k < f.d; ++k)
+      r += (x[t * f.d + k] - f.c[k]) * f.hinv[k] * acc[(int64_t)(1 + k) * n + t];
+    for (int l = 0; l < f.d; ++l) r -= acc[(int64_t)(1 + f.d + l) * n + t];
+    r = r + (w ? w[t] : 1.0);
+    out[t] = r * f.scale;
+  }
+}
+}  // namespace
+}  // namespace fcg
+
+extern "C" int fcg_kde_points_matern32(const double *x, int64_t n, int32_t d, const double *w,
+                                       const double *h, const double *centre, double *out,
+                                       void *ws, size_t *ws_bytes, void *stream) {
+  FCG_TRY(check_pts(n, d));
+  const bool dom_ok = (d == 2 && n <= kMaxDominanceN);
+  const int nchan = 2 * d + 1;
+  Workspace W(ws);
+  PtsWs p;
+  carve(W, p, n, d < 2 ? d : 2, 2, dom_ok, true, d == 1 ? n * 2 : 0);
+  SelfWs q{};
+  if (dom_ok) carve_self(W, q, n, 2);
+  double *wv = W.take<double>((size_t)n * nchan);
+  double *acc = W.take<double>((size_t)n * nchan);
+  double *psi1 = nullptr, *F1 = nullptr;
+  if (d == 1) {
+    psi1 = W.take<double>((size_t)n);
+    F1 = W.take<double>((size_t)n);
+  }
+  double *dpar = W.take<double>(2 * FCG_MAX_DIM);
+  if (ws == nullptr) {
+    *ws_bytes = W.bytes();
+    return FCG_OK;
+  }
+  if (n == 0) return FCG_OK;
+  for (int k = 0; k < d; ++k)
+    if (!(h[k] > 0.0)) return fail(FCG_EINVAL, "bandwidth must be > 0");
+  cudaStream_t st = as_stream(stream);
+  double prod_h = 1.0;
+  for (int k = 0; k < d; ++k) prod_h *= h[k];
+  double scale = 1.0 / (std::ldexp(1.0, d) * (double)n * prod_h);
+  scale /= 1.0 + d;  // dnc.py:683-685
+
+  if (d >= 3 || !(d == 1 || dom_ok)) {  // direct pairs with the matern32-additive kernel
+    Brute B;
+    B.n = n;
+    B.d = d;
+    B.x = x;
+    B.w = w;
+    B.nw = 1;
+    B.out = out;
+    for (int k = 0; k < d; ++k) B.inv_h[k] = 1.0 / h[k];
+    {
+      FCG_PROF("pts_brute", st);
+      brute_kernel<BR_MATERN><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(B);
+      FCG_LAUNCH_CHECK();
+    }
+    FCG_PROF("pts_finish", st);
+    kde_finish_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, 1, w, scale, out);
+    FCG_LAUNCH_CHECK();
+    return FCG_OK;
+  }
+  MatFin f{};
+  f.d = d;
+  f.scale = scale;
+  double hp[2 * FCG_MAX_DIM];
+  for (int k = 0; k < d; ++k) {
+    f.c[k] = centre[k];
+    f.hinv[k] = 1.0 / h[k];
+    hp[k] = centre[k];
+    hp[FCG_MAX_DIM + k] = 1.0 / h[k];
+  }
+  FCG_CUDA_TRY(cudaMemcpyAsync(dpar, hp, sizeof(hp), cudaMemcpyHostToDevice, st));
+  {
+    FCG_PROF("pts_psi", st);
+    matern_channels_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, d, w, dpar, dpar + FCG_MAX_DIM, wv);
+    FCG_LAUNCH_CHECK();
+  }
+  if (d == 2) {
+    // channels: 0 A, 1-2 B_k (sign s_k), 3-4 C_l (sign s_l); two per pass
+    const unsigned m01[2] = {0u, 1u}, m23[2] = {2u, 1u}, m4[1] = {2u};
+    FCG_TRY(self_dom2d(x, wv, n, 2, 1, h, centre, 0, 0.0, 0.0, p, q, acc, st, m01));
+    FCG_TRY(self_dom2d(x, wv + 2 * n, n, 2, 1, h, centre, 0, 0.0, 0.0, p, q, acc + 2 * n, st, m23));
+    FCG_TRY(self_dom2d(x, wv + 4 * n, n, 1, 1, h, centre, 0, 0.0, 0.0, p, q, acc + 4 * n, st, m4));
+  } else {  // d == 1: code 0 = strictly below (prefix), code 1 = strictly above (suffix)
+    FCG_TRY(rank_dim(x, n, 1, 0, p, st));
+    const unsigned masks[3] = {0u, 1u, 1u};
+    for (int ch = 0; ch < 3; ++ch) {
+      for (int code = 0; code < 2; ++code) {
+        KdeP kp{};
+        kp.d = 1;
+        kp.code = code;
+        kp.smask[0] = masks[ch];
+        kp.c[0] = centre[0];
+        kp.a[0] = (code ? -1.0 : 1.0) / h[0];
+        {
+          FCG_PROF("pts_psi", st);
+          kde_psi_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, kp, wv + (size_t)ch * n, 1, p.expo,
+                                                           psi1);
+          FCG_LAUNCH_CHECK();
+        }
+        FCG_TRY(sorted_exclusive(psi1, p.r[0].order, n, code == 1, p.lat, p.scratch, F1, st));
+        FCG_PROF("pts_kde_accum", st);
+        kde_accum_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, 1, p.expo, F1, acc + (size_t)ch * n,
+                                                          code == 0);
+        FCG_LAUNCH_CHECK();
+      }
+    }
+  }
+  FCG_PROF("pts_finish", st);
+  matern_finish_kernel<<<grid_for(n, 256), 256, 0, st>>>(acc, x, n, w, f, out);
   FCG_LAUNCH_CHECK();
   return FCG_OK;
 }

@@ -106,21 +106,35 @@ def _kde_points(sample: Sample, weights_list, h: np.ndarray):
     return out
 
 
+def _kde_points_matern32(sample: Sample, h: np.ndarray):
+    import torch
+
+    c = _span_guard_and_centre(sample, h)
+    x = _lib.to_device_f64(sample.points)
+    n, d = x.shape
+    w = None if sample.unit_weights else _lib.to_device_f64(sample.weights)
+    out = torch.empty(n, dtype=torch.float64, device=x.device)
+    _lib.call_ws("fcg_kde_points_matern32", _lib.ptr(x), n, d, _lib.ptr(w), _lib.f64_array(h),
+                 _lib.f64_array(c), _lib.ptr(out))
+    return out
+
+
 def kde_dnc(sample: Sample, kernel: KernelSpec, bandwidth: Bandwidth) -> EvalResult:
-    """Kernel density estimate at the sample points (dnc.py:635-690), Laplacian family."""
+    """Kernel density estimate at the sample points (dnc.py:635-690): laplacian and
+    matern32-additive families."""
     sample = as_sample(sample)
     t0 = time.perf_counter()
     _require_distinct(sample)
     fam = kernel.family
-    if fam == "matern32-additive":
-        raise ParameterError("matern32-additive is not implemented on the B200 path yet "
-                             "(SURVEY §8f #1)")
-    if fam != "laplacian":
+    if fam not in ("laplacian", "matern32-additive"):
         raise ParameterError(f"kde_dnc supports laplacian and matern32-additive kernels, "
                              f"got {fam!r}")
     h = _diag_bandwidth(sample, bandwidth)
     w = None if sample.unit_weights else sample.weights
-    vals = _kde_points(sample, [w], h)[0]
+    if fam == "matern32-additive":
+        vals = _kde_points_matern32(sample, h)
+    else:
+        vals = _kde_points(sample, [w], h)[0]
     return EvalResult(_out(sample, vals), POINT_ALIGNED, {
         "method": "dnc", "kernel": str(kernel),
         "runtime_seconds": time.perf_counter() - t0})

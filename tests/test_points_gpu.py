@@ -151,6 +151,33 @@ def test_kde_dnc_golden(small_golden):
         assert np.max(np.abs(got - g[key + ".naive"])) <= 1e-13  # reference bound
 
 
+def test_kde_dnc_matern32_golden(small_golden):
+    """matern32-additive at the points (dnc.py:659-685) vs the reference's own output."""
+    g = small_golden
+    for d in (1, 2, 3):
+        key = f"kdednc.{d}"
+        s = fcb.validate_sample(g[key + ".x"], g[key + ".w"])
+        got = fcb.kde_dnc(s, fcb.matern32_additive(), fcb.Bandwidth.diag(g[key + ".h"])).values
+        assert rel_err(got, g[key + ".mat"]) <= 1e-9
+        assert np.max(np.abs(got - g[key + ".matnaive"])) <= 1e-13
+
+
+@pytest.mark.parametrize("n", [7, 5000, 300_001])
+def test_kde_dnc_matern32_vs_oracle_signed(n, oracle):
+    rng = np.random.default_rng(3000 + n)
+    x = rng.standard_normal((n, 2))
+    w = rng.standard_normal(n)
+    h = [0.25, 0.4]
+    got = fcb.kde_dnc(fcb.validate_sample(x, w), fcb.matern32_additive(), fcb.Bandwidth.diag(h)).values
+    ref = oracle.kde_dnc_matern32(x, w, h)
+    absk = oracle.kde_dnc_matern32(x, np.abs(w), h)
+    assert rel_err(got, ref, absk) <= 1e-9
+    x1 = rng.standard_normal((n, 1))  # d = 1: prefix / suffix channels
+    got = fcb.kde_dnc(fcb.validate_sample(x1, w), fcb.matern32_additive(), fcb.Bandwidth.diag([0.3])).values
+    assert rel_err(got, oracle.kde_dnc_matern32(x1, w, [0.3]),
+                   oracle.kde_dnc_matern32(x1, np.abs(w), [0.3])) <= 1e-9
+
+
 @pytest.mark.parametrize("n", [5, 4096, 9000, 250_000])
 def test_kde_dnc_vs_oracle_signed(n, oracle):
     rng = np.random.default_rng(1000 + n)
