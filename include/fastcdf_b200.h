@@ -120,6 +120,15 @@ int fcg_kde_grid_matern32(const double *x, int64_t n, int32_t d, const double *w
                           const double *centre, double *out,
                           void *ws, size_t *ws_bytes, void *stream);
 
+/* Multilinear interpolation of grid-aligned values at nq query points (device arrays; knots
+ * concatenated per dimension, m host (d,), every m_k >= 2).  Queries are clamped to the knot
+ * hull per coordinate; out[t] is bit-identical to the reference.  *clamp_count (host, may be
+ * NULL; non-NULL synchronises the stream) receives the number of clamped queries.
+ * Replaces: interp.py:24-75 multilinear_interp. */
+int fcg_multilinear_interp(const double *knots, const int64_t *m, int32_t d, const double *values,
+                           const double *q, int64_t nq, double *out, int64_t *clamp_count,
+                           void *ws, size_t *ws_bytes, void *stream);
+
 /* ---------------------------------------------------------------------------------------
  * Multi-GPU slab decomposition along axis 1 (used by paper_2005_03246_b200.distributed)
  * ------------------------------------------------------------------------------------- */

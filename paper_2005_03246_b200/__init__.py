@@ -47,5 +47,6 @@ from .kernels import (
 
 from .dnc import ecdf_dnc, kde_dnc
 from .points import ecdf_at_points, esf_at_points, kde_numerators, kernel_regression
+from .interp import multilinear_interp
 
 __version__ = "0.1.0"

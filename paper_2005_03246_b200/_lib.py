@@ -46,6 +46,7 @@ _SIGS = {
     "fcg_minmax": ([_P, _I64, _I32, _P, _P, _SZP, _P], C.c_int),
     "fcg_kde_grid_laplacian": ([_P, _I64, _I32, _P, _P, _P, _P, _P, _P, _P, _SZP, _P], C.c_int),
     "fcg_kde_grid_matern32": ([_P, _I64, _I32, _P, _P, _P, _P, _P, _P, _P, _SZP, _P], C.c_int),
+    "fcg_multilinear_interp": ([_P, _P, _I32, _P, _P, _I64, _P, _P, _P, _SZP, _P], C.c_int),
     "fcg_rank_f64": ([_P, _I64, _I64, _P, _P, _P, _P, _P, _P, _SZP, _P], C.c_int),
     "fcg_distinct": ([_P, _I64, _I32, _P, _P, _SZP, _P], C.c_int),
     "fcg_ecdf_points": ([_P, _I64, _I32, _P, _P, _I32, _I32, _P, _P, _SZP, _P], C.c_int),

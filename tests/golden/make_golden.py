@@ -161,6 +161,30 @@ def small():
     b.put_knots("kdeknots", knots)
     b.put("kdeknots.fast", fc.kde_fastsum(s, g, fc.laplacian(), fc.Bandwidth.diag([0.25, 0.4])).values)
 
+    # ---- multilinear interpolation grid -> points (interp.py:24-75) ----
+    for d in (1, 2, 3):
+        rng = np.random.default_rng(900 + d)
+        knots = [np.sort(rng.uniform(-1, 1, int(rng.integers(2, 9)))) for _ in range(d)]
+        g = fc.RectilinearGrid.from_knots(knots)
+        vals = rng.standard_normal(g.size)
+        q = rng.uniform(-1.3, 1.3, (257, d))   # some outside the hull (clamped)
+        q[:5] = g.lattice()[:5]                # nodes reproduce bitwise
+        q[5, 0] = knots[0][-1]                 # on the last knot
+        r = fc.multilinear_interp(g, fc.EvalResult(vals, "grid"), q)
+        key = f"interp.{d}"
+        b.put_knots(key, knots)
+        b.put(key + ".vals", vals)
+        b.put(key + ".q", q)
+        b.put(key + ".out", r.values)
+        b.put(key + ".clamp", np.array(r.metadata["clamp_count"]))
+    rng = np.random.default_rng(77)  # interpolated grid ECDF at the sample points (crit. 5)
+    pts = rng.standard_normal((400, 2))
+    s = fc.validate_sample(pts)
+    g = fc.build_grid_auto(s, [20, 20])
+    b.put("interp.ecdf.x", pts)
+    b.put_knots("interp.ecdf", g.knots)
+    b.put("interp.ecdf.out", fc.multilinear_interp(g, fc.ecdf_fastsum(s, g), pts).values)
+
     # ---- naive oracles (naive.py) ----
     rng = np.random.default_rng(4)
     pts = rng.standard_normal((300, 2))

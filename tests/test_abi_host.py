@@ -127,3 +127,16 @@ def test_reference_style_objects_are_accepted():
         fcb.local_sums(ref_like, g)
     with pytest.raises(fcb.TieError):
         fcb.ecdf_dnc(ref_like)
+
+
+def test_interp_errors_before_device_work():
+    g = fcb.RectilinearGrid.from_knots([np.array([0.0, 1.0])])
+    with pytest.raises(fcb.ShapeError):
+        fcb.multilinear_interp(g, fcb.EvalResult(np.zeros(2), "points"), [[0.5]])
+    with pytest.raises(fcb.ShapeError):
+        fcb.multilinear_interp(g, fcb.EvalResult(np.zeros(3), "grid"), [[0.5]])
+    with pytest.raises(fcb.ShapeError, match=r"queries must be \(Q, 1\), got \(1, 2\)"):
+        fcb.multilinear_interp(g, fcb.EvalResult(np.zeros(2), "grid"), [[0.5, 0.5]])
+    g1 = fcb.RectilinearGrid.from_knots([np.array([0.0])])
+    with pytest.raises(fcb.ParameterError):
+        fcb.multilinear_interp(g1, fcb.EvalResult(np.zeros(1), "grid"), [[0.0]])

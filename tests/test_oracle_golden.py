@@ -132,3 +132,12 @@ def test_matern32_additive(small_golden, oracle):
         got = oracle.kde_dnc_matern32(g[key + ".x"], g[key + ".w"], g[key + ".h"])
         np.testing.assert_allclose(got, g[key + ".mat"], rtol=1e-13, atol=0)
         np.testing.assert_allclose(got, g[key + ".matnaive"], rtol=1e-12, atol=0)
+
+
+def test_multilinear_interp(small_golden, oracle):
+    g = small_golden
+    for d in (1, 2, 3):
+        key = f"interp.{d}"
+        out, cc = oracle.multilinear_interp(g.knots(key), g[key + ".vals"], g[key + ".q"])
+        np.testing.assert_array_equal(out, g[key + ".out"])
+        assert cc == int(g[key + ".clamp"])
