@@ -24,7 +24,11 @@ from .core import (
     all_deltas,
     build_grid_auto,
     generate_gaussian_sample,
+    read_result_csv,
+    read_sample_csv,
     validate_sample,
+    write_result_csv,
+    write_sample_csv,
 )
 from .fastsum import (
     CumulativeTensor,

@@ -1,7 +1,7 @@
 """Generate golden fixtures by running the REFERENCE package itself (build container only).
 
     NUMBA_CACHE_DIR=/tmp/numba_golden PYTHONPATH=/root/reference/pkg/src \
-        python -B tests/golden/make_golden.py [--small] [--configs cfg1,cfg2,...]
+        python -B tests/golden/make_golden.py [--small] [--csv] [--configs cfg1,cfg2,...]
 
 Writes small .npz fixtures next to this file; they are committed and travel to the GPU box
 (the reference itself does not).  Inputs are stored with the outputs wherever they are small,
@@ -353,12 +353,33 @@ def cfg_golden(which):
         print(name, json.dumps(entry), flush=True)
 
 
+def csv_golden():
+    """Bytes of the reference's CSV writers (core.py:350-377) for the wire-format tests."""
+    import tempfile
+
+    rng = np.random.default_rng(11)
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        s = fc.validate_sample(rng.standard_normal((7, 3)), rng.uniform(0.5, 2.0, 7))
+        fc.write_sample_csv(s, f"{td}/w.csv")
+        fc.write_sample_csv(fc.validate_sample(rng.standard_normal((5, 2))), f"{td}/u.csv")
+        g = fc.RectilinearGrid.from_knots([np.array([0.0, 0.5]), np.array([1.0, 2.0, 3.0])])
+        fc.write_result_csv(g.lattice(), np.arange(6.0) / 7.0, f"{td}/r.csv")
+        for k in "wur":
+            out[k] = np.frombuffer(open(f"{td}/{k}.csv", "rb").read(), dtype=np.uint8)
+    np.savez_compressed(HERE / "csv.npz", **out)
+    print("wrote csv.npz", flush=True)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--small", action="store_true")
+    ap.add_argument("--csv", action="store_true")
     ap.add_argument("--configs", default="")
     a = ap.parse_args()
     if a.small:
         small()
+    if a.csv:
+        csv_golden()
     if a.configs:
         cfg_golden([c for c in a.configs.split(",") if c])

@@ -140,3 +140,28 @@ def test_interp_errors_before_device_work():
     g1 = fcb.RectilinearGrid.from_knots([np.array([0.0])])
     with pytest.raises(fcb.ParameterError):
         fcb.multilinear_interp(g1, fcb.EvalResult(np.zeros(1), "grid"), [[0.0]])
+
+
+def test_csv_wire_formats_match_reference_bytes(tmp_path):
+    """write_sample_csv / write_result_csv produce the reference's exact bytes
+    (tests/golden/csv.npz, written by the reference's own writers) and read back losslessly."""
+    gold = np.load(ROOT / "tests" / "golden" / "csv.npz")
+    rng = np.random.default_rng(11)
+    s = fcb.validate_sample(rng.standard_normal((7, 3)), rng.uniform(0.5, 2.0, 7))
+    fcb.write_sample_csv(s, tmp_path / "w.csv")
+    su = fcb.validate_sample(rng.standard_normal((5, 2)))
+    fcb.write_sample_csv(su, tmp_path / "u.csv")
+    g = fcb.RectilinearGrid.from_knots([np.array([0.0, 0.5]), np.array([1.0, 2.0, 3.0])])
+    fcb.write_result_csv(g.lattice(), np.arange(6.0) / 7.0, tmp_path / "r.csv")
+    for k in "wur":
+        assert (tmp_path / f"{k}.csv").read_bytes() == gold[k].tobytes(), k
+    back = fcb.read_sample_csv(tmp_path / "w.csv")
+    np.testing.assert_array_equal(back.points, s.points)
+    np.testing.assert_array_equal(back.weights, s.weights)
+    assert fcb.read_sample_csv(tmp_path / "u.csv").unit_weights
+    z, v = fcb.read_result_csv(tmp_path / "r.csv")
+    np.testing.assert_array_equal(z, g.lattice())
+    np.testing.assert_array_equal(v, np.arange(6.0) / 7.0)
+    (tmp_path / "bad.csv").write_text("x1,w,q\n1,2\n")
+    with pytest.raises(fcb.ShapeError):
+        fcb.read_sample_csv(tmp_path / "bad.csv")
