@@ -424,7 +424,7 @@ static int kde_grid_impl(const double *x, int64_t n, int32_t d, const double *w,
   if (planes && d < 2) return fail(FCG_EINVAL, "slab planes need d >= 2");
   cudaStream_t st = as_stream(stream);
   Workspace W(ws);
-  const PartPlan plan = plan_kde_partition(d, m, n);
+  const PartPlan plan = plan_kde_partition(d, m, n, u_bound > 0.0 && u_bound <= 600.0);
   if (plan.ok) {
     FCG_TRY(kde_partitioned(x, n, w, knots, m, d, h, centre, u_bound > 0.0 ? u_bound : 1e300,
                             n_scale, planes, plan, out, W, ws != nullptr, st));

@@ -828,6 +828,295 @@ __global__ void __launch_bounds__(kKdeThreads, 2) plane_kde_group_kernel(
   }
 }
 
+// ---- all term groups in one plane pass (d = 3, 4; factored records) ----------------------
+// The groups (leading-axis sign patterns g) differ only in which full-space plane feeds an
+// output plane (shift s_g along each leading axis) and in the leading factors q_k of psi.  A
+// CTA therefore owns one FULL-space plane F and, from one pass over its bucket's records per
+// row sign, builds the column-sign tile pairs of every group (output plane F - s_g), so the
+// records are streamed 2 times instead of 2 * 2^(d-2).  Warp g walks group g's tile pair with
+// the raw column sums kept in registers across the row blocks (no segment pass), and writes
+// the weighted rows of the group's lattice.
+constexpr int kAllThreads = 128;
+constexpr size_t kAllTileBytes = 55 * 1024;  // 4 CTAs per SM
+
+struct KdeAll {
+  int d, nlead;
+  int64_t Mr, Mc, Rf, nrb;
+  int64_t lead_m[FCG_MAX_DIM];
+  int cell_bits, col_bits;
+  int row_split;              // 1: each row sign has its own lattice (slab planes at d = 3)
+  const double *zr_pos, *zr_neg, *zc_pos, *zc_neg;
+  double *lat[16];            // output lattice of (group, row sign) -> lat[row_split ? 2g+ph : g]
+};
+
+template <int NG>
+struct AllVals {
+  double v[2 * NG];  // (psi_+, psi_-) per group
+};
+
+template <int NG>
+__device__ __forceinline__ void all_put(double *tiles, int tile_elems, int W, int nr, int rowoff,
+                                        int col_bits, uint32_t rmask, uint32_t cmask,
+                                        unsigned vmask, uint32_t key, const AllVals<NG> &a,
+                                        bool atomic) {
+  const int cr = (int)((key >> col_bits) & rmask) + rowoff;
+  const int col = (int)(key & cmask);
+  if (cr < 0 || cr >= nr) return;
+  const int ip = cr * W + swz_col(col);
+  const int im = cr * W + swz_col(col - 1);
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    if (!((vmask >> g) & 1)) continue;
+    double *tp = tiles + (size_t)(2 * g) * tile_elems;
+    double *tm = tp + tile_elems;
+    if (col < W) {
+      if (atomic) atomicAdd(tp + ip, a.v[2 * g]);
+      else tp[ip] = a.v[2 * g];
+    }
+    if (col >= 1) {
+      if (atomic) atomicAdd(tm + im, a.v[2 * g + 1]);
+      else tm[im] = a.v[2 * g + 1];
+    }
+  }
+}
+
+template <int E, int NG>
+__global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
+    KdeAll t, const int32_t *__restrict__ start, const double *__restrict__ rec, int64_t nrec,
+    const uint32_t *__restrict__ keys) {
+  constexpr int W = 32 * E, C = E / 2;
+  extern __shared__ __align__(16) unsigned char smem[];
+  double *tiles = reinterpret_cast<double *>(smem);  // [2 NG][Rf][W], swizzled rows
+  const int Rf = (int)t.Rf, H = (int)t.Mr;
+  const int tile_elems = Rf * W;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int d = t.d, kr = d - 2, kcol = d - 1;
+  // full-space leading indices of this CTA's plane, and each group's output plane
+  int64_t fidx[FCG_MAX_DIM];
+  {
+    int64_t rem = blockIdx.x;
+    for (int k = t.nlead - 1; k >= 0; --k) {
+      fidx[k] = rem % (t.lead_m[k] + 1);
+      rem /= t.lead_m[k] + 1;
+    }
+  }
+  unsigned vmask = 0;
+  int64_t oplane[NG];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    bool ok = true;
+    int64_t pidx = 0;
+    for (int k = 0; k < t.nlead; ++k) {
+      const int64_t i = fidx[k] - ((g >> k) & 1);
+      ok = ok && i >= 0 && i < t.lead_m[k];
+      pidx = pidx * t.lead_m[k] + i;
+    }
+    oplane[g] = pidx;
+    if (ok) vmask |= 1u << g;
+  }
+  if (vmask == 0) return;  // uniform
+  const int64_t fplane = blockIdx.x;
+  tile_zero<double>(tiles, 2 * NG * tile_elems);
+  const uint32_t cmask = (1u << t.col_bits) - 1u, rmask = (1u << (t.cell_bits - t.col_bits)) - 1u;
+  const int c0 = lane * E;
+  int pc[C];
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    const int ch = lane * C + j;
+    pc[j] = (ch ^ ((ch >> 3) & 7)) * 2;
+  }
+  double zp[E], zm[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    zp[e] = t.zc_pos[c0 + e];
+    zm[e] = t.zc_neg[c0 + e];
+  }
+  // field pointers: A, q_lead, q_row, q_col (factored records)
+  const double *fA = rec, *fr = rec + (int64_t)(1 + kr) * nrec, *fc = rec + (int64_t)(1 + kcol) * nrec;
+  const double *fq0 = rec + nrec, *fq1 = rec + 2 * nrec;
+  for (int ph = 0; ph < 2; ++ph) {
+    const int rneg = ph, sr = ph;
+    const double *zr = t.row_split ? nullptr : (rneg ? t.zr_neg : t.zr_pos);
+    double up[E], um[E];  // this warp's group: raw column sums through the rows walked so far
+#pragma unroll
+    for (int e = 0; e < E; ++e) up[e] = um[e] = 0.0;
+    for (int64_t rbi = 0; rbi < t.nrb; ++rbi) {
+      const int64_t rb = rneg ? t.nrb - 1 - rbi : rbi;
+      const int lo = (int)(rb * Rf - sr), hi = lo + Rf;
+      const int clo = lo < 0 ? 0 : lo, chi = hi > H ? H : hi;
+      if (chi <= clo) continue;
+      const int nr = chi - clo;
+      const int rowoff = (int)(rb * Rf) - sr - clo;
+      __syncthreads();  // the previous block's walk has re-zeroed the tiles
+      {
+        const int64_t b = fplane * t.nrb + rb;
+        const int32_t q0 = start[b], q1 = start[b + 1];
+        // warp shares aligned to run boundaries: no run of equal keys straddles two warps, so
+        // every run is complete inside one share and all tile writes are plain stores
+        const int32_t per = (q1 - q0 + nw - 1) / nw;
+        auto run_start = [&](int32_t p) -> int32_t {  // first q >= p that starts a run
+          if (p <= q0) return q0;
+          if (p >= q1) return q1;
+          const uint32_t k0 = keys[p - 1];
+          while (p < q1 && keys[p] == k0) ++p;
+          return p;
+        };
+        int32_t sb = 0, se = 0;
+        if (lane == 0) {
+          sb = run_start(q0 + warp * per);
+          se = run_start(q0 + (warp + 1) * per);
+        }
+        sb = __shfl_sync(0xffffffffu, sb, 0);
+        se = __shfl_sync(0xffffffffu, se, 0);
+        uint32_t ckey = 0xFFFFFFFFu;
+        AllVals<NG> cv;
+#pragma unroll
+        for (int i = 0; i < 2 * NG; ++i) cv.v[i] = 0.0;
+        for (int32_t qb = sb; qb < se; qb += 32) {
+          const int32_t q = qb + lane;
+          const bool in = q < se;
+          const int32_t qq = in ? q : sb;
+          const uint32_t key = in ? keys[q] : 0xFFFFFFFFu;
+          const double A = fA[qq], qcv = fc[qq];
+          const double q0v = t.nlead > 0 ? fq0[qq] : 1.0;
+          const double q1v = t.nlead > 1 ? fq1[qq] : 1.0;
+          const double qrv = rneg ? fr[qq] : 1.0;
+          AllVals<NG> a;
+          const double base = in ? A * qrv : 0.0;
+#pragma unroll
+          for (int g = 0; g < NG; ++g) {
+            double v = base;
+            if (g & 1) v *= q0v;
+            if (g & 2) v *= q1v;
+            a.v[2 * g] = v;
+            a.v[2 * g + 1] = v * qcv;
+          }
+          // segmented run sums over the window (see window_reduce)
+          const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+          const bool head = lane == 0 || key != prev;
+          const unsigned heads = __ballot_sync(0xffffffffu, head);
+          const int hl = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+          const int span = lane - hl;
+          const int maxspan = __reduce_max_sync(0xffffffffu, span);
+          AllVals<NG> sv = a;
+          for (int o = 1; o <= maxspan; ++o) {
+#pragma unroll
+            for (int i = 0; i < 2 * NG; ++i) {
+              const double u = __shfl_up_sync(0xffffffffu, a.v[i], o);
+              if (o <= span) sv.v[i] += u;
+            }
+          }
+          const uint32_t key0 = __shfl_sync(0xffffffffu, key, 0);
+          const bool cont = key0 == ckey;
+          if (cont && hl == 0) {
+#pragma unroll
+            for (int i = 0; i < 2 * NG; ++i) sv.v[i] += cv.v[i];
+          }
+          if (!cont && ckey != 0xFFFFFFFFu && lane == 0)
+            all_put<NG>(tiles, tile_elems, W, nr, rowoff, t.col_bits, rmask, cmask, vmask, ckey, cv,
+                        false);
+          const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1);
+          if (tail && lane != 31 && key != 0xFFFFFFFFu)
+            all_put<NG>(tiles, tile_elems, W, nr, rowoff, t.col_bits, rmask, cmask, vmask, key, sv,
+                        false);
+          ckey = __shfl_sync(0xffffffffu, key, 31);
+#pragma unroll
+          for (int i = 0; i < 2 * NG; ++i) cv.v[i] = __shfl_sync(0xffffffffu, sv.v[i], 31);
+        }
+        if (ckey != 0xFFFFFFFFu && lane == 0)
+          all_put<NG>(tiles, tile_elems, W, nr, rowoff, t.col_bits, rmask, cmask, vmask, ckey, cv,
+                      false);
+      }
+      __syncthreads();
+      // walk: warp g owns group g's tile pair
+      if (warp < NG) {
+        const int g = warp;
+        double *tp = tiles + (size_t)(2 * g) * tile_elems;
+        double *tm = tp + tile_elems;
+        const bool wr = (vmask >> g) & 1;
+        double *gp = wr ? t.lat[t.row_split ? 2 * g + ph : g] + oplane[g] * H * W + (int64_t)clo * W
+                        : nullptr;
+        const bool rmw = ph > 0 && !t.row_split;
+        const double2 zero2 = make_double2(0.0, 0.0);
+        double2 na[C], nb[C], nold[C];  // next row: tiles and (accumulate pass) plane values
+        auto fetch = [&](int qr) {
+          const int r = rneg ? nr - 1 - qr : qr;
+#pragma unroll
+          for (int j = 0; j < C; ++j) {
+            na[j] = *reinterpret_cast<const double2 *>(tp + r * W + pc[j]);
+            nb[j] = *reinterpret_cast<const double2 *>(tm + r * W + pc[j]);
+            nold[j] = (wr && rmw) ? reinterpret_cast<const double2 *>(gp + (int64_t)r * W + c0)[j]
+                                  : zero2;
+          }
+        };
+        fetch(0);
+        for (int qr = 0; qr < nr; ++qr) {
+          const int r = rneg ? nr - 1 - qr : qr;
+          double2 ca[C], cb[C], old[C];
+#pragma unroll
+          for (int j = 0; j < C; ++j) {
+            ca[j] = na[j];
+            cb[j] = nb[j];
+            old[j] = nold[j];
+          }
+          if (qr + 1 < nr) fetch(qr + 1);
+#pragma unroll
+          for (int j = 0; j < C; ++j) {
+            *reinterpret_cast<double2 *>(tp + r * W + pc[j]) = zero2;
+            *reinterpret_cast<double2 *>(tm + r * W + pc[j]) = zero2;
+            up[2 * j] += ca[j].x; up[2 * j + 1] += ca[j].y;
+            um[2 * j] += cb[j].x; um[2 * j + 1] += cb[j].y;
+          }
+          if (!wr) continue;  // warp-uniform
+          double tsp = 0.0, tsm = 0.0;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            tsp += up[e];
+            tsm += um[e];
+          }
+          double ip = tsp, im = tsm;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const double xp = __shfl_up_sync(0xffffffffu, ip, off);
+            const double xm = __shfl_down_sync(0xffffffffu, im, off);
+            if (lane >= off) ip += xp;
+            if (lane + off < 32) im += xm;
+          }
+          double sp[E], sm[E];
+          double run = ip - tsp;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            run += up[e];
+            sp[e] = run;
+          }
+          run = im - tsm;
+#pragma unroll
+          for (int e = E - 1; e >= 0; --e) {
+            run += um[e];
+            sm[e] = run;
+          }
+          const double zrv = zr ? __ldg(zr + clo + r) : 1.0;
+          double2 *o = reinterpret_cast<double2 *>(gp + (int64_t)r * W + c0);
+#pragma unroll
+          for (int j = 0; j < C; ++j) {
+            const int e = 2 * j;
+            double2 v;
+            v.x = zrv * (zp[e] * sp[e] + zm[e] * sm[e]);
+            v.y = zrv * (zp[e + 1] * sp[e + 1] + zm[e + 1] * sm[e + 1]);
+            if (rmw) {
+              v.x += old[j].x;
+              v.y += old[j].y;
+            }
+            o[j] = v;
+          }
+        }
+      } else {
+        // idle warps: nothing to walk (NG < warps)
+      }
+    }
+  }
+}
+
 // KDE records, built in the coarse partition pass (partition.cuh) from coalesced reads of x, w:
 //   factored (f != 0): fields (A, q_0..q_{d-1}) with A = w e^{sum_k u_k}, q_k = e^{-2 u_k},
 //                      u_k = (x_k - c_k) / h_k, so a term's psi = A * prod_{k: delta_k=-1} q_k;
@@ -1136,7 +1425,7 @@ int ecdf_partitioned(const double *x, int64_t n, const double *knots, const BinG
   return scan_axis<int32_t>(lat, s, 0, rev[0], epi, scratch, st);
 }
 
-PartPlan plan_kde_partition(int d, const int64_t *m, int64_t n) {
+PartPlan plan_kde_partition(int d, const int64_t *m, int64_t n, bool factored) {
   PartPlan pl;
   if (d < 3 || n < kMinPartitionN) return pl;
   pl.W = m[d - 1];
@@ -1144,12 +1433,18 @@ PartPlan plan_kde_partition(int d, const int64_t *m, int64_t n) {
   if (pl.W + 1 > 65535 || pl.H + 1 > 65535) return pl;  // packed 16-bit (row, col) offsets
   const int64_t G = seg_rows(kKdeThreads, pl.W, 2);
   const int64_t Hf = pl.H + 1;
-  // fewest full-space row blocks whose tile fits the budget
+  // all term groups in one pass (plane_kde_all_kernel): d = 3, 4, factored records,
+  // W = 32 E with E in {2, 4, 8}; otherwise one launch per group (plane_kde_group_kernel)
+  const int ng = 1 << (d - 2);
+  const int e_all = scan_variant(pl.W, 2);
+  pl.all = factored && (d == 3 || d == 4) && (e_all == 2 || e_all == 4);
+  // fewest full-space row blocks whose tiles fit the budget
   int64_t nrb = 1, Rf = Hf;
   while (true) {
     Rf = ceil_div(Hf, nrb);
-    const size_t bytes = kde_group_smem(Rf, pl.W, G);
-    if (bytes <= kKdeTileBytes) break;
+    const size_t bytes = pl.all ? (size_t)(2 * ng) * Rf * pl.W * sizeof(double)
+                                : kde_group_smem(Rf, pl.W, G);
+    if (bytes <= (pl.all ? kAllTileBytes : kKdeTileBytes)) break;
     if (Rf == 1) return pl;
     ++nrb;
   }
@@ -1198,7 +1493,8 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   const int ngroups = 1 << kz;
   const int per0 = ngroups / 2;  // groups per delta_0 sign
   const int nbatch = per0 < kMaxGroup ? per0 : kMaxGroup;
-  double *lats = W.take<double>((size_t)s.size() * nbatch);
+  // all-groups pass: every group lattice alive at once; else one batch of groups at a time
+  double *lats = W.take<double>((size_t)s.size() * (pl.all ? ngroups : nbatch));
   double *scratch = W.take<double>(scan_scratch_bound());
   double *zfs = W.take<double>((size_t)total_knots * (nbatch + 2));
   if (!run) return FCG_OK;
@@ -1280,6 +1576,47 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   FCG_TRY(launch_kde_zf(knots, d, m, centre, h, 0, zpos, st));
   FCG_TRY(launch_kde_zf(knots, d, m, centre, h, (1 << d) - 1, zneg, st));
   const int kr = d - 2, kc = d - 1;
+  if (pl.all) {  // one pass over the records per row sign for every group
+    KdeAll ta{};
+    ta.d = d;
+    ta.nlead = d - 2;
+    ta.Mr = m[kr];
+    ta.Mc = m[kc];
+    ta.Rf = pl.R;
+    ta.nrb = pl.nrb;
+    for (int k = 0; k < d - 2; ++k) ta.lead_m[k] = m[k];
+    ta.cell_bits = pl.cell_bits;
+    ta.col_bits = pl.col_bits;
+    ta.row_split = kz > kr ? 1 : 0;
+    ta.zr_pos = zpos + zoff[kr];
+    ta.zr_neg = zneg + zoff[kr];
+    ta.zc_pos = zpos + zoff[kc];
+    ta.zc_neg = zneg + zoff[kc];
+    const int ng = 1 << (d - 2);
+    for (int g = 0; g < ng; ++g) {
+      if (ta.row_split) {  // lattice of group code gl = lead signs | row sign << kr
+        for (int ph = 0; ph < 2; ++ph) ta.lat[2 * g + ph] = lats + (size_t)(g | (ph << kr)) * L;
+      } else {
+        ta.lat[g] = lats + (size_t)g * L;
+      }
+    }
+    const size_t asmem = (size_t)(2 * ng) * pl.R * pl.W * sizeof(double);
+    int64_t np_full = 1;
+    for (int k = 0; k < d - 2; ++k) np_full *= m[k] + 1;
+    FCG_PROF("plane_kde", st);
+    auto launch = [&](auto kern) -> int {
+      FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asmem));
+      kern<<<(unsigned)np_full, kAllThreads, asmem, st>>>(ta, b.start, rec, n, keys_c);
+      FCG_LAUNCH_CHECK();
+      return FCG_OK;
+    };
+    const int E = scan_variant(pl.W, 2);
+    if (d == 4) {
+      FCG_TRY(E == 2 ? launch(plane_kde_all_kernel<2, 4>) : launch(plane_kde_all_kernel<4, 4>));
+    } else {
+      FCG_TRY(E == 2 ? launch(plane_kde_all_kernel<2, 2>) : launch(plane_kde_all_kernel<4, 2>));
+    }
+  }
   for (int s0 = 0; s0 < 2; ++s0) {
     for (int b0 = 0; b0 < per0; b0 += nbatch) {
       const int nt = (per0 - b0) < nbatch ? (per0 - b0) : nbatch;
@@ -1293,7 +1630,7 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
       }
       for (int tt = 0; tt < nt; ++tt) {
         const int gl = s0 | ((b0 + tt) << 1);  // signs of axes < kz (bit k: delta_k = -1)
-        double *lat = lats + (size_t)tt * L;
+        double *lat = lats + (size_t)(pl.all ? gl : tt) * L;
         double *zf = zfs + (size_t)tt * total_knots;
         KdeGroup t{};
         t.d = d;
@@ -1336,7 +1673,7 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
         t.col_bits = pl.col_bits;
         t.exp = getenv("FCG_KDE_EXP") ? atoi(getenv("FCG_KDE_EXP")) : 0;
         FCG_TRY(launch_kde_zf(knots, d, m, centre, h, gl, zf, st));
-        {
+        if (!pl.all) {
           FCG_PROF("plane_kde", st);
           kde_kern<<<(unsigned)pl.NP, kKdeThreads, smem, st>>>(t, b.start, rec, n, keys_c,
                                                                factored, lat);

@@ -19,6 +19,7 @@ struct PartPlan {
   int64_t NB = 0;   // buckets
   int nbits = 0;    // radix key bits
   int cell_bits = 0;  // KDE: in-bucket cell bits of the sorted key (0: bucket-only keys)
+  bool all = false;   // KDE: every term group from one plane pass (plane_kde_all_kernel)
   int col_bits = 0;
 };
 
@@ -35,7 +36,7 @@ int ecdf_partitioned(const double *x, int64_t n, const double *knots, const BinG
 inline int kde_cap_kw(int d) { return d - 2 > 2 ? d - 2 : 2; }
 
 // Laplacian KDE: full-space binning (dims M_k + 1) shared by all 2^d terms.
-PartPlan plan_kde_partition(int d, const int64_t *m, int64_t n);
+PartPlan plan_kde_partition(int d, const int64_t *m, int64_t n, bool factored);
 // bound_u_sum: an upper bound of sum_k max_i |x_ik - c_k| / h_k (selects the factored psi
 // records); n_scale: the N of the 1/(2^d N prod h) normalisation (the global N on a slab);
 // planes: optional [2^d][A * B1] capture of each term's slab-boundary S plane (may be null).
