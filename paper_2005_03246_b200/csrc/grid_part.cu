@@ -998,12 +998,14 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
           const int hl = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
           const int span = lane - hl;
           const int maxspan = __reduce_max_sync(0xffffffffu, span);
+          // log-step segmented scan (Hillis-Steele bounded by the run head), only as many
+          // steps as the longest run needs
           AllVals<NG> sv = a;
-          for (int o = 1; o <= maxspan; ++o) {
+          for (int o = 1; o <= maxspan; o <<= 1) {
 #pragma unroll
             for (int i = 0; i < 2 * NG; ++i) {
-              const double u = __shfl_up_sync(0xffffffffu, a.v[i], o);
-              if (o <= span) sv.v[i] += u;
+              const double u = __shfl_up_sync(0xffffffffu, sv.v[i], o);
+              if (lane - o >= hl) sv.v[i] += u;
             }
           }
           const uint32_t key0 = __shfl_sync(0xffffffffu, key, 0);
