@@ -954,35 +954,49 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
         // warp shares aligned to run boundaries: no run of equal keys straddles two warps, so
         // every run is complete inside one share and all tile writes are plain stores
         const int32_t per = (q1 - q0 + nw - 1) / nw;
-        auto run_start = [&](int32_t p) -> int32_t {  // first q >= p that starts a run
+        auto run_start = [&](int32_t p) -> int32_t {  // first q >= p that starts a run (warp)
           if (p <= q0) return q0;
           if (p >= q1) return q1;
           const uint32_t k0 = keys[p - 1];
-          while (p < q1 && keys[p] == k0) ++p;
-          return p;
+          while (true) {
+            const int32_t qq = p + lane;
+            const bool diff = qq >= q1 || keys[qq] != k0;
+            const unsigned bal = __ballot_sync(0xffffffffu, diff);
+            if (bal) return p + __ffs(bal) - 1;
+            p += 32;
+          }
         };
-        int32_t sb = 0, se = 0;
-        if (lane == 0) {
-          sb = run_start(q0 + warp * per);
-          se = run_start(q0 + (warp + 1) * per);
-        }
-        sb = __shfl_sync(0xffffffffu, sb, 0);
-        se = __shfl_sync(0xffffffffu, se, 0);
+        const int32_t sb = run_start(q0 + warp * per);
+        const int32_t se = run_start(q0 + (warp + 1) * per);
         uint32_t ckey = 0xFFFFFFFFu;
         AllVals<NG> cv;
 #pragma unroll
         for (int i = 0; i < 2 * NG; ++i) cv.v[i] = 0.0;
-        for (int32_t qb = sb; qb < se; qb += 32) {
+        // raw fields of the next window are loaded before this one is reduced
+        struct Raw {
+          uint32_t key;
+          double A, qc, q0, q1, qr;
+        };
+        auto load = [&](Raw &r, int32_t qb) {
           const int32_t q = qb + lane;
           const bool in = q < se;
           const int32_t qq = in ? q : sb;
-          const uint32_t key = in ? keys[q] : 0xFFFFFFFFu;
-          const double A = fA[qq], qcv = fc[qq];
-          const double q0v = t.nlead > 0 ? fq0[qq] : 1.0;
-          const double q1v = t.nlead > 1 ? fq1[qq] : 1.0;
-          const double qrv = rneg ? fr[qq] : 1.0;
+          r.key = in ? keys[q] : 0xFFFFFFFFu;
+          r.A = fA[qq];
+          r.qc = fc[qq];
+          r.q0 = t.nlead > 0 ? fq0[qq] : 1.0;
+          r.q1 = t.nlead > 1 ? fq1[qq] : 1.0;
+          r.qr = rneg ? fr[qq] : 1.0;
+        };
+        Raw nx;
+        if (sb < se) load(nx, sb);
+        for (int32_t qb = sb; qb < se; qb += 32) {
+          const Raw cur = nx;
+          if (qb + 32 < se) load(nx, qb + 32);
+          const uint32_t key = cur.key;
+          const double qcv = cur.qc, q0v = cur.q0, q1v = cur.q1;
           AllVals<NG> a;
-          const double base = in ? A * qrv : 0.0;
+          const double base = key != 0xFFFFFFFFu ? cur.A * cur.qr : 0.0;
 #pragma unroll
           for (int g = 0; g < NG; ++g) {
             double v = base;
