@@ -1143,26 +1143,37 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
 // record-major next to their keys; the full sort then only moves (key, slot) pairs and the
 // final gather reads each coarse bucket from L2 (sorted order walks the buckets in turn)
 // instead of paying a DRAM line per random record.
+template <int D>
 struct KdeBuild {
-  const double *x, *w;
-  int d, factored;
+  static constexpr int kD = D;
+  int factored;
   PsiParams pp;
-  __device__ __forceinline__ void operator()(int64_t i, double *r) const {
-    const double wi = w ? w[i] : 1.0;
+  __device__ __forceinline__ void operator()(const double *xi, double wi, double *r) const {
     if (factored) {
       double su = 0.0;
-      for (int k = 0; k < d; ++k) {
-        const double u = (x[i * d + k] - pp.c[k]) * pp.a[k];  // a_k = 1 / h_k
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const double u = (xi[k] - pp.c[k]) * pp.a[k];  // a_k = 1 / h_k
         su += u;
         r[1 + k] = exp(-2.0 * u);
       }
       r[0] = wi * exp(su);
     } else {
-      for (int k = 0; k < d; ++k) r[k] = x[i * d + k];
-      r[d] = wi;
+#pragma unroll
+      for (int k = 0; k < D; ++k) r[k] = xi[k];
+      r[D] = wi;
     }
   }
 };
+
+template <int D>
+int kde_build_records(const uint32_t *keys, int64_t n, int shift, const double *x, const double *w,
+                      int factored, const PsiParams &pp, double *rec_c, uint32_t *keys_c,
+                      int32_t *slot, int32_t *hist, int32_t *partial, cudaStream_t st) {
+  KdeBuild<D> kb{factored, pp};
+  return digit_partition_build<KdeBuild<D>, D + 1>(keys, n, shift, x, w, kb, rec_c, keys_c, slot,
+                                                   hist, partial, st);
+}
 
 // sorted records, field-major (rec[f * n + q], so a warp's loads of one field are coalesced and
 // a phase loads only the fields it multiplies), from the coarse-bucketed record-major array
@@ -1549,9 +1560,32 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   // keys -> records grouped by the key's top 8 bits -> sort (key, slot) -> L2-local gather
   const int sort_bits = ((pl.nbits + 7) / 8) * 8;
   FCG_TRY(launch_part_bin(x, n, d, knots, g, p, b.keys, b.vals, st));
-  KdeBuild kb{x, w, d, factored, pp};
-  FCG_TRY(digit_partition_build(b.keys, n, pl.nbits > 8 ? pl.nbits - 8 : 0, d + 1, kb, rec_c, keys_c,
-                                b.vals, b.rw.hist, b.rw.partial, st));
+  {
+    const int shift = pl.nbits > 8 ? pl.nbits - 8 : 0;
+    const bool al = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    int rc;
+    switch (d) {  // the partitioned path runs for d >= 3
+      case 3: rc = kde_build_records<3>(b.keys, n, shift, x, w, factored, pp, rec_c, keys_c, b.vals,
+                                        b.rw.hist, b.rw.partial, st); break;
+      case 4:
+        if (!al) return fail(FCG_EINVAL, "points must be 16-byte aligned");
+        rc = kde_build_records<4>(b.keys, n, shift, x, w, factored, pp, rec_c, keys_c, b.vals,
+                                  b.rw.hist, b.rw.partial, st); break;
+      case 5: rc = kde_build_records<5>(b.keys, n, shift, x, w, factored, pp, rec_c, keys_c, b.vals,
+                                        b.rw.hist, b.rw.partial, st); break;
+      case 6:
+        if (!al) return fail(FCG_EINVAL, "points must be 16-byte aligned");
+        rc = kde_build_records<6>(b.keys, n, shift, x, w, factored, pp, rec_c, keys_c, b.vals,
+                                  b.rw.hist, b.rw.partial, st); break;
+      case 7: rc = kde_build_records<7>(b.keys, n, shift, x, w, factored, pp, rec_c, keys_c, b.vals,
+                                        b.rw.hist, b.rw.partial, st); break;
+      default:
+        if (!al) return fail(FCG_EINVAL, "points must be 16-byte aligned");
+        rc = kde_build_records<8>(b.keys, n, shift, x, w, factored, pp, rec_c, keys_c, b.vals,
+                                  b.rw.hist, b.rw.partial, st); break;
+    }
+    FCG_TRY(rc);
+  }
   FCG_TRY(radix_sort_pairs<uint32_t>(keys_c, b.vals, n, 0, sort_bits, b.rw, st));
   {
     FCG_PROF("part_bucket_start", st);

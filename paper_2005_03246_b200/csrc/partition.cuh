@@ -43,14 +43,17 @@ __global__ void __launch_bounds__(kPartThreads) digit_hist_kernel(const uint32_t
   hist[(int64_t)threadIdx.x * tiles + blockIdx.x] = tot;
 }
 
-template <class Build>
-__global__ void __launch_bounds__(kPartThreads) digit_stage_kernel(
+// Build: struct with `static constexpr int kD` (point dimension, > 0) and
+//   void operator()(const double *xi, double wi, double *out) const  (writes kWords doubles)
+template <class Build, int WORDS>
+__global__ void __launch_bounds__(kPartThreads, 2) digit_stage_kernel(
     const uint32_t *__restrict__ keys, int64_t n, int shift, const int32_t *__restrict__ offs,
-    int64_t tiles, int words, Build build, double *__restrict__ rec_out,
-    uint32_t *__restrict__ keys_out, int32_t *__restrict__ slot_out) {
+    int64_t tiles, const double *__restrict__ x, const double *__restrict__ w, Build build,
+    double *__restrict__ rec_out, uint32_t *__restrict__ keys_out, int32_t *__restrict__ slot_out) {
+  constexpr int D = Build::kD;
   extern __shared__ __align__(16) unsigned char ps_smem[];
-  double *s_rec = reinterpret_cast<double *>(ps_smem);                       // [tile][words]
-  uint32_t *s_key = reinterpret_cast<uint32_t *>(s_rec + (size_t)kPartTile * words);
+  double *s_rec = reinterpret_cast<double *>(ps_smem);                       // [tile][WORDS]
+  uint32_t *s_key = reinterpret_cast<uint32_t *>(s_rec + (size_t)kPartTile * WORDS);
   int32_t *s_cnt = reinterpret_cast<int32_t *>(s_key + kPartTile);            // [8][256]
   int32_t *s_goff = s_cnt + (kPartThreads / 32) * 256;
   int32_t *s_tstart = s_goff + 256;
@@ -64,12 +67,32 @@ __global__ void __launch_bounds__(kPartThreads) digit_stage_kernel(
   const int tile_n = (int)((n - tile0) < kPartTile ? (n - tile0) : kPartTile);
   uint32_t k[kPartItems];
   int32_t r[kPartItems];
+  double xs[kPartItems][D], ws[kPartItems];
+  // every item's key, point and weight in flight before the ranking needs them
+#pragma unroll
+  for (int j = 0; j < kPartItems; ++j) {
+    const int64_t i = base + (int64_t)j * 32 + lane;
+    const bool ok = i < n;
+    const int64_t ii = ok ? i : 0;
+    k[j] = ok ? keys[i] : 0u;
+    if constexpr (D % 2 == 0) {
+#pragma unroll
+      for (int c = 0; c < D; c += 2) {
+        const double2 v = reinterpret_cast<const double2 *>(x + ii * D)[c / 2];
+        xs[j][c] = v.x;
+        xs[j][c + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < D; ++c) xs[j][c] = x[ii * D + c];
+    }
+    ws[j] = w ? w[ii] : 1.0;
+  }
   const unsigned lt = lane_lt();
 #pragma unroll
   for (int j = 0; j < kPartItems; ++j) {
     const int64_t i = base + (int64_t)j * 32 + lane;
     const bool ok = i < n;
-    k[j] = ok ? keys[i] : 0u;
     const unsigned dig = ok ? ((k[j] >> shift) & 0xFFu) : 256u + lane;
     const unsigned peers = __match_any_sync(0xffffffffu, dig);
     int32_t before = 0;
@@ -84,31 +107,32 @@ __global__ void __launch_bounds__(kPartThreads) digit_stage_kernel(
     const int d = threadIdx.x;
     int32_t run = 0;
 #pragma unroll
-    for (int w = 0; w < kPartThreads / 32; ++w) {
-      const int32_t t = s_cnt[w * 256 + d];
-      s_cnt[w * 256 + d] = run;
+    for (int wp = 0; wp < kPartThreads / 32; ++wp) {
+      const int32_t t = s_cnt[wp * 256 + d];
+      s_cnt[wp * 256 + d] = run;
       run += t;
     }
-    int32_t x = run;
+    int32_t xx = run;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+      const int32_t y = __shfl_up_sync(0xffffffffu, xx, o);
+      if (lane >= o) xx += y;
     }
-    if (lane == 31) s_wsum[warp] = x;
+    if (lane == 31) s_wsum[warp] = xx;
     __syncthreads();
     int32_t wpre = 0;
-    for (int w = 0; w < warp; ++w) wpre += s_wsum[w];
-    s_tstart[d] = wpre + x - run;
+    for (int wp = 0; wp < warp; ++wp) wpre += s_wsum[wp];
+    s_tstart[d] = wpre + xx - run;
   }
   __syncthreads();
+#pragma unroll
   for (int j = 0; j < kPartItems; ++j) {
     const int64_t i = base + (int64_t)j * 32 + lane;
     if (i < n) {
       const unsigned dig = (k[j] >> shift) & 0xFFu;
       const int pos = s_tstart[dig] + s_cnt[warp * 256 + dig] + r[j];
       s_key[pos] = k[j];
-      build(i, s_rec + (size_t)pos * words);
+      build(xs[j], ws[j], s_rec + (size_t)pos * WORDS);
     }
   }
   __syncthreads();
@@ -119,12 +143,12 @@ __global__ void __launch_bounds__(kPartThreads) digit_stage_kernel(
     keys_out[dst] = key;
     slot_out[dst] = (int32_t)dst;
   }
-  const int tw = tile_n * words;
+  const int tw = tile_n * WORDS;
   for (int idx = threadIdx.x; idx < tw; idx += kPartThreads) {
-    const int pos = idx / words;
+    const int pos = idx / WORDS;  // compile-time divisor
     const unsigned dig = (s_key[pos] >> shift) & 0xFFu;
     const int64_t dst = (int64_t)s_goff[dig] + (pos - s_tstart[dig]);
-    rec_out[dst * words + (idx - pos * words)] = s_rec[idx];
+    rec_out[dst * WORDS + (idx - pos * WORDS)] = s_rec[idx];
   }
 }
 
@@ -138,10 +162,12 @@ inline size_t digit_stage_smem(int words) {
 inline size_t digit_hist_elems(int64_t n) { return (size_t)256 * (size_t)ceil_div(n, kPartTile) + 1; }
 
 // Workspace: hist = digit_hist_elems(n) ints, partial = scan_ws_partial_elems(hist elems).
-template <class Build>
-int digit_partition_build(const uint32_t *keys, int64_t n, int shift, int words, const Build &build,
-                          double *rec_out, uint32_t *keys_out, int32_t *slot_out, int32_t *hist,
-                          int32_t *partial, cudaStream_t st) {
+// x: (n, Build::kD) row-major points (16-byte aligned when kD is even), w: weights or NULL.
+template <class Build, int WORDS>
+int digit_partition_build(const uint32_t *keys, int64_t n, int shift, const double *x,
+                          const double *w, const Build &build, double *rec_out,
+                          uint32_t *keys_out, int32_t *slot_out, int32_t *hist, int32_t *partial,
+                          cudaStream_t st) {
   if (n <= 0) return FCG_OK;
   const int64_t tiles = ceil_div(n, kPartTile);
   {
@@ -152,11 +178,11 @@ int digit_partition_build(const uint32_t *keys, int64_t n, int shift, int words,
   }
   FCG_TRY(scan_i32(hist, hist, 256 * tiles, false, partial, st));
   FCG_PROF("part_emit", st);
-  const size_t sm = digit_stage_smem(words);
-  FCG_CUDA_TRY(cudaFuncSetAttribute(part_detail::digit_stage_kernel<Build>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  part_detail::digit_stage_kernel<Build><<<(unsigned)tiles, kPartThreads, sm, st>>>(
-      keys, n, shift, hist, tiles, words, build, rec_out, keys_out, slot_out);
+  const size_t sm = digit_stage_smem(WORDS);
+  auto kern = part_detail::digit_stage_kernel<Build, WORDS>;
+  FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  kern<<<(unsigned)tiles, kPartThreads, sm, st>>>(keys, n, shift, hist, tiles, x, w, build,
+                                                  rec_out, keys_out, slot_out);
   FCG_LAUNCH_CHECK();
   return FCG_OK;
 }
