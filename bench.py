@@ -162,9 +162,10 @@ def grid_kde_bytes(n, d, m, unit_w):
         "radix_scatter": 16 * n,
         # sorted field-major records from the grouped record-major ones
         "kde_materialize": 4 * n + 16 * n * (d + 1),
-        # one group: per row-sign phase the keys and the fields it multiplies (on average
-        # d + 3 fields over both phases), the weighted plane lattice written once
-        "plane_kde": 8 * n + 8 * n * (d + 3) + 8 * L,
+        # all term groups in one launch (d = 3, 4): two passes over the records (keys, A, the
+        # leading q's, q_col; q_row in the second), and per group lattice the first row-sign
+        # pass writes it and the second reads and rewrites it
+        "plane_kde": 8 * n + 8 * n * (2 * (d + 1) - 1) + (1 << (d - 2)) * 24 * L,
         # one axis-0 pass over the group lattices sharing delta_0; accumulator written by the
         # first pass, read + written by the second
         "kde_final_group": per0 * 8 * L + (8 * L + 16 * L) // 2,

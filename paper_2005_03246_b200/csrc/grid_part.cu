@@ -847,6 +847,7 @@ struct KdeAll {
   int row_split;              // 1: each row sign has its own lattice (slab planes at d = 3)
   const double *zr_pos, *zr_neg, *zc_pos, *zc_neg;
   double *lat[16];            // output lattice of (group, row sign) -> lat[row_split ? 2g+ph : g]
+  int exp;                    // profiling experiments (FCG_KDE_EXP): 1 no records, 2 no walk
 };
 
 template <int NG>
@@ -967,7 +968,7 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
           }
         };
         const int32_t sb = run_start(q0 + warp * per);
-        const int32_t se = run_start(q0 + (warp + 1) * per);
+        const int32_t se = (t.exp & 1) ? sb : run_start(q0 + (warp + 1) * per);
         uint32_t ckey = 0xFFFFFFFFu;
         AllVals<NG> cv;
 #pragma unroll
@@ -1045,7 +1046,7 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
       }
       __syncthreads();
       // walk: warp g owns group g's tile pair
-      if (warp < NG) {
+      if (warp < NG && !(t.exp & 2)) {
         const int g = warp;
         double *tp = tiles + (size_t)(2 * g) * tile_elems;
         double *tm = tp + tile_elems;
@@ -1638,6 +1639,7 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
     ta.cell_bits = pl.cell_bits;
     ta.col_bits = pl.col_bits;
     ta.row_split = kz > kr ? 1 : 0;
+    ta.exp = getenv("FCG_KDE_EXP") ? atoi(getenv("FCG_KDE_EXP")) : 0;
     ta.zr_pos = zpos + zoff[kr];
     ta.zr_neg = zneg + zoff[kr];
     ta.zc_pos = zpos + zoff[kc];
