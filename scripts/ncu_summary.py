@@ -17,7 +17,8 @@ SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12,
 
 
 # ncu kernel name -> the launch profiler's scope name (what bench.py's roofline reports)
-SCOPES = [(r"^plane_kde_kernel", "plane_kde"), (r"^kde_materialize", "kde_materialize"),
+SCOPES = [(r"^plane_kde", "plane_kde"), (r"^kde_gather", "kde_materialize"),
+          (r"digit_stage", "part_emit"), (r"digit_hist", "part_hist"), (r"^kde_materialize", "kde_materialize"),
           (r"^kde_final_multi", "kde_final_group"), (r"^lines_kernel<\w+, \d, 1>", "scan_lines_final"),
           (r"^lines_kernel", "scan_lines"), (r"^rows_kernel", "scan_rows"),
           (r"^radix_scatter", "radix_scatter"), (r"^radix_hist", "radix_hist"),
