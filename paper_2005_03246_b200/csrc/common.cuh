@@ -93,4 +93,17 @@ __device__ __forceinline__ uint64_t f64_key(double v) {
   return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
 }
 
+// Lanes of the warp holding the same 8-bit digit (+ a 9th bit for out-of-range lanes): the
+// multisplit by 9 ballots (one per digit bit) instead of match.any -- the radix ranking's hot
+// instruction.
+__device__ __forceinline__ unsigned digit_peers(unsigned dig) {
+  unsigned peers = 0xffffffffu;
+#pragma unroll
+  for (int bit = 0; bit < 9; ++bit) {
+    const unsigned b = __ballot_sync(0xffffffffu, (dig >> bit) & 1u);
+    peers &= ((dig >> bit) & 1u) ? b : ~b;
+  }
+  return peers;
+}
+
 }  // namespace fcg

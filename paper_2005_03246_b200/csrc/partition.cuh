@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kPartThreads, 2) digit_stage_kernel(
     const int64_t i = base + (int64_t)j * 32 + lane;
     const bool ok = i < n;
     const unsigned dig = ok ? ((k[j] >> shift) & 0xFFu) : 256u + lane;
-    const unsigned peers = __match_any_sync(0xffffffffu, dig);
+    const unsigned peers = digit_peers(dig);
     int32_t before = 0;
     if (ok) before = s_cnt[warp * 256 + dig];
     __syncwarp();

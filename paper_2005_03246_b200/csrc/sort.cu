@@ -195,14 +195,20 @@ __global__ void __launch_bounds__(kSortThreads, 3) radix_scatter_kernel(
   int32_t v[kSortItems];
   int32_t r[kSortItems];
   const unsigned lt = lanemask_lt();
+  // all of the tile's keys and values in flight before the ranking (which orders on syncwarps)
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const int64_t i = base + (int64_t)j * 32 + lane;
     const bool ok = i < n;
     k[j] = ok ? kin[i] : KeyT(0);
     v[j] = ok ? vin[i] : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const int64_t i = base + (int64_t)j * 32 + lane;
+    const bool ok = i < n;
     const unsigned dig = ok ? (unsigned)((k[j] >> shift) & 0xFF) : 256u + lane;
-    const unsigned peers = __match_any_sync(0xffffffffu, dig);
+    const unsigned peers = digit_peers(dig);
     int32_t before = 0;
     if (ok) before = s_cnt[warp * 256 + dig];
     __syncwarp();
