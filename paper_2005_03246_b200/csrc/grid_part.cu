@@ -34,6 +34,37 @@ struct PartGeo {
 };
 
 template <int D>
+__device__ __forceinline__ void part_key(const double *xi, int d, const double *kb, const BinGrid &g,
+                                         const double *s_z0, const double *s_idz,
+                                         const PartGeo &p, int64_t i, uint32_t &key,
+                                         int32_t &val) {
+  uint32_t plane = 0;
+  int row = 0, col = 0;
+  bool live = true;
+#pragma unroll
+  for (int k = 0; k < (D > 0 ? D : FCG_MAX_DIM); ++k) {
+    if (k < d) {
+      const int c = knot_count(xi[k], kb + g.koff[k], (int)g.m[k], g.le[k], s_z0[k], s_idz[k]) -
+                    (int)p.shift[k];
+      live = live && c >= 0 && c < (int)p.E[k];
+      if (k < d - 2) plane = plane * (uint32_t)p.E[k] + (uint32_t)c;
+      else if (k == d - 2) row = c;
+      else col = c;
+    }
+  }
+  key = kDead;
+  val = (int32_t)i;
+  if (live) {
+    const int rb = row / (int)p.R;
+    key = plane * (uint32_t)p.nrb + (uint32_t)rb;
+    if (p.ecdf) val = (row - rb * (int)p.R) * (int)p.W + col;
+    if (p.cell_bits > 0)
+      key = (key << p.cell_bits) | ((uint32_t)(row - rb * (int)p.R) << p.col_bits) | (uint32_t)col;
+  }
+}
+
+// keys (and payloads) of every point; U points per thread per step, all loaded before binning
+template <int D>
 __global__ void __launch_bounds__(256, 4) part_bin_kernel(const double *__restrict__ x, int64_t n,
                                                        int drt, const double *__restrict__ knots,
                                                        BinGrid g, PartGeo p,
@@ -44,43 +75,35 @@ __global__ void __launch_bounds__(256, 4) part_bin_kernel(const double *__restri
   const int d = D > 0 ? D : drt;
   const double *kb = stage_knots(g, knots, s_knots, s_z0, s_idz);
   __syncthreads();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double xi[D > 0 ? D : FCG_MAX_DIM];
-    if constexpr (D == 4) {
-      const double2 v0 = reinterpret_cast<const double2 *>(x)[2 * i];
-      const double2 v1 = reinterpret_cast<const double2 *>(x)[2 * i + 1];
-      xi[0] = v0.x; xi[1] = v0.y; xi[2] = v1.x; xi[3] = v1.y;
-    } else {
+  constexpr int U = D == 4 ? 2 : 1;
+  constexpr int DD = D > 0 ? D : FCG_MAX_DIM;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+    double xi[U][DD];
 #pragma unroll
-      for (int k = 0; k < (D > 0 ? D : FCG_MAX_DIM); ++k)
-        if (k < d) xi[k] = x[i * d + k];
-    }
-    uint32_t plane = 0;
-    int row = 0, col = 0;
-    bool live = true;
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      const int64_t ii = i < n ? i : 0;
+      if constexpr (D == 4) {
+        const double2 v0 = __ldcs(reinterpret_cast<const double2 *>(x) + 2 * ii);
+        const double2 v1 = __ldcs(reinterpret_cast<const double2 *>(x) + 2 * ii + 1);
+        xi[u][0] = v0.x; xi[u][1] = v0.y; xi[u][2] = v1.x; xi[u][3] = v1.y;
+      } else {
 #pragma unroll
-    for (int k = 0; k < (D > 0 ? D : FCG_MAX_DIM); ++k) {
-      if (k < d) {
-        const int c = knot_count(xi[k], kb + g.koff[k], (int)g.m[k], g.le[k], s_z0[k], s_idz[k]) -
-                      (int)p.shift[k];
-        live = live && c >= 0 && c < (int)p.E[k];
-        if (k < d - 2) plane = plane * (uint32_t)p.E[k] + (uint32_t)c;
-        else if (k == d - 2) row = c;
-        else col = c;
+        for (int k = 0; k < DD; ++k)
+          if (k < d) xi[u][k] = x[ii * d + k];
       }
     }
-    uint32_t key = kDead;
-    int32_t val = (int32_t)i;
-    if (live) {
-      const int rb = row / (int)p.R;
-      key = plane * (uint32_t)p.nrb + (uint32_t)rb;
-      if (p.ecdf) val = (row - rb * (int)p.R) * (int)p.W + col;
-      if (p.cell_bits > 0)
-        key = (key << p.cell_bits) | ((uint32_t)(row - rb * (int)p.R) << p.col_bits) | (uint32_t)col;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= n) break;
+      uint32_t key;
+      int32_t val;
+      part_key<D>(xi[u], d, kb, g, s_z0, s_idz, p, i, key, val);
+      keys[i] = key;
+      if (vals) vals[i] = val;
     }
-    keys[i] = key;
-    vals[i] = val;
   }
 }
 
@@ -1560,7 +1583,7 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   const int factored = bound_u_sum <= 600.0 ? 1 : 0;
   // keys -> records grouped by the key's top 8 bits -> sort (key, slot) -> L2-local gather
   const int sort_bits = ((pl.nbits + 7) / 8) * 8;
-  FCG_TRY(launch_part_bin(x, n, d, knots, g, p, b.keys, b.vals, st));
+  FCG_TRY(launch_part_bin(x, n, d, knots, g, p, b.keys, nullptr, st));  // slots come later
   {
     const int shift = pl.nbits > 8 ? pl.nbits - 8 : 0;
     const bool al = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
