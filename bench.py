@@ -48,6 +48,9 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--slab", action="store_true",
+                    help="run the grid configs through the multi-GPU slab path even on one GPU "
+                         "(exercises the NCCL routing / carry exchange with world size 1)")
     return ap.parse_args()
 
 
@@ -233,6 +236,8 @@ class GridWorkload:
             if self.n * self.d * 8 > 126e6 else "L2-resident (launch-bound config)",
         }
 
+    slab = False
+
     def shard(self, rank, world):
         """Strong scaling over the fixed config: rank r holds points r::world."""
         self.rank, self.world = rank, world
@@ -273,14 +278,14 @@ class GridWorkload:
         self.d2h_bytes = nloc * 8 * (int(self.do_ecdf) + int(self.do_kde)) // self.world
 
     def _ecdf(self, s):
-        if self.world > 1:
+        if self.world > 1 or self.slab:
             from paper_2005_03246_b200 import distributed as fdist
 
             return fdist.ecdf_fastsum_slab(s, self.grid, self.delta).values
         return self.fcb.ecdf_fastsum(s, self.grid, self.delta).values
 
     def _kde(self, s):
-        if self.world > 1:
+        if self.world > 1 or self.slab:
             from paper_2005_03246_b200 import distributed as fdist
 
             return fdist.kde_fastsum_slab(s, self.grid, self.fcb.laplacian(), self.bw).values
@@ -555,12 +560,17 @@ def main():
     import torch.distributed as dist
 
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if world > 1 or args.slab:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local))
     from paper_2005_03246_b200 import _lib
 
     _lib.load_library()
     w = make_workload(args.workload)
+    if args.slab and hasattr(w, "slab"):
+        w.slab = True
     w.shard(rank, world)
     w.to_device()
     torch.cuda.synchronize()
@@ -661,3 +671,10 @@ def main():
 
 if __name__ == "__main__":
     main()
+    try:
+        import torch.distributed as _dist
+
+        if _dist.is_available() and _dist.is_initialized():
+            _dist.destroy_process_group()
+    except ImportError:
+        pass

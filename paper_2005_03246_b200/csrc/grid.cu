@@ -533,28 +533,49 @@ struct FixP {
   double scale;
 };
 
-__global__ void kde_fixup_kernel(double *__restrict__ out, FixP p, const double *__restrict__ zf,
-                                 const double *__restrict__ C) {
-  int64_t L = 1;
-  for (int k = 0; k < p.d; ++k) L *= p.dims[k];
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L;
-       t += (int64_t)gridDim.x * blockDim.x) {
+// Q[b1][pi] = sum over the codes with delta_1 bit b1 of prod_{k<kw, k!=1} zf_code,k(i_k) * C_code[pi]
+// (pi = (i0, i2, ..)): the carry planes folded per axis-1 sign, so the lattice pass needs two
+// plane reads per element instead of one per code.
+__global__ void kde_fixup_fold_kernel(FixP p, const double *__restrict__ zf,
+                                      const double *__restrict__ C, double *__restrict__ Q) {
+  for (int64_t pi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pi < p.plane_sz;
+       pi += (int64_t)gridDim.x * blockDim.x) {
     int64_t idx[FCG_MAX_DIM];
-    int64_t rem = t;
-    for (int k = p.d - 1; k >= 0; --k) {
+    int64_t rem = pi;
+    for (int k = p.d - 1; k >= 2; --k) {
       idx[k] = rem % p.dims[k];
       rem /= p.dims[k];
     }
-    int64_t pi = idx[0];
-    for (int k = 2; k < p.d; ++k) pi = pi * p.dims[k] + idx[k];
-    double acc = 0.0;
+    idx[0] = rem;
+    double q0 = 0.0, q1 = 0.0;
     for (int code = 0; code < p.ncodes; ++code) {
       const double *z = zf + code * p.zsz;
       double zz = 1.0;
-      for (int k = 0; k < p.kw; ++k) zz *= z[p.zoff[k] + idx[k]];
-      acc += zz * C[code * p.plane_sz + pi];
+      for (int k = 0; k < p.kw; ++k)
+        if (k != 1) zz *= z[p.zoff[k] + idx[k]];
+      const double v = zz * C[code * p.plane_sz + pi];
+      if ((code >> 1) & 1) q1 += v;
+      else q0 += v;
     }
-    out[t] += p.scale * acc;
+    Q[pi] = q0;
+    Q[p.plane_sz + pi] = q1;
+  }
+}
+
+// out[i] += scale * (zf_{+,1}(i1) Q[0][pi] + zf_{-,1}(i1) Q[1][pi])
+__global__ void kde_fixup_kernel(double *__restrict__ out, FixP p, const double *__restrict__ z1p,
+                                 const double *__restrict__ z1m, const double *__restrict__ Q) {
+  int64_t L = 1;
+  for (int k = 0; k < p.d; ++k) L *= p.dims[k];
+  const int64_t B = p.plane_sz / p.dims[0];  // extent of the axes 2..d-1
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < L;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t % B;
+    const int64_t r = t / B;
+    const int64_t i1 = r % p.dims[1];
+    const int64_t i0 = r / p.dims[1];
+    const int64_t pi = i0 * B + b;
+    out[t] += p.scale * (z1p[i1] * Q[pi] + z1m[i1] * Q[p.plane_sz + pi]);
   }
 }
 }  // namespace
@@ -661,8 +682,11 @@ extern "C" int fcg_kde_carry_fixup(double *out, int32_t d, const int64_t *m, con
   int64_t total_knots = 0;
   for (int k = 0; k < d; ++k) total_knots += m[k];
   const int ncodes = 1 << d;
+  int64_t L = 1;
+  for (int k = 0; k < d; ++k) L *= m[k];
   Workspace W(ws);
   double *zf = W.take<double>((size_t)ncodes * total_knots);
+  double *Q = W.take<double>((size_t)2 * (L / (m[1] > 0 ? m[1] : 1)));
   if (ws == nullptr) {
     *ws_bytes = W.bytes();
     return FCG_OK;
@@ -674,12 +698,11 @@ extern "C" int fcg_kde_carry_fixup(double *out, int32_t d, const int64_t *m, con
   p.d = d;
   p.ncodes = ncodes;
   p.kw = kde_cap_kw(d);
-  int64_t off = 0, L = 1;
+  int64_t off = 0;
   for (int k = 0; k < d; ++k) {
     p.dims[k] = m[k];
     p.zoff[k] = off;
     off += m[k];
-    L *= m[k];
   }
   p.zsz = total_knots;
   p.plane_sz = L / m[1];
@@ -688,7 +711,11 @@ extern "C" int fcg_kde_carry_fixup(double *out, int32_t d, const int64_t *m, con
   p.scale = 1.0 / (std::ldexp(1.0, d) * n_scale * prod_h);
   if (L == 0) return FCG_OK;
   FCG_PROF("dist_kde_fixup", st);
-  kde_fixup_kernel<<<grid_for(L, 256), 256, 0, st>>>(out, p, zf, planes);
+  kde_fixup_fold_kernel<<<grid_for(p.plane_sz, 256), 256, 0, st>>>(p, zf, planes, Q);
+  FCG_LAUNCH_CHECK();
+  // axis-1 factor tables of the two signs: codes 0 (delta_1 = +1) and 2 (delta_1 = -1)
+  kde_fixup_kernel<<<grid_for(L, 256), 256, 0, st>>>(out, p, zf + p.zoff[1],
+                                                     zf + 2 * total_knots + p.zoff[1], Q);
   FCG_LAUNCH_CHECK();
   return FCG_OK;
 }
