@@ -1317,6 +1317,175 @@ __global__ void __launch_bounds__(256) kde_final_multi(MultiFinal f) {
   }
 }
 
+// ---- fused axis-1 + axis-0 final pass (d >= 4) ------------------------------------------
+// For up to two group lattices sharing delta_0: the 2-D prefix over (i0, i1) of every in-plane
+// column, times the leading factors, accumulated into the density -- replacing a separate
+// read + write pass along axis 1 per lattice.  A CTA owns 32 consecutive columns and walks i0;
+// the [i1][32] slabs of row i0 + 1 are copied into shared memory (cp.async) while row i0 is
+// scanned: thread (column, segment) scans 16 axis-1 positions serially, segments are stitched
+// through shared memory, and the axis-0 carries stay in registers.  A lattice running the
+// other way along axis 1 hands its values back through its slab so both are combined per cell.
+constexpr int kF2Cols = 16, kF2Seg = 8, kF2Segs = 16;  // 16 columns per CTA, axis 1 <= 128
+struct Final2D {
+  int nt, d, kz;
+  const double *lat[2];
+  const double *zf[2];
+  double *plane[2];
+  int64_t plane_idx[2];
+  int rev1[2];
+  int64_t zoff[FCG_MAX_DIM], dims[FCG_MAX_DIM];
+  int accumulate, apply_scale;
+  double scale;
+  double *out;
+};
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <int NT, bool REV0>
+__global__ void __launch_bounds__(256, 2) final2d_kernel(Final2D f) {
+  extern __shared__ __align__(16) double f2_smem[];
+  constexpr int CW = kF2Cols;
+  const int64_t D0 = f.dims[0], D1 = f.dims[1];
+  int64_t B = 1;
+  for (int k = 2; k < f.d; ++k) B *= f.dims[k];
+  const int slab = (int)D1 * CW;                        // doubles per [i1][CW] slab
+  double *buf = f2_smem;                                // [2][NT + 1][D1][CW] (lattices, density)
+  double *segs = buf + 2 * (NT + 1) * slab;             // [NT][kF2Segs][CW]
+  double *z1 = segs + NT * kF2Segs * CW;                // [NT][D1] axis-1 factors
+  const int c = threadIdx.x % CW, sg = threadIdx.x / CW;
+  const int64_t b0 = (int64_t)blockIdx.x * CW;
+  const int64_t b = b0 + c;
+  for (int i = threadIdx.x; i < NT * (int)D1; i += blockDim.x) {
+    const int t = i / (int)D1, i1 = i - t * (int)D1;
+    z1[i] = f.zf[t][f.zoff[1] + i1];
+  }
+  // leading factors of the axes 2 .. kz-1 (d >= 5): functions of the column only
+  double zb[NT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) zb[t] = 1.0;
+  {
+    int64_t rem = b;
+    for (int k = f.d - 1; k >= 2; --k) {
+      const int64_t i = rem % f.dims[k];
+      rem /= f.dims[k];
+      if (k < f.kz)
+#pragma unroll
+        for (int t = 0; t < NT; ++t) zb[t] *= f.zf[t][f.zoff[k] + i];
+    }
+  }
+  auto stage = [&](int64_t jj, int which) {
+    const int64_t i0 = REV0 ? D0 - 1 - jj : jj;
+#pragma unroll
+    for (int t = 0; t <= NT; ++t) {  // t == NT: the density accumulator's row
+      if (t == NT && !f.accumulate) break;
+      double *dst = buf + (which * (NT + 1) + t) * slab;
+      const double *src = (t < NT ? f.lat[t] : f.out) + (i0 * D1) * B + b0;
+      for (int ch = threadIdx.x; ch < (int)D1 * (CW / 2); ch += blockDim.x) {  // 16-byte chunks
+        const int r = ch / (CW / 2), q = ch % (CW / 2);
+        cp_async16(dst + r * CW + q * 2, src + (int64_t)r * B + q * 2);
+      }
+    }
+    cp_async_commit();
+  };
+  double carry[NT][kF2Seg];
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+#pragma unroll
+    for (int s = 0; s < kF2Seg; ++s) carry[t][s] = 0.0;
+  const int p0 = sg * kF2Seg;
+  const bool swap = NT > 1 && f.rev1[1] != f.rev1[0];
+  stage(0, 0);
+  for (int64_t jj = 0; jj < D0; ++jj) {
+    const int64_t i0 = REV0 ? D0 - 1 - jj : jj;
+    const int cur = (int)(jj & 1);
+    if (jj + 1 < D0) stage(jj + 1, cur ^ 1);
+    else cp_async_commit();  // keep the group count uniform
+    cp_async_wait1();
+    __syncthreads();
+    double v[NT][kF2Seg];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const double *sl = buf + (cur * (NT + 1) + t) * slab;
+      double run = 0.0;
+#pragma unroll
+      for (int s = 0; s < kF2Seg; ++s) {
+        const int p = p0 + s;
+        double x = 0.0;
+        if (p < D1) x = sl[(f.rev1[t] ? (int)D1 - 1 - p : p) * CW + c];
+        run += x;
+        v[t][s] = run;
+      }
+      segs[(t * kF2Segs + sg) * CW + c] = run;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      double off = 0.0;
+      for (int w = 0; w < sg; ++w) off += segs[(t * kF2Segs + w) * CW + c];
+#pragma unroll
+      for (int s = 0; s < kF2Seg; ++s) carry[t][s] += v[t][s] + off;
+      if (f.plane[t] != nullptr) {  // slab carry capture (scanned over axes 0 and 1)
+#pragma unroll
+        for (int s = 0; s < kF2Seg; ++s) {
+          const int p = p0 + s;
+          if (p < D1 && (f.rev1[t] ? D1 - 1 - p : p) == f.plane_idx[t])
+            f.plane[t][i0 * B + b] = carry[t][s];
+        }
+      }
+    }
+    if (swap) {  // lattice 1 back to cell order, into its (consumed) slab
+      double *sl = buf + (cur * (NT + 1) + (NT - 1)) * slab;
+#pragma unroll
+      for (int s = 0; s < kF2Seg; ++s) {
+        const int p = p0 + s;
+        if (p < D1) sl[(f.rev1[1] ? (int)D1 - 1 - p : p) * CW + c] = carry[NT - 1][s];
+      }
+      __syncthreads();
+    }
+    const double z00 = f.zf[0][f.zoff[0] + i0] * zb[0];
+    const double z01 = NT > 1 ? f.zf[NT - 1][f.zoff[0] + i0] * zb[NT - 1] : 0.0;
+    const double *sl1 = buf + (cur * (NT + 1) + (NT - 1)) * slab;
+    const double *slo = buf + (cur * (NT + 1) + NT) * slab;
+#pragma unroll
+    for (int s = 0; s < kF2Seg; ++s) {
+      const int p = p0 + s;
+      if (p >= D1) continue;
+      const int i1 = f.rev1[0] ? (int)D1 - 1 - p : p;
+      double val = (z00 * z1[i1]) * carry[0][s];
+      if (NT > 1) {
+        const double c1 = swap ? sl1[i1 * CW + c] : carry[NT - 1][s];
+        val += (z01 * z1[(NT - 1) * (int)D1 + i1]) * c1;
+      }
+      double r = f.accumulate ? slo[i1 * CW + c] + val : val;
+      if (f.apply_scale) r = r * f.scale;
+      f.out[(i0 * D1 + i1) * B + b] = r;
+    }
+    __syncthreads();  // the slab buffer `cur` is refilled next row
+  }
+}
+
+int launch_final2d(const Final2D &f, bool rev0, cudaStream_t st) {
+  int64_t B = 1;
+  for (int k = 2; k < f.d; ++k) B *= f.dims[k];
+  const unsigned grid = (unsigned)(B / kF2Cols);
+  const size_t smem = (size_t)(2 * (f.nt + 1) * f.dims[1] * kF2Cols + f.nt * kF2Segs * kF2Cols +
+                               f.nt * f.dims[1]) * sizeof(double);
+  FCG_PROF("kde_final_group", st);
+  auto go = [&](auto kern) -> int {
+    FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, 256, smem, st>>>(f);
+    FCG_LAUNCH_CHECK();
+    return FCG_OK;
+  };
+  if (f.nt == 1) return rev0 ? go(final2d_kernel<1, true>) : go(final2d_kernel<1, false>);
+  return rev0 ? go(final2d_kernel<2, true>) : go(final2d_kernel<2, false>);
+}
+
 int launch_final_multi(const MultiFinal &f, bool rev, cudaStream_t st) {
   int64_t B = 1;
   for (int k = 1; k < f.d; ++k) B *= f.dims[k];
@@ -1695,6 +1864,12 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   for (int s0 = 0; s0 < 2; ++s0) {
     for (int b0 = 0; b0 < per0; b0 += nbatch) {
       const int nt = (per0 - b0) < nbatch ? (per0 - b0) : nbatch;
+      // axes 1 and 0 in one pass (final2d_kernel) when the batch, axis 1 and the columns fit
+      int64_t bcols = 1;
+      for (int k = 2; k < d; ++k) bcols *= m[k];
+      const bool fuse01 = d >= 4 && kz >= 2 && nt <= 2 && m[1] <= kF2Seg * kF2Segs &&
+                          bcols % kF2Cols == 0;
+      Final2D f2{};
       MultiFinal f{};
       f.nt = nt;
       f.d = d;
@@ -1755,8 +1930,13 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
           FCG_LAUNCH_CHECK();
         }
         Epi inplace;
-        for (int ax = d - 3; ax >= 1; --ax)
+        for (int ax = d - 3; ax >= (fuse01 ? 2 : 1); --ax)
           FCG_TRY(scan_axis<double>(lat, s, ax, rev[ax], inplace, scratch, st));
+        f2.lat[tt] = lat;
+        f2.zf[tt] = zf;
+        f2.plane[tt] = planes ? planes + (int64_t)gl * plane_sz : nullptr;
+        f2.plane_idx[tt] = planes ? (rev[1] ? 0 : m[1] - 1) : -1;
+        f2.rev1[tt] = rev[1] ? 1 : 0;
         f.lat[tt] = lat;
         f.zf[tt] = zf;
         f.plane[tt] = planes ? planes + (int64_t)gl * plane_sz : nullptr;
@@ -1766,7 +1946,22 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
       f.apply_scale = (s0 == 1 && b0 + nt >= per0) ? 1 : 0;
       f.scale = scale;
       f.out = out;
-      FCG_TRY(launch_final_multi(f, s0 == 1, st));
+      if (fuse01) {
+        f2.nt = nt;
+        f2.d = d;
+        f2.kz = kz;
+        for (int k = 0; k < d; ++k) {
+          f2.zoff[k] = zoff[k];
+          f2.dims[k] = m[k];
+        }
+        f2.accumulate = f.accumulate;
+        f2.apply_scale = f.apply_scale;
+        f2.scale = scale;
+        f2.out = out;
+        FCG_TRY(launch_final2d(f2, s0 == 1, st));
+      } else {
+        FCG_TRY(launch_final_multi(f, s0 == 1, st));
+      }
     }
   }
   return FCG_OK;
