@@ -1486,6 +1486,96 @@ int launch_final2d(const Final2D &f, bool rev0, cudaStream_t st) {
   return rev0 ? go(final2d_kernel<2, true>) : go(final2d_kernel<2, false>);
 }
 
+// Fused axis-1 + axis-0 final pass of the partitioned ECDF (d >= 4): int32 counts in, the
+// output epilogue (count / N as fp64, or int64 counts) out, 16 columns per CTA as in
+// final2d_kernel; the axis-1 lattice pass disappears.
+template <bool REV0, bool REV1, int EK>
+__global__ void __launch_bounds__(256, 2) ecdf_final2d_kernel(const int32_t *__restrict__ lat,
+                                                              int64_t D0, int64_t D1, int64_t B,
+                                                              double div, void *out) {
+  extern __shared__ __align__(16) int32_t e2_smem[];
+  constexpr int CW = kF2Cols;
+  const int slab = (int)D1 * CW;
+  int32_t *buf = e2_smem;                 // [2][D1][CW]
+  int32_t *segs = buf + 2 * slab;         // [kF2Segs][CW]
+  const int c = threadIdx.x % CW, sg = threadIdx.x / CW;
+  const int64_t b0 = (int64_t)blockIdx.x * CW;
+  const int64_t b = b0 + c;
+  auto stage = [&](int64_t jj, int which) {
+    const int64_t i0 = REV0 ? D0 - 1 - jj : jj;
+    int32_t *dst = buf + which * slab;
+    const int32_t *src = lat + (i0 * D1) * B + b0;
+    for (int ch = threadIdx.x; ch < (int)D1 * (CW / 4); ch += blockDim.x) {  // 16-byte chunks
+      const int r = ch / (CW / 4), q = ch % (CW / 4);
+      cp_async16(dst + r * CW + q * 4, src + (int64_t)r * B + q * 4);
+    }
+    cp_async_commit();
+  };
+  int32_t carry[kF2Seg];
+#pragma unroll
+  for (int s = 0; s < kF2Seg; ++s) carry[s] = 0;
+  const int p0 = sg * kF2Seg;
+  stage(0, 0);
+  for (int64_t jj = 0; jj < D0; ++jj) {
+    const int64_t i0 = REV0 ? D0 - 1 - jj : jj;
+    const int cur = (int)(jj & 1);
+    if (jj + 1 < D0) stage(jj + 1, cur ^ 1);
+    else cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();
+    const int32_t *sl = buf + cur * slab;
+    int32_t v[kF2Seg];
+    int32_t run = 0;
+#pragma unroll
+    for (int s = 0; s < kF2Seg; ++s) {
+      const int p = p0 + s;
+      if (p < D1) run += sl[(REV1 ? (int)D1 - 1 - p : p) * CW + c];
+      v[s] = run;
+    }
+    segs[sg * CW + c] = run;
+    __syncthreads();
+    int32_t off = 0;
+    for (int w = 0; w < sg; ++w) off += segs[w * CW + c];
+#pragma unroll
+    for (int s = 0; s < kF2Seg; ++s) {
+      const int p = p0 + s;
+      carry[s] += v[s] + off;
+      if (p >= D1) continue;
+      const int64_t i1 = REV1 ? D1 - 1 - p : p;
+      const int64_t o = (i0 * D1 + i1) * B + b;
+      if constexpr (EK == EPI_I64) {
+        static_cast<int64_t *>(out)[o] = (int64_t)carry[s];
+      } else {
+        double r = (double)carry[s];
+        if (div > 0.0) r = r / div;  // the single IEEE division of fastsum.py:87-88
+        static_cast<double *>(out)[o] = r;
+      }
+    }
+    __syncthreads();  // slab `cur` and the segment totals are rewritten next row
+  }
+}
+
+int launch_ecdf_final2d(const int32_t *lat, const int64_t *dims, int d, bool rev0, bool rev1,
+                        const Epi &epi, cudaStream_t st) {
+  int64_t B = 1;
+  for (int k = 2; k < d; ++k) B *= dims[k];
+  const unsigned grid = (unsigned)(B / kF2Cols);
+  const size_t smem = (size_t)(2 * dims[1] * kF2Cols + kF2Segs * kF2Cols) * sizeof(int32_t);
+  FCG_PROF("scan_lines_final", st);
+  auto go = [&](auto kern) -> int {
+    FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, 256, smem, st>>>(lat, dims[0], dims[1], B, epi.div, epi.out);
+    FCG_LAUNCH_CHECK();
+    return FCG_OK;
+  };
+  if (epi.kind == EPI_I64) {
+    if (rev0) return rev1 ? go(ecdf_final2d_kernel<true, true, EPI_I64>) : go(ecdf_final2d_kernel<true, false, EPI_I64>);
+    return rev1 ? go(ecdf_final2d_kernel<false, true, EPI_I64>) : go(ecdf_final2d_kernel<false, false, EPI_I64>);
+  }
+  if (rev0) return rev1 ? go(ecdf_final2d_kernel<true, true, EPI_F64>) : go(ecdf_final2d_kernel<true, false, EPI_F64>);
+  return rev1 ? go(ecdf_final2d_kernel<false, true, EPI_F64>) : go(ecdf_final2d_kernel<false, false, EPI_F64>);
+}
+
 int launch_final_multi(const MultiFinal &f, bool rev, cudaStream_t st) {
   int64_t B = 1;
   for (int k = 1; k < f.d; ++k) B *= f.dims[k];
@@ -1640,8 +1730,13 @@ int ecdf_partitioned(const double *x, int64_t n, const double *knots, const BinG
     FCG_LAUNCH_CHECK();
   }
   Epi inplace;
-  for (int ax = d - 3; ax >= 1; --ax)
+  int64_t bcols = 1;
+  for (int k = 2; k < d; ++k) bcols *= s.dims[k];
+  const bool fuse01 = d >= 4 && (epi.kind == EPI_F64 || epi.kind == EPI_I64) &&
+                      s.dims[1] <= kF2Seg * kF2Segs && bcols % kF2Cols == 0;
+  for (int ax = d - 3; ax >= (fuse01 ? 2 : 1); --ax)
     FCG_TRY(scan_axis<int32_t>(lat, s, ax, rev[ax], inplace, scratch, st));
+  if (fuse01) return launch_ecdf_final2d(lat, s.dims, d, rev[0], rev[1], epi, st);
   return scan_axis<int32_t>(lat, s, 0, rev[0], epi, scratch, st);
 }
 
