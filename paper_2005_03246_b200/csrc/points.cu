@@ -546,6 +546,46 @@ struct GrpArrays {
   int32_t *inv;      // source id -> group-order index
 };
 
+// per point (input order): both dimension positions, coordinates and weights in one 40-byte
+// record, so the two group-order gathers read one record per point instead of six arrays
+struct PtRec {
+  int32_t p0, p1;
+  double x0, x1, w0, w1;
+};
+
+__global__ void pack_points_kernel(const int32_t *__restrict__ pos0, const int32_t *__restrict__ pos1,
+                                   const double *__restrict__ x, const double *__restrict__ w,
+                                   int nw, int64_t n, PtRec *__restrict__ rec) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    PtRec r;
+    r.p0 = pos0[i];
+    r.p1 = pos1[i];
+    const double2 xv = reinterpret_cast<const double2 *>(x)[i];
+    r.x0 = xv.x;
+    r.x1 = xv.y;
+    r.w0 = w ? w[i] : 1.0;
+    r.w1 = nw > 1 ? (w ? w[n + i] : 1.0) : 0.0;
+    rec[i] = r;
+  }
+}
+
+// group order k <- point order[k]; chunk grouping: slot = p1, rank = p0 (block: swapped)
+__global__ void group_gather_packed(const int32_t *__restrict__ order, const PtRec *__restrict__ rec,
+                                    int chunk, int nw, int64_t n, GrpArrays g) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = order[k];
+    const PtRec r = rec[i];
+    g.slot[k] = chunk ? r.p1 : r.p0;
+    g.rankpos[k] = chunk ? r.p0 : r.p1;
+    reinterpret_cast<double2 *>(g.x)[k] = make_double2(r.x0, r.x1);
+    g.w[k] = r.w0;
+    if (nw > 1) g.w[n + k] = r.w1;
+    g.inv[i] = (int32_t)k;
+  }
+}
+
 __global__ void group_gather_kernel(const int32_t *__restrict__ order,
                                     const int32_t *__restrict__ pos_slot,
                                     const int32_t *__restrict__ pos_rank,
@@ -1011,6 +1051,7 @@ int sorted_exclusive(const double *vals, const int32_t *order, int64_t n, bool r
 struct SelfWs {
   GrpArrays gc, gb;
   double *accq;
+  PtRec *rec;
 };
 
 void carve_self(Workspace &W, SelfWs &q, int64_t n, int nw) {
@@ -1025,6 +1066,7 @@ void carve_self(Workspace &W, SelfWs &q, int64_t n, int nw) {
     g->inv = W.take<int32_t>(n);
   }
   q.accq = W.take<double>((size_t)n * nw);
+  q.rec = W.take<PtRec>(n);
 }
 
 // Strict-dominance sums at the points for d = 2 in group order: the plain ECDF (kde = 0, one
@@ -1037,8 +1079,14 @@ int self_dom2d(const double *x, const double *w, int64_t n, int nw, int kde, con
   const int g = grid_for(n, 256);
   {
     FCG_PROF("pts_group_gather", st);
-    group_gather_kernel<<<g, 256, 0, st>>>(p.bychunk, p.r[1].pos, p.r[0].pos, x, w, nw, n, q.gc);
-    group_gather_kernel<<<g, 256, 0, st>>>(p.byblock, p.r[0].pos, p.r[1].pos, x, w, nw, n, q.gb);
+    if ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && nw <= 2) {
+      pack_points_kernel<<<g, 256, 0, st>>>(p.r[0].pos, p.r[1].pos, x, w, nw, n, q.rec);
+      group_gather_packed<<<g, 256, 0, st>>>(p.bychunk, q.rec, 1, nw, n, q.gc);
+      group_gather_packed<<<g, 256, 0, st>>>(p.byblock, q.rec, 0, nw, n, q.gb);
+    } else {
+      group_gather_kernel<<<g, 256, 0, st>>>(p.bychunk, p.r[1].pos, p.r[0].pos, x, w, nw, n, q.gc);
+      group_gather_kernel<<<g, 256, 0, st>>>(p.byblock, p.r[0].pos, p.r[1].pos, x, w, nw, n, q.gb);
+    }
     FCG_LAUNCH_CHECK();
   }
   FCG_CUDA_TRY(cudaMemsetAsync(q.gc.acc, 0, (size_t)n * nw * 8, st));
