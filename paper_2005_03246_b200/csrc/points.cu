@@ -892,10 +892,14 @@ void carve(Workspace &W, PtsWs &p, int64_t n, int d, int nch, bool need_dom, boo
   if (need_kde) p.expo = W.take<double>(n);
 }
 
-int rank_dim(const double *x, int64_t n, int d, int k, PtsWs &p, cudaStream_t st) {
+// ties = false: only the order and the positions (distinct coordinates, the self path)
+int rank_dim(const double *x, int64_t n, int d, int k, PtsWs &p, cudaStream_t st, bool ties = true) {
   FCG_TRY(radix_init_f64(x + k, n, d, p.k, p.v, st));
   FCG_TRY(radix_sort_pairs_pruned(p.k, p.v, n, p.rw, st));
   FCG_CUDA_TRY(cudaMemcpyAsync(p.r[k].order, p.v, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+  if (!ties)
+    return rank_outputs(p.k, p.v, n, p.r[k].pos, nullptr, nullptr, nullptr, p.heads, p.start,
+                        p.rw.partial, nullptr, st);
   return rank_outputs(p.k, p.v, n, p.r[k].pos, p.r[k].lower, p.r[k].upper, p.r[k].dense, p.heads,
                       p.start, p.rw.partial, p.ndist + k, st);
 }
@@ -1021,8 +1025,8 @@ int dom2d(PtsWs &p, int64_t n, int nch, int f0, int f1, const double *psi, doubl
 }
 
 int prep2d(const double *x, int64_t n, PtsWs &p, cudaStream_t st) {
-  FCG_TRY(rank_dim(x, n, 2, 0, p, st));
-  FCG_TRY(rank_dim(x, n, 2, 1, p, st));
+  FCG_TRY(rank_dim(x, n, 2, 0, p, st, false));
+  FCG_TRY(rank_dim(x, n, 2, 1, p, st, false));
   FCG_TRY(group_by(p.r[0].order, p.r[1].pos, n, p.P, p.bychunk, p, st));
   FCG_TRY(group_by(p.r[1].order, p.r[0].pos, n, p.P, p.byblock, p, st));
   return FCG_OK;

@@ -447,6 +447,7 @@ int rank_outputs(const uint64_t *sorted_keys, const int32_t *order, int64_t n, i
     rank_heads_kernel<<<g, 256, 0, st>>>(sorted_keys, order, n, heads, pos);
     FCG_LAUNCH_CHECK();
   }
+  if (!lower && !upper && !dense && !n_distinct_dev) return FCG_OK;  // positions only
   FCG_TRY(scan_i32(heads, heads, n, true, partial, st));
   FCG_PROF("rank_scatter", st);
   rank_start_kernel<<<g, 256, 0, st>>>(sorted_keys, heads, n, start, n_distinct_dev);
