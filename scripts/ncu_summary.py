@@ -17,7 +17,8 @@ SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12,
 
 
 # ncu kernel name -> the launch profiler's scope name (what bench.py's roofline reports)
-SCOPES = [(r"^plane_kde", "plane_kde"), (r"^kde_gather", "kde_materialize"),
+SCOPES = [(r"^ecdf_final2d", "scan_lines_final"), (r"^final2d", "kde_final_group"),
+          (r"^group_gather_packed|^pack_points", "pts_group_gather"), (r"^plane_kde", "plane_kde"), (r"^kde_gather", "kde_materialize"),
           (r"digit_stage", "part_emit"), (r"digit_hist", "part_hist"), (r"^kde_materialize", "kde_materialize"),
           (r"^kde_final_multi", "kde_final_group"), (r"^lines_kernel<\w+, \d, 1>", "scan_lines_final"),
           (r"^lines_kernel", "scan_lines"), (r"^rows_kernel", "scan_rows"),
@@ -43,7 +44,17 @@ def short(name):
 
 
 def main():
-    wl, path = sys.argv[1], sys.argv[2]
+    wl = sys.argv[1]
+    paths = [a for a in sys.argv[2:] if a.endswith(".csv") and not a.endswith(".json")]
+    if "--traffic" in sys.argv:
+        paths = [a for a in paths if a != sys.argv[sys.argv.index("--traffic") + 1]]
+    out = []
+    for path in paths:
+        out.extend(read_raw(path))
+    emit(wl, out)
+
+
+def read_raw(path):
     rows = list(csv.reader(open(path)))
     head, units = rows[0], rows[1]
     idx = {c: i for i, c in enumerate(head)}
@@ -62,6 +73,10 @@ def main():
                 v = v * SCALE.get(u, 1.0) / 1e9
             rec[col] = v
         out.append(rec)
+    return out
+
+
+def emit(wl, out):
     print(f"# {wl}: ncu --set full --clock-control none (per captured launch)")
     print("kernel,ms,dram_read_GB,dram_write_GB,mem_pct,sm_pct,occupancy_pct,regs,grid,block")
     for o in out:
