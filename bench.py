@@ -266,6 +266,7 @@ class GridWorkload:
         xp = torch.from_numpy(self.pts).pin_memory()
         self.p_x = xp
         self.side_stream = torch.cuda.Stream()
+        self.ones_dev = torch.ones(1, device="cuda")
         self.p_unit = fcb.Sample(xp, torch.ones(1), None, True)
         nloc = int(np.prod(self.m))
         self.out_pinned = torch.empty(nloc, dtype=torch.float64).pin_memory()
@@ -306,13 +307,16 @@ class GridWorkload:
         main = torch.cuda.current_stream()
         side = self.side_stream
         xd = self.p_x.to("cuda", non_blocking=True)
-        s_unit = self.fcb.Sample(xd, torch.ones(1, device="cuda"), None, True)
+        s_unit = self.fcb.Sample(xd, self.ones_dev, None, True)
         if self.do_kde:
             side.wait_stream(main)
             with torch.cuda.stream(side):
                 yd = self.p_yv.to("cuda", non_blocking=True)
             ev_y = side.record_event()
-        if self.do_ecdf:
+        if self.do_ecdf and not self.do_kde:
+            v = self._ecdf(s_unit)
+            self.out_pinned[: v.numel()].copy_(v, non_blocking=True)
+        elif self.do_ecdf:
             v = self._ecdf(s_unit)
             ev_e = main.record_event()
             side.wait_event(ev_e)
@@ -324,7 +328,8 @@ class GridWorkload:
             yd.record_stream(main)
             v = self._kde(self.fcb.Sample(xd, yd, None, False))
             self.out2_pinned[: v.numel()].copy_(v, non_blocking=True)
-        main.wait_stream(side)
+        if self.do_kde:
+            main.wait_stream(side)
 
     def bytes_per_launch(self):
         # per rank: ~1/world of the points and of the lattice (axis-1 slab) when sharded
