@@ -249,7 +249,9 @@ def test_cfg3_full_bit_exact(oracle, cfg_meta):
 
 # planes >= 2 x 148 SMs so the partitioned route is taken; (300, 700, 300) needs 9 row blocks
 @pytest.mark.parametrize("dims,delta", [((300, 53, 61), (1, -1, 1)), ((40, 9, 150, 77), (-1, 1, 1, -1)),
-                                        ((300, 700, 300), (1, 1, -1)), ((12, 10, 5, 7, 9), (1, 1, 1, 1, 1))])
+                                        ((300, 700, 300), (1, 1, -1)), ((12, 10, 5, 7, 9), (1, 1, 1, 1, 1)),
+                                        # d = 4 with 16 | columns: the fused axis-1 + axis-0 final
+                                        ((37, 11, 24, 40), (1, -1, -1, 1)), ((30, 13, 16, 64), (-1, 1, 1, -1))])
 def test_partitioned_ecdf_esf_vs_oracle(dims, delta, oracle):
     oracle.set_threads(0)
     d = len(dims)
@@ -293,8 +295,11 @@ def test_kde_matern32_vs_oracle(d, oracle):
     assert_rel(got, oracle.kde_fastsum_matern32(x, w, knots, h), REL_KDE)
 
 
-@pytest.mark.parametrize("dims", [(320, 17, 40), (20, 16, 33, 21)])
+@pytest.mark.parametrize("dims", [(320, 17, 40), (20, 16, 33, 21), (300, 40, 128), (24, 20, 16, 128),
+                                  (19, 21, 8, 64)])
 def test_partitioned_kde_vs_oracle(dims, oracle):
+    """Partitioned KDE paths vs the oracle: per-group plane kernel (W = 40, 21), all-groups
+    plane kernel (W = 64, 128) with the fused axis-1 + axis-0 final (d = 4, 16 | columns)."""
     oracle.set_threads(0)
     d = len(dims)
     rng = np.random.default_rng(7 * sum(dims))
