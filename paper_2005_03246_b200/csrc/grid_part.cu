@@ -417,7 +417,6 @@ struct KdeGroup {
   unsigned fmask[2];                 // factored record fields multiplied into psi per phase
   int nf[2];                         // ... as a list (fast path)
   int fidx[2][FCG_MAX_DIM + 1];
-  int exp;                           // profiling experiments (FCG_KDE_EXP): 1 no records, 2 no walk
 };
 
 // ---- accumulation of cell-sorted records into the two row-block tiles -------------------
@@ -802,7 +801,7 @@ __global__ void __launch_bounds__(kKdeThreads, 2) plane_kde_group_kernel(
       T.swz = SE > 0;
       const int nwin = (q1 - q0 + 31) >> 5;
       const int per = (nwin + nw - 1) / nw;
-      const int wb = warp * per, we = (t.exp & 1) ? wb : min(nwin, wb + per);
+      const int wb = warp * per, we = min(nwin, wb + per);
       const int nf = factored ? t.nf[ph] : 0;
       if (nf >= 1 && nf <= 5) {
         AccParams P;
@@ -831,8 +830,7 @@ __global__ void __launch_bounds__(kKdeThreads, 2) plane_kde_group_kernel(
       }
       __syncthreads();
       double *g = plane_out + (int64_t)clo * W;
-      if (t.exp & 2) {
-      } else if constexpr (SE > 0) {
+      if constexpr (SE > 0) {
         kde_tiles_walk<SE>(tp, tm, cp, cm, seg, seg + nw * W, nr, rneg, zr ? zr + clo : nullptr, t.zcp, t.zcm, g,
                            ph);
       } else {
@@ -870,7 +868,6 @@ struct KdeAll {
   int row_split;              // 1: each row sign has its own lattice (slab planes at d = 3)
   const double *zr_pos, *zr_neg, *zc_pos, *zc_neg;
   double *lat[16];            // output lattice of (group, row sign) -> lat[row_split ? 2g+ph : g]
-  int exp;                    // profiling experiments (FCG_KDE_EXP): 1 no records, 2 no walk
 };
 
 template <int NG>
@@ -991,7 +988,7 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
           }
         };
         const int32_t sb = run_start(q0 + warp * per);
-        const int32_t se = (t.exp & 1) ? sb : run_start(q0 + (warp + 1) * per);
+        const int32_t se = run_start(q0 + (warp + 1) * per);
         uint32_t ckey = 0xFFFFFFFFu;
         AllVals<NG> cv;
 #pragma unroll
@@ -1069,7 +1066,7 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
       }
       __syncthreads();
       // walk: warp g owns group g's tile pair
-      if (warp < NG && !(t.exp & 2)) {
+      if (warp < NG) {
         const int g = warp;
         double *tp = tiles + (size_t)(2 * g) * tile_elems;
         double *tm = tp + tile_elems;
@@ -1926,7 +1923,6 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
     ta.cell_bits = pl.cell_bits;
     ta.col_bits = pl.col_bits;
     ta.row_split = kz > kr ? 1 : 0;
-    ta.exp = getenv("FCG_KDE_EXP") ? atoi(getenv("FCG_KDE_EXP")) : 0;
     ta.zr_pos = zpos + zoff[kr];
     ta.zr_neg = zneg + zoff[kr];
     ta.zc_pos = zpos + zoff[kc];
@@ -2016,7 +2012,6 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
         t.zcm = zneg + zoff[kc];
         t.cell_bits = pl.cell_bits;
         t.col_bits = pl.col_bits;
-        t.exp = getenv("FCG_KDE_EXP") ? atoi(getenv("FCG_KDE_EXP")) : 0;
         FCG_TRY(launch_kde_zf(knots, d, m, centre, h, gl, zf, st));
         if (!pl.all) {
           FCG_PROF("plane_kde", st);
