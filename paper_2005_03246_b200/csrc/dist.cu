@@ -3,6 +3,7 @@
 // cell and finish a slab with the carry plane the ranks exchange over NCCL.
 #include "bin.cuh"
 #include "common.cuh"
+#include "partition.cuh"
 #include "sort.cuh"
 
 namespace fcg {
@@ -63,6 +64,32 @@ __global__ void owner_counts_kernel(const uint32_t *__restrict__ keys, int64_t n
   start[r] = lo;
 }
 
+// routing records: the point's row and its weight (split again on the way out)
+template <int D>
+struct RouteBuild {
+  static constexpr int kD = D;
+  __device__ __forceinline__ void operator()(const double *xi, double wi, double *out) const {
+#pragma unroll
+    for (int k = 0; k < D; ++k) out[k] = xi[k];
+    out[D] = wi;
+  }
+};
+
+// start[r] = first position of owner r in the partitioned order (digit-major scanned counts)
+__global__ void route_starts_kernel(const int32_t *__restrict__ hist, int64_t tiles, int G,
+                                    int64_t *__restrict__ start) {
+  const int r = threadIdx.x;
+  if (r <= G) start[r] = hist[(int64_t)r * tiles];
+}
+
+template <int D>
+int route_partition(const uint32_t *keys, int64_t n, const double *x, const double *w,
+                    double *x_out, double *w_out, int32_t *hist, int32_t *partial, cudaStream_t st) {
+  RouteBuild<D> rb;
+  return digit_partition_build<RouteBuild<D>, D + 1>(keys, n, 0, x, w, rb, x_out, nullptr, nullptr,
+                                                     hist, partial, st, w_out, "dist_partition");
+}
+
 // out[a][j][b] = (local[a][j][b] + carry[a][b]) / div   (div <= 0: no division)
 template <typename T>
 __global__ void slab_finish_kernel(const T *__restrict__ local, const T *__restrict__ carry,
@@ -111,15 +138,15 @@ extern "C" int fcg_partition_rows(const double *x, int64_t n, int32_t d, const d
                                   const int32_t *owner, int32_t G, double *x_out, double *w_out,
                                   int64_t *counts, void *ws, size_t *ws_bytes, void *stream) {
   if (G < 1 || G > 64) return fail(FCG_EUNSUPPORTED, "1..64 owners supported");
+  if (d < 1 || d > FCG_MAX_DIM) return fail(FCG_EINVAL, "dimension out of range");
   Workspace W(ws);
   uint32_t *keys = W.take<uint32_t>(n);
   int32_t *vals = W.take<int32_t>(n);
-  RadixWs rw;
-  rw.keys_alt = reinterpret_cast<uint64_t *>(W.take<uint32_t>(n));
-  rw.vals_alt = W.take<int32_t>(n);
-  rw.hist = W.take<int32_t>(radix_ws_hist_elems(n));
-  rw.partial = W.take<int32_t>(scan_ws_partial_elems(256 * (n / kSortTile + 1) + 2));
+  const size_t hist_elems = digit_hist_elems(n);
+  int32_t *hist = W.take<int32_t>(hist_elems);
+  int32_t *partial = W.take<int32_t>(scan_ws_partial_elems((int64_t)hist_elems + 2));
   int64_t *start = W.take<int64_t>(G + 1);
+  double *w_scratch = W.take<double>(w_out ? 0 : n);  // unit weights: the routed w is dropped
   if (ws == nullptr) {
     *ws_bytes = W.bytes();
     return FCG_OK;
@@ -131,11 +158,23 @@ extern "C" int fcg_partition_rows(const double *x, int64_t n, int32_t d, const d
       owner_keys_kernel<<<grid_for(n, 256), 256, 0, st>>>(owner, n, keys, vals);
       FCG_LAUNCH_CHECK();
     }
-    FCG_TRY(radix_sort_pairs<uint32_t>(keys, vals, n, 0, 8, rw, st));
-    FCG_PROF("dist_partition", st);
-    gather_rows_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, w, n, d, vals, x_out, w_out);
-    FCG_LAUNCH_CHECK();
-    owner_counts_kernel<<<1, 128, 0, st>>>(keys, n, G, start);
+    // one payload-carrying pass: rows and weights read once (coalesced), written by owner
+    if ((d % 2 == 0) && (reinterpret_cast<uintptr_t>(x) & 15) != 0)
+      return fail(FCG_EINVAL, "points must be 16-byte aligned");
+    double *wo = w_out ? w_out : w_scratch;
+    int rc;
+    switch (d) {
+      case 1: rc = route_partition<1>(keys, n, x, w, x_out, wo, hist, partial, st); break;
+      case 2: rc = route_partition<2>(keys, n, x, w, x_out, wo, hist, partial, st); break;
+      case 3: rc = route_partition<3>(keys, n, x, w, x_out, wo, hist, partial, st); break;
+      case 4: rc = route_partition<4>(keys, n, x, w, x_out, wo, hist, partial, st); break;
+      case 5: rc = route_partition<5>(keys, n, x, w, x_out, wo, hist, partial, st); break;
+      case 6: rc = route_partition<6>(keys, n, x, w, x_out, wo, hist, partial, st); break;
+      case 7: rc = route_partition<7>(keys, n, x, w, x_out, wo, hist, partial, st); break;
+      default: rc = route_partition<8>(keys, n, x, w, x_out, wo, hist, partial, st); break;
+    }
+    FCG_TRY(rc);
+    route_starts_kernel<<<1, 128, 0, st>>>(hist, ceil_div(n, kPartTile), G, start);
     FCG_LAUNCH_CHECK();
   } else {
     FCG_CUDA_TRY(cudaMemsetAsync(start, 0, (G + 1) * sizeof(int64_t), st));

@@ -22,7 +22,7 @@ __device__ __forceinline__ unsigned lane_lt() {
   return m;
 }
 
-__global__ void __launch_bounds__(kPartThreads) digit_hist_kernel(const uint32_t *__restrict__ keys,
+static __global__ void __launch_bounds__(kPartThreads) digit_hist_kernel(const uint32_t *__restrict__ keys,
                                                                   int64_t n, int shift,
                                                                   int32_t *__restrict__ hist,
                                                                   int64_t tiles) {
@@ -49,7 +49,8 @@ template <class Build, int WORDS>
 __global__ void __launch_bounds__(kPartThreads, 2) digit_stage_kernel(
     const uint32_t *__restrict__ keys, int64_t n, int shift, const int32_t *__restrict__ offs,
     int64_t tiles, const double *__restrict__ x, const double *__restrict__ w, Build build,
-    double *__restrict__ rec_out, uint32_t *__restrict__ keys_out, int32_t *__restrict__ slot_out) {
+    double *__restrict__ rec_out, uint32_t *__restrict__ keys_out, int32_t *__restrict__ slot_out,
+    double *__restrict__ last_out) {
   constexpr int D = Build::kD;
   extern __shared__ __align__(16) unsigned char ps_smem[];
   double *s_rec = reinterpret_cast<double *>(ps_smem);                       // [tile][WORDS]
@@ -136,19 +137,38 @@ __global__ void __launch_bounds__(kPartThreads, 2) digit_stage_kernel(
     }
   }
   __syncthreads();
-  for (int pos = threadIdx.x; pos < tile_n; pos += kPartThreads) {
-    const uint32_t key = s_key[pos];
-    const unsigned dig = (key >> shift) & 0xFFu;
-    const int64_t dst = (int64_t)s_goff[dig] + (pos - s_tstart[dig]);
-    keys_out[dst] = key;
-    slot_out[dst] = (int32_t)dst;
+  if (keys_out || slot_out) {
+    for (int pos = threadIdx.x; pos < tile_n; pos += kPartThreads) {
+      const uint32_t key = s_key[pos];
+      const unsigned dig = (key >> shift) & 0xFFu;
+      const int64_t dst = (int64_t)s_goff[dig] + (pos - s_tstart[dig]);
+      if (keys_out) keys_out[dst] = key;
+      if (slot_out) slot_out[dst] = (int32_t)dst;
+    }
   }
-  const int tw = tile_n * WORDS;
-  for (int idx = threadIdx.x; idx < tw; idx += kPartThreads) {
-    const int pos = idx / WORDS;  // compile-time divisor
-    const unsigned dig = (s_key[pos] >> shift) & 0xFFu;
-    const int64_t dst = (int64_t)s_goff[dig] + (pos - s_tstart[dig]);
-    rec_out[dst * WORDS + (idx - pos * WORDS)] = s_rec[idx];
+  if (last_out == nullptr) {
+    const int tw = tile_n * WORDS;
+    for (int idx = threadIdx.x; idx < tw; idx += kPartThreads) {
+      const int pos = idx / WORDS;  // compile-time divisor
+      const unsigned dig = (s_key[pos] >> shift) & 0xFFu;
+      const int64_t dst = (int64_t)s_goff[dig] + (pos - s_tstart[dig]);
+      rec_out[dst * WORDS + (idx - pos * WORDS)] = s_rec[idx];
+    }
+  } else {  // split records: the first WORDS-1 words to rec_out, the last word to last_out
+    constexpr int W1 = WORDS - 1;
+    const int tw = tile_n * W1;
+    for (int idx = threadIdx.x; idx < tw; idx += kPartThreads) {
+      const int pos = idx / W1;
+      const int wd = idx - pos * W1;
+      const unsigned dig = (s_key[pos] >> shift) & 0xFFu;
+      const int64_t dst = (int64_t)s_goff[dig] + (pos - s_tstart[dig]);
+      rec_out[dst * W1 + wd] = s_rec[pos * WORDS + wd];
+    }
+    for (int pos = threadIdx.x; pos < tile_n; pos += kPartThreads) {
+      const unsigned dig = (s_key[pos] >> shift) & 0xFFu;
+      const int64_t dst = (int64_t)s_goff[dig] + (pos - s_tstart[dig]);
+      last_out[dst] = s_rec[pos * WORDS + W1];
+    }
   }
 }
 
@@ -167,7 +187,8 @@ template <class Build, int WORDS>
 int digit_partition_build(const uint32_t *keys, int64_t n, int shift, const double *x,
                           const double *w, const Build &build, double *rec_out,
                           uint32_t *keys_out, int32_t *slot_out, int32_t *hist, int32_t *partial,
-                          cudaStream_t st) {
+                          cudaStream_t st, double *last_out = nullptr,
+                          const char *label = "part_emit") {
   if (n <= 0) return FCG_OK;
   const int64_t tiles = ceil_div(n, kPartTile);
   {
@@ -177,12 +198,12 @@ int digit_partition_build(const uint32_t *keys, int64_t n, int shift, const doub
     FCG_LAUNCH_CHECK();
   }
   FCG_TRY(scan_i32(hist, hist, 256 * tiles, false, partial, st));
-  FCG_PROF("part_emit", st);
+  FCG_PROF(label, st);
   const size_t sm = digit_stage_smem(WORDS);
   auto kern = part_detail::digit_stage_kernel<Build, WORDS>;
   FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   kern<<<(unsigned)tiles, kPartThreads, sm, st>>>(keys, n, shift, hist, tiles, x, w, build,
-                                                  rec_out, keys_out, slot_out);
+                                                  rec_out, keys_out, slot_out, last_out);
   FCG_LAUNCH_CHECK();
   return FCG_OK;
 }
