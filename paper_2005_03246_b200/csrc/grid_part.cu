@@ -1653,7 +1653,8 @@ void carve_part(Workspace &W, PartBufs &b, int64_t n, int64_t NB) {
 int partition(const double *x, int64_t n, int d, const double *knots, const BinGrid &g,
               const PartGeo &p, int64_t NB, int nbits, PartBufs &b, cudaStream_t st) {
   FCG_TRY(launch_part_bin(x, n, d, knots, g, p, b.keys, b.vals, st));
-  FCG_TRY(radix_sort_pairs<uint32_t>(b.keys, b.vals, n, 0, ((nbits + 7) / 8) * 8, b.rw, st));
+  // equal bucket keys may come out in any order (the plane kernel only groups by bucket)
+  FCG_TRY(radix_sort_pairs<uint32_t>(b.keys, b.vals, n, 0, ((nbits + 7) / 8) * 8, b.rw, st, false));
   FCG_PROF("part_bucket_start", st);
   bucket_start_kernel<<<grid_for(NB + 1, 256, 4), 256, 0, st>>>(b.keys, n, NB, p.cell_bits,
                                                                  b.start);
@@ -1871,7 +1872,8 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
     }
     FCG_TRY(rc);
   }
-  FCG_TRY(radix_sort_pairs<uint32_t>(keys_c, b.vals, n, 0, sort_bits, b.rw, st));
+  // equal keys are the same cell: their order is irrelevant
+  FCG_TRY(radix_sort_pairs<uint32_t>(keys_c, b.vals, n, 0, sort_bits, b.rw, st, false));
   {
     FCG_PROF("part_bucket_start", st);
     bucket_start_kernel<<<grid_for(pl.NB + 1, 256, 4), 256, 0, st>>>(keys_c, n, pl.NB, p.cell_bits,

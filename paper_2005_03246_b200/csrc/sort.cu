@@ -172,7 +172,9 @@ __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const KeyT *__
 // the tile (warp peers via __match_any_sync + per-warp digit counters), staged in shared memory
 // in digit order, then written out so that consecutive threads write consecutive addresses of
 // each digit's run (coalesced) instead of 32 scattered 4-byte stores per warp.
-template <typename KeyT>
+// STABLE = false (first LSD pass of a sort whose equal keys may come out in any order): items
+// are ranked by a shared-memory atomic on their warp's digit counter instead of peer masks.
+template <typename KeyT, bool STABLE>
 __global__ void __launch_bounds__(kSortThreads, 3) radix_scatter_kernel(
     const KeyT *__restrict__ kin, const int32_t *__restrict__ vin, KeyT *__restrict__ kout,
     int32_t *__restrict__ vout, int64_t n, int shift, const int32_t *__restrict__ offs,
@@ -203,18 +205,26 @@ __global__ void __launch_bounds__(kSortThreads, 3) radix_scatter_kernel(
     k[j] = ok ? kin[i] : KeyT(0);
     v[j] = ok ? vin[i] : 0;
   }
+  if constexpr (STABLE) {
 #pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
-    const int64_t i = base + (int64_t)j * 32 + lane;
-    const bool ok = i < n;
-    const unsigned dig = ok ? (unsigned)((k[j] >> shift) & 0xFF) : 256u + lane;
-    const unsigned peers = digit_peers(dig);
-    int32_t before = 0;
-    if (ok) before = s_cnt[warp * 256 + dig];
-    __syncwarp();
-    if (ok && lane == __ffs(peers) - 1) s_cnt[warp * 256 + dig] = before + __popc(peers);
-    __syncwarp();
-    r[j] = before + __popc(peers & lt);
+    for (int j = 0; j < kSortItems; ++j) {
+      const int64_t i = base + (int64_t)j * 32 + lane;
+      const bool ok = i < n;
+      const unsigned dig = ok ? (unsigned)((k[j] >> shift) & 0xFF) : 256u + lane;
+      const unsigned peers = digit_peers(dig);
+      int32_t before = 0;
+      if (ok) before = s_cnt[warp * 256 + dig];
+      __syncwarp();
+      if (ok && lane == __ffs(peers) - 1) s_cnt[warp * 256 + dig] = before + __popc(peers);
+      __syncwarp();
+      r[j] = before + __popc(peers & lt);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+      const int64_t i = base + (int64_t)j * 32 + lane;
+      if (i < n) r[j] = atomicAdd(s_cnt + warp * 256 + (unsigned)((k[j] >> shift) & 0xFF), 1);
+    }
   }
   __syncthreads();
   {
@@ -367,7 +377,7 @@ int radix_init_f64(const double *x, int64_t n, int64_t stride, uint64_t *keys, i
 
 template <typename KeyT>
 static int radix_sort_digits(KeyT *keys, int32_t *vals, int64_t n, uint32_t digit_mask,
-                             const RadixWs &ws, cudaStream_t st) {
+                             const RadixWs &ws, cudaStream_t st, bool stable = true) {
   if (n <= 1) return FCG_OK;
   const int64_t tiles = ceil_div(n, kSortTile);
   KeyT *ka = keys, *kb = reinterpret_cast<KeyT *>(ws.keys_alt);
@@ -385,10 +395,10 @@ static int radix_sort_digits(KeyT *keys, int32_t *vals, int64_t n, uint32_t digi
     {
       FCG_PROF("radix_scatter", st);
       constexpr size_t sm = radix_scatter_smem<KeyT>();
-      FCG_CUDA_TRY(cudaFuncSetAttribute(radix_scatter_kernel<KeyT>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      radix_scatter_kernel<KeyT><<<(unsigned)tiles, kSortThreads, sm, st>>>(ka, va, kb, vb, n, shift,
-                                                                            ws.hist, tiles);
+      // only the first pass may reorder equal keys: later passes must keep the earlier order
+      auto kern = (stable || passes > 0) ? radix_scatter_kernel<KeyT, true> : radix_scatter_kernel<KeyT, false>;
+      FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      kern<<<(unsigned)tiles, kSortThreads, sm, st>>>(ka, va, kb, vb, n, shift, ws.hist, tiles);
       FCG_LAUNCH_CHECK();
     }
     std::swap(ka, kb);
@@ -404,10 +414,10 @@ static int radix_sort_digits(KeyT *keys, int32_t *vals, int64_t n, uint32_t digi
 
 template <typename KeyT>
 int radix_sort_pairs(KeyT *keys, int32_t *vals, int64_t n, int begin_bit, int end_bit,
-                     const RadixWs &ws, cudaStream_t st) {
+                     const RadixWs &ws, cudaStream_t st, bool stable) {
   uint32_t mask = 0;
   for (int shift = begin_bit; shift < end_bit; shift += 8) mask |= 1u << (shift / 8);
-  return radix_sort_digits<KeyT>(keys, vals, n, mask, ws, st);
+  return radix_sort_digits<KeyT>(keys, vals, n, mask, ws, st, stable);
 }
 
 int radix_sort_pairs_pruned(uint64_t *keys, int32_t *vals, int64_t n, const RadixWs &ws,
@@ -433,9 +443,9 @@ int radix_sort_pairs_pruned(uint64_t *keys, int32_t *vals, int64_t n, const Radi
 }
 
 template int radix_sort_pairs<uint64_t>(uint64_t *, int32_t *, int64_t, int, int, const RadixWs &,
-                                        cudaStream_t);
+                                        cudaStream_t, bool);
 template int radix_sort_pairs<uint32_t>(uint32_t *, int32_t *, int64_t, int, int, const RadixWs &,
-                                        cudaStream_t);
+                                        cudaStream_t, bool);
 
 int rank_outputs(const uint64_t *sorted_keys, const int32_t *order, int64_t n, int32_t *pos,
                  int32_t *lower, int32_t *upper, int32_t *dense, int32_t *heads, int32_t *start,
