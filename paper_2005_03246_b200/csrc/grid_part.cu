@@ -1612,6 +1612,79 @@ int bits_for(int64_t v) {  // smallest b with v < 2^b
   return b;
 }
 
+// keys + payloads of one radix tile per CTA, with the tile's histogram of the keys' low byte
+// (the first LSD pass's digit-major histogram, so that pass needs no histogram kernel)
+template <int D>
+__global__ void __launch_bounds__(256) part_bin_tile_kernel(const double *__restrict__ x, int64_t n,
+                                                            int drt, const double *__restrict__ knots,
+                                                            BinGrid g, PartGeo p,
+                                                            uint32_t *__restrict__ keys,
+                                                            int32_t *__restrict__ vals,
+                                                            int32_t *__restrict__ hist,
+                                                            int64_t tiles) {
+  extern __shared__ double s_knots[];
+  __shared__ double s_z0[FCG_MAX_DIM], s_idz[FCG_MAX_DIM];
+  __shared__ int32_t s_hist[8][256];
+  const int d = D > 0 ? D : drt;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x & 31; i < 256; i += 32) s_hist[warp][i] = 0;
+  const double *kb = stage_knots(g, knots, s_knots, s_z0, s_idz);
+  __syncthreads();
+  constexpr int DD = D > 0 ? D : FCG_MAX_DIM;
+  const int64_t tile0 = (int64_t)blockIdx.x * kSortTile;
+  constexpr int U = 4;  // points in flight per thread
+  for (int j0 = 0; j0 < kSortTile; j0 += U * 256) {
+    double xi[U][DD];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = tile0 + j0 + u * 256 + threadIdx.x;
+      const int64_t ii = i < n ? i : 0;
+      if constexpr (D == 4) {
+        const double2 v0 = __ldcs(reinterpret_cast<const double2 *>(x) + 2 * ii);
+        const double2 v1 = __ldcs(reinterpret_cast<const double2 *>(x) + 2 * ii + 1);
+        xi[u][0] = v0.x; xi[u][1] = v0.y; xi[u][2] = v1.x; xi[u][3] = v1.y;
+      } else {
+#pragma unroll
+        for (int k = 0; k < DD; ++k)
+          if (k < d) xi[u][k] = x[ii * d + k];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = tile0 + j0 + u * 256 + threadIdx.x;
+      if (i >= n) continue;
+      uint32_t key;
+      int32_t val;
+      part_key<D>(xi[u], d, kb, g, s_z0, s_idz, p, i, key, val);
+      keys[i] = key;
+      if (vals) vals[i] = val;
+      atomicAdd(&s_hist[warp][key & 0xFFu], 1);
+    }
+  }
+  __syncthreads();
+  int32_t tot = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) tot += s_hist[w][threadIdx.x];
+  hist[(int64_t)threadIdx.x * tiles + blockIdx.x] = tot;
+}
+
+int launch_part_bin_tiles(const double *x, int64_t n, int d, const double *knots, const BinGrid &g,
+                          const PartGeo &p, uint32_t *keys, int32_t *vals, int32_t *hist,
+                          cudaStream_t st) {
+  const size_t smem = g.total_knots <= kSmemKnots ? (size_t)g.total_knots * sizeof(double) : 0;
+  const int64_t tiles = ceil_div(n, kSortTile);
+  FCG_PROF("part_bin", st);
+  const bool al = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  if (d == 4 && al)
+    part_bin_tile_kernel<4><<<(unsigned)tiles, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals, hist, tiles);
+  else if (d == 3)
+    part_bin_tile_kernel<3><<<(unsigned)tiles, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals, hist, tiles);
+  else
+    part_bin_tile_kernel<0><<<(unsigned)tiles, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals, hist, tiles);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}
+
 int launch_part_bin(const double *x, int64_t n, int d, const double *knots, const BinGrid &g,
                     const PartGeo &p, uint32_t *keys, int32_t *vals, cudaStream_t st) {
   const size_t smem = g.total_knots <= kSmemKnots ? (size_t)g.total_knots * sizeof(double) : 0;
@@ -1652,9 +1725,10 @@ void carve_part(Workspace &W, PartBufs &b, int64_t n, int64_t NB) {
 
 int partition(const double *x, int64_t n, int d, const double *knots, const BinGrid &g,
               const PartGeo &p, int64_t NB, int nbits, PartBufs &b, cudaStream_t st) {
-  FCG_TRY(launch_part_bin(x, n, d, knots, g, p, b.keys, b.vals, st));
+  FCG_TRY(launch_part_bin_tiles(x, n, d, knots, g, p, b.keys, b.vals, b.rw.hist, st));
   // equal bucket keys may come out in any order (the plane kernel only groups by bucket)
-  FCG_TRY(radix_sort_pairs<uint32_t>(b.keys, b.vals, n, 0, ((nbits + 7) / 8) * 8, b.rw, st, false));
+  FCG_TRY(radix_sort_pairs<uint32_t>(b.keys, b.vals, n, 0, ((nbits + 7) / 8) * 8, b.rw, st, false,
+                                     true));
   FCG_PROF("part_bucket_start", st);
   bucket_start_kernel<<<grid_for(NB + 1, 256, 4), 256, 0, st>>>(b.keys, n, NB, p.cell_bits,
                                                                  b.start);

@@ -377,7 +377,8 @@ int radix_init_f64(const double *x, int64_t n, int64_t stride, uint64_t *keys, i
 
 template <typename KeyT>
 static int radix_sort_digits(KeyT *keys, int32_t *vals, int64_t n, uint32_t digit_mask,
-                             const RadixWs &ws, cudaStream_t st, bool stable = true) {
+                             const RadixWs &ws, cudaStream_t st, bool stable = true,
+                             bool first_hist_ready = false) {
   if (n <= 1) return FCG_OK;
   const int64_t tiles = ceil_div(n, kSortTile);
   KeyT *ka = keys, *kb = reinterpret_cast<KeyT *>(ws.keys_alt);
@@ -386,7 +387,7 @@ static int radix_sort_digits(KeyT *keys, int32_t *vals, int64_t n, uint32_t digi
   for (int dg = 0; dg < (int)sizeof(KeyT); ++dg) {
     if (!((digit_mask >> dg) & 1u)) continue;
     const int shift = 8 * dg;
-    {
+    if (!(first_hist_ready && passes == 0)) {
       FCG_PROF("radix_hist", st);
       radix_hist_kernel<KeyT><<<(unsigned)tiles, kSortThreads, 0, st>>>(ka, n, shift, ws.hist, tiles);
       FCG_LAUNCH_CHECK();
@@ -414,10 +415,10 @@ static int radix_sort_digits(KeyT *keys, int32_t *vals, int64_t n, uint32_t digi
 
 template <typename KeyT>
 int radix_sort_pairs(KeyT *keys, int32_t *vals, int64_t n, int begin_bit, int end_bit,
-                     const RadixWs &ws, cudaStream_t st, bool stable) {
+                     const RadixWs &ws, cudaStream_t st, bool stable, bool first_hist_ready) {
   uint32_t mask = 0;
   for (int shift = begin_bit; shift < end_bit; shift += 8) mask |= 1u << (shift / 8);
-  return radix_sort_digits<KeyT>(keys, vals, n, mask, ws, st, stable);
+  return radix_sort_digits<KeyT>(keys, vals, n, mask, ws, st, stable, first_hist_ready);
 }
 
 int radix_sort_pairs_pruned(uint64_t *keys, int32_t *vals, int64_t n, const RadixWs &ws,
@@ -443,9 +444,9 @@ int radix_sort_pairs_pruned(uint64_t *keys, int32_t *vals, int64_t n, const Radi
 }
 
 template int radix_sort_pairs<uint64_t>(uint64_t *, int32_t *, int64_t, int, int, const RadixWs &,
-                                        cudaStream_t, bool);
+                                        cudaStream_t, bool, bool);
 template int radix_sort_pairs<uint32_t>(uint32_t *, int32_t *, int64_t, int, int, const RadixWs &,
-                                        cudaStream_t, bool);
+                                        cudaStream_t, bool, bool);
 
 int rank_outputs(const uint64_t *sorted_keys, const int32_t *order, int64_t n, int32_t *pos,
                  int32_t *lower, int32_t *upper, int32_t *dense, int32_t *heads, int32_t *start,

@@ -22,9 +22,12 @@ size_t scan_ws_partial_elems(int64_t n);
 // Sort of (keys, vals) by bits [begin_bit, end_bit) of keys; in place (result in keys/vals),
 // ping-ponging through ws.keys_alt / ws.vals_alt.  Stable unless stable == false, in which case
 // items with equal keys may come out in any order (the first pass ranks without peer masks).
+// first_hist_ready: ws.hist already holds the first pass's digit-major per-tile histogram
+// (kSortTile items per tile), e.g. built by the kernel that produced the keys.
 template <typename KeyT>
 int radix_sort_pairs(KeyT *keys, int32_t *vals, int64_t n, int begin_bit, int end_bit,
-                     const RadixWs &ws, cudaStream_t st, bool stable = true);
+                     const RadixWs &ws, cudaStream_t st, bool stable = true,
+                     bool first_hist_ready = false);
 
 // Stable sort of 64-bit keys over the digits where they differ (one AND/OR reduction and a
 // 16-byte device-to-host read decide which 8-bit passes are identities).  Synchronises `st`.
