@@ -63,49 +63,6 @@ __device__ __forceinline__ void part_key(const double *xi, int d, const double *
   }
 }
 
-// keys (and payloads) of every point; U points per thread per step, all loaded before binning
-template <int D>
-__global__ void __launch_bounds__(256, 4) part_bin_kernel(const double *__restrict__ x, int64_t n,
-                                                       int drt, const double *__restrict__ knots,
-                                                       BinGrid g, PartGeo p,
-                                                       uint32_t *__restrict__ keys,
-                                                       int32_t *__restrict__ vals) {
-  extern __shared__ double s_knots[];
-  __shared__ double s_z0[FCG_MAX_DIM], s_idz[FCG_MAX_DIM];
-  const int d = D > 0 ? D : drt;
-  const double *kb = stage_knots(g, knots, s_knots, s_z0, s_idz);
-  __syncthreads();
-  constexpr int U = D == 4 ? 2 : 1;
-  constexpr int DD = D > 0 ? D : FCG_MAX_DIM;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
-    double xi[U][DD];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = i0 + u * stride;
-      const int64_t ii = i < n ? i : 0;
-      if constexpr (D == 4) {
-        const double2 v0 = __ldcs(reinterpret_cast<const double2 *>(x) + 2 * ii);
-        const double2 v1 = __ldcs(reinterpret_cast<const double2 *>(x) + 2 * ii + 1);
-        xi[u][0] = v0.x; xi[u][1] = v0.y; xi[u][2] = v1.x; xi[u][3] = v1.y;
-      } else {
-#pragma unroll
-        for (int k = 0; k < DD; ++k)
-          if (k < d) xi[u][k] = x[ii * d + k];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = i0 + u * stride;
-      if (i >= n) break;
-      uint32_t key;
-      int32_t val;
-      part_key<D>(xi[u], d, kb, g, s_z0, s_idz, p, i, key, val);
-      keys[i] = key;
-      if (vals) vals[i] = val;
-    }
-  }
-}
 
 // start[b] = first sorted position whose key >= b << shift, for b in [0, NB]
 __global__ void bucket_start_kernel(const uint32_t *__restrict__ keys, int64_t n, int64_t NB,
@@ -1193,7 +1150,7 @@ int kde_build_records(const uint32_t *keys, int64_t n, int shift, const double *
                       int32_t *slot, int32_t *hist, int32_t *partial, cudaStream_t st) {
   KdeBuild<D> kb{factored, pp};
   return digit_partition_build<KdeBuild<D>, D + 1>(keys, n, shift, x, w, kb, rec_c, keys_c, slot,
-                                                   hist, partial, st);
+                                                   hist, partial, st, nullptr, "part_emit", true);
 }
 
 // sorted records, field-major (rec[f * n + q], so a warp's loads of one field are coalesced and
@@ -1621,7 +1578,7 @@ __global__ void __launch_bounds__(256) part_bin_tile_kernel(const double *__rest
                                                             uint32_t *__restrict__ keys,
                                                             int32_t *__restrict__ vals,
                                                             int32_t *__restrict__ hist,
-                                                            int64_t tiles) {
+                                                            int64_t tiles, int tile, int hshift) {
   extern __shared__ double s_knots[];
   __shared__ double s_z0[FCG_MAX_DIM], s_idz[FCG_MAX_DIM];
   __shared__ int32_t s_hist[8][256];
@@ -1631,9 +1588,9 @@ __global__ void __launch_bounds__(256) part_bin_tile_kernel(const double *__rest
   const double *kb = stage_knots(g, knots, s_knots, s_z0, s_idz);
   __syncthreads();
   constexpr int DD = D > 0 ? D : FCG_MAX_DIM;
-  const int64_t tile0 = (int64_t)blockIdx.x * kSortTile;
+  const int64_t tile0 = (int64_t)blockIdx.x * tile;
   constexpr int U = 4;  // points in flight per thread
-  for (int j0 = 0; j0 < kSortTile; j0 += U * 256) {
+  for (int j0 = 0; j0 < tile; j0 += U * 256) {
     double xi[U][DD];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -1658,7 +1615,7 @@ __global__ void __launch_bounds__(256) part_bin_tile_kernel(const double *__rest
       part_key<D>(xi[u], d, kb, g, s_z0, s_idz, p, i, key, val);
       keys[i] = key;
       if (vals) vals[i] = val;
-      atomicAdd(&s_hist[warp][key & 0xFFu], 1);
+      atomicAdd(&s_hist[warp][(key >> hshift) & 0xFFu], 1);
     }
   }
   __syncthreads();
@@ -1668,41 +1625,25 @@ __global__ void __launch_bounds__(256) part_bin_tile_kernel(const double *__rest
   hist[(int64_t)threadIdx.x * tiles + blockIdx.x] = tot;
 }
 
+// tile: items per histogram tile (the consuming pass's tile); hshift: the digit's shift
 int launch_part_bin_tiles(const double *x, int64_t n, int d, const double *knots, const BinGrid &g,
                           const PartGeo &p, uint32_t *keys, int32_t *vals, int32_t *hist,
-                          cudaStream_t st) {
+                          cudaStream_t st, int tile = kSortTile, int hshift = 0) {
   const size_t smem = g.total_knots <= kSmemKnots ? (size_t)g.total_knots * sizeof(double) : 0;
-  const int64_t tiles = ceil_div(n, kSortTile);
+  const int64_t tiles = ceil_div(n, tile);
   FCG_PROF("part_bin", st);
   const bool al = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  const unsigned gr = (unsigned)tiles;
   if (d == 4 && al)
-    part_bin_tile_kernel<4><<<(unsigned)tiles, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals, hist, tiles);
+    part_bin_tile_kernel<4><<<gr, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals, hist, tiles, tile, hshift);
   else if (d == 3)
-    part_bin_tile_kernel<3><<<(unsigned)tiles, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals, hist, tiles);
+    part_bin_tile_kernel<3><<<gr, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals, hist, tiles, tile, hshift);
   else
-    part_bin_tile_kernel<0><<<(unsigned)tiles, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals, hist, tiles);
+    part_bin_tile_kernel<0><<<gr, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals, hist, tiles, tile, hshift);
   FCG_LAUNCH_CHECK();
   return FCG_OK;
 }
 
-int launch_part_bin(const double *x, int64_t n, int d, const double *knots, const BinGrid &g,
-                    const PartGeo &p, uint32_t *keys, int32_t *vals, cudaStream_t st) {
-  const size_t smem = g.total_knots <= kSmemKnots ? (size_t)g.total_knots * sizeof(double) : 0;
-  const int grid = grid_for(n, 256, 8);
-  FCG_PROF("part_bin", st);
-  switch (d) {
-    case 3: part_bin_kernel<3><<<grid, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals); break;
-    case 4:
-      if ((reinterpret_cast<uintptr_t>(x) & 15) == 0)
-        part_bin_kernel<4><<<grid, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals);
-      else
-        part_bin_kernel<0><<<grid, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals);
-      break;
-    default: part_bin_kernel<0><<<grid, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals); break;
-  }
-  FCG_LAUNCH_CHECK();
-  return FCG_OK;
-}
 
 struct PartBufs {
   uint32_t *keys;
@@ -1919,9 +1860,11 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   const int factored = bound_u_sum <= 600.0 ? 1 : 0;
   // keys -> records grouped by the key's top 8 bits -> sort (key, slot) -> L2-local gather
   const int sort_bits = ((pl.nbits + 7) / 8) * 8;
-  FCG_TRY(launch_part_bin(x, n, d, knots, g, p, b.keys, nullptr, st));  // slots come later
+  const int cshift = pl.nbits > 8 ? pl.nbits - 8 : 0;  // coarse digit: the key's top 8 bits
+  FCG_TRY(launch_part_bin_tiles(x, n, d, knots, g, p, b.keys, nullptr, b.rw.hist, st, kPartTile,
+                                cshift));  // slots come later
   {
-    const int shift = pl.nbits > 8 ? pl.nbits - 8 : 0;
+    const int shift = cshift;
     const bool al = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
     int rc;
     switch (d) {  // the partitioned path runs for d >= 3

@@ -188,10 +188,10 @@ int digit_partition_build(const uint32_t *keys, int64_t n, int shift, const doub
                           const double *w, const Build &build, double *rec_out,
                           uint32_t *keys_out, int32_t *slot_out, int32_t *hist, int32_t *partial,
                           cudaStream_t st, double *last_out = nullptr,
-                          const char *label = "part_emit") {
+                          const char *label = "part_emit", bool hist_ready = false) {
   if (n <= 0) return FCG_OK;
   const int64_t tiles = ceil_div(n, kPartTile);
-  {
+  if (!hist_ready) {  // else: the key producer already wrote the per-tile digit histogram
     FCG_PROF("part_hist", st);
     part_detail::digit_hist_kernel<<<(unsigned)tiles, kPartThreads, 0, st>>>(keys, n, shift, hist,
                                                                             tiles);
