@@ -858,9 +858,31 @@ __device__ __forceinline__ void all_put(double *tiles, int tile_elems, int W, in
   }
 }
 
+// Warp shares of every bucket, aligned to run boundaries (no run of equal keys straddles two
+// warps): bounds[b * (nw + 1) + w] = first record of warp w's share of bucket b.  Computed once
+// for all buckets so the plane kernel reads two numbers instead of searching the keys.
+__global__ void share_bounds_kernel(const uint32_t *__restrict__ keys,
+                                    const int32_t *__restrict__ start, int64_t NB, int nw,
+                                    int32_t *__restrict__ bounds) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < NB * (nw + 1);
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t / (nw + 1);
+    const int w = (int)(t - b * (nw + 1));
+    const int32_t q0 = start[b], q1 = start[b + 1];
+    const int32_t per = (q1 - q0 + nw - 1) / nw;
+    int32_t p = q0 + w * per;
+    if (p > q1) p = q1;
+    if (p > q0 && p < q1) {
+      const uint32_t k0 = keys[p - 1];
+      while (p < q1 && keys[p] == k0) ++p;
+    }
+    bounds[t] = p;
+  }
+}
+
 template <int E, int NG>
 __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
-    KdeAll t, const int32_t *__restrict__ start, const double *__restrict__ rec, int64_t nrec,
+    KdeAll t, const int32_t *__restrict__ bounds, const double *__restrict__ rec, int64_t nrec,
     const uint32_t *__restrict__ keys) {
   constexpr int W = 32 * E, C = E / 2;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -927,25 +949,10 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
       const int rowoff = (int)(rb * Rf) - sr - clo;
       __syncthreads();  // the previous block's walk has re-zeroed the tiles
       {
+        // warp shares aligned to run boundaries (share_bounds_kernel): every run of equal keys
+        // is complete inside one share, so all tile writes are plain stores
         const int64_t b = fplane * t.nrb + rb;
-        const int32_t q0 = start[b], q1 = start[b + 1];
-        // warp shares aligned to run boundaries: no run of equal keys straddles two warps, so
-        // every run is complete inside one share and all tile writes are plain stores
-        const int32_t per = (q1 - q0 + nw - 1) / nw;
-        auto run_start = [&](int32_t p) -> int32_t {  // first q >= p that starts a run (warp)
-          if (p <= q0) return q0;
-          if (p >= q1) return q1;
-          const uint32_t k0 = keys[p - 1];
-          while (true) {
-            const int32_t qq = p + lane;
-            const bool diff = qq >= q1 || keys[qq] != k0;
-            const unsigned bal = __ballot_sync(0xffffffffu, diff);
-            if (bal) return p + __ffs(bal) - 1;
-            p += 32;
-          }
-        };
-        const int32_t sb = run_start(q0 + warp * per);
-        const int32_t se = run_start(q0 + (warp + 1) * per);
+        const int32_t sb = bounds[b * (nw + 1) + warp], se = bounds[b * (nw + 1) + warp + 1];
         uint32_t ckey = 0xFFFFFFFFu;
         AllVals<NG> cv;
 #pragma unroll
@@ -1806,6 +1813,7 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   double *rec = W.take<double>((size_t)n * (d + 1));
   double *rec_c = W.take<double>((size_t)n * (d + 1));
   uint32_t *keys_c = W.take<uint32_t>(n);
+  int32_t *share_b = W.take<int32_t>((size_t)pl.NB * (kAllThreads / 32 + 1));
   LatShape s;
   s.d = d;
   int64_t total_knots = 0;
@@ -1896,6 +1904,12 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
     bucket_start_kernel<<<grid_for(pl.NB + 1, 256, 4), 256, 0, st>>>(keys_c, n, pl.NB, p.cell_bits,
                                                                       b.start);
     FCG_LAUNCH_CHECK();
+    if (pl.all) {
+      const int nw = kAllThreads / 32;
+      share_bounds_kernel<<<grid_for(pl.NB * (nw + 1), 256, 4), 256, 0, st>>>(keys_c, b.start, pl.NB,
+                                                                              nw, share_b);
+      FCG_LAUNCH_CHECK();
+    }
   }
   {
     FCG_PROF("kde_materialize", st);
@@ -1960,7 +1974,7 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
     FCG_PROF("plane_kde", st);
     auto launch = [&](auto kern) -> int {
       FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asmem));
-      kern<<<(unsigned)np_full, kAllThreads, asmem, st>>>(ta, b.start, rec, n, keys_c);
+      kern<<<(unsigned)np_full, kAllThreads, asmem, st>>>(ta, share_b, rec, n, keys_c);
       FCG_LAUNCH_CHECK();
       return FCG_OK;
     };
