@@ -1913,7 +1913,9 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   }
   {
     FCG_PROF("kde_materialize", st);
-    kde_gather_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(rec_c, b.vals, n, d, rec);
+    // two CTAs per SM: the sorted positions in flight span ~half a coarse bucket, so its
+    // records are re-read from L2 (a full grid spreads over several buckets and misses)
+    kde_gather_kernel<<<grid_for(n, 256, 2), 256, 0, st>>>(rec_c, b.vals, n, d, rec);
     FCG_LAUNCH_CHECK();
   }
   double prod_h = 1.0;
