@@ -1369,6 +1369,10 @@ __global__ void __launch_bounds__(256, 2) final2d_kernel(Final2D f) {
     cp_async_wait1();
     __syncthreads();
     double v[NT][kF2Seg];
+    // a warp holds two segments of the same 16 columns: their totals pair up with one shuffle,
+    // so the cross-warp prefix runs over the 8 warp totals (both lattices in one double2)
+    const int warp = threadIdx.x >> 5, upper = (threadIdx.x >> 4) & 1;
+    double inner[NT], wtot[NT];
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
       const double *sl = buf + (cur * (NT + 1) + t) * slab;
@@ -1381,13 +1385,27 @@ __global__ void __launch_bounds__(256, 2) final2d_kernel(Final2D f) {
         run += x;
         v[t][s] = run;
       }
-      segs[(t * kF2Segs + sg) * CW + c] = run;
+      const double other = __shfl_xor_sync(0xffffffffu, run, 16);
+      inner[t] = upper ? other : 0.0;
+      wtot[t] = run + other;
     }
+    if (!upper)
+      reinterpret_cast<double2 *>(segs)[warp * CW + c] =
+          make_double2(wtot[0], NT > 1 ? wtot[NT - 1] : 0.0);
     __syncthreads();
+    {
+      double o0 = inner[0], o1 = inner[NT - 1];
+      for (int w = 0; w < warp; ++w) {
+        const double2 a = reinterpret_cast<const double2 *>(segs)[w * CW + c];
+        o0 += a.x;
+        o1 += a.y;
+      }
+      inner[0] = o0;
+      if (NT > 1) inner[NT - 1] = o1;
+    }
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
-      double off = 0.0;
-      for (int w = 0; w < sg; ++w) off += segs[(t * kF2Segs + w) * CW + c];
+      const double off = inner[t];
 #pragma unroll
       for (int s = 0; s < kF2Seg; ++s) carry[t][s] += v[t][s] + off;
       if (f.plane[t] != nullptr) {  // slab carry capture (scanned over axes 0 and 1)
