@@ -42,6 +42,7 @@ extern "C" {
 #define FCG_OK 0
 #define FCG_EINVAL 22      /* bad argument (maps to ParameterError / ShapeError host-side) */
 #define FCG_EUNSUPPORTED 95 /* shape outside what the kernels implement (e.g. d > FCG_MAX_DIM) */
+#define FCG_ERANGE 34      /* exponential overflow guard (maps to OverflowGuardError host-side) */
 #define FCG_ECUDA 100      /* a CUDA launch or copy failed */
 #define FCG_EWORKSPACE 101 /* ws too small */
 
@@ -161,6 +162,10 @@ int fcg_slab_finish(const void *local, int32_t kind, const void *carry, int64_t 
  * term's factors zf_k(i_k) = exp(-delta_k (z_k - c_k) / h_k) of the axes k >= kw, kw =
  * max(2, d - 2); terms that differ only in the signs of those axes may be summed into the slot
  * of the lowest such code (the other slots are then zero).  Linear, so the exchange is a sum. */
+/* centre == NULL (auto centre): the kernels take the hull of the data and the knot ends while
+ * binning (no separate min/max pass), derive c = (lo + hi) / 2 and u_bound themselves and fail
+ * with FCG_ERANGE when some span_k / h_k > 600 (fastsum.py:114-129, core.py:22); this
+ * synchronises the stream once, after the binning pass.  u_bound is then ignored. */
 int fcg_kde_grid_laplacian_ex(const double *x, int64_t n, int32_t d, const double *w,
                               const double *knots, const int64_t *m, const double *h,
                               const double *centre, double n_scale, double u_bound,

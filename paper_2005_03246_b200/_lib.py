@@ -13,7 +13,7 @@ from pathlib import Path
 
 import numpy as np
 
-from .core import ParameterError, ShapeError
+from .core import OverflowGuardError, ParameterError, ShapeError
 
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libfastcdf_b200.so"
@@ -22,6 +22,7 @@ ABI_VERSION = 1
 FCG_OK = 0
 FCG_EINVAL = 22
 FCG_EUNSUPPORTED = 95
+FCG_ERANGE = 34
 FCG_ECUDA = 100
 FCG_EWORKSPACE = 101
 
@@ -123,6 +124,8 @@ def check(rc: int, name: str):
     msg = load_library().fcg_last_error().decode(errors="replace")
     if rc in (FCG_EINVAL, FCG_EUNSUPPORTED):
         raise ParameterError(f"{name}: {msg}")
+    if rc == FCG_ERANGE:
+        raise OverflowGuardError(msg)
     raise RuntimeError(f"{name} failed (status {rc}): {msg}")
 
 

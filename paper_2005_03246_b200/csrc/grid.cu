@@ -371,6 +371,26 @@ extern "C" int fcg_ecdf_grid(const double *x, int64_t n, int32_t d, const double
                               static_cast<double *>(scratch), st);
 }
 
+namespace fcg {
+// widen the order-key hull mm[0..2d) by the n points of x
+static int launch_minmax_accum(const double *x, int64_t n, int d, unsigned long long *mm,
+                               cudaStream_t st) {
+  if (n <= 0) return FCG_OK;
+  // grid: a multiple of d blocks (so the flat stride is a multiple of d), ~4 per SM
+  const int64_t total = n * d;
+  const bool vec = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  const int64_t per = vec ? 512 : 256;
+  int64_t blocks = std::min<int64_t>(ceil_div(total, per), 4 * (int64_t)sm_count());
+  blocks = ceil_div(blocks, d) * d;
+  if (vec)
+    minmax_kernel<2><<<(unsigned)blocks, 256, 0, st>>>(x, total, d, mm);
+  else
+    minmax_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(x, total, d, mm);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}
+}  // namespace fcg
+
 extern "C" int fcg_minmax(const double *x, int64_t n, int32_t d, double *out_minmax, void *ws,
                           size_t *ws_bytes, void *stream) {
   if (d < 1 || d > FCG_MAX_DIM) return fail(FCG_EUNSUPPORTED, "dimension out of range");
@@ -384,19 +404,7 @@ extern "C" int fcg_minmax(const double *x, int64_t n, int32_t d, double *out_min
   FCG_PROF("minmax", st);
   minmax_init<<<1, 32, 0, st>>>(mm, d);
   FCG_LAUNCH_CHECK();
-  if (n > 0) {
-    // grid: a multiple of d blocks (so the flat stride is a multiple of d), ~4 per SM
-    const int64_t total = n * d;
-    const bool vec = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
-    const int64_t per = vec ? 512 : 256;
-    int64_t blocks = std::min<int64_t>(ceil_div(total, per), 4 * (int64_t)sm_count());
-    blocks = ceil_div(blocks, d) * d;
-    if (vec)
-      minmax_kernel<2><<<(unsigned)blocks, 256, 0, st>>>(x, total, d, mm);
-    else
-      minmax_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(x, total, d, mm);
-    FCG_LAUNCH_CHECK();
-  }
+  FCG_TRY(launch_minmax_accum(x, n, d, mm, st));
   minmax_finish<<<1, 32, 0, st>>>(mm, d, out_minmax);
   FCG_LAUNCH_CHECK();
   return FCG_OK;
@@ -424,7 +432,10 @@ static int kde_grid_impl(const double *x, int64_t n, int32_t d, const double *w,
   if (planes && d < 2) return fail(FCG_EINVAL, "slab planes need d >= 2");
   cudaStream_t st = as_stream(stream);
   Workspace W(ws);
-  const PartPlan plan = plan_kde_partition(d, m, n, u_bound > 0.0 && u_bound <= 600.0);
+  // auto centre: plan for factored records (the hull decides at run time)
+  const bool auto_centre = centre == nullptr;
+  const PartPlan plan =
+      plan_kde_partition(d, m, n, auto_centre || (u_bound > 0.0 && u_bound <= 600.0));
   if (plan.ok) {
     FCG_TRY(kde_partitioned(x, n, w, knots, m, d, h, centre, u_bound > 0.0 ? u_bound : 1e300,
                             n_scale, planes, plan, out, W, ws != nullptr, st));
@@ -434,9 +445,17 @@ static int kde_grid_impl(const double *x, int64_t n, int32_t d, const double *w,
   double *lat = W.take<double>((size_t)L);
   double *scratch = W.take<double>((size_t)scan_scratch_elems(s));
   double *zf = W.take<double>((size_t)total_knots);
+  unsigned long long *mm = W.take<unsigned long long>(2 * FCG_MAX_DIM);
   if (ws == nullptr) {
     *ws_bytes = W.bytes();
     return FCG_OK;
+  }
+  double c_auto[FCG_MAX_DIM];
+  if (auto_centre) {
+    FCG_TRY(hull_init(knots, d, m, mm, st));
+    FCG_TRY(launch_minmax_accum(x, n, d, mm, st));
+    FCG_TRY(hull_centre(mm, d, h, c_auto, &u_bound, st));
+    centre = c_auto;
   }
   double prod_h = 1.0;
   for (int k = 0; k < d; ++k) prod_h *= h[k];

@@ -5,6 +5,11 @@
 // 12-16% of HBM peak).  Bucketing by plane first turns it into streaming: each CTA reads its
 // bucket's records contiguously, accumulates in shared memory and writes its plane once, with
 // the two in-plane scan passes (Algorithm 1's sweeps along axes d-2, d-1) fused in.
+#include <math_constants.h>
+
+#include <cstdio>
+#include <cstring>
+
 #include "grid_part.cuh"
 #include "partition.cuh"
 #include "sort.cuh"
@@ -1596,17 +1601,19 @@ int bits_for(int64_t v) {  // smallest b with v < 2^b
 
 // keys + payloads of one radix tile per CTA, with the tile's histogram of the keys' low byte
 // (the first LSD pass's digit-major histogram, so that pass needs no histogram kernel)
-template <int D>
-__global__ void __launch_bounds__(256) part_bin_tile_kernel(const double *__restrict__ x, int64_t n,
+template <int D, bool MM>
+__global__ void __launch_bounds__(256, D == 3 || D == 4 ? 4 : 1) part_bin_tile_kernel(const double *__restrict__ x, int64_t n,
                                                             int drt, const double *__restrict__ knots,
                                                             BinGrid g, PartGeo p,
                                                             uint32_t *__restrict__ keys,
                                                             int32_t *__restrict__ vals,
                                                             int32_t *__restrict__ hist,
-                                                            int64_t tiles, int tile, int hshift) {
+                                                            int64_t tiles, int tile, int hshift,
+                                                            unsigned long long *__restrict__ mm) {
   extern __shared__ double s_knots[];
   __shared__ double s_z0[FCG_MAX_DIM], s_idz[FCG_MAX_DIM];
   __shared__ int32_t s_hist[8][256];
+  __shared__ double s_mm[8][2][FCG_MAX_DIM];
   const int d = D > 0 ? D : drt;
   const int warp = threadIdx.x >> 5;
   for (int i = threadIdx.x & 31; i < 256; i += 32) s_hist[warp][i] = 0;
@@ -1615,6 +1622,13 @@ __global__ void __launch_bounds__(256) part_bin_tile_kernel(const double *__rest
   constexpr int DD = D > 0 ? D : FCG_MAX_DIM;
   const int64_t tile0 = (int64_t)blockIdx.x * tile;
   constexpr int U = 4;  // points in flight per thread
+  // data hull (auto centre of the KDE): per-thread, then warp, then CTA, then one atomic each
+  double lo[DD], hi[DD];
+#pragma unroll
+  for (int k = 0; k < DD; ++k) {
+    lo[k] = CUDART_INF;
+    hi[k] = -CUDART_INF;
+  }
   for (int j0 = 0; j0 < tile; j0 += U * 256) {
     double xi[U][DD];
 #pragma unroll
@@ -1641,6 +1655,31 @@ __global__ void __launch_bounds__(256) part_bin_tile_kernel(const double *__rest
       keys[i] = key;
       if (vals) vals[i] = val;
       atomicAdd(&s_hist[warp][(key >> hshift) & 0xFFu], 1);
+      if constexpr (MM) {
+#pragma unroll
+        for (int k = 0; k < DD; ++k) {
+          if (k < d) {
+            lo[k] = fmin(lo[k], xi[u][k]);
+            hi[k] = fmax(hi[k], xi[u][k]);
+          }
+        }
+      }
+    }
+  }
+  if constexpr (MM) {
+#pragma unroll
+    for (int k = 0; k < DD; ++k) {
+      if (k < d) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          lo[k] = fmin(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+          hi[k] = fmax(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+          s_mm[warp][0][k] = lo[k];
+          s_mm[warp][1][k] = hi[k];
+        }
+      }
     }
   }
   __syncthreads();
@@ -1648,23 +1687,42 @@ __global__ void __launch_bounds__(256) part_bin_tile_kernel(const double *__rest
 #pragma unroll
   for (int w = 0; w < 8; ++w) tot += s_hist[w][threadIdx.x];
   hist[(int64_t)threadIdx.x * tiles + blockIdx.x] = tot;
+  if (MM && threadIdx.x < 2 * d) {
+    const int k = threadIdx.x >> 1, side = threadIdx.x & 1;
+    double v = s_mm[0][side][k];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) v = side ? fmax(v, s_mm[w][side][k]) : fmin(v, s_mm[w][side][k]);
+    unsigned long long *slot = mm + side * d + k;
+    const unsigned long long key = f64_key(v);
+    // most CTAs cannot move the running hull any more: skip their atomics
+    const unsigned long long cur = *reinterpret_cast<volatile unsigned long long *>(slot);
+    if (side ? key > cur : key < cur) {
+      if (side) atomicMax(slot, key);
+      else atomicMin(slot, key);
+    }
+  }
 }
+
 
 // tile: items per histogram tile (the consuming pass's tile); hshift: the digit's shift
 int launch_part_bin_tiles(const double *x, int64_t n, int d, const double *knots, const BinGrid &g,
                           const PartGeo &p, uint32_t *keys, int32_t *vals, int32_t *hist,
-                          cudaStream_t st, int tile = kSortTile, int hshift = 0) {
+                          cudaStream_t st, int tile = kSortTile, int hshift = 0,
+                          unsigned long long *mm = nullptr) {
   const size_t smem = g.total_knots <= kSmemKnots ? (size_t)g.total_knots * sizeof(double) : 0;
   const int64_t tiles = ceil_div(n, tile);
   FCG_PROF("part_bin", st);
   const bool al = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
   const unsigned gr = (unsigned)tiles;
+  auto launch = [&](auto kern) {
+    kern<<<gr, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals, hist, tiles, tile, hshift, mm);
+  };
   if (d == 4 && al)
-    part_bin_tile_kernel<4><<<gr, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals, hist, tiles, tile, hshift);
+    mm ? launch(part_bin_tile_kernel<4, true>) : launch(part_bin_tile_kernel<4, false>);
   else if (d == 3)
-    part_bin_tile_kernel<3><<<gr, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals, hist, tiles, tile, hshift);
+    mm ? launch(part_bin_tile_kernel<3, true>) : launch(part_bin_tile_kernel<3, false>);
   else
-    part_bin_tile_kernel<0><<<gr, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals, hist, tiles, tile, hshift);
+    mm ? launch(part_bin_tile_kernel<0, true>) : launch(part_bin_tile_kernel<0, false>);
   FCG_LAUNCH_CHECK();
   return FCG_OK;
 }
@@ -1703,6 +1761,60 @@ int partition(const double *x, int64_t n, int d, const double *knots, const BinG
 }
 
 }  // namespace
+
+__global__ void hull_init_kernel(const double *__restrict__ knots, HullKnots hk,
+                                 unsigned long long *mm) {
+  const int k = threadIdx.x;
+  if (k < hk.d) {
+    mm[k] = f64_key(knots[hk.first[k]]);
+    mm[hk.d + k] = f64_key(knots[hk.last[k]]);
+  }
+}
+
+int hull_init(const double *knots, int d, const int64_t *m, unsigned long long *mm, cudaStream_t st) {
+  HullKnots hk{};
+  hk.d = d;
+  int64_t off = 0;
+  for (int k = 0; k < d; ++k) {
+    hk.first[k] = off;
+    hk.last[k] = off + m[k] - 1;
+    off += m[k];
+  }
+  hull_init_kernel<<<1, 32, 0, st>>>(knots, hk, mm);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}
+
+static double f64_unkey(uint64_t k) {
+  const uint64_t u = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+  double v;
+  std::memcpy(&v, &u, sizeof v);
+  return v;
+}
+
+int hull_centre(const unsigned long long *mm, int d, const double *h, double *c, double *u_bound,
+                cudaStream_t st) {
+  unsigned long long host[2 * FCG_MAX_DIM];
+  FCG_CUDA_TRY(cudaMemcpyAsync(host, mm, 2 * d * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  FCG_CUDA_TRY(cudaStreamSynchronize(st));
+  double ub = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const double lo = f64_unkey(host[k]), hi = f64_unkey(host[d + k]);
+    const double span = hi - lo;
+    // fastsum.py:114-129 with EXP_OVERFLOW_GUARD = 600 (core.py:22)
+    if (span / h[k] > 600.0) {
+      char msg[160];
+      std::snprintf(msg, sizeof msg,
+                    "dimension %d: span/bandwidth = %.1f exceeds 600; enlarge the bandwidth or rescale",
+                    k, span / h[k]);
+      return fail(FCG_ERANGE, msg);
+    }
+    c[k] = 0.5 * (lo + hi);
+    ub += span / (2.0 * h[k]);
+  }
+  *u_bound = ub * 1.000001;
+  return FCG_OK;
+}
 
 PartPlan plan_ecdf_partition(const BinGrid &g, int64_t n) {
   PartPlan pl;
@@ -1851,7 +1963,10 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   double *lats = W.take<double>((size_t)s.size() * (pl.all ? ngroups : nbatch));
   double *scratch = W.take<double>(scan_scratch_bound());
   double *zfs = W.take<double>((size_t)total_knots * (nbatch + 2));
+  unsigned long long *mm = W.take<unsigned long long>(2 * FCG_MAX_DIM);
   if (!run) return FCG_OK;
+  const bool auto_centre = centre == nullptr;
+  double c_auto[FCG_MAX_DIM];
 
   // one delta=+1 binning in the full (M+1)^d space serves every term (fastsum.py:146-149)
   int le[FCG_MAX_DIM];
@@ -1878,17 +1993,24 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   // factored psi records when every partial product stays inside e^{+-600}: needs
   // sum_k max|u_k| <= 600 with u_k = (x_k - c_k)/h_k; bounded here by the hull of the knots
   // and the data (the caller's centre is that hull's midrange, fastsum.py:118-129)
+  // keys -> records grouped by the key's top 8 bits -> sort (key, slot) -> L2-local gather
+  const int sort_bits = ((pl.nbits + 7) / 8) * 8;
+  const int cshift = pl.nbits > 8 ? pl.nbits - 8 : 0;  // coarse digit: the key's top 8 bits
+  if (auto_centre) FCG_TRY(hull_init(knots, d, m, mm, st));
+  FCG_TRY(launch_part_bin_tiles(x, n, d, knots, g, p, b.keys, nullptr, b.rw.hist, st, kPartTile,
+                                cshift, auto_centre ? mm : nullptr));  // slots come later
+  if (auto_centre) {  // the hull came with the binning pass
+    FCG_TRY(hull_centre(mm, d, h, c_auto, &bound_u_sum, st));
+    centre = c_auto;
+  }
   PsiParams pp{};
   for (int k = 0; k < d; ++k) {
     pp.c[k] = centre[k];
     pp.a[k] = 1.0 / h[k];
   }
   const int factored = bound_u_sum <= 600.0 ? 1 : 0;
-  // keys -> records grouped by the key's top 8 bits -> sort (key, slot) -> L2-local gather
-  const int sort_bits = ((pl.nbits + 7) / 8) * 8;
-  const int cshift = pl.nbits > 8 ? pl.nbits - 8 : 0;  // coarse digit: the key's top 8 bits
-  FCG_TRY(launch_part_bin_tiles(x, n, d, knots, g, p, b.keys, nullptr, b.rw.hist, st, kPartTile,
-                                cshift));  // slots come later
+  // the all-groups kernel takes factored records only (an auto-centre plan assumed them)
+  const bool all_run = pl.all && factored;
   {
     const int shift = cshift;
     const bool al = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
@@ -1922,7 +2044,7 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
     bucket_start_kernel<<<grid_for(pl.NB + 1, 256, 4), 256, 0, st>>>(keys_c, n, pl.NB, p.cell_bits,
                                                                       b.start);
     FCG_LAUNCH_CHECK();
-    if (pl.all) {
+    if (all_run) {
       const int nw = kAllThreads / 32;
       share_bounds_kernel<<<grid_for(pl.NB * (nw + 1), 256, 4), 256, 0, st>>>(keys_c, b.start, pl.NB,
                                                                               nw, share_b);
@@ -1964,7 +2086,7 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   FCG_TRY(launch_kde_zf(knots, d, m, centre, h, 0, zpos, st));
   FCG_TRY(launch_kde_zf(knots, d, m, centre, h, (1 << d) - 1, zneg, st));
   const int kr = d - 2, kc = d - 1;
-  if (pl.all) {  // one pass over the records per row sign for every group
+  if (all_run) {  // one pass over the records per row sign for every group
     KdeAll ta{};
     ta.d = d;
     ta.nlead = d - 2;
@@ -2024,7 +2146,7 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
       }
       for (int tt = 0; tt < nt; ++tt) {
         const int gl = s0 | ((b0 + tt) << 1);  // signs of axes < kz (bit k: delta_k = -1)
-        double *lat = lats + (size_t)(pl.all ? gl : tt) * L;
+        double *lat = lats + (size_t)(all_run ? gl : tt) * L;
         double *zf = zfs + (size_t)tt * total_knots;
         KdeGroup t{};
         t.d = d;
@@ -2066,7 +2188,7 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
         t.cell_bits = pl.cell_bits;
         t.col_bits = pl.col_bits;
         FCG_TRY(launch_kde_zf(knots, d, m, centre, h, gl, zf, st));
-        if (!pl.all) {
+        if (!all_run) {
           FCG_PROF("plane_kde", st);
           kde_kern<<<(unsigned)pl.NP, kKdeThreads, smem, st>>>(t, b.start, rec, n, keys_c,
                                                                factored, lat);

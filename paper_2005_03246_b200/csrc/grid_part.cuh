@@ -45,4 +45,16 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
                     double bound_u_sum, double n_scale, double *planes, const PartPlan &plan,
                     double *out, Workspace &W, bool run, cudaStream_t st);
 
+// Auto centre of the KDE (centre == NULL): mm[0..d) / mm[d..2d) = order keys of the hull's
+// lower / upper ends, seeded with the knot ends by hull_init and widened by the binning pass.
+struct HullKnots {
+  int d;
+  int64_t first[FCG_MAX_DIM], last[FCG_MAX_DIM];
+};
+int hull_init(const double *knots, int d, const int64_t *m, unsigned long long *mm, cudaStream_t st);
+// Synchronises; c = (lo + hi) / 2 and u_bound = sum_k span_k / (2 h_k) (with a 1e-6 margin), or
+// FCG_ERANGE past span_k / h_k > 600 (fastsum.py:114-129).
+int hull_centre(const unsigned long long *mm, int d, const double *h, double *c, double *u_bound,
+                cudaStream_t st);
+
 }  // namespace fcg

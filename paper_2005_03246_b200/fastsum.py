@@ -127,17 +127,18 @@ def _exp_guard_and_center(sample: Sample, grid: RectilinearGrid, h: np.ndarray):
 
 
 def _kde_laplacian_grid(sample: Sample, grid: RectilinearGrid, h: np.ndarray):
+    """Laplacian terms (fastsum.py:139-169).  The library takes the hull midrange and applies
+    the overflow guard of fastsum.py:114-129 itself (auto centre), from the binning pass."""
     import torch
 
-    c, ubound = _exp_guard_and_center(sample, grid, h)
     x = _lib.to_device_f64(sample.points)
     n, d = x.shape
     w = None if sample.unit_weights else _lib.to_device_f64(sample.weights)
     kn = _lib.device_knots(grid)
     out = torch.empty(grid.size, dtype=torch.float64, device=x.device)
     _lib.call_ws("fcg_kde_grid_laplacian_ex", _lib.ptr(x), n, d, _lib.ptr(w), _lib.ptr(kn),
-                 _lib.i64_array(grid.shape), _lib.f64_array(h), _lib.f64_array(c), float(n),
-                 ubound * 1.000001, None, _lib.ptr(out))
+                 _lib.i64_array(grid.shape), _lib.f64_array(h), None, float(n), -1.0, None,
+                 _lib.ptr(out))
     return out
 
 

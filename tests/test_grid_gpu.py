@@ -315,6 +315,72 @@ def test_partitioned_kde_vs_oracle(dims, oracle):
     assert_rel(got, ref, REL_KDE)
 
 
+def _kde_ex(x, w, knots, h, centre, u_bound):
+    import torch
+    from paper_2005_03246_b200 import _lib
+
+    grid = _grid(knots)
+    xd = _lib.to_device_f64(x)
+    wd = _lib.to_device_f64(w)
+    kn = _lib.device_knots(grid)
+    out = torch.empty(grid.size, dtype=torch.float64, device=xd.device)
+    _lib.call_ws("fcg_kde_grid_laplacian_ex", _lib.ptr(xd), x.shape[0], x.shape[1], _lib.ptr(wd),
+                 _lib.ptr(kn), _lib.i64_array(grid.shape), _lib.f64_array(h),
+                 None if centre is None else _lib.f64_array(centre), float(x.shape[0]), u_bound,
+                 None, _lib.ptr(out))
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("dims", [(24, 20, 16, 64), (300, 40, 128), (9, 11)])
+def test_kde_auto_centre_matches_explicit(dims):
+    """centre == NULL: the hull taken by the binning pass gives the caller-side midrange of
+    fastsum.py:118-129 exactly, so the partitioned densities are bit-identical."""
+    d = len(dims)
+    rng = np.random.default_rng(11 * sum(dims))
+    n = 1_100_000
+    x = rng.uniform(-1, 1.3, (n, d))
+    w = rng.exponential(1.0, n)
+    knots = [np.linspace(-1.4, 0.9, m) for m in dims]
+    h = rng.uniform(0.05, 0.3, d)
+    lo = np.minimum(x.min(0), [z[0] for z in knots])
+    hi = np.maximum(x.max(0), [z[-1] for z in knots])
+    c = 0.5 * (lo + hi)
+    ub = float(np.sum((hi - lo) / (2 * h))) * 1.000001
+    got, ref = _kde_ex(x, w, knots, h, None, -1.0), _kde_ex(x, w, knots, h, c, ub)
+    if d >= 3:  # the partitioned pipeline is deterministic
+        np.testing.assert_array_equal(got, ref)
+    else:  # fp64 atomics: run-to-run summation order
+        assert_rel(got, ref, 1e-13)
+
+
+def test_partitioned_kde_raw_records(oracle):
+    """sum_k span_k / (2 h_k) > 600 with every span_k / h_k <= 600: the auto-centre plan assumed
+    factored records, the run falls back to per-term exponentials on the group kernel."""
+    oracle.set_threads(0)
+    dims = (24, 20, 16, 64)
+    rng = np.random.default_rng(5)
+    n = 1_100_000
+    x = rng.uniform(-1, 1, (n, 4))
+    w = rng.exponential(1.0, n)
+    knots = [np.linspace(-1.0, 1.0, m) for m in dims]
+    h = np.full(4, 0.006)  # span / h = 333 per axis, bound 667
+    got = fcb.kde_fastsum(fcb.validate_sample(x, w), _grid(knots), fcb.laplacian(),
+                          fcb.Bandwidth.diag(h)).values
+    ref = oracle.kde_fastsum_laplacian(x, w, knots, h)
+    assert_rel(got, ref, REL_KDE)
+
+
+def test_partitioned_kde_overflow_guard():
+    rng = np.random.default_rng(6)
+    n = 1_100_000
+    x = rng.uniform(0, 1, (n, 4))
+    x[:, 2] *= 700.0
+    knots = [np.linspace(0.0, 1.0, 64)] * 4
+    with pytest.raises(fcb.OverflowGuardError, match="dimension 2: span/bandwidth = "):
+        fcb.kde_fastsum(fcb.validate_sample(x), _grid(knots), fcb.laplacian(),
+                        fcb.Bandwidth.diag([1.0] * 4))
+
+
 @pytest.mark.slow
 def test_cfg5_full(oracle, cfg_meta):
     """Config 5 at full size (N = 1e8, 128^4): the ECDF's int64 counts must equal the digest of
