@@ -32,13 +32,14 @@ struct PsiParams {  // psi_i = w_i * exp(sum_k (x_ik - c_k) * a_k), a_k = delta_
 // the result is the exact count for any rectilinear grid.
 __device__ __forceinline__ int knot_count(double x, const double *kn, int m, int le, double z0,
                                           double inv_dz) {
-  double t = (x - z0) * inv_dz;
-  t = fmin(fmax(t, -1.0), (double)m + 1.0);
-  int g = le ? (int)floor(t) + 1 : (int)ceil(t);
-  g = g < 0 ? 0 : (g > m ? m : g);
-  // pred(k) := knot k counts (kn[k] < x, or <= x when le)
-  const bool lo_ok = (g == 0) || (le ? (kn[g - 1] <= x) : (kn[g - 1] < x));
-  const bool hi_ok = (g == m) || (le ? (x < kn[g]) : (x <= kn[g]));
+  const double t = (x - z0) * inv_dz;
+  // floor(t) + 1 (le) or ceil(t), clamped to [0, m]: the conversions saturate (NaN -> 0)
+  const int f = le ? __double2int_rd(t) : __double2int_ru(t - 1.0);
+  const int g = min(max(f, -1), m - 1) + 1;
+  // pred(k) := knot k counts (kn[k] < x, or <= x when le); valid iff pred(g-1) && !pred(g)
+  const double a = kn[g > 0 ? g - 1 : 0], b = kn[g < m ? g : m - 1];
+  const bool lo_ok = (g == 0) || a < x || (le && a == x);
+  const bool hi_ok = (g == m) || x < b || (!le && x == b);
   if (lo_ok && hi_ok) return g;
   const int g2 = lo_ok ? g + 1 : g - 1;  // one nudge (knot hits land one bin off)
   const bool lo2 = (g2 == 0) || (le ? (kn[g2 - 1] <= x) : (kn[g2 - 1] < x));

@@ -33,6 +33,7 @@ struct PartGeo {
   int64_t E[FCG_MAX_DIM];      // extents of the bucketed space
   int64_t shift[FCG_MAX_DIM];  // bucket-space index = b - shift
   int64_t W, R, nrb, H;
+  float inv_R;                 // 1 / R (row-block division by reciprocal + one correction)
   int ecdf;                    // 1: val = in-block cell offset; 0: val = point index
   int cell_bits;               // > 0: key = bucket << cell_bits | r_in << col_bits | col
   int col_bits;
@@ -60,11 +61,20 @@ __device__ __forceinline__ void part_key(const double *xi, int d, const double *
   key = kDead;
   val = (int32_t)i;
   if (live) {
-    const int rb = row / (int)p.R;
+    // row < 2^24: the float quotient is within one of row / R
+    const int R = (int)p.R;
+    int rb = __float2int_rz((float)row * p.inv_R);
+    int r_in = row - rb * R;
+    if (r_in < 0) {
+      --rb;
+      r_in += R;
+    } else if (r_in >= R) {
+      ++rb;
+      r_in -= R;
+    }
     key = plane * (uint32_t)p.nrb + (uint32_t)rb;
-    if (p.ecdf) val = (row - rb * (int)p.R) * (int)p.W + col;
-    if (p.cell_bits > 0)
-      key = (key << p.cell_bits) | ((uint32_t)(row - rb * (int)p.R) << p.col_bits) | (uint32_t)col;
+    if (p.ecdf) val = r_in * (int)p.W + col;
+    if (p.cell_bits > 0) key = (key << p.cell_bits) | ((uint32_t)r_in << p.col_bits) | (uint32_t)col;
   }
 }
 
@@ -1613,7 +1623,7 @@ __global__ void __launch_bounds__(256, D == 3 || D == 4 ? 4 : 1) part_bin_tile_k
   extern __shared__ double s_knots[];
   __shared__ double s_z0[FCG_MAX_DIM], s_idz[FCG_MAX_DIM];
   __shared__ int32_t s_hist[8][256];
-  __shared__ double s_mm[8][2][FCG_MAX_DIM];
+  __shared__ unsigned long long s_mm[8][2][FCG_MAX_DIM];
   const int d = D > 0 ? D : drt;
   const int warp = threadIdx.x >> 5;
   for (int i = threadIdx.x & 31; i < 256; i += 32) s_hist[warp][i] = 0;
@@ -1666,18 +1676,20 @@ __global__ void __launch_bounds__(256, D == 3 || D == 4 ? 4 : 1) part_bin_tile_k
       }
     }
   }
-  if constexpr (MM) {
+  if constexpr (MM) {  // warp reduce in order-key space: two redux.sync per 64-bit value
 #pragma unroll
     for (int k = 0; k < DD; ++k) {
       if (k < d) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          lo[k] = fmin(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
-          hi[k] = fmax(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
-        }
+        const uint64_t kl = f64_key(lo[k]), kh = f64_key(hi[k]);
+        const unsigned lhi = __reduce_min_sync(0xffffffffu, (unsigned)(kl >> 32));
+        const unsigned hhi = __reduce_max_sync(0xffffffffu, (unsigned)(kh >> 32));
+        const unsigned llo =
+            __reduce_min_sync(0xffffffffu, (unsigned)(kl >> 32) == lhi ? (unsigned)kl : ~0u);
+        const unsigned hlo =
+            __reduce_max_sync(0xffffffffu, (unsigned)(kh >> 32) == hhi ? (unsigned)kh : 0u);
         if ((threadIdx.x & 31) == 0) {
-          s_mm[warp][0][k] = lo[k];
-          s_mm[warp][1][k] = hi[k];
+          s_mm[warp][0][k] = ((unsigned long long)lhi << 32) | llo;
+          s_mm[warp][1][k] = ((unsigned long long)hhi << 32) | hlo;
         }
       }
     }
@@ -1689,17 +1701,15 @@ __global__ void __launch_bounds__(256, D == 3 || D == 4 ? 4 : 1) part_bin_tile_k
   hist[(int64_t)threadIdx.x * tiles + blockIdx.x] = tot;
   if (MM && threadIdx.x < 2 * d) {
     const int k = threadIdx.x >> 1, side = threadIdx.x & 1;
-    double v = s_mm[0][side][k];
+    unsigned long long key = s_mm[0][side][k];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) v = side ? fmax(v, s_mm[w][side][k]) : fmin(v, s_mm[w][side][k]);
-    unsigned long long *slot = mm + side * d + k;
-    const unsigned long long key = f64_key(v);
-    // most CTAs cannot move the running hull any more: skip their atomics
-    const unsigned long long cur = *reinterpret_cast<volatile unsigned long long *>(slot);
-    if (side ? key > cur : key < cur) {
-      if (side) atomicMax(slot, key);
-      else atomicMin(slot, key);
+    for (int w = 1; w < 8; ++w) {
+      const unsigned long long v = s_mm[w][side][k];
+      key = side ? (v > key ? v : key) : (v < key ? v : key);
     }
+    unsigned long long *slot = mm + side * d + k;
+    if (side) atomicMax(slot, key);  // result unused: a fire-and-forget RED
+    else atomicMin(slot, key);
   }
 }
 
@@ -1864,6 +1874,7 @@ int ecdf_partitioned(const double *x, int64_t n, const double *knots, const BinG
   }
   p.W = pl.W;
   p.R = pl.R;
+  p.inv_R = 1.0f / (float)pl.R;
   p.nrb = pl.nrb;
   p.H = pl.H;
   p.ecdf = 1;
@@ -1986,6 +1997,7 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   p.W = full[d - 1];
   p.H = full[d - 2];
   p.R = pl.R;
+  p.inv_R = 1.0f / (float)pl.R;
   p.nrb = pl.nrb;
   p.ecdf = 0;
   p.cell_bits = pl.cell_bits;
