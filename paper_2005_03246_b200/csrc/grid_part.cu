@@ -831,6 +831,10 @@ __global__ void __launch_bounds__(kKdeThreads, 2) plane_kde_group_kernel(
 // the weighted rows of the group's lattice.
 constexpr int kAllThreads = 128;
 constexpr size_t kAllTileBytes = 55 * 1024;  // 4 CTAs per SM
+// rows per tile of the all-groups kernel: 2 NG tiles of W fp64 columns inside the budget
+__host__ __device__ constexpr int all_tile_rows(int ng, int64_t w) {
+  return (int)(kAllTileBytes / (size_t)(2 * ng * w * (int64_t)sizeof(double)));
+}
 
 struct KdeAll {
   int d, nlead;
@@ -847,29 +851,38 @@ struct AllVals {
   double v[2 * NG];  // (psi_+, psi_-) per group
 };
 
-template <int NG>
-__device__ __forceinline__ void all_put(double *tiles, int tile_elems, int W, int nr, int rowoff,
-                                        int col_bits, uint32_t rmask, uint32_t cmask,
-                                        unsigned vmask, uint32_t key, const AllVals<NG> &a,
-                                        bool atomic) {
+// 32-bit shared-window stores / loads (no generic-address materialisation per access)
+__device__ __forceinline__ void sts_f64(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void sts_f64x2(uint32_t a, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  return v;
+}
+
+// One run sum into every group's tile pair.  Tiles sit TSB bytes apart (compile-time stride);
+// tiles of groups whose output plane does not exist are written too and simply never read
+// (the walk re-zeroes every tile), which keeps the stores unpredicated.
+template <int NG, int TSB>
+__device__ __forceinline__ void all_put(uint32_t sbase, int W, int nr, int rowoff, int col_bits,
+                                        uint32_t rmask, uint32_t cmask, uint32_t key,
+                                        const AllVals<NG> &a) {
   const int cr = (int)((key >> col_bits) & rmask) + rowoff;
   const int col = (int)(key & cmask);
   if (cr < 0 || cr >= nr) return;
-  const int ip = cr * W + swz_col(col);
-  const int im = cr * W + swz_col(col - 1);
+  const uint32_t ap = sbase + (uint32_t)(cr * W + swz_col(col)) * 8u;
+  const uint32_t am = sbase + (uint32_t)(cr * W + swz_col(col - 1)) * 8u + TSB;
+  if (col < W) {
 #pragma unroll
-  for (int g = 0; g < NG; ++g) {
-    if (!((vmask >> g) & 1)) continue;
-    double *tp = tiles + (size_t)(2 * g) * tile_elems;
-    double *tm = tp + tile_elems;
-    if (col < W) {
-      if (atomic) atomicAdd(tp + ip, a.v[2 * g]);
-      else tp[ip] = a.v[2 * g];
-    }
-    if (col >= 1) {
-      if (atomic) atomicAdd(tm + im, a.v[2 * g + 1]);
-      else tm[im] = a.v[2 * g + 1];
-    }
+    for (int g = 0; g < NG; ++g) sts_f64(ap + 2 * g * TSB, a.v[2 * g]);
+  }
+  if (col >= 1) {
+#pragma unroll
+    for (int g = 0; g < NG; ++g) sts_f64(am + 2 * g * TSB, a.v[2 * g + 1]);
   }
 }
 
@@ -900,10 +913,12 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
     KdeAll t, const int32_t *__restrict__ bounds, const double *__restrict__ rec, int64_t nrec,
     const uint32_t *__restrict__ keys) {
   constexpr int W = 32 * E, C = E / 2;
+  constexpr int TS = all_tile_rows(NG, W) * W;  // tile stride (elements), Rf <= that many rows
+  constexpr int TSB = TS * (int)sizeof(double);
   extern __shared__ __align__(16) unsigned char smem[];
-  double *tiles = reinterpret_cast<double *>(smem);  // [2 NG][Rf][W], swizzled rows
+  double *tiles = reinterpret_cast<double *>(smem);  // [2 NG][TS], swizzled rows
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   const int Rf = (int)t.Rf, H = (int)t.Mr;
-  const int tile_elems = Rf * W;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int d = t.d, kr = d - 2, kcol = d - 1;
   // full-space leading indices of this CTA's plane, and each group's output plane
@@ -931,7 +946,7 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
   }
   if (vmask == 0) return;  // uniform
   const int64_t fplane = blockIdx.x;
-  tile_zero<double>(tiles, 2 * NG * tile_elems);
+  tile_zero<double>(tiles, 2 * NG * TS);
   const uint32_t cmask = (1u << t.col_bits) - 1u, rmask = (1u << (t.cell_bits - t.col_bits)) - 1u;
   const int c0 = lane * E;
   int pc[C];
@@ -1029,26 +1044,22 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
             for (int i = 0; i < 2 * NG; ++i) sv.v[i] += cv.v[i];
           }
           if (!cont && ckey != 0xFFFFFFFFu && lane == 0)
-            all_put<NG>(tiles, tile_elems, W, nr, rowoff, t.col_bits, rmask, cmask, vmask, ckey, cv,
-                        false);
+            all_put<NG, TSB>(sbase, W, nr, rowoff, t.col_bits, rmask, cmask, ckey, cv);
           const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1);
           if (tail && lane != 31 && key != 0xFFFFFFFFu)
-            all_put<NG>(tiles, tile_elems, W, nr, rowoff, t.col_bits, rmask, cmask, vmask, key, sv,
-                        false);
+            all_put<NG, TSB>(sbase, W, nr, rowoff, t.col_bits, rmask, cmask, key, sv);
           ckey = __shfl_sync(0xffffffffu, key, 31);
 #pragma unroll
           for (int i = 0; i < 2 * NG; ++i) cv.v[i] = __shfl_sync(0xffffffffu, sv.v[i], 31);
         }
         if (ckey != 0xFFFFFFFFu && lane == 0)
-          all_put<NG>(tiles, tile_elems, W, nr, rowoff, t.col_bits, rmask, cmask, vmask, ckey, cv,
-                      false);
+          all_put<NG, TSB>(sbase, W, nr, rowoff, t.col_bits, rmask, cmask, ckey, cv);
       }
       __syncthreads();
       // walk: warp g owns group g's tile pair
       if (warp < NG) {
         const int g = warp;
-        double *tp = tiles + (size_t)(2 * g) * tile_elems;
-        double *tm = tp + tile_elems;
+        const uint32_t tp = sbase + (uint32_t)(2 * g) * TSB, tm = tp + TSB;
         const bool wr = (vmask >> g) & 1;
         double *gp = wr ? t.lat[t.row_split ? 2 * g + ph : g] + oplane[g] * H * W + (int64_t)clo * W
                         : nullptr;
@@ -1059,8 +1070,8 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
           const int r = rneg ? nr - 1 - qr : qr;
 #pragma unroll
           for (int j = 0; j < C; ++j) {
-            na[j] = *reinterpret_cast<const double2 *>(tp + r * W + pc[j]);
-            nb[j] = *reinterpret_cast<const double2 *>(tm + r * W + pc[j]);
+            na[j] = lds_f64x2(tp + (uint32_t)(r * W + pc[j]) * 8u);
+            nb[j] = lds_f64x2(tm + (uint32_t)(r * W + pc[j]) * 8u);
             nold[j] = (wr && rmw) ? reinterpret_cast<const double2 *>(gp + (int64_t)r * W + c0)[j]
                                   : zero2;
           }
@@ -1078,8 +1089,8 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
           if (qr + 1 < nr) fetch(qr + 1);
 #pragma unroll
           for (int j = 0; j < C; ++j) {
-            *reinterpret_cast<double2 *>(tp + r * W + pc[j]) = zero2;
-            *reinterpret_cast<double2 *>(tm + r * W + pc[j]) = zero2;
+            sts_f64x2(tp + (uint32_t)(r * W + pc[j]) * 8u, zero2);
+            sts_f64x2(tm + (uint32_t)(r * W + pc[j]) * 8u, zero2);
             up[2 * j] += ca[j].x; up[2 * j + 1] += ca[j].y;
             um[2 * j] += cb[j].x; um[2 * j + 1] += cb[j].y;
           }
@@ -2122,7 +2133,7 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
         ta.lat[g] = lats + (size_t)g * L;
       }
     }
-    const size_t asmem = (size_t)(2 * ng) * pl.R * pl.W * sizeof(double);
+    const size_t asmem = (size_t)(2 * ng) * all_tile_rows(ng, pl.W) * pl.W * sizeof(double);
     int64_t np_full = 1;
     for (int k = 0; k < d - 2; ++k) np_full *= m[k] + 1;
     FCG_PROF("plane_kde", st);
