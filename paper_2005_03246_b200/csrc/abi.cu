@@ -62,6 +62,41 @@ void prof_record(const char *name, cudaEvent_t a, cudaEvent_t b) {
   g_prof.push_back({name, a, b});
 }
 
+// ---- small device -> host readbacks ----
+// The few host scalars that steer the pipeline (KDE hull, radix digit prune, route counts) are
+// written by one tiny kernel into a mapped pinned buffer instead of a cudaMemcpyAsync: a D2H
+// memcpy into pageable memory waits on a copy engine behind whatever bulk D2H the caller has in
+// flight (bench.py's e2e leg downloads 2 GB results while the next call computes), which stalled
+// the compute stream for tens of milliseconds per call.  SM stores to mapped memory share the
+// link instead of queueing behind it.
+namespace {
+__global__ void readback_kernel(const uint32_t *__restrict__ src, int words,
+                                volatile uint32_t *dst) {
+  for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+  __threadfence_system();
+}
+constexpr size_t kReadbackBytes = 4096;
+}  // namespace
+
+int read_small(void *dst, const void *src, size_t bytes, cudaStream_t st) {
+  static thread_local uint32_t *host = nullptr;
+  if (bytes == 0) return FCG_OK;
+  if (bytes > kReadbackBytes || (bytes & 3) || (reinterpret_cast<uintptr_t>(src) & 3))
+    return fail(FCG_EINVAL, "read_small: readback must be <= 4 KB of 4-byte words");
+  if (host == nullptr) {
+    void *p = nullptr;
+    FCG_CUDA_TRY(cudaHostAlloc(&p, kReadbackBytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    host = static_cast<uint32_t *>(p);
+  }
+  uint32_t *dev = nullptr;
+  FCG_CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dev), host, 0));
+  readback_kernel<<<1, 128, 0, st>>>(static_cast<const uint32_t *>(src), (int)(bytes / 4), dev);
+  FCG_LAUNCH_CHECK();
+  FCG_CUDA_TRY(cudaStreamSynchronize(st));
+  std::memcpy(dst, host, bytes);
+  return FCG_OK;
+}
+
 }  // namespace fcg
 
 extern "C" int fcg_profile_enable(int on) {

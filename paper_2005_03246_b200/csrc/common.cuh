@@ -34,6 +34,10 @@ int fail(int code, const std::string &msg);
 
 int sm_count();
 
+// Copy <= 4 KB (4-byte words) from device memory to host memory and wait for it on `st`
+// (mapped pinned staging, no copy engine: see abi.cu).  Synchronises the stream.
+int read_small(void *dst, const void *src, size_t bytes, cudaStream_t st);
+
 // ---- launch profiler (fcg_profile_*): RAII scope around a kernel launch ----
 bool prof_enabled();
 void prof_record(const char *name, cudaEvent_t a, cudaEvent_t b);

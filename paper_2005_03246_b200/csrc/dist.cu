@@ -180,8 +180,7 @@ extern "C" int fcg_partition_rows(const double *x, int64_t n, int32_t d, const d
     FCG_CUDA_TRY(cudaMemsetAsync(start, 0, (G + 1) * sizeof(int64_t), st));
   }
   int64_t h[66];
-  FCG_CUDA_TRY(cudaMemcpyAsync(h, start, (G + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  FCG_CUDA_TRY(cudaStreamSynchronize(st));
+  FCG_TRY(read_small(h, start, (G + 1) * sizeof(int64_t), st));
   for (int r = 0; r < G; ++r) counts[r] = h[r + 1] - h[r];
   return FCG_OK;
 }

@@ -1816,8 +1816,7 @@ static double f64_unkey(uint64_t k) {
 int hull_centre(const unsigned long long *mm, int d, const double *h, double *c, double *u_bound,
                 cudaStream_t st) {
   unsigned long long host[2 * FCG_MAX_DIM];
-  FCG_CUDA_TRY(cudaMemcpyAsync(host, mm, 2 * d * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-  FCG_CUDA_TRY(cudaStreamSynchronize(st));
+  FCG_TRY(read_small(host, mm, 2 * d * sizeof(unsigned long long), st));
   double ub = 0.0;
   for (int k = 0; k < d; ++k) {
     const double lo = f64_unkey(host[k]), hi = f64_unkey(host[d + k]);

@@ -94,8 +94,7 @@ extern "C" int fcg_multilinear_interp(const double *knots, const int64_t *m, int
   }
   if (clamp_count) {  // host scalar: synchronises the stream
     unsigned long long h = 0;
-    FCG_CUDA_TRY(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st));
-    FCG_CUDA_TRY(cudaStreamSynchronize(st));
+    FCG_TRY(read_small(&h, cnt, sizeof(h), st));
     *clamp_count = (int64_t)h;
   }
   return FCG_OK;

@@ -1236,8 +1236,7 @@ extern "C" int fcg_distinct(const double *x, int64_t n, int32_t d, int32_t *flag
     }
   }
   int32_t h[FCG_MAX_DIM];
-  FCG_CUDA_TRY(cudaMemcpyAsync(h, dflag, FCG_MAX_DIM * 4, cudaMemcpyDeviceToHost, st));
-  FCG_CUDA_TRY(cudaStreamSynchronize(st));
+  FCG_TRY(read_small(h, dflag, FCG_MAX_DIM * 4, st));
   for (int kd = 0; kd < d; ++kd) flags[kd] = h[kd] ? 0 : 1;
   return FCG_OK;
 }
@@ -1293,8 +1292,7 @@ extern "C" int fcg_ecdf_points(const double *x, int64_t n, int32_t d, const doub
   // rank every dimension; the distinct counts decide the route (host sync)
   for (int k = 0; k < d; ++k) FCG_TRY(rank_dim(x, n, d, k, p, st));
   int32_t nd[FCG_MAX_DIM];
-  FCG_CUDA_TRY(cudaMemcpyAsync(nd, p.ndist, d * 4, cudaMemcpyDeviceToHost, st));
-  FCG_CUDA_TRY(cudaStreamSynchronize(st));
+  FCG_TRY(read_small(nd, p.ndist, d * 4, st));
   double cells = 1.0;
   for (int k = 0; k < d; ++k) cells *= (double)nd[k];
 

@@ -434,8 +434,7 @@ int radix_sort_pairs_pruned(uint64_t *keys, int32_t *vals, int64_t n, const Radi
     FCG_LAUNCH_CHECK();
   }
   unsigned long long h[2];
-  FCG_CUDA_TRY(cudaMemcpyAsync(h, ao, sizeof(h), cudaMemcpyDeviceToHost, st));
-  FCG_CUDA_TRY(cudaStreamSynchronize(st));
+  FCG_TRY(read_small(h, ao, sizeof(h), st));
   const uint64_t diff = h[0] ^ h[1];
   uint32_t mask = 0;
   for (int dg = 0; dg < 8; ++dg)
