@@ -831,9 +831,17 @@ __global__ void __launch_bounds__(kKdeThreads, 2) plane_kde_group_kernel(
 // the weighted rows of the group's lattice.
 constexpr int kAllThreads = 128;
 constexpr size_t kAllTileBytes = 55 * 1024;  // 4 CTAs per SM
-// rows per tile of the all-groups kernel: 2 NG tiles of W fp64 columns inside the budget
+// Tile layout of the all-groups kernel: 2 NG tiles (group g: column sign + at 2g, - at 2g+1) of
+// rows RS = W + 2 fp64 apart and TS fp64 apart, so a row starts 16 bytes further round the banks
+// than the row above it and a tile (TS / 2 odd in 16-byte units) likewise: the horizontal
+// pre-scan, where 8 consecutive lanes walk 8 different (tile, row) sequences in lock step, and
+// the walk, where the lanes read one row's consecutive 16-byte chunks, are both conflict-free
+// without an index swizzle.
 __host__ __device__ constexpr int all_tile_rows(int ng, int64_t w) {
-  return (int)(kAllTileBytes / (size_t)(2 * ng * w * (int64_t)sizeof(double)));
+  return (int)(((int64_t)(kAllTileBytes / (16 * (size_t)ng)) - 2) / (w + 2));
+}
+__host__ __device__ constexpr int all_tile_stride(int ng, int64_t w) {
+  return all_tile_rows(ng, w) * (int)(w + 2) + 2 * (1 - (all_tile_rows(ng, w) & 1));
 }
 
 struct KdeAll {
@@ -864,25 +872,24 @@ __device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
   return v;
 }
 
-// One run sum into every group's tile pair.  Tiles sit TSB bytes apart (compile-time stride);
-// tiles of groups whose output plane does not exist are written too and simply never read
-// (the walk re-zeroes every tile), which keeps the stores unpredicated.
-template <int NG, int TSB>
-__device__ __forceinline__ void all_put(uint32_t sbase, int W, int nr, int rowoff, int col_bits,
+// One run sum into every group's tile pair (raw cell values; the column sign - tile holds the
+// cell at column col - 1).  Tiles of groups whose output plane does not exist are written too
+// and simply never read (the walk re-zeroes every tile), which keeps the stores unpredicated.
+template <int NG, int W, int TSB>
+__device__ __forceinline__ void all_put(uint32_t sbase, int nr, int rowoff, int col_bits,
                                         uint32_t rmask, uint32_t cmask, uint32_t key,
                                         const AllVals<NG> &a) {
   const int cr = (int)((key >> col_bits) & rmask) + rowoff;
   const int col = (int)(key & cmask);
   if (cr < 0 || cr >= nr) return;
-  const uint32_t ap = sbase + (uint32_t)(cr * W + swz_col(col)) * 8u;
-  const uint32_t am = sbase + (uint32_t)(cr * W + swz_col(col - 1)) * 8u + TSB;
+  const uint32_t ap = sbase + (uint32_t)(cr * (W + 2) + col) * 8u;
   if (col < W) {
 #pragma unroll
     for (int g = 0; g < NG; ++g) sts_f64(ap + 2 * g * TSB, a.v[2 * g]);
   }
   if (col >= 1) {
 #pragma unroll
-    for (int g = 0; g < NG; ++g) sts_f64(am + 2 * g * TSB, a.v[2 * g + 1]);
+    for (int g = 0; g < NG; ++g) sts_f64(ap + (2 * g + 1) * TSB - 8u, a.v[2 * g + 1]);
   }
 }
 
@@ -913,10 +920,11 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
     KdeAll t, const int32_t *__restrict__ bounds, const double *__restrict__ rec, int64_t nrec,
     const uint32_t *__restrict__ keys) {
   constexpr int W = 32 * E, C = E / 2;
-  constexpr int TS = all_tile_rows(NG, W) * W;  // tile stride (elements), Rf <= that many rows
+  constexpr int RS = W + 2;                      // row stride (fp64)
+  constexpr int TS = all_tile_stride(NG, W);     // tile stride (fp64); Rf <= all_tile_rows
   constexpr int TSB = TS * (int)sizeof(double);
   extern __shared__ __align__(16) unsigned char smem[];
-  double *tiles = reinterpret_cast<double *>(smem);  // [2 NG][TS], swizzled rows
+  double *tiles = reinterpret_cast<double *>(smem);  // [2 NG][TS] tiles, RS-strided rows
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   const int Rf = (int)t.Rf, H = (int)t.Mr;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -948,18 +956,16 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
   const int64_t fplane = blockIdx.x;
   tile_zero<double>(tiles, 2 * NG * TS);
   const uint32_t cmask = (1u << t.col_bits) - 1u, rmask = (1u << (t.cell_bits - t.col_bits)) - 1u;
-  const int c0 = lane * E;
-  int pc[C];
-#pragma unroll
-  for (int j = 0; j < C; ++j) {
-    const int ch = lane * C + j;
-    pc[j] = (ch ^ ((ch >> 3) & 7)) * 2;
-  }
+  // walk ownership: lane l holds the column pairs (2 l, 2 l + 1) + 64 j, j < C, so a warp's
+  // accesses of one row are consecutive 16-byte chunks (tiles and the plane alike)
   double zp[E], zm[E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    zp[e] = t.zc_pos[c0 + e];
-    zm[e] = t.zc_neg[c0 + e];
+  for (int j = 0; j < C; ++j) {
+    const int c = 64 * j + 2 * lane;
+    zp[2 * j] = t.zc_pos[c];
+    zp[2 * j + 1] = t.zc_pos[c + 1];
+    zm[2 * j] = t.zc_neg[c];
+    zm[2 * j + 1] = t.zc_neg[c + 1];
   }
   // field pointers: A, q_lead, q_row, q_col (factored records)
   const double *fA = rec, *fr = rec + (int64_t)(1 + kr) * nrec, *fc = rec + (int64_t)(1 + kcol) * nrec;
@@ -1044,22 +1050,55 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
             for (int i = 0; i < 2 * NG; ++i) sv.v[i] += cv.v[i];
           }
           if (!cont && ckey != 0xFFFFFFFFu && lane == 0)
-            all_put<NG, TSB>(sbase, W, nr, rowoff, t.col_bits, rmask, cmask, ckey, cv);
+            all_put<NG, W, TSB>(sbase, nr, rowoff, t.col_bits, rmask, cmask, ckey, cv);
           const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1);
           if (tail && lane != 31 && key != 0xFFFFFFFFu)
-            all_put<NG, TSB>(sbase, W, nr, rowoff, t.col_bits, rmask, cmask, key, sv);
+            all_put<NG, W, TSB>(sbase, nr, rowoff, t.col_bits, rmask, cmask, key, sv);
           ckey = __shfl_sync(0xffffffffu, key, 31);
 #pragma unroll
           for (int i = 0; i < 2 * NG; ++i) cv.v[i] = __shfl_sync(0xffffffffu, sv.v[i], 31);
         }
         if (ckey != 0xFFFFFFFFu && lane == 0)
-          all_put<NG, TSB>(sbase, W, nr, rowoff, t.col_bits, rmask, cmask, ckey, cv);
+          all_put<NG, W, TSB>(sbase, nr, rowoff, t.col_bits, rmask, cmask, ckey, cv);
       }
       __syncthreads();
-      // walk: warp g owns group g's tile pair
+      // horizontal pre-scan of every tile row in place: warps of even index run the column
+      // sign + tiles (inclusive prefix), odd ones the - tiles (inclusive suffix); lane q of a
+      // direction owns (group q % NG, row q / NG)
+      {
+        const int dir = warp & 1;
+        const int q = (warp >> 1) * 32 + lane;
+        const int g = q % NG, r = q / NG;
+        if (r < nr) {
+          const uint32_t ra = sbase + (uint32_t)((2 * g + dir) * TS + r * RS) * 8u;
+          double run = 0.0;
+          if (dir == 0) {
+#pragma unroll 8
+            for (int c = 0; c < W; c += 2) {
+              double2 v = lds_f64x2(ra + c * 8);
+              v.x += run;
+              v.y += v.x;
+              run = v.y;
+              sts_f64x2(ra + c * 8, v);
+            }
+          } else {
+#pragma unroll 8
+            for (int c = W - 2; c >= 0; c -= 2) {
+              double2 v = lds_f64x2(ra + c * 8);
+              v.y += run;
+              v.x += v.y;
+              run = v.x;
+              sts_f64x2(ra + c * 8, v);
+            }
+          }
+        }
+      }
+      __syncthreads();
+      // walk: warp g owns group g's tile pair; the rows are already prefix-summed along the
+      // columns, so the 2-D prefix is a per-column running sum kept in registers across blocks
       if (warp < NG) {
         const int g = warp;
-        const uint32_t tp = sbase + (uint32_t)(2 * g) * TSB, tm = tp + TSB;
+        const uint32_t tp = sbase + (uint32_t)(2 * g) * TSB + lane * 16u, tm = tp + TSB;
         const bool wr = (vmask >> g) & 1;
         double *gp = wr ? t.lat[t.row_split ? 2 * g + ph : g] + oplane[g] * H * W + (int64_t)clo * W
                         : nullptr;
@@ -1070,9 +1109,9 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
           const int r = rneg ? nr - 1 - qr : qr;
 #pragma unroll
           for (int j = 0; j < C; ++j) {
-            na[j] = lds_f64x2(tp + (uint32_t)(r * W + pc[j]) * 8u);
-            nb[j] = lds_f64x2(tm + (uint32_t)(r * W + pc[j]) * 8u);
-            nold[j] = (wr && rmw) ? reinterpret_cast<const double2 *>(gp + (int64_t)r * W + c0)[j]
+            na[j] = lds_f64x2(tp + (uint32_t)(r * RS + 64 * j) * 8u);
+            nb[j] = lds_f64x2(tm + (uint32_t)(r * RS + 64 * j) * 8u);
+            nold[j] = (wr && rmw) ? reinterpret_cast<const double2 *>(gp + (int64_t)r * W + 2 * lane)[32 * j]
                                   : zero2;
           }
         };
@@ -1089,56 +1128,27 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
           if (qr + 1 < nr) fetch(qr + 1);
 #pragma unroll
           for (int j = 0; j < C; ++j) {
-            sts_f64x2(tp + (uint32_t)(r * W + pc[j]) * 8u, zero2);
-            sts_f64x2(tm + (uint32_t)(r * W + pc[j]) * 8u, zero2);
+            sts_f64x2(tp + (uint32_t)(r * RS + 64 * j) * 8u, zero2);
+            sts_f64x2(tm + (uint32_t)(r * RS + 64 * j) * 8u, zero2);
             up[2 * j] += ca[j].x; up[2 * j + 1] += ca[j].y;
             um[2 * j] += cb[j].x; um[2 * j + 1] += cb[j].y;
           }
           if (!wr) continue;  // warp-uniform
-          double tsp = 0.0, tsm = 0.0;
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            tsp += up[e];
-            tsm += um[e];
-          }
-          double ip = tsp, im = tsm;
-#pragma unroll
-          for (int off = 1; off < 32; off <<= 1) {
-            const double xp = __shfl_up_sync(0xffffffffu, ip, off);
-            const double xm = __shfl_down_sync(0xffffffffu, im, off);
-            if (lane >= off) ip += xp;
-            if (lane + off < 32) im += xm;
-          }
-          double sp[E], sm[E];
-          double run = ip - tsp;
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            run += up[e];
-            sp[e] = run;
-          }
-          run = im - tsm;
-#pragma unroll
-          for (int e = E - 1; e >= 0; --e) {
-            run += um[e];
-            sm[e] = run;
-          }
           const double zrv = zr ? __ldg(zr + clo + r) : 1.0;
-          double2 *o = reinterpret_cast<double2 *>(gp + (int64_t)r * W + c0);
+          double2 *o = reinterpret_cast<double2 *>(gp + (int64_t)r * W + 2 * lane);
 #pragma unroll
           for (int j = 0; j < C; ++j) {
             const int e = 2 * j;
             double2 v;
-            v.x = zrv * (zp[e] * sp[e] + zm[e] * sm[e]);
-            v.y = zrv * (zp[e + 1] * sp[e + 1] + zm[e + 1] * sm[e + 1]);
+            v.x = zrv * (zp[e] * up[e] + zm[e] * um[e]);
+            v.y = zrv * (zp[e + 1] * up[e + 1] + zm[e + 1] * um[e + 1]);
             if (rmw) {
               v.x += old[j].x;
               v.y += old[j].y;
             }
-            o[j] = v;
+            o[32 * j] = v;
           }
         }
-      } else {
-        // idle warps: nothing to walk (NG < warps)
       }
     }
   }
@@ -1928,9 +1938,7 @@ PartPlan plan_kde_partition(int d, const int64_t *m, int64_t n, bool factored) {
   int64_t nrb = 1, Rf = Hf;
   while (true) {
     Rf = ceil_div(Hf, nrb);
-    const size_t bytes = pl.all ? (size_t)(2 * ng) * Rf * pl.W * sizeof(double)
-                                : kde_group_smem(Rf, pl.W, G);
-    if (bytes <= (pl.all ? kAllTileBytes : kKdeTileBytes)) break;
+    if (pl.all ? Rf <= all_tile_rows(ng, pl.W) : kde_group_smem(Rf, pl.W, G) <= kKdeTileBytes) break;
     if (Rf == 1) return pl;
     ++nrb;
   }
@@ -2132,7 +2140,7 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
         ta.lat[g] = lats + (size_t)g * L;
       }
     }
-    const size_t asmem = (size_t)(2 * ng) * all_tile_rows(ng, pl.W) * pl.W * sizeof(double);
+    const size_t asmem = (size_t)(2 * ng) * all_tile_stride(ng, pl.W) * sizeof(double);
     int64_t np_full = 1;
     for (int k = 0; k < d - 2; ++k) np_full *= m[k] + 1;
     FCG_PROF("plane_kde", st);
