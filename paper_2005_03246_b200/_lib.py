@@ -16,7 +16,7 @@ import numpy as np
 from .core import OverflowGuardError, ParameterError, ShapeError
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libfastcdf_b200.so"
+LIB_PATH = Path(os.environ["FCG_LIB_PATH"]) if os.environ.get("FCG_LIB_PATH") else _HERE / "libfastcdf_b200.so"  # dev A/B override
 ABI_VERSION = 1
 
 FCG_OK = 0

@@ -97,6 +97,16 @@ __device__ __forceinline__ uint64_t f64_key(double v) {
   return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
 }
 
+// Bulk prefetch of [p, p + bytes) into L2 (one TMA-unit request; rounded out to 16 bytes).
+// Used to pull the next work item's rows toward the SM while the current one computes.
+__device__ __forceinline__ void l2_prefetch(const void *p, size_t bytes) {
+  if (bytes == 0) return;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a))
+               : "memory");
+}
+
 // Lanes of the warp holding the same 8-bit digit (+ a 9th bit for out-of-range lanes): the
 // multisplit by 9 ballots (one per digit bit) instead of match.any -- the radix ranking's hot
 // instruction.

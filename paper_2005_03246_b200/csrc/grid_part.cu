@@ -984,6 +984,40 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
       const int nr = chi - clo;
       const int rowoff = (int)(rb * Rf) - sr - clo;
       __syncthreads();  // the previous block's walk has re-zeroed the tiles
+      // L2 prefetch of the next row block's records and (second row sign) of the plane rows its
+      // walk reads back, so their DRAM latency is off the next block's critical path
+      if (warp == nw - 1 && lane < 8 + NG) {
+        int nph = ph;
+        int64_t nrbi = rbi + 1;
+        if (nrbi >= t.nrb) {
+          nph = ph + 1;
+          nrbi = 0;
+        }
+        if (nph < 2) {
+          const int64_t rbn = nph ? t.nrb - 1 - nrbi : nrbi;
+          const int64_t bn = fplane * t.nrb + rbn;
+          if (lane < 6) {
+            const int32_t a0 = bounds[bn * (nw + 1)], a1 = bounds[bn * (nw + 1) + nw];
+            const size_t cnt = (size_t)(a1 - a0);
+            if (lane == 0) l2_prefetch(keys + a0, cnt * sizeof(uint32_t));
+            else if (lane == 1) l2_prefetch(fA + a0, cnt * sizeof(double));
+            else if (lane == 2) l2_prefetch(fc + a0, cnt * sizeof(double));
+            else if (lane == 3 && t.nlead > 0) l2_prefetch(fq0 + a0, cnt * sizeof(double));
+            else if (lane == 4 && t.nlead > 1) l2_prefetch(fq1 + a0, cnt * sizeof(double));
+            else if (lane == 5 && nph) l2_prefetch(fr + a0, cnt * sizeof(double));
+          } else if (lane >= 8 && nph && !t.row_split) {
+            const int g = lane - 8;
+            const int nlo = (int)(rbn * Rf - nph), nclo = nlo < 0 ? 0 : nlo;
+            const int nchi = nlo + Rf > H ? H : nlo + Rf;
+            const double *lp = nullptr;
+#pragma unroll
+            for (int gg = 0; gg < NG; ++gg)
+              if (gg == g) lp = t.lat[gg] + oplane[gg] * H * W;
+            if (((vmask >> g) & 1) && nchi > nclo)
+              l2_prefetch(lp + (int64_t)nclo * W, (size_t)(nchi - nclo) * W * sizeof(double));
+          }
+        }
+      }
       {
         // warp shares aligned to run boundaries (share_bounds_kernel): every run of equal keys
         // is complete inside one share, so all tile writes are plain stores
