@@ -930,10 +930,12 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int d = t.d, kr = d - 2, kcol = d - 1;
   // full-space leading indices of this CTA's plane, and each group's output plane
-  int64_t fidx[FCG_MAX_DIM];
+  constexpr int NL = NG == 4 ? 2 : 1;  // leading axes (t.nlead = log2 NG)
+  int64_t fidx[NL];
   {
     int64_t rem = blockIdx.x;
-    for (int k = t.nlead - 1; k >= 0; --k) {
+#pragma unroll
+    for (int k = NL - 1; k >= 0; --k) {
       fidx[k] = rem % (t.lead_m[k] + 1);
       rem /= t.lead_m[k] + 1;
     }
@@ -944,7 +946,8 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
   for (int g = 0; g < NG; ++g) {
     bool ok = true;
     int64_t pidx = 0;
-    for (int k = 0; k < t.nlead; ++k) {
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
       const int64_t i = fidx[k] - ((g >> k) & 1);
       ok = ok && i >= 0 && i < t.lead_m[k];
       pidx = pidx * t.lead_m[k] + i;
@@ -970,6 +973,15 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
   // field pointers: A, q_lead, q_row, q_col (factored records)
   const double *fA = rec, *fr = rec + (int64_t)(1 + kr) * nrec, *fc = rec + (int64_t)(1 + kcol) * nrec;
   const double *fq0 = rec + nrec, *fq1 = rec + 2 * nrec;
+  // this warp's output plane per row sign (selected with compile-time indices so oplane stays in
+  // registers)
+  double *gbase0 = nullptr, *gbase1 = nullptr;
+#pragma unroll
+  for (int gg = 0; gg < NG; ++gg)
+    if (gg == warp) {
+      gbase0 = t.lat[t.row_split ? 2 * gg : gg] + oplane[gg] * H * W;
+      gbase1 = t.lat[t.row_split ? 2 * gg + 1 : gg] + oplane[gg] * H * W;
+    }
   for (int ph = 0; ph < 2; ++ph) {
     const int rneg = ph, sr = ph;
     const double *zr = t.row_split ? nullptr : (rneg ? t.zr_neg : t.zr_pos);
@@ -1134,8 +1146,7 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
         const int g = warp;
         const uint32_t tp = sbase + (uint32_t)(2 * g) * TSB + lane * 16u, tm = tp + TSB;
         const bool wr = (vmask >> g) & 1;
-        double *gp = wr ? t.lat[t.row_split ? 2 * g + ph : g] + oplane[g] * H * W + (int64_t)clo * W
-                        : nullptr;
+        double *gp = wr ? (ph ? gbase1 : gbase0) + (int64_t)clo * W : nullptr;
         const bool rmw = ph > 0 && !t.row_split;
         const double2 zero2 = make_double2(0.0, 0.0);
         double2 na[C], nb[C], nold[C];  // next row: tiles and (accumulate pass) plane values
