@@ -923,6 +923,7 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
   constexpr int RS = W + 2;                      // row stride (fp64)
   constexpr int TS = all_tile_stride(NG, W);     // tile stride (fp64); Rf <= all_tile_rows
   constexpr int TSB = TS * (int)sizeof(double);
+  static_assert(NG * all_tile_rows(NG, W) <= 64, "pre-scan needs a lane per (group, row) and direction");
   extern __shared__ __align__(16) unsigned char smem[];
   double *tiles = reinterpret_cast<double *>(smem);  // [2 NG][TS] tiles, RS-strided rows
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
@@ -1110,31 +1111,45 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
       __syncthreads();
       // horizontal pre-scan of every tile row in place: warps of even index run the column
       // sign + tiles (inclusive prefix), odd ones the - tiles (inclusive suffix); lane q of a
-      // direction owns (group q % NG, row q / NG)
+      // direction owns (group q % NG, row q / NG).  Chunks are loaded 8 at a time ahead of the
+      // dependent adds.
       {
         const int dir = warp & 1;
         const int q = (warp >> 1) * 32 + lane;
-        const int g = q % NG, r = q / NG;
+        const int gq = q % NG, r = q / NG;
+        constexpr int SPAN = W;
         if (r < nr) {
-          const uint32_t ra = sbase + (uint32_t)((2 * g + dir) * TS + r * RS) * 8u;
+          const uint32_t ra = sbase + (uint32_t)((2 * gq + dir) * TS + r * RS) * 8u;
           double run = 0.0;
           if (dir == 0) {
-#pragma unroll 8
-            for (int c = 0; c < W; c += 2) {
-              double2 v = lds_f64x2(ra + c * 8);
-              v.x += run;
-              v.y += v.x;
-              run = v.y;
-              sts_f64x2(ra + c * 8, v);
+#pragma unroll
+            for (int b = 0; b < SPAN / 16; ++b) {
+              double2 v[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) v[k] = lds_f64x2(ra + (16 * b + 2 * k) * 8);
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                v[k].x += run;
+                v[k].y += v[k].x;
+                run = v[k].y;
+              }
+#pragma unroll
+              for (int k = 0; k < 8; ++k) sts_f64x2(ra + (16 * b + 2 * k) * 8, v[k]);
             }
           } else {
-#pragma unroll 8
-            for (int c = W - 2; c >= 0; c -= 2) {
-              double2 v = lds_f64x2(ra + c * 8);
-              v.y += run;
-              v.x += v.y;
-              run = v.x;
-              sts_f64x2(ra + c * 8, v);
+#pragma unroll
+            for (int b = 0; b < SPAN / 16; ++b) {
+              double2 v[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) v[k] = lds_f64x2(ra + (SPAN - 2 - 16 * b - 2 * k) * 8);
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                v[k].y += run;
+                v[k].x += v[k].y;
+                run = v[k].x;
+              }
+#pragma unroll
+              for (int k = 0; k < 8; ++k) sts_f64x2(ra + (SPAN - 2 - 16 * b - 2 * k) * 8, v[k]);
             }
           }
         }
