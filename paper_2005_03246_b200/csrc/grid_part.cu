@@ -1164,49 +1164,92 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
         double *gp = wr ? (ph ? gbase1 : gbase0) + (int64_t)clo * W : nullptr;
         const bool rmw = ph > 0 && !t.row_split;
         const double2 zero2 = make_double2(0.0, 0.0);
-        double2 na[C], nb[C], nold[C];  // next row: tiles and (accumulate pass) plane values
-        auto fetch = [&](int qr) {
-          const int r = rneg ? nr - 1 - qr : qr;
-#pragma unroll
-          for (int j = 0; j < C; ++j) {
-            na[j] = lds_f64x2(tp + (uint32_t)(r * RS + 64 * j) * 8u);
-            nb[j] = lds_f64x2(tm + (uint32_t)(r * RS + 64 * j) * 8u);
-            nold[j] = (wr && rmw) ? reinterpret_cast<const double2 *>(gp + (int64_t)r * W + 2 * lane)[32 * j]
-                                  : zero2;
+        constexpr int RMAX = all_tile_rows(NG, W);
+        if constexpr (RMAX <= 8) {  // few rows per block: all of them unrolled, loads up front
+          // every row's read-back plane values and row factor in flight at once
+          double2 oldr[RMAX][C];
+          double zrr[RMAX];
+  #pragma unroll
+          for (int qr = 0; qr < RMAX; ++qr) {
+            const int r = rneg ? nr - 1 - qr : qr;
+            const bool in = qr < nr && wr;
+            zrr[qr] = (in && zr) ? __ldg(zr + clo + r) : 1.0;
+  #pragma unroll
+            for (int j = 0; j < C; ++j)
+              oldr[qr][j] = (in && rmw) ? reinterpret_cast<const double2 *>(gp + (int64_t)r * W + 2 * lane)[32 * j]
+                                        : zero2;
           }
-        };
-        fetch(0);
-        for (int qr = 0; qr < nr; ++qr) {
-          const int r = rneg ? nr - 1 - qr : qr;
-          double2 ca[C], cb[C], old[C];
-#pragma unroll
-          for (int j = 0; j < C; ++j) {
-            ca[j] = na[j];
-            cb[j] = nb[j];
-            old[j] = nold[j];
-          }
-          if (qr + 1 < nr) fetch(qr + 1);
-#pragma unroll
-          for (int j = 0; j < C; ++j) {
-            sts_f64x2(tp + (uint32_t)(r * RS + 64 * j) * 8u, zero2);
-            sts_f64x2(tm + (uint32_t)(r * RS + 64 * j) * 8u, zero2);
-            up[2 * j] += ca[j].x; up[2 * j + 1] += ca[j].y;
-            um[2 * j] += cb[j].x; um[2 * j + 1] += cb[j].y;
-          }
-          if (!wr) continue;  // warp-uniform
-          const double zrv = zr ? __ldg(zr + clo + r) : 1.0;
-          double2 *o = reinterpret_cast<double2 *>(gp + (int64_t)r * W + 2 * lane);
-#pragma unroll
-          for (int j = 0; j < C; ++j) {
-            const int e = 2 * j;
-            double2 v;
-            v.x = zrv * (zp[e] * up[e] + zm[e] * um[e]);
-            v.y = zrv * (zp[e + 1] * up[e + 1] + zm[e + 1] * um[e + 1]);
-            if (rmw) {
-              v.x += old[j].x;
-              v.y += old[j].y;
+  #pragma unroll
+          for (int qr = 0; qr < RMAX; ++qr) {
+            if (qr < nr) {
+              const int r = rneg ? nr - 1 - qr : qr;
+  #pragma unroll
+              for (int j = 0; j < C; ++j) {
+                const uint32_t o = (uint32_t)(r * RS + 64 * j) * 8u;
+                const double2 a = lds_f64x2(tp + o), b = lds_f64x2(tm + o);
+                sts_f64x2(tp + o, zero2);
+                sts_f64x2(tm + o, zero2);
+                up[2 * j] += a.x; up[2 * j + 1] += a.y;
+                um[2 * j] += b.x; um[2 * j + 1] += b.y;
+              }
+              if (wr) {  // warp-uniform
+                double2 *o = reinterpret_cast<double2 *>(gp + (int64_t)r * W + 2 * lane);
+  #pragma unroll
+                for (int j = 0; j < C; ++j) {
+                  const int e = 2 * j;
+                  double2 v;
+                  v.x = zrr[qr] * (zp[e] * up[e] + zm[e] * um[e]) + oldr[qr][j].x;
+                  v.y = zrr[qr] * (zp[e + 1] * up[e + 1] + zm[e + 1] * um[e + 1]) + oldr[qr][j].y;
+                  o[32 * j] = v;
+                }
+              }
             }
-            o[32 * j] = v;
+          }
+        } else {  // many rows: one row of look-ahead (keeps the registers in budget)
+          double2 na[C], nb[C], nold[C];  // next row: tiles and (accumulate pass) plane values
+          auto fetch = [&](int qr) {
+            const int r = rneg ? nr - 1 - qr : qr;
+  #pragma unroll
+            for (int j = 0; j < C; ++j) {
+              na[j] = lds_f64x2(tp + (uint32_t)(r * RS + 64 * j) * 8u);
+              nb[j] = lds_f64x2(tm + (uint32_t)(r * RS + 64 * j) * 8u);
+              nold[j] = (wr && rmw) ? reinterpret_cast<const double2 *>(gp + (int64_t)r * W + 2 * lane)[32 * j]
+                                    : zero2;
+            }
+          };
+          fetch(0);
+          for (int qr = 0; qr < nr; ++qr) {
+            const int r = rneg ? nr - 1 - qr : qr;
+            double2 ca[C], cb[C], old[C];
+  #pragma unroll
+            for (int j = 0; j < C; ++j) {
+              ca[j] = na[j];
+              cb[j] = nb[j];
+              old[j] = nold[j];
+            }
+            if (qr + 1 < nr) fetch(qr + 1);
+  #pragma unroll
+            for (int j = 0; j < C; ++j) {
+              sts_f64x2(tp + (uint32_t)(r * RS + 64 * j) * 8u, zero2);
+              sts_f64x2(tm + (uint32_t)(r * RS + 64 * j) * 8u, zero2);
+              up[2 * j] += ca[j].x; up[2 * j + 1] += ca[j].y;
+              um[2 * j] += cb[j].x; um[2 * j + 1] += cb[j].y;
+            }
+            if (!wr) continue;  // warp-uniform
+            const double zrv = zr ? __ldg(zr + clo + r) : 1.0;
+            double2 *o = reinterpret_cast<double2 *>(gp + (int64_t)r * W + 2 * lane);
+  #pragma unroll
+            for (int j = 0; j < C; ++j) {
+              const int e = 2 * j;
+              double2 v;
+              v.x = zrv * (zp[e] * up[e] + zm[e] * um[e]);
+              v.y = zrv * (zp[e + 1] * up[e + 1] + zm[e + 1] * um[e + 1]);
+              if (rmw) {
+                v.x += old[j].x;
+                v.y += old[j].y;
+              }
+              o[32 * j] = v;
+            }
           }
         }
       }
