@@ -1060,7 +1060,8 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
         if (sb < se) load(nx, sb);
         for (int32_t qb = sb; qb < se; qb += 32) {
           const Raw cur = nx;
-          if (qb + 32 < se) load(nx, qb + 32);
+          const bool more = qb + 32 < se;  // warp-uniform
+          if (more) load(nx, qb + 32);
           const uint32_t key = cur.key;
           const double qcv = cur.qc, q0v = cur.q0, q1v = cur.q1;
           AllVals<NG> a;
@@ -1090,23 +1091,26 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
               if (lane - o >= hl) sv.v[i] += u;
             }
           }
-          const uint32_t key0 = __shfl_sync(0xffffffffu, key, 0);
-          const bool cont = key0 == ckey;
-          if (cont && hl == 0) {
+          // a run carried in from the previous window continues in this window's first run
+          if (ckey != 0xFFFFFFFFu && hl == 0) {
 #pragma unroll
             for (int i = 0; i < 2 * NG; ++i) sv.v[i] += cv.v[i];
           }
-          if (!cont && ckey != 0xFFFFFFFFu && lane == 0)
-            all_put<NG, W, TSB>(sbase, nr, rowoff, t.col_bits, rmask, cmask, ckey, cv);
-          const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1);
-          if (tail && lane != 31 && key != 0xFFFFFFFFu)
+          // lane 31's run ends here unless the next window starts with the same key (the
+          // prefetched next window tells), so only a continuing run is carried
+          const uint32_t nk0 = __shfl_sync(0xffffffffu, more ? nx.key : 0xFFFFFFFFu, 0);
+          const uint32_t k31 = __shfl_sync(0xffffffffu, key, 31);
+          const bool cont_out = k31 != 0xFFFFFFFFu && k31 == nk0;  // warp-uniform
+          const bool tail = lane == 31 ? !cont_out : ((heads >> (lane + 1)) & 1);
+          if (tail && key != 0xFFFFFFFFu)
             all_put<NG, W, TSB>(sbase, nr, rowoff, t.col_bits, rmask, cmask, key, sv);
-          ckey = __shfl_sync(0xffffffffu, key, 31);
+          ckey = 0xFFFFFFFFu;
+          if (cont_out) {
+            ckey = k31;
 #pragma unroll
-          for (int i = 0; i < 2 * NG; ++i) cv.v[i] = __shfl_sync(0xffffffffu, sv.v[i], 31);
+            for (int i = 0; i < 2 * NG; ++i) cv.v[i] = __shfl_sync(0xffffffffu, sv.v[i], 31);
+          }
         }
-        if (ckey != 0xFFFFFFFFu && lane == 0)
-          all_put<NG, W, TSB>(sbase, nr, rowoff, t.col_bits, rmask, cmask, ckey, cv);
       }
       __syncthreads();
       // horizontal pre-scan of every tile row in place: warps of even index run the column
