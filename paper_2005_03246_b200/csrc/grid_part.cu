@@ -1049,7 +1049,7 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
           const int32_t q = qb + lane;
           const bool in = q < se;
           const int32_t qq = in ? q : sb;
-          r.key = in ? keys[q] : 0xFFFFFFFFu;
+          r.key = in ? keys[q] : 0x80000000u | (uint32_t)lane;  // padding: distinct invalid keys
           r.A = fA[qq];
           r.qc = fc[qq];
           r.q0 = t.nlead > 0 ? fq0[qq] : 1.0;
@@ -1065,7 +1065,8 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
           const uint32_t key = cur.key;
           const double qcv = cur.qc, q0v = cur.q0, q1v = cur.q1;
           AllVals<NG> a;
-          const double base = key != 0xFFFFFFFFu ? cur.A * cur.qr : 0.0;
+          const bool valid = key < 0x80000000u;  // keys have <= 31 bits (plan_kde_partition)
+          const double base = valid ? cur.A * cur.qr : 0.0;
 #pragma unroll
           for (int g = 0; g < NG; ++g) {
             double v = base;
@@ -1098,11 +1099,11 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
           }
           // lane 31's run ends here unless the next window starts with the same key (the
           // prefetched next window tells), so only a continuing run is carried
-          const uint32_t nk0 = __shfl_sync(0xffffffffu, more ? nx.key : 0xFFFFFFFFu, 0);
+          const uint32_t nk0 = __shfl_sync(0xffffffffu, more ? nx.key : 0x80000000u, 0);
           const uint32_t k31 = __shfl_sync(0xffffffffu, key, 31);
-          const bool cont_out = k31 != 0xFFFFFFFFu && k31 == nk0;  // warp-uniform
+          const bool cont_out = k31 < 0x80000000u && k31 == nk0;  // warp-uniform
           const bool tail = lane == 31 ? !cont_out : ((heads >> (lane + 1)) & 1);
-          if (tail && key != 0xFFFFFFFFu)
+          if (tail && valid)
             all_put<NG, W, TSB>(sbase, nr, rowoff, t.col_bits, rmask, cmask, key, sv);
           ckey = 0xFFFFFFFFu;
           if (cont_out) {
