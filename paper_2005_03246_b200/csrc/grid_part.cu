@@ -22,6 +22,9 @@ int launch_kde_zf(const double *knots, int d, const int64_t *m, const double *c,
 namespace {
 
 constexpr uint32_t kDead = 0xFFFFFFFFu;
+// KDE record keys have <= 31 bits (plan_kde_partition); window lanes past a share's end carry
+// kPadKey | lane, distinct per lane so they never form a run (which would cost scan steps)
+constexpr uint32_t kPadKey = 0x80000000u;
 constexpr int kPlaneThreads = 512;
 constexpr int kKdeThreads = 256;
 constexpr size_t kEcdfTileBytes = 96 * 1024;   // int32 tile budget (2 CTAs per SM)
@@ -438,7 +441,7 @@ __device__ __forceinline__ KdeRec kde_load(const uint32_t *__restrict__ keys,
                                            int mfield, int d, const double *c, const double *a,
                                            unsigned negmask) {
   KdeRec r;
-  r.key = in ? keys[q] : 0xFFFFFFFFu;
+  r.key = in ? keys[q] : kPadKey | (uint32_t)(threadIdx.x & 31);  // distinct dead keys
   r.pp = 0.0;
   r.pm = 0.0;
   if (!in) return r;
@@ -486,7 +489,7 @@ template <int NF>
 __device__ __forceinline__ void raw_load(RawWin<NF> &r, const uint32_t *__restrict__ keys,
                                          const double *const *fp, const double *fq, int32_t q,
                                          bool in) {
-  r.key = in ? keys[q] : 0xFFFFFFFFu;
+  r.key = in ? keys[q] : kPadKey | (uint32_t)(threadIdx.x & 31);  // distinct dead keys
   const int32_t qq = in ? q : 0;
 #pragma unroll
   for (int j = 0; j < NF; ++j) r.f[j] = fp[j][qq];
@@ -524,10 +527,10 @@ __device__ __forceinline__ void window_reduce(const TileTarget &T, uint32_t key,
     sp += c.p;
     sm += c.m;
   }
-  if (!cont && c.key != 0xFFFFFFFFu && lane == 0) tile_put(T, c.key, c.p, c.m, c.first);
+  if (!cont && c.key < kPadKey && lane == 0) tile_put(T, c.key, c.p, c.m, c.first);
   const bool ffirst = share_first || (cont && c.first);  // window's first run = share's first
   const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1);
-  if (tail && lane != 31 && key != 0xFFFFFFFFu) tile_put(T, key, sp, sm, hl == 0 && ffirst);
+  if (tail && lane != 31 && key < kPadKey) tile_put(T, key, sp, sm, hl == 0 && ffirst);
   c.key = __shfl_sync(0xffffffffu, key, 31);
   c.p = __shfl_sync(0xffffffffu, sp, 31);
   c.m = __shfl_sync(0xffffffffu, sm, 31);
@@ -559,12 +562,12 @@ __device__ __forceinline__ void accumulate_factored(const TileTarget &T, const A
         double pp = 1.0;
 #pragma unroll
         for (int j = 0; j < NF; ++j) pp *= cur.f[j];
-        if (cur.key == 0xFFFFFFFFu) pp = 0.0;
+        if (cur.key >= kPadKey) pp = 0.0;
         window_reduce(T, cur.key, pp, pp * cur.qc, win + k == wb, c, lane);
       }
     }
   }
-  if (c.key != 0xFFFFFFFFu && lane == 0) tile_put(T, c.key, c.p, c.m, true);
+  if (c.key < kPadKey && lane == 0) tile_put(T, c.key, c.p, c.m, true);
 }
 
 // In-plane 2-D scan of the two row-block tiles fused with the factor weighting and the plane
@@ -798,7 +801,7 @@ __global__ void __launch_bounds__(kKdeThreads, 2) plane_kde_group_kernel(
                                       d, t.c, t.a, negmask);
           window_reduce(T, cur.key, cur.pp, cur.pm, win == wb, c, lane);
         }
-        if (c.key != 0xFFFFFFFFu && lane == 0) tile_put(T, c.key, c.p, c.m, true);
+        if (c.key < kPadKey && lane == 0) tile_put(T, c.key, c.p, c.m, true);
       }
       __syncthreads();
       double *g = plane_out + (int64_t)clo * W;
@@ -1049,7 +1052,7 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
           const int32_t q = qb + lane;
           const bool in = q < se;
           const int32_t qq = in ? q : sb;
-          r.key = in ? keys[q] : 0x80000000u | (uint32_t)lane;  // padding: distinct invalid keys
+          r.key = in ? keys[q] : kPadKey | (uint32_t)lane;  // padding: distinct dead keys
           r.A = fA[qq];
           r.qc = fc[qq];
           r.q0 = t.nlead > 0 ? fq0[qq] : 1.0;
@@ -1065,7 +1068,7 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
           const uint32_t key = cur.key;
           const double qcv = cur.qc, q0v = cur.q0, q1v = cur.q1;
           AllVals<NG> a;
-          const bool valid = key < 0x80000000u;  // keys have <= 31 bits (plan_kde_partition)
+          const bool valid = key < kPadKey;
           const double base = valid ? cur.A * cur.qr : 0.0;
 #pragma unroll
           for (int g = 0; g < NG; ++g) {
@@ -1099,9 +1102,9 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
           }
           // lane 31's run ends here unless the next window starts with the same key (the
           // prefetched next window tells), so only a continuing run is carried
-          const uint32_t nk0 = __shfl_sync(0xffffffffu, more ? nx.key : 0x80000000u, 0);
+          const uint32_t nk0 = __shfl_sync(0xffffffffu, more ? nx.key : kPadKey, 0);
           const uint32_t k31 = __shfl_sync(0xffffffffu, key, 31);
-          const bool cont_out = k31 < 0x80000000u && k31 == nk0;  // warp-uniform
+          const bool cont_out = k31 < kPadKey && k31 == nk0;  // warp-uniform
           const bool tail = lane == 31 ? !cont_out : ((heads >> (lane + 1)) & 1);
           if (tail && valid)
             all_put<NG, W, TSB>(sbase, nr, rowoff, t.col_bits, rmask, cmask, key, sv);
