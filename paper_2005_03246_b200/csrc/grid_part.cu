@@ -1883,7 +1883,8 @@ void carve_part(Workspace &W, PartBufs &b, int64_t n, int64_t NB) {
   b.rw.keys_alt = reinterpret_cast<uint64_t *>(W.take<uint32_t>(n));
   b.rw.vals_alt = W.take<int32_t>(n);
   // histograms of the radix passes (4096-item tiles) and of the record partition (2048)
-  const size_t hist = std::max(radix_ws_hist_elems(n), digit_hist_elems(n));
+  const size_t hist = std::max(std::max(radix_ws_hist_elems(n), digit_hist_elems(n)),
+                               (size_t)256 * seg_sort_tiles(n) + 1);
   b.rw.hist = W.take<int32_t>(hist);
   b.rw.partial = W.take<int32_t>(scan_ws_partial_elems((int64_t)hist + 2));
   b.start = W.take<int32_t>(NB + 1);
@@ -2084,6 +2085,10 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   double *rec_c = W.take<double>((size_t)n * (d + 1));
   uint32_t *keys_c = W.take<uint32_t>(n);
   int32_t *share_b = W.take<int32_t>((size_t)pl.NB * (kAllThreads / 32 + 1));
+  SegSortWs sw;
+  sw.seg_start = W.take<int32_t>(kSortSegs + 1);
+  sw.tile_base = W.take<int32_t>(kSortSegs + 1);
+  sw.tile_seg = W.take<int32_t>(seg_sort_tiles(n));
   LatShape s;
   s.d = d;
   int64_t total_knots = 0;
@@ -2178,21 +2183,30 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
     }
     FCG_TRY(rc);
   }
-  // equal keys are the same cell: their order is irrelevant
-  FCG_TRY(radix_sort_pairs<uint32_t>(keys_c, b.vals, n, 0, sort_bits, b.rw, st, false));
+  // Records are grouped by the key's top 8 bits (coarse segments); sort every segment by the
+  // bits below (equal keys are the same cell: their order is irrelevant).  For d = 3, 4 the last
+  // pass writes the records themselves, field-major, from their segment-local slots (no
+  // separate gather); otherwise the (key, slot) sort is followed by the gather kernel.
+  uint32_t *skeys = keys_c;
+  const bool fused_gather = cshift > 0 && (d + 1 == 4 || d + 1 == 5);
+  if (fused_gather) {
+    FCG_TRY(seg_sort_pairs_u32(keys_c, b.vals, n, cshift, b.rw, sw, st, rec_c, d + 1, rec, &skeys));
+  } else {
+    FCG_TRY(radix_sort_pairs<uint32_t>(keys_c, b.vals, n, 0, sort_bits, b.rw, st, false));
+  }
   {
     FCG_PROF("part_bucket_start", st);
-    bucket_start_kernel<<<grid_for(pl.NB + 1, 256, 4), 256, 0, st>>>(keys_c, n, pl.NB, p.cell_bits,
+    bucket_start_kernel<<<grid_for(pl.NB + 1, 256, 4), 256, 0, st>>>(skeys, n, pl.NB, p.cell_bits,
                                                                       b.start);
     FCG_LAUNCH_CHECK();
     if (all_run) {
       const int nw = kAllThreads / 32;
-      share_bounds_kernel<<<grid_for(pl.NB * (nw + 1), 256, 4), 256, 0, st>>>(keys_c, b.start, pl.NB,
+      share_bounds_kernel<<<grid_for(pl.NB * (nw + 1), 256, 4), 256, 0, st>>>(skeys, b.start, pl.NB,
                                                                               nw, share_b);
       FCG_LAUNCH_CHECK();
     }
   }
-  {
+  if (!fused_gather) {
     FCG_PROF("kde_materialize", st);
     // two CTAs per SM: the sorted positions in flight span ~half a coarse bucket, so its
     // records are re-read from L2 (a full grid spreads over several buckets and misses)
@@ -2257,7 +2271,7 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
     FCG_PROF("plane_kde", st);
     auto launch = [&](auto kern) -> int {
       FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asmem));
-      kern<<<(unsigned)np_full, kAllThreads, asmem, st>>>(ta, share_b, rec, n, keys_c);
+      kern<<<(unsigned)np_full, kAllThreads, asmem, st>>>(ta, share_b, rec, n, skeys);
       FCG_LAUNCH_CHECK();
       return FCG_OK;
     };
@@ -2331,7 +2345,7 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
         FCG_TRY(launch_kde_zf(knots, d, m, centre, h, gl, zf, st));
         if (!all_run) {
           FCG_PROF("plane_kde", st);
-          kde_kern<<<(unsigned)pl.NP, kKdeThreads, smem, st>>>(t, b.start, rec, n, keys_c,
+          kde_kern<<<(unsigned)pl.NP, kKdeThreads, smem, st>>>(t, b.start, rec, n, skeys,
                                                                factored, lat);
           FCG_LAUNCH_CHECK();
         }

@@ -146,26 +146,62 @@ __global__ void radix_init_kernel(const double *__restrict__ x, int64_t n, int64
   }
 }
 
-template <typename KeyT>
+// Tile maps: which items tile g covers and where its digit counts live in the histogram that
+// the exclusive scan turns into global offsets.
+//   FlatMap: tile g = items [g T, min(n, g T + T)), counts digit-major over all tiles.
+//   SegMap:  items are grouped in segments (seg_start[s] .. seg_start[s+1]); tiles never straddle
+//            a segment, counts are laid out [segment][digit][tile of the segment], so one scan
+//            yields offsets that keep every item inside its segment (a segmented LSD pass).
+struct FlatMap {
+  int64_t n, tiles;
+  __device__ __forceinline__ bool range(int64_t g, int64_t &start, int &len) const {
+    start = g * kSortTile;
+    const int64_t r = n - start;
+    len = (int)(r < kSortTile ? r : kSortTile);
+    return true;
+  }
+  __device__ __forceinline__ int64_t hidx(int64_t g, int d) const { return (int64_t)d * tiles + g; }
+};
+
+struct SegMap {
+  const int32_t *seg_start, *tile_base, *tile_seg;
+  __device__ __forceinline__ bool range(int64_t g, int64_t &start, int &len) const {
+    if (g >= tile_base[kSortSegs]) return false;  // past the last segment's tiles
+    const int s = tile_seg[g];
+    const int64_t t = g - tile_base[s];
+    start = seg_start[s] + t * kSortTile;
+    const int64_t r = seg_start[s + 1] - start;
+    len = (int)(r < kSortTile ? r : kSortTile);
+    return true;
+  }
+  __device__ __forceinline__ int64_t hidx(int64_t g, int d) const {
+    const int s = tile_seg[g];
+    const int64_t nt = tile_base[s + 1] - tile_base[s];
+    return (int64_t)256 * tile_base[s] + (int64_t)d * nt + (g - tile_base[s]);
+  }
+};
+
+template <typename KeyT, class Map>
 __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const KeyT *__restrict__ keys,
-                                                                  int64_t n, int shift,
-                                                                  int32_t *__restrict__ hist,
-                                                                  int64_t tiles) {
+                                                                  Map map, int shift,
+                                                                  int32_t *__restrict__ hist) {
   __shared__ int32_t s_hist[kSortThreads / 32][256];
+  int64_t base;
+  int len;
+  if (!map.range(blockIdx.x, base, len)) return;
   const int warp = threadIdx.x >> 5;
   for (int d = threadIdx.x & 31; d < 256; d += 32) s_hist[warp][d] = 0;
   __syncwarp();
-  const int64_t base = (int64_t)blockIdx.x * kSortTile;
 #pragma unroll 4
   for (int j = 0; j < kSortItems; ++j) {
-    const int64_t i = base + (int64_t)j * kSortThreads + threadIdx.x;
-    if (i < n) atomicAdd(&s_hist[warp][(unsigned)((keys[i] >> shift) & 0xFF)], 1);
+    const int ii = j * kSortThreads + threadIdx.x;
+    if (ii < len) atomicAdd(&s_hist[warp][(unsigned)((keys[base + ii] >> shift) & 0xFF)], 1);
   }
   __syncthreads();
   int32_t tot = 0;
 #pragma unroll
   for (int w = 0; w < kSortThreads / 32; ++w) tot += s_hist[w][threadIdx.x];
-  hist[(int64_t)threadIdx.x * tiles + blockIdx.x] = tot;
+  hist[map.hidx(blockIdx.x, threadIdx.x)] = tot;
 }
 
 // Stable scatter of one tile (4096 items) by one 8-bit digit.  Items are first ranked inside
@@ -174,11 +210,13 @@ __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const KeyT *__
 // each digit's run (coalesced) instead of 32 scattered 4-byte stores per warp.
 // STABLE = false (first LSD pass of a sort whose equal keys may come out in any order): items
 // are ranked by a shared-memory atomic on their warp's digit counter instead of peer masks.
-template <typename KeyT, bool STABLE>
+// GW > 0 (record gather, last pass of a segmented sort): instead of the value, item v's record
+// rec_in[v * GW + f] is written field-major to rec_out[f * rec_n + dst].
+template <typename KeyT, bool STABLE, class Map, int GW>
 __global__ void __launch_bounds__(kSortThreads, 3) radix_scatter_kernel(
     const KeyT *__restrict__ kin, const int32_t *__restrict__ vin, KeyT *__restrict__ kout,
-    int32_t *__restrict__ vout, int64_t n, int shift, const int32_t *__restrict__ offs,
-    int64_t tiles) {
+    int32_t *__restrict__ vout, Map map, int shift, const int32_t *__restrict__ offs,
+    const double *__restrict__ rec_in, double *__restrict__ rec_out, int64_t rec_n) {
   extern __shared__ __align__(16) unsigned char rs_smem[];
   KeyT *s_key = reinterpret_cast<KeyT *>(rs_smem);                       // [kSortTile]
   int32_t *s_val = reinterpret_cast<int32_t *>(s_key + kSortTile);        // [kSortTile]
@@ -187,12 +225,14 @@ __global__ void __launch_bounds__(kSortThreads, 3) radix_scatter_kernel(
   int32_t *s_tstart = s_goff + 256;                                       // [256]
   int32_t *s_wsum = s_tstart + 256;                                       // [8]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t tile0;
+  int tile_n;
+  if (!map.range(blockIdx.x, tile0, tile_n)) return;
   for (int d = lane; d < 256; d += 32) s_cnt[warp * 256 + d] = 0;
-  s_goff[threadIdx.x] = offs[(int64_t)threadIdx.x * tiles + blockIdx.x];
+  s_goff[threadIdx.x] = offs[map.hidx(blockIdx.x, threadIdx.x)];
   __syncwarp();
-  const int64_t tile0 = (int64_t)blockIdx.x * kSortTile;
   const int64_t base = tile0 + (int64_t)warp * (kSortTile / 8);
-  const int tile_n = (int)((n - tile0) < kSortTile ? (n - tile0) : kSortTile);
+  const int64_t n = tile0 + tile_n;  // end of this tile's items
   KeyT k[kSortItems];
   int32_t v[kSortItems];
   int32_t r[kSortItems];
@@ -267,7 +307,16 @@ __global__ void __launch_bounds__(kSortThreads, 3) radix_scatter_kernel(
     const unsigned dig = (unsigned)((key >> shift) & 0xFF);
     const int64_t dst = (int64_t)s_goff[dig] + (pos - s_tstart[dig]);
     kout[dst] = key;
-    vout[dst] = s_val[pos];
+    if constexpr (GW > 0) {
+      const double *r = rec_in + (int64_t)s_val[pos] * GW;
+      double f[GW];
+#pragma unroll
+      for (int w = 0; w < GW; ++w) f[w] = r[w];
+#pragma unroll
+      for (int w = 0; w < GW; ++w) __stcs(rec_out + (int64_t)w * rec_n + dst, f[w]);
+    } else {
+      vout[dst] = s_val[pos];
+    }
   }
 }
 
@@ -341,6 +390,44 @@ __global__ void key_andor_init(unsigned long long *out) {
   out[1] = 0ull;
 }
 
+// seg_start[c] = first item of segment c (key >> seg_shift == c) of keys grouped by segment;
+// empty segments start where the next one does; seg_start[kSortSegs] = n
+__global__ void seg_bounds_kernel(const uint32_t *__restrict__ keys, int64_t n, int seg_shift,
+                                  int32_t *__restrict__ seg_start) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(keys[i] >> seg_shift);
+    const int cp = i ? (int)(keys[i - 1] >> seg_shift) : -1;
+    for (int x = cp + 1; x <= c; ++x) seg_start[x] = (int32_t)i;
+    if (i == n - 1)
+      for (int x = c + 1; x <= kSortSegs; ++x) seg_start[x] = (int32_t)n;
+  }
+}
+
+// one CTA of kSortSegs threads: tiles per segment, their exclusive scan (tile_base, with the
+// total at [kSortSegs]) and the tile -> segment map
+__global__ void __launch_bounds__(kSortSegs) seg_tiles_kernel(const int32_t *__restrict__ seg_start,
+                                                              int32_t *__restrict__ tile_base,
+                                                              int32_t *__restrict__ tile_seg) {
+  __shared__ int32_t s_warp[kSortSegs / 32];
+  const int sg = threadIdx.x, lane = sg & 31, warp = sg >> 5;
+  const int32_t nt = (seg_start[sg + 1] - seg_start[sg] + kSortTile - 1) / kSortTile;
+  int32_t x = nt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  int32_t pre = 0;
+  for (int w = 0; w < warp; ++w) pre += s_warp[w];
+  const int32_t ex = pre + x - nt;
+  tile_base[sg] = ex;
+  if (sg == kSortSegs - 1) tile_base[kSortSegs] = ex + nt;
+  for (int32_t t = 0; t < nt; ++t) tile_seg[ex + t] = sg;
+}
+
 }  // namespace
 
 size_t radix_ws_hist_elems(int64_t n) { return (size_t)256 * (size_t)ceil_div(n, kSortTile) + 1; }
@@ -387,9 +474,10 @@ static int radix_sort_digits(KeyT *keys, int32_t *vals, int64_t n, uint32_t digi
   for (int dg = 0; dg < (int)sizeof(KeyT); ++dg) {
     if (!((digit_mask >> dg) & 1u)) continue;
     const int shift = 8 * dg;
+    const FlatMap map{n, tiles};
     if (!(first_hist_ready && passes == 0)) {
       FCG_PROF("radix_hist", st);
-      radix_hist_kernel<KeyT><<<(unsigned)tiles, kSortThreads, 0, st>>>(ka, n, shift, ws.hist, tiles);
+      radix_hist_kernel<KeyT, FlatMap><<<(unsigned)tiles, kSortThreads, 0, st>>>(ka, map, shift, ws.hist);
       FCG_LAUNCH_CHECK();
     }
     FCG_TRY(scan_i32(ws.hist, ws.hist, 256 * tiles, false, ws.partial, st));
@@ -397,9 +485,11 @@ static int radix_sort_digits(KeyT *keys, int32_t *vals, int64_t n, uint32_t digi
       FCG_PROF("radix_scatter", st);
       constexpr size_t sm = radix_scatter_smem<KeyT>();
       // only the first pass may reorder equal keys: later passes must keep the earlier order
-      auto kern = (stable || passes > 0) ? radix_scatter_kernel<KeyT, true> : radix_scatter_kernel<KeyT, false>;
+      auto kern = (stable || passes > 0) ? radix_scatter_kernel<KeyT, true, FlatMap, 0>
+                                         : radix_scatter_kernel<KeyT, false, FlatMap, 0>;
       FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      kern<<<(unsigned)tiles, kSortThreads, sm, st>>>(ka, va, kb, vb, n, shift, ws.hist, tiles);
+      kern<<<(unsigned)tiles, kSortThreads, sm, st>>>(ka, va, kb, vb, map, shift, ws.hist, nullptr,
+                                                      nullptr, 0);
       FCG_LAUNCH_CHECK();
     }
     std::swap(ka, kb);
@@ -440,6 +530,61 @@ int radix_sort_pairs_pruned(uint64_t *keys, int32_t *vals, int64_t n, const Radi
   for (int dg = 0; dg < 8; ++dg)
     if ((diff >> (8 * dg)) & 0xFFull) mask |= 1u << dg;
   return radix_sort_digits<uint64_t>(keys, vals, n, mask, ws, st);
+}
+
+size_t seg_sort_tiles(int64_t n) { return (size_t)ceil_div(n, kSortTile) + kSortSegs; }
+
+int seg_sort_pairs_u32(uint32_t *keys, int32_t *vals, int64_t n, int seg_shift, const RadixWs &ws,
+                       const SegSortWs &sw, cudaStream_t st, const double *rec_in, int words,
+                       double *rec_out, uint32_t **sorted_keys) {
+  *sorted_keys = keys;
+  if (n <= 0) return FCG_OK;
+  if (rec_in && words != 4 && words != 5)
+    return fail(FCG_EUNSUPPORTED, "seg_sort_pairs_u32: record gather supports 4 or 5 words");
+  const int64_t tmax = (int64_t)seg_sort_tiles(n);
+  {
+    FCG_PROF("radix_hist", st);
+    seg_bounds_kernel<<<grid_for(n, 256, 4), 256, 0, st>>>(keys, n, seg_shift, sw.seg_start);
+    FCG_LAUNCH_CHECK();
+    seg_tiles_kernel<<<1, kSortSegs, 0, st>>>(sw.seg_start, sw.tile_base, sw.tile_seg);
+    FCG_LAUNCH_CHECK();
+  }
+  const SegMap map{sw.seg_start, sw.tile_base, sw.tile_seg};
+  uint32_t *ka = keys, *kb = reinterpret_cast<uint32_t *>(ws.keys_alt);
+  int32_t *va = vals, *vb = ws.vals_alt;
+  constexpr size_t sm = radix_scatter_smem<uint32_t>();
+  for (int shift = 0, pass = 0; shift < seg_shift; shift += 8, ++pass) {
+    const bool last = shift + 8 >= seg_shift;
+    {
+      FCG_PROF("radix_hist", st);
+      radix_hist_kernel<uint32_t, SegMap><<<(unsigned)tmax, kSortThreads, 0, st>>>(ka, map, shift, ws.hist);
+      FCG_LAUNCH_CHECK();
+    }
+    FCG_TRY(scan_i32(ws.hist, ws.hist, 256 * tmax, false, ws.partial, st));
+    FCG_PROF(last && rec_in ? "kde_materialize" : "radix_scatter", st);
+    // equal keys are interchangeable for the callers: only the first pass ranks unstably
+    auto kern = pass > 0 ? radix_scatter_kernel<uint32_t, true, SegMap, 0>
+                         : radix_scatter_kernel<uint32_t, false, SegMap, 0>;
+    if (last && rec_in) {
+      kern = words == 4 ? (pass > 0 ? radix_scatter_kernel<uint32_t, true, SegMap, 4>
+                                    : radix_scatter_kernel<uint32_t, false, SegMap, 4>)
+                        : (pass > 0 ? radix_scatter_kernel<uint32_t, true, SegMap, 5>
+                                    : radix_scatter_kernel<uint32_t, false, SegMap, 5>);
+    }
+    FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    kern<<<(unsigned)tmax, kSortThreads, sm, st>>>(ka, va, kb, vb, map, shift, ws.hist, rec_in,
+                                                   rec_out, n);
+    FCG_LAUNCH_CHECK();
+    std::swap(ka, kb);
+    std::swap(va, vb);
+  }
+  *sorted_keys = ka;
+  if (rec_in == nullptr && ka != keys) {
+    FCG_CUDA_TRY(cudaMemcpyAsync(keys, ka, (size_t)n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+    FCG_CUDA_TRY(cudaMemcpyAsync(vals, va, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    *sorted_keys = keys;
+  }
+  return FCG_OK;
 }
 
 template int radix_sort_pairs<uint64_t>(uint64_t *, int32_t *, int64_t, int, int, const RadixWs &,
