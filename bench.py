@@ -163,8 +163,9 @@ def grid_kde_bytes(n, d, m, unit_w):
         "part_emit": 4 * n + 8 * n * d + wb + 8 * n * (d + 1) + 8 * n,
         "radix_hist": 4 * n,
         "radix_scatter": 16 * n,
-        # sorted field-major records from the grouped record-major ones
-        "kde_materialize": 4 * n + 16 * n * (d + 1),
+        # last segmented sort pass: (key, slot) in, key out, and each slot's record gathered
+        # from its coarse segment (L2-resident window) and written field-major
+        "kde_materialize": 12 * n + 16 * n * (d + 1),
         # all term groups in one launch (d = 3, 4): two passes over the records (keys, A, the
         # leading q's, q_col; q_row in the second), and per group lattice the first row-sign
         # pass writes it and the second reads and rewrites it
