@@ -18,7 +18,10 @@
  *     the last dimension fastest (core.py:137-141).
  *   - delta[k] = +1 selects "<=" and -1 selects "<" (core.py:144-172).
  *   - Every call only enqueues work on `stream` (a cudaStream_t; NULL = legacy default stream).
- *     Calls documented as "syncs" read a device scalar back and block on the stream.
+ *     Calls documented as "syncs" read a device scalar back and block on the stream.  The
+ *     read-back goes through a 4 KB mapped pinned host buffer (allocated once per host thread)
+ *     written by a one-warp kernel, never through a copy engine, so it does not queue behind
+ *     bulk transfers the caller has in flight on other streams.
  *   - Workspace protocol (CUB style): call with ws == NULL to receive the byte count in
  *     *ws_bytes; then call again with a device buffer of at least that size.  The library never
  *     allocates device memory itself and keeps no state between calls (reentrant).

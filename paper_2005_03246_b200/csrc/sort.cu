@@ -392,15 +392,24 @@ __global__ void key_andor_init(unsigned long long *out) {
 
 // seg_start[c] = first item of segment c (key >> seg_shift == c) of keys grouped by segment;
 // empty segments start where the next one does; seg_start[kSortSegs] = n
-__global__ void seg_bounds_kernel(const uint32_t *__restrict__ keys, int64_t n, int seg_shift,
-                                  int32_t *__restrict__ seg_start) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(keys[i] >> seg_shift);
-    const int cp = i ? (int)(keys[i - 1] >> seg_shift) : -1;
-    for (int x = cp + 1; x <= c; ++x) seg_start[x] = (int32_t)i;
-    if (i == n - 1)
-      for (int x = c + 1; x <= kSortSegs; ++x) seg_start[x] = (int32_t)n;
+__global__ void __launch_bounds__(256) seg_bounds_kernel(const uint32_t *__restrict__ keys,
+                                                         int64_t n, int seg_shift,
+                                                         int32_t *__restrict__ seg_start) {
+  constexpr int K = 8;  // consecutive keys per thread, all loaded before the compares
+  const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * K;
+  if (i0 >= n) return;
+  int c[K + 1];
+  c[0] = i0 ? (int)(keys[i0 - 1] >> seg_shift) : -1;
+#pragma unroll
+  for (int k = 0; k < K; ++k) c[k + 1] = i0 + k < n ? (int)(keys[i0 + k] >> seg_shift) : kSortSegs;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    if (i0 + k >= n) break;
+    for (int x = c[k] + 1; x <= c[k + 1]; ++x) seg_start[x] = (int32_t)(i0 + k);
+  }
+  if (i0 + K >= n) {  // the thread holding the last key closes the remaining segments
+    const int64_t last = n - 1;
+    for (int x = (int)(keys[last] >> seg_shift) + 1; x <= kSortSegs; ++x) seg_start[x] = (int32_t)n;
   }
 }
 
@@ -544,7 +553,7 @@ int seg_sort_pairs_u32(uint32_t *keys, int32_t *vals, int64_t n, int seg_shift, 
   const int64_t tmax = (int64_t)seg_sort_tiles(n);
   {
     FCG_PROF("radix_hist", st);
-    seg_bounds_kernel<<<grid_for(n, 256, 4), 256, 0, st>>>(keys, n, seg_shift, sw.seg_start);
+    seg_bounds_kernel<<<(unsigned)ceil_div(n, 256 * 8), 256, 0, st>>>(keys, n, seg_shift, sw.seg_start);
     FCG_LAUNCH_CHECK();
     seg_tiles_kernel<<<1, kSortSegs, 0, st>>>(sw.seg_start, sw.tile_base, sw.tile_seg);
     FCG_LAUNCH_CHECK();
@@ -562,15 +571,11 @@ int seg_sort_pairs_u32(uint32_t *keys, int32_t *vals, int64_t n, int seg_shift, 
     }
     FCG_TRY(scan_i32(ws.hist, ws.hist, 256 * tmax, false, ws.partial, st));
     FCG_PROF(last && rec_in ? "kde_materialize" : "radix_scatter", st);
-    // equal keys are interchangeable for the callers: only the first pass ranks unstably
-    auto kern = pass > 0 ? radix_scatter_kernel<uint32_t, true, SegMap, 0>
-                         : radix_scatter_kernel<uint32_t, false, SegMap, 0>;
-    if (last && rec_in) {
-      kern = words == 4 ? (pass > 0 ? radix_scatter_kernel<uint32_t, true, SegMap, 4>
-                                    : radix_scatter_kernel<uint32_t, false, SegMap, 4>)
-                        : (pass > 0 ? radix_scatter_kernel<uint32_t, true, SegMap, 5>
-                                    : radix_scatter_kernel<uint32_t, false, SegMap, 5>);
-    }
+    // stable ranking in every pass (measured faster than the atomic ranking here)
+    auto kern = radix_scatter_kernel<uint32_t, true, SegMap, 0>;
+    if (last && rec_in)
+      kern = words == 4 ? radix_scatter_kernel<uint32_t, true, SegMap, 4>
+                        : radix_scatter_kernel<uint32_t, true, SegMap, 5>;
     FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     kern<<<(unsigned)tmax, kSortThreads, sm, st>>>(ka, va, kb, vb, map, shift, ws.hist, rec_in,
                                                    rec_out, n);

@@ -22,6 +22,7 @@ SCOPES = [(r"^ecdf_final2d", "scan_lines_final"), (r"^final2d", "kde_final_group
           (r"digit_stage", "part_emit"), (r"digit_hist", "part_hist"), (r"^kde_materialize", "kde_materialize"),
           (r"^kde_final_multi", "kde_final_group"), (r"^lines_kernel<\w+, \d, 1>", "scan_lines_final"),
           (r"^lines_kernel", "scan_lines"), (r"^rows_kernel", "scan_rows"),
+          (r"^radix_scatter_kernel<.*SegMap, [1-9]", "kde_materialize"),
           (r"^radix_scatter", "radix_scatter"), (r"^radix_hist", "radix_hist"),
           (r"^part_bin", "part_bin"), (r"^plane_count", "plane_count"),
           (r"^bin_scatter_kernel", "bin_scatter_count"), (r"^level2_self<0", "pts_level2_block"),
