@@ -1304,7 +1304,8 @@ int kde_build_records(const uint32_t *keys, int64_t n, int shift, const double *
                       int32_t *slot, int32_t *hist, int32_t *partial, cudaStream_t st) {
   KdeBuild<D> kb{factored, pp};
   return digit_partition_build<KdeBuild<D>, D + 1>(keys, n, shift, x, w, kb, rec_c, keys_c, slot,
-                                                   hist, partial, st, nullptr, "part_emit", true);
+                                                   hist, partial, st, nullptr, "part_emit", true,
+                                                   true);
 }
 
 // sorted records, field-major (rec[f * n + q], so a warp's loads of one field are coalesced and

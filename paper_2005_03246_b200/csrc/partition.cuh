@@ -172,6 +172,124 @@ __global__ void __launch_bounds__(kPartThreads, 2) digit_stage_kernel(
   }
 }
 
+// Variant for costly builds (the KDE records: d + 1 exponentials per item).  The tile is ranked
+// from its keys alone and only (key, item index) is staged in shared memory; each item's record
+// is built at write-out time from x / w re-read in tile order (a 2048-item window, so the
+// re-read is sector-dense and the points are fetched from DRAM once).  6 bytes of shared
+// memory and a handful of registers per item instead of a staged record: 4 CTAs per SM.
+template <class Build, int WORDS>
+__global__ void __launch_bounds__(kPartThreads, 4) digit_stage_late_kernel(
+    const uint32_t *__restrict__ keys, int64_t n, int shift, const int32_t *__restrict__ offs,
+    int64_t tiles, const double *__restrict__ x, const double *__restrict__ w, Build build,
+    double *__restrict__ rec_out, uint32_t *__restrict__ keys_out, int32_t *__restrict__ slot_out) {
+  constexpr int D = Build::kD;
+  __shared__ uint32_t s_key[kPartTile];
+  __shared__ uint16_t s_src[kPartTile];
+  __shared__ int32_t s_cnt[(kPartThreads / 32) * 256];
+  __shared__ int32_t s_goff[256], s_tstart[256], s_wsum[kPartThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int d = lane; d < 256; d += 32) s_cnt[warp * 256 + d] = 0;
+  s_goff[threadIdx.x] = offs[(int64_t)threadIdx.x * tiles + blockIdx.x];
+  __syncwarp();
+  const int64_t tile0 = (int64_t)blockIdx.x * kPartTile;
+  const int wbase = warp * (kPartTile / 8);
+  const int tile_n = (int)((n - tile0) < kPartTile ? (n - tile0) : kPartTile);
+  uint32_t k[kPartItems];
+  int32_t r[kPartItems];
+#pragma unroll
+  for (int j = 0; j < kPartItems; ++j) {
+    const int li = wbase + j * 32 + lane;
+    k[j] = li < tile_n ? keys[tile0 + li] : 0u;
+  }
+  const unsigned lt = lane_lt();
+#pragma unroll
+  for (int j = 0; j < kPartItems; ++j) {
+    const bool ok = wbase + j * 32 + lane < tile_n;
+    const unsigned dig = ok ? ((k[j] >> shift) & 0xFFu) : 256u + lane;
+    const unsigned peers = digit_peers(dig);
+    int32_t before = 0;
+    if (ok) before = s_cnt[warp * 256 + dig];
+    __syncwarp();
+    if (ok && lane == __ffs(peers) - 1) s_cnt[warp * 256 + dig] = before + __popc(peers);
+    __syncwarp();
+    r[j] = before + __popc(peers & lt);
+  }
+  __syncthreads();
+  {
+    const int d = threadIdx.x;
+    int32_t run = 0;
+#pragma unroll
+    for (int wp = 0; wp < kPartThreads / 32; ++wp) {
+      const int32_t t = s_cnt[wp * 256 + d];
+      s_cnt[wp * 256 + d] = run;
+      run += t;
+    }
+    int32_t xx = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, xx, o);
+      if (lane >= o) xx += y;
+    }
+    if (lane == 31) s_wsum[warp] = xx;
+    __syncthreads();
+    int32_t wpre = 0;
+    for (int wp = 0; wp < warp; ++wp) wpre += s_wsum[wp];
+    s_tstart[d] = wpre + xx - run;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kPartItems; ++j) {
+    const int li = wbase + j * 32 + lane;
+    if (li < tile_n) {
+      const unsigned dig = (k[j] >> shift) & 0xFFu;
+      const int pos = s_tstart[dig] + s_cnt[warp * 256 + dig] + r[j];
+      s_key[pos] = k[j];
+      s_src[pos] = (uint16_t)li;
+    }
+  }
+  __syncthreads();
+  // write-out in grouped order: two items per thread step, their point loads issued together
+  for (int p0 = threadIdx.x; p0 < tile_n; p0 += 2 * kPartThreads) {
+    double xs[2][D], ws[2];
+    uint32_t kk[2];
+    int64_t dst[2];
+    bool ok[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int pos = p0 + u * kPartThreads;
+      ok[u] = pos < tile_n;
+      const int pp = ok[u] ? pos : p0;
+      kk[u] = s_key[pp];
+      const unsigned dig = (kk[u] >> shift) & 0xFFu;
+      dst[u] = (int64_t)s_goff[dig] + (pp - s_tstart[dig]);
+      const int64_t i = tile0 + s_src[pp];
+      if constexpr (D % 2 == 0) {
+#pragma unroll
+        for (int c = 0; c < D; c += 2) {
+          const double2 v = reinterpret_cast<const double2 *>(x + i * D)[c / 2];
+          xs[u][c] = v.x;
+          xs[u][c + 1] = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < D; ++c) xs[u][c] = x[i * D + c];
+      }
+      ws[u] = w ? w[i] : 1.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (!ok[u]) continue;
+      double rr[WORDS];
+      build(xs[u], ws[u], rr);
+      double *o = rec_out + dst[u] * WORDS;
+#pragma unroll
+      for (int f = 0; f < WORDS; ++f) o[f] = rr[f];
+      if (keys_out) keys_out[dst[u]] = kk[u];
+      if (slot_out) slot_out[dst[u]] = (int32_t)dst[u];
+    }
+  }
+}
+
 }  // namespace part_detail
 
 inline size_t digit_stage_smem(int words) {
@@ -188,7 +306,8 @@ int digit_partition_build(const uint32_t *keys, int64_t n, int shift, const doub
                           const double *w, const Build &build, double *rec_out,
                           uint32_t *keys_out, int32_t *slot_out, int32_t *hist, int32_t *partial,
                           cudaStream_t st, double *last_out = nullptr,
-                          const char *label = "part_emit", bool hist_ready = false) {
+                          const char *label = "part_emit", bool hist_ready = false,
+                          bool late_build = false) {
   if (n <= 0) return FCG_OK;
   const int64_t tiles = ceil_div(n, kPartTile);
   if (!hist_ready) {  // else: the key producer already wrote the per-tile digit histogram
@@ -199,6 +318,12 @@ int digit_partition_build(const uint32_t *keys, int64_t n, int shift, const doub
   }
   FCG_TRY(scan_i32(hist, hist, 256 * tiles, false, partial, st));
   FCG_PROF(label, st);
+  if (late_build && last_out == nullptr) {
+    part_detail::digit_stage_late_kernel<Build, WORDS><<<(unsigned)tiles, kPartThreads, 0, st>>>(
+        keys, n, shift, hist, tiles, x, w, build, rec_out, keys_out, slot_out);
+    FCG_LAUNCH_CHECK();
+    return FCG_OK;
+  }
   const size_t sm = digit_stage_smem(WORDS);
   auto kern = part_detail::digit_stage_kernel<Build, WORDS>;
   FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
