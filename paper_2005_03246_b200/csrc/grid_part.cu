@@ -885,14 +885,18 @@ __device__ __forceinline__ void all_put(uint32_t sbase, int nr, int rowoff, int 
   const int cr = (int)((key >> col_bits) & rmask) + rowoff;
   const int col = (int)(key & cmask);
   if (cr < 0 || cr >= nr) return;
-  const uint32_t ap = sbase + (uint32_t)(cr * (W + 2) + col) * 8u;
+  // columns XOR-swizzled by 16-byte chunk within aligned 16-column groups: a window's lanes span
+  // ~90 columns of a row, and columns 16 apart would otherwise share a bank pair
+  const uint32_t rowa = sbase + (uint32_t)(cr * (W + 2)) * 8u;
   if (col < W) {
+    const uint32_t ap = rowa + (uint32_t)swz_col(col) * 8u;
 #pragma unroll
     for (int g = 0; g < NG; ++g) sts_f64(ap + 2 * g * TSB, a.v[2 * g]);
   }
   if (col >= 1) {
+    const uint32_t am = rowa + (uint32_t)swz_col(col - 1) * 8u + TSB;
 #pragma unroll
-    for (int g = 0; g < NG; ++g) sts_f64(ap + (2 * g + 1) * TSB - 8u, a.v[2 * g + 1]);
+    for (int g = 0; g < NG; ++g) sts_f64(am + 2 * g * TSB, a.v[2 * g + 1]);
   }
 }
 
@@ -1134,7 +1138,7 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
             for (int b = 0; b < SPAN / 16; ++b) {
               double2 v[8];
 #pragma unroll
-              for (int k = 0; k < 8; ++k) v[k] = lds_f64x2(ra + (16 * b + 2 * k) * 8);
+              for (int k = 0; k < 8; ++k) v[k] = lds_f64x2(ra + swz_col(16 * b + 2 * k) * 8);
 #pragma unroll
               for (int k = 0; k < 8; ++k) {
                 v[k].x += run;
@@ -1142,14 +1146,14 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
                 run = v[k].y;
               }
 #pragma unroll
-              for (int k = 0; k < 8; ++k) sts_f64x2(ra + (16 * b + 2 * k) * 8, v[k]);
+              for (int k = 0; k < 8; ++k) sts_f64x2(ra + swz_col(16 * b + 2 * k) * 8, v[k]);
             }
           } else {
 #pragma unroll
             for (int b = 0; b < SPAN / 16; ++b) {
               double2 v[8];
 #pragma unroll
-              for (int k = 0; k < 8; ++k) v[k] = lds_f64x2(ra + (SPAN - 2 - 16 * b - 2 * k) * 8);
+              for (int k = 0; k < 8; ++k) v[k] = lds_f64x2(ra + swz_col(SPAN - 2 - 16 * b - 2 * k) * 8);
 #pragma unroll
               for (int k = 0; k < 8; ++k) {
                 v[k].y += run;
@@ -1157,7 +1161,7 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
                 run = v[k].x;
               }
 #pragma unroll
-              for (int k = 0; k < 8; ++k) sts_f64x2(ra + (SPAN - 2 - 16 * b - 2 * k) * 8, v[k]);
+              for (int k = 0; k < 8; ++k) sts_f64x2(ra + swz_col(SPAN - 2 - 16 * b - 2 * k) * 8, v[k]);
             }
           }
         }
@@ -1167,7 +1171,10 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
       // columns, so the 2-D prefix is a per-column running sum kept in registers across blocks
       if (warp < NG) {
         const int g = warp;
-        const uint32_t tp = sbase + (uint32_t)(2 * g) * TSB + lane * 16u, tm = tp + TSB;
+        const uint32_t tp = sbase + (uint32_t)(2 * g) * TSB, tm = tp + TSB;
+        int cj[C];  // this lane's (swizzled) column pairs
+#pragma unroll
+        for (int j = 0; j < C; ++j) cj[j] = swz_col(64 * j + 2 * lane);
         const bool wr = (vmask >> g) & 1;
         double *gp = wr ? (ph ? gbase1 : gbase0) + (int64_t)clo * W : nullptr;
         const bool rmw = ph > 0 && !t.row_split;
@@ -1193,7 +1200,7 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
               const int r = rneg ? nr - 1 - qr : qr;
   #pragma unroll
               for (int j = 0; j < C; ++j) {
-                const uint32_t o = (uint32_t)(r * RS + 64 * j) * 8u;
+                const uint32_t o = (uint32_t)(r * RS + cj[j]) * 8u;
                 const double2 a = lds_f64x2(tp + o), b = lds_f64x2(tm + o);
                 sts_f64x2(tp + o, zero2);
                 sts_f64x2(tm + o, zero2);
@@ -1219,8 +1226,8 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
             const int r = rneg ? nr - 1 - qr : qr;
   #pragma unroll
             for (int j = 0; j < C; ++j) {
-              na[j] = lds_f64x2(tp + (uint32_t)(r * RS + 64 * j) * 8u);
-              nb[j] = lds_f64x2(tm + (uint32_t)(r * RS + 64 * j) * 8u);
+              na[j] = lds_f64x2(tp + (uint32_t)(r * RS + cj[j]) * 8u);
+              nb[j] = lds_f64x2(tm + (uint32_t)(r * RS + cj[j]) * 8u);
               nold[j] = (wr && rmw) ? reinterpret_cast<const double2 *>(gp + (int64_t)r * W + 2 * lane)[32 * j]
                                     : zero2;
             }
@@ -1238,8 +1245,8 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
             if (qr + 1 < nr) fetch(qr + 1);
   #pragma unroll
             for (int j = 0; j < C; ++j) {
-              sts_f64x2(tp + (uint32_t)(r * RS + 64 * j) * 8u, zero2);
-              sts_f64x2(tm + (uint32_t)(r * RS + 64 * j) * 8u, zero2);
+              sts_f64x2(tp + (uint32_t)(r * RS + cj[j]) * 8u, zero2);
+              sts_f64x2(tm + (uint32_t)(r * RS + cj[j]) * 8u, zero2);
               up[2 * j] += ca[j].x; up[2 * j + 1] += ca[j].y;
               um[2 * j] += cb[j].x; um[2 * j + 1] += cb[j].y;
             }
