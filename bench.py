@@ -129,6 +129,7 @@ def grid_ecdf_bytes(n, d, m, unit=True):
         # atomic path (sparse lattices)
         "lattice_zero": e * L,
         "bin_scatter_count" if unit else "bin_scatter_w": 8 * n * d + (0 if unit else 8 * n) + 2 * e * n,
+        "scan_chunk_carry": e * L,  # chunk totals of a long axis (one read of the lattice)
         "scan_rows": 2 * e * L,
         "scan_lines": 2 * e * L,
         "scan_lines_final": e * L + 8 * L,
