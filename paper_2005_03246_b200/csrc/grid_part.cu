@@ -1623,15 +1623,17 @@ int launch_final2d(const Final2D &f, bool rev0, cudaStream_t st) {
 // Fused axis-1 + axis-0 final pass of the partitioned ECDF (d >= 4): int32 counts in, the
 // output epilogue (count / N as fp64, or int64 counts) out, 16 columns per CTA as in
 // final2d_kernel; the axis-1 lattice pass disappears.
+constexpr int kE2Stages = 4;
 template <bool REV0, bool REV1, int EK>
 __global__ void __launch_bounds__(256, 2) ecdf_final2d_kernel(const int32_t *__restrict__ lat,
                                                               int64_t D0, int64_t D1, int64_t B,
                                                               double div, void *out) {
   extern __shared__ __align__(16) int32_t e2_smem[];
   constexpr int CW = kF2Cols;
+  constexpr int ST = kE2Stages;           // slabs in flight (rows i0 + 1 .. i0 + ST - 1 arriving)
   const int slab = (int)D1 * CW;
-  int32_t *buf = e2_smem;                 // [2][D1][CW]
-  int32_t *segs = buf + 2 * slab;         // [kF2Segs][CW]
+  int32_t *buf = e2_smem;                 // [ST][D1][CW]
+  int32_t *segs = buf + ST * slab;        // [kF2Segs][CW]
   const int c = threadIdx.x % CW, sg = threadIdx.x / CW;
   const int64_t b0 = (int64_t)blockIdx.x * CW;
   const int64_t b = b0 + c;
@@ -1649,13 +1651,17 @@ __global__ void __launch_bounds__(256, 2) ecdf_final2d_kernel(const int32_t *__r
 #pragma unroll
   for (int s = 0; s < kF2Seg; ++s) carry[s] = 0;
   const int p0 = sg * kF2Seg;
-  stage(0, 0);
+#pragma unroll
+  for (int q = 0; q < ST - 1; ++q) {
+    if (q < D0) stage(q, q);
+    else cp_async_commit();
+  }
   for (int64_t jj = 0; jj < D0; ++jj) {
     const int64_t i0 = REV0 ? D0 - 1 - jj : jj;
-    const int cur = (int)(jj & 1);
-    if (jj + 1 < D0) stage(jj + 1, cur ^ 1);
-    else cp_async_commit();
-    cp_async_wait1();
+    const int cur = (int)(jj % ST);
+    if (jj + ST - 1 < D0) stage(jj + ST - 1, (int)((jj + ST - 1) % ST));
+    else cp_async_commit();  // keep the group count uniform
+    asm volatile("cp.async.wait_group %0;" ::"n"(kE2Stages - 1) : "memory");
     __syncthreads();
     const int32_t *sl = buf + cur * slab;
     int32_t v[kF2Seg];
@@ -1694,7 +1700,7 @@ int launch_ecdf_final2d(const int32_t *lat, const int64_t *dims, int d, bool rev
   int64_t B = 1;
   for (int k = 2; k < d; ++k) B *= dims[k];
   const unsigned grid = (unsigned)(B / kF2Cols);
-  const size_t smem = (size_t)(2 * dims[1] * kF2Cols + kF2Segs * kF2Cols) * sizeof(int32_t);
+  const size_t smem = (size_t)(kE2Stages * dims[1] * kF2Cols + kF2Segs * kF2Cols) * sizeof(int32_t);
   FCG_PROF("scan_lines_final", st);
   auto go = [&](auto kern) -> int {
     FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
