@@ -295,11 +295,13 @@ def test_kde_matern32_vs_oracle(d, oracle):
     assert_rel(got, oracle.kde_fastsum_matern32(x, w, knots, h), REL_KDE)
 
 
-@pytest.mark.parametrize("dims", [(320, 17, 40), (20, 16, 33, 21), (300, 40, 128), (24, 20, 16, 128),
-                                  (19, 21, 8, 64)])
+@pytest.mark.parametrize("dims", [(320, 17, 40), (20, 16, 33, 21), (300, 40, 128), (300, 40, 64),
+                                  (24, 20, 16, 128), (19, 21, 8, 64)])
 def test_partitioned_kde_vs_oracle(dims, oracle):
     """Partitioned KDE paths vs the oracle: per-group plane kernel (W = 40, 21), all-groups
-    plane kernel (W = 64, 128) with the fused axis-1 + axis-0 final (d = 4, 16 | columns)."""
+    plane kernel for every (E, NG) instance (W = 64, 128 at d = 3 and 4; blocks of <= 8 rows
+    take the unrolled walk, taller ones the look-ahead walk) with the fused axis-1 + axis-0
+    final (d = 4, 16 | columns)."""
     oracle.set_threads(0)
     d = len(dims)
     rng = np.random.default_rng(7 * sum(dims))
