@@ -42,7 +42,8 @@ struct PartGeo {
   int col_bits;
 };
 
-template <int D>
+// LEU: 0 / 1 = every axis counts knots < x / <= x (folded at compile time), 2 = per-axis g.le
+template <int D, int LEU = 2>
 __device__ __forceinline__ void part_key(const double *xi, int d, const double *kb, const BinGrid &g,
                                          const double *s_z0, const double *s_idz,
                                          const PartGeo &p, int64_t i, uint32_t &key,
@@ -53,7 +54,8 @@ __device__ __forceinline__ void part_key(const double *xi, int d, const double *
 #pragma unroll
   for (int k = 0; k < (D > 0 ? D : FCG_MAX_DIM); ++k) {
     if (k < d) {
-      const int c = knot_count(xi[k], kb + g.koff[k], (int)g.m[k], g.le[k], s_z0[k], s_idz[k]) -
+      const int c = knot_count(xi[k], kb + g.koff[k], (int)g.m[k], LEU == 2 ? g.le[k] : LEU,
+                               s_z0[k], s_idz[k]) -
                     (int)p.shift[k];
       live = live && c >= 0 && c < (int)p.E[k];
       if (k < d - 2) plane = plane * (uint32_t)p.E[k] + (uint32_t)c;
@@ -1757,7 +1759,7 @@ int bits_for(int64_t v) {  // smallest b with v < 2^b
 
 // keys + payloads of one radix tile per CTA, with the tile's histogram of the keys' low byte
 // (the first LSD pass's digit-major histogram, so that pass needs no histogram kernel)
-template <int D, bool MM>
+template <int D, bool MM, int LEU>
 __global__ void __launch_bounds__(256, D == 3 || D == 4 ? 4 : 1) part_bin_tile_kernel(const double *__restrict__ x, int64_t n,
                                                             int drt, const double *__restrict__ knots,
                                                             BinGrid g, PartGeo p,
@@ -1807,7 +1809,7 @@ __global__ void __launch_bounds__(256, D == 3 || D == 4 ? 4 : 1) part_bin_tile_k
       if (i >= n) continue;
       uint32_t key;
       int32_t val;
-      part_key<D>(xi[u], d, kb, g, s_z0, s_idz, p, i, key, val);
+      part_key<D, LEU>(xi[u], d, kb, g, s_z0, s_idz, p, i, key, val);
       keys[i] = key;
       if (vals) vals[i] = val;
       atomicAdd(&s_hist[warp][(key >> hshift) & 0xFFu], 1);
@@ -1873,12 +1875,25 @@ int launch_part_bin_tiles(const double *x, int64_t n, int d, const double *knots
   auto launch = [&](auto kern) {
     kern<<<gr, 256, smem, st>>>(x, n, d, knots, g, p, keys, vals, hist, tiles, tile, hshift, mm);
   };
-  if (d == 4 && al)
-    mm ? launch(part_bin_tile_kernel<4, true>) : launch(part_bin_tile_kernel<4, false>);
-  else if (d == 3)
-    mm ? launch(part_bin_tile_kernel<3, true>) : launch(part_bin_tile_kernel<3, false>);
-  else
-    mm ? launch(part_bin_tile_kernel<0, true>) : launch(part_bin_tile_kernel<0, false>);
+  bool le0 = true, le1 = true;
+  for (int k = 0; k < d; ++k) {
+    le0 = le0 && g.le[k] == 0;
+    le1 = le1 && g.le[k] == 1;
+  }
+  auto by_le = [&](auto k0, auto k1, auto k2) {
+    if (le0) launch(k0);
+    else if (le1) launch(k1);
+    else launch(k2);
+  };
+  if (d == 4 && al) {
+    if (mm) by_le(part_bin_tile_kernel<4, true, 0>, part_bin_tile_kernel<4, true, 1>, part_bin_tile_kernel<4, true, 2>);
+    else by_le(part_bin_tile_kernel<4, false, 0>, part_bin_tile_kernel<4, false, 1>, part_bin_tile_kernel<4, false, 2>);
+  } else if (d == 3) {
+    if (mm) by_le(part_bin_tile_kernel<3, true, 0>, part_bin_tile_kernel<3, true, 1>, part_bin_tile_kernel<3, true, 2>);
+    else by_le(part_bin_tile_kernel<3, false, 0>, part_bin_tile_kernel<3, false, 1>, part_bin_tile_kernel<3, false, 2>);
+  } else {
+    mm ? launch(part_bin_tile_kernel<0, true, 2>) : launch(part_bin_tile_kernel<0, false, 2>);
+  }
   FCG_LAUNCH_CHECK();
   return FCG_OK;
 }
