@@ -87,7 +87,8 @@ int route_partition(const uint32_t *keys, int64_t n, const double *x, const doub
                     double *x_out, double *w_out, int32_t *hist, int32_t *partial, cudaStream_t st) {
   RouteBuild<D> rb;
   return digit_partition_build<RouteBuild<D>, D + 1>(keys, n, 0, x, w, rb, x_out, nullptr, nullptr,
-                                                     hist, partial, st, w_out, "dist_partition");
+                                                     hist, partial, st, w_out, "dist_partition",
+                                                     false, true);
 }
 
 // out[a][j][b] = (local[a][j][b] + carry[a][b]) / div   (div <= 0: no division)

@@ -181,7 +181,8 @@ template <class Build, int WORDS>
 __global__ void __launch_bounds__(kPartThreads, 4) digit_stage_late_kernel(
     const uint32_t *__restrict__ keys, int64_t n, int shift, const int32_t *__restrict__ offs,
     int64_t tiles, const double *__restrict__ x, const double *__restrict__ w, Build build,
-    double *__restrict__ rec_out, uint32_t *__restrict__ keys_out, int32_t *__restrict__ slot_out) {
+    double *__restrict__ rec_out, uint32_t *__restrict__ keys_out, int32_t *__restrict__ slot_out,
+    double *__restrict__ last_out) {
   constexpr int D = Build::kD;
   __shared__ uint32_t s_key[kPartTile];
   __shared__ uint16_t s_src[kPartTile];
@@ -281,9 +282,16 @@ __global__ void __launch_bounds__(kPartThreads, 4) digit_stage_late_kernel(
       if (!ok[u]) continue;
       double rr[WORDS];
       build(xs[u], ws[u], rr);
-      double *o = rec_out + dst[u] * WORDS;
+      if (last_out == nullptr) {
+        double *o = rec_out + dst[u] * WORDS;
 #pragma unroll
-      for (int f = 0; f < WORDS; ++f) o[f] = rr[f];
+        for (int f = 0; f < WORDS; ++f) o[f] = rr[f];
+      } else {  // split records: the first WORDS-1 words to rec_out, the last to last_out
+        double *o = rec_out + dst[u] * (WORDS - 1);
+#pragma unroll
+        for (int f = 0; f < WORDS - 1; ++f) o[f] = rr[f];
+        last_out[dst[u]] = rr[WORDS - 1];
+      }
       if (keys_out) keys_out[dst[u]] = kk[u];
       if (slot_out) slot_out[dst[u]] = (int32_t)dst[u];
     }
@@ -318,9 +326,9 @@ int digit_partition_build(const uint32_t *keys, int64_t n, int shift, const doub
   }
   FCG_TRY(scan_i32(hist, hist, 256 * tiles, false, partial, st));
   FCG_PROF(label, st);
-  if (late_build && last_out == nullptr) {
+  if (late_build) {
     part_detail::digit_stage_late_kernel<Build, WORDS><<<(unsigned)tiles, kPartThreads, 0, st>>>(
-        keys, n, shift, hist, tiles, x, w, build, rec_out, keys_out, slot_out);
+        keys, n, shift, hist, tiles, x, w, build, rec_out, keys_out, slot_out, last_out);
     FCG_LAUNCH_CHECK();
     return FCG_OK;
   }
