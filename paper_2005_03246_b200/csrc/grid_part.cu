@@ -2184,6 +2184,8 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
     pp.a[k] = 1.0 / h[k];
   }
   const int factored = bound_u_sum <= 600.0 ? 1 : 0;
+  // d = 3, 4: the segmented sort's last pass writes the records (no slots, no gather kernel)
+  const bool fused_gather = cshift > 0 && (d + 1 == 4 || d + 1 == 5);
   // the all-groups kernel takes factored records only (an auto-centre plan assumed them)
   const bool all_run = pl.all && factored;
   {
@@ -2191,23 +2193,23 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
     const bool al = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
     int rc;
     switch (d) {  // the partitioned path runs for d >= 3
-      case 3: rc = kde_build_records<3>(b.keys, n, shift, x, w, factored, pp, rec_c, keys_c, b.vals,
+      case 3: rc = kde_build_records<3>(b.keys, n, shift, x, w, factored, pp, rec_c, keys_c, fused_gather ? nullptr : b.vals,
                                         b.rw.hist, b.rw.partial, st); break;
       case 4:
         if (!al) return fail(FCG_EINVAL, "points must be 16-byte aligned");
-        rc = kde_build_records<4>(b.keys, n, shift, x, w, factored, pp, rec_c, keys_c, b.vals,
+        rc = kde_build_records<4>(b.keys, n, shift, x, w, factored, pp, rec_c, keys_c, fused_gather ? nullptr : b.vals,
                                   b.rw.hist, b.rw.partial, st); break;
-      case 5: rc = kde_build_records<5>(b.keys, n, shift, x, w, factored, pp, rec_c, keys_c, b.vals,
+      case 5: rc = kde_build_records<5>(b.keys, n, shift, x, w, factored, pp, rec_c, keys_c, fused_gather ? nullptr : b.vals,
                                         b.rw.hist, b.rw.partial, st); break;
       case 6:
         if (!al) return fail(FCG_EINVAL, "points must be 16-byte aligned");
-        rc = kde_build_records<6>(b.keys, n, shift, x, w, factored, pp, rec_c, keys_c, b.vals,
+        rc = kde_build_records<6>(b.keys, n, shift, x, w, factored, pp, rec_c, keys_c, fused_gather ? nullptr : b.vals,
                                   b.rw.hist, b.rw.partial, st); break;
-      case 7: rc = kde_build_records<7>(b.keys, n, shift, x, w, factored, pp, rec_c, keys_c, b.vals,
+      case 7: rc = kde_build_records<7>(b.keys, n, shift, x, w, factored, pp, rec_c, keys_c, fused_gather ? nullptr : b.vals,
                                         b.rw.hist, b.rw.partial, st); break;
       default:
         if (!al) return fail(FCG_EINVAL, "points must be 16-byte aligned");
-        rc = kde_build_records<8>(b.keys, n, shift, x, w, factored, pp, rec_c, keys_c, b.vals,
+        rc = kde_build_records<8>(b.keys, n, shift, x, w, factored, pp, rec_c, keys_c, fused_gather ? nullptr : b.vals,
                                   b.rw.hist, b.rw.partial, st); break;
     }
     FCG_TRY(rc);
@@ -2217,9 +2219,9 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   // pass writes the records themselves, field-major, from their segment-local slots (no
   // separate gather); otherwise the (key, slot) sort is followed by the gather kernel.
   uint32_t *skeys = keys_c;
-  const bool fused_gather = cshift > 0 && (d + 1 == 4 || d + 1 == 5);
   if (fused_gather) {
-    FCG_TRY(seg_sort_pairs_u32(keys_c, b.vals, n, cshift, b.rw, sw, st, rec_c, d + 1, rec, &skeys));
+    FCG_TRY(seg_sort_pairs_u32(keys_c, b.vals, n, cshift, b.rw, sw, st, rec_c, d + 1, rec, &skeys,
+                               true));
   } else {
     FCG_TRY(radix_sort_pairs<uint32_t>(keys_c, b.vals, n, 0, sort_bits, b.rw, st, false));
   }

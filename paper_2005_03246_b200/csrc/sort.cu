@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) radix_scatter_kernel(
     const int64_t i = base + (int64_t)j * 32 + lane;
     const bool ok = i < n;
     k[j] = ok ? kin[i] : KeyT(0);
-    v[j] = ok ? vin[i] : 0;
+    v[j] = ok ? (vin ? vin[i] : (int32_t)i) : 0;  // vin == NULL: the values are the positions
   }
   if constexpr (STABLE) {
 #pragma unroll
@@ -545,7 +545,7 @@ size_t seg_sort_tiles(int64_t n) { return (size_t)ceil_div(n, kSortTile) + kSort
 
 int seg_sort_pairs_u32(uint32_t *keys, int32_t *vals, int64_t n, int seg_shift, const RadixWs &ws,
                        const SegSortWs &sw, cudaStream_t st, const double *rec_in, int words,
-                       double *rec_out, uint32_t **sorted_keys) {
+                       double *rec_out, uint32_t **sorted_keys, bool iota_vals) {
   *sorted_keys = keys;
   if (n <= 0) return FCG_OK;
   if (rec_in && words != 4 && words != 5)
@@ -560,7 +560,7 @@ int seg_sort_pairs_u32(uint32_t *keys, int32_t *vals, int64_t n, int seg_shift, 
   }
   const SegMap map{sw.seg_start, sw.tile_base, sw.tile_seg};
   uint32_t *ka = keys, *kb = reinterpret_cast<uint32_t *>(ws.keys_alt);
-  int32_t *va = vals, *vb = ws.vals_alt;
+  int32_t *va = vals, *vb = ws.vals_alt;  // iota_vals: the first pass synthesises positions
   constexpr size_t sm = radix_scatter_smem<uint32_t>();
   for (int shift = 0, pass = 0; shift < seg_shift; shift += 8, ++pass) {
     const bool last = shift + 8 >= seg_shift;
@@ -577,8 +577,8 @@ int seg_sort_pairs_u32(uint32_t *keys, int32_t *vals, int64_t n, int seg_shift, 
       kern = words == 4 ? radix_scatter_kernel<uint32_t, true, SegMap, 4>
                         : radix_scatter_kernel<uint32_t, true, SegMap, 5>;
     FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    kern<<<(unsigned)tmax, kSortThreads, sm, st>>>(ka, va, kb, vb, map, shift, ws.hist, rec_in,
-                                                   rec_out, n);
+    kern<<<(unsigned)tmax, kSortThreads, sm, st>>>(ka, (pass == 0 && iota_vals) ? nullptr : va, kb,
+                                                   vb, map, shift, ws.hist, rec_in, rec_out, n);
     FCG_LAUNCH_CHECK();
     std::swap(ka, kb);
     std::swap(va, vb);

@@ -36,7 +36,9 @@ int radix_sort_pairs(KeyT *keys, int32_t *vals, int64_t n, int begin_bit, int en
 // narrow, L2-resident window).  Equal keys may come out in any order.  With rec_in (4 or 5
 // words per item, indexed by the item's value) the last pass writes the records field-major to
 // rec_out[f * n + position] instead of the values.  The sorted keys end in *sorted_keys (keys
-// or ws.keys_alt).  Workspace: ws.hist >= 256 * seg_sort_tiles(n) + 1 ints, sw as below.
+// or ws.keys_alt).  iota_vals: the values are the items' positions (not read; vals is then
+// only a ping-pong buffer).
+// Workspace: ws.hist >= 256 * seg_sort_tiles(n) + 1 ints, sw as below.
 constexpr int kSortSegs = 256;
 struct SegSortWs {
   int32_t *seg_start;  // kSortSegs + 1
@@ -46,7 +48,7 @@ struct SegSortWs {
 size_t seg_sort_tiles(int64_t n);
 int seg_sort_pairs_u32(uint32_t *keys, int32_t *vals, int64_t n, int seg_shift, const RadixWs &ws,
                        const SegSortWs &sw, cudaStream_t st, const double *rec_in, int words,
-                       double *rec_out, uint32_t **sorted_keys);
+                       double *rec_out, uint32_t **sorted_keys, bool iota_vals = false);
 
 // Stable sort of 64-bit keys over the digits where they differ (one AND/OR reduction and a
 // 16-byte device-to-host read decide which 8-bit passes are identities).  Synchronises `st`.
