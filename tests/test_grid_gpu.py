@@ -268,6 +268,22 @@ def test_partitioned_ecdf_esf_vs_oracle(dims, delta, oracle):
     np.testing.assert_array_equal(got, oracle.esf_fastsum(x, None, knots))
 
 
+@pytest.mark.parametrize("dims", [(300, 53, 61), (30, 13, 16, 64)])
+def test_partitioned_ecdf_clustered(dims, oracle):
+    """90% of the points in one cell (one bucket holding most keys), the rest spread out."""
+    oracle.set_threads(0)
+    d = len(dims)
+    rng = np.random.default_rng(3 * sum(dims))
+    n = 1_200_000
+    x = rng.standard_normal((n, d))
+    k = int(0.9 * n)
+    x[:k] = 0.31 + 1e-5 * rng.random((k, d))
+    knots = [np.linspace(-2.2, 2.2, m) for m in dims]
+    got = fcb.ecdf_fastsum_counts(fcb.validate_sample(x), _grid(knots), fcb.DeltaVector((1,) * d))
+    ref = oracle.ecdf_fastsum(x, None, knots, (1,) * d, scaled=False)
+    np.testing.assert_array_equal(got, ref.astype(np.int64))
+
+
 def test_kde_matern32_golden(small_golden):
     """matern32-additive grid KDE (fastsum.py:170-181) against the reference's own output."""
     g = small_golden
@@ -315,6 +331,25 @@ def test_partitioned_kde_vs_oracle(dims, oracle):
                           fcb.Bandwidth.diag(h)).values
     ref = oracle.kde_fastsum_laplacian(x, w, knots, h)
     assert_rel(got, ref, REL_KDE)
+
+
+@pytest.mark.parametrize("dims", [(24, 20, 16, 128), (300, 40, 128)])
+def test_partitioned_kde_clustered(dims, oracle):
+    """Most points in one cell (runs of equal keys far longer than a window, one coarse segment
+    holding most of the records, most segments empty) plus a uniform background."""
+    oracle.set_threads(0)
+    d = len(dims)
+    rng = np.random.default_rng(13 * sum(dims))
+    n = 1_100_000
+    x = rng.uniform(-1, 1, (n, d))
+    k = int(0.9 * n)
+    x[:k] = 0.0123 + 1e-4 * rng.random((k, d))
+    w = rng.exponential(1.0, n)
+    knots = [np.linspace(-1.1, 0.9, m) for m in dims]
+    h = rng.uniform(0.1, 0.3, d)
+    got = fcb.kde_fastsum(fcb.validate_sample(x, w), _grid(knots), fcb.laplacian(),
+                          fcb.Bandwidth.diag(h)).values
+    assert_rel(got, oracle.kde_fastsum_laplacian(x, w, knots, h), REL_KDE)
 
 
 def _kde_ex(x, w, knots, h, centre, u_bound):
