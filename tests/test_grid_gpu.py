@@ -445,3 +445,36 @@ def test_cfg5_full(oracle, cfg_meta):
     if gold_b is not None and meta_b.get("input_sha") == wl.digest(w.points):
         assert_rel(vals[gold_b["idx"]], gold_b["vals"], REL_KDE)
     assert np.all(vals > 0)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_grid_configs_vs_oracle(seed, oracle):
+    """Seeded sweep over dimension, grid shape (uniform and irregular knots, knot hits), delta,
+    weights and sample size: grid ECDF counts bit-exact, weighted ECDF / ESF to 1e-12, the
+    Laplacian KDE to 1e-9."""
+    oracle.set_threads(0)
+    rng = np.random.default_rng(1000 + seed)
+    d = int(rng.integers(1, 5))
+    n = int(rng.choice([1, 2, 7, 500, 20_000]))
+    x = rng.standard_normal((n, d)) * rng.uniform(0.5, 2.0)
+    knots = []
+    for _ in range(d):
+        m = int(rng.integers(1, 40))
+        z = np.linspace(-2.5, 2.5, m) if rng.random() < 0.5 else np.sort(rng.uniform(-3, 3, m))
+        z = np.unique(np.concatenate([z, x[: int(rng.integers(0, 3)), len(knots)]]))
+        knots.append(z)
+    delta = tuple(int(v) for v in rng.choice([-1, 1], d))
+    grid = _grid(knots)
+    got = fcb.ecdf_fastsum_counts(fcb.validate_sample(x), grid, fcb.DeltaVector(delta))
+    np.testing.assert_array_equal(got, oracle.ecdf_fastsum(x, None, knots, delta, scaled=False)
+                                  .astype(np.int64))
+    w = rng.uniform(0.1, 2.0, n)
+    s = fcb.validate_sample(x, w)
+    assert_rel(fcb.ecdf_fastsum(s, grid, fcb.DeltaVector(delta)).values,
+               oracle.ecdf_fastsum(x, w, knots, delta), 1e-12)
+    assert_rel(fcb.esf_fastsum(s, grid).values, oracle.esf_fastsum(x, w, knots), 1e-12)
+    lo = np.minimum(x.min(0), [z[0] for z in knots])
+    hi = np.maximum(x.max(0), [z[-1] for z in knots])
+    h = np.maximum((hi - lo) / rng.uniform(5, 40, d), 1e-3)
+    assert_rel(fcb.kde_fastsum(s, grid, fcb.laplacian(), fcb.Bandwidth.diag(h)).values,
+               oracle.kde_fastsum_laplacian(x, w, knots, h), REL_KDE)
