@@ -132,6 +132,7 @@ def grid_ecdf_bytes(n, d, m, unit=True):
         "scan_chunk_carry": e * L,  # chunk totals of a long axis (one read of the lattice)
         "scan_rows": 2 * e * L,
         "scan_lines": 2 * e * L,
+        "scan_plane2d": 2 * e * L,  # both in-plane axes in one read + write
         "scan_lines_final": e * L + 8 * L,
         # plane-partitioned path: bucket keys + payloads (u32 each), one 8-bit radix pass each
         "part_bin": 8 * n * d + 8 * n,

@@ -338,13 +338,145 @@ int scan_axis(T *lat, const LatShape &s, int ax, bool rev, const Epi &epi, T *sc
   return fail(FCG_EINVAL, "unknown epilogue kind");
 }
 
+// ---- fused in-plane pass: axes d-1 (columns) and d-2 (rows) of every plane in one sweep ----
+// One CTA per plane of H x W (W = 256 E).  Thread t owns E contiguous columns (the column block
+// order is reversed for a suffix along the columns); RB rows at a time are loaded, scanned along
+// the columns (thread-local E, then a warp shuffle scan and the warp totals through shared
+// memory), added to the per-column running sums along the rows (registers), and stored; the
+// next RB rows are in flight meanwhile.  Saves one read + write of the lattice against the two
+// separate axis passes.
+constexpr int kP2Threads = 256;
+
+template <typename T, int E, int RB, int ST, bool REVR, bool REVC>
+__global__ void __launch_bounds__(kP2Threads, 4) plane2d_kernel(T *__restrict__ lat, int64_t H) {
+  constexpr int W = kP2Threads * E;
+  constexpr int CH = W * (int)sizeof(T) / 16;  // 16-byte chunks per row
+  extern __shared__ __align__(16) unsigned char p2_smem[];
+  T *s_buf = reinterpret_cast<T *>(p2_smem);  // [ST][RB][W] staged rows (cp.async ring)
+  __shared__ T s_w[RB][kP2Threads / 32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int cb = REVC ? kP2Threads - 1 - t : t;  // this thread's column block
+  T *pbase = lat + (int64_t)blockIdx.x * H * W;
+  const int64_t nb = (H + RB - 1) / RB;
+  auto stage = [&](int64_t k) {
+    if (k < nb) {
+      T *dst = s_buf + (int)(k % ST) * RB * W;
+      for (int c = t; c < RB * CH; c += kP2Threads) {
+        const int q = c / CH, o = c - q * CH;
+        const int64_t rr = k * RB + q;
+        if (rr < H) {
+          const int64_t r = REVR ? H - 1 - rr : rr;
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + q * W + o * (16 / (int)sizeof(T)));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
+                       "l"(pbase + r * W + o * (16 / (int)sizeof(T)))
+                       : "memory");
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  T carry[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) carry[e] = T(0);
+#pragma unroll
+  for (int k = 0; k < ST - 1; ++k) stage(k);
+  for (int64_t k = 0; k < nb; ++k) {
+    stage(k + ST - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(ST - 1) : "memory");
+    __syncthreads();
+    const T *bf = s_buf + (int)(k % ST) * RB * W + cb * E;
+    const int64_t r0 = k * RB;
+    T v[RB][E], tot[RB];
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+      T run = T(0);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int ee = REVC ? E - 1 - e : e;
+        run += bf[q * W + ee];
+        v[q][ee] = run;
+      }
+      // inclusive scan of the thread totals over the warp
+      T x = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const T y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      tot[q] = x - run;  // exclusive within the warp
+      if (lane == 31) s_w[q][warp] = x;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+      T off = tot[q];
+      for (int w = 0; w < warp; ++w) off += s_w[q][w];
+      const int64_t rr = r0 + q;
+      if (rr < H) {
+        const int64_t r = REVR ? H - 1 - rr : rr;
+        T *row = pbase + r * W + cb * E;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          carry[e] += v[q][e] + off;
+          row[e] = carry[e];
+        }
+      }
+    }
+    __syncthreads();  // s_w and the staged slot are rewritten next
+  }
+}
+
+template <typename T>
+static int plane2d_scan(T *lat, const LatShape &s, bool rev_row, bool rev_col, cudaStream_t st) {
+  const int d = s.d;
+  const int64_t W = s.dims[d - 1], H = s.dims[d - 2];
+  int64_t A = 1;
+  for (int k = 0; k < d - 2; ++k) A *= s.dims[k];
+  const int E = (int)(W / kP2Threads);
+  if (W % kP2Threads || (E != 1 && E != 2 && E != 4) || A < 2 * (int64_t)sm_count() || A > 65535 * 32)
+    return -1;  // not applicable: the caller runs the two axis passes
+  FCG_PROF("scan_plane2d", st);
+  constexpr int RB = 4, ST = 4;  // 4 rows per step, 3 steps in flight
+  const size_t smem = (size_t)ST * RB * W * sizeof(T);
+  int rc = FCG_OK;
+  auto go = [&](auto kern) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      rc = fail(FCG_ECUDA, "plane2d: shared memory attribute");
+    else
+      kern<<<(unsigned)A, kP2Threads, smem, st>>>(lat, H);
+  };
+#define FCG_P2(EE)                                                                         \
+  do {                                                                                     \
+    if (rev_row) {                                                                         \
+      if (rev_col) go(plane2d_kernel<T, EE, RB, ST, true, true>);                              \
+      else go(plane2d_kernel<T, EE, RB, ST, true, false>);                                     \
+    } else {                                                                               \
+      if (rev_col) go(plane2d_kernel<T, EE, RB, ST, false, true>);                             \
+      else go(plane2d_kernel<T, EE, RB, ST, false, false>);                                    \
+    }                                                                                      \
+  } while (0)
+  if (E == 1) FCG_P2(1);
+  else if (E == 2) FCG_P2(2);
+  else FCG_P2(4);
+#undef FCG_P2
+  FCG_TRY(rc);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}
+
 template <typename T>
 int scan_lattice(T *lat, const LatShape &s, const bool *rev, const Epi &epi, T *scratch,
                  cudaStream_t st) {
   // last (contiguous) axis first, axis 0 last so that its coalesced line walk carries the
-  // epilogue.
+  // epilogue.  With d >= 3 the two in-plane axes go in one fused pass when the shape allows.
   Epi inplace;
-  for (int ax = s.d - 1; ax >= 0; --ax) {
+  int ax = s.d - 1;
+  if (s.d >= 3) {
+    const int rc = plane2d_scan<T>(lat, s, rev[s.d - 2], rev[s.d - 1], st);
+    if (rc == FCG_OK) ax = s.d - 3;
+    else if (rc != -1) return rc;
+  }
+  for (; ax >= 0; --ax) {
     FCG_TRY(scan_axis<T>(lat, s, ax, rev[ax], ax == 0 ? epi : inplace, scratch, st));
   }
   return FCG_OK;

@@ -478,3 +478,27 @@ def test_random_grid_configs_vs_oracle(seed, oracle):
     h = np.maximum((hi - lo) / rng.uniform(5, 40, d), 1e-3)
     assert_rel(fcb.kde_fastsum(s, grid, fcb.laplacian(), fcb.Bandwidth.diag(h)).values,
                oracle.kde_fastsum_laplacian(x, w, knots, h), REL_KDE)
+
+
+@pytest.mark.parametrize("dims", [(300, 5, 256), (320, 3, 512), (4, 80, 7, 256)])
+def test_fused_plane_scan_vs_oracle(dims, oracle):
+    """Lattices whose last axis is a multiple of 256 with >= 2 x 148 planes take the fused
+    in-plane (axes d-1, d-2) scan: int32 counts (both delta signs on the in-plane axes), fp64
+    weighted ESF (suffix sums) and the per-term Laplacian KDE."""
+    oracle.set_threads(0)
+    d = len(dims)
+    rng = np.random.default_rng(77 + sum(dims))
+    n = 60_000
+    x = rng.standard_normal((n, d))
+    w = rng.uniform(0.1, 2.0, n)
+    knots = [np.linspace(-2.6, 2.6, m) for m in dims]
+    grid = _grid(knots)
+    for delta in [(1,) * d, (1,) * (d - 2) + (-1, 1), (1,) * (d - 2) + (1, -1)]:
+        got = fcb.ecdf_fastsum_counts(fcb.validate_sample(x), grid, fcb.DeltaVector(delta))
+        np.testing.assert_array_equal(got, oracle.ecdf_fastsum(x, None, knots, delta, scaled=False)
+                                      .astype(np.int64))
+    s = fcb.validate_sample(x, w)
+    assert_rel(fcb.esf_fastsum(s, grid).values, oracle.esf_fastsum(x, w, knots), 1e-12)
+    h = np.full(d, 0.4)
+    assert_rel(fcb.kde_fastsum(s, grid, fcb.laplacian(), fcb.Bandwidth.diag(h)).values,
+               oracle.kde_fastsum_laplacian(x, w, knots, h), REL_KDE)
