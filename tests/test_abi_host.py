@@ -165,3 +165,22 @@ def test_csv_wire_formats_match_reference_bytes(tmp_path):
     (tmp_path / "bad.csv").write_text("x1,w,q\n1,2\n")
     with pytest.raises(fcb.ShapeError):
         fcb.read_sample_csv(tmp_path / "bad.csv")
+
+
+def test_plain_c_consumer_links_and_runs(tmp_path):
+    """The boundary is a plain C ABI: a C program compiled against include/fastcdf_b200.h and
+    linked with -lfastcdf_b200 runs its host-side calls (no device needed)."""
+    import shutil
+    import subprocess
+
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    lib_dir = _lib.LIB_PATH.parent
+    exe = tmp_path / "abi_host"
+    subprocess.run([cc, "-std=c99", "-Wall", "-Werror", "-I", str(ROOT / "include"),
+                    str(ROOT / "tests" / "c" / "abi_host.c"), "-L", str(lib_dir), "-lfastcdf_b200",
+                    f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True, capture_output=True)
+    res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert res.returncode == 0, res.stderr
+    assert res.stdout.startswith("abi 1 ok")
