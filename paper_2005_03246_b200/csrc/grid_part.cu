@@ -1904,6 +1904,7 @@ struct PartBufs {
   int32_t *vals;
   RadixWs rw;
   int32_t *start;
+  SegSortWs sw;
 };
 
 void carve_part(Workspace &W, PartBufs &b, int64_t n, int64_t NB) {
@@ -1917,14 +1918,22 @@ void carve_part(Workspace &W, PartBufs &b, int64_t n, int64_t NB) {
   b.rw.hist = W.take<int32_t>(hist);
   b.rw.partial = W.take<int32_t>(scan_ws_partial_elems((int64_t)hist + 2));
   b.start = W.take<int32_t>(NB + 1);
+  b.sw.seg_start = W.take<int32_t>(kSortSegs + 1);
+  b.sw.tile_base = W.take<int32_t>(kSortSegs + 1);
+  b.sw.tile_seg = W.take<int32_t>(seg_sort_tiles(n));
 }
 
 int partition(const double *x, int64_t n, int d, const double *knots, const BinGrid &g,
               const PartGeo &p, int64_t NB, int nbits, PartBufs &b, cudaStream_t st) {
-  FCG_TRY(launch_part_bin_tiles(x, n, d, knots, g, p, b.keys, b.vals, b.rw.hist, st));
   // equal bucket keys may come out in any order (the plane kernel only groups by bucket)
-  FCG_TRY(radix_sort_pairs<uint32_t>(b.keys, b.vals, n, 0, ((nbits + 7) / 8) * 8, b.rw, st, false,
-                                     true));
+  if (nbits > 8 && nbits <= 16) {  // high digit first, then the low digit per segment
+    FCG_TRY(launch_part_bin_tiles(x, n, d, knots, g, p, b.keys, b.vals, b.rw.hist, st, kSortTile, 8));
+    FCG_TRY(msd2_sort_pairs_u32(b.keys, b.vals, n, nbits, b.rw, b.sw, st, true));
+  } else {
+    FCG_TRY(launch_part_bin_tiles(x, n, d, knots, g, p, b.keys, b.vals, b.rw.hist, st));
+    FCG_TRY(radix_sort_pairs<uint32_t>(b.keys, b.vals, n, 0, ((nbits + 7) / 8) * 8, b.rw, st,
+                                       false, true));
+  }
   FCG_PROF("part_bucket_start", st);
   bucket_start_kernel<<<grid_for(NB + 1, 256, 4), 256, 0, st>>>(b.keys, n, NB, p.cell_bits,
                                                                  b.start);
@@ -2114,10 +2123,7 @@ int kde_partitioned(const double *x, int64_t n, const double *w, const double *k
   double *rec_c = W.take<double>((size_t)n * (d + 1));
   uint32_t *keys_c = W.take<uint32_t>(n);
   int32_t *share_b = W.take<int32_t>((size_t)pl.NB * (kAllThreads / 32 + 1));
-  SegSortWs sw;
-  sw.seg_start = W.take<int32_t>(kSortSegs + 1);
-  sw.tile_base = W.take<int32_t>(kSortSegs + 1);
-  sw.tile_seg = W.take<int32_t>(seg_sort_tiles(n));
+  const SegSortWs &sw = b.sw;
   LatShape s;
   s.d = d;
   int64_t total_knots = 0;

@@ -398,10 +398,12 @@ __global__ void __launch_bounds__(256) seg_bounds_kernel(const uint32_t *__restr
   constexpr int K = 8;  // consecutive keys per thread, all loaded before the compares
   const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * K;
   if (i0 >= n) return;
+  // segment digits saturate at the last segment (dead keys, all ones, sort there)
+  auto seg = [&](uint32_t key) { return (int)min(key >> seg_shift, (uint32_t)(kSortSegs - 1)); };
   int c[K + 1];
-  c[0] = i0 ? (int)(keys[i0 - 1] >> seg_shift) : -1;
+  c[0] = i0 ? seg(keys[i0 - 1]) : -1;
 #pragma unroll
-  for (int k = 0; k < K; ++k) c[k + 1] = i0 + k < n ? (int)(keys[i0 + k] >> seg_shift) : kSortSegs;
+  for (int k = 0; k < K; ++k) c[k + 1] = i0 + k < n ? seg(keys[i0 + k]) : kSortSegs;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     if (i0 + k >= n) break;
@@ -409,7 +411,7 @@ __global__ void __launch_bounds__(256) seg_bounds_kernel(const uint32_t *__restr
   }
   if (i0 + K >= n) {  // the thread holding the last key closes the remaining segments
     const int64_t last = n - 1;
-    for (int x = (int)(keys[last] >> seg_shift) + 1; x <= kSortSegs; ++x) seg_start[x] = (int32_t)n;
+    for (int x = seg(keys[last]) + 1; x <= kSortSegs; ++x) seg_start[x] = (int32_t)n;
   }
 }
 
@@ -588,6 +590,53 @@ int seg_sort_pairs_u32(uint32_t *keys, int32_t *vals, int64_t n, int seg_shift, 
     FCG_CUDA_TRY(cudaMemcpyAsync(keys, ka, (size_t)n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
     FCG_CUDA_TRY(cudaMemcpyAsync(vals, va, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
     *sorted_keys = keys;
+  }
+  return FCG_OK;
+}
+
+int msd2_sort_pairs_u32(uint32_t *keys, int32_t *vals, int64_t n, int nbits, const RadixWs &ws,
+                        const SegSortWs &sw, cudaStream_t st, bool first_hist_ready) {
+  if (n <= 1) return FCG_OK;
+  if (nbits <= 8 || nbits > 16) return fail(FCG_EINVAL, "msd2 sort: 9..16 key bits");
+  const int64_t tiles = ceil_div(n, kSortTile);
+  uint32_t *kb = reinterpret_cast<uint32_t *>(ws.keys_alt);
+  int32_t *vb = ws.vals_alt;
+  constexpr size_t sm = radix_scatter_smem<uint32_t>();
+  {  // pass 1: the high digit over the whole array, keys -> alt (any order within a digit)
+    const FlatMap map{n, tiles};
+    if (!first_hist_ready) {
+      FCG_PROF("radix_hist", st);
+      radix_hist_kernel<uint32_t, FlatMap><<<(unsigned)tiles, kSortThreads, 0, st>>>(keys, map, 8, ws.hist);
+      FCG_LAUNCH_CHECK();
+    }
+    FCG_TRY(scan_i32(ws.hist, ws.hist, 256 * tiles, false, ws.partial, st));
+    FCG_PROF("radix_scatter", st);
+    auto kern = radix_scatter_kernel<uint32_t, false, FlatMap, 0>;
+    FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    kern<<<(unsigned)tiles, kSortThreads, sm, st>>>(keys, vals, kb, vb, map, 8, ws.hist, nullptr,
+                                                    nullptr, 0);
+    FCG_LAUNCH_CHECK();
+  }
+  const int64_t tmax = (int64_t)seg_sort_tiles(n);
+  {  // pass 2: the low digit inside each high-digit segment, alt -> keys
+    FCG_PROF("radix_hist", st);
+    seg_bounds_kernel<<<(unsigned)ceil_div(n, 256 * 8), 256, 0, st>>>(kb, n, 8, sw.seg_start);
+    FCG_LAUNCH_CHECK();
+    seg_tiles_kernel<<<1, kSortSegs, 0, st>>>(sw.seg_start, sw.tile_base, sw.tile_seg);
+    FCG_LAUNCH_CHECK();
+    const SegMap map{sw.seg_start, sw.tile_base, sw.tile_seg};
+    radix_hist_kernel<uint32_t, SegMap><<<(unsigned)tmax, kSortThreads, 0, st>>>(kb, map, 0, ws.hist);
+    FCG_LAUNCH_CHECK();
+  }
+  FCG_TRY(scan_i32(ws.hist, ws.hist, 256 * tmax, false, ws.partial, st));
+  {
+    FCG_PROF("radix_scatter", st);
+    const SegMap map{sw.seg_start, sw.tile_base, sw.tile_seg};
+    auto kern = radix_scatter_kernel<uint32_t, false, SegMap, 0>;
+    FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    kern<<<(unsigned)tmax, kSortThreads, sm, st>>>(kb, vb, keys, vals, map, 0, ws.hist, nullptr,
+                                                   nullptr, 0);
+    FCG_LAUNCH_CHECK();
   }
   return FCG_OK;
 }

@@ -50,6 +50,13 @@ int seg_sort_pairs_u32(uint32_t *keys, int32_t *vals, int64_t n, int seg_shift, 
                        const SegSortWs &sw, cudaStream_t st, const double *rec_in, int words,
                        double *rec_out, uint32_t **sorted_keys, bool iota_vals = false);
 
+// Sort of 32-bit keys of 9..16 bits in two unstable passes, most significant digit first: the
+// high digit over the whole array (its per-tile histogram may already be in ws.hist), then the
+// low digit inside each high-digit segment.  Result in keys / vals.  Workspace: ws.hist >=
+// 256 * seg_sort_tiles(n) + 1 ints and sw.
+int msd2_sort_pairs_u32(uint32_t *keys, int32_t *vals, int64_t n, int nbits, const RadixWs &ws,
+                        const SegSortWs &sw, cudaStream_t st, bool first_hist_ready);
+
 // Stable sort of 64-bit keys over the digits where they differ (one AND/OR reduction and a
 // 16-byte device-to-host read decide which 8-bit passes are identities).  Synchronises `st`.
 int radix_sort_pairs_pruned(uint64_t *keys, int32_t *vals, int64_t n, const RadixWs &ws,
