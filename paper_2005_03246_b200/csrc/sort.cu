@@ -573,8 +573,9 @@ int seg_sort_pairs_u32(uint32_t *keys, int32_t *vals, int64_t n, int seg_shift, 
     }
     FCG_TRY(scan_i32(ws.hist, ws.hist, 256 * tmax, false, ws.partial, st));
     FCG_PROF(last && rec_in ? "kde_materialize" : "radix_scatter", st);
-    // stable ranking in every pass (measured faster than the atomic ranking here)
-    auto kern = radix_scatter_kernel<uint32_t, true, SegMap, 0>;
+    // the first pass may rank unstably (equal keys are interchangeable)
+    auto kern = pass == 0 ? radix_scatter_kernel<uint32_t, false, SegMap, 0>
+                          : radix_scatter_kernel<uint32_t, true, SegMap, 0>;
     if (last && rec_in)
       kern = words == 4 ? radix_scatter_kernel<uint32_t, true, SegMap, 4>
                         : radix_scatter_kernel<uint32_t, true, SegMap, 5>;
