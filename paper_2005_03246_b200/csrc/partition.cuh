@@ -176,9 +176,10 @@ __global__ void __launch_bounds__(kPartThreads, 2) digit_stage_kernel(
 // from its keys alone and only (key, item index) is staged in shared memory; each item's record
 // is built at write-out time from x / w re-read in tile order (a 2048-item window, so the
 // re-read is sector-dense and the points are fetched from DRAM once).  6 bytes of shared
-// memory and a handful of registers per item instead of a staged record: 4 CTAs per SM.
+// memory and a handful of registers per item instead of a staged record (3 CTAs per SM: the
+// record build keeps its exponentials in registers).
 template <class Build, int WORDS>
-__global__ void __launch_bounds__(kPartThreads, 4) digit_stage_late_kernel(
+__global__ void __launch_bounds__(kPartThreads, 3) digit_stage_late_kernel(
     const uint32_t *__restrict__ keys, int64_t n, int shift, const int32_t *__restrict__ offs,
     int64_t tiles, const double *__restrict__ x, const double *__restrict__ w, Build build,
     double *__restrict__ rec_out, uint32_t *__restrict__ keys_out, int32_t *__restrict__ slot_out,
