@@ -11,8 +11,8 @@
 namespace fcg {
 
 constexpr int kPartThreads = 256;
-constexpr int kPartItems = 8;
-constexpr int kPartTile = kPartThreads * kPartItems;  // 2048 items per CTA
+constexpr int kPartItems = 16;
+constexpr int kPartTile = kPartThreads * kPartItems;  // 4096 items per CTA
 
 namespace part_detail {
 
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kPartThreads, 2) digit_stage_kernel(
 
 // Variant for costly builds (the KDE records: d + 1 exponentials per item).  The tile is ranked
 // from its keys alone and only (key, item index) is staged in shared memory; each item's record
-// is built at write-out time from x / w re-read in tile order (a 2048-item window, so the
+// is built at write-out time from x / w re-read in tile order (a 4096-item window, so the
 // re-read is sector-dense and the points are fetched from DRAM once).  6 bytes of shared
 // memory and a handful of registers per item instead of a staged record (3 CTAs per SM: the
 // record build keeps its exponentials in registers).
