@@ -1779,7 +1779,7 @@ __global__ void __launch_bounds__(256, D == 3 || D == 4 ? 4 : 1) part_bin_tile_k
   __syncthreads();
   constexpr int DD = D > 0 ? D : FCG_MAX_DIM;
   const int64_t tile0 = (int64_t)blockIdx.x * tile;
-  constexpr int U = 4;  // points in flight per thread
+  constexpr int U = 2;  // points in flight per thread
   // data hull (auto centre of the KDE): per-thread, then warp, then CTA, then one atomic each
   double lo[DD], hi[DD];
 #pragma unroll
