@@ -436,7 +436,7 @@ static int plane2d_scan(T *lat, const LatShape &s, bool rev_row, bool rev_col, c
   if (W % kP2Threads || (E != 1 && E != 2 && E != 4) || A < 2 * (int64_t)sm_count() || A > 65535 * 32)
     return -1;  // not applicable: the caller runs the two axis passes
   FCG_PROF("scan_plane2d", st);
-  constexpr int RB = 4, ST = 4;  // 4 rows per step, 3 steps in flight
+  constexpr int RB = 8, ST = 3;  // 8 rows per step, 2 steps in flight
   const size_t smem = (size_t)ST * RB * W * sizeof(T);
   int rc = FCG_OK;
   auto go = [&](auto kern) {
