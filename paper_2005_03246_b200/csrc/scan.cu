@@ -5,7 +5,7 @@ namespace fcg {
 
 namespace {
 
-constexpr int kUnroll = 8;
+constexpr int kUnroll = 16;
 
 template <typename T>
 __device__ __forceinline__ T warp_incl_scan(T v, int lane) {
