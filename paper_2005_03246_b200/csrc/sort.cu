@@ -192,10 +192,16 @@ __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const KeyT *__
   const int warp = threadIdx.x >> 5;
   for (int d = threadIdx.x & 31; d < 256; d += 32) s_hist[warp][d] = 0;
   __syncwarp();
-#pragma unroll 4
+  KeyT k[kSortItems];  // every key of the tile in flight before the counting
+#pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const int ii = j * kSortThreads + threadIdx.x;
-    if (ii < len) atomicAdd(&s_hist[warp][(unsigned)((keys[base + ii] >> shift) & 0xFF)], 1);
+    k[j] = ii < len ? keys[base + ii] : KeyT(0);
+  }
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const int ii = j * kSortThreads + threadIdx.x;
+    if (ii < len) atomicAdd(&s_hist[warp][(unsigned)((k[j] >> shift) & 0xFF)], 1);
   }
   __syncthreads();
   int32_t tot = 0;
