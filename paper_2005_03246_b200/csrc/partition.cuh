@@ -31,10 +31,16 @@ static __global__ void __launch_bounds__(kPartThreads) digit_hist_kernel(const u
   for (int d = threadIdx.x & 31; d < 256; d += 32) s_hist[warp][d] = 0;
   __syncwarp();
   const int64_t base = (int64_t)blockIdx.x * kPartTile;
-#pragma unroll 4
+  uint32_t k[kPartItems];  // every key of the tile in flight before the counting
+#pragma unroll
   for (int j = 0; j < kPartItems; ++j) {
     const int64_t i = base + (int64_t)j * kPartThreads + threadIdx.x;
-    if (i < n) atomicAdd(&s_hist[warp][(keys[i] >> shift) & 0xFFu], 1);
+    k[j] = i < n ? keys[i] : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < kPartItems; ++j) {
+    const int64_t i = base + (int64_t)j * kPartThreads + threadIdx.x;
+    if (i < n) atomicAdd(&s_hist[warp][(k[j] >> shift) & 0xFFu], 1);
   }
   __syncthreads();
   int32_t tot = 0;
