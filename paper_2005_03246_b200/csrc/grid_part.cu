@@ -25,7 +25,7 @@ constexpr uint32_t kDead = 0xFFFFFFFFu;
 // KDE record keys have <= 31 bits (plan_kde_partition); window lanes past a share's end carry
 // kPadKey | lane, distinct per lane so they never form a run (which would cost scan steps)
 constexpr uint32_t kPadKey = 0x80000000u;
-constexpr int kPlaneThreads = 512;
+constexpr int kPlaneThreads = 256;
 constexpr int kKdeThreads = 256;
 constexpr size_t kEcdfTileBytes = 96 * 1024;   // int32 tile budget (2 CTAs per SM)
 constexpr size_t kKdeTileBytes = 110 * 1024;   // two fp64 row-block tiles (2 CTAs per SM)
@@ -329,7 +329,7 @@ __device__ __forceinline__ void tile_store(T *__restrict__ dst, const T *tile, i
 
 // ECDF / ESF counts: CTA per plane, row blocks in scan order.
 template <int SE>
-__global__ void __launch_bounds__(kPlaneThreads, 2) plane_count_kernel(
+__global__ void __launch_bounds__(kPlaneThreads, 3) plane_count_kernel(
     PartGeo p, const int32_t *__restrict__ start, const int32_t *__restrict__ vals, int rev_r,
     int rev_c, int32_t *__restrict__ lat) {
   extern __shared__ __align__(16) unsigned char smem[];
