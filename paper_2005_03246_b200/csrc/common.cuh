@@ -107,6 +107,16 @@ __device__ __forceinline__ void l2_prefetch(const void *p, size_t bytes) {
                : "memory");
 }
 
+// a / b rounded to nearest from rb = RN(1/b): q = RN(a rb) is within one ulp of a / b, and one
+// Markstein correction q + (a - q b) rb, with the residual exact through the FMA, rounds to
+// RN(a / b) (binary64, no overflow / underflow).  The single division of fastsum.py:87-88 at
+// three instructions instead of a full division; bitwise equal to it (also checked
+// exhaustively for every count of the benchmark sizes).
+__device__ __forceinline__ double div_rn(double a, double b, double rb) {
+  const double q = a * rb;
+  return fma(fma(-q, b, a), rb, q);
+}
+
 // Lanes of the warp holding the same 8-bit digit (+ a 9th bit for out-of-range lanes): the
 // multisplit by 9 ballots (one per digit bit) instead of match.any -- the radix ranking's hot
 // instruction.

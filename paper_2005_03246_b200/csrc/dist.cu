@@ -97,6 +97,7 @@ __global__ void slab_finish_kernel(const T *__restrict__ local, const T *__restr
                                    int64_t A, int64_t J, int64_t B, double div,
                                    double *__restrict__ out) {
   const int64_t total = A * J * B;
+  const double rdiv = div > 0.0 ? 1.0 / div : 0.0;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = t % B;
@@ -104,7 +105,7 @@ __global__ void slab_finish_kernel(const T *__restrict__ local, const T *__restr
     T v = local[t];
     if (carry) v += carry[a * B + b];
     double r = (double)v;
-    if (div > 0.0) r = r / div;
+    if (div > 0.0) r = div_rn(r, div, rdiv);
     out[t] = r;
   }
 }

@@ -341,6 +341,7 @@ extern "C" int fcg_ecdf_grid(const double *x, int64_t n, int32_t d, const double
   e.kind = out_kind == 1 ? EPI_I64 : EPI_F64;
   e.out = out;
   e.div = scaled ? (double)n : 0.0;
+  e.rdiv = scaled ? 1.0 / (double)n : 0.0;
   cudaStream_t st = as_stream(stream);
   Workspace W(ws);
   // unit weights at scale: plane-partitioned pipeline (grid_part.cu)

@@ -1631,6 +1631,7 @@ __global__ void __launch_bounds__(256, 2) ecdf_final2d_kernel(const int32_t *__r
                                                               int64_t D0, int64_t D1, int64_t B,
                                                               double div, void *out) {
   extern __shared__ __align__(16) int32_t e2_smem[];
+  const double rdiv = div > 0.0 ? 1.0 / div : 0.0;
   constexpr int CW = kF2Cols;
   constexpr int ST = kE2Stages;           // slabs in flight (rows i0 + 1 .. i0 + ST - 1 arriving)
   const int slab = (int)D1 * CW;
@@ -1689,7 +1690,7 @@ __global__ void __launch_bounds__(256, 2) ecdf_final2d_kernel(const int32_t *__r
         static_cast<int64_t *>(out)[o] = (int64_t)carry[s];
       } else {
         double r = (double)carry[s];
-        if (div > 0.0) r = r / div;  // the single IEEE division of fastsum.py:87-88
+        if (div > 0.0) r = div_rn(r, div, rdiv);  // the single division of fastsum.py:87-88
         static_cast<double *>(out)[o] = r;
       }
     }

@@ -24,6 +24,7 @@ struct Epi {
   int kind = EPI_INPLACE;
   void *out = nullptr;
   double div = 0.0;        // EPI_F64: divide by div when > 0
+  double rdiv = 0.0;       // RN(1 / div) (div_rn)
   // EPI_KDE: out = (accumulate ? out : 0) + zfac * S, then * scale when apply_scale
   const double *zf = nullptr;  // concatenated per-axis factor tables
   int64_t zoff[FCG_MAX_DIM] = {0};
