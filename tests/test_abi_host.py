@@ -184,3 +184,20 @@ def test_plain_c_consumer_links_and_runs(tmp_path):
     res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
     assert res.returncode == 0, res.stderr
     assert res.stdout.startswith("abi 1 ok")
+
+
+def test_count_over_n_division_is_ieee_exact(tmp_path):
+    """The ECDF epilogue's reciprocal + Markstein correction equals the IEEE quotient c / N for
+    every count of the benchmark sizes (tests/c/div_rn_check.c)."""
+    import shutil
+    import subprocess
+
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    exe = tmp_path / "div_rn_check"
+    subprocess.run([cc, "-O2", "-ffp-contract=off", str(ROOT / "tests" / "c" / "div_rn_check.c"),
+                    "-o", str(exe), "-lm"], check=True, capture_output=True)
+    res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stdout
+    assert ", 0 mismatches" in res.stdout
