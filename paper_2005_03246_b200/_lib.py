@@ -233,3 +233,15 @@ def profile_report() -> dict:
 def check_rows(points, d: int):
     if points.shape[1] != d:
         raise ShapeError(f"expected {d} columns, got {points.shape[1]}")
+
+
+def rank_f64(keys):
+    """Device ranking of one fp64 key vector (``fcg_rank_f64``, subsystem 1): returns the int32
+    CUDA tensors (order, pos, lower, upper, dense) — stable argsort, its inverse, #keys < key,
+    #keys <= key and #distinct keys < key (-0.0 and +0.0 rank equal)."""
+    torch = _torch()
+    k = to_device_f64(keys).reshape(-1)
+    n = k.numel()
+    outs = [torch.empty(n, dtype=torch.int32, device=k.device) for _ in range(5)]
+    call_ws("fcg_rank_f64", ptr(k), n, 1, *[ptr(o) for o in outs])
+    return tuple(outs)

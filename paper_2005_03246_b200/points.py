@@ -80,3 +80,16 @@ def kernel_regression(sample: Sample, y, kernel: KernelSpec, bandwidth: Bandwidt
     return EvalResult(ratio, POINT_ALIGNED, {
         "method": "dnc-nadaraya-watson", "kernel": str(kernel),
         "runtime_seconds": time.perf_counter() - t0})
+
+
+def rank_f64(keys):
+    """Per-dimension ranking (north_star subsystem 1) of a 1-D key vector on the device:
+    (order, pos, lower, upper, dense).  ``order`` is ``np.argsort(keys, kind="stable")``
+    (dnc.py:523-528), ``dense`` / ``dense + 1`` are the reference's sorted-scan bins with
+    knots = the distinct values for delta = +1 / -1 (histogram.py:122-133), ``lower`` /
+    ``upper`` count the keys strictly below / at-or-below each key (the < and <= tie rules).
+    Returns numpy arrays for host input, int32 CUDA tensors for device input."""
+    outs = _lib.rank_f64(keys)
+    if _lib.is_torch(keys) and keys.device.type == "cuda":
+        return outs
+    return tuple(o.cpu().numpy() for o in outs)
