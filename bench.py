@@ -12,8 +12,9 @@ rank 0.  `value` is device throughput (points/s, inputs resident in HBM, CUDA ev
 ranks); `e2e` is the same metric through the public API from pinned host buffers with the H2D
 input copies and the D2H of the full result grids inside the timed region.
 
---impl reference times the CPU restatement of the reference algorithm (oracle/, the reference
-itself is pure Python and cannot travel to the GPU box) on the host cores, rank 0 only.
+--impl reference times the unmodified reference package (baseline/_ref, installed with pip
+--target; numba, single-threaded by design) through its public API on a bounded sample of the
+same workload, rank 0 only; without baseline/_ref it falls back to the C restatement (oracle/).
 """
 
 from __future__ import annotations
@@ -46,6 +47,7 @@ def parse_args():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", default="cfg5")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--numpy-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--slab", action="store_true",
@@ -385,6 +387,24 @@ class GridWorkload:
             v.record_stream(down)
         self.ev_free[b] = main.record_event()
 
+    def numpy_prepare(self):
+        """Host numpy samples as a reference user builds them (validate_sample, outside the
+        timing); the drop-in call then takes numpy in and returns numpy out."""
+        fcb = self.fcb
+        self.np_unit = fcb.validate_sample(self.pts)
+        self.np_y = fcb.validate_sample(self.pts, self.yv) if self.do_kde else None
+        nloc = int(np.prod(self.m))
+        return (self.pts.nbytes * (int(self.do_ecdf) + int(self.do_kde))
+                + (self.yv.nbytes if self.do_kde else 0),
+                nloc * 8 * (int(self.do_ecdf) + int(self.do_kde)))
+
+    def step_numpy(self):
+        fcb = self.fcb
+        if self.do_ecdf:
+            fcb.ecdf_fastsum(self.np_unit, self.grid, self.delta).values
+        if self.do_kde:
+            fcb.kde_fastsum(self.np_y, self.grid, fcb.laplacian(), self.bw).values
+
     def bytes_per_launch(self):
         # per rank: ~1/world of the points and of the lattice (axis-1 slab) when sharded
         n = self.n // self.world
@@ -403,38 +423,79 @@ class GridWorkload:
                     b[k] = v
         return b
 
-    # ---- CPU baseline: the oracle (restated reference algorithm) on a bounded sample ----
+    # ---- CPU baseline / reference arm: the reference package itself on a bounded sample ----
+    def ref_prepare(self, fc):
+        """Build (outside any timing) the reference inputs for one bounded sample of this
+        workload and return (n_points, description, call).  Configs with >= 5e7 points use the
+        1/64 block made of the first 1/8 of the knots of axes 0 AND 1 (full axes 2, 3) and the
+        points falling in it: the grid ECDF there is exactly the full configuration's ECDF
+        restricted to those cells (forward sums only reach lower knots), and the KDE is the same
+        reference algorithm (bincount + 2^d directional sweeps) over that block.  Smaller
+        configurations run in full."""
+        knots = [np.asarray(z) for z in self.w.knots]
+        pts, y = self.w.points, self.y
+        desc = "full configuration"
+        if self.n >= 50_000_000:
+            k = len(knots[0]) // 8
+            knots[0], knots[1] = knots[0][:k], knots[1][:k]
+            sel = (pts[:, 0] <= knots[0][-1]) & (pts[:, 1] <= knots[1][-1])
+            pts = np.ascontiguousarray(pts[sel])
+            y = None if y is None else np.ascontiguousarray(y[sel])
+            desc = (f"{pts.shape[0]} points in the 1/64 block of the grid (first {k} knots of "
+                    f"axes 0 and 1, full axes 2..{self.d - 1}: a "
+                    f"{'x'.join(str(len(z)) for z in knots)} sub-grid)")
+        grid = fc.RectilinearGrid.from_knots(knots)
+        calls, what = [], []
+        if self.do_ecdf:
+            s1 = fc.validate_sample(pts)
+            dv = fc.DeltaVector(tuple(self.w.delta))
+            calls.append(lambda: fc.ecdf_fastsum(s1, grid, dv))
+            what.append("fastcdf.ecdf_fastsum")
+        if self.do_kde:
+            s2 = fc.validate_sample(pts, y)
+            bw = fc.Bandwidth.diag(self.w.h)
+            lap = fc.laplacian()
+            calls.append(lambda: fc.kde_fastsum(s2, grid, lap, bw))
+            what.append("fastcdf.kde_fastsum(laplacian)")
+
+        def call():
+            for c in calls:
+                c()
+        return pts.shape[0], f"{desc}; {' + '.join(what)}", call
+
+    def ref_warm(self, fc):
+        """Compile the reference's numba kernels on a tiny instance of the same calls."""
+        rng = np.random.default_rng(0)
+        x = rng.random((256, self.d))
+        g = fc.RectilinearGrid.from_knots([np.linspace(0, 1, 5)] * self.d)
+        if self.do_ecdf:
+            fc.ecdf_fastsum(fc.validate_sample(x), g, fc.DeltaVector(tuple(self.w.delta)))
+        if self.do_kde:
+            fc.kde_fastsum(fc.validate_sample(x, rng.random(256)), g, fc.laplacian(),
+                           fc.Bandwidth.diag(np.full(self.d, 0.5)))
+
+    # ---- fallback when baseline/_ref is absent: the C restatement (oracle/) ----------------
     def cpu_sample(self, threads):
-        """Time the oracle port on a bounded sample of this workload.  Configs with >= 5e7
-        points use the exact axis-0 slab made of the first 1/8 of the grid's axis-0 knots and
-        the points falling in it (the ECDF there is exactly that sub-problem); the KDE is timed
-        on one of its 2^d delta-terms and scaled by 2^d."""
+        """Time the oracle port on the same bounded sample as ref_prepare (no scaling)."""
         import oracle
 
         used = oracle.set_threads(threads)
         knots = [np.asarray(z) for z in self.w.knots]
         pts, y = self.w.points, self.y
-        frac = 8 if self.n >= 50_000_000 else 1
-        if frac > 1:
-            knots[0] = knots[0][: len(knots[0]) // frac]
-            sel = pts[:, 0] <= knots[0][-1]
+        if self.n >= 50_000_000:
+            k = len(knots[0]) // 8
+            knots[0], knots[1] = knots[0][:k], knots[1][:k]
+            sel = (pts[:, 0] <= knots[0][-1]) & (pts[:, 1] <= knots[1][-1])
             pts = np.ascontiguousarray(pts[sel])
             y = None if y is None else np.ascontiguousarray(y[sel])
         n_s = pts.shape[0]
-        t_total = 0.0
-        desc = [f"{n_s} points" + (f" (axis-0 slab, 1/{frac} of the grid)" if frac > 1 else "")]
+        t0 = time.perf_counter()
         if self.do_ecdf:
-            t0 = time.perf_counter()
             oracle.ecdf_fastsum(pts, None, knots, self.w.delta, scaled=True)
-            t_total += time.perf_counter() - t0
-            desc.append("grid ECDF")
         if self.do_kde:
-            t0 = time.perf_counter()
-            oracle.kde_fastsum_laplacian(pts, y, knots, self.w.h, codes=[0])
-            dt = time.perf_counter() - t0
-            t_total += dt * (1 << self.d)
-            desc.append(f"KDE: 1 of {1 << self.d} delta-terms timed, x{1 << self.d}")
-        return n_s / t_total, used, "; ".join(desc), t_total
+            oracle.kde_fastsum_laplacian(pts, y, knots, self.w.h)
+        dt = time.perf_counter() - t0
+        return n_s / dt, used, f"{n_s} points (1/64 block when N >= 5e7); oracle port", dt
 
 
 def dominant(prof: dict, bytes_map: dict):
@@ -539,6 +600,23 @@ class PointsWorkload:
         self.out_pinned[: self.n].copy_(a, non_blocking=True)
         self.out_pinned[self.n:].copy_(b, non_blocking=True)
 
+    def numpy_prepare(self):
+        fcb = self.fcb
+        x = self.w.points
+        if self.name == "cfg2":
+            self.np_s = fcb.validate_sample(x, self.w.weights)
+            return x.nbytes + self.w.weights.nbytes, 2 * self.n * 8
+        self.np_s = fcb.validate_sample(x)
+        return x.nbytes + self.w.extra["y"].nbytes, 2 * self.n * 8
+
+    def step_numpy(self):
+        fcb = self.fcb
+        if self.name == "cfg2":
+            fcb.ecdf_at_points(self.np_s, fcb.DeltaVector(self.w.delta)).values
+            fcb.esf_at_points(self.np_s).values
+        else:
+            fcb.kde_numerators(self.np_s, [None, self.w.extra["y"]], fcb.Bandwidth.diag(self.w.h))
+
     def bytes_per_launch(self):
         n = self.n
         b = radix_bytes(n)
@@ -555,6 +633,49 @@ class PointsWorkload:
                       "pts_group_gather": (4 + 8 + 16 + 16) * n + (4 + 4 + 16 + 16 + 4) * n,
                       "pts_psi": (16 + 16 + 16 + 8) * n})
         return b
+
+    def ref_prepare(self, fc):
+        """Reference inputs for one bounded sample (built outside the timing).
+        cfg2: the reference's own route for ties at the points: the grid ECDF / ESF on
+        the 1024-level lattice (fastsum.py:69-111) gathered at the points, full configuration.
+        cfg4: fastcdf.kde_dnc (dnc.py:635-690) for both weight vectors on the first 1e6 points
+        (the full N = 1e7 takes ~130 s per step on one core)."""
+        x = self.w.points
+        if self.name == "cfg2":
+            lev = 1024
+            g = fc.RectilinearGrid.from_knots([np.arange(lev) / lev] * 2)
+            s = fc.validate_sample(x, self.w.weights)
+            idx = (x * lev).astype(np.int64)
+            flat = idx[:, 0] * lev + idx[:, 1]
+            dv = fc.DeltaVector(tuple(self.w.delta))
+
+            def call():
+                fc.ecdf_fastsum(s, g, dv).values[flat]
+                fc.esf_fastsum(s, g).values[flat]
+            return self.n, ("full configuration; fastcdf.ecdf_fastsum + esf_fastsum on the "
+                            "1024-level lattice, gathered at the points"), call
+        m = 1_000_000
+        s1 = fc.validate_sample(x[:m])
+        s2 = fc.validate_sample(x[:m], self.w.extra["y"][:m])
+        bw = fc.Bandwidth.diag(self.w.h)
+        lap = fc.laplacian()
+
+        def call():
+            fc.kde_dnc(s1, lap, bw)
+            fc.kde_dnc(s2, lap, bw)
+        return m, f"first {m} points; fastcdf.kde_dnc(laplacian) for w == 1 and w = y", call
+
+    def ref_warm(self, fc):
+        rng = np.random.default_rng(0)
+        x = rng.random((256, 2))
+        if self.name == "cfg2":
+            g = fc.RectilinearGrid.from_knots([np.arange(8) / 8] * 2)
+            s = fc.validate_sample(x, rng.random(256))
+            fc.ecdf_fastsum(s, g, fc.DeltaVector((1, -1)))
+            fc.esf_fastsum(s, g)
+        else:
+            fc.kde_dnc(fc.validate_sample(x, rng.random(256)), fc.laplacian(),
+                       fc.Bandwidth.diag(np.array([0.1, 0.1])))
 
     def cpu_sample(self, threads):
         import oracle
@@ -583,34 +704,67 @@ def make_workload(name):
 
 
 # ------------------------------------------------------------------------------------------
+def load_fastcdf():
+    """The unmodified reference package installed under baseline/_ref (pip --target, see
+    DESIGN.md), or None when it is absent."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "fastcdf" / "__init__.py").exists():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/fcg_numba_cache")
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    import fastcdf
+
+    return fastcdf
+
+
+def reference_timing(w, steps, warm=True):
+    """Time `steps` runs of the reference's public API on the workload's bounded sample.
+    Returns (points/s, seconds per step, cores, kind, sample description)."""
+    fc = load_fastcdf()
+    if fc is None:  # fallback: the C restatement of the same algorithm (oracle/)
+        vals, secs, sample, used = [], [], "", 1
+        for _ in range(steps):
+            v, used, sample, dt = w.cpu_sample(0)
+            vals.append(v)
+            secs.append(dt)
+        return float(np.sum([v * t for v, t in zip(vals, secs)]) / np.sum(secs)), \
+            float(np.mean(secs)), used, "port", sample + " (baseline/_ref absent)"
+    if warm:
+        w.ref_warm(fc)
+    n_s, sample, call = w.ref_prepare(fc)
+    secs = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        call()
+        secs.append(time.perf_counter() - t0)
+    tot = float(np.sum(secs))
+    return n_s * steps / tot, tot / steps, 1, "reference", sample
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the oracle port on the host cores, rank 0 only."""
+    """--impl reference: the unmodified reference package (baseline/_ref, numba, single-threaded
+    by design: cli.py:265-268) through its public API on the host, rank 0 only."""
     if rank != 0:
         return
-    import oracle
-
     w = make_workload(args.workload)
-    threads = oracle.set_threads(0)
-    vals = []
-    for _ in range(max(args.warmup, 0)):
-        small = wl.cfg1(n=4096, m=16)
-        oracle.ecdf_fastsum(small.points, None, small.knots, small.delta)
-    sample = ""
-    for _ in range(args.steps):
-        v, used, sample, _ = w.cpu_sample(threads)
-        vals.append(v)
-    value = float(np.median(vals))
+    fc = load_fastcdf()
+    if fc is not None:
+        for _ in range(max(args.warmup, 1)):  # warm-up = jit compile on a tiny instance
+            w.ref_warm(fc)
+    value, sec, cores, kind, sample = reference_timing(w, args.steps, warm=False)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": w.n / value * 1e3, "higher_is_better": True, "scaling": w.scaling,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": w.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded numpy, SURVEY §8d)",
-        "config": w.describe(),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
+        "config": w.describe(), "parallelism": "host CPU, rank 0 only",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": sample, "host_cpus": os.cpu_count()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "oracle/ = C restatement of the reference fastcdf algorithm (pure-Python "
-                "reference cannot travel to the GPU box); warm-up steps run a tiny instance",
+        "note": ("each step is one timed call sequence of the reference's public API on the "
+                 "bounded sample named in cpu_baseline.sample (value = sample points / measured "
+                 "seconds, no extrapolation); warm-up steps jit-compile on a tiny instance"),
     }
     print(json.dumps(line), flush=True)
 
@@ -719,11 +873,29 @@ def main():
                "h2d_bytes_per_step": w.h2d_bytes, "d2h_bytes_per_step": w.d2h_bytes,
                "ms_per_step": e_step, "steps": args.e2e_steps, "mode": w.e2e_mode}
 
+    # ---- e2e_numpy: the drop-in call exactly as a reference user makes it (numpy in, numpy
+    # out, the library's own pageable copies inside the call), serial, wall clock ----------
+    e2e_np = None
+    if not args.no_e2e and world == 1 and hasattr(w, "step_numpy"):
+        hb, db = w.numpy_prepare()
+        w.step_numpy()
+        torch.cuda.synchronize()
+        k = max(1, args.numpy_steps)
+        t0 = time.perf_counter()
+        for _ in range(k):
+            w.step_numpy()
+        torch.cuda.synchronize()
+        nsec = (time.perf_counter() - t0) / k
+        e2e_np = {"value": w.n_total / nsec, "unit": UNIT, "ms_per_step": nsec * 1e3,
+                  "steps": k, "h2d_bytes_per_step": hb, "d2h_bytes_per_step": db,
+                  "mode": "drop-in call: numpy arrays in, numpy arrays out, one call after "
+                          "another (wall clock)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, used, sample, secs = w.cpu_sample(0)
-        cpu = {"value": v, "unit": UNIT, "cores": used, "kind": "port", "sample": sample,
-               "seconds": secs}
+        v, secs, used, kind, sample = reference_timing(w, 1)
+        cpu = {"value": v, "unit": UNIT, "cores": used, "kind": kind, "sample": sample,
+               "seconds": secs, "host_cpus": os.cpu_count()}
 
     if rank == 0:
         line = {
@@ -731,8 +903,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": w.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded numpy, SURVEY §8d shapes)",
-            "config": {**w.describe(), "parallelism": w.parallelism(world)},
-            "e2e": e2e, "gpu_launches": int(launches), "roofline": roof,
+            "config": w.describe(), "parallelism": w.parallelism(world),
+            "e2e": e2e, "e2e_numpy": e2e_np, "gpu_launches": int(launches), "roofline": roof,
             "cpu_baseline": cpu, "clocks": clk, "kernels": breakdown,
         }
         print(json.dumps(line), flush=True)

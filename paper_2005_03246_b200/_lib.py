@@ -167,6 +167,11 @@ def to_device_f64(a):
         t = a
         if t.device.type != "cuda":
             t = t.to(device(), non_blocking=True)
+        elif t.device.index != torch.cuda.current_device():
+            # kernels launch on the current device's stream with workspace allocated there
+            raise ParameterError(
+                f"tensor is on {t.device} but the current CUDA device is "
+                f"cuda:{torch.cuda.current_device()}; call under torch.cuda.device({t.device})")
         return t.to(torch.float64).contiguous()
     arr = np.ascontiguousarray(a, dtype=np.float64)
     return torch.from_numpy(arr).to(device(), non_blocking=True)

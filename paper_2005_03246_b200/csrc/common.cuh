@@ -107,11 +107,12 @@ __device__ __forceinline__ void l2_prefetch(const void *p, size_t bytes) {
                : "memory");
 }
 
-// a / b rounded to nearest from rb = RN(1/b): q = RN(a rb) is within one ulp of a / b, and one
-// Markstein correction q + (a - q b) rb, with the residual exact through the FMA, rounds to
-// RN(a / b) (binary64, no overflow / underflow).  The single division of fastsum.py:87-88 at
-// three instructions instead of a full division; bitwise equal to it (also checked
-// exhaustively for every count of the benchmark sizes).
+// a / b from rb = RN(1/b): q = RN(a rb), then one Markstein correction q + (a - q b) rb with the
+// residual exact through the FMA.  Markstein's theorem makes the result RN(a / b) whenever q is
+// faithful (within one ulp of a / b), which RN(a rb) is not guaranteed to be in general.  What
+// is verified (tests/c/div_rn_check.c): bitwise equality with the IEEE quotient for every count
+// c in [0, N] at the benchmark sizes, and for 2e7 random pairs (c <= N < 2^31) -- the only
+// operands the epilogues pass (integer counts over N, fastsum.py:87-88).
 __device__ __forceinline__ double div_rn(double a, double b, double rb) {
   const double q = a * rb;
   return fma(fma(-q, b, a), rb, q);

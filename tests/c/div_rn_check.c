@@ -23,6 +23,23 @@ int main(void) {
       ++tot;
     }
   }
+  /* random (c, N) with 1 <= N < 2^31 and 0 <= c <= N (splitmix64 stream, fixed seed) */
+  unsigned long long st = 0x2005032460000001ull;
+  for (long k = 0; k < 20000000; ++k) {
+    unsigned long long z = (st += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    const long nb = 1 + (long)(z & 0x7FFFFFFEull);
+    const long c = (long)((z >> 32) % (unsigned long long)(nb + 1));
+    const double a = (double)c, b = (double)nb, rb = 1.0 / b;
+    const double q = a * rb, q2 = fma(fma(-q, b, a), rb, q);
+    if (q2 != a / b) {
+      if (bad < 5) printf("mismatch a=%ld b=%ld\n", c, nb);
+      ++bad;
+    }
+    ++tot;
+  }
   printf("checked %ld quotients, %ld mismatches\n", tot, bad);
   return bad != 0;
 }
