@@ -19,6 +19,8 @@
 //    problem (flip p0 and/or p1), sharing one ranking and one chunk/block grouping.
 //  * brute force O(n^2) tiles (d >= 3 without a feasible rank lattice; SURVEY §8f #3 widens
 //    this later).
+#include <string>
+
 #include "common.cuh"
 #include "scan.cuh"
 #include "sort.cuh"
@@ -33,7 +35,10 @@ constexpr int SUBL = 6;
 constexpr int SUB = 1 << SUBL;  // level-2 sub-block size
 constexpr int NSUB = S / SUB;   // 64
 constexpr int kSolverThreads = 1024;
-constexpr int64_t kMaxDominanceN = int64_t(1) << 26;  // coarse grid (n/S)^2 must fit in HBM
+// The d = 2 dominance route keeps a (n/S)^2 x channels fp64 coarse grid: up to 48 GB of the
+// 180 GB HBM (n ~ 2.5e8 with two channels); larger n is refused up front with a clear error.
+constexpr int64_t kMaxCoarseBytes = int64_t(48) << 30;
+constexpr int kCoarseRowBytes = 96 * 1024;  // shared-memory row segment of the coarse histogram
 
 // ------------------------------------------------------------------------------------------
 // helpers
@@ -112,33 +117,40 @@ __device__ __forceinline__ int32_t flipp(int32_t p, int f, int64_t npad) {
   return f ? (int32_t)(npad - 1 - p) : p;
 }
 
-// coarse rows: CTA per flipped chunk c; row[b][ch] accumulated in shared memory
-__global__ void __launch_bounds__(512) coarse_rows_smem(Dom2 D) {
-  extern __shared__ double s_row[];  // [P][nch]
+// blocks per shared-memory segment of a coarse row
+inline int64_t coarse_tb(int nch) { return kCoarseRowBytes / (8 * (int64_t)nch); }
+
+// the d = 2 dominance route's coarse grid fits the device budget
+inline bool dom_fits(int64_t n, int nch) {
+  const int64_t P = ceil_div(n, S);
+  return P * P * nch * 8 <= kMaxCoarseBytes;
+}
+inline int dom_too_large(int64_t n) {
+  return fail(FCG_EUNSUPPORTED,
+              "n = " + std::to_string(n) + " points: the d = 2 dominance coarse grid would "
+              "exceed the 48 GB device budget (n <= ~2.5e8 with two weight channels)");
+}
+
+// coarse rows: CTA per (flipped chunk c, segment of TB blocks); row[b][ch] accumulated in
+// shared memory, so a row of any length is built in ceil(P / TB) segments
+__global__ void __launch_bounds__(512) coarse_rows_smem(Dom2 D, int64_t TB) {
+  extern __shared__ double s_row[];  // [TB][nch]
   const int64_t c = blockIdx.x;
   const int64_t g = D.f1 ? D.P - 1 - c : c;
   const int64_t P = D.P;
-  for (int64_t i = threadIdx.x; i < P * D.nch; i += blockDim.x) s_row[i] = 0.0;
+  const int64_t b0 = (int64_t)blockIdx.y * TB, nb = (b0 + TB < P ? TB : P - b0);
+  for (int64_t i = threadIdx.x; i < nb * D.nch; i += blockDim.x) s_row[i] = 0.0;
   __syncthreads();
   const int64_t lo = g * S, hi = (g + 1) * S < D.n ? (g + 1) * S : D.n;
   for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) {
     const int32_t src = D.bychunk[k];
-    const int64_t b = flipp(D.pos0[src], D.f0, D.npad) >> LS;
+    const int64_t b = (flipp(D.pos0[src], D.f0, D.npad) >> LS) - b0;
+    if (b < 0 || b >= nb) continue;
     for (int ch = 0; ch < D.nch; ++ch) atomicAdd(&s_row[b * D.nch + ch], D.psi[ch * D.n + src]);
   }
   __syncthreads();
-  double *row = D.G + c * P * D.nch;
-  for (int64_t i = threadIdx.x; i < P * D.nch; i += blockDim.x) row[i] = s_row[i];
-}
-
-__global__ void coarse_atomic(Dom2 D) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < D.n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = flipp(D.pos1[i], D.f1, D.npad) >> LS;
-    const int64_t b = flipp(D.pos0[i], D.f0, D.npad) >> LS;
-    for (int ch = 0; ch < D.nch; ++ch)
-      atomicAdd(&D.G[(c * D.P + b) * D.nch + ch], D.psi[ch * D.n + i]);
-  }
+  double *row = D.G + (c * P + b0) * D.nch;
+  for (int64_t i = threadIdx.x; i < nb * D.nch; i += blockDim.x) row[i] = s_row[i];
 }
 
 // out = inclusive-prefix coarse grid at (chunk(Q1f) - 1, block(Q0f) - 1)
@@ -625,21 +637,23 @@ struct Dom2S {
   double *G;         // coarse grid [P][P][nch]
 };
 
-__global__ void __launch_bounds__(512) coarse_rows_group(Dom2S D) {
-  extern __shared__ double s_row[];  // [P][nch]
+__global__ void __launch_bounds__(512) coarse_rows_group(Dom2S D, int64_t TB) {
+  extern __shared__ double s_row[];  // [TB][nch]
   const int64_t c = blockIdx.x;
   const int64_t g = D.f1 ? D.P - 1 - c : c;
   const int64_t P = D.P;
-  for (int64_t i = threadIdx.x; i < P * D.nch; i += blockDim.x) s_row[i] = 0.0;
+  const int64_t b0 = (int64_t)blockIdx.y * TB, nb = (b0 + TB < P ? TB : P - b0);
+  for (int64_t i = threadIdx.x; i < nb * D.nch; i += blockDim.x) s_row[i] = 0.0;
   __syncthreads();
   const int64_t lo = g * S, hi = (g + 1) * S < D.n ? (g + 1) * S : D.n;
   for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) {
-    const int64_t b = flipp(D.gc.rankpos[k], D.f0, D.npad) >> LS;
+    const int64_t b = (flipp(D.gc.rankpos[k], D.f0, D.npad) >> LS) - b0;
+    if (b < 0 || b >= nb) continue;
     for (int ch = 0; ch < D.nch; ++ch) atomicAdd(&s_row[b * D.nch + ch], D.gc.psi[ch * D.n + k]);
   }
   __syncthreads();
-  double *row = D.G + c * P * D.nch;
-  for (int64_t i = threadIdx.x; i < P * D.nch; i += blockDim.x) row[i] = s_row[i];
+  double *row = D.G + (c * P + b0) * D.nch;
+  for (int64_t i = threadIdx.x; i < nb * D.nch; i += blockDim.x) row[i] = s_row[i];
 }
 
 // acc_q[ch][t] += z_t * G[chunk(t) - 1][block(t) - 1]   (query order, self thresholds)
@@ -969,18 +983,15 @@ int dom2d(PtsWs &p, int64_t n, int nch, int f0, int f1, const double *psi, doubl
     FCG_TRY(bucket(p.kc, n, P + 1, p.qc_list, p.qc_start, p.cursor, p, st));
     FCG_TRY(bucket(p.kb, n, P + 1, p.qb_list, p.qb_start, p.cursor, p, st));
   }
-  // level 1: coarse grid
-  const size_t row_smem = (size_t)P * nch * sizeof(double);
-  if (row_smem <= 96 * 1024) {
+  // level 1: coarse grid (rows in shared-memory segments of TB blocks)
+  {
     FCG_PROF("pts_coarse_hist", st);
+    const int64_t TB = coarse_tb(nch);
+    const int64_t nseg = ceil_div(P, TB);
+    const size_t row_smem = (size_t)(TB < P ? TB : P) * nch * sizeof(double);
     FCG_CUDA_TRY(cudaFuncSetAttribute(coarse_rows_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(96 * 1024)));
-    coarse_rows_smem<<<(unsigned)P, 512, row_smem, st>>>(D);
-    FCG_LAUNCH_CHECK();
-  } else {
-    FCG_PROF("pts_coarse_hist", st);
-    FCG_CUDA_TRY(cudaMemsetAsync(p.G, 0, (size_t)P * P * nch * sizeof(double), st));
-    coarse_atomic<<<grid_for(n, 256), 256, 0, st>>>(D);
+                                      kCoarseRowBytes));
+    coarse_rows_smem<<<dim3((unsigned)P, (unsigned)nseg), 512, row_smem, st>>>(D, TB);
     FCG_LAUNCH_CHECK();
   }
   LatShape gs;
@@ -1114,11 +1125,10 @@ int self_dom2d(const double *x, const double *w, int64_t n, int nw, int kde, con
     FCG_CUDA_TRY(cudaFuncSetAttribute(level2_self<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     FCG_CUDA_TRY(cudaFuncSetAttribute(level2_self<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   }
-  const size_t row_smem = (size_t)P * nw * sizeof(double);
-  const bool smem_rows = row_smem <= 96 * 1024;
-  if (smem_rows)
-    FCG_CUDA_TRY(cudaFuncSetAttribute(coarse_rows_group, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(96 * 1024)));
+  const int64_t TB = coarse_tb(nw), nseg = ceil_div(P, TB);
+  const size_t row_smem = (size_t)(TB < P ? TB : P) * nw * sizeof(double);
+  FCG_CUDA_TRY(cudaFuncSetAttribute(coarse_rows_group, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kCoarseRowBytes));
   const int ncodes = kde ? 4 : 1;
   for (int code = 0; code < ncodes; ++code) {
     KdeP kp{};
@@ -1140,11 +1150,7 @@ int self_dom2d(const double *x, const double *w, int64_t n, int nw, int kde, con
     }
     {
       FCG_PROF("pts_coarse_hist", st);
-      if (smem_rows) {
-        coarse_rows_group<<<(unsigned)P, 512, row_smem, st>>>(D);
-      } else {
-        return fail(FCG_EUNSUPPORTED, "coarse grid row exceeds shared memory (n too large)");
-      }
+      coarse_rows_group<<<dim3((unsigned)P, (unsigned)nseg), 512, row_smem, st>>>(D, TB);
       FCG_LAUNCH_CHECK();
     }
     LatShape gs;
@@ -1249,7 +1255,7 @@ extern "C" int fcg_ecdf_points(const double *x, int64_t n, int32_t d, const doub
     for (int k = 0; k < d; ++k)
       if (delta[k] != 1 && delta[k] != -1) return fail(FCG_EINVAL, "delta entries must be -1 or +1");
   // Workspace is sized for the worst case of the routes chosen at run time.
-  const bool dom_ok = (d == 2 && n <= kMaxDominanceN);
+  const bool dom_ok = (d == 2 && dom_fits(n, 1));
   const int64_t budget = lattice_budget(n);
   Workspace W(ws);
   PtsWs p;
@@ -1360,7 +1366,8 @@ extern "C" int fcg_ecdf_points(const double *x, int64_t n, int32_t d, const doub
     return FCG_OK;
   }
 
-  // brute force
+  if (d == 2) return dom_too_large(n);
+  // brute force (d >= 3 without a feasible rank lattice)
   Brute B;
   B.n = n;
   B.d = d;
@@ -1384,7 +1391,8 @@ extern "C" int fcg_dnc_ecdf(const double *x, int64_t n, int32_t d, const double 
                             int32_t include_self, int32_t scaled, double *out, void *ws,
                             size_t *ws_bytes, void *stream) {
   FCG_TRY(check_pts(n, d));
-  const bool dom_ok = (d == 2 && n <= kMaxDominanceN);
+  if (d == 2 && !dom_fits(n, 1)) return dom_too_large(n);
+  const bool dom_ok = d == 2;
   Workspace W(ws);
   PtsWs p;
   carve(W, p, n, d < 2 ? d : 2, 1, dom_ok, false, d == 1 ? 2 * n : 0);
@@ -1426,7 +1434,8 @@ extern "C" int fcg_kde_points_laplacian(const double *x, int64_t n, int32_t d, c
                                         double *out, void *ws, size_t *ws_bytes, void *stream) {
   FCG_TRY(check_pts(n, d));
   if (nw < 1 || nw > 2) return fail(FCG_EUNSUPPORTED, "nw must be 1 or 2 weight vectors per call");
-  const bool dom_ok = (d == 2 && n <= kMaxDominanceN);
+  if (d == 2 && !dom_fits(n, nw)) return dom_too_large(n);
+  const bool dom_ok = d == 2;
   Workspace W(ws);
   PtsWs p;
   carve(W, p, n, d < 2 ? d : 2, nw, dom_ok, true, d == 1 ? n * 2 : 0);
@@ -1549,7 +1558,8 @@ extern "C" int fcg_kde_points_matern32(const double *x, int64_t n, int32_t d, co
                                        const double *h, const double *centre, double *out,
                                        void *ws, size_t *ws_bytes, void *stream) {
   FCG_TRY(check_pts(n, d));
-  const bool dom_ok = (d == 2 && n <= kMaxDominanceN);
+  if (d == 2 && !dom_fits(n, 2)) return dom_too_large(n);
+  const bool dom_ok = d == 2;
   const int nchan = 2 * d + 1;
   Workspace W(ws);
   PtsWs p;

@@ -236,6 +236,37 @@ def test_cfg4_full(cfg_meta):
     assert np.all(num[0] > 0)
 
 
+@pytest.mark.slow
+def test_cfg4_3e7_two_vectors(oracle):
+    """N = 3e7 with two weight vectors: coarse rows (7,325 blocks x 2 channels = 117 KB) exceed
+    one shared-memory segment, so the row histogram runs in segments (no N ceiling below the
+    device budget).  Checked on a seeded subset of queries against the direct O(N) sum
+    (naive.py's Laplacian kernel), density relative and the regression numerator on the
+    |y|-weighted scale."""
+    import workloads as wl
+
+    oracle.set_threads(0)
+    w = wl.cfg4(30_000_000)
+    y = w.extra["y"]
+    s = fcb.validate_sample(w.points)
+    num = fcb.kde_numerators(s, [None, y], fcb.Bandwidth.diag(w.h))
+    q = np.random.default_rng(17).integers(0, w.n, 96)
+    dens = oracle.kde_naive_laplacian(w.points, None, w.points[q], w.h)
+    reg = oracle.kde_naive_laplacian(w.points, y, w.points[q], w.h)
+    absreg = oracle.kde_naive_laplacian(w.points, np.abs(y), w.points[q], w.h)
+    assert rel_err(num[0][q], dens) <= 1e-9
+    assert rel_err(num[1][q], reg, absreg) <= 1e-9
+
+
+def test_dominance_size_guard():
+    """A d = 2 problem whose coarse grid would exceed the device budget is refused up front with
+    ParameterError (never the O(N^2) fallback)."""
+    from paper_2005_03246_b200 import _lib
+
+    with pytest.raises(fcb.ParameterError, match="coarse grid"):
+        _lib.call_ws("fcg_dnc_ecdf", None, 400_000_000, 2, None, 0, 1, None)
+
+
 def test_d3_brute_paths(oracle):
     rng = np.random.default_rng(3)
     x = rng.standard_normal((3000, 3))
