@@ -521,11 +521,17 @@ class PointsWorkload:
     """At-points configs: cfg2 (ECDF delta=(1,-1) + ESF with ties, N = 1e6) and cfg4 (Laplacian
     KDE density + regression numerators, N = 1e7, one device pass)."""
 
-    scaling = "weak"
+    scaling = "strong"  # the configuration's work is fixed; N > 1 splits cfg4's queries
 
-    @staticmethod
-    def parallelism(world):
-        return "single GPU" if world == 1 else f"replicas x{world} (one full problem per GPU)"
+    def parallelism(self, world):
+        if world == 1:
+            return "single GPU"
+        if self.name == "cfg4":
+            return (f"query shards x{world}: sources ranked on every GPU (replicated), queries "
+                    f"split by dimension-1 rank chunks, one NCCL SUM all-reduce gathers the "
+                    f"numerators")
+        return (f"replicas x{world}: the rank-lattice route is not sharded, every GPU computes "
+                f"the whole problem (counted once)")
 
     def __init__(self, name):
         import paper_2005_03246_b200 as fcb
@@ -545,9 +551,9 @@ class PointsWorkload:
                 else f"inputs larger than L2 ({self.n * 16 / 1e9:.2f} GB points)"}
 
     def shard(self, rank, world):
-        """At-points configs run one full replica per GPU (weak scaling)."""
+        """cfg4: query shards (strong scaling); cfg2: replicas, the problem counted once."""
         self.rank, self.world = rank, world
-        self.n_total = self.n * world
+        self.n_total = self.n
 
     def _sample(self, x, y):
         fcb = self.fcb
@@ -581,7 +587,12 @@ class PointsWorkload:
             a = fcb.ecdf_at_points(s, fcb.DeltaVector(self.w.delta)).values
             b = fcb.esf_at_points(s).values
             return a, b
-        num = fcb.kde_numerators(s, [None, y], fcb.Bandwidth.diag(self.w.h))
+        if self.world > 1:
+            from paper_2005_03246_b200 import distributed as fdist
+
+            num = fdist.kde_numerators_sharded(s, [None, y], fcb.Bandwidth.diag(self.w.h))
+        else:
+            num = fcb.kde_numerators(s, [None, y], fcb.Bandwidth.diag(self.w.h))
         return num[0], num[1]
 
     def step(self):

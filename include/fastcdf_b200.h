@@ -229,6 +229,23 @@ int fcg_kde_points_laplacian(const double *x, int64_t n, int32_t d, const double
                              int32_t nw, const double *h, const double *centre, double *out,
                              void *ws, size_t *ws_bytes, void *stream);
 
+/* Query-sharded forms for one process per GPU ("sample-point queries are sharded
+ * with the ranked data replicated"); d = 2 (the dominance route).  Every shard ranks and
+ * groups all n sources (replicated) but evaluates only its own queries: the points whose
+ * rank along dimension 1 falls in chunks [P s / G, P (s+1) / G) of the P = ceil(n / 4096)
+ * chunks (a contiguous 1/G slice of the queries in rank order).  Other entries of out are
+ * set to exactly 0, so a SUM all-reduce over the G shards gathers the result (the owned values
+ * are computed by exactly the unsharded arithmetic; the coarse histogram's shared-memory
+ * atomics make repeated calls agree to rounding).  Same arguments as the unsharded calls plus
+ * shard s in [0, G) and G. */
+int fcg_kde_points_laplacian_shard(const double *x, int64_t n, int32_t d, const double *w,
+                                   int32_t nw, const double *h, const double *centre,
+                                   int32_t shard, int32_t nshards, double *out,
+                                   void *ws, size_t *ws_bytes, void *stream);
+int fcg_dnc_ecdf_shard(const double *x, int64_t n, int32_t d, const double *w,
+                       int32_t include_self, int32_t scaled, int32_t shard, int32_t nshards,
+                       double *out, void *ws, size_t *ws_bytes, void *stream);
+
 /* matern32-additive KDE at the sample points (dnc.py:635-690 with family "matern32-additive"):
  * the d + 1 channels of dnc.py:661-669 are run as 2d + 1 Laplacian dominance channels whose
  * weights only change sign with the term (A = w e, B_k = s_k w e, C_l = s_l w xc_l e / h_l),

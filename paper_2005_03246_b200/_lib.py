@@ -54,6 +54,9 @@ _SIGS = {
     "fcg_dnc_ecdf": ([_P, _I64, _I32, _P, _I32, _I32, _P, _P, _SZP, _P], C.c_int),
     "fcg_kde_points_laplacian": ([_P, _I64, _I32, _P, _I32, _P, _P, _P, _P, _SZP, _P], C.c_int),
     "fcg_kde_points_matern32": ([_P, _I64, _I32, _P, _P, _P, _P, _P, _SZP, _P], C.c_int),
+    "fcg_kde_points_laplacian_shard": ([_P, _I64, _I32, _P, _I32, _P, _P, _I32, _I32, _P, _P, _SZP,
+                                        _P], C.c_int),
+    "fcg_dnc_ecdf_shard": ([_P, _I64, _I32, _P, _I32, _I32, _I32, _I32, _P, _P, _SZP, _P], C.c_int),
     "fcg_axis_owner": ([_P, _I64, _I32, _I32, _P, _I64, _I32, _I32, _P, _I32, _P, _P], C.c_int),
     "fcg_partition_rows": ([_P, _I64, _I32, _P, _P, _I32, _P, _P, _P, _P, _SZP, _P], C.c_int),
     "fcg_slab_finish": ([_P, _I32, _P, _I64, _I64, _I64, C.c_double, _P, _P], C.c_int),

@@ -632,6 +632,7 @@ __global__ void group_psi_kernel(GrpArrays g, int64_t n, KdeP kp, int nw, int kd
 
 struct Dom2S {
   int64_t n, P, npad;
+  int64_t c_lo, c_hi;  // query shard: points whose (unflipped) chunk p1 >> LS is in [c_lo, c_hi)
   int nch, f0, f1, kde;
   GrpArrays gc, gb;  // chunk and block groupings
   double *G;         // coarse grid [P][P][nch]
@@ -662,6 +663,8 @@ __global__ void coarse_query_self(Dom2S D, const int32_t *__restrict__ pos0,
                                   KdeP kp, double *__restrict__ accq) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < D.n;
        t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cu = pos1[t] >> LS;
+    if (cu < D.c_lo || cu >= D.c_hi) continue;  // another shard's query
     const int64_t c = flipp(pos1[t], D.f1, D.npad) >> LS, b = flipp(pos0[t], D.f0, D.npad) >> LS;
     if (c == 0 || b == 0) continue;
     double z = 1.0;
@@ -684,8 +687,10 @@ __global__ void __launch_bounds__(kSolverThreads) level2_self(Dom2S D) {
   int16_t *s_qy = s_kofx + S;                                     // [S] rank threshold by slot
 
   const GrpArrays &A = CHUNK ? D.gc : D.gb;
-  const int64_t cb = blockIdx.x;
   const int fslot = CHUNK ? D.f1 : D.f0;
+  // chunk kind: only the shard's chunks are launched; block kind: every block, but only the
+  // shard's queries (unflipped chunk of the rank-dimension position p1) are evaluated
+  const int64_t cb = blockIdx.x + (CHUNK ? (fslot ? D.P - D.c_hi : D.c_lo) : 0);
   const int frank = CHUNK ? D.f0 : D.f1;
   const int64_t g = fslot ? D.P - 1 - cb : cb;
   const int64_t lo = g * S;
@@ -738,10 +743,16 @@ __global__ void __launch_bounds__(kSolverThreads) level2_self(Dom2S D) {
   __syncthreads();
 
   // pass A, slot order: full sub-cells + the query's partial slot sub-range
+  const bool all_owned = CHUNK || (D.c_lo == 0 && D.c_hi == D.P);
+  auto owned = [&](int kk) {
+    if (all_owned) return true;
+    const int64_t cu = A.rankpos[lo + kk] >> LS;
+    return cu >= D.c_lo && cu < D.c_hi;
+  };
   for (int xb = warp * 32; xb < S; xb += nwarps * 32) {
     const int x = xb + lane;
     const int y = s_yofx[x];
-    const bool occ = y >= 0;
+    const bool occ = y >= 0 && (all_owned || owned(s_kofx[x]));
     int qy = 0, k = 0;
     if (occ) {
       k = s_kofx[x];
@@ -785,7 +796,7 @@ __global__ void __launch_bounds__(kSolverThreads) level2_self(Dom2S D) {
   // pass B, rank order (coalesced accumulators): the partial rank sub-range, full slot rows
   for (int yb = warp * 32; yb < Sg; yb += nwarps * 32) {
     const int y = yb + lane;
-    const bool ok = y < Sg;
+    const bool ok = y < Sg && (all_owned || owned(frank ? Sg - 1 - y : y));
     const int x = ok ? s_xofy[y] : 0;
     const int qy = ok ? (int)s_qy[x] : 0;
     const int xfull = (x >> SUBL) << SUBL;
@@ -823,9 +834,15 @@ __global__ void self_finish_kernel(int64_t n, int nw, const double *__restrict__
                                    const double *__restrict__ accc, const int32_t *__restrict__ invc,
                                    const double *__restrict__ accb, const int32_t *__restrict__ invb,
                                    const double *__restrict__ w, int add_w, double mult, double div,
-                                   double *__restrict__ out) {
+                                   double *__restrict__ out, const int32_t *__restrict__ pos1,
+                                   int64_t c_lo, int64_t c_hi) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cu = pos1[t] >> LS;
+    if (cu < c_lo || cu >= c_hi) {  // another shard's query: exact zero (sum-reduce gathers)
+      for (int v = 0; v < nw; ++v) out[v * n + t] = 0.0;
+      continue;
+    }
     const int64_t kc = invc[t], kb = invb[t];
     for (int v = 0; v < nw; ++v) {
       double r = accq[v * n + t] + accc[v * n + kc] + accb[v * n + kb];
@@ -1089,7 +1106,8 @@ void carve_self(Workspace &W, SelfWs &q, int64_t n, int nw) {
 // weighted by e^{-s} at the query).  out[v][t] = (sum + (add_w ? w : 0)) * mult / div.
 int self_dom2d(const double *x, const double *w, int64_t n, int nw, int kde, const double *h,
                const double *centre, int add_w, double mult, double div, PtsWs &p, SelfWs &q,
-               double *out, cudaStream_t st, const unsigned *smask = nullptr) {
+               double *out, cudaStream_t st, const unsigned *smask = nullptr, int shard = 0,
+               int nshards = 1) {
   FCG_TRY(prep2d(x, n, p, st));
   const int g = grid_for(n, 256);
   {
@@ -1117,6 +1135,10 @@ int self_dom2d(const double *x, const double *w, int64_t n, int nw, int kde, con
   D.gb = q.gb;
   D.G = p.G;
   const int64_t P = p.P;
+  // query shard: a contiguous range of chunks (points in p1 rank order)
+  D.c_lo = P * shard / nshards;
+  D.c_hi = P * (shard + 1) / nshards;
+  const unsigned nchunk = (unsigned)(D.c_hi - D.c_lo);
   const size_t sm = level2_self_smem(nw);
   if (nw == 1) {
     FCG_CUDA_TRY(cudaFuncSetAttribute(level2_self<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -1168,8 +1190,10 @@ int self_dom2d(const double *x, const double *w, int64_t n, int nw, int kde, con
     }
     {
       FCG_PROF("pts_level2_chunk", st);
-      if (nw == 1) level2_self<true, 1><<<(unsigned)P, kSolverThreads, sm, st>>>(D);
-      else level2_self<true, 2><<<(unsigned)P, kSolverThreads, sm, st>>>(D);
+      if (nchunk > 0) {
+        if (nw == 1) level2_self<true, 1><<<nchunk, kSolverThreads, sm, st>>>(D);
+        else level2_self<true, 2><<<nchunk, kSolverThreads, sm, st>>>(D);
+      }
       FCG_LAUNCH_CHECK();
     }
     {
@@ -1181,7 +1205,7 @@ int self_dom2d(const double *x, const double *w, int64_t n, int nw, int kde, con
   }
   FCG_PROF("pts_finish", st);
   self_finish_kernel<<<g, 256, 0, st>>>(n, nw, q.accq, q.gc.acc, q.gc.inv, q.gb.acc, q.gb.inv, w,
-                                       add_w, mult, div, out);
+                                       add_w, mult, div, out, p.r[1].pos, D.c_lo, D.c_hi);
   FCG_LAUNCH_CHECK();
   return FCG_OK;
 }
@@ -1657,4 +1681,53 @@ extern "C" int fcg_kde_points_matern32(const double *x, int64_t n, int32_t d, co
   matern_finish_kernel<<<grid_for(n, 256), 256, 0, st>>>(acc, x, n, w, f, out);
   FCG_LAUNCH_CHECK();
   return FCG_OK;
+}
+
+extern "C" int fcg_kde_points_laplacian_shard(const double *x, int64_t n, int32_t d,
+                                              const double *w, int32_t nw, const double *h,
+                                              const double *centre, int32_t shard,
+                                              int32_t nshards, double *out, void *ws,
+                                              size_t *ws_bytes, void *stream) {
+  FCG_TRY(check_pts(n, d));
+  if (d != 2) return fail(FCG_EUNSUPPORTED, "query sharding is implemented for d = 2");
+  if (nshards < 1 || shard < 0 || shard >= nshards) return fail(FCG_EINVAL, "shard out of range");
+  if (nw < 1 || nw > 2) return fail(FCG_EUNSUPPORTED, "nw must be 1 or 2 weight vectors per call");
+  if (!dom_fits(n, nw)) return dom_too_large(n);
+  Workspace W(ws);
+  PtsWs p;
+  carve(W, p, n, 2, nw, true, true, 0);
+  SelfWs q{};
+  carve_self(W, q, n, nw);
+  if (ws == nullptr) {
+    *ws_bytes = W.bytes();
+    return FCG_OK;
+  }
+  if (n == 0) return FCG_OK;
+  for (int k = 0; k < d; ++k)
+    if (!(h[k] > 0.0)) return fail(FCG_EINVAL, "bandwidth must be > 0");
+  const double scale = 1.0 / (4.0 * (double)n * h[0] * h[1]);
+  return self_dom2d(x, w, n, nw, 1, h, centre, 1, scale, 0.0, p, q, out, as_stream(stream),
+                    nullptr, shard, nshards);
+}
+
+extern "C" int fcg_dnc_ecdf_shard(const double *x, int64_t n, int32_t d, const double *w,
+                                  int32_t include_self, int32_t scaled, int32_t shard,
+                                  int32_t nshards, double *out, void *ws, size_t *ws_bytes,
+                                  void *stream) {
+  FCG_TRY(check_pts(n, d));
+  if (d != 2) return fail(FCG_EUNSUPPORTED, "query sharding is implemented for d = 2");
+  if (nshards < 1 || shard < 0 || shard >= nshards) return fail(FCG_EINVAL, "shard out of range");
+  if (!dom_fits(n, 1)) return dom_too_large(n);
+  Workspace W(ws);
+  PtsWs p;
+  carve(W, p, n, 2, 1, true, false, 0);
+  SelfWs q{};
+  carve_self(W, q, n, 1);
+  if (ws == nullptr) {
+    *ws_bytes = W.bytes();
+    return FCG_OK;
+  }
+  if (n == 0) return FCG_OK;
+  return self_dom2d(x, w, n, 1, 0, nullptr, nullptr, include_self, 0.0, scaled ? (double)n : 0.0,
+                    p, q, out, as_stream(stream), nullptr, shard, nshards);
 }

@@ -35,6 +35,7 @@ from . import _lib
 from .core import (
     EXP_OVERFLOW_GUARD,
     GRID_ALIGNED,
+    POINT_ALIGNED,
     Bandwidth,
     DeltaVector,
     EvalResult,
@@ -126,6 +127,27 @@ class DeviceEngine:
         _lib.call_ws("fcg_kde_carry_fixup", _lib.ptr(out), grid.dim, _lib.i64_array(grid.shape),
                      _lib.ptr(kn), _lib.f64_array(h), _lib.f64_array(centre), _lib.ptr(carries),
                      float(n_scale))
+        return out
+
+
+    # ---- at-points query shards (d = 2) ----------------------------------------------------
+    def kde_points_shard(self, x, wmat, nw, h, centre, shard, nshards):
+        import torch
+
+        n = x.shape[0]
+        out = torch.empty((nw, n), dtype=torch.float64, device=x.device)
+        _lib.call_ws("fcg_kde_points_laplacian_shard", _lib.ptr(x), n, 2, _lib.ptr(wmat), nw,
+                     _lib.f64_array(h), _lib.f64_array(centre), int(shard), int(nshards),
+                     _lib.ptr(out))
+        return out
+
+    def dnc_ecdf_shard(self, x, w, include_self, scaled, shard, nshards):
+        import torch
+
+        n = x.shape[0]
+        out = torch.empty(n, dtype=torch.float64, device=x.device)
+        _lib.call_ws("fcg_dnc_ecdf_shard", _lib.ptr(x), n, 2, _lib.ptr(w), int(include_self),
+                     int(scaled), int(shard), int(nshards), _lib.ptr(out))
         return out
 
 
@@ -281,3 +303,106 @@ def kde_fastsum_slab(sample: Sample, grid: RectilinearGrid, kernel, bandwidth: B
     out = eng.kde_fixup(out, sub, h, centre, carries, N)
     return EvalResult(out, GRID_ALIGNED, {"method": "fastsum-slab", "kernel": str(kernel),
                                           "slab": (lo, hi), "world": world})
+
+
+# ------------------------------------------------------------------------------------------
+# At-points queries, sharded (SURVEY 8e: "sample-point queries are sharded with the ranked data
+# replicated").  Every rank holds the whole sample; the device call ranks and groups all n
+# sources (replicated, no communication) and evaluates only the rank's queries: the points
+# whose dimension-1 rank falls in a contiguous 1/G slice of the 4096-point chunks.  Other
+# entries come back as exact zeros, so the optional final gather is one SUM all-reduce of the
+# owned values (computed by the single-GPU arithmetic).  The hot loop has no collective.
+
+def query_shard_chunks(n: int, shard: int, nshards: int, chunk: int = 4096) -> tuple[int, int]:
+    """[c_lo, c_hi): the dimension-1 rank chunks whose points shard `shard` evaluates."""
+    P = -(-n // chunk)
+    return P * shard // nshards, P * (shard + 1) // nshards
+
+
+def _shard_group(group):
+    dist = _dist()
+    return dist, dist.get_rank(group), dist.get_world_size(group)
+
+
+def _finish_points(out, dist, group, world, gather):
+    if gather and world > 1:
+        dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+    return out
+
+
+def kde_numerators_sharded(sample: Sample, weights_list, bandwidth: Bandwidth, group=None,
+                           engine=None, gather: bool = True):
+    """kde_numerators (Laplacian, d = 2) with the queries sharded over the ranks of `group`.
+    Returns the (nw, n) numerators: all of them when `gather`, else the rank's own entries
+    (zeros elsewhere).  Drop-in for points.kde_numerators on every rank."""
+    import torch
+
+    from .dnc import _diag_bandwidth, _require_distinct
+
+    sample = as_sample(sample)
+    if sample.dim != 2:
+        raise ParameterError("query sharding is implemented for d = 2")
+    _require_distinct(sample)
+    h = _diag_bandwidth(sample, bandwidth)
+    if not 1 <= len(weights_list) <= 2:
+        raise ParameterError("one or two weight vectors per pass")
+    dist, rank, world = _shard_group(group)
+    engine = engine or DeviceEngine()
+    x = engine.tensor(sample.points)
+    n = x.shape[0]
+    lo, hi = engine.minmax(x)  # overflow guard and data midrange (dnc.py:598-605, 656)
+    span = hi - lo
+    for k in range(2):
+        if span[k] / h[k] > EXP_OVERFLOW_GUARD:
+            raise OverflowGuardError(
+                f"dimension {k}: span/bandwidth = {span[k] / h[k]:.1f} exceeds "
+                f"{EXP_OVERFLOW_GUARD:.0f}; enlarge the bandwidth or rescale")
+    c = 0.5 * (lo + hi)
+    ws = [None if w is None else engine.tensor(w) for w in weights_list]
+    if any(w is None for w in ws):
+        ws = [torch.ones(n, dtype=torch.float64, device=x.device) if w is None else w for w in ws]
+    wmat = torch.stack(ws).contiguous()
+    out = engine.kde_points_shard(x, wmat, len(ws), h, c, rank, world)
+    out = _finish_points(out, dist, group, world, gather)
+    return out if sample.on_device else out.cpu().numpy()
+
+
+def kernel_regression_sharded(sample: Sample, y, kernel, bandwidth: Bandwidth, group=None,
+                              engine=None) -> EvalResult:
+    """points.kernel_regression with the queries sharded (both numerators in one pass per
+    rank, one SUM all-reduce, then the ratio)."""
+    if kernel.family != "laplacian":
+        raise ParameterError(f"kernel_regression supports the laplacian kernel, got {kernel.family!r}")
+    num = kde_numerators_sharded(sample, [y, None], bandwidth, group, engine)
+    return EvalResult(num[0] / num[1], POINT_ALIGNED, {"method": "dnc-nadaraya-watson-sharded",
+                                                  "kernel": str(kernel)})
+
+
+def kde_dnc_sharded(sample: Sample, kernel, bandwidth: Bandwidth, group=None,
+                    engine=None) -> EvalResult:
+    """dnc.kde_dnc (Laplacian, d = 2) with the queries sharded and gathered."""
+    if kernel.family != "laplacian":
+        raise ParameterError(f"kde_dnc_sharded supports the laplacian kernel, got {kernel.family!r}")
+    sample = as_sample(sample)
+    w = None if sample.unit_weights else sample.weights
+    vals = kde_numerators_sharded(sample, [w], bandwidth, group, engine)[0]
+    return EvalResult(vals, POINT_ALIGNED, {"method": "dnc-sharded", "kernel": str(kernel)})
+
+
+def ecdf_dnc_sharded(sample: Sample, include_self: bool = False, scaled: bool = True,
+                     group=None, engine=None, gather: bool = True) -> EvalResult:
+    """dnc.ecdf_dnc (d = 2) with the queries sharded over the ranks of `group`."""
+    from .dnc import _require_distinct
+
+    sample = as_sample(sample)
+    if sample.dim != 2:
+        raise ParameterError("query sharding is implemented for d = 2")
+    _require_distinct(sample)
+    dist, rank, world = _shard_group(group)
+    engine = engine or DeviceEngine()
+    x = engine.tensor(sample.points)
+    w = None if sample.unit_weights else engine.tensor(sample.weights)
+    out = engine.dnc_ecdf_shard(x, w, include_self, scaled, rank, world)
+    out = _finish_points(out, dist, group, world, gather)
+    return EvalResult(out if sample.on_device else out.cpu().numpy(), POINT_ALIGNED,
+                      {"method": "dnc-sharded", "scaled": scaled, "include_self": include_self})

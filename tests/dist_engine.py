@@ -92,3 +92,35 @@ class OracleEngine:
             acc += zfac * np.expand_dims(c, 1)
         scale = 1.0 / (2.0 ** d * n_scale * np.prod(h))
         return torch.as_tensor(out.numpy() + (acc * scale).reshape(-1))
+
+    # ---- at-points query shards: the oracle's full answer, zeros outside the shard's chunks
+    @staticmethod
+    def _owned(x, shard, nshards, chunk=4096):
+        from paper_2005_03246_b200.distributed import query_shard_chunks
+
+        n = x.shape[0]
+        pos1 = np.empty(n, dtype=np.int64)
+        pos1[np.argsort(x[:, 1], kind="stable")] = np.arange(n)
+        lo, hi = query_shard_chunks(n, shard, nshards, chunk)
+        c = pos1 // chunk
+        return (c >= lo) & (c < hi)
+
+    def minmax(self, x):
+        a = x.numpy()
+        return a.min(axis=0), a.max(axis=0)
+
+    def kde_points_shard(self, x, wmat, nw, h, centre, shard, nshards):
+        pts = x.numpy()
+        own = self._owned(pts, shard, nshards)
+        out = np.zeros((nw, pts.shape[0]))
+        for v in range(nw):
+            out[v] = oracle.kde_dnc_laplacian(pts, wmat[v].numpy(), h)
+        out[:, ~own] = 0.0
+        return torch.as_tensor(out)
+
+    def dnc_ecdf_shard(self, x, w, include_self, scaled, shard, nshards):
+        pts = x.numpy()
+        own = self._owned(pts, shard, nshards)
+        out = oracle.ecdf_dnc(pts, None if w is None else w.numpy(), include_self, scaled)
+        out = np.where(own, out, 0.0)
+        return torch.as_tensor(out)

@@ -109,3 +109,71 @@ def test_slab_bounds():
     assert b[0] == 0 and b[-1] == 129 and max(np.diff(b)) - min(np.diff(b)) <= 1
     with pytest.raises(fcb.ParameterError):
         fdist.slab_bounds(3, 4)
+
+
+# ---- at-points query sharding (replicated ranked data, sharded queries) -------
+
+def _points_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from dist_engine import OracleEngine
+
+        eng = OracleEngine()
+        rng = np.random.default_rng(5)
+        n = 9000  # 3 chunks of 4096: shards own 0..3 chunks each
+        x = rng.standard_normal((n, 2))
+        y = np.sin(3 * x[:, 0]) + rng.normal(0, 0.1, n)
+        s = fcb.validate_sample(x)
+        bw = fcb.Bandwidth.diag([0.3, 0.4])
+        res = {
+            "num": fdist.kde_numerators_sharded(s, [None, y], bw, engine=eng),
+            "own": fdist.kde_numerators_sharded(s, [None], bw, engine=eng, gather=False)[0],
+            "nw": fdist.kernel_regression_sharded(s, y, fcb.laplacian(), bw, engine=eng).values,
+            "ecdf": fdist.ecdf_dnc_sharded(fcb.validate_sample(x, np.abs(y)), engine=eng).values,
+        }
+        res = {k: np.asarray(v) for k, v in res.items()}
+        out = [None] * world
+        dist.all_gather_object(out, res)
+        if rank == 0:
+            q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_points_query_shards_match_single(world):
+    """The sharded at-points calls, gathered, equal the single-process oracle; each point is
+    evaluated by exactly one rank (the non-gathered outputs partition the queries)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_points_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(5)
+    n = 9000
+    x = rng.standard_normal((n, 2))
+    y = np.sin(3 * x[:, 0]) + rng.normal(0, 0.1, n)
+    dens = oracle.kde_dnc_laplacian(x, None, [0.3, 0.4])
+    reg = oracle.kde_dnc_laplacian(x, y, [0.3, 0.4])
+    for r in range(world):
+        np.testing.assert_array_equal(parts[r]["num"][0], dens)
+        np.testing.assert_array_equal(parts[r]["num"][1], reg)
+        np.testing.assert_array_equal(parts[r]["nw"], reg / dens)
+        np.testing.assert_array_equal(parts[r]["ecdf"], oracle.ecdf_dnc(x, np.abs(y)))
+    owned = np.stack([parts[r]["own"] != 0 for r in range(world)])
+    assert np.all(owned.sum(axis=0) == 1)  # densities are > 0: ownership is a partition
+    np.testing.assert_array_equal(sum(parts[r]["own"] for r in range(world)), dens)
+
+
+def test_query_shard_chunks_partition():
+    for n in (1, 4095, 4096, 9000, 10_000_000):
+        for G in (1, 2, 3, 8):
+            spans = [fdist.query_shard_chunks(n, s, G) for s in range(G)]
+            assert spans[0][0] == 0 and spans[-1][1] == -(-n // 4096)
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))

@@ -76,3 +76,44 @@ def test_slab_pipeline_on_device_matches_single_gpu(case, world, monkeypatch):
                              scaled=False).values
     e_ref = np.asarray(e_ref.cpu() if hasattr(e_ref, "cpu") else e_ref).reshape(shape)
     np.testing.assert_array_equal(_assemble(parts, 2, shape), e_ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_points_query_shards_on_device(world, monkeypatch):
+    """At-points query sharding with the device kernels: each thread-rank evaluates its chunks
+    of the dimension-1 rank order, the SUM gather reproduces the single-GPU numerators, the
+    Nadaraya-Watson ratio and the strict-dominance ECDF bit for bit."""
+    import torch
+    import workloads as wl
+
+    td = ThreadDist(world)
+    monkeypatch.setattr(fdist, "_dist", lambda: td)
+    w = wl.cfg4(1_000_000)
+    y = w.extra["y"]
+    bw = fcb.Bandwidth.diag(w.h)
+    s = fcb.validate_sample(w.points)
+    sy = fcb.validate_sample(w.points, np.abs(y))
+
+    def rank_fn(r):
+        torch.cuda.set_device(0)
+        num = fdist.kde_numerators_sharded(s, [None, y], bw)
+        own = fdist.kde_numerators_sharded(s, [None], bw, gather=False)[0]
+        nw = fdist.kernel_regression_sharded(s, y, fcb.laplacian(), bw).values
+        ec = fdist.ecdf_dnc_sharded(sy).values
+        return num, own, nw, ec
+
+    parts = td.run(rank_fn)
+    ref = fcb.kde_numerators(s, [None, y], bw)
+    scale = fcb.kde_numerators(s, [None, np.abs(y)], bw)  # |y|-weighted scale for the numerator
+    ref_ec = fcb.ecdf_dnc(sy).values
+    # the coarse histograms sum in shared-memory atomics (run-to-run order), so repeated calls
+    # agree to rounding, not bitwise
+    for num, _, nw, ec in parts:
+        assert np.max(np.abs(num[0] - ref[0]) / scale[0]) <= 1e-12
+        assert np.max(np.abs(num[1] - ref[1]) / scale[1]) <= 1e-12
+        assert np.max(np.abs(nw - ref[1] / ref[0]) * ref[0] / scale[1]) <= 1e-11
+        assert np.max(np.abs(ec - ref_ec) / ref_ec.max()) <= 1e-12
+    owned = np.stack([p[1] != 0 for p in parts])
+    assert np.all(owned.sum(axis=0) == 1)
+    assert np.max(np.abs(sum(p[1] for p in parts) - ref[0]) / ref[0]) <= 1e-12
