@@ -98,12 +98,19 @@ def load_library(path: Path | str | None = None, require_all: bool = True):
         return lib
 
 
+_torch_ok = None
+
+
 def _torch():
+    global _torch_ok
+    if _torch_ok is not None:
+        return _torch_ok
     import torch
 
     if not torch.cuda.is_available():
         raise RuntimeError("paper_2005_03246_b200 needs a CUDA device (B200, sm_100a); "
                            "there is no CPU fallback")
+    _torch_ok = torch
     return torch
 
 
@@ -133,15 +140,33 @@ def check(rc: int, name: str):
 
 
 def call_ws(name: str, *args):
-    """Two-phase workspace call: size query, torch allocation, real call on current stream."""
+    """Two-phase workspace call: size query, torch allocation (the caching allocator, so the
+    buffer is stream-ordered), real call on the current stream."""
     torch = _torch()
-    lib = load_library()
+    lib = _lib if _lib is not None else load_library()
     fn = getattr(lib, name)
+    stream = torch.cuda.current_stream()
+    sh = C.c_void_p(stream.cuda_stream)
     nbytes = C.c_size_t(0)
-    check(fn(*args, None, C.byref(nbytes), stream_handle()), name)
-    ws = torch.empty(max(int(nbytes.value), 1), dtype=torch.uint8, device=device())
-    check(fn(*args, C.c_void_p(ws.data_ptr()), C.byref(nbytes), stream_handle()), name)
+    check(fn(*args, None, C.byref(nbytes), sh), name)
+    need = max(int(nbytes.value), 1)
+    key = (threading.get_ident(), stream.cuda_stream)
+    ws = _ws_cache.get(key)
+    if ws is None or ws.numel() < need or ws.device != stream.device:
+        ws = torch.empty(need, dtype=torch.uint8, device=stream.device)
+        if need <= _WS_CACHE_MAX:
+            _ws_cache[key] = ws
+    check(fn(*args, C.c_void_p(ws.data_ptr()), C.byref(nbytes), sh), name)
     return ws
+
+
+# Small workspaces are reused per (host thread, stream): one thread's calls on one stream are
+# issued in order, so the next call's kernels only touch the scratch after the previous call's
+# kernels are done (threads sharing a stream get separate buffers); launch-bound
+# configurations otherwise pay an allocator round trip per call.  Large ones go back to torch's
+# caching allocator so the memory stays available to other tensors.
+_ws_cache: dict = {}
+_WS_CACHE_MAX = 64 << 20
 
 
 def i64_array(vals) -> C.Array:

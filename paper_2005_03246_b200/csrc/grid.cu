@@ -18,6 +18,10 @@
 // pipelines therefore scatter into an exactly prod(M_k)-cell lattice (cell = b - shift_k,
 // points falling in the dead layer are skipped) and the final scan pass writes the output in
 // place of the reference's slice + copy.
+#include <cooperative_groups.h>
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "scan.cuh"
 #include "bin.cuh"
@@ -92,6 +96,159 @@ __global__ void __launch_bounds__(256, 4) bin_scatter_kernel(const double *__res
       atomicAdd(reinterpret_cast<double *>(lat) + flat, v);
     }
   }
+}
+
+// ---- one-launch pipeline for small 2-D lattices (BASELINE config 1: 256 x 256) ------------
+// Launch-bound sizes spend more in launch gaps than in work (five kernels of a few microseconds
+// each).  One cooperative kernel runs the whole ecdf_fastsum pipeline with grid-wide barriers:
+// zero the lattice, bin + scatter (global atomics into an L2-resident lattice), scan every row
+// along axis 1 (warp per row, shuffles), then the axis-0 pass as kSmallChunks row chunks:
+// per-(chunk, column) totals, and each (chunk, column) thread adds the totals of the chunks
+// before it (in scan order) and walks its rows writing the epilogue (count / N or int64).
+constexpr int kSmallThreads = 256;
+constexpr int kSmallChunks = 16;
+constexpr int64_t kSmallCells = int64_t(1) << 20;
+
+template <typename T, int EK>
+__global__ void __launch_bounds__(kSmallThreads, 4) small2d_kernel(
+    const double *__restrict__ x, int64_t n, const double *__restrict__ w,
+    const double *__restrict__ knots, BinGrid g, int rev0, int rev1, T *__restrict__ lat,
+    T *__restrict__ csum, Epi e) {
+  namespace cg = cooperative_groups;
+  extern __shared__ double s_knots[];
+  __shared__ double s_z0[FCG_MAX_DIM], s_idz[FCG_MAX_DIM];
+  const double *kb = stage_knots(g, knots, s_knots, s_z0, s_idz);
+  // 32-bit indexing: the lattice has <= kSmallCells cells
+  const int m0 = (int)g.dims[0], m1 = (int)g.dims[1], L = m0 * m1;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  for (int i = tid; i < L; i += nth) lat[i] = T(0);
+  __syncthreads();
+  cg::this_grid().sync();
+  {
+    const double *k0 = kb + g.koff[0], *k1 = kb + g.koff[1];
+    const int M0 = (int)g.m[0], M1 = (int)g.m[1], le0 = g.le[0], le1 = g.le[1];
+    const int sh0 = (int)g.shift[0], sh1 = (int)g.shift[1];
+    const double z00 = s_z0[0], z01 = s_z0[1], i00 = s_idz[0], i01 = s_idz[1];
+    for (int64_t i = tid; i < n; i += nth) {
+      const double2 v = reinterpret_cast<const double2 *>(x)[i];
+      const int c0 = knot_count(v.x, k0, M0, le0, z00, i00) - sh0;
+      const int c1 = knot_count(v.y, k1, M1, le1, z01, i01) - sh1;
+      if (c0 < 0 || c0 >= m0 || c1 < 0 || c1 >= m1) continue;
+      if constexpr (sizeof(T) == 4) atomicAdd(reinterpret_cast<int *>(lat) + c0 * m1 + c1, 1);
+      else atomicAdd(reinterpret_cast<double *>(lat) + c0 * m1 + c1, w[i]);
+    }
+  }
+  cg::this_grid().sync();
+  {  // axis 1: warp per row; rows of <= 256 columns load all 8 segments first (one round trip)
+    const int lane = threadIdx.x & 31;
+    for (int r = tid >> 5; r < m0; r += nth >> 5) {
+      T *row = lat + r * m1;
+      if (m1 <= 256) {
+        T v[8];
+#pragma unroll
+        for (int sg = 0; sg < 8; ++sg) {
+          const int jj = sg * 32 + lane;
+          v[sg] = jj < m1 ? row[rev1 ? m1 - 1 - jj : jj] : T(0);
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+          for (int sg = 0; sg < 8; ++sg) {
+            const T u = __shfl_up_sync(0xffffffffu, v[sg], o);
+            if (lane >= o) v[sg] += u;
+          }
+        }
+        T carry = T(0);
+#pragma unroll
+        for (int sg = 0; sg < 8; ++sg) {
+          v[sg] += carry;
+          carry = __shfl_sync(0xffffffffu, v[sg], 31);
+          const int jj = sg * 32 + lane;
+          if (jj < m1) row[rev1 ? m1 - 1 - jj : jj] = v[sg];
+        }
+        continue;
+      }
+      T carry = T(0);
+      for (int j0 = 0; j0 < m1; j0 += 32) {
+        const int j = rev1 ? m1 - 1 - (j0 + lane) : j0 + lane;
+        const bool in = j0 + lane < m1;
+        T v = in ? row[j] : T(0);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const T u = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= o) v += u;
+        }
+        v += carry;
+        if (in) row[j] = v;
+        carry = __shfl_sync(0xffffffffu, v, 31);
+      }
+    }
+  }
+  cg::this_grid().sync();
+  // axis 0: C chunks of Dc rows; loops of fixed trip count with independent loads
+  const int C = m0 < kSmallChunks ? m0 : kSmallChunks;
+  const int Dc = (m0 + C - 1) / C;
+  for (int t = tid; t < C * m1; t += nth) {  // chunk totals along axis 0
+    const int c = t / m1, col = t - c * m1;
+    const int a = c * Dc, b = a + Dc < m0 ? a + Dc : m0;
+    T s = T(0);
+#pragma unroll 16
+    for (int r = a; r < b; ++r) s += lat[r * m1 + col];
+    csum[t] = s;
+  }
+  cg::this_grid().sync();
+  double *of = static_cast<double *>(e.out);
+  int64_t *oi = static_cast<int64_t *>(e.out);
+  const double div = e.div;
+  for (int t = tid; t < C * m1; t += nth) {  // carry-in + walk (scan order) + epilogue
+    const int c = t / m1, col = t - c * m1;
+    T run = T(0);
+#pragma unroll
+    for (int q = 0; q < kSmallChunks; ++q)
+      if (q < C && (rev0 ? q > c : q < c)) run += csum[q * m1 + col];
+    const int a = c * Dc, b = a + Dc < m0 ? a + Dc : m0;
+#pragma unroll 16
+    for (int k = 0; k < b - a; ++k) {
+      const int f = (rev0 ? b - 1 - k : a + k) * m1 + col;
+      run += lat[f];
+      if constexpr (EK == EPI_F64) {
+        double v = (double)run;
+        if (div > 0.0) v = v / div;
+        of[f] = v;
+      } else {
+        oi[f] = (int64_t)run;
+      }
+    }
+  }
+}
+
+template <typename T, int EK>
+int launch_small2d(const double *x, int64_t n, const double *w, const double *knots,
+                   const BinGrid &g, bool rev0, bool rev1, T *lat, T *csum, const Epi &e,
+                   cudaStream_t st) {
+  auto kern = small2d_kernel<T, EK>;
+  const size_t smem = g.total_knots <= kSmemKnots ? (size_t)g.total_knots * sizeof(double) : 0;
+  // residency of the cooperative grid (a per-instantiation constant: knots <= kSmemKnots use
+  // at most 32 KB of shared memory, so the 32 KB figure bounds every launch)
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    int v = 0;
+    FCG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, kSmallThreads,
+                                                               kSmemKnots * sizeof(double)));
+    per_sm = v;
+  }
+  if (per_sm < 1) return fail(FCG_ECUDA, "small2d kernel cannot be resident");
+  const int64_t L = g.dims[0] * g.dims[1];
+  const int64_t work = std::max<int64_t>(std::max<int64_t>(n, L / 4), 1);
+  int64_t blocks = std::min<int64_t>(ceil_div(work, kSmallThreads), (int64_t)per_sm * sm_count());
+  blocks = std::max<int64_t>(blocks, 1);
+  int r0 = rev0 ? 1 : 0, r1 = rev1 ? 1 : 0;
+  void *args[] = {(void *)&x, (void *)&n, (void *)&w, (void *)&knots, (void *)&g, (void *)&r0,
+                  (void *)&r1, (void *)&lat, (void *)&csum, (void *)&e};
+  FCG_PROF(sizeof(T) == 4 ? "small2d_count" : "small2d_w", st);
+  FCG_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)kern, dim3((unsigned)blocks),
+                                           dim3(kSmallThreads), args, smem, st));
+  return FCG_OK;
 }
 
 template <int WK, typename T>
@@ -353,9 +510,26 @@ extern "C" int fcg_ecdf_grid(const double *x, int64_t n, int32_t d, const double
   }
   void *lat = W.take<char>((size_t)L * esz);
   void *scratch = W.take<char>((size_t)scan_scratch_elems(s) * esz);
+  // small 2-D lattices: the whole pipeline in one cooperative launch
+  const bool small = d == 2 && L <= kSmallCells && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                     !(getenv("FCG_SMALL2D") && getenv("FCG_SMALL2D")[0] == '0');
+  void *csum = small ? W.take<char>((size_t)kSmallChunks * m[1] * esz) : nullptr;
   if (ws == nullptr) {
     *ws_bytes = W.bytes();
     return FCG_OK;
+  }
+  if (small) {
+    if (unit)
+      return e.kind == EPI_I64
+                 ? launch_small2d<int32_t, EPI_I64>(x, n, w, knots, g, rev[0], rev[1],
+                                                    static_cast<int32_t *>(lat),
+                                                    static_cast<int32_t *>(csum), e, st)
+                 : launch_small2d<int32_t, EPI_F64>(x, n, w, knots, g, rev[0], rev[1],
+                                                    static_cast<int32_t *>(lat),
+                                                    static_cast<int32_t *>(csum), e, st);
+    return launch_small2d<double, EPI_F64>(x, n, w, knots, g, rev[0], rev[1],
+                                           static_cast<double *>(lat), static_cast<double *>(csum),
+                                           e, st);
   }
   PsiParams pp{};
   {
