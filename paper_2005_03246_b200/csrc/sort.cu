@@ -50,45 +50,6 @@ __device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t *s_warp, i
   return warp_excl + x - v;
 }
 
-__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const int32_t *__restrict__ in,
-                                                                   int64_t n,
-                                                                   int32_t *__restrict__ partial) {
-  __shared__ int32_t s_warp[32];
-  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
-  int32_t s = 0;
-#pragma unroll
-  for (int j = 0; j < kScanItems; ++j)
-    if (base + j < n) s += in[base + j];
-  int32_t tot;
-  block_excl_scan(s, s_warp, &tot);
-  if (threadIdx.x == 0) partial[blockIdx.x] = tot;
-}
-
-// single CTA: exclusive scan of partial[0..np) in place
-__global__ void __launch_bounds__(kScanThreads) scan_partials_kernel(int32_t *partial, int64_t np) {
-  __shared__ int32_t s_warp[32];
-  int32_t carry = 0;
-  for (int64_t b0 = 0; b0 < np; b0 += kScanTile) {
-    const int64_t base = b0 + (int64_t)threadIdx.x * kScanItems;
-    int32_t v[kScanItems];
-    int32_t s = 0;
-#pragma unroll
-    for (int j = 0; j < kScanItems; ++j) {
-      v[j] = (base + j < np) ? partial[base + j] : 0;
-      s += v[j];
-    }
-    int32_t tot;
-    int32_t run = block_excl_scan(s, s_warp, &tot) + carry;
-#pragma unroll
-    for (int j = 0; j < kScanItems; ++j) {
-      if (base + j < np) partial[base + j] = run;
-      run += v[j];
-    }
-    carry += tot;
-    __syncthreads();
-  }
-}
-
 // single CTA, whole array (small scans: one launch instead of three)
 __global__ void __launch_bounds__(kScanThreads) scan_single_kernel(const int32_t *in, int32_t *out,
                                                                    int64_t n, int inclusive) {
@@ -115,25 +76,99 @@ __global__ void __launch_bounds__(kScanThreads) scan_single_kernel(const int32_t
   }
 }
 
-__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const int32_t *in, int32_t *out,
-                                                                  int64_t n,
-                                                                  const int32_t *__restrict__ partial,
-                                                                  int inclusive) {
+// ---- single-pass scan with decoupled look-back ------------------------------------------
+// One launch per scan (plus a memset of the tile status words): tile t publishes its aggregate
+// (flag 1), then its inclusive prefix (flag 2) as soon as the look-back over its predecessors
+// (a warp reading 32 status words at a time) has found one.  Tiles are taken in blockIdx order
+// (lower tiles are dispatched first, so every tile waited on is resident or done).
+constexpr int kLbThreads = 512;
+constexpr int kLbItems = 8;
+constexpr int kLbTile = kLbThreads * kLbItems;
+
+__device__ __forceinline__ void lb_publish(unsigned long long *p, unsigned flag, int32_t v) {
+  const unsigned long long w = ((unsigned long long)flag << 32) | (uint32_t)v;
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ unsigned long long lb_read(const unsigned long long *p) {
+  unsigned long long w;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  return w;
+}
+
+__global__ void __launch_bounds__(kLbThreads) scan_lookback_kernel(
+    const int32_t *in, int32_t *out, int64_t n, int inclusive, unsigned long long *status) {
   __shared__ int32_t s_warp[32];
-  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
-  int32_t v[kScanItems];
-  int32_t s = 0;
+  __shared__ int32_t s_prefix;
+  const int64_t tile = blockIdx.x;
+  const int64_t base = tile * kLbTile + (int64_t)threadIdx.x * kLbItems;
+  int32_t v[kLbItems];
+  int32_t sum = 0;
+  if (base + kLbItems <= n && (reinterpret_cast<uintptr_t>(in + base) & 15) == 0) {
+    const int4 a = reinterpret_cast<const int4 *>(in + base)[0];
+    const int4 b = reinterpret_cast<const int4 *>(in + base)[1];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
 #pragma unroll
-  for (int j = 0; j < kScanItems; ++j) {
-    v[j] = (base + j < n) ? in[base + j] : 0;
-    s += v[j];
+    for (int j = 0; j < kLbItems; ++j) v[j] = base + j < n ? in[base + j] : 0;
   }
-  int32_t tot;
-  int32_t run = block_excl_scan(s, s_warp, &tot) + partial[blockIdx.x];
 #pragma unroll
-  for (int j = 0; j < kScanItems; ++j) {
-    if (base + j < n) out[base + j] = inclusive ? run + v[j] : run;
+  for (int j = 0; j < kLbItems; ++j) sum += v[j];
+  int32_t agg;
+  const int32_t excl = block_excl_scan(sum, s_warp, &agg);
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int32_t prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) lb_publish(status, 2u, agg);
+    } else {
+      if (lane == 0) lb_publish(status + tile, 1u, agg);
+      int64_t idx = tile - 1;
+      while (true) {
+        const int64_t j = idx - lane;
+        unsigned long long w = 0;
+        unsigned flag = 2;  // before tile 0: an inclusive 0
+        if (j >= 0) {
+          do {
+            w = lb_read(status + j);
+            flag = (unsigned)(w >> 32);
+          } while (flag == 0);
+        }
+        const int32_t val = j >= 0 ? (int32_t)(uint32_t)w : 0;
+        const unsigned inc = __ballot_sync(0xffffffffu, flag == 2);
+        if (inc) {
+          const int first = __ffs(inc) - 1;  // nearest predecessor with its inclusive prefix
+          int32_t x = lane <= first ? val : 0;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+          prefix += x;
+          break;
+        }
+        int32_t x = val;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        prefix += x;
+        idx -= 32;
+      }
+      if (lane == 0) lb_publish(status + tile, 2u, prefix + agg);
+    }
+    if (lane == 0) s_prefix = prefix;
+  }
+  __syncthreads();
+  int32_t run = s_prefix + excl;
+#pragma unroll
+  for (int j = 0; j < kLbItems; ++j) {
+    const int32_t o = inclusive ? run + v[j] : run;
     run += v[j];
+    v[j] = o;
+  }
+  if (base + kLbItems <= n && (reinterpret_cast<uintptr_t>(out + base) & 15) == 0) {
+    reinterpret_cast<int4 *>(out + base)[0] = make_int4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<int4 *>(out + base)[1] = make_int4(v[4], v[5], v[6], v[7]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kLbItems; ++j)
+      if (base + j < n) out[base + j] = v[j];
   }
 }
 
@@ -449,7 +484,8 @@ __global__ void __launch_bounds__(kSortSegs) seg_tiles_kernel(const int32_t *__r
 
 size_t radix_ws_hist_elems(int64_t n) { return (size_t)256 * (size_t)ceil_div(n, kSortTile) + 1; }
 
-size_t scan_ws_partial_elems(int64_t n) { return (size_t)ceil_div(n, kScanTile) + 1; }
+// int32 elements: the single-pass scan's 64-bit status word per kLbTile tile (+ alignment slack)
+size_t scan_ws_partial_elems(int64_t n) { return 2 * (size_t)ceil_div(n, kLbTile) + 4; }
 
 int scan_i32(const int32_t *in, int32_t *out, int64_t n, bool inclusive, int32_t *partial,
              cudaStream_t st) {
@@ -461,11 +497,13 @@ int scan_i32(const int32_t *in, int32_t *out, int64_t n, bool inclusive, int32_t
     FCG_LAUNCH_CHECK();
     return FCG_OK;
   }
-  scan_reduce_kernel<<<(unsigned)blocks, kScanThreads, 0, st>>>(in, n, partial);
-  FCG_LAUNCH_CHECK();
-  scan_partials_kernel<<<1, kScanThreads, 0, st>>>(partial, blocks);
-  FCG_LAUNCH_CHECK();
-  scan_apply_kernel<<<(unsigned)blocks, kScanThreads, 0, st>>>(in, out, n, partial, inclusive);
+  // single pass: status words live in the partials buffer (sized for kScanTile tiles of 32-bit
+  // words, i.e. room for as many 64-bit words as kLbTile = kScanTile / 2 tiles need)
+  const int64_t tiles = ceil_div(n, kLbTile);
+  unsigned long long *status = reinterpret_cast<unsigned long long *>(partial);
+  FCG_CUDA_TRY(cudaMemsetAsync(status, 0, (size_t)tiles * sizeof(unsigned long long), st));
+  scan_lookback_kernel<<<(unsigned)tiles, kLbThreads, 0, st>>>(in, out, n, inclusive ? 1 : 0,
+                                                              status);
   FCG_LAUNCH_CHECK();
   return FCG_OK;
 }

@@ -27,7 +27,7 @@ SCOPES = [(r"^ecdf_final2d", "scan_lines_final"), (r"^final2d", "kde_final_group
           (r"^part_bin", "part_bin"), (r"^plane_count", "plane_count"),
           (r"^bin_scatter_kernel", "bin_scatter_count"), (r"^level2_self<0", "pts_level2_block"),
           (r"^level2_self<1", "pts_level2_chunk"), (r"^group_gather", "pts_group_gather"),
-          (r"^group_psi", "pts_psi"), (r"^scan_(apply|reduce|partials)", "scan_i32"),
+          (r"^group_psi", "pts_psi"), (r"^scan_(lookback|single)", "scan_i32"),
           (r"^minmax", "minmax")]
 
 
