@@ -583,10 +583,9 @@ class PointsWorkload:
 
     def _run(self, s, y):
         fcb = self.fcb
-        if self.name == "cfg2":
-            a = fcb.ecdf_at_points(s, fcb.DeltaVector(self.w.delta)).values
-            b = fcb.esf_at_points(s).values
-            return a, b
+        if self.name == "cfg2":  # both outputs from one ranking of the points
+            a, b = fcb.ecdf_esf_at_points(s, fcb.DeltaVector(self.w.delta))
+            return a.values, b.values
         if self.world > 1:
             from paper_2005_03246_b200 import distributed as fdist
 

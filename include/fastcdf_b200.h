@@ -213,6 +213,13 @@ int fcg_ecdf_points(const double *x, int64_t n, int32_t d, const double *w,
                     const int32_t *delta, int32_t survival, int32_t scaled, double *out,
                     void *ws, size_t *ws_bytes, void *stream);
 
+/* Both at-points outputs of BASELINE config 2 from one ranking of every dimension:
+ * out_ecdf as fcg_ecdf_points(delta, survival = 0) and out_esf as fcg_ecdf_points(survival = 1)
+ * (naive.py:90-114, 210-217).  One host sync (the distinct-level counts). */
+int fcg_ecdf_esf_points(const double *x, int64_t n, int32_t d, const double *w,
+                        const int32_t *delta, int32_t scaled, double *out_ecdf, double *out_esf,
+                        void *ws, size_t *ws_bytes, void *stream);
+
 /* Strict-dominance ECDF at the sample points (requires pairwise-distinct coordinates per
  * dimension, checked by the caller): out[j] = sum_{i != j, x_i < x_j in every dim} w_i,
  * + w_j when include_self, / n when scaled.  Replaces dnc.py:531-561 ecdf_dnc. */

@@ -50,7 +50,14 @@ from .kernels import (
 )
 
 from .dnc import ecdf_dnc, kde_dnc
-from .points import ecdf_at_points, esf_at_points, kde_numerators, kernel_regression, rank_f64
+from .points import (
+    ecdf_at_points,
+    ecdf_esf_at_points,
+    esf_at_points,
+    kde_numerators,
+    kernel_regression,
+    rank_f64,
+)
 from .interp import multilinear_interp
 
 __version__ = "0.1.0"

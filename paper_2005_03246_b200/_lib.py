@@ -51,6 +51,7 @@ _SIGS = {
     "fcg_rank_f64": ([_P, _I64, _I64, _P, _P, _P, _P, _P, _P, _SZP, _P], C.c_int),
     "fcg_distinct": ([_P, _I64, _I32, _P, _P, _SZP, _P], C.c_int),
     "fcg_ecdf_points": ([_P, _I64, _I32, _P, _P, _I32, _I32, _P, _P, _SZP, _P], C.c_int),
+    "fcg_ecdf_esf_points": ([_P, _I64, _I32, _P, _P, _I32, _P, _P, _P, _SZP, _P], C.c_int),
     "fcg_dnc_ecdf": ([_P, _I64, _I32, _P, _I32, _I32, _P, _P, _SZP, _P], C.c_int),
     "fcg_kde_points_laplacian": ([_P, _I64, _I32, _P, _I32, _P, _P, _P, _P, _SZP, _P], C.c_int),
     "fcg_kde_points_matern32": ([_P, _I64, _I32, _P, _P, _P, _P, _P, _SZP, _P], C.c_int),

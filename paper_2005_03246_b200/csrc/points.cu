@@ -923,10 +923,13 @@ void carve(Workspace &W, PtsWs &p, int64_t n, int d, int nch, bool need_dom, boo
   if (need_kde) p.expo = W.take<double>(n);
 }
 
-// ties = false: only the order and the positions (distinct coordinates, the self path)
-int rank_dim(const double *x, int64_t n, int d, int k, PtsWs &p, cudaStream_t st, bool ties = true) {
+// ties = false: only the order and the positions (distinct coordinates, the self path).
+// mask: the dimension's digit mask (radix_digit_masks_f64), or ~0u to compute it here (syncs).
+int rank_dim(const double *x, int64_t n, int d, int k, PtsWs &p, cudaStream_t st, bool ties = true,
+             uint32_t mask = ~0u) {
   FCG_TRY(radix_init_f64(x + k, n, d, p.k, p.v, st));
-  FCG_TRY(radix_sort_pairs_pruned(p.k, p.v, n, p.rw, st));
+  if (mask == ~0u) FCG_TRY(radix_sort_pairs_pruned(p.k, p.v, n, p.rw, st));
+  else FCG_TRY(radix_sort_pairs_mask(p.k, p.v, n, mask, p.rw, st));
   FCG_CUDA_TRY(cudaMemcpyAsync(p.r[k].order, p.v, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
   if (!ties)
     return rank_outputs(p.k, p.v, n, p.r[k].pos, nullptr, nullptr, nullptr, p.heads, p.start,
@@ -1052,9 +1055,17 @@ int dom2d(PtsWs &p, int64_t n, int nch, int f0, int f1, const double *psi, doubl
   return FCG_OK;
 }
 
+// every dimension's ranking after one digit-mask read-back for all of them
+int rank_all(const double *x, int64_t n, int d, PtsWs &p, cudaStream_t st, bool ties = true) {
+  uint32_t masks[FCG_MAX_DIM];
+  FCG_TRY(radix_digit_masks_f64(x, n, d, reinterpret_cast<unsigned long long *>(p.rw.hist),
+                                masks, st));
+  for (int k = 0; k < d; ++k) FCG_TRY(rank_dim(x, n, d, k, p, st, ties, masks[k]));
+  return FCG_OK;
+}
+
 int prep2d(const double *x, int64_t n, PtsWs &p, cudaStream_t st) {
-  FCG_TRY(rank_dim(x, n, 2, 0, p, st, false));
-  FCG_TRY(rank_dim(x, n, 2, 1, p, st, false));
+  FCG_TRY(rank_all(x, n, 2, p, st, false));
   FCG_TRY(group_by(p.r[0].order, p.r[1].pos, n, p.P, p.bychunk, p, st));
   FCG_TRY(group_by(p.r[1].order, p.r[0].pos, n, p.P, p.byblock, p, st));
   return FCG_OK;
@@ -1271,13 +1282,25 @@ extern "C" int fcg_distinct(const double *x, int64_t n, int32_t d, int32_t *flag
   return FCG_OK;
 }
 
-extern "C" int fcg_ecdf_points(const double *x, int64_t n, int32_t d, const double *w,
-                               const int32_t *delta, int32_t survival, int32_t scaled,
-                               double *out, void *ws, size_t *ws_bytes, void *stream) {
+namespace fcg {
+namespace {
+// One at-points request: out[j] = sum_i w_i prod_k [x_ik <= / < x_jk] (delta) or, survival,
+// prod_k [x_ik > x_jk]; divided by n when scaled.
+struct PtsReq {
+  const int32_t *delta;
+  int survival;
+  double *out;
+};
+
+// Requests sharing one ranking of every dimension (the expensive part at BASELINE config 2).
+int ecdf_points_multi(const double *x, int64_t n, int d, const double *w, int scaled,
+                      const PtsReq *req, int nreq, void *ws, size_t *ws_bytes, cudaStream_t st) {
   FCG_TRY(check_pts(n, d));
-  if (!survival)
-    for (int k = 0; k < d; ++k)
-      if (delta[k] != 1 && delta[k] != -1) return fail(FCG_EINVAL, "delta entries must be -1 or +1");
+  for (int q = 0; q < nreq; ++q)
+    if (!req[q].survival)
+      for (int k = 0; k < d; ++k)
+        if (req[q].delta[k] != 1 && req[q].delta[k] != -1)
+          return fail(FCG_EINVAL, "delta entries must be -1 or +1");
   // Workspace is sized for the worst case of the routes chosen at run time.
   const bool dom_ok = (d == 2 && dom_fits(n, 1));
   const int64_t budget = lattice_budget(n);
@@ -1289,7 +1312,6 @@ extern "C" int fcg_ecdf_points(const double *x, int64_t n, int32_t d, const doub
     return FCG_OK;
   }
   if (n == 0) return FCG_OK;
-  cudaStream_t st = as_stream(stream);
   const double div = scaled ? (double)n : 0.0;
 
   if (d == 1) {  // sort, prefix (or suffix) scan of sorted weights, gather
@@ -1299,116 +1321,150 @@ extern "C" int fcg_ecdf_points(const double *x, int64_t n, int32_t d, const doub
       gather_sorted_w<<<grid_for(n, 256), 256, 0, st>>>(p.r[0].order, w, n, p.lat);
       FCG_LAUNCH_CHECK();
     }
-    LatShape s1;
-    s1.d = 1;
-    s1.dims[0] = n;
-    Epi inplace;
-    const bool rev = survival != 0;
-    FCG_TRY(scan_axis<double>(p.lat, s1, 0, rev, inplace, p.scratch, st));
-    const int32_t *q = survival ? p.r[0].upper : (delta[0] > 0 ? p.r[0].upper : p.r[0].lower);
-    {
-      FCG_PROF("pts_gather", st);
-      gather1d_kernel<<<grid_for(n, 256), 256, 0, st>>>(p.lat, q, n, survival ? 1 : 0, out);
-      FCG_LAUNCH_CHECK();
-    }
-    {
+    // both scan directions may be requested: the prefix first, the suffix from a fresh copy
+    for (int q = 0; q < nreq; ++q) {
+      const bool rev = req[q].survival != 0;
+      if (q > 0) {
+        FCG_PROF("pts_sorted_w", st);
+        gather_sorted_w<<<grid_for(n, 256), 256, 0, st>>>(p.r[0].order, w, n, p.lat);
+        FCG_LAUNCH_CHECK();
+      }
+      LatShape s1;
+      s1.d = 1;
+      s1.dims[0] = n;
+      Epi inplace;
+      FCG_TRY(scan_axis<double>(p.lat, s1, 0, rev, inplace, p.scratch, st));
+      const int32_t *qq = req[q].survival ? p.r[0].upper
+                                          : (req[q].delta[0] > 0 ? p.r[0].upper : p.r[0].lower);
+      {
+        FCG_PROF("pts_gather", st);
+        gather1d_kernel<<<grid_for(n, 256), 256, 0, st>>>(p.lat, qq, n, rev ? 1 : 0, req[q].out);
+        FCG_LAUNCH_CHECK();
+      }
       FCG_PROF("pts_finish", st);
-      finish_ecdf_kernel<<<grid_for(n, 256), 256, 0, st>>>(out, n, w, 0, div);
+      finish_ecdf_kernel<<<grid_for(n, 256), 256, 0, st>>>(req[q].out, n, w, 0, div);
       FCG_LAUNCH_CHECK();
     }
     return FCG_OK;
   }
 
-  // rank every dimension; the distinct counts decide the route (host sync)
-  for (int k = 0; k < d; ++k) FCG_TRY(rank_dim(x, n, d, k, p, st));
+  // rank every dimension once; the distinct counts decide the route (host sync)
+  FCG_TRY(rank_all(x, n, d, p, st));
   int32_t nd[FCG_MAX_DIM];
   FCG_TRY(read_small(nd, p.ndist, d * 4, st));
   double cells = 1.0;
   for (int k = 0; k < d; ++k) cells *= (double)nd[k];
 
   if (cells <= (double)budget) {  // rank lattice route
-    RankLat r;
-    LatShape s;
-    r.d = s.d = d;
-    bool rev[FCG_MAX_DIM];
-    int64_t stride = 1;
-    for (int k = d - 1; k >= 0; --k) {
-      r.dense[k] = p.r[k].dense;
-      r.shift[k] = survival ? 1 : (delta[k] > 0 ? 0 : -1);
-      r.dims[k] = s.dims[k] = nd[k];
-      r.stride[k] = stride;
-      stride *= nd[k];
-      rev[k] = survival != 0;
-    }
-    const bool unit = (w == nullptr);
-    {
-      FCG_PROF("lattice_zero", st);
-      FCG_CUDA_TRY(cudaMemsetAsync(p.lat, 0, (size_t)stride * (unit ? 4 : 8), st));
-    }
-    {
-      FCG_PROF("pts_rank_scatter", st);
-      if (unit) rank_scatter_kernel<true><<<grid_for(n, 256), 256, 0, st>>>(r, n, w, p.lat);
-      else rank_scatter_kernel<false><<<grid_for(n, 256), 256, 0, st>>>(r, n, w, p.lat);
+    for (int q = 0; q < nreq; ++q) {
+      const int survival = req[q].survival;
+      const int32_t *delta = req[q].delta;
+      double *out = req[q].out;
+      RankLat r;
+      LatShape s;
+      r.d = s.d = d;
+      bool rev[FCG_MAX_DIM];
+      int64_t stride = 1;
+      for (int k = d - 1; k >= 0; --k) {
+        r.dense[k] = p.r[k].dense;
+        r.shift[k] = survival ? 1 : (delta[k] > 0 ? 0 : -1);
+        r.dims[k] = s.dims[k] = nd[k];
+        r.stride[k] = stride;
+        stride *= nd[k];
+        rev[k] = survival != 0;
+      }
+      const bool unit = (w == nullptr);
+      {
+        FCG_PROF("lattice_zero", st);
+        FCG_CUDA_TRY(cudaMemsetAsync(p.lat, 0, (size_t)stride * (unit ? 4 : 8), st));
+      }
+      {
+        FCG_PROF("pts_rank_scatter", st);
+        if (unit) rank_scatter_kernel<true><<<grid_for(n, 256), 256, 0, st>>>(r, n, w, p.lat);
+        else rank_scatter_kernel<false><<<grid_for(n, 256), 256, 0, st>>>(r, n, w, p.lat);
+        FCG_LAUNCH_CHECK();
+      }
+      Epi inplace;
+      if (unit) {
+        FCG_TRY(scan_lattice<int32_t>(reinterpret_cast<int32_t *>(p.lat), s, rev, inplace,
+                                      reinterpret_cast<int32_t *>(p.scratch), st));
+        FCG_PROF("pts_gather", st);
+        rank_gather_kernel<int32_t><<<grid_for(n, 256), 256, 0, st>>>(
+            r, n, reinterpret_cast<const int32_t *>(p.lat), div, out);
+      } else {
+        FCG_TRY(scan_lattice<double>(p.lat, s, rev, inplace, p.scratch, st));
+        FCG_PROF("pts_gather", st);
+        rank_gather_kernel<double><<<grid_for(n, 256), 256, 0, st>>>(r, n, p.lat, div, out);
+      }
       FCG_LAUNCH_CHECK();
     }
-    Epi inplace;
-    if (unit) {
-      FCG_TRY(scan_lattice<int32_t>(reinterpret_cast<int32_t *>(p.lat), s, rev, inplace,
-                                    reinterpret_cast<int32_t *>(p.scratch), st));
-      FCG_PROF("pts_gather", st);
-      rank_gather_kernel<int32_t><<<grid_for(n, 256), 256, 0, st>>>(
-          r, n, reinterpret_cast<const int32_t *>(p.lat), div, out);
-    } else {
-      FCG_TRY(scan_lattice<double>(p.lat, s, rev, inplace, p.scratch, st));
-      FCG_PROF("pts_gather", st);
-      rank_gather_kernel<double><<<grid_for(n, 256), 256, 0, st>>>(r, n, p.lat, div, out);
-    }
-    FCG_LAUNCH_CHECK();
     return FCG_OK;
   }
 
   if (dom_ok) {  // d == 2 rank-space dominance
     FCG_TRY(group_by(p.r[0].order, p.r[1].pos, n, p.P, p.bychunk, p, st));
     FCG_TRY(group_by(p.r[1].order, p.r[0].pos, n, p.P, p.byblock, p, st));
-    if (survival) {  // [x_i > x_t] <=> flipped p_i < npad - upper_t
-      FCG_TRY(make_q(p.r[0].upper, n, 2, p.npad, p.Q0f, st));
-      FCG_TRY(make_q(p.r[1].upper, n, 2, p.npad, p.Q1f, st));
-    } else {
-      FCG_TRY(make_q(delta[0] > 0 ? p.r[0].upper : p.r[0].lower, n, 0, p.npad, p.Q0f, st));
-      FCG_TRY(make_q(delta[1] > 0 ? p.r[1].upper : p.r[1].lower, n, 0, p.npad, p.Q1f, st));
-    }
     {
       FCG_PROF("pts_psi", st);
       if (w) FCG_CUDA_TRY(cudaMemcpyAsync(p.psi, w, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
       else fill_f64<<<grid_for(n, 256), 256, 0, st>>>(p.psi, n, 1.0);
       FCG_LAUNCH_CHECK();
     }
-    FCG_TRY(dom2d(p, n, 1, survival, survival, p.psi, out, st));
-    FCG_PROF("pts_finish", st);
-    finish_ecdf_kernel<<<grid_for(n, 256), 256, 0, st>>>(out, n, w, 0, div);
-    FCG_LAUNCH_CHECK();
+    for (int q = 0; q < nreq; ++q) {
+      const int survival = req[q].survival;
+      const int32_t *delta = req[q].delta;
+      if (survival) {  // [x_i > x_t] <=> flipped p_i < npad - upper_t
+        FCG_TRY(make_q(p.r[0].upper, n, 2, p.npad, p.Q0f, st));
+        FCG_TRY(make_q(p.r[1].upper, n, 2, p.npad, p.Q1f, st));
+      } else {
+        FCG_TRY(make_q(delta[0] > 0 ? p.r[0].upper : p.r[0].lower, n, 0, p.npad, p.Q0f, st));
+        FCG_TRY(make_q(delta[1] > 0 ? p.r[1].upper : p.r[1].lower, n, 0, p.npad, p.Q1f, st));
+      }
+      FCG_TRY(dom2d(p, n, 1, survival, survival, p.psi, req[q].out, st));
+      FCG_PROF("pts_finish", st);
+      finish_ecdf_kernel<<<grid_for(n, 256), 256, 0, st>>>(req[q].out, n, w, 0, div);
+      FCG_LAUNCH_CHECK();
+    }
     return FCG_OK;
   }
 
   if (d == 2) return dom_too_large(n);
   // brute force (d >= 3 without a feasible rank lattice)
-  Brute B;
-  B.n = n;
-  B.d = d;
-  B.x = x;
-  B.w = w;
-  B.nw = 1;
-  B.out = out;
-  for (int k = 0; k < d; ++k) B.sign[k] = survival ? 2 : delta[k];
-  {
-    FCG_PROF("pts_brute", st);
-    brute_kernel<BR_ECDF><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(B);
+  for (int q = 0; q < nreq; ++q) {
+    Brute B;
+    B.n = n;
+    B.d = d;
+    B.x = x;
+    B.w = w;
+    B.nw = 1;
+    B.out = req[q].out;
+    for (int k = 0; k < d; ++k) B.sign[k] = req[q].survival ? 2 : req[q].delta[k];
+    {
+      FCG_PROF("pts_brute", st);
+      brute_kernel<BR_ECDF><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(B);
+      FCG_LAUNCH_CHECK();
+    }
+    FCG_PROF("pts_finish", st);
+    finish_ecdf_kernel<<<grid_for(n, 256), 256, 0, st>>>(req[q].out, n, w, 0, div);
     FCG_LAUNCH_CHECK();
   }
-  FCG_PROF("pts_finish", st);
-  finish_ecdf_kernel<<<grid_for(n, 256), 256, 0, st>>>(out, n, w, 0, div);
-  FCG_LAUNCH_CHECK();
   return FCG_OK;
+}
+}  // namespace
+}  // namespace fcg
+
+extern "C" int fcg_ecdf_points(const double *x, int64_t n, int32_t d, const double *w,
+                               const int32_t *delta, int32_t survival, int32_t scaled,
+                               double *out, void *ws, size_t *ws_bytes, void *stream) {
+  const PtsReq r{delta, survival, out};
+  return ecdf_points_multi(x, n, d, w, scaled, &r, 1, ws, ws_bytes, as_stream(stream));
+}
+
+extern "C" int fcg_ecdf_esf_points(const double *x, int64_t n, int32_t d, const double *w,
+                                   const int32_t *delta, int32_t scaled, double *out_ecdf,
+                                   double *out_esf, void *ws, size_t *ws_bytes, void *stream) {
+  const PtsReq r[2] = {{delta, 0, out_ecdf}, {delta, 1, out_esf}};
+  return ecdf_points_multi(x, n, d, w, scaled, r, 2, ws, ws_bytes, as_stream(stream));
 }
 
 extern "C" int fcg_dnc_ecdf(const double *x, int64_t n, int32_t d, const double *w,

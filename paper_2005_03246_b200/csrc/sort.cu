@@ -426,9 +426,35 @@ __global__ void key_andor_kernel(const uint64_t *__restrict__ keys, int64_t n,
   }
 }
 
-__global__ void key_andor_init(unsigned long long *out) {
-  out[0] = ~0ull;
-  out[1] = 0ull;
+__global__ void key_andor_init(unsigned long long *out, int pairs = 1) {
+  for (int i = threadIdx.x; i < pairs; i += blockDim.x) {
+    out[2 * i] = ~0ull;
+    out[2 * i + 1] = 0ull;
+  }
+}
+
+// AND / OR of the order-preserving keys of every column of x (n, d): one pass over x for all
+// dimensions (the rank path then needs one host read-back for every dimension's digit mask)
+__global__ void key_andor_dims_kernel(const double *__restrict__ x, int64_t n, int d,
+                                      unsigned long long *__restrict__ out) {
+  for (int k = 0; k < d; ++k) {
+    uint64_t a = ~0ull, o = 0ull;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const uint64_t key = f64_key(x[i * d + k]);
+      a &= key;
+      o |= key;
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      a &= __shfl_xor_sync(0xffffffffu, a, s);
+      o |= __shfl_xor_sync(0xffffffffu, o, s);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicAnd(out + 2 * k, (unsigned long long)a);
+      atomicOr(out + 2 * k + 1, (unsigned long long)o);
+    }
+  }
 }
 
 // seg_start[c] = first item of segment c (key >> seg_shift == c) of keys grouped by segment;
@@ -566,6 +592,36 @@ int radix_sort_pairs(KeyT *keys, int32_t *vals, int64_t n, int begin_bit, int en
   return radix_sort_digits<KeyT>(keys, vals, n, mask, ws, st, stable, first_hist_ready);
 }
 
+int radix_digit_masks_f64(const double *x, int64_t n, int d, unsigned long long *ao,
+                          uint32_t *masks, cudaStream_t st) {
+  if (n <= 0) {
+    for (int k = 0; k < d; ++k) masks[k] = 0;
+    return FCG_OK;
+  }
+  {
+    FCG_PROF("radix_prune", st);
+    key_andor_init<<<1, 32, 0, st>>>(ao, d);
+    FCG_LAUNCH_CHECK();
+    key_andor_dims_kernel<<<grid_for(n, 256, 4), 256, 0, st>>>(x, n, d, ao);
+    FCG_LAUNCH_CHECK();
+  }
+  unsigned long long h[2 * FCG_MAX_DIM];
+  FCG_TRY(read_small(h, ao, 2 * d * sizeof(unsigned long long), st));
+  for (int k = 0; k < d; ++k) {
+    const uint64_t diff = h[2 * k] ^ h[2 * k + 1];
+    uint32_t mask = 0;
+    for (int dg = 0; dg < 8; ++dg)
+      if ((diff >> (8 * dg)) & 0xFFull) mask |= 1u << dg;
+    masks[k] = mask;
+  }
+  return FCG_OK;
+}
+
+int radix_sort_pairs_mask(uint64_t *keys, int32_t *vals, int64_t n, uint32_t mask,
+                          const RadixWs &ws, cudaStream_t st) {
+  return radix_sort_digits<uint64_t>(keys, vals, n, mask, ws, st);
+}
+
 int radix_sort_pairs_pruned(uint64_t *keys, int32_t *vals, int64_t n, const RadixWs &ws,
                             cudaStream_t st) {
   if (n <= 1) return FCG_OK;
@@ -573,7 +629,7 @@ int radix_sort_pairs_pruned(uint64_t *keys, int32_t *vals, int64_t n, const Radi
   unsigned long long *ao = reinterpret_cast<unsigned long long *>(ws.hist);
   {
     FCG_PROF("radix_prune", st);
-    key_andor_init<<<1, 1, 0, st>>>(ao);
+    key_andor_init<<<1, 1, 0, st>>>(ao, 1);
     FCG_LAUNCH_CHECK();
     key_andor_kernel<<<grid_for(n, 256, 4), 256, 0, st>>>(keys, n, ao);
     FCG_LAUNCH_CHECK();

@@ -59,6 +59,13 @@ int msd2_sort_pairs_u32(uint32_t *keys, int32_t *vals, int64_t n, int nbits, con
 
 // Stable sort of 64-bit keys over the digits where they differ (one AND/OR reduction and a
 // 16-byte device-to-host read decide which 8-bit passes are identities).  Synchronises `st`.
+// Digit masks of the fp64 keys of every column of x (n, d): bit g set when digit g varies.
+// ao: 2 d device words of scratch.  One host read-back for all dimensions (syncs).
+int radix_digit_masks_f64(const double *x, int64_t n, int d, unsigned long long *ao,
+                          uint32_t *masks, cudaStream_t st);
+// LSD radix sort of 64-bit keys over the digits set in mask (from radix_digit_masks_f64).
+int radix_sort_pairs_mask(uint64_t *keys, int32_t *vals, int64_t n, uint32_t mask,
+                          const RadixWs &ws, cudaStream_t st);
 int radix_sort_pairs_pruned(uint64_t *keys, int32_t *vals, int64_t n, const RadixWs &ws,
                             cudaStream_t st);
 

@@ -58,6 +58,28 @@ def esf_at_points(sample: Sample, scaled: bool = True) -> EvalResult:
         "runtime_seconds": time.perf_counter() - t0})
 
 
+def ecdf_esf_at_points(sample: Sample, delta: DeltaVector | None = None,
+                       scaled: bool = True) -> tuple[EvalResult, EvalResult]:
+    """``(ecdf_at_points(sample, delta), esf_at_points(sample))`` from one device ranking of
+    every dimension (``fcg_ecdf_esf_points``): the two outputs of BASELINE config 2."""
+    import torch
+
+    sample = as_sample(sample)
+    t0 = time.perf_counter()
+    x = _lib.to_device_f64(sample.points)
+    n, d = x.shape
+    signs = delta.signs if delta is not None else (1,) * d
+    if len(signs) != d:
+        raise ParameterError("delta dimension does not match sample")
+    w = None if sample.unit_weights else _lib.to_device_f64(sample.weights)
+    out = torch.empty((2, n), dtype=torch.float64, device=x.device)
+    _lib.call_ws("fcg_ecdf_esf_points", _lib.ptr(x), n, d, _lib.ptr(w), _lib.i32_array(signs),
+                 int(scaled), _lib.ptr(out[0]), _lib.ptr(out[1]))
+    meta = {"scaled": scaled, "runtime_seconds": time.perf_counter() - t0}
+    return (EvalResult(_out(sample, out[0]), POINT_ALIGNED, {"method": "rank-dominance", **meta}),
+            EvalResult(_out(sample, out[1]), POINT_ALIGNED, {"method": "rank-dominance-esf", **meta}))
+
+
 def kde_numerators(sample: Sample, weights_list, bandwidth: Bandwidth):
     """Laplacian KDE numerators at the points for one or two weight vectors (None = unit) in a
     single device pass; (nw, n) tensor (device sample) or array."""

@@ -122,6 +122,33 @@ def test_cfg2_full(oracle, cfg_meta):
     # unit weights: exact integer counts
     cnt = fcb.ecdf_at_points(fcb.validate_sample(w.points), fcb.DeltaVector(w.delta), scaled=False).values
     np.testing.assert_array_equal(cnt, oracle.ecdf_at_points(w.points, None, w.delta, scaled=False))
+    # both outputs from one ranking (fp64 atomics in the lattice scatter: run-to-run rounding)
+    e2, s2 = fcb.ecdf_esf_at_points(s, fcb.DeltaVector(w.delta))
+    assert rel_err(e2.values, ecdf) <= 1e-14
+    assert rel_err(s2.values, esf) <= 1e-14
+
+
+@pytest.mark.parametrize("case", ["lattice_d3", "dominance_d2", "d1"])
+def test_ecdf_esf_at_points_routes(case, oracle):
+    """The shared-ranking pair on every route: rank lattice (d = 3, ties), dominance (d = 2
+    with too many levels for the lattice budget) and d = 1 (prefix and suffix from one sort)."""
+    rng = np.random.default_rng(23)
+    if case == "lattice_d3":
+        x = np.floor(rng.random((20_000, 3)) * 17) / 17
+        delta = (1, -1, 1)
+    elif case == "dominance_d2":
+        x = np.floor(rng.random((300_000, 2)) * 1e5) / 1e5  # ~1e10 level pairs > budget
+        delta = (-1, 1)
+    else:
+        x = np.floor(rng.random((50_000, 1)) * 999) / 999
+        delta = (-1,)
+    y = rng.random(x.shape[0])
+    s = fcb.validate_sample(x, y)
+    e, f = fcb.ecdf_esf_at_points(s, fcb.DeltaVector(delta))
+    q = rng.integers(0, x.shape[0], 400)
+    assert rel_err(e.values[q], oracle.ecdf_naive(x, y, x[q], delta)) <= 1e-12
+    assert rel_err(f.values[q], oracle.esf_naive(x, y, x[q])) <= 1e-12
+    assert rel_err(e.values, fcb.ecdf_at_points(s, fcb.DeltaVector(delta)).values) <= 1e-14
 
 
 # ---- kde_dnc (dnc.py:635-690; reference tests test_dnc.py:163-189) ---------------------
