@@ -156,3 +156,53 @@ extern "C" int fcg_abi_version(void) { return FCG_ABI_VERSION; }
 extern "C" const char *fcg_last_error(void) { return fcg::g_last_error.c_str(); }
 
 extern "C" int fcg_device_sm_count(void) { return fcg::sm_count(); }
+
+// ---- TMA tensor maps (tma.cuh) ----------------------------------------------------------
+#include "tma.cuh"
+
+namespace fcg {
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool tma_map_2d(CUtensorMap *map, CUtensorMapDataType dt, size_t esz, const void *base,
+                uint64_t inner, uint64_t outer, uint64_t pitch, uint32_t box_inner,
+                uint32_t box_outer) {
+  auto fn = tma_encode_fn();
+  if (!fn || !base || (reinterpret_cast<uintptr_t>(base) & 15) || (pitch * esz) % 16 ||
+      box_inner == 0 || box_outer == 0 || box_inner > 256 || box_outer > 256 ||
+      (box_inner * esz) % 16)
+    return false;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {pitch * esz};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, dt, 2, const_cast<void *>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
+bool tma_map_2d_f64(CUtensorMap *map, const void *base, uint64_t inner, uint64_t outer,
+                    uint64_t pitch, uint32_t box_inner, uint32_t box_outer) {
+  return tma_map_2d(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, base, inner, outer, pitch,
+                    box_inner, box_outer);
+}
+bool tma_map_2d_i32(CUtensorMap *map, const void *base, uint64_t inner, uint64_t outer,
+                    uint64_t pitch, uint32_t box_inner, uint32_t box_outer) {
+  return tma_map_2d(map, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, base, inner, outer, pitch, box_inner,
+                    box_outer);
+}
+}  // namespace fcg

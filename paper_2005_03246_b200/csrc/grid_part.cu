@@ -8,9 +8,11 @@
 #include <math_constants.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "grid_part.cuh"
+#include "tma.cuh"
 #include "partition.cuh"
 #include "sort.cuh"
 
@@ -1464,9 +1466,13 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-template <int NT, bool REV0>
-__global__ void __launch_bounds__(256, 2) final2d_kernel(Final2D f) {
-  extern __shared__ __align__(16) double f2_smem[];
+struct F2Maps {  // TMA boxes [D1][kF2Cols] of the group lattices (0 .. NT-1) and the output (NT)
+  CUtensorMap tm[3];
+};
+
+template <int NT, bool REV0, bool TMA>
+__global__ void __launch_bounds__(256, 2) final2d_kernel(Final2D f, const __grid_constant__ F2Maps maps) {
+  extern __shared__ __align__(128) double f2_smem[];
   constexpr int CW = kF2Cols;
   const int64_t D0 = f.dims[0], D1 = f.dims[1];
   int64_t B = 1;
@@ -1475,6 +1481,7 @@ __global__ void __launch_bounds__(256, 2) final2d_kernel(Final2D f) {
   double *buf = f2_smem;                                // [2][NT + 1][D1][CW] (lattices, density)
   double *segs = buf + 2 * (NT + 1) * slab;             // [NT][kF2Segs][CW]
   double *z1 = segs + NT * kF2Segs * CW;                // [NT][D1] axis-1 factors
+  uint64_t *s_bar = reinterpret_cast<uint64_t *>(z1 + NT * D1);  // [2] TMA stage barriers
   const int c = threadIdx.x % CW, sg = threadIdx.x / CW;
   const int64_t b0 = (int64_t)blockIdx.x * CW;
   const int64_t b = b0 + c;
@@ -1496,8 +1503,31 @@ __global__ void __launch_bounds__(256, 2) final2d_kernel(Final2D f) {
         for (int t = 0; t < NT; ++t) zb[t] *= f.zf[t][f.zoff[k] + i];
     }
   }
+  if (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_init(&s_bar[0], 1);
+      mbar_init(&s_bar[1], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+  }
+  // TMA: one thread issues the [D1][CW] box of every slab of row i0 (no per-thread copies);
+  // otherwise 16-byte cp.async chunks from every thread
   auto stage = [&](int64_t jj, int which) {
     const int64_t i0 = REV0 ? D0 - 1 - jj : jj;
+    if constexpr (TMA) {
+      if (threadIdx.x == 0) {
+        const int nsl = NT + (f.accumulate ? 1 : 0);
+        mbar_expect_tx(&s_bar[which], (uint32_t)(nsl * slab * sizeof(double)));
+#pragma unroll
+        for (int t = 0; t <= NT; ++t) {
+          if (t == NT && !f.accumulate) break;
+          tma_load_2d(buf + (which * (NT + 1) + t) * slab, &maps.tm[t], (int32_t)b0,
+                      (int32_t)(i0 * D1), &s_bar[which]);
+        }
+      }
+      return;
+    }
 #pragma unroll
     for (int t = 0; t <= NT; ++t) {  // t == NT: the density accumulator's row
       if (t == NT && !f.accumulate) break;
@@ -1521,10 +1551,15 @@ __global__ void __launch_bounds__(256, 2) final2d_kernel(Final2D f) {
   for (int64_t jj = 0; jj < D0; ++jj) {
     const int64_t i0 = REV0 ? D0 - 1 - jj : jj;
     const int cur = (int)(jj & 1);
-    if (jj + 1 < D0) stage(jj + 1, cur ^ 1);
-    else cp_async_commit();  // keep the group count uniform
-    cp_async_wait1();
-    __syncthreads();
+    if constexpr (TMA) {
+      if (jj + 1 < D0) stage(jj + 1, cur ^ 1);
+      mbar_wait(&s_bar[cur], (uint32_t)((jj >> 1) & 1));
+    } else {
+      if (jj + 1 < D0) stage(jj + 1, cur ^ 1);
+      else cp_async_commit();  // keep the group count uniform
+      cp_async_wait1();
+      __syncthreads();
+    }
     double v[NT][kF2Seg];
     // a warp holds two segments of the same 16 columns: their totals pair up with one shuffle,
     // so the cross-warp prefix runs over the 8 warp totals (both lattices in one double2)
@@ -1601,6 +1636,7 @@ __global__ void __launch_bounds__(256, 2) final2d_kernel(Final2D f) {
       if (f.apply_scale) r = r * f.scale;
       f.out[(i0 * D1 + i1) * B + b] = r;
     }
+    if constexpr (TMA) fence_proxy_async_smem();  // generic slab accesses before the next TMA
     __syncthreads();  // the slab buffer `cur` is refilled next row
   }
 }
@@ -1610,16 +1646,30 @@ int launch_final2d(const Final2D &f, bool rev0, cudaStream_t st) {
   for (int k = 2; k < f.d; ++k) B *= f.dims[k];
   const unsigned grid = (unsigned)(B / kF2Cols);
   const size_t smem = (size_t)(2 * (f.nt + 1) * f.dims[1] * kF2Cols + f.nt * kF2Segs * kF2Cols +
-                               f.nt * f.dims[1]) * sizeof(double);
+                               f.nt * f.dims[1]) * sizeof(double) + 2 * sizeof(uint64_t);
   FCG_PROF("kde_final_group", st);
+  // TMA boxes: [D1][kF2Cols] fp64 of each lattice (and of the accumulator), rows i0 * D1 + i1
+  // of a 2-D (B, D0 * D1) view
+  F2Maps maps{};
+  static const bool no_tma = getenv("FCG_NO_TMA") && getenv("FCG_NO_TMA")[0] == '1';
+  bool tma = !no_tma && f.dims[1] <= 256;
+  const uint64_t rows = (uint64_t)f.dims[0] * f.dims[1];
+  for (int t = 0; t < f.nt && tma; ++t)
+    tma = tma_map_2d_f64(&maps.tm[t], f.lat[t], B, rows, B, kF2Cols, (uint32_t)f.dims[1]);
+  if (tma && f.accumulate)  // box NT: the accumulator
+    tma = tma_map_2d_f64(&maps.tm[f.nt], f.out, B, rows, B, kF2Cols, (uint32_t)f.dims[1]);
   auto go = [&](auto kern) -> int {
     FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, 256, smem, st>>>(f);
+    kern<<<grid, 256, smem, st>>>(f, maps);
     FCG_LAUNCH_CHECK();
     return FCG_OK;
   };
-  if (f.nt == 1) return rev0 ? go(final2d_kernel<1, true>) : go(final2d_kernel<1, false>);
-  return rev0 ? go(final2d_kernel<2, true>) : go(final2d_kernel<2, false>);
+  if (tma) {
+    if (f.nt == 1) return rev0 ? go(final2d_kernel<1, true, true>) : go(final2d_kernel<1, false, true>);
+    return rev0 ? go(final2d_kernel<2, true, true>) : go(final2d_kernel<2, false, true>);
+  }
+  if (f.nt == 1) return rev0 ? go(final2d_kernel<1, true, false>) : go(final2d_kernel<1, false, false>);
+  return rev0 ? go(final2d_kernel<2, true, false>) : go(final2d_kernel<2, false, false>);
 }
 
 // Fused axis-1 + axis-0 final pass of the partitioned ECDF (d >= 4): int32 counts in, the

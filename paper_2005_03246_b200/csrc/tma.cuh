@@ -1,0 +1,60 @@
+// TMA (cp.async.bulk.tensor) staging helpers for sm_100a: host-side 2-D tensor-map encoding
+// through the driver entry point (no -lcuda link) and the device-side mbarrier protocol.
+#pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace fcg {
+
+// 2-D fp64 view (inner extent `inner` elements, `outer` rows, row pitch `pitch` elements) with
+// a box of box_inner x box_outer elements.  Returns false when TMA cannot describe it.
+bool tma_map_2d_f64(CUtensorMap *map, const void *base, uint64_t inner, uint64_t outer,
+                    uint64_t pitch, uint32_t box_inner, uint32_t box_outer);
+// same for int32 elements
+bool tma_map_2d_i32(CUtensorMap *map, const void *base, uint64_t inner, uint64_t outer,
+                    uint64_t pitch, uint32_t box_inner, uint32_t box_outer);
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared box load, completion counted on `bar`
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int32_t c0,
+                                            int32_t c1, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+// generic-proxy shared-memory accesses before this are ordered before later async-proxy (TMA)
+// accesses of the same shared memory
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+}  // namespace fcg
