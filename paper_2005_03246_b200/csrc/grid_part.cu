@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "grid_part.cuh"
 #include "tma.cuh"
@@ -1676,22 +1677,38 @@ int launch_final2d(const Final2D &f, bool rev0, cudaStream_t st) {
 // output epilogue (count / N as fp64, or int64 counts) out, 16 columns per CTA as in
 // final2d_kernel; the axis-1 lattice pass disappears.
 constexpr int kE2Stages = 4;
-template <bool REV0, bool REV1, int EK>
+template <bool REV0, bool REV1, int EK, bool TMA>
 __global__ void __launch_bounds__(256, 2) ecdf_final2d_kernel(const int32_t *__restrict__ lat,
                                                               int64_t D0, int64_t D1, int64_t B,
-                                                              double div, void *out) {
-  extern __shared__ __align__(16) int32_t e2_smem[];
+                                                              double div, void *out,
+                                                              const __grid_constant__ CUtensorMap tm) {
+  extern __shared__ __align__(128) int32_t e2_smem[];
   const double rdiv = div > 0.0 ? 1.0 / div : 0.0;
   constexpr int CW = kF2Cols;
   constexpr int ST = kE2Stages;           // slabs in flight (rows i0 + 1 .. i0 + ST - 1 arriving)
   const int slab = (int)D1 * CW;
   int32_t *buf = e2_smem;                 // [ST][D1][CW]
   int32_t *segs = buf + ST * slab;        // [kF2Segs][CW]
+  uint64_t *bar = reinterpret_cast<uint64_t *>(segs + kF2Segs * CW);  // [ST] TMA barriers
   const int c = threadIdx.x % CW, sg = threadIdx.x / CW;
   const int64_t b0 = (int64_t)blockIdx.x * CW;
   const int64_t b = b0 + c;
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      for (int q = 0; q < ST; ++q) mbar_init(&bar[q], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+  }
   auto stage = [&](int64_t jj, int which) {
     const int64_t i0 = REV0 ? D0 - 1 - jj : jj;
+    if constexpr (TMA) {  // one thread: the [D1][CW] box of row i0
+      if (threadIdx.x == 0) {
+        mbar_expect_tx(&bar[which], (uint32_t)(slab * sizeof(int32_t)));
+        tma_load_2d(buf + which * slab, &tm, (int32_t)b0, (int32_t)(i0 * D1), &bar[which]);
+      }
+      return;
+    }
     int32_t *dst = buf + which * slab;
     const int32_t *src = lat + (i0 * D1) * B + b0;
     for (int ch = threadIdx.x; ch < (int)D1 * (CW / 4); ch += blockDim.x) {  // 16-byte chunks
@@ -1707,15 +1724,20 @@ __global__ void __launch_bounds__(256, 2) ecdf_final2d_kernel(const int32_t *__r
 #pragma unroll
   for (int q = 0; q < ST - 1; ++q) {
     if (q < D0) stage(q, q);
-    else cp_async_commit();
+    else if (!TMA) cp_async_commit();
   }
   for (int64_t jj = 0; jj < D0; ++jj) {
     const int64_t i0 = REV0 ? D0 - 1 - jj : jj;
     const int cur = (int)(jj % ST);
-    if (jj + ST - 1 < D0) stage(jj + ST - 1, (int)((jj + ST - 1) % ST));
-    else cp_async_commit();  // keep the group count uniform
-    asm volatile("cp.async.wait_group %0;" ::"n"(kE2Stages - 1) : "memory");
-    __syncthreads();
+    if constexpr (TMA) {
+      if (jj + ST - 1 < D0) stage(jj + ST - 1, (int)((jj + ST - 1) % ST));
+      mbar_wait(&bar[cur], (uint32_t)((jj / ST) & 1));
+    } else {
+      if (jj + ST - 1 < D0) stage(jj + ST - 1, (int)((jj + ST - 1) % ST));
+      else cp_async_commit();  // keep the group count uniform
+      asm volatile("cp.async.wait_group %0;" ::"n"(kE2Stages - 1) : "memory");
+      __syncthreads();
+    }
     const int32_t *sl = buf + cur * slab;
     int32_t v[kF2Seg];
     int32_t run = 0;
@@ -1753,20 +1775,31 @@ int launch_ecdf_final2d(const int32_t *lat, const int64_t *dims, int d, bool rev
   int64_t B = 1;
   for (int k = 2; k < d; ++k) B *= dims[k];
   const unsigned grid = (unsigned)(B / kF2Cols);
-  const size_t smem = (size_t)(kE2Stages * dims[1] * kF2Cols + kF2Segs * kF2Cols) * sizeof(int32_t);
+  const size_t smem = (size_t)(kE2Stages * dims[1] * kF2Cols + kF2Segs * kF2Cols) * sizeof(int32_t) +
+                      kE2Stages * sizeof(uint64_t);
   FCG_PROF("scan_lines_final", st);
+  // TMA box [D1][kF2Cols] int32 of the 2-D (B, D0 * D1) view of the count lattice
+  CUtensorMap tm{};
+  static const bool no_tma = getenv("FCG_NO_TMA") && getenv("FCG_NO_TMA")[0] == '1';
+  const bool tma = !no_tma && dims[1] <= 256 &&
+                   tma_map_2d_i32(&tm, lat, B, (uint64_t)dims[0] * dims[1], B, kF2Cols,
+                                  (uint32_t)dims[1]);
   auto go = [&](auto kern) -> int {
     FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, 256, smem, st>>>(lat, dims[0], dims[1], B, epi.div, epi.out);
+    kern<<<grid, 256, smem, st>>>(lat, dims[0], dims[1], B, epi.div, epi.out, tm);
     FCG_LAUNCH_CHECK();
     return FCG_OK;
   };
-  if (epi.kind == EPI_I64) {
-    if (rev0) return rev1 ? go(ecdf_final2d_kernel<true, true, EPI_I64>) : go(ecdf_final2d_kernel<true, false, EPI_I64>);
-    return rev1 ? go(ecdf_final2d_kernel<false, true, EPI_I64>) : go(ecdf_final2d_kernel<false, false, EPI_I64>);
-  }
-  if (rev0) return rev1 ? go(ecdf_final2d_kernel<true, true, EPI_F64>) : go(ecdf_final2d_kernel<true, false, EPI_F64>);
-  return rev1 ? go(ecdf_final2d_kernel<false, true, EPI_F64>) : go(ecdf_final2d_kernel<false, false, EPI_F64>);
+  auto pick = [&](auto tma_tag) -> int {
+    constexpr bool T = decltype(tma_tag)::value;
+    if (epi.kind == EPI_I64) {
+      if (rev0) return rev1 ? go(ecdf_final2d_kernel<true, true, EPI_I64, T>) : go(ecdf_final2d_kernel<true, false, EPI_I64, T>);
+      return rev1 ? go(ecdf_final2d_kernel<false, true, EPI_I64, T>) : go(ecdf_final2d_kernel<false, false, EPI_I64, T>);
+    }
+    if (rev0) return rev1 ? go(ecdf_final2d_kernel<true, true, EPI_F64, T>) : go(ecdf_final2d_kernel<true, false, EPI_F64, T>);
+    return rev1 ? go(ecdf_final2d_kernel<false, true, EPI_F64, T>) : go(ecdf_final2d_kernel<false, false, EPI_F64, T>);
+  };
+  return tma ? pick(std::true_type{}) : pick(std::false_type{});
 }
 
 int launch_final_multi(const MultiFinal &f, bool rev, cudaStream_t st) {
