@@ -1687,8 +1687,9 @@ __global__ void __launch_bounds__(256, 2) ecdf_final2d_kernel(const int32_t *__r
   constexpr int CW = kF2Cols;
   constexpr int ST = kE2Stages;           // slabs in flight (rows i0 + 1 .. i0 + ST - 1 arriving)
   const int slab = (int)D1 * CW;
+  const int sstr = (slab + 31) & ~31;      // buffer stride: 128-byte aligned TMA destinations
   int32_t *buf = e2_smem;                 // [ST][D1][CW]
-  int32_t *segs = buf + ST * slab;        // [kF2Segs][CW]
+  int32_t *segs = buf + ST * sstr;        // [kF2Segs][CW]
   uint64_t *bar = reinterpret_cast<uint64_t *>(segs + kF2Segs * CW);  // [ST] TMA barriers
   const int c = threadIdx.x % CW, sg = threadIdx.x / CW;
   const int64_t b0 = (int64_t)blockIdx.x * CW;
@@ -1705,11 +1706,11 @@ __global__ void __launch_bounds__(256, 2) ecdf_final2d_kernel(const int32_t *__r
     if constexpr (TMA) {  // one thread: the [D1][CW] box of row i0
       if (threadIdx.x == 0) {
         mbar_expect_tx(&bar[which], (uint32_t)(slab * sizeof(int32_t)));
-        tma_load_2d(buf + which * slab, &tm, (int32_t)b0, (int32_t)(i0 * D1), &bar[which]);
+        tma_load_2d(buf + which * sstr, &tm, (int32_t)b0, (int32_t)(i0 * D1), &bar[which]);
       }
       return;
     }
-    int32_t *dst = buf + which * slab;
+    int32_t *dst = buf + which * sstr;
     const int32_t *src = lat + (i0 * D1) * B + b0;
     for (int ch = threadIdx.x; ch < (int)D1 * (CW / 4); ch += blockDim.x) {  // 16-byte chunks
       const int r = ch / (CW / 4), q = ch % (CW / 4);
@@ -1738,7 +1739,7 @@ __global__ void __launch_bounds__(256, 2) ecdf_final2d_kernel(const int32_t *__r
       asm volatile("cp.async.wait_group %0;" ::"n"(kE2Stages - 1) : "memory");
       __syncthreads();
     }
-    const int32_t *sl = buf + cur * slab;
+    const int32_t *sl = buf + cur * sstr;
     int32_t v[kF2Seg];
     int32_t run = 0;
 #pragma unroll
@@ -1775,8 +1776,8 @@ int launch_ecdf_final2d(const int32_t *lat, const int64_t *dims, int d, bool rev
   int64_t B = 1;
   for (int k = 2; k < d; ++k) B *= dims[k];
   const unsigned grid = (unsigned)(B / kF2Cols);
-  const size_t smem = (size_t)(kE2Stages * dims[1] * kF2Cols + kF2Segs * kF2Cols) * sizeof(int32_t) +
-                      kE2Stages * sizeof(uint64_t);
+  const size_t smem = (size_t)(kE2Stages * ((dims[1] * kF2Cols + 31) & ~int64_t(31)) +
+                               kF2Segs * kF2Cols) * sizeof(int32_t) + kE2Stages * sizeof(uint64_t);
   FCG_PROF("scan_lines_final", st);
   // TMA box [D1][kF2Cols] int32 of the 2-D (B, D0 * D1) view of the count lattice
   CUtensorMap tm{};
