@@ -201,6 +201,17 @@ int fcg_distinct(const double *x, int64_t n, int32_t d, int32_t *flags,
                  void *ws, size_t *ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------------------
+ * Host <-> device transfers of the drop-in numpy path (numpy in, numpy out)
+ * ------------------------------------------------------------------------------------- */
+
+/* Pageable host -> device copy staged through a pinned ring with multi-threaded host copies;
+ * enqueued on `stream`, returns once the source may be reused (like cudaMemcpyAsync from
+ * pageable memory).  Replaces the implicit np.asarray upload of every reference call. */
+int fcg_copy_h2d(void *dst_dev, const void *src_host, size_t bytes, void *stream);
+/* Device -> pageable host copy after the work queued on `stream`; returns when dst is filled. */
+int fcg_copy_d2h(void *dst_host, const void *src_dev, size_t bytes, void *stream);
+
+/* ---------------------------------------------------------------------------------------
  * At-points path (subsystem 4)
  * ------------------------------------------------------------------------------------- */
 

@@ -58,6 +58,8 @@ _SIGS = {
     "fcg_kde_points_laplacian_shard": ([_P, _I64, _I32, _P, _I32, _P, _P, _I32, _I32, _P, _P, _SZP,
                                         _P], C.c_int),
     "fcg_dnc_ecdf_shard": ([_P, _I64, _I32, _P, _I32, _I32, _I32, _I32, _P, _P, _SZP, _P], C.c_int),
+    "fcg_copy_h2d": ([_P, _P, C.c_size_t, _P], C.c_int),
+    "fcg_copy_d2h": ([_P, _P, C.c_size_t, _P], C.c_int),
     "fcg_axis_owner": ([_P, _I64, _I32, _I32, _P, _I64, _I32, _I32, _P, _I32, _P, _P], C.c_int),
     "fcg_partition_rows": ([_P, _I64, _I32, _P, _P, _I32, _P, _P, _P, _P, _SZP, _P], C.c_int),
     "fcg_slab_finish": ([_P, _I32, _P, _I64, _I64, _I64, C.c_double, _P, _P], C.c_int),
@@ -203,7 +205,33 @@ def to_device_f64(a):
                 f"cuda:{torch.cuda.current_device()}; call under torch.cuda.device({t.device})")
         return t.to(torch.float64).contiguous()
     arr = np.ascontiguousarray(a, dtype=np.float64)
+    if arr.nbytes >= _STAGED_MIN:  # large uploads: pinned ring + threaded staging
+        t = torch.empty(arr.shape, dtype=torch.float64, device=device())
+        lib = _lib if _lib is not None else load_library()
+        check(lib.fcg_copy_h2d(C.c_void_p(t.data_ptr()), arr.ctypes.data_as(C.c_void_p),
+                               arr.nbytes, stream_handle()), "fcg_copy_h2d")
+        return t
     return torch.from_numpy(arr).to(device(), non_blocking=True)
+
+
+_STAGED_MIN = 8 << 20
+
+
+def to_host(t) -> np.ndarray:
+    """Device tensor -> freshly allocated numpy array (staged and threaded when large)."""
+    if t.device.type != "cuda":
+        return t.numpy()
+    torch = _torch()
+    dt = {torch.float64: np.float64, torch.int64: np.int64, torch.int32: np.int32}.get(t.dtype)
+    if (dt is None or not t.is_contiguous()
+            or t.numel() * t.element_size() < _STAGED_MIN):
+        return t.cpu().numpy()
+    out = np.empty(tuple(t.shape), dtype=dt)
+    lib = _lib if _lib is not None else load_library()
+    with _torch().cuda.device(t.device):
+        check(lib.fcg_copy_d2h(out.ctypes.data_as(C.c_void_p), C.c_void_p(t.data_ptr()),
+                               out.nbytes, stream_handle()), "fcg_copy_d2h")
+    return out
 
 
 def device_knots(grid):

@@ -364,7 +364,7 @@ def kde_numerators_sharded(sample: Sample, weights_list, bandwidth: Bandwidth, g
     wmat = torch.stack(ws).contiguous()
     out = engine.kde_points_shard(x, wmat, len(ws), h, c, rank, world)
     out = _finish_points(out, dist, group, world, gather)
-    return out if sample.on_device else out.cpu().numpy()
+    return out if sample.on_device else _lib.to_host(out)
 
 
 def kernel_regression_sharded(sample: Sample, y, kernel, bandwidth: Bandwidth, group=None,
@@ -404,5 +404,5 @@ def ecdf_dnc_sharded(sample: Sample, include_self: bool = False, scaled: bool = 
     w = None if sample.unit_weights else engine.tensor(sample.weights)
     out = engine.dnc_ecdf_shard(x, w, include_self, scaled, rank, world)
     out = _finish_points(out, dist, group, world, gather)
-    return EvalResult(out if sample.on_device else out.cpu().numpy(), POINT_ALIGNED,
+    return EvalResult(out if sample.on_device else _lib.to_host(out), POINT_ALIGNED,
                       {"method": "dnc-sharded", "scaled": scaled, "include_self": include_self})

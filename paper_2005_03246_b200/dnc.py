@@ -65,7 +65,7 @@ def _span_guard_and_centre(sample: Sample, h: np.ndarray) -> np.ndarray:
 
 
 def _out(sample: Sample, t):
-    return t if sample.on_device else t.cpu().numpy()
+    return t if sample.on_device else _lib.to_host(t)
 
 
 def ecdf_dnc(sample: Sample, include_self: bool = False, scaled: bool = True) -> EvalResult:

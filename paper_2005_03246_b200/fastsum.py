@@ -39,7 +39,7 @@ class CumulativeTensor:
 
 
 def _out(sample: Sample, t):
-    return t if sample.on_device else t.cpu().numpy()
+    return t if sample.on_device else _lib.to_host(t)
 
 
 def directional_sweep(tensor: LocalSumTensor, delta: DeltaVector) -> CumulativeTensor:
@@ -56,7 +56,7 @@ def directional_sweep(tensor: LocalSumTensor, delta: DeltaVector) -> CumulativeT
         lat = lat.clone()
     _lib.call_ws("fcg_directional_sweep", _lib.ptr(lat), _lib.LAT_F64, len(dims),
                  _lib.i64_array(dims), _lib.i32_array(delta.signs))
-    return CumulativeTensor(lat if was_torch else lat.cpu().numpy(), tensor.scaled)
+    return CumulativeTensor(lat if was_torch else _lib.to_host(lat), tensor.scaled)
 
 
 def _ecdf_grid_device(sample: Sample, grid: RectilinearGrid, delta: DeltaVector | None,

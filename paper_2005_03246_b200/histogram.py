@@ -58,7 +58,7 @@ def _local_sums_device(sample: Sample, grid: RectilinearGrid, delta: DeltaVector
 
 
 def _wrap(sample: Sample, t):
-    return t if sample.on_device else t.cpu().numpy()
+    return t if sample.on_device else _lib.to_host(t)
 
 
 def local_sums(sample: Sample, grid: RectilinearGrid,

@@ -47,7 +47,7 @@ def multilinear_interp(grid: RectilinearGrid, values: EvalResult, queries) -> Ev
     _lib.call_ws("fcg_multilinear_interp", _lib.ptr(_lib.device_knots(grid)),
                  _lib.i64_array(grid.shape), d, _lib.ptr(vd), _lib.ptr(qd), nq, _lib.ptr(out),
                  C.addressof(cc))
-    res = out if on_device else out.cpu().numpy()
+    res = out if on_device else _lib.to_host(out)
     return EvalResult(res, POINT_ALIGNED, {
         "method": "multilinear",
         "clamp_count": int(cc.value),
