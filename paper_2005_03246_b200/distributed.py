@@ -220,8 +220,11 @@ def ecdf_fastsum_slab(sample: Sample, grid: RectilinearGrid, delta: DeltaVector 
     w = None if sample.unit_weights else eng.tensor(sample.weights)
     le = 0 if survival else int(delta.signs[1] < 0)
     shift = 1 if survival else 0
-    owner = eng.axis_owner(x, grid.knots[1], le, shift, bounds)
-    xr, wr = _exchange_rows(x, w, owner, world, eng, group)
+    if world > 1:
+        owner = eng.axis_owner(x, grid.knots[1], le, shift, bounds)
+        xr, wr = _exchange_rows(x, w, owner, world, eng, group)
+    else:  # one slab: every point is already on its owner (dead points are skipped locally)
+        xr, wr = x, w
     n_total = torch.tensor([sample.count], dtype=torch.int64, device=x.device)
     dist.all_reduce(n_total, group=group)
     sub = _sub_grid(grid, lo, hi)
@@ -232,9 +235,8 @@ def ecdf_fastsum_slab(sample: Sample, grid: RectilinearGrid, delta: DeltaVector 
     plane = (cube[:, 0, :] if survival else cube[:, J - 1, :]).contiguous()
     planes = _gather_planes(plane, world, group)
     others = planes[rank + 1:] if survival else planes[:rank]
-    carry = torch.zeros_like(plane)
-    for p in others:
-        carry += p
+    # carry = sum of the lower (forward) / higher (survival) ranks' boundary planes, on device
+    carry = torch.stack(others).sum(0) if others else None
     out = eng.slab_finish(local, carry, A, J, B, float(n_total.item()) if scaled else 0.0)
     return EvalResult(out, GRID_ALIGNED, {"method": "fastsum-slab", "scaled": scaled,
                                           "slab": (lo, hi), "world": world})
@@ -277,29 +279,37 @@ def kde_fastsum_slab(sample: Sample, grid: RectilinearGrid, kernel, bandwidth: B
                 f"dimension {k}: span/bandwidth = {span[k] / h[k]:.1f} exceeds "
                 f"{EXP_OVERFLOW_GUARD:.0f}; enlarge the bandwidth or rescale")
     centre = 0.5 * (lo_h + hi_h)
-    # route by the delta=+1 cell and, for the delta_1 = -1 terms, by the cell one bin lower
-    own_a = eng.axis_owner(x, grid.knots[1], 0, 0, bounds)
-    own_b = eng.axis_owner(x, grid.knots[1], 0, 1, bounds)
-    own_b = torch.where(own_b == own_a, torch.full_like(own_b, -1), own_b)
-    xa, wa = _exchange_rows(x, w, own_a, world, eng, group)
-    xb, wb = _exchange_rows(x, w, own_b, world, eng, group)
-    xr = torch.cat([xa, xb])
-    wr = None if w is None else torch.cat([wa, wb])
+    # route by the delta=+1 cell and, for the delta_1 = -1 terms, by the cell one bin lower:
+    # a point in the first bin of slab r > 0 is also needed by slab r - 1.  Those duplicates are
+    # a thin layer (about G / M_1 of the points), so they are compacted first and routed alone.
+    if world > 1:
+        own_a = eng.axis_owner(x, grid.knots[1], 0, 0, bounds)
+        own_b = eng.axis_owner(x, grid.knots[1], 0, 1, bounds)
+        dup = torch.nonzero((own_b != own_a) & (own_b >= 0)).flatten()
+        xa, wa = _exchange_rows(x, w, own_a, world, eng, group)
+        xd = x[dup].contiguous()
+        wd = None if w is None else w[dup].contiguous()
+        xb, wb = _exchange_rows(xd, wd, own_b[dup].contiguous(), world, eng, group)
+        xr = torch.cat([xa, xb]) if xb.shape[0] else xa
+        wr = None if w is None else (torch.cat([wa, wb]) if wb.shape[0] else wa)
+    else:  # one slab: no routing and no slab boundary to duplicate across
+        xr, wr = x, w
     n_total = torch.tensor([sample.count], dtype=torch.int64, device=x.device)
     dist.all_reduce(n_total, group=group)
     N = float(n_total.item())
     sub = _sub_grid(grid, lo, hi)
     out, planes = eng.local_kde(xr, wr, sub, h, centre, N, float(np.sum(span / (2.0 * h))) * 1.000001)
     ncodes = 1 << d
-    gathered = _gather_planes(planes, world, group)
-    plane_sz = planes.numel() // ncodes
-    carries = torch.zeros_like(planes)
-    for code in range(ncodes):
-        reverse = bool((code >> 1) & 1)  # delta_1 = -1: suffix along axis 1
-        sel = gathered[rank + 1:] if reverse else gathered[:rank]
-        seg = slice(code * plane_sz, (code + 1) * plane_sz)
-        for g in sel:
-            carries[seg] += g[seg]
+    if world == 1:  # no other slab: every carry plane is zero
+        return EvalResult(out, GRID_ALIGNED, {"method": "fastsum-slab", "kernel": str(kernel),
+                                              "slab": (lo, hi), "world": world})
+    gathered = torch.stack(_gather_planes(planes, world, group)).view(world, ncodes, -1)
+    # forward codes (delta_1 = +1) add the lower ranks' planes, reverse codes the higher ones';
+    # two prefix sums over the rank axis, on device
+    fwd = gathered[:rank].sum(0) if rank > 0 else torch.zeros_like(gathered[0])
+    rev = gathered[rank + 1:].sum(0) if rank + 1 < world else torch.zeros_like(gathered[0])
+    is_rev = torch.tensor([bool((c >> 1) & 1) for c in range(ncodes)], device=planes.device)
+    carries = torch.where(is_rev[:, None], rev, fwd).reshape(-1).contiguous()
     out = eng.kde_fixup(out, sub, h, centre, carries, N)
     return EvalResult(out, GRID_ALIGNED, {"method": "fastsum-slab", "kernel": str(kernel),
                                           "slab": (lo, hi), "world": world})

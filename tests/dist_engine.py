@@ -42,7 +42,9 @@ class OracleEngine:
         return torch.as_tensor(v.astype(np.int64) if w is None else v)
 
     def slab_finish(self, local, carry, A, J, B, div):
-        v = local.numpy().reshape(A, J, B) + carry.numpy().reshape(A, 1, B)
+        v = local.numpy().reshape(A, J, B)
+        if carry is not None:
+            v = v + carry.numpy().reshape(A, 1, B)
         v = v.astype(np.float64)
         if div > 0:
             v = v / div

@@ -75,7 +75,7 @@ def _assemble(parts, key, shape):
     return full.reshape(-1)
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [1, 2, 3])
 def test_slab_decomposition_matches_single_grid(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
