@@ -239,8 +239,11 @@ int launch_small2d(const double *x, int64_t n, const double *w, const double *kn
   }
   if (per_sm < 1) return fail(FCG_ECUDA, "small2d kernel cannot be resident");
   const int64_t L = g.dims[0] * g.dims[1];
+  // few blocks: the grid barriers' cost grows with the block count, the phases are tiny
+  static const int64_t per_thread = getenv("FCG_SMALL_PER_THREAD") ? atoll(getenv("FCG_SMALL_PER_THREAD")) : 4;
   const int64_t work = std::max<int64_t>(std::max<int64_t>(n, L / 4), 1);
-  int64_t blocks = std::min<int64_t>(ceil_div(work, kSmallThreads), (int64_t)per_sm * sm_count());
+  int64_t blocks = std::min<int64_t>(ceil_div(work, kSmallThreads * per_thread),
+                                     (int64_t)per_sm * sm_count());
   blocks = std::max<int64_t>(blocks, 1);
   int r0 = rev0 ? 1 : 0, r1 = rev1 ? 1 : 0;
   void *args[] = {(void *)&x, (void *)&n, (void *)&w, (void *)&knots, (void *)&g, (void *)&r0,

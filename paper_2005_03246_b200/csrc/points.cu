@@ -127,8 +127,9 @@ inline bool dom_fits(int64_t n, int nch) {
 }
 inline int dom_too_large(int64_t n) {
   return fail(FCG_EUNSUPPORTED,
-              "n = " + std::to_string(n) + " points: the d = 2 dominance coarse grid would "
-              "exceed the 48 GB device budget (n <= ~2.5e8 with two weight channels)");
+              "n = " + std::to_string(n) + " points: the d = 2 dominance coarse grids would "
+              "exceed the 48 GB device budget (n <= ~3.5e8 for one channel, ~1.2e8 for the "
+              "Laplacian KDE with two weight vectors)");
 }
 
 // coarse rows: CTA per (flipped chunk c, segment of TB blocks); row[b][ch] accumulated in
@@ -552,8 +553,6 @@ struct GrpArrays {
   int32_t *rankpos;  // unflipped rank-dimension position (p0 for chunks, p1 for blocks)
   double *x;         // [n][2] points
   double *w;         // [nw][n] weights
-  double *psi;       // [nch][n] current code's psi
-  double *z;         // [n] current code's exp(-expo) (KDE) or unused
   double *acc;       // [nch][n] accumulated z * partial dominance sums
   int32_t *inv;      // source id -> group-order index
 };
@@ -615,63 +614,83 @@ __global__ void group_gather_kernel(const int32_t *__restrict__ order,
   }
 }
 
-// psi[v][k] = w[v][k] e^{s}, z[k] = e^{-s}, s = sum_j (x_kj - c_j) a_j  (dnc.py:661-669,673)
-// kde == 0: psi = w (plain strict-dominance ECDF)
-__global__ void group_psi_kernel(GrpArrays g, int64_t n, KdeP kp, int nw, int kde) {
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    double e = 1.0;
-    if (kde) {
-      const double s = (g.x[2 * k] - kp.c[0]) * kp.a[0] + (g.x[2 * k + 1] - kp.c[1]) * kp.a[1];
-      e = exp(s);
-      g.z[k] = exp(-s);
-    }
-    for (int v = 0; v < nw; ++v) g.psi[v * n + k] = g.w[v * n + k] * e * (kde ? chan_sign(kp, v) : 1.0);
-  }
-}
-
 struct Dom2S {
   int64_t n, P, npad;
   int64_t c_lo, c_hi;  // query shard: points whose (unflipped) chunk p1 >> LS is in [c_lo, c_hi)
   int nch, f0, f1, kde;
   GrpArrays gc, gb;  // chunk and block groupings
-  double *G;         // coarse grid [P][P][nch]
+  double *G;         // coarse grids [ncodes][P][P][nch], each in its code's flipped frame
+  KdeP kp;           // the current code (level-2 solvers: psi and z computed on the fly)
 };
 
-__global__ void __launch_bounds__(512) coarse_rows_group(Dom2S D, int64_t TB) {
-  extern __shared__ double s_row[];  // [TB][nch]
-  const int64_t c = blockIdx.x;
-  const int64_t g = D.f1 ? D.P - 1 - c : c;
-  const int64_t P = D.P;
+// The sign codes of one self-dominance call: the 2^2 Laplacian orientations (kde) or the plain
+// strict-dominance ECDF (one code, psi = w).
+struct Codes {
+  int n, kde;
+  KdeP kp[4];
+};
+
+// exponent s_code(x) = sum_j (x_j - c_j) a_j (dnc.py:661-669: a_j carries the code's sign)
+__device__ __forceinline__ double code_s(const KdeP &kp, double x0, double x1) {
+  return (x0 - kp.c[0]) * kp.a[0] + (x1 - kp.c[1]) * kp.a[1];
+}
+
+// Coarse rows of every code in one pass over the chunk-grouped points: CTA per (unflipped chunk
+// g, segment of TB unflipped blocks); a point adds its code-c psi to row (f1 ? P-1-g : g) at
+// block (f0 ? P-1-b : b) of grid c (every code's grid is stored in its own flipped frame).
+__global__ void __launch_bounds__(512) coarse_rows_codes(Dom2S D, Codes K, int64_t TB) {
+  extern __shared__ double s_row[];  // [ncodes][TB][nch]
+  const int64_t g = blockIdx.x, P = D.P;
   const int64_t b0 = (int64_t)blockIdx.y * TB, nb = (b0 + TB < P ? TB : P - b0);
-  for (int64_t i = threadIdx.x; i < nb * D.nch; i += blockDim.x) s_row[i] = 0.0;
+  const int nch = D.nch;
+  for (int64_t i = threadIdx.x; i < K.n * nb * nch; i += blockDim.x) s_row[i] = 0.0;
   __syncthreads();
   const int64_t lo = g * S, hi = (g + 1) * S < D.n ? (g + 1) * S : D.n;
   for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) {
-    const int64_t b = (flipp(D.gc.rankpos[k], D.f0, D.npad) >> LS) - b0;
-    if (b < 0 || b >= nb) continue;
-    for (int ch = 0; ch < D.nch; ++ch) atomicAdd(&s_row[b * D.nch + ch], D.gc.psi[ch * D.n + k]);
+    const int64_t bl = (D.gc.rankpos[k] >> LS) - b0;
+    if (bl < 0 || bl >= nb) continue;
+    const double x0 = D.gc.x[2 * k], x1 = D.gc.x[2 * k + 1];
+    for (int c = 0; c < K.n; ++c) {
+      const double e = K.kde ? exp(code_s(K.kp[c], x0, x1)) : 1.0;
+      for (int v = 0; v < nch; ++v)
+        atomicAdd(&s_row[(c * nb + bl) * nch + v],
+                  D.gc.w[v * D.n + k] * e * (K.kde ? chan_sign(K.kp[c], v) : 1.0));
+    }
   }
   __syncthreads();
-  double *row = D.G + (c * P + b0) * D.nch;
-  for (int64_t i = threadIdx.x; i < nb * D.nch; i += blockDim.x) row[i] = s_row[i];
+  for (int c = 0; c < K.n; ++c) {
+    const int f0 = c & 1, f1 = (c >> 1) & 1;
+    const int64_t row = f1 ? P - 1 - g : g;
+    double *grid = D.G + ((int64_t)c * P + row) * P * nch;
+    for (int64_t i = threadIdx.x; i < nb * nch; i += blockDim.x) {
+      const int64_t bl = i / nch, v = i - bl * nch;
+      const int64_t b = f0 ? P - 1 - (b0 + bl) : b0 + bl;
+      grid[b * nch + v] = s_row[(c * nb + bl) * nch + v];
+    }
+  }
 }
 
-// acc_q[ch][t] += z_t * G[chunk(t) - 1][block(t) - 1]   (query order, self thresholds)
-__global__ void coarse_query_self(Dom2S D, const int32_t *__restrict__ pos0,
-                                  const int32_t *__restrict__ pos1, const double *__restrict__ x,
-                                  KdeP kp, double *__restrict__ accq) {
+// acc_q[ch][t] = sum_codes z_code(t) * G_code[chunk(t) - 1][block(t) - 1] (flipped frames),
+// codes summed in order (the shard's queries only; the others stay untouched)
+__global__ void coarse_query_codes(Dom2S D, Codes K, const int32_t *__restrict__ pos0,
+                                   const int32_t *__restrict__ pos1, const double *__restrict__ x,
+                                   double *__restrict__ accq) {
+  const int64_t P = D.P;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < D.n;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t cu = pos1[t] >> LS;
+    const int64_t cu = pos1[t] >> LS, bu = pos0[t] >> LS;
     if (cu < D.c_lo || cu >= D.c_hi) continue;  // another shard's query
-    const int64_t c = flipp(pos1[t], D.f1, D.npad) >> LS, b = flipp(pos0[t], D.f0, D.npad) >> LS;
-    if (c == 0 || b == 0) continue;
-    double z = 1.0;
-    if (D.kde)
-      z = exp(-((x[2 * t] - kp.c[0]) * kp.a[0] + (x[2 * t + 1] - kp.c[1]) * kp.a[1]));
-    for (int ch = 0; ch < D.nch; ++ch)
-      accq[ch * D.n + t] += z * D.G[((c - 1) * D.P + (b - 1)) * D.nch + ch];
+    const double x0 = x[2 * t], x1 = x[2 * t + 1];
+    double acc[2] = {0.0, 0.0};
+    for (int c = 0; c < K.n; ++c) {
+      const int f0 = c & 1, f1 = (c >> 1) & 1;
+      const int64_t cc = f1 ? P - 1 - cu : cu, bb = f0 ? P - 1 - bu : bu;
+      if (cc == 0 || bb == 0) continue;
+      const double z = K.kde ? exp(-code_s(K.kp[c], x0, x1)) : 1.0;
+      const double *gv = D.G + (((int64_t)c * P + cc - 1) * P + bb - 1) * D.nch;
+      for (int v = 0; v < D.nch; ++v) acc[v] += z * gv[v];
+    }
+    for (int v = 0; v < D.nch; ++v) accq[v * D.n + t] = acc[v];
   }
 }
 
@@ -712,8 +731,12 @@ __global__ void __launch_bounds__(kSolverThreads) level2_self(Dom2S D) {
     s_xofy[y] = (int16_t)x;
     s_kofx[x] = (int16_t)k;
     s_key[y] = flipp(A.rankpos[lo + k], frank, D.npad);
+    {  // psi of the current code from the grouped point and weights (dnc.py:661-669)
+      const double e = D.kde ? exp(code_s(D.kp, A.x[2 * (lo + k)], A.x[2 * (lo + k) + 1])) : 1.0;
 #pragma unroll
-    for (int ch = 0; ch < NCH; ++ch) s_psi[ch * S + x] = A.psi[ch * D.n + lo + k];
+      for (int ch = 0; ch < NCH; ++ch)
+        s_psi[ch * S + x] = A.w[ch * D.n + lo + k] * e * (D.kde ? chan_sign(D.kp, ch) : 1.0);
+    }
   }
   __syncthreads();
   for (int r = threadIdx.x; r < NCH * NSUB; r += blockDim.x) {  // sub-grid cell sums, row-owned
@@ -787,7 +810,7 @@ __global__ void __launch_bounds__(kSolverThreads) level2_self(Dom2S D) {
       }
     }
     if (occ) {
-      const double z = D.kde ? A.z[lo + k] : 1.0;
+      const double z = D.kde ? exp(-code_s(D.kp, A.x[2 * (lo + k)], A.x[2 * (lo + k) + 1])) : 1.0;
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) A.acc[ch * D.n + lo + k] += z * acc[ch];
     }
@@ -817,7 +840,7 @@ __global__ void __launch_bounds__(kSolverThreads) level2_self(Dom2S D) {
     }
     if (ok) {
       const int k = frank ? Sg - 1 - y : y;
-      const double z = D.kde ? A.z[lo + k] : 1.0;
+      const double z = D.kde ? exp(-code_s(D.kp, A.x[2 * (lo + k)], A.x[2 * (lo + k) + 1])) : 1.0;
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) A.acc[ch * D.n + lo + k] += z * acc[ch];
     }
@@ -916,7 +939,7 @@ void carve(Workspace &W, PtsWs &p, int64_t n, int d, int nch, bool need_dom, boo
     p.qc_start = W.take<int32_t>(p.P + 2);
     p.qb_start = W.take<int32_t>(p.P + 2);
     p.cursor = W.take<int32_t>(p.P + 2);
-    p.G = W.take<double>(p.P * p.P * nch);
+    p.G = W.take<double>(p.P * p.P * nch * (need_kde ? 4 : 1));
     p.psi = W.take<double>((size_t)n * nch);
     p.F = W.take<double>((size_t)n * nch);
   }
@@ -1103,8 +1126,6 @@ void carve_self(Workspace &W, SelfWs &q, int64_t n, int nw) {
     g->rankpos = W.take<int32_t>(n);
     g->x = W.take<double>((size_t)n * 2);
     g->w = W.take<double>((size_t)n * nw);
-    g->psi = W.take<double>((size_t)n * nw);
-    g->z = W.take<double>(n);
     g->acc = W.take<double>((size_t)n * nw);
     g->inv = W.take<int32_t>(n);
   }
@@ -1135,7 +1156,6 @@ int self_dom2d(const double *x, const double *w, int64_t n, int nw, int kde, con
   }
   FCG_CUDA_TRY(cudaMemsetAsync(q.gc.acc, 0, (size_t)n * nw * 8, st));
   FCG_CUDA_TRY(cudaMemsetAsync(q.gb.acc, 0, (size_t)n * nw * 8, st));
-  FCG_CUDA_TRY(cudaMemsetAsync(q.accq, 0, (size_t)n * nw * 8, st));
   Dom2S D{};
   D.n = n;
   D.P = p.P;
@@ -1158,13 +1178,13 @@ int self_dom2d(const double *x, const double *w, int64_t n, int nw, int kde, con
     FCG_CUDA_TRY(cudaFuncSetAttribute(level2_self<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     FCG_CUDA_TRY(cudaFuncSetAttribute(level2_self<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   }
-  const int64_t TB = coarse_tb(nw), nseg = ceil_div(P, TB);
-  const size_t row_smem = (size_t)(TB < P ? TB : P) * nw * sizeof(double);
-  FCG_CUDA_TRY(cudaFuncSetAttribute(coarse_rows_group, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kCoarseRowBytes));
-  const int ncodes = kde ? 4 : 1;
-  for (int code = 0; code < ncodes; ++code) {
-    KdeP kp{};
+  // every code's coarse grid from one pass over the points (rows built in shared-memory
+  // segments of TB blocks), both prefix axes of all grids in two scans, one query pass
+  Codes K{};
+  K.n = kde ? 4 : 1;
+  K.kde = kde;
+  for (int code = 0; code < K.n; ++code) {
+    KdeP &kp = K.kp[code];
     kp.d = 2;
     kp.code = code;
     for (int v = 0; v < nw; ++v) kp.smask[v] = smask ? smask[v] : 0u;
@@ -1173,32 +1193,36 @@ int self_dom2d(const double *x, const double *w, int64_t n, int nw, int kde, con
       kp.c[k] = kde ? centre[k] : 0.0;
       kp.a[k] = kde ? sgn / h[k] : 0.0;
     }
+  }
+  {
+    FCG_PROF("pts_coarse_hist", st);
+    const int64_t TB = kCoarseRowBytes / (8 * (int64_t)nw * K.n), nseg = ceil_div(P, TB);
+    const size_t row_smem = (size_t)K.n * (TB < P ? TB : P) * nw * sizeof(double);
+    FCG_CUDA_TRY(cudaFuncSetAttribute(coarse_rows_codes, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kCoarseRowBytes));
+    coarse_rows_codes<<<dim3((unsigned)P, (unsigned)nseg), 512, row_smem, st>>>(D, K, TB);
+    FCG_LAUNCH_CHECK();
+  }
+  {
+    LatShape gs;
+    gs.d = 4;
+    gs.dims[0] = K.n;
+    gs.dims[1] = P;
+    gs.dims[2] = P;
+    gs.dims[3] = nw;
+    Epi inplace;
+    FCG_TRY(scan_axis<double>(p.G, gs, 2, false, inplace, p.scratch, st));
+    FCG_TRY(scan_axis<double>(p.G, gs, 1, false, inplace, p.scratch, st));
+  }
+  {
+    FCG_PROF("pts_coarse_query", st);
+    coarse_query_codes<<<g, 256, 0, st>>>(D, K, p.r[0].pos, p.r[1].pos, x, q.accq);
+    FCG_LAUNCH_CHECK();
+  }
+  for (int code = 0; code < K.n; ++code) {
+    D.kp = K.kp[code];
     D.f0 = code & 1;
     D.f1 = (code >> 1) & 1;
-    {
-      FCG_PROF("pts_psi", st);
-      group_psi_kernel<<<g, 256, 0, st>>>(q.gc, n, kp, nw, kde);
-      group_psi_kernel<<<g, 256, 0, st>>>(q.gb, n, kp, nw, kde);
-      FCG_LAUNCH_CHECK();
-    }
-    {
-      FCG_PROF("pts_coarse_hist", st);
-      coarse_rows_group<<<dim3((unsigned)P, (unsigned)nseg), 512, row_smem, st>>>(D, TB);
-      FCG_LAUNCH_CHECK();
-    }
-    LatShape gs;
-    gs.d = 3;
-    gs.dims[0] = P;
-    gs.dims[1] = P;
-    gs.dims[2] = nw;
-    Epi inplace;
-    FCG_TRY(scan_axis<double>(p.G, gs, 1, false, inplace, p.scratch, st));
-    FCG_TRY(scan_axis<double>(p.G, gs, 0, false, inplace, p.scratch, st));
-    {
-      FCG_PROF("pts_coarse_query", st);
-      coarse_query_self<<<g, 256, 0, st>>>(D, p.r[0].pos, p.r[1].pos, x, kp, q.accq);
-      FCG_LAUNCH_CHECK();
-    }
     {
       FCG_PROF("pts_level2_chunk", st);
       if (nchunk > 0) {
@@ -1514,7 +1538,7 @@ extern "C" int fcg_kde_points_laplacian(const double *x, int64_t n, int32_t d, c
                                         double *out, void *ws, size_t *ws_bytes, void *stream) {
   FCG_TRY(check_pts(n, d));
   if (nw < 1 || nw > 2) return fail(FCG_EUNSUPPORTED, "nw must be 1 or 2 weight vectors per call");
-  if (d == 2 && !dom_fits(n, nw)) return dom_too_large(n);
+  if (d == 2 && !dom_fits(n, 4 * nw)) return dom_too_large(n);  // 4 sign codes' grids
   const bool dom_ok = d == 2;
   Workspace W(ws);
   PtsWs p;
@@ -1638,7 +1662,7 @@ extern "C" int fcg_kde_points_matern32(const double *x, int64_t n, int32_t d, co
                                        const double *h, const double *centre, double *out,
                                        void *ws, size_t *ws_bytes, void *stream) {
   FCG_TRY(check_pts(n, d));
-  if (d == 2 && !dom_fits(n, 2)) return dom_too_large(n);
+  if (d == 2 && !dom_fits(n, 8)) return dom_too_large(n);  // 4 codes x 2 channels
   const bool dom_ok = d == 2;
   const int nchan = 2 * d + 1;
   Workspace W(ws);
@@ -1748,7 +1772,7 @@ extern "C" int fcg_kde_points_laplacian_shard(const double *x, int64_t n, int32_
   if (d != 2) return fail(FCG_EUNSUPPORTED, "query sharding is implemented for d = 2");
   if (nshards < 1 || shard < 0 || shard >= nshards) return fail(FCG_EINVAL, "shard out of range");
   if (nw < 1 || nw > 2) return fail(FCG_EUNSUPPORTED, "nw must be 1 or 2 weight vectors per call");
-  if (!dom_fits(n, nw)) return dom_too_large(n);
+  if (!dom_fits(n, 4 * nw)) return dom_too_large(n);
   Workspace W(ws);
   PtsWs p;
   carve(W, p, n, 2, nw, true, true, 0);
