@@ -1547,7 +1547,6 @@ __global__ void __launch_bounds__(256, 2) final2d_kernel(Final2D f, const __grid
 #pragma unroll
     for (int s = 0; s < kF2Seg; ++s) carry[t][s] = 0.0;
   const int p0 = sg * kF2Seg;
-  const bool swap = NT > 1 && f.rev1[1] != f.rev1[0];
   stage(0, 0);
   for (int64_t jj = 0; jj < D0; ++jj) {
     const int64_t i0 = REV0 ? D0 - 1 - jj : jj;
@@ -1562,24 +1561,35 @@ __global__ void __launch_bounds__(256, 2) final2d_kernel(Final2D f, const __grid
       __syncthreads();
     }
     double v[NT][kF2Seg];
-    // a warp holds two segments of the same 16 columns: their totals pair up with one shuffle,
-    // so the cross-warp prefix runs over the 8 warp totals (both lattices in one double2)
+    // Cells in order for every lattice: a forward lattice (rev1 = 0) takes inclusive prefixes
+    // inside the thread's 8-cell segment plus the totals of the segments below, a reversed one
+    // inclusive suffixes plus the totals of the segments above.  A warp holds two segments of
+    // the same 16 columns: their totals pair up with one shuffle, so the cross-warp sums run
+    // over the 8 warp totals (both lattices in one double2).
     const int warp = threadIdx.x >> 5, upper = (threadIdx.x >> 4) & 1;
     double inner[NT], wtot[NT];
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
       const double *sl = buf + (cur * (NT + 1) + t) * slab;
-      double run = 0.0;
+      double x[kF2Seg];
 #pragma unroll
-      for (int s = 0; s < kF2Seg; ++s) {
-        const int p = p0 + s;
-        double x = 0.0;
-        if (p < D1) x = sl[(f.rev1[t] ? (int)D1 - 1 - p : p) * CW + c];
-        run += x;
-        v[t][s] = run;
+      for (int s = 0; s < kF2Seg; ++s) x[s] = p0 + s < D1 ? sl[(p0 + s) * CW + c] : 0.0;
+      double run = 0.0;
+      if (!f.rev1[t]) {
+#pragma unroll
+        for (int s = 0; s < kF2Seg; ++s) {
+          run += x[s];
+          v[t][s] = run;
+        }
+      } else {
+#pragma unroll
+        for (int s = kF2Seg - 1; s >= 0; --s) {
+          run += x[s];
+          v[t][s] = run;
+        }
       }
       const double other = __shfl_xor_sync(0xffffffffu, run, 16);
-      inner[t] = upper ? other : 0.0;
+      inner[t] = (f.rev1[t] ? !upper : upper) ? other : 0.0;
       wtot[t] = run + other;
     }
     if (!upper)
@@ -1587,11 +1597,13 @@ __global__ void __launch_bounds__(256, 2) final2d_kernel(Final2D f, const __grid
           make_double2(wtot[0], NT > 1 ? wtot[NT - 1] : 0.0);
     __syncthreads();
     {
+      const int nwarp = blockDim.x >> 5;
       double o0 = inner[0], o1 = inner[NT - 1];
-      for (int w = 0; w < warp; ++w) {
+      for (int w = 0; w < nwarp; ++w) {
+        if (w == warp) continue;
         const double2 a = reinterpret_cast<const double2 *>(segs)[w * CW + c];
-        o0 += a.x;
-        o1 += a.y;
+        if (f.rev1[0] ? w > warp : w < warp) o0 += a.x;
+        if (NT > 1 && (f.rev1[NT - 1] ? w > warp : w < warp)) o1 += a.y;
       }
       inner[0] = o0;
       if (NT > 1) inner[NT - 1] = o1;
@@ -1603,36 +1615,19 @@ __global__ void __launch_bounds__(256, 2) final2d_kernel(Final2D f, const __grid
       for (int s = 0; s < kF2Seg; ++s) carry[t][s] += v[t][s] + off;
       if (f.plane[t] != nullptr) {  // slab carry capture (scanned over axes 0 and 1)
 #pragma unroll
-        for (int s = 0; s < kF2Seg; ++s) {
-          const int p = p0 + s;
-          if (p < D1 && (f.rev1[t] ? D1 - 1 - p : p) == f.plane_idx[t])
-            f.plane[t][i0 * B + b] = carry[t][s];
-        }
+        for (int s = 0; s < kF2Seg; ++s)
+          if (p0 + s < D1 && p0 + s == f.plane_idx[t]) f.plane[t][i0 * B + b] = carry[t][s];
       }
-    }
-    if (swap) {  // lattice 1 back to cell order, into its (consumed) slab
-      double *sl = buf + (cur * (NT + 1) + (NT - 1)) * slab;
-#pragma unroll
-      for (int s = 0; s < kF2Seg; ++s) {
-        const int p = p0 + s;
-        if (p < D1) sl[(f.rev1[1] ? (int)D1 - 1 - p : p) * CW + c] = carry[NT - 1][s];
-      }
-      __syncthreads();
     }
     const double z00 = f.zf[0][f.zoff[0] + i0] * zb[0];
     const double z01 = NT > 1 ? f.zf[NT - 1][f.zoff[0] + i0] * zb[NT - 1] : 0.0;
-    const double *sl1 = buf + (cur * (NT + 1) + (NT - 1)) * slab;
     const double *slo = buf + (cur * (NT + 1) + NT) * slab;
 #pragma unroll
     for (int s = 0; s < kF2Seg; ++s) {
-      const int p = p0 + s;
-      if (p >= D1) continue;
-      const int i1 = f.rev1[0] ? (int)D1 - 1 - p : p;
+      const int i1 = p0 + s;
+      if (i1 >= D1) continue;
       double val = (z00 * z1[i1]) * carry[0][s];
-      if (NT > 1) {
-        const double c1 = swap ? sl1[i1 * CW + c] : carry[NT - 1][s];
-        val += (z01 * z1[(NT - 1) * (int)D1 + i1]) * c1;
-      }
+      if (NT > 1) val += (z01 * z1[(NT - 1) * (int)D1 + i1]) * carry[NT - 1][s];
       double r = f.accumulate ? slo[i1 * CW + c] + val : val;
       if (f.apply_scale) r = r * f.scale;
       f.out[(i0 * D1 + i1) * B + b] = r;
