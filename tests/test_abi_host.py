@@ -201,3 +201,16 @@ def test_count_over_n_division_is_ieee_exact(tmp_path):
     res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert res.returncode == 0, res.stdout
     assert ", 0 mismatches" in res.stdout
+
+
+def test_bench_csv_schema(tmp_path):
+    """The ladder CSV is the reference's (cli.py:189-192): header and %.17g seconds."""
+    from paper_2005_03246_b200 import harness
+
+    rows = [("ecdf", "fastsum", 2, 1000, 0, 0.1 + 0.2), ("kde", "dnc", 3, 10, 1, 1e-7)]
+    p = tmp_path / "b.csv"
+    harness.write_rows(rows, p)
+    txt = p.read_text()
+    assert txt.splitlines()[0] == "task,method,dim,n,repeat,seconds"
+    assert txt.splitlines()[1] == "ecdf,fastsum,2,1000,0,0.30000000000000004"
+    assert txt.splitlines()[2] == "kde,dnc,3,10,1,9.9999999999999995e-08"

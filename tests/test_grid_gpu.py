@@ -501,3 +501,15 @@ def test_fused_plane_scan_vs_oracle(dims, oracle):
     h = np.full(d, 0.4)
     assert_rel(fcb.kde_fastsum(s, grid, fcb.laplacian(), fcb.Bandwidth.diag(h)).values,
                oracle.kde_fastsum_laplacian(x, w, knots, h), REL_KDE)
+
+
+def test_bench_ladder_small(tmp_path):
+    """The reference-schema ladder drives the device functions (cli.py:163-196)."""
+    from paper_2005_03246_b200 import harness
+
+    rows = harness.bench_ladder("ecdf", ["fastsum", "dnc"], [2], [2000], repeats=2,
+                                out=tmp_path / "l.csv")
+    assert len(rows) == 4 and all(r[5] > 0 for r in rows)
+    rows = harness.bench_ladder("kde", ["fastsum", "dnc"], [2], [500], repeats=1)
+    assert len(rows) == 2
+    assert (tmp_path / "l.csv").read_text().startswith("task,method,dim,n,repeat,seconds\n")
