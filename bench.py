@@ -638,8 +638,10 @@ class PointsWorkload:
             # group-ordered self dominance, per launch and per point: slot + rank positions,
             # 2-channel psi, the z factor, and two read-modify-writes of the 2-channel
             # accumulator (slot-order pass, rank-order pass)
-            b.update({"pts_level2_chunk": (4 + 4 + 16 + 8 + 2 * 32) * n,
-                      "pts_level2_block": (4 + 4 + 16 + 8 + 2 * 32) * n,
+            # level-2 solvers, all four sign codes per launch: slot + rank position once, the
+            # point and its two weights re-read per code, one 2-channel store per point
+            b.update({"pts_level2_chunk": (4 + 4 + 4 * (16 + 16) + 16) * n,
+                      "pts_level2_block": (4 + 4 + 4 * (16 + 16) + 16) * n,
                       "pts_group_gather": (4 + 8 + 16 + 16) * n + (4 + 4 + 16 + 16 + 4) * n,
                       "pts_psi": (16 + 16 + 16 + 8) * n})
         return b

@@ -694,11 +694,20 @@ __global__ void coarse_query_codes(Dom2S D, Codes K, const int32_t *__restrict__
   }
 }
 
+// All sign codes of one level-2 grouping in one CTA (CHUNK: chunk g, sources = the chunk's
+// points by p0 rank; BLOCK: block g by p1 rank).  The CTA loads its sources once (registers:
+// thread t holds sources t, t + 1024, ...), and for every code rebuilds the flipped-frame layout,
+// the sub-grid and both partial passes.  Each thread owns the same queries in every code (pass A:
+// the sources of its unflipped slots, pass B: the sources of its ranks), so the code sum
+// z_c * F_c accumulates in registers; the two halves meet in shared memory once and are written
+// with plain coalesced stores (no global read-modify-write per code).
+constexpr int kL2Per = S / kSolverThreads;  // sources per thread
+
 template <bool CHUNK, int NCH>
-__global__ void __launch_bounds__(kSolverThreads) level2_self(Dom2S D) {
+__global__ void __launch_bounds__(kSolverThreads) level2_codes(Dom2S D, Codes K) {
   extern __shared__ __align__(16) unsigned char smem[];
   double *s_sub = reinterpret_cast<double *>(smem);               // [NCH][NSUB][NSUB]
-  double *s_psi = s_sub + NCH * NSUB * NSUB;                      // [NCH][S] by slot
+  double *s_psi = s_sub + NCH * NSUB * NSUB;                      // [S][NCH] by slot
   int32_t *s_key = reinterpret_cast<int32_t *>(s_psi + NCH * S);  // [S] rank-dim positions by rank
   int16_t *s_yofx = reinterpret_cast<int16_t *>(s_key + S);       // [S]
   int16_t *s_xofy = s_yofx + S;                                   // [S]
@@ -706,144 +715,203 @@ __global__ void __launch_bounds__(kSolverThreads) level2_self(Dom2S D) {
   int16_t *s_qy = s_kofx + S;                                     // [S] rank threshold by slot
 
   const GrpArrays &A = CHUNK ? D.gc : D.gb;
-  const int fslot = CHUNK ? D.f1 : D.f0;
-  // chunk kind: only the shard's chunks are launched; block kind: every block, but only the
-  // shard's queries (unflipped chunk of the rank-dimension position p1) are evaluated
-  const int64_t cb = blockIdx.x + (CHUNK ? (fslot ? D.P - D.c_hi : D.c_lo) : 0);
-  const int frank = CHUNK ? D.f0 : D.f1;
-  const int64_t g = fslot ? D.P - 1 - cb : cb;
+  const int64_t g = blockIdx.x + (CHUNK ? D.c_lo : 0);  // unflipped chunk / block
   const int64_t lo = g * S;
   const int Sg = (int)(lo + S < D.n ? S : D.n - lo);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-
-  for (int i = threadIdx.x; i < NCH * NSUB * NSUB; i += blockDim.x) s_sub[i] = 0.0;
-  for (int i = threadIdx.x; i < S; i += blockDim.x) {
-    s_yofx[i] = -1;
+  const int lane = threadIdx.x & 31;
+  const bool all_owned = CHUNK || (D.c_lo == 0 && D.c_hi == D.P);
+  auto owned_key = [&](int32_t key) {  // BLOCK kind: the query's chunk is the shard's
+    const int64_t cu = key >> LS;
+    return all_owned || (cu >= D.c_lo && cu < D.c_hi);
+  };
+  // this thread's sources (group indices k = threadIdx.x + j * 1024): positions in registers,
+  // coordinates and weights re-read per code (L1 / L2 hits)
+  int slot_u[kL2Per];
+  int32_t key_u[kL2Per];
 #pragma unroll
-    for (int ch = 0; ch < NCH; ++ch) s_psi[ch * S + i] = 0.0;
+  for (int j = 0; j < kL2Per; ++j) {
+    const int k = threadIdx.x + j * kSolverThreads;
+    const bool in = k < Sg;
+    slot_u[j] = in ? A.slot[lo + k] - (int32_t)lo : 0;
+    key_u[j] = in ? A.rankpos[lo + k] : 0;
   }
-  __syncthreads();
-  for (int k = threadIdx.x; k < Sg; k += blockDim.x) {  // contiguous, coalesced
-    const int y = frank ? Sg - 1 - k : k;
-    int x = A.slot[lo + k] - (int32_t)lo;
-    if (fslot) x = S - 1 - x;
-    s_yofx[x] = (int16_t)y;
-    s_xofy[y] = (int16_t)x;
-    s_kofx[x] = (int16_t)k;
-    s_key[y] = flipp(A.rankpos[lo + k], frank, D.npad);
-    {  // psi of the current code from the grouped point and weights (dnc.py:661-669)
-      const double e = D.kde ? exp(code_s(D.kp, A.x[2 * (lo + k)], A.x[2 * (lo + k) + 1])) : 1.0;
+  const double2 *ax = reinterpret_cast<const double2 *>(A.x);
+  double accA[kL2Per][NCH], accB[kL2Per][NCH];
+  int kA[kL2Per];
+#pragma unroll
+  for (int j = 0; j < kL2Per; ++j) {
+    kA[j] = -1;
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) accA[j][ch] = accB[j][ch] = 0.0;
+  }
+
+  for (int code = 0; code < K.n; ++code) {
+    const KdeP &kp = K.kp[code];
+    const int f0 = code & 1, f1 = (code >> 1) & 1;
+    const int fslot = CHUNK ? f1 : f0, frank = CHUNK ? f0 : f1;
+    __syncthreads();  // the previous code's passes are done with the shared arrays
+    for (int i = threadIdx.x; i < NCH * NSUB * NSUB; i += blockDim.x) s_sub[i] = 0.0;
+    for (int i = threadIdx.x; i < S; i += blockDim.x) {
+      s_yofx[i] = -1;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) s_psi[i * NCH + ch] = 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kL2Per; ++j) {
+      const int k = threadIdx.x + j * kSolverThreads;
+      if (k >= Sg) continue;
+      const int y = frank ? Sg - 1 - k : k;
+      const int x = fslot ? S - 1 - slot_u[j] : slot_u[j];
+      s_yofx[x] = (int16_t)y;
+      s_xofy[y] = (int16_t)x;
+      s_kofx[x] = (int16_t)k;
+      s_key[y] = flipp(key_u[j], frank, D.npad);
+      const double2 xv = ax[lo + k];
+      const double e = K.kde ? exp(code_s(kp, xv.x, xv.y)) : 1.0;
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch)
-        s_psi[ch * S + x] = A.w[ch * D.n + lo + k] * e * (D.kde ? chan_sign(D.kp, ch) : 1.0);
+        s_psi[x * NCH + ch] = A.w[ch * D.n + lo + k] * e * (K.kde ? chan_sign(kp, ch) : 1.0);
     }
-  }
-  __syncthreads();
-  for (int r = threadIdx.x; r < NCH * NSUB; r += blockDim.x) {  // sub-grid cell sums, row-owned
-    const int ch = r / NSUB, u = r % NSUB;
-    double *row = s_sub + (ch * NSUB + u) * NSUB;
-    for (int x = u << SUBL; x < (u + 1) << SUBL; ++x) {
+    __syncthreads();
+    for (int r = threadIdx.x; r < NCH * NSUB; r += blockDim.x) {  // sub-grid cell sums
+      const int ch = r / NSUB, u = r % NSUB;
+      double *row = s_sub + (ch * NSUB + u) * NSUB;
+      for (int x = u << SUBL; x < (u + 1) << SUBL; ++x) {
+        const int y = s_yofx[x];
+        if (y >= 0) row[y >> SUBL] += s_psi[x * NCH + ch];
+      }
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < NCH * NSUB; r += blockDim.x) {
+      double *row = s_sub + r * NSUB;
+      double run = 0.0;
+      for (int v = 0; v < NSUB; ++v) { run += row[v]; row[v] = run; }
+    }
+    __syncthreads();
+    for (int cidx = threadIdx.x; cidx < NCH * NSUB; cidx += blockDim.x) {
+      const int ch = cidx / NSUB, v = cidx % NSUB;
+      double run = 0.0;
+      for (int u = 0; u < NSUB; ++u) {
+        double *pp = s_sub + (ch * NSUB + u) * NSUB + v;
+        run += *pp;
+        *pp = run;
+      }
+    }
+    __syncthreads();
+    // pass A: this thread's unflipped slots (a warp's 32 slots stay in one sub-row)
+#pragma unroll
+    for (int j = 0; j < kL2Per; ++j) {
+      const int uu = threadIdx.x + j * kSolverThreads;
+      const int x = fslot ? S - 1 - uu : uu;
       const int y = s_yofx[x];
-      if (y >= 0) row[y >> SUBL] += s_psi[ch * S + x];
-    }
-  }
-  __syncthreads();
-  for (int r = threadIdx.x; r < NCH * NSUB; r += blockDim.x) {
-    double *row = s_sub + r * NSUB;
-    double run = 0.0;
-    for (int v = 0; v < NSUB; ++v) { run += row[v]; row[v] = run; }
-  }
-  __syncthreads();
-  for (int cidx = threadIdx.x; cidx < NCH * NSUB; cidx += blockDim.x) {
-    const int ch = cidx / NSUB, v = cidx % NSUB;
-    double run = 0.0;
-    for (int u = 0; u < NSUB; ++u) {
-      double *pp = s_sub + (ch * NSUB + u) * NSUB + v;
-      run += *pp;
-      *pp = run;
-    }
-  }
-  __syncthreads();
-
-  // pass A, slot order: full sub-cells + the query's partial slot sub-range
-  const bool all_owned = CHUNK || (D.c_lo == 0 && D.c_hi == D.P);
-  auto owned = [&](int kk) {
-    if (all_owned) return true;
-    const int64_t cu = A.rankpos[lo + kk] >> LS;
-    return cu >= D.c_lo && cu < D.c_hi;
-  };
-  for (int xb = warp * 32; xb < S; xb += nwarps * 32) {
-    const int x = xb + lane;
-    const int y = s_yofx[x];
-    const bool occ = y >= 0 && (all_owned || owned(s_kofx[x]));
-    int qy = 0, k = 0;
-    if (occ) {
-      k = s_kofx[x];
-      if (CHUNK) {
-        qy = y;
-      } else {
-        const int64_t c = s_key[y] >> LS;  // own chunk (self threshold)
-        const int32_t ythr = (int32_t)((c > D.P ? D.P : c) * S);
-        int a = 0, bnd = Sg;
-        while (a < bnd) {
-          const int mid = (a + bnd) >> 1;
-          if (s_key[mid] < ythr) a = mid + 1;
-          else bnd = mid;
+      int k = 0;
+      bool occ = y >= 0;
+      if (occ) {
+        k = s_kofx[x];
+        occ = CHUNK || owned_key(A.rankpos[lo + k]);
+      }
+      int qy = 0;
+      if (occ) {
+        if (CHUNK) {
+          qy = y;
+        } else {
+          const int64_t c = s_key[y] >> LS;  // own chunk (self threshold)
+          const int32_t ythr = (int32_t)((c > D.P ? D.P : c) * S);
+          int a = 0, bnd = Sg;
+          while (a < bnd) {
+            const int mid = (a + bnd) >> 1;
+            if (s_key[mid] < ythr) a = mid + 1;
+            else bnd = mid;
+          }
+          qy = a;
         }
-        qy = a;
+        s_qy[x] = (int16_t)qy;
       }
-      s_qy[x] = (int16_t)qy;
-    }
-    const int u = xb >> SUBL, v = qy >> SUBL;
-    double acc[NCH];
+      const int u = x >> SUBL, v = qy >> SUBL;
+      double acc[NCH];
 #pragma unroll
-    for (int ch = 0; ch < NCH; ++ch)
-      acc[ch] = (occ && u > 0 && v > 0) ? s_sub[(ch * NSUB + (u - 1)) * NSUB + (v - 1)] : 0.0;
-    const int cend = (int)__reduce_max_sync(0xffffffffu, occ ? (unsigned)x : 0u);
-    for (int c = u << SUBL; c < cend; ++c) {
-      const int yc = s_yofx[c];
-      const bool hit = occ && c < x && yc >= 0 && yc < qy;
+      for (int ch = 0; ch < NCH; ++ch)
+        acc[ch] = (occ && u > 0 && v > 0) ? s_sub[(ch * NSUB + (u - 1)) * NSUB + (v - 1)] : 0.0;
+      const int cend = (int)__reduce_max_sync(0xffffffffu, occ ? (unsigned)x : 0u);
+      for (int c = u << SUBL; c < cend; ++c) {
+        const int yc = s_yofx[c];
+        const bool hit = occ && c < x && yc >= 0 && yc < qy;
+        if constexpr (NCH == 2) {
+          const double2 pc = reinterpret_cast<const double2 *>(s_psi)[c];
+          if (hit) {
+            acc[0] += pc.x;
+            acc[1] += pc.y;
+          }
+        } else {
+          const double pc = s_psi[c];
+          if (hit) acc[0] += pc;
+        }
+      }
+      if (occ) {
+        const double2 xv = ax[lo + k];
+        const double z = K.kde ? exp(-code_s(kp, xv.x, xv.y)) : 1.0;
+        kA[j] = k;
 #pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) {
-        const double pc = s_psi[ch * S + c];
-        if (hit) acc[ch] += pc;
+        for (int ch = 0; ch < NCH; ++ch) accA[j][ch] += z * acc[ch];
       }
     }
-    if (occ) {
-      const double z = D.kde ? exp(-code_s(D.kp, A.x[2 * (lo + k)], A.x[2 * (lo + k) + 1])) : 1.0;
+    (void)lane;
+    __syncthreads();
+    // pass B: this thread's ranks (= its own sources k), coalesced
 #pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) A.acc[ch * D.n + lo + k] += z * acc[ch];
+    for (int j = 0; j < kL2Per; ++j) {
+      const int k = threadIdx.x + j * kSolverThreads;
+      const bool ok = k < Sg && (CHUNK || owned_key(key_u[j]));
+      const int y = frank ? Sg - 1 - k : k;
+      const int x = ok ? s_xofy[y] : 0;
+      const int qy = ok ? (int)s_qy[x] : 0;
+      const int xfull = (x >> SUBL) << SUBL;
+      const int cbeg = ok ? (qy >> SUBL) << SUBL : S;
+      const int cstart = (int)__reduce_min_sync(0xffffffffu, (unsigned)cbeg);
+      const int cend = (int)__reduce_max_sync(0xffffffffu, ok ? (unsigned)qy : 0u);
+      double acc[NCH];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) acc[ch] = 0.0;
+      for (int c = cstart; c < cend; ++c) {
+        const int xc = s_xofy[c];
+        const bool hit = ok && c >= cbeg && c < qy && xc < xfull;
+        if constexpr (NCH == 2) {
+          const double2 pc = reinterpret_cast<const double2 *>(s_psi)[xc];
+          if (hit) {
+            acc[0] += pc.x;
+            acc[1] += pc.y;
+          }
+        } else {
+          const double pc = s_psi[xc];
+          if (hit) acc[0] += pc;
+        }
+      }
+      if (ok) {
+        const double2 xv = ax[lo + k];
+        const double z = K.kde ? exp(-code_s(kp, xv.x, xv.y)) : 1.0;
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) accB[j][ch] += z * acc[ch];
+      }
     }
   }
+  // the two halves of every query meet in shared memory (reusing the psi rows), one store each
   __syncthreads();
-  // pass B, rank order (coalesced accumulators): the partial rank sub-range, full slot rows
-  for (int yb = warp * 32; yb < Sg; yb += nwarps * 32) {
-    const int y = yb + lane;
-    const bool ok = y < Sg && (all_owned || owned(frank ? Sg - 1 - y : y));
-    const int x = ok ? s_xofy[y] : 0;
-    const int qy = ok ? (int)s_qy[x] : 0;
-    const int xfull = (x >> SUBL) << SUBL;
-    const int cbeg = ok ? (qy >> SUBL) << SUBL : S;
-    const int cstart = (int)__reduce_min_sync(0xffffffffu, (unsigned)cbeg);
-    const int cend = (int)__reduce_max_sync(0xffffffffu, ok ? (unsigned)qy : 0u);
-    double acc[NCH];
+  double *s_acc = s_psi;  // [S][NCH] by group index
+  for (int i = threadIdx.x; i < S * NCH; i += blockDim.x) s_acc[i] = 0.0;
+  __syncthreads();
 #pragma unroll
-    for (int ch = 0; ch < NCH; ++ch) acc[ch] = 0.0;
-    for (int c = cstart; c < cend; ++c) {
-      const int xc = s_xofy[c];
-      const bool hit = ok && c >= cbeg && c < qy && xc < xfull;
+  for (int j = 0; j < kL2Per; ++j)
+    if (kA[j] >= 0)
 #pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) {
-        const double pc = s_psi[ch * S + xc];
-        if (hit) acc[ch] += pc;
-      }
-    }
-    if (ok) {
-      const int k = frank ? Sg - 1 - y : y;
-      const double z = D.kde ? exp(-code_s(D.kp, A.x[2 * (lo + k)], A.x[2 * (lo + k) + 1])) : 1.0;
+      for (int ch = 0; ch < NCH; ++ch) s_acc[kA[j] * NCH + ch] = accA[j][ch];
+  __syncthreads();
 #pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) A.acc[ch * D.n + lo + k] += z * acc[ch];
-    }
+  for (int j = 0; j < kL2Per; ++j) {
+    const int k = threadIdx.x + j * kSolverThreads;
+    if (k >= Sg) continue;
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) A.acc[ch * D.n + lo + k] = s_acc[k * NCH + ch] + accB[j][ch];
   }
 }
 
@@ -1154,8 +1222,6 @@ int self_dom2d(const double *x, const double *w, int64_t n, int nw, int kde, con
     }
     FCG_LAUNCH_CHECK();
   }
-  FCG_CUDA_TRY(cudaMemsetAsync(q.gc.acc, 0, (size_t)n * nw * 8, st));
-  FCG_CUDA_TRY(cudaMemsetAsync(q.gb.acc, 0, (size_t)n * nw * 8, st));
   Dom2S D{};
   D.n = n;
   D.P = p.P;
@@ -1172,11 +1238,11 @@ int self_dom2d(const double *x, const double *w, int64_t n, int nw, int kde, con
   const unsigned nchunk = (unsigned)(D.c_hi - D.c_lo);
   const size_t sm = level2_self_smem(nw);
   if (nw == 1) {
-    FCG_CUDA_TRY(cudaFuncSetAttribute(level2_self<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    FCG_CUDA_TRY(cudaFuncSetAttribute(level2_self<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    FCG_CUDA_TRY(cudaFuncSetAttribute(level2_codes<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    FCG_CUDA_TRY(cudaFuncSetAttribute(level2_codes<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   } else {
-    FCG_CUDA_TRY(cudaFuncSetAttribute(level2_self<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    FCG_CUDA_TRY(cudaFuncSetAttribute(level2_self<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    FCG_CUDA_TRY(cudaFuncSetAttribute(level2_codes<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    FCG_CUDA_TRY(cudaFuncSetAttribute(level2_codes<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   }
   // every code's coarse grid from one pass over the points (rows built in shared-memory
   // segments of TB blocks), both prefix axes of all grids in two scans, one query pass
@@ -1219,24 +1285,20 @@ int self_dom2d(const double *x, const double *w, int64_t n, int nw, int kde, con
     coarse_query_codes<<<g, 256, 0, st>>>(D, K, p.r[0].pos, p.r[1].pos, x, q.accq);
     FCG_LAUNCH_CHECK();
   }
-  for (int code = 0; code < K.n; ++code) {
-    D.kp = K.kp[code];
-    D.f0 = code & 1;
-    D.f1 = (code >> 1) & 1;
-    {
-      FCG_PROF("pts_level2_chunk", st);
-      if (nchunk > 0) {
-        if (nw == 1) level2_self<true, 1><<<nchunk, kSolverThreads, sm, st>>>(D);
-        else level2_self<true, 2><<<nchunk, kSolverThreads, sm, st>>>(D);
-      }
-      FCG_LAUNCH_CHECK();
+  // level 2: every code of a chunk / block in one CTA (the chunk solvers for the shard's chunks)
+  {
+    FCG_PROF("pts_level2_chunk", st);
+    if (nchunk > 0) {
+      if (nw == 1) level2_codes<true, 1><<<nchunk, kSolverThreads, sm, st>>>(D, K);
+      else level2_codes<true, 2><<<nchunk, kSolverThreads, sm, st>>>(D, K);
     }
-    {
-      FCG_PROF("pts_level2_block", st);
-      if (nw == 1) level2_self<false, 1><<<(unsigned)P, kSolverThreads, sm, st>>>(D);
-      else level2_self<false, 2><<<(unsigned)P, kSolverThreads, sm, st>>>(D);
-      FCG_LAUNCH_CHECK();
-    }
+    FCG_LAUNCH_CHECK();
+  }
+  {
+    FCG_PROF("pts_level2_block", st);
+    if (nw == 1) level2_codes<false, 1><<<(unsigned)P, kSolverThreads, sm, st>>>(D, K);
+    else level2_codes<false, 2><<<(unsigned)P, kSolverThreads, sm, st>>>(D, K);
+    FCG_LAUNCH_CHECK();
   }
   FCG_PROF("pts_finish", st);
   self_finish_kernel<<<g, 256, 0, st>>>(n, nw, q.accq, q.gc.acc, q.gc.inv, q.gb.acc, q.gb.inv, w,
