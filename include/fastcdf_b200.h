@@ -264,6 +264,14 @@ int fcg_dnc_ecdf_shard(const double *x, int64_t n, int32_t d, const double *w,
                        int32_t include_self, int32_t scaled, int32_t shard, int32_t nshards,
                        double *out, void *ws, size_t *ws_bytes, void *stream);
 
+/* As fcg_kde_points_laplacian for d = 2, with one pointer per weight vector (NULL = unit
+ * weights for that channel), so callers mixing a unit density and a response need no stacked
+ * copy (the config-4 pair: w0 = NULL, w1 = y). */
+int fcg_kde_points_laplacian_w2(const double *x, int64_t n, int32_t d, const double *w0,
+                                const double *w1, int32_t nw, const double *h,
+                                const double *centre, double *out, void *ws, size_t *ws_bytes,
+                                void *stream);
+
 /* matern32-additive KDE at the sample points (dnc.py:635-690 with family "matern32-additive"):
  * the d + 1 channels of dnc.py:661-669 are run as 2d + 1 Laplacian dominance channels whose
  * weights only change sign with the term (A = w e, B_k = s_k w e, C_l = s_l w xc_l e / h_l),

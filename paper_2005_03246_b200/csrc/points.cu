@@ -564,8 +564,17 @@ struct PtRec {
   double x0, x1, w0, w1;
 };
 
+// per-channel weight vectors of the self path (nullptr = unit weights for that channel)
+struct WPtr {
+  const double *p[2];
+  __host__ __device__ double at(int v, int64_t i) const { return p[v] ? p[v][i] : 1.0; }
+};
+inline WPtr wptr(const double *w, int nw, int64_t n) {  // the [nw][n] matrix layout
+  return WPtr{{w, (w && nw > 1) ? w + n : nullptr}};
+}
+
 __global__ void pack_points_kernel(const int32_t *__restrict__ pos0, const int32_t *__restrict__ pos1,
-                                   const double *__restrict__ x, const double *__restrict__ w,
+                                   const double *__restrict__ x, WPtr w,
                                    int nw, int64_t n, PtRec *__restrict__ rec) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -575,8 +584,8 @@ __global__ void pack_points_kernel(const int32_t *__restrict__ pos0, const int32
     const double2 xv = reinterpret_cast<const double2 *>(x)[i];
     r.x0 = xv.x;
     r.x1 = xv.y;
-    r.w0 = w ? w[i] : 1.0;
-    r.w1 = nw > 1 ? (w ? w[n + i] : 1.0) : 0.0;
+    r.w0 = w.at(0, i);
+    r.w1 = nw > 1 ? w.at(1, i) : 0.0;
     rec[i] = r;
   }
 }
@@ -600,7 +609,7 @@ __global__ void group_gather_packed(const int32_t *__restrict__ order, const PtR
 __global__ void group_gather_kernel(const int32_t *__restrict__ order,
                                     const int32_t *__restrict__ pos_slot,
                                     const int32_t *__restrict__ pos_rank,
-                                    const double *__restrict__ x, const double *__restrict__ w,
+                                    const double *__restrict__ x, WPtr w,
                                     int nw, int64_t n, GrpArrays g) {
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
@@ -609,7 +618,7 @@ __global__ void group_gather_kernel(const int32_t *__restrict__ order,
     g.rankpos[k] = pos_rank[i];
     g.x[2 * k] = x[2 * (int64_t)i];
     g.x[2 * k + 1] = x[2 * (int64_t)i + 1];
-    for (int v = 0; v < nw; ++v) g.w[v * n + k] = w ? w[v * n + i] : 1.0;
+    for (int v = 0; v < nw; ++v) g.w[v * n + k] = w.at(v, i);
     g.inv[i] = (int32_t)k;
   }
 }
@@ -924,7 +933,7 @@ size_t level2_self_smem(int nch) {
 __global__ void self_finish_kernel(int64_t n, int nw, const double *__restrict__ accq,
                                    const double *__restrict__ accc, const int32_t *__restrict__ invc,
                                    const double *__restrict__ accb, const int32_t *__restrict__ invb,
-                                   const double *__restrict__ w, int add_w, double mult, double div,
+                                   WPtr w, int add_w, double mult, double div,
                                    double *__restrict__ out, const int32_t *__restrict__ pos1,
                                    int64_t c_lo, int64_t c_hi) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
@@ -937,7 +946,7 @@ __global__ void self_finish_kernel(int64_t n, int nw, const double *__restrict__
     const int64_t kc = invc[t], kb = invb[t];
     for (int v = 0; v < nw; ++v) {
       double r = accq[v * n + t] + accc[v * n + kc] + accb[v * n + kb];
-      if (add_w) r = r + (w ? w[v * n + t] : 1.0);
+      if (add_w) r = r + w.at(v, t);
       if (mult != 0.0) r = r * mult;
       if (div != 0.0) r = r / div;
       out[v * n + t] = r;
@@ -1204,7 +1213,7 @@ void carve_self(Workspace &W, SelfWs &q, int64_t n, int nw) {
 // Strict-dominance sums at the points for d = 2 in group order: the plain ECDF (kde = 0, one
 // orientation, psi = w) or the 2^2 Laplacian orientations (kde = 1, psi = w e^{s}, each term
 // weighted by e^{-s} at the query).  out[v][t] = (sum + (add_w ? w : 0)) * mult / div.
-int self_dom2d(const double *x, const double *w, int64_t n, int nw, int kde, const double *h,
+int self_dom2d(const double *x, WPtr w, int64_t n, int nw, int kde, const double *h,
                const double *centre, int add_w, double mult, double div, PtsWs &p, SelfWs &q,
                double *out, cudaStream_t st, const unsigned *smask = nullptr, int shard = 0,
                int nshards = 1) {
@@ -1575,7 +1584,8 @@ extern "C" int fcg_dnc_ecdf(const double *x, int64_t n, int32_t d, const double 
     FCG_TRY(rank_dim(x, n, 1, 0, p, st));
     FCG_TRY(sorted_exclusive(w, p.r[0].order, n, false, p.lat, p.scratch, out, st));
   } else if (dom_ok) {
-    return self_dom2d(x, w, n, 1, 0, nullptr, nullptr, include_self, 0.0, div, p, q, out, st);
+    return self_dom2d(x, wptr(w, 1, n), n, 1, 0, nullptr, nullptr, include_self, 0.0, div, p, q,
+                      out, st);
   } else {
     Brute B;
     B.n = n;
@@ -1645,7 +1655,7 @@ extern "C" int fcg_kde_points_laplacian(const double *x, int64_t n, int32_t d, c
   }
 
   if (d == 2)  // group-ordered self dominance over the 4 orientations (dnc.py:459-468)
-    return self_dom2d(x, w, n, nw, 1, h, centre, 1, scale, 0.0, p, q, out, st);
+    return self_dom2d(x, wptr(w, nw, n), n, nw, 1, h, centre, 1, scale, 0.0, p, q, out, st);
   const int ncodes = 1 << d;
   FCG_TRY(rank_dim(x, n, 1, 0, p, st));
   for (int code = 0; code < ncodes; ++code) {
@@ -1791,9 +1801,11 @@ extern "C" int fcg_kde_points_matern32(const double *x, int64_t n, int32_t d, co
   if (d == 2) {
     // channels: 0 A, 1-2 B_k (sign s_k), 3-4 C_l (sign s_l); two per pass
     const unsigned m01[2] = {0u, 1u}, m23[2] = {2u, 1u}, m4[1] = {2u};
-    FCG_TRY(self_dom2d(x, wv, n, 2, 1, h, centre, 0, 0.0, 0.0, p, q, acc, st, m01));
-    FCG_TRY(self_dom2d(x, wv + 2 * n, n, 2, 1, h, centre, 0, 0.0, 0.0, p, q, acc + 2 * n, st, m23));
-    FCG_TRY(self_dom2d(x, wv + 4 * n, n, 1, 1, h, centre, 0, 0.0, 0.0, p, q, acc + 4 * n, st, m4));
+    FCG_TRY(self_dom2d(x, wptr(wv, 2, n), n, 2, 1, h, centre, 0, 0.0, 0.0, p, q, acc, st, m01));
+    FCG_TRY(self_dom2d(x, wptr(wv + 2 * n, 2, n), n, 2, 1, h, centre, 0, 0.0, 0.0, p, q,
+                       acc + 2 * n, st, m23));
+    FCG_TRY(self_dom2d(x, wptr(wv + 4 * n, 1, n), n, 1, 1, h, centre, 0, 0.0, 0.0, p, q,
+                       acc + 4 * n, st, m4));
   } else {  // d == 1: code 0 = strictly below (prefix), code 1 = strictly above (suffix)
     FCG_TRY(rank_dim(x, n, 1, 0, p, st));
     const unsigned masks[3] = {0u, 1u, 1u};
@@ -1848,7 +1860,7 @@ extern "C" int fcg_kde_points_laplacian_shard(const double *x, int64_t n, int32_
   for (int k = 0; k < d; ++k)
     if (!(h[k] > 0.0)) return fail(FCG_EINVAL, "bandwidth must be > 0");
   const double scale = 1.0 / (4.0 * (double)n * h[0] * h[1]);
-  return self_dom2d(x, w, n, nw, 1, h, centre, 1, scale, 0.0, p, q, out, as_stream(stream),
+  return self_dom2d(x, wptr(w, nw, n), n, nw, 1, h, centre, 1, scale, 0.0, p, q, out, as_stream(stream),
                     nullptr, shard, nshards);
 }
 
@@ -1870,6 +1882,31 @@ extern "C" int fcg_dnc_ecdf_shard(const double *x, int64_t n, int32_t d, const d
     return FCG_OK;
   }
   if (n == 0) return FCG_OK;
-  return self_dom2d(x, w, n, 1, 0, nullptr, nullptr, include_self, 0.0, scaled ? (double)n : 0.0,
+  return self_dom2d(x, wptr(w, 1, n), n, 1, 0, nullptr, nullptr, include_self, 0.0, scaled ? (double)n : 0.0,
                     p, q, out, as_stream(stream), nullptr, shard, nshards);
+}
+
+extern "C" int fcg_kde_points_laplacian_w2(const double *x, int64_t n, int32_t d, const double *w0,
+                                           const double *w1, int32_t nw, const double *h,
+                                           const double *centre, double *out, void *ws,
+                                           size_t *ws_bytes, void *stream) {
+  FCG_TRY(check_pts(n, d));
+  if (d != 2) return fail(FCG_EUNSUPPORTED, "per-channel weight pointers: d = 2 only");
+  if (nw < 1 || nw > 2) return fail(FCG_EUNSUPPORTED, "nw must be 1 or 2 weight vectors per call");
+  if (!dom_fits(n, 4 * nw)) return dom_too_large(n);
+  Workspace W(ws);
+  PtsWs p;
+  carve(W, p, n, 2, nw, true, true, 0);
+  SelfWs q{};
+  carve_self(W, q, n, nw);
+  if (ws == nullptr) {
+    *ws_bytes = W.bytes();
+    return FCG_OK;
+  }
+  if (n == 0) return FCG_OK;
+  for (int k = 0; k < d; ++k)
+    if (!(h[k] > 0.0)) return fail(FCG_EINVAL, "bandwidth must be > 0");
+  const double scale = 1.0 / (4.0 * (double)n * h[0] * h[1]);
+  return self_dom2d(x, WPtr{{w0, nw > 1 ? w1 : nullptr}}, n, nw, 1, h, centre, 1, scale, 0.0, p,
+                    q, out, as_stream(stream));
 }

@@ -97,10 +97,15 @@ def _kde_points(sample: Sample, weights_list, h: np.ndarray):
     n, d = x.shape
     ws = [None if w is None else _lib.to_device_f64(w) for w in weights_list]
     nw = len(ws)
+    out = torch.empty((nw, n), dtype=torch.float64, device=x.device)
+    if d == 2:  # one pointer per weight vector, NULL = unit: no stacked copy
+        _lib.call_ws("fcg_kde_points_laplacian_w2", _lib.ptr(x), n, d, _lib.ptr(ws[0]),
+                     _lib.ptr(ws[1] if nw > 1 else None), nw, _lib.f64_array(h),
+                     _lib.f64_array(c), _lib.ptr(out))
+        return out
     if any(w is None for w in ws):
         ws = [torch.ones(n, dtype=torch.float64, device=x.device) if w is None else w for w in ws]
     wmat = torch.stack(ws).contiguous()
-    out = torch.empty((nw, n), dtype=torch.float64, device=x.device)
     _lib.call_ws("fcg_kde_points_laplacian", _lib.ptr(x), n, d, _lib.ptr(wmat), nw,
                  _lib.f64_array(h), _lib.f64_array(c), _lib.ptr(out))
     return out
