@@ -1659,7 +1659,7 @@ extern "C" int fcg_kde_points_laplacian(const double *x, int64_t n, int32_t d, c
   const int ncodes = 1 << d;
   FCG_TRY(rank_dim(x, n, 1, 0, p, st));
   for (int code = 0; code < ncodes; ++code) {
-    KdeP kp;
+    KdeP kp{};  // smask = 0: plain (unsigned) channels
     kp.d = d;
     for (int k = 0; k < d; ++k) {
       const double sgn = ((code >> k) & 1) ? -1.0 : 1.0;  // DeltaVector.from_code
