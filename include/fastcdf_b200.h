@@ -272,6 +272,13 @@ int fcg_kde_points_laplacian_w2(const double *x, int64_t n, int32_t d, const dou
                                 const double *centre, double *out, void *ws, size_t *ws_bytes,
                                 void *stream);
 
+/* All-delta strict-dominance tables (dnc.py:608-632 kde_terms_dnc, _run_all_delta): psi and
+ * table are (n, 2^d) row-major; table[j][b] = sum of psi[i][b] over the points i != j with
+ * x_ik < x_jk where bit k of b is 0 and x_ik > x_jk where it is 1.  Requires distinct
+ * coordinates per dimension; d <= 6.  Direct tiled pairs, O(n^2). */
+int fcg_dominance_terms(const double *x, int64_t n, int32_t d, const double *psi, double *table,
+                        void *ws, size_t *ws_bytes, void *stream);
+
 /* matern32-additive KDE at the sample points (dnc.py:635-690 with family "matern32-additive"):
  * the d + 1 channels of dnc.py:661-669 are run as 2d + 1 Laplacian dominance channels whose
  * weights only change sign with the term (A = w e, B_k = s_k w e, C_l = s_l w xc_l e / h_l),

@@ -49,7 +49,7 @@ from .kernels import (
     uniform,
 )
 
-from .dnc import ecdf_dnc, kde_dnc
+from .dnc import DeltaTermTable, ecdf_dnc, kde_dnc, kde_terms_dnc, rank_tiebreak
 from .points import (
     ecdf_at_points,
     ecdf_esf_at_points,

@@ -57,6 +57,7 @@ _SIGS = {
     "fcg_kde_points_matern32": ([_P, _I64, _I32, _P, _P, _P, _P, _P, _SZP, _P], C.c_int),
     "fcg_kde_points_laplacian_w2": ([_P, _I64, _I32, _P, _P, _I32, _P, _P, _P, _P, _SZP, _P],
                                     C.c_int),
+    "fcg_dominance_terms": ([_P, _I64, _I32, _P, _P, _P, _SZP, _P], C.c_int),
     "fcg_kde_points_laplacian_shard": ([_P, _I64, _I32, _P, _I32, _P, _P, _I32, _I32, _P, _P, _SZP,
                                         _P], C.c_int),
     "fcg_dnc_ecdf_shard": ([_P, _I64, _I32, _P, _I32, _I32, _I32, _I32, _P, _P, _SZP, _P], C.c_int),

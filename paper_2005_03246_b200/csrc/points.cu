@@ -1910,3 +1910,67 @@ extern "C" int fcg_kde_points_laplacian_w2(const double *x, int64_t n, int32_t d
   return self_dom2d(x, WPtr{{w0, nw > 1 ? w1 : nullptr}}, n, nw, 1, h, centre, 1, scale, 0.0, p,
                     q, out, as_stream(stream));
 }
+
+// ---- all-delta dominance tables (kde_terms_dnc, dnc.py:608-632), tiled direct pairs -------
+// table[j][b] = sum of psi[i][b] over the points i strictly dominating j under the sign code b
+// (bit k of b: delta_k = -1, i.e. x_ik > x_jk; otherwise x_ik < x_jk), i != j.  With distinct
+// coordinates every pair (i, j) lands in exactly one code: b(i, j) = sum_k [x_ik > x_jk] << k.
+namespace fcg {
+namespace {
+constexpr int kTermQ = 128;  // queries per CTA (one per thread)
+constexpr int kTermS = 64;   // sources per shared-memory tile
+
+__global__ void __launch_bounds__(kTermQ) terms_kernel(const double *__restrict__ x, int64_t n,
+                                                       int d, const double *__restrict__ psi,
+                                                       double *__restrict__ table) {
+  extern __shared__ double t_smem[];
+  const int nc = 1 << d, stride = nc + 1;           // per-thread accumulator row (bank skew)
+  double *s_acc = t_smem;                           // [kTermQ][stride]
+  double *s_x = s_acc + kTermQ * stride;            // [kTermS][d]
+  double *s_psi = s_x + kTermS * FCG_MAX_DIM;       // [kTermS][nc]
+  const int64_t t = (int64_t)blockIdx.x * kTermQ + threadIdx.x;
+  double xt[FCG_MAX_DIM];
+  for (int k = 0; k < d; ++k) xt[k] = t < n ? x[t * d + k] : 0.0;
+  double *acc = s_acc + threadIdx.x * stride;
+  for (int b = 0; b < nc; ++b) acc[b] = 0.0;
+  for (int64_t s0 = 0; s0 < n; s0 += kTermS) {
+    const int ns = (int)(n - s0 < kTermS ? n - s0 : kTermS);
+    __syncthreads();
+    for (int i = threadIdx.x; i < ns * d; i += blockDim.x) s_x[i] = x[s0 * d + i];
+    for (int i = threadIdx.x; i < ns * nc; i += blockDim.x) s_psi[i] = psi[s0 * nc + i];
+    __syncthreads();
+    if (t < n) {
+      for (int j = 0; j < ns; ++j) {
+        if (s0 + j == t) continue;
+        int b = 0;
+        for (int k = 0; k < d; ++k) b |= (s_x[j * d + k] > xt[k] ? 1 : 0) << k;
+        acc[b] += s_psi[j * nc + b];
+      }
+    }
+  }
+  if (t < n)
+    for (int b = 0; b < nc; ++b) table[t * nc + b] = acc[b];
+}
+}  // namespace
+}  // namespace fcg
+
+extern "C" int fcg_dominance_terms(const double *x, int64_t n, int32_t d, const double *psi,
+                                   double *table, void *ws, size_t *ws_bytes, void *stream) {
+  FCG_TRY(check_pts(n, d));
+  if (d > 6) return fail(FCG_EUNSUPPORTED, "dominance tables support d <= 6 (2^d columns)");
+  if (ws == nullptr) {
+    *ws_bytes = 256;
+    return FCG_OK;
+  }
+  if (n == 0) return FCG_OK;
+  const int nc = 1 << d;
+  const size_t smem = ((size_t)kTermQ * (nc + 1) + (size_t)kTermS * FCG_MAX_DIM +
+                       (size_t)kTermS * nc) * sizeof(double);
+  cudaStream_t st = as_stream(stream);
+  FCG_CUDA_TRY(cudaFuncSetAttribute(terms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+  FCG_PROF("pts_terms", st);
+  terms_kernel<<<(unsigned)ceil_div(n, kTermQ), kTermQ, smem, st>>>(x, n, d, psi, table);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}

@@ -13,6 +13,7 @@ exponentials on midrange-centred coordinates, the self term w_j added before the
 from __future__ import annotations
 
 import time
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -22,6 +23,7 @@ from .core import (
     EXP_OVERFLOW_GUARD,
     POINT_ALIGNED,
     Bandwidth,
+    DeltaVector,
     EvalResult,
     OverflowGuardError,
     ParameterError,
@@ -143,3 +145,71 @@ def kde_dnc(sample: Sample, kernel: KernelSpec, bandwidth: Bandwidth) -> EvalRes
     return EvalResult(_out(sample, vals), POINT_ALIGNED, {
         "method": "dnc", "kernel": str(kernel),
         "runtime_seconds": time.perf_counter() - t0})
+
+
+@dataclass(frozen=True)
+class DeltaTermTable:
+    """Per-point, per-sign-code weighted strict-dominance sums (dnc.py:475-487): column ``b``
+    of ``table`` sums ``psi[i, b]`` over the points i strictly dominating j under
+    ``DeltaVector.from_code(b, dim)`` (the point itself excluded)."""
+
+    table: object
+    psi: object
+    dim: int
+
+    def delta_for_column(self, b: int) -> DeltaVector:
+        return DeltaVector.from_code(b, self.dim)
+
+
+def kde_terms_dnc(sample: Sample, bandwidth: Bandwidth,
+                  monomial: tuple[int, int, int, int] = (0, 0, 0, 0)) -> DeltaTermTable:
+    """All-delta dominance tables for exponential kernel compositions (dnc.py:608-632):
+    psi(x_i, delta) = w_i x_{l,i}^p x_{m,i}^q exp(sum_k delta_k x_{k,i} / h_k), formed exactly
+    as the reference does (numpy, host inputs) and summed over the dominating points on the
+    device (``fcg_dominance_terms``, tiled direct pairs)."""
+    import torch
+
+    sample = as_sample(sample)
+    _require_distinct(sample)
+    h = _diag_bandwidth(sample, bandwidth)
+    _span_guard_and_centre(sample, h)
+    l, m, p, q = monomial
+    d, n = sample.dim, sample.count
+    if not (0 <= l < d and 0 <= m < d) or p < 0 or q < 0:
+        raise ParameterError(f"invalid monomial {monomial} for dimension {d}")
+    if sample.on_device:
+        pts = _lib.to_device_f64(sample.points)
+        w = _lib.to_device_f64(sample.weights) if sample.weights is not None else None
+        poly = pts[:, l] ** p * pts[:, m] ** q
+        psi = torch.empty((n, 1 << d), dtype=torch.float64, device=pts.device)
+        for code in range(1 << d):
+            signs = torch.tensor(DeltaVector.from_code(code, d).as_array() / h, device=pts.device)
+            psi[:, code] = (w if w is not None else 1.0) * poly * torch.exp(pts @ signs)
+        psi_d, x = psi, pts
+    else:
+        pts = np.ascontiguousarray(sample.points, dtype=np.float64)
+        w = np.ones(n) if sample.weights is None else np.asarray(sample.weights, dtype=np.float64)
+        poly = pts[:, l] ** p * pts[:, m] ** q
+        psi = np.empty((n, 1 << d))
+        for code in range(1 << d):
+            signs = DeltaVector.from_code(code, d).as_array()
+            psi[:, code] = w * poly * np.exp(pts @ (signs / h))
+        psi_d, x = _lib.to_device_f64(psi), _lib.to_device_f64(pts)
+    table = torch.empty((n, 1 << d), dtype=torch.float64, device=x.device)
+    _lib.call_ws("fcg_dominance_terms", _lib.ptr(x), n, d, _lib.ptr(psi_d), _lib.ptr(table))
+    return DeltaTermTable(table if sample.on_device else _lib.to_host(table), psi, d)
+
+
+def rank_tiebreak(points):
+    """Each dimension's values replaced by their stable sort ranks (dnc.py:502-520): ties
+    broken by input index, an infinitesimal index-ordered perturbation for ECDF counting.  The
+    ranks come from the device ranking (``fcg_rank_f64``, stable order)."""
+    on_dev = _lib.is_torch(points)
+    pts = _lib.to_device_f64(points)
+    if pts.dim() == 1:
+        pts = pts.reshape(-1, 1)
+    out = pts.new_empty(pts.shape)
+    for k in range(pts.shape[1]):
+        _, pos, _, _, _ = _lib.rank_f64(pts[:, k].contiguous())
+        out[:, k] = pos.to(out.dtype)
+    return out if on_dev else _lib.to_host(out)

@@ -378,3 +378,67 @@ def test_rank_f64_device_tensor_and_empty():
     assert dense.cpu().tolist() == [2, 1, 2, 0]
     outs = fcb.rank_f64(np.empty(0))
     assert all(o.size == 0 for o in outs)
+
+
+# ---- kde_terms_dnc / rank_tiebreak (dnc.py:502-520, 608-632; reference tests test_dnc.py:95-146)
+
+def _brute_delta_table(points, psi):
+    n, d = points.shape
+    out = np.zeros((n, 1 << d))
+    for code in range(1 << d):
+        signs = fcb.DeltaVector.from_code(code, d).as_array()
+        sp = points * signs
+        for j in range(n):
+            out[j, code] = psi[np.all(sp < sp[j], axis=1), code].sum()
+    return out
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 4, 5])
+def test_kde_terms_matches_brute_force(d):
+    rng = np.random.default_rng(50 + d)
+    n = 120
+    pts = rng.standard_normal((n, d))
+    w = rng.uniform(0.5, 2.0, n)
+    h = rng.uniform(0.6, 1.4, d)
+    monomial = (int(rng.integers(0, d)), int(rng.integers(0, d)), 1, 0)
+    tt = fcb.kde_terms_dnc(fcb.validate_sample(pts, w), fcb.Bandwidth.diag(h), monomial)
+    l, m, p, q = monomial
+    psi = np.empty((n, 1 << d))
+    for code in range(1 << d):
+        signs = fcb.DeltaVector.from_code(code, d).as_array()
+        psi[:, code] = w * pts[:, l] ** p * pts[:, m] ** q * np.exp(pts @ (signs / h))
+    np.testing.assert_array_equal(tt.psi, psi)
+    expected = _brute_delta_table(pts, psi)
+    assert np.max(np.abs(tt.table - expected)) <= 1e-13 * max(1.0, np.max(np.abs(expected)))
+    assert tt.delta_for_column(1) == fcb.DeltaVector.from_code(1, d)
+
+
+def test_kde_terms_fingerprint_and_guards():
+    rng = np.random.default_rng(81)
+    pts = rng.standard_normal((3000, 3))
+    w = rng.standard_normal(3000)  # signed weights: any double-counted pair breaks equality
+    tt = fcb.kde_terms_dnc(fcb.validate_sample(pts, w), fcb.Bandwidth.diag(np.full(3, 5.0)))
+    q = rng.integers(0, 3000, 50)
+    exp_q = np.zeros((50, 8))
+    for code in range(8):
+        sp = pts * fcb.DeltaVector.from_code(code, 3).as_array()
+        for a, j in enumerate(q):
+            exp_q[a, code] = tt.psi[np.all(sp < sp[j], axis=1), code].sum()
+    assert np.max(np.abs(tt.table[q] - exp_q)) <= 1e-12
+    single = fcb.kde_terms_dnc(fcb.validate_sample([[0.3, 0.4]]), fcb.Bandwidth.diag([1.0, 1.0]))
+    np.testing.assert_array_equal(single.table, np.zeros((1, 4)))
+    with pytest.raises(fcb.ParameterError):
+        fcb.kde_terms_dnc(fcb.validate_sample([[0.0], [1.0]]), fcb.Bandwidth.diag([1.0]), (2, 0, 1, 0))
+    with pytest.raises(fcb.TieError):
+        fcb.kde_terms_dnc(fcb.validate_sample([[0.0, 1.0], [0.0, 2.0]]), fcb.Bandwidth.diag([1.0, 1.0]))
+
+
+def test_rank_tiebreak_matches_stable_argsort():
+    rng = np.random.default_rng(9)
+    pts = np.floor(rng.random((5000, 3)) * 17)
+    ref = np.empty_like(pts)
+    for k in range(3):
+        ref[np.argsort(pts[:, k], kind="stable"), k] = np.arange(5000)
+    np.testing.assert_array_equal(fcb.rank_tiebreak(pts), ref)
+    # ranks restore distinct coordinates: the strict ECDF then counts index-ordered ties
+    assert fcb.validate_sample(fcb.rank_tiebreak(pts)).distinct
