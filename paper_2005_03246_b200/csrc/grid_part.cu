@@ -334,7 +334,7 @@ __device__ __forceinline__ void tile_store(T *__restrict__ dst, const T *tile, i
 template <int SE>
 __global__ void __launch_bounds__(kPlaneThreads, 3) plane_count_kernel(
     PartGeo p, const int32_t *__restrict__ start, const int32_t *__restrict__ vals, int rev_r,
-    int rev_c, int32_t *__restrict__ lat) {
+    int rev_c, int32_t *__restrict__ lat, const uint32_t *__restrict__ pkeys) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int W = (int)p.W, R = (int)p.R;
   const int G = (int)blockDim.x >= W ? (int)blockDim.x / W : 1;
@@ -354,10 +354,22 @@ __global__ void __launch_bounds__(kPlaneThreads, 3) plane_count_kernel(
     constexpr int KB = 8;
     for (int32_t qb = q0 + threadIdx.x; qb < q1; qb += KB * blockDim.x) {
       int32_t v[KB];
+      if (pkeys) {  // packed keys: in-block cell r_in << col_bits | col
+        const uint32_t cm = (1u << p.col_bits) - 1u;
 #pragma unroll
-      for (int u = 0; u < KB; ++u) {
-        const int32_t q = qb + u * (int32_t)blockDim.x;
-        v[u] = q < q1 ? vals[q] : -1;
+        for (int u = 0; u < KB; ++u) {
+          const int32_t q = qb + u * (int32_t)blockDim.x;
+          const uint32_t kk = q < q1 ? pkeys[q] : 0u;
+          v[u] = q < q1 ? (int32_t)(((kk & ((1u << p.cell_bits) - 1u)) >> p.col_bits) * (uint32_t)W +
+                                    (kk & cm))
+                        : -1;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < KB; ++u) {
+          const int32_t q = qb + u * (int32_t)blockDim.x;
+          v[u] = q < q1 ? vals[q] : -1;
+        }
       }
 #pragma unroll
       for (int u = 0; u < KB; ++u)
@@ -2005,13 +2017,19 @@ void carve_part(Workspace &W, PartBufs &b, int64_t n, int64_t NB) {
 
 int partition(const double *x, int64_t n, int d, const double *knots, const BinGrid &g,
               const PartGeo &p, int64_t NB, int nbits, PartBufs &b, cudaStream_t st) {
-  // equal bucket keys may come out in any order (the plane kernel only groups by bucket)
+  // equal bucket keys may come out in any order (the plane kernel only groups by bucket).
+  // Packed keys (p.cell_bits > 0): bucket << cell_bits | in-block cell, keys only, sorted on
+  // the bucket bits [cell_bits, cell_bits + nbits): half the bytes per sort pass.
+  const int lo = p.cell_bits;
+  int32_t *vals = lo > 0 ? nullptr : b.vals;
   if (nbits > 8 && nbits <= 16) {  // high digit first, then the low digit per segment
-    FCG_TRY(launch_part_bin_tiles(x, n, d, knots, g, p, b.keys, b.vals, b.rw.hist, st, kSortTile, 8));
-    FCG_TRY(msd2_sort_pairs_u32(b.keys, b.vals, n, nbits, b.rw, b.sw, st, true));
+    FCG_TRY(launch_part_bin_tiles(x, n, d, knots, g, p, b.keys, vals, b.rw.hist, st, kSortTile,
+                                  lo + 8));
+    FCG_TRY(msd2_sort_pairs_u32(b.keys, vals, n, nbits, b.rw, b.sw, st, true, lo));
   } else {
-    FCG_TRY(launch_part_bin_tiles(x, n, d, knots, g, p, b.keys, b.vals, b.rw.hist, st));
-    FCG_TRY(radix_sort_pairs<uint32_t>(b.keys, b.vals, n, 0, ((nbits + 7) / 8) * 8, b.rw, st,
+    FCG_TRY(launch_part_bin_tiles(x, n, d, knots, g, p, b.keys, vals, b.rw.hist, st, kSortTile,
+                                  lo));
+    FCG_TRY(radix_sort_pairs<uint32_t>(b.keys, vals, n, lo, lo + ((nbits + 7) / 8) * 8, b.rw, st,
                                        false, true));
   }
   FCG_PROF("part_bucket_start", st);
@@ -2100,6 +2118,14 @@ PartPlan plan_ecdf_partition(const BinGrid &g, int64_t n) {
   pl.NB = pl.NP * pl.nrb;
   if (pl.NB >= (int64_t(1) << 31) - 2 || n >= (int64_t(1) << 31) - 1) return pl;
   pl.nbits = bits_for(pl.NB);  // kDead's low nbits are all ones > NB - 1
+  // packed keys bucket << cell_bits | r_in << col_bits | col when they fit 31 bits (the dead
+  // key 0xFFFFFFFF then sorts last): keys only through the sort
+  static const bool unpacked = getenv("FCG_ECDF_UNPACKED") && getenv("FCG_ECDF_UNPACKED")[0] == '1';
+  const int colb = bits_for(pl.W - 1), rowb = pl.R > 1 ? bits_for(pl.R - 1) : 0;
+  if (!unpacked && colb + rowb > 0 && pl.nbits + colb + rowb <= 31) {
+    pl.col_bits = colb;  // (nbits stays bits_for(NB): the dead key's bucket bits exceed NB - 1)
+    pl.cell_bits = colb + rowb;
+  }
   pl.ok = true;
   return pl;
 }
@@ -2128,6 +2154,8 @@ int ecdf_partitioned(const double *x, int64_t n, const double *knots, const BinG
   p.nrb = pl.nrb;
   p.H = pl.H;
   p.ecdf = 1;
+  p.cell_bits = pl.cell_bits;  // > 0: packed keys (no value array)
+  p.col_bits = pl.col_bits;
   FCG_TRY(partition(x, n, d, knots, g, p, pl.NB, pl.nbits, b, st));
   const int64_t G = seg_rows(kPlaneThreads, pl.W, 4);
   const size_t smem = (size_t)(pl.R * pl.W + pl.W + G * pl.W) * sizeof(int32_t);
@@ -2137,7 +2165,7 @@ int ecdf_partitioned(const double *x, int64_t n, const double *knots, const BinG
     auto kern = se == 4 ? plane_count_kernel<4> : (se == 8 ? plane_count_kernel<8> : plane_count_kernel<0>);
     FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<(unsigned)pl.NP, kPlaneThreads, smem, st>>>(p, b.start, b.vals, rev[d - 2], rev[d - 1],
-                                                      lat);
+                                                      lat, p.cell_bits > 0 ? b.keys : nullptr);
     FCG_LAUNCH_CHECK();
   }
   Epi inplace;

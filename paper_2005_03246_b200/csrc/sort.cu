@@ -284,7 +284,8 @@ __global__ void __launch_bounds__(kSortThreads, 3) radix_scatter_kernel(
     const int64_t i = base + (int64_t)j * 32 + lane;
     const bool ok = i < n;
     k[j] = ok ? kin[i] : KeyT(0);
-    v[j] = ok ? (vin ? vin[i] : (int32_t)i) : 0;  // vin == NULL: the values are the positions
+    // vin == NULL: the values are the positions; vout == NULL (and no records): keys only
+    v[j] = (ok && (vout || GW > 0)) ? (vin ? vin[i] : (int32_t)i) : 0;
   }
   if constexpr (STABLE) {
 #pragma unroll
@@ -356,7 +357,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) radix_scatter_kernel(
 #pragma unroll
       for (int w = 0; w < GW; ++w) __stcs(rec_out + (int64_t)w * rec_n + dst, f[w]);
     } else {
-      vout[dst] = s_val[pos];
+      if (vout) vout[dst] = s_val[pos];
     }
   }
 }
@@ -696,9 +697,10 @@ int seg_sort_pairs_u32(uint32_t *keys, int32_t *vals, int64_t n, int seg_shift, 
 }
 
 int msd2_sort_pairs_u32(uint32_t *keys, int32_t *vals, int64_t n, int nbits, const RadixWs &ws,
-                        const SegSortWs &sw, cudaStream_t st, bool first_hist_ready) {
+                        const SegSortWs &sw, cudaStream_t st, bool first_hist_ready, int lo) {
   if (n <= 1) return FCG_OK;
   if (nbits <= 8 || nbits > 16) return fail(FCG_EINVAL, "msd2 sort: 9..16 key bits");
+  // the sorted field is bits [lo, lo + nbits) (lo > 0: packed keys, the low bits ride along)
   const int64_t tiles = ceil_div(n, kSortTile);
   uint32_t *kb = reinterpret_cast<uint32_t *>(ws.keys_alt);
   int32_t *vb = ws.vals_alt;
@@ -707,26 +709,26 @@ int msd2_sort_pairs_u32(uint32_t *keys, int32_t *vals, int64_t n, int nbits, con
     const FlatMap map{n, tiles};
     if (!first_hist_ready) {
       FCG_PROF("radix_hist", st);
-      radix_hist_kernel<uint32_t, FlatMap><<<(unsigned)tiles, kSortThreads, 0, st>>>(keys, map, 8, ws.hist);
+      radix_hist_kernel<uint32_t, FlatMap><<<(unsigned)tiles, kSortThreads, 0, st>>>(keys, map, lo + 8, ws.hist);
       FCG_LAUNCH_CHECK();
     }
     FCG_TRY(scan_i32(ws.hist, ws.hist, 256 * tiles, false, ws.partial, st));
     FCG_PROF("radix_scatter", st);
     auto kern = radix_scatter_kernel<uint32_t, false, FlatMap, 0>;
     FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    kern<<<(unsigned)tiles, kSortThreads, sm, st>>>(keys, vals, kb, vb, map, 8, ws.hist, nullptr,
-                                                    nullptr, 0);
+    kern<<<(unsigned)tiles, kSortThreads, sm, st>>>(keys, vals, kb, vals ? vb : nullptr, map,
+                                                    lo + 8, ws.hist, nullptr, nullptr, 0);
     FCG_LAUNCH_CHECK();
   }
   const int64_t tmax = (int64_t)seg_sort_tiles(n);
   {  // pass 2: the low digit inside each high-digit segment, alt -> keys
     FCG_PROF("radix_hist", st);
-    seg_bounds_kernel<<<(unsigned)ceil_div(n, 256 * 8), 256, 0, st>>>(kb, n, 8, sw.seg_start);
+    seg_bounds_kernel<<<(unsigned)ceil_div(n, 256 * 8), 256, 0, st>>>(kb, n, lo + 8, sw.seg_start);
     FCG_LAUNCH_CHECK();
     seg_tiles_kernel<<<1, kSortSegs, 0, st>>>(sw.seg_start, sw.tile_base, sw.tile_seg);
     FCG_LAUNCH_CHECK();
     const SegMap map{sw.seg_start, sw.tile_base, sw.tile_seg};
-    radix_hist_kernel<uint32_t, SegMap><<<(unsigned)tmax, kSortThreads, 0, st>>>(kb, map, 0, ws.hist);
+    radix_hist_kernel<uint32_t, SegMap><<<(unsigned)tmax, kSortThreads, 0, st>>>(kb, map, lo, ws.hist);
     FCG_LAUNCH_CHECK();
   }
   FCG_TRY(scan_i32(ws.hist, ws.hist, 256 * tmax, false, ws.partial, st));
@@ -735,8 +737,8 @@ int msd2_sort_pairs_u32(uint32_t *keys, int32_t *vals, int64_t n, int nbits, con
     const SegMap map{sw.seg_start, sw.tile_base, sw.tile_seg};
     auto kern = radix_scatter_kernel<uint32_t, false, SegMap, 0>;
     FCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    kern<<<(unsigned)tmax, kSortThreads, sm, st>>>(kb, vb, keys, vals, map, 0, ws.hist, nullptr,
-                                                   nullptr, 0);
+    kern<<<(unsigned)tmax, kSortThreads, sm, st>>>(kb, vals ? vb : nullptr, keys, vals, map, lo,
+                                                   ws.hist, nullptr, nullptr, 0);
     FCG_LAUNCH_CHECK();
   }
   return FCG_OK;

@@ -55,7 +55,7 @@ int seg_sort_pairs_u32(uint32_t *keys, int32_t *vals, int64_t n, int seg_shift, 
 // low digit inside each high-digit segment.  Result in keys / vals.  Workspace: ws.hist >=
 // 256 * seg_sort_tiles(n) + 1 ints and sw.
 int msd2_sort_pairs_u32(uint32_t *keys, int32_t *vals, int64_t n, int nbits, const RadixWs &ws,
-                        const SegSortWs &sw, cudaStream_t st, bool first_hist_ready);
+                        const SegSortWs &sw, cudaStream_t st, bool first_hist_ready, int lo = 0);
 
 // Stable sort of 64-bit keys over the digits where they differ (one AND/OR reduction and a
 // 16-byte device-to-host read decide which 8-bit passes are identities).  Synchronises `st`.
