@@ -14,6 +14,9 @@
 #include <thread>
 #include <vector>
 
+#include <sys/mman.h>
+#include <unistd.h>
+
 #include "common.cuh"
 
 namespace fcg {
@@ -161,6 +164,12 @@ extern "C" int fcg_copy_d2h(void *dst, const void *src, size_t bytes, void *stre
   std::lock_guard<std::mutex> lk(r.mu);
   FCG_TRY(ring_init(r));
   cudaStream_t st = as_stream(stream);
+  {  // a fresh numpy result is first touched here: ask for 2 MB pages (THP in madvise mode)
+    const uintptr_t pg = (uintptr_t)sysconf(_SC_PAGESIZE);
+    const uintptr_t a = (reinterpret_cast<uintptr_t>(dst) + pg - 1) & ~(pg - 1);
+    const uintptr_t e = (reinterpret_cast<uintptr_t>(dst) + bytes) & ~(pg - 1);
+    if (e > a) madvise(reinterpret_cast<void *>(a), e - a, MADV_HUGEPAGE);  // advisory only
+  }
   const size_t nch = (bytes + kChunk - 1) / kChunk;
   auto issue = [&](size_t i) -> int {
     const int b = (int)(i % kRing);
