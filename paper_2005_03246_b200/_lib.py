@@ -125,9 +125,16 @@ def device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+def _raw_stream(torch, dev: int) -> int:
+    """The current CUDA stream of device `dev` as an integer handle (the cheap accessor when
+    this torch build has it: current_stream() builds a Stream object per call)."""
+    f = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    return f(dev) if f is not None else torch.cuda.current_stream(dev).cuda_stream
+
+
 def stream_handle():
     torch = _torch()
-    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return C.c_void_p(_raw_stream(torch, torch.cuda.current_device()))
 
 
 def ptr(t) -> C.c_void_p:
@@ -151,15 +158,16 @@ def call_ws(name: str, *args):
     torch = _torch()
     lib = _lib if _lib is not None else load_library()
     fn = getattr(lib, name)
-    stream = torch.cuda.current_stream()
-    sh = C.c_void_p(stream.cuda_stream)
+    dev = torch.cuda.current_device()
+    raw = _raw_stream(torch, dev)
+    sh = C.c_void_p(raw)
     nbytes = C.c_size_t(0)
     check(fn(*args, None, C.byref(nbytes), sh), name)
     need = max(int(nbytes.value), 1)
-    key = (threading.get_ident(), stream.cuda_stream)
+    key = (threading.get_ident(), dev, raw)
     ws = _ws_cache.get(key)
-    if ws is None or ws.numel() < need or ws.device != stream.device:
-        ws = torch.empty(need, dtype=torch.uint8, device=stream.device)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=torch.device("cuda", dev))
         if need <= _WS_CACHE_MAX:
             _ws_cache[key] = ws
     check(fn(*args, C.c_void_p(ws.data_ptr()), C.byref(nbytes), sh), name)

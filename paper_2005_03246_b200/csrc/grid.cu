@@ -21,6 +21,7 @@
 #include <cooperative_groups.h>
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 
 #include "common.cuh"
 #include "scan.cuh"
@@ -113,8 +114,16 @@ template <typename T, int EK>
 __global__ void __launch_bounds__(kSmallThreads, 4) small2d_kernel(
     const double *__restrict__ x, int64_t n, const double *__restrict__ w,
     const double *__restrict__ knots, BinGrid g, int rev0, int rev1, T *__restrict__ lat,
-    T *__restrict__ csum, Epi e) {
+    T *__restrict__ csum, Epi e, unsigned long long *trace) {
   namespace cg = cooperative_groups;
+  auto stamp = [&](int i) {  // dev timing of the phases (trace != nullptr)
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[i] = t;
+    }
+  };
+  stamp(0);
   extern __shared__ double s_knots[];
   __shared__ double s_z0[FCG_MAX_DIM], s_idz[FCG_MAX_DIM];
   const double *kb = stage_knots(g, knots, s_knots, s_z0, s_idz);
@@ -124,6 +133,7 @@ __global__ void __launch_bounds__(kSmallThreads, 4) small2d_kernel(
   for (int i = tid; i < L; i += nth) lat[i] = T(0);
   __syncthreads();
   cg::this_grid().sync();
+  stamp(1);
   {
     const double *k0 = kb + g.koff[0], *k1 = kb + g.koff[1];
     const int M0 = (int)g.m[0], M1 = (int)g.m[1], le0 = g.le[0], le1 = g.le[1];
@@ -139,6 +149,7 @@ __global__ void __launch_bounds__(kSmallThreads, 4) small2d_kernel(
     }
   }
   cg::this_grid().sync();
+  stamp(2);
   {  // axis 1: warp per row; rows of <= 256 columns load all 8 segments first (one round trip)
     const int lane = threadIdx.x & 31;
     for (int r = tid >> 5; r < m0; r += nth >> 5) {
@@ -185,6 +196,7 @@ __global__ void __launch_bounds__(kSmallThreads, 4) small2d_kernel(
     }
   }
   cg::this_grid().sync();
+  stamp(3);
   // axis 0: C chunks of Dc rows; loops of fixed trip count with independent loads
   const int C = m0 < kSmallChunks ? m0 : kSmallChunks;
   const int Dc = (m0 + C - 1) / C;
@@ -192,33 +204,63 @@ __global__ void __launch_bounds__(kSmallThreads, 4) small2d_kernel(
     const int c = t / m1, col = t - c * m1;
     const int a = c * Dc, b = a + Dc < m0 ? a + Dc : m0;
     T s = T(0);
-#pragma unroll 16
-    for (int r = a; r < b; ++r) s += lat[r * m1 + col];
+    for (int r0 = a; r0 < b; r0 += kSmallChunks) {
+      T v[kSmallChunks];
+#pragma unroll
+      for (int u = 0; u < kSmallChunks; ++u) v[u] = r0 + u < b ? lat[(r0 + u) * m1 + col] : T(0);
+#pragma unroll
+      for (int u = 0; u < kSmallChunks; ++u) s += v[u];
+    }
     csum[t] = s;
   }
   cg::this_grid().sync();
+  stamp(4);
   double *of = static_cast<double *>(e.out);
   int64_t *oi = static_cast<int64_t *>(e.out);
-  const double div = e.div;
+  const double div = e.div, rdiv = e.div > 0.0 ? 1.0 / e.div : 0.0;
   for (int t = tid; t < C * m1; t += nth) {  // carry-in + walk (scan order) + epilogue
     const int c = t / m1, col = t - c * m1;
+    // every load of the thread is issued before the first store (the output may alias the
+    // lattice as far as the compiler knows, which would serialise load / store pairs)
+    T cs[kSmallChunks];
+#pragma unroll
+    for (int q = 0; q < kSmallChunks; ++q) cs[q] = csum[(q < C ? q : 0) * m1 + col];
     T run = T(0);
 #pragma unroll
     for (int q = 0; q < kSmallChunks; ++q)
-      if (q < C && (rev0 ? q > c : q < c)) run += csum[q * m1 + col];
+      if (q < C && (rev0 ? q > c : q < c)) run += cs[q];
     const int a = c * Dc, b = a + Dc < m0 ? a + Dc : m0;
-#pragma unroll 16
-    for (int k = 0; k < b - a; ++k) {
-      const int f = (rev0 ? b - 1 - k : a + k) * m1 + col;
-      run += lat[f];
-      if constexpr (EK == EPI_F64) {
-        double v = (double)run;
-        if (div > 0.0) v = v / div;
-        of[f] = v;
-      } else {
-        oi[f] = (int64_t)run;
+    for (int k0 = 0; k0 < b - a; k0 += kSmallChunks) {
+      T v[kSmallChunks];
+#pragma unroll
+      for (int u = 0; u < kSmallChunks; ++u) {
+        const int k = k0 + u;
+        v[u] = k < b - a ? lat[(rev0 ? b - 1 - k : a + k) * m1 + col] : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < kSmallChunks; ++u) {
+        const int k = k0 + u;
+        if (k >= b - a) break;
+        run += v[u];
+        const int f = (rev0 ? b - 1 - k : a + k) * m1 + col;
+        if constexpr (EK == EPI_F64) {
+          double vv = (double)run;
+          if (div > 0.0) {
+            // integer counts: the Markstein-corrected reciprocal is the IEEE quotient
+            // (common.cuh div_rn, checked by tests/c/div_rn_check.c); weighted sums divide
+            if constexpr (sizeof(T) == 4) vv = div_rn(vv, div, rdiv);
+            else vv = vv / div;
+          }
+          of[f] = vv;
+        } else {
+          oi[f] = (int64_t)run;
+        }
       }
     }
+  }
+  if (trace) {
+    cg::this_grid().sync();
+    stamp(5);
   }
 }
 
@@ -246,11 +288,23 @@ int launch_small2d(const double *x, int64_t n, const double *w, const double *kn
                                      (int64_t)per_sm * sm_count());
   blocks = std::max<int64_t>(blocks, 1);
   int r0 = rev0 ? 1 : 0, r1 = rev1 ? 1 : 0;
+  // FCG_SMALL_TRACE=1 (dev): phase timestamps, printed after the launch (synchronises)
+  static unsigned long long *trace = nullptr;
+  static const bool want_trace = getenv("FCG_SMALL_TRACE") && getenv("FCG_SMALL_TRACE")[0] == '1';
+  if (want_trace && !trace) FCG_CUDA_TRY(cudaMalloc(&trace, 8 * sizeof(unsigned long long)));
   void *args[] = {(void *)&x, (void *)&n, (void *)&w, (void *)&knots, (void *)&g, (void *)&r0,
-                  (void *)&r1, (void *)&lat, (void *)&csum, (void *)&e};
+                  (void *)&r1, (void *)&lat, (void *)&csum, (void *)&e, (void *)&trace};
   FCG_PROF(sizeof(T) == 4 ? "small2d_count" : "small2d_w", st);
   FCG_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)kern, dim3((unsigned)blocks),
                                            dim3(kSmallThreads), args, smem, st));
+  if (trace) {
+    unsigned long long h[8];
+    FCG_CUDA_TRY(cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st));
+    FCG_CUDA_TRY(cudaStreamSynchronize(st));
+    fprintf(stderr, "small2d blocks=%lld phases(us):", (long long)blocks);
+    for (int i = 1; i <= 5; ++i) fprintf(stderr, " %.2f", (h[i] - h[i - 1]) * 1e-3);
+    fprintf(stderr, "\n");
+  }
   return FCG_OK;
 }
 
