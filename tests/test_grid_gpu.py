@@ -513,3 +513,55 @@ def test_bench_ladder_small(tmp_path):
     rows = harness.bench_ladder("kde", ["fastsum", "dnc"], [2], [500], repeats=1)
     assert len(rows) == 2
     assert (tmp_path / "l.csv").read_text().startswith("task,method,dim,n,repeat,seconds\n")
+
+
+@pytest.mark.parametrize("m", [(256, 256), (3, 1000), (17, 300), (1000, 5), (1024, 1024), (1, 7)])
+def test_small2d_one_launch_vs_oracle(m, oracle):
+    """The one-launch small 2-D pipeline (lattices <= 2^20 cells) on every shape class: rows
+    longer than 256 (generic row loop), fewer rows than axis-0 chunks, uneven chunks, the 2^20
+    boundary; counts, int64 counts, weighted sums, every delta and the ESF."""
+    oracle.set_threads(0)
+    rng = np.random.default_rng(sum(m))
+    n = 40_000
+    x = rng.standard_normal((n, 2))
+    knots = [np.sort(rng.uniform(-2.5, 2.5, mk)) if mk > 1 else np.array([0.1]) for mk in m]
+    knots[0] = np.unique(np.concatenate([knots[0], x[:2, 0]]))  # knot hits
+    grid = _grid(knots)
+    w = rng.uniform(0.1, 2.0, n)
+    for delta in [(1, 1), (-1, 1), (1, -1), (-1, -1)]:
+        dv = fcb.DeltaVector(delta)
+        ref = oracle.ecdf_fastsum(x, None, knots, delta, scaled=False)
+        np.testing.assert_array_equal(fcb.ecdf_fastsum_counts(fcb.validate_sample(x), grid, dv),
+                                      ref.astype(np.int64))
+        np.testing.assert_array_equal(fcb.ecdf_fastsum(fcb.validate_sample(x), grid, dv).values,
+                                      ref / n)  # count / N: the IEEE quotient bit for bit
+        assert_rel(fcb.ecdf_fastsum(fcb.validate_sample(x, w), grid, dv).values,
+                   oracle.ecdf_fastsum(x, w, knots, delta), REL_F64)
+    np.testing.assert_array_equal(fcb.esf_fastsum(fcb.validate_sample(x), grid, scaled=False).values,
+                                  oracle.esf_fastsum(x, None, knots, scaled=False))
+
+
+@pytest.mark.parametrize("nbytes", [8, 8 << 20, (32 << 20) + 8, (100 << 20) + 24, 3 * (32 << 20)])
+def test_staged_copies_roundtrip(nbytes):
+    """fcg_copy_h2d / fcg_copy_d2h (the numpy path): exact round trips across chunk boundaries
+    (32 MB chunks, ring of 4) and for small sizes."""
+    import ctypes as C
+
+    import torch
+    from paper_2005_03246_b200 import _lib
+
+    n = nbytes // 8
+    a = np.random.default_rng(n).standard_normal(n)
+    lib = _lib.load_library()
+    d = torch.empty(n, dtype=torch.float64, device="cuda")
+    _lib.check(lib.fcg_copy_h2d(C.c_void_p(d.data_ptr()), a.ctypes.data_as(C.c_void_p), a.nbytes,
+                                _lib.stream_handle()), "fcg_copy_h2d")
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(d.cpu().numpy(), a)
+    d.mul_(2.0)
+    out = np.empty_like(a)
+    _lib.check(lib.fcg_copy_d2h(out.ctypes.data_as(C.c_void_p), C.c_void_p(d.data_ptr()), a.nbytes,
+                                _lib.stream_handle()), "fcg_copy_d2h")
+    np.testing.assert_array_equal(out, 2.0 * a)
+    # the package paths: numpy in -> device, device -> numpy out
+    np.testing.assert_array_equal(_lib.to_host(_lib.to_device_f64(a)), a)
