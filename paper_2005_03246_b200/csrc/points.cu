@@ -543,24 +543,17 @@ __global__ void adjacent_equal_kernel(const uint64_t *__restrict__ keys, int64_t
 }
 
 // ------------------------------------------------------------------------------------------
-// Self-query dominance in group order (kde_dnc / ecdf_dnc, d = 2).  All per-source data is
-// laid out in the order of the chunk grouping (sources sorted by (p1 >> LS, p0)) and of the
-// block grouping ((p0 >> LS, p1)), so the level-2 CTAs read and accumulate contiguous ranges;
-// the three partial results (coarse grid in query order, chunk part, block part) are combined
-// once at the end with two gathers per point.
-struct GrpArrays {
-  int32_t *slot;     // unflipped slot-dimension position (p1 for chunks, p0 for blocks)
-  int32_t *rankpos;  // unflipped rank-dimension position (p0 for chunks, p1 for blocks)
-  double *x;         // [n][2] points
-  double *w;         // [nw][n] weights
-  double *acc;       // [nch][n] accumulated z * partial dominance sums
-  int32_t *inv;      // source id -> group-order index
-};
+// Self-query dominance (kde_dnc / ecdf_dnc, d = 2).  The chunk grouping (sources sorted by
+// (p1 >> LS, p0)) and the block grouping ((p0 >> LS, p1)) are index lists; the level-2 CTAs and
+// the coarse rows gather their sources' records through them (one 32-byte sector per point for
+// coordinates and weights, L2-resident after a CTA's first code), and the level-2 results land
+// in point order, so the finish is a streaming pass.
 
-// per point (input order): both dimension positions, coordinates and weights in one 40-byte
-// record, so the two group-order gathers read one record per point instead of six arrays
-struct PtRec {
+// per point (input order): both dimension positions; coordinates and weights in one sector
+struct PtPos {
   int32_t p0, p1;
+};
+struct __align__(16) PtXW {
   double x0, x1, w0, w1;
 };
 
@@ -573,53 +566,32 @@ inline WPtr wptr(const double *w, int nw, int64_t n) {  // the [nw][n] matrix la
   return WPtr{{w, (w && nw > 1) ? w + n : nullptr}};
 }
 
+// group order k <- point list[k]: (slot, rank) positions and the coordinate / weight sector,
+// both coalesced for the level-2 CTAs (chunk grouping: slot = p1, rank = p0; block: swapped)
+__global__ void group_gather_kernel(const int32_t *__restrict__ list, const PtPos *__restrict__ pos,
+                                    const PtXW *__restrict__ xw, int chunk, int64_t n,
+                                    int2 *__restrict__ gpos, PtXW *__restrict__ gxw) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = list[k];
+    const PtPos pp = pos[i];
+    gpos[k] = chunk ? make_int2(pp.p1, pp.p0) : make_int2(pp.p0, pp.p1);
+    gxw[k] = xw[i];
+  }
+}
+
 __global__ void pack_points_kernel(const int32_t *__restrict__ pos0, const int32_t *__restrict__ pos1,
-                                   const double *__restrict__ x, WPtr w,
-                                   int nw, int64_t n, PtRec *__restrict__ rec) {
+                                   const double *__restrict__ x, WPtr w, int nw, int64_t n,
+                                   PtPos *__restrict__ pos, PtXW *__restrict__ xw) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    PtRec r;
-    r.p0 = pos0[i];
-    r.p1 = pos1[i];
-    const double2 xv = reinterpret_cast<const double2 *>(x)[i];
-    r.x0 = xv.x;
-    r.x1 = xv.y;
+    pos[i] = PtPos{pos0[i], pos1[i]};
+    PtXW r;
+    r.x0 = x[2 * i];
+    r.x1 = x[2 * i + 1];
     r.w0 = w.at(0, i);
     r.w1 = nw > 1 ? w.at(1, i) : 0.0;
-    rec[i] = r;
-  }
-}
-
-// group order k <- point order[k]; chunk grouping: slot = p1, rank = p0 (block: swapped)
-__global__ void group_gather_packed(const int32_t *__restrict__ order, const PtRec *__restrict__ rec,
-                                    int chunk, int nw, int64_t n, GrpArrays g) {
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t i = order[k];
-    const PtRec r = rec[i];
-    g.slot[k] = chunk ? r.p1 : r.p0;
-    g.rankpos[k] = chunk ? r.p0 : r.p1;
-    reinterpret_cast<double2 *>(g.x)[k] = make_double2(r.x0, r.x1);
-    g.w[k] = r.w0;
-    if (nw > 1) g.w[n + k] = r.w1;
-    g.inv[i] = (int32_t)k;
-  }
-}
-
-__global__ void group_gather_kernel(const int32_t *__restrict__ order,
-                                    const int32_t *__restrict__ pos_slot,
-                                    const int32_t *__restrict__ pos_rank,
-                                    const double *__restrict__ x, WPtr w,
-                                    int nw, int64_t n, GrpArrays g) {
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t i = order[k];
-    g.slot[k] = pos_slot[i];
-    g.rankpos[k] = pos_rank[i];
-    g.x[2 * k] = x[2 * (int64_t)i];
-    g.x[2 * k + 1] = x[2 * (int64_t)i + 1];
-    for (int v = 0; v < nw; ++v) g.w[v * n + k] = w.at(v, i);
-    g.inv[i] = (int32_t)k;
+    xw[i] = r;
   }
 }
 
@@ -627,7 +599,10 @@ struct Dom2S {
   int64_t n, P, npad;
   int64_t c_lo, c_hi;  // query shard: points whose (unflipped) chunk p1 >> LS is in [c_lo, c_hi)
   int nch, f0, f1, kde;
-  GrpArrays gc, gb;  // chunk and block groupings
+  const int32_t *bychunk, *byblock;  // the two groupings (point ids)
+  const int2 *gpos_c, *gpos_b;  // (slot, rank) positions in group order
+  const PtXW *gxw_c, *gxw_b;    // coordinates and weights in group order
+  double *accc, *accb;          // level-2 results [n][nch] in p1 (chunks) / p0 (blocks) order
   double *G;         // coarse grids [ncodes][P][P][nch], each in its code's flipped frame
   KdeP kp;           // the current code (level-2 solvers: psi and z computed on the fly)
 };
@@ -656,14 +631,14 @@ __global__ void __launch_bounds__(512) coarse_rows_codes(Dom2S D, Codes K, int64
   __syncthreads();
   const int64_t lo = g * S, hi = (g + 1) * S < D.n ? (g + 1) * S : D.n;
   for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) {
-    const int64_t bl = (D.gc.rankpos[k] >> LS) - b0;
+    const int64_t bl = (D.gpos_c[k].y >> LS) - b0;
     if (bl < 0 || bl >= nb) continue;
-    const double x0 = D.gc.x[2 * k], x1 = D.gc.x[2 * k + 1];
+    const PtXW r = D.gxw_c[k];
     for (int c = 0; c < K.n; ++c) {
-      const double e = K.kde ? exp(code_s(K.kp[c], x0, x1)) : 1.0;
+      const double e = K.kde ? exp(code_s(K.kp[c], r.x0, r.x1)) : 1.0;
       for (int v = 0; v < nch; ++v)
         atomicAdd(&s_row[(c * nb + bl) * nch + v],
-                  D.gc.w[v * D.n + k] * e * (K.kde ? chan_sign(K.kp[c], v) : 1.0));
+                  (v ? r.w1 : r.w0) * e * (K.kde ? chan_sign(K.kp[c], v) : 1.0));
     }
   }
   __syncthreads();
@@ -710,46 +685,86 @@ __global__ void coarse_query_codes(Dom2S D, Codes K, const int32_t *__restrict__
 // the sources of its unflipped slots, pass B: the sources of its ranks), so the code sum
 // z_c * F_c accumulates in registers; the two halves meet in shared memory once and are written
 // with plain coalesced stores (no global read-modify-write per code).
+//
+// Shared-memory discipline (ncu: the first version lost half its shared wavefronts to bank
+// conflicts and a third of its warp time to barriers behind 4-warp serial loops): the sub-grid is
+// built by one WARP per sub-row with the lanes on the 64 column cells (broadcast reads of the
+// sub-row's slots, the row prefix accumulated in registers), the column prefix by all 1024
+// threads as 8-row segments plus segment carries, and both partial passes read 4 candidates per
+// step (one 8-byte load of four int16 positions, four independent broadcast psi loads).
 constexpr int kL2Per = S / kSolverThreads;  // sources per thread
+constexpr int16_t kEmptyY = 0x7fff;          // an empty slot: above every rank threshold
+
+// Masked accumulate a += h * p: one select of the mask's high word and an FMA per channel (a
+// predicated add compiles to an add plus four 32-bit selects on the ALU pipe).  p is finite
+// (validated inputs; empty slots hold 0), so h = 0 adds exactly +0.0.
+template <int NCH>
+struct PsiT;
+template <>
+struct PsiT<1> {
+  using T = double;
+  __device__ static void add(double (&a)[1], double p, bool h) {
+    const double m = h ? 1.0 : 0.0;
+    a[0] = fma(p, m, a[0]);
+  }
+};
+template <>
+struct PsiT<2> {
+  using T = double2;
+  __device__ static void add(double (&a)[2], double2 p, bool h) {
+    const double m = h ? 1.0 : 0.0;
+    a[0] = fma(p.x, m, a[0]);
+    a[1] = fma(p.y, m, a[1]);
+  }
+};
 
 template <bool CHUNK, int NCH>
 __global__ void __launch_bounds__(kSolverThreads) level2_codes(Dom2S D, Codes K) {
+  using PT = typename PsiT<NCH>::T;
   extern __shared__ __align__(16) unsigned char smem[];
   double *s_sub = reinterpret_cast<double *>(smem);               // [NCH][NSUB][NSUB]
   double *s_psi = s_sub + NCH * NSUB * NSUB;                      // [S][NCH] by slot
-  int32_t *s_key = reinterpret_cast<int32_t *>(s_psi + NCH * S);  // [S] rank-dim positions by rank
+  double *s_tot = s_psi + NCH * S;                                // [1024] column-scan carries
+  double *s_z = s_tot + kSolverThreads;                           // [S] e^{-s} by group index
+  int32_t *s_key = reinterpret_cast<int32_t *>(s_z + S);          // [S] rank-dim positions by rank
   int16_t *s_yofx = reinterpret_cast<int16_t *>(s_key + S);       // [S]
   int16_t *s_xofy = s_yofx + S;                                   // [S]
   int16_t *s_kofx = s_xofy + S;                                   // [S] group index by slot
-  int16_t *s_qy = s_kofx + S;                                     // [S] rank threshold by slot
+  int16_t *s_qy = s_kofx + S;                                     // [S] rank threshold by
+                                                                  // UNFLIPPED slot
+  int16_t *s_slot = s_qy + S;                                     // [S] unflipped slot by k
+  const PT *s_p = reinterpret_cast<const PT *>(s_psi);
 
-  const GrpArrays &A = CHUNK ? D.gc : D.gb;
+  const int32_t *list = CHUNK ? D.bychunk : D.byblock;
+  double *out = CHUNK ? D.accc : D.accb;
+  (void)list;
   const int64_t g = blockIdx.x + (CHUNK ? D.c_lo : 0);  // unflipped chunk / block
   const int64_t lo = g * S;
   const int Sg = (int)(lo + S < D.n ? S : D.n - lo);
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool all_owned = CHUNK || (D.c_lo == 0 && D.c_hi == D.P);
   auto owned_key = [&](int32_t key) {  // BLOCK kind: the query's chunk is the shard's
     const int64_t cu = key >> LS;
     return all_owned || (cu >= D.c_lo && cu < D.c_hi);
   };
-  // this thread's sources (group indices k = threadIdx.x + j * 1024): positions in registers,
-  // coordinates and weights re-read per code (L1 / L2 hits)
-  int slot_u[kL2Per];
+  // ranks past the group's end are never written; pass B may read their positions (masked)
+  for (int i = Sg + threadIdx.x; i < S; i += blockDim.x) s_xofy[i] = 0;
+  const int2 *gpos = CHUNK ? D.gpos_c : D.gpos_b;
+  const PtXW *gxw = CHUNK ? D.gxw_c : D.gxw_b;
+  // this thread's sources (group indices k = threadIdx.x + j * 1024): rank keys in registers,
+  // slots in shared memory, coordinates and weights re-read per code (coalesced; L2 hits after
+  // the first code)
   int32_t key_u[kL2Per];
 #pragma unroll
   for (int j = 0; j < kL2Per; ++j) {
     const int k = threadIdx.x + j * kSolverThreads;
-    const bool in = k < Sg;
-    slot_u[j] = in ? A.slot[lo + k] - (int32_t)lo : 0;
-    key_u[j] = in ? A.rankpos[lo + k] : 0;
+    const int2 pp = k < Sg ? gpos[lo + k] : make_int2(0, 0);
+    key_u[j] = pp.y;
+    if (k < Sg) s_slot[k] = (int16_t)(pp.x - (int32_t)lo);
   }
-  const double2 *ax = reinterpret_cast<const double2 *>(A.x);
   double accA[kL2Per][NCH], accB[kL2Per][NCH];
-  int kA[kL2Per];
 #pragma unroll
   for (int j = 0; j < kL2Per; ++j) {
-    kA[j] = -1;
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) accA[j][ch] = accB[j][ch] = 0.0;
   }
@@ -758,54 +773,88 @@ __global__ void __launch_bounds__(kSolverThreads) level2_codes(Dom2S D, Codes K)
     const KdeP &kp = K.kp[code];
     const int f0 = code & 1, f1 = (code >> 1) & 1;
     const int fslot = CHUNK ? f1 : f0, frank = CHUNK ? f0 : f1;
+    // BLOCK thresholds depend on the rank frame only: searched at the first code of each frame
+    // (codes run 0..3, so the rank frame f1 changes at codes 0 and 2)
+    const bool search = !CHUNK && (code == 0 || code == 2);
     __syncthreads();  // the previous code's passes are done with the shared arrays
-    for (int i = threadIdx.x; i < NCH * NSUB * NSUB; i += blockDim.x) s_sub[i] = 0.0;
-    for (int i = threadIdx.x; i < S; i += blockDim.x) {
-      s_yofx[i] = -1;
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) s_psi[i * NCH + ch] = 0.0;
-    }
+    for (int i = threadIdx.x; i < S / 2; i += blockDim.x)
+      reinterpret_cast<uint32_t *>(s_yofx)[i] = (uint32_t)(uint16_t)kEmptyY * 0x10001u;
+    if (Sg < S)  // empty slots are read (masked) by the passes: keep them finite
+      for (int i = threadIdx.x; i < S * NCH; i += blockDim.x) s_psi[i] = 0.0;
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < kL2Per; ++j) {
       const int k = threadIdx.x + j * kSolverThreads;
       if (k >= Sg) continue;
       const int y = frank ? Sg - 1 - k : k;
-      const int x = fslot ? S - 1 - slot_u[j] : slot_u[j];
+      const int sl = s_slot[k];
+      const int x = fslot ? S - 1 - sl : sl;
       s_yofx[x] = (int16_t)y;
       s_xofy[y] = (int16_t)x;
       s_kofx[x] = (int16_t)k;
       s_key[y] = flipp(key_u[j], frank, D.npad);
-      const double2 xv = ax[lo + k];
-      const double e = K.kde ? exp(code_s(kp, xv.x, xv.y)) : 1.0;
+      const PtXW r = gxw[lo + k];
+      double e = 1.0;
+      if (K.kde) {
+        const double sv = code_s(kp, r.x0, r.x1);
+        e = exp(sv);
+        s_z[k] = exp(-sv);
+      }
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch)
-        s_psi[x * NCH + ch] = A.w[ch * D.n + lo + k] * e * (K.kde ? chan_sign(kp, ch) : 1.0);
+        s_psi[x * NCH + ch] = (ch ? r.w1 : r.w0) * e * (K.kde ? chan_sign(kp, ch) : 1.0);
     }
     __syncthreads();
-    for (int r = threadIdx.x; r < NCH * NSUB; r += blockDim.x) {  // sub-grid cell sums
-      const int ch = r / NSUB, u = r % NSUB;
-      double *row = s_sub + (ch * NSUB + u) * NSUB;
-      for (int x = u << SUBL; x < (u + 1) << SUBL; ++x) {
-        const int y = s_yofx[x];
-        if (y >= 0) row[y >> SUBL] += s_psi[x * NCH + ch];
+    // sub-grid rows: warp per sub-row u, lane l owns column cells l and l + 32; the inclusive
+    // row prefix sum_{x in row u, y >> SUBL <= v} psi_x is accumulated directly
+    for (int u = warp; u < NSUB; u += kSolverThreads / 32) {
+      double a0[NCH], a1[NCH];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) a0[ch] = a1[ch] = 0.0;
+      const int base = u << SUBL;
+      const int lim0 = (lane + 1) << SUBL, lim1 = (lane + 33) << SUBL;  // cells <= l, <= l + 32
+#pragma unroll 4
+      for (int i = 0; i < SUB; i += 4) {
+        const short4 y4 = *reinterpret_cast<const short4 *>(s_yofx + base + i);
+        const int yy[4] = {y4.x, y4.y, y4.z, y4.w};
+        PT pp[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) pp[t] = s_p[base + i + t];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {  // empty slots (kEmptyY) are past every cell
+          PsiT<NCH>::add(a0, pp[t], yy[t] < lim0);
+          PsiT<NCH>::add(a1, pp[t], yy[t] < lim1);
+        }
+      }
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        s_sub[(ch * NSUB + u) * NSUB + lane] = a0[ch];
+        s_sub[(ch * NSUB + u) * NSUB + lane + 32] = a1[ch];
       }
     }
     __syncthreads();
-    for (int r = threadIdx.x; r < NCH * NSUB; r += blockDim.x) {
-      double *row = s_sub + r * NSUB;
+    // column prefix over the sub-rows: thread (segment sg, column cc), lanes on consecutive
+    // columns; segment totals meet in s_tot
+    {
+      constexpr int NCC = NCH * NSUB, SEGS = kSolverThreads / NCC, RPS = NSUB / SEGS;
+      const int cc = threadIdx.x % NCC, sg = threadIdx.x / NCC;
+      const int ch = cc / NSUB, v = cc % NSUB;
+      double *col = s_sub + (ch * NSUB + sg * RPS) * NSUB + v;
+      double vals[RPS];
       double run = 0.0;
-      for (int v = 0; v < NSUB; ++v) { run += row[v]; row[v] = run; }
-    }
-    __syncthreads();
-    for (int cidx = threadIdx.x; cidx < NCH * NSUB; cidx += blockDim.x) {
-      const int ch = cidx / NSUB, v = cidx % NSUB;
-      double run = 0.0;
-      for (int u = 0; u < NSUB; ++u) {
-        double *pp = s_sub + (ch * NSUB + u) * NSUB + v;
-        run += *pp;
-        *pp = run;
+#pragma unroll
+      for (int r = 0; r < RPS; ++r) vals[r] = col[r * NSUB];
+#pragma unroll
+      for (int r = 0; r < RPS; ++r) {
+        run += vals[r];
+        vals[r] = run;
       }
+      s_tot[sg * NCC + cc] = run;
+      __syncthreads();
+      double carry = 0.0;
+      for (int t = 0; t < sg; ++t) carry += s_tot[t * NCC + cc];
+#pragma unroll
+      for (int r = 0; r < RPS; ++r) col[r * NSUB] = vals[r] + carry;
     }
     __syncthreads();
     // pass A: this thread's unflipped slots (a warp's 32 slots stay in one sub-row)
@@ -815,16 +864,17 @@ __global__ void __launch_bounds__(kSolverThreads) level2_codes(Dom2S D, Codes K)
       const int x = fslot ? S - 1 - uu : uu;
       const int y = s_yofx[x];
       int k = 0;
-      bool occ = y >= 0;
+      bool occ = y != kEmptyY;
       if (occ) {
         k = s_kofx[x];
-        occ = CHUNK || owned_key(A.rankpos[lo + k]);
+        occ = CHUNK || owned_key(flipp(s_key[y], frank, D.npad));
       }
       int qy = 0;
       if (occ) {
         if (CHUNK) {
           qy = y;
-        } else {
+          s_qy[uu] = (int16_t)qy;
+        } else if (search) {
           const int64_t c = s_key[y] >> LS;  // own chunk (self threshold)
           const int32_t ythr = (int32_t)((c > D.P ? D.P : c) * S);
           int a = 0, bnd = Sg;
@@ -834,38 +884,33 @@ __global__ void __launch_bounds__(kSolverThreads) level2_codes(Dom2S D, Codes K)
             else bnd = mid;
           }
           qy = a;
+          s_qy[uu] = (int16_t)qy;
+        } else {
+          qy = s_qy[uu];  // the previous code's: same rank frame
         }
-        s_qy[x] = (int16_t)qy;
       }
       const int u = x >> SUBL, v = qy >> SUBL;
       double acc[NCH];
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch)
         acc[ch] = (occ && u > 0 && v > 0) ? s_sub[(ch * NSUB + (u - 1)) * NSUB + (v - 1)] : 0.0;
-      const int cend = (int)__reduce_max_sync(0xffffffffu, occ ? (unsigned)x : 0u);
-      for (int c = u << SUBL; c < cend; ++c) {
-        const int yc = s_yofx[c];
-        const bool hit = occ && c < x && yc >= 0 && yc < qy;
-        if constexpr (NCH == 2) {
-          const double2 pc = reinterpret_cast<const double2 *>(s_psi)[c];
-          if (hit) {
-            acc[0] += pc.x;
-            acc[1] += pc.y;
-          }
-        } else {
-          const double pc = s_psi[c];
-          if (hit) acc[0] += pc;
-        }
+      const int xe = occ ? x : 0;  // candidates c < xe
+      const int cend = (int)__reduce_max_sync(0xffffffffu, (unsigned)xe);
+      for (int c0 = u << SUBL; c0 < cend; c0 += 4) {
+        const short4 y4 = *reinterpret_cast<const short4 *>(s_yofx + c0);
+        const int yc[4] = {y4.x, y4.y, y4.z, y4.w};
+        PT pc[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) pc[t] = s_p[c0 + t];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) PsiT<NCH>::add(acc, pc[t], c0 + t < xe && yc[t] < qy);
       }
       if (occ) {
-        const double2 xv = ax[lo + k];
-        const double z = K.kde ? exp(-code_s(kp, xv.x, xv.y)) : 1.0;
-        kA[j] = k;
+        const double z = K.kde ? s_z[k] : 1.0;
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) accA[j][ch] += z * acc[ch];
       }
     }
-    (void)lane;
     __syncthreads();
     // pass B: this thread's ranks (= its own sources k), coalesced
 #pragma unroll
@@ -874,68 +919,66 @@ __global__ void __launch_bounds__(kSolverThreads) level2_codes(Dom2S D, Codes K)
       const bool ok = k < Sg && (CHUNK || owned_key(key_u[j]));
       const int y = frank ? Sg - 1 - k : k;
       const int x = ok ? s_xofy[y] : 0;
-      const int qy = ok ? (int)s_qy[x] : 0;
+      const int qy = ok ? (int)s_qy[fslot ? S - 1 - x : x] : 0;
       const int xfull = (x >> SUBL) << SUBL;
-      const int cbeg = ok ? (qy >> SUBL) << SUBL : S;
+      const int cbeg = ok ? (qy >> SUBL) << SUBL : S;  // candidates cbeg <= c < qy (none: S, 0)
       const int cstart = (int)__reduce_min_sync(0xffffffffu, (unsigned)cbeg);
       const int cend = (int)__reduce_max_sync(0xffffffffu, ok ? (unsigned)qy : 0u);
       double acc[NCH];
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) acc[ch] = 0.0;
-      for (int c = cstart; c < cend; ++c) {
-        const int xc = s_xofy[c];
-        const bool hit = ok && c >= cbeg && c < qy && xc < xfull;
-        if constexpr (NCH == 2) {
-          const double2 pc = reinterpret_cast<const double2 *>(s_psi)[xc];
-          if (hit) {
-            acc[0] += pc.x;
-            acc[1] += pc.y;
-          }
-        } else {
-          const double pc = s_psi[xc];
-          if (hit) acc[0] += pc;
-        }
+      for (int c0 = cstart; c0 < cend; c0 += 4) {
+        const short4 x4 = *reinterpret_cast<const short4 *>(s_xofy + c0);
+        const int xc[4] = {x4.x, x4.y, x4.z, x4.w};
+        PT pc[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) pc[t] = s_p[xc[t]];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          PsiT<NCH>::add(acc, pc[t], c0 + t >= cbeg && c0 + t < qy && xc[t] < xfull);
       }
       if (ok) {
-        const double2 xv = ax[lo + k];
-        const double z = K.kde ? exp(-code_s(kp, xv.x, xv.y)) : 1.0;
+        const double z = K.kde ? s_z[k] : 1.0;
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) accB[j][ch] += z * acc[ch];
       }
     }
   }
-  // the two halves of every query meet in shared memory (reusing the psi rows), one store each
+  // the two halves of every query meet in shared memory (reusing the psi rows) by unflipped slot
+  // (the slot-dimension position, so the store is coalesced in that dimension's rank order:
+  // chunks write p1 order, blocks p0 order); the pass-B half moves, pass A is already by slot
   __syncthreads();
-  double *s_acc = s_psi;  // [S][NCH] by group index
-  for (int i = threadIdx.x; i < S * NCH; i += blockDim.x) s_acc[i] = 0.0;
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < kL2Per; ++j)
-    if (kA[j] >= 0)
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) s_acc[kA[j] * NCH + ch] = accA[j][ch];
-  __syncthreads();
+  double *s_acc = s_psi;  // [S][NCH] by unflipped slot
 #pragma unroll
   for (int j = 0; j < kL2Per; ++j) {
     const int k = threadIdx.x + j * kSolverThreads;
     if (k >= Sg) continue;
+    const int sl = s_slot[k];
 #pragma unroll
-    for (int ch = 0; ch < NCH; ++ch) A.acc[ch * D.n + lo + k] = s_acc[k * NCH + ch] + accB[j][ch];
+    for (int ch = 0; ch < NCH; ++ch) s_acc[sl * NCH + ch] = accB[j][ch];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kL2Per; ++j) {
+    const int uu = threadIdx.x + j * kSolverThreads;
+    if (uu >= Sg) continue;
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) out[(lo + uu) * NCH + ch] = accA[j][ch] + s_acc[uu * NCH + ch];
   }
 }
 
 size_t level2_self_smem(int nch) {
-  return (size_t)nch * NSUB * NSUB * 8 + (size_t)nch * S * 8 + (size_t)S * 4 + (size_t)S * 2 * 4;
+  return (size_t)nch * NSUB * NSUB * 8 + (size_t)nch * S * 8 + (size_t)kSolverThreads * 8 +
+         (size_t)S * 8 + (size_t)S * 4 + (size_t)S * 2 * 5;
 }
 
-// out[v][t] = (acc_q[v][t] + acc_c[v][inv_c[t]] + acc_b[v][inv_b[t]] + (add_w ? w[v][t] : 0))
+// out[v][t] = (acc_q[v][t] + acc_c[p1(t)][v] + acc_b[p0(t)][v] + (add_w ? w[v][t] : 0))
 //             * mult / div      (mult == 0: none, div == 0: none)
 __global__ void self_finish_kernel(int64_t n, int nw, const double *__restrict__ accq,
-                                   const double *__restrict__ accc, const int32_t *__restrict__ invc,
-                                   const double *__restrict__ accb, const int32_t *__restrict__ invb,
+                                   const double *__restrict__ accc, const double *__restrict__ accb,
                                    WPtr w, int add_w, double mult, double div,
-                                   double *__restrict__ out, const int32_t *__restrict__ pos1,
-                                   int64_t c_lo, int64_t c_hi) {
+                                   double *__restrict__ out, const int32_t *__restrict__ pos0,
+                                   const int32_t *__restrict__ pos1, int64_t c_lo, int64_t c_hi) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t cu = pos1[t] >> LS;
@@ -943,9 +986,9 @@ __global__ void self_finish_kernel(int64_t n, int nw, const double *__restrict__
       for (int v = 0; v < nw; ++v) out[v * n + t] = 0.0;
       continue;
     }
-    const int64_t kc = invc[t], kb = invb[t];
+    const int64_t kc = pos1[t], kb = pos0[t];
     for (int v = 0; v < nw; ++v) {
-      double r = accq[v * n + t] + accc[v * n + kc] + accb[v * n + kb];
+      double r = accq[v * n + t] + accc[kc * nw + v] + accb[kb * nw + v];
       if (add_w) r = r + w.at(v, t);
       if (mult != 0.0) r = r * mult;
       if (div != 0.0) r = r / div;
@@ -1192,22 +1235,24 @@ int sorted_exclusive(const double *vals, const int32_t *order, int64_t n, bool r
 }
 
 struct SelfWs {
-  GrpArrays gc, gb;
-  double *accq;
-  PtRec *rec;
+  PtPos *pos;
+  PtXW *xw;
+  int2 *gpos_c, *gpos_b;
+  PtXW *gxw_c, *gxw_b;
+  double *accq;        // [nw][n]
+  double *accc, *accb;  // [n][nw]
 };
 
 void carve_self(Workspace &W, SelfWs &q, int64_t n, int nw) {
-  for (GrpArrays *g : {&q.gc, &q.gb}) {
-    g->slot = W.take<int32_t>(n);
-    g->rankpos = W.take<int32_t>(n);
-    g->x = W.take<double>((size_t)n * 2);
-    g->w = W.take<double>((size_t)n * nw);
-    g->acc = W.take<double>((size_t)n * nw);
-    g->inv = W.take<int32_t>(n);
-  }
+  q.pos = W.take<PtPos>(n);
+  q.xw = W.take<PtXW>(n);
+  q.gpos_c = W.take<int2>(n);
+  q.gpos_b = W.take<int2>(n);
+  q.gxw_c = W.take<PtXW>(n);
+  q.gxw_b = W.take<PtXW>(n);
   q.accq = W.take<double>((size_t)n * nw);
-  q.rec = W.take<PtRec>(n);
+  q.accc = W.take<double>((size_t)n * nw);
+  q.accb = W.take<double>((size_t)n * nw);
 }
 
 // Strict-dominance sums at the points for d = 2 in group order: the plain ECDF (kde = 0, one
@@ -1220,15 +1265,10 @@ int self_dom2d(const double *x, WPtr w, int64_t n, int nw, int kde, const double
   FCG_TRY(prep2d(x, n, p, st));
   const int g = grid_for(n, 256);
   {
-    FCG_PROF("pts_group_gather", st);
-    if ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && nw <= 2) {
-      pack_points_kernel<<<g, 256, 0, st>>>(p.r[0].pos, p.r[1].pos, x, w, nw, n, q.rec);
-      group_gather_packed<<<g, 256, 0, st>>>(p.bychunk, q.rec, 1, nw, n, q.gc);
-      group_gather_packed<<<g, 256, 0, st>>>(p.byblock, q.rec, 0, nw, n, q.gb);
-    } else {
-      group_gather_kernel<<<g, 256, 0, st>>>(p.bychunk, p.r[1].pos, p.r[0].pos, x, w, nw, n, q.gc);
-      group_gather_kernel<<<g, 256, 0, st>>>(p.byblock, p.r[0].pos, p.r[1].pos, x, w, nw, n, q.gb);
-    }
+    FCG_PROF("pts_pack", st);
+    pack_points_kernel<<<g, 256, 0, st>>>(p.r[0].pos, p.r[1].pos, x, w, nw, n, q.pos, q.xw);
+    group_gather_kernel<<<g, 256, 0, st>>>(p.bychunk, q.pos, q.xw, 1, n, q.gpos_c, q.gxw_c);
+    group_gather_kernel<<<g, 256, 0, st>>>(p.byblock, q.pos, q.xw, 0, n, q.gpos_b, q.gxw_b);
     FCG_LAUNCH_CHECK();
   }
   Dom2S D{};
@@ -1237,8 +1277,14 @@ int self_dom2d(const double *x, WPtr w, int64_t n, int nw, int kde, const double
   D.npad = p.npad;
   D.nch = nw;
   D.kde = kde;
-  D.gc = q.gc;
-  D.gb = q.gb;
+  D.bychunk = p.bychunk;
+  D.byblock = p.byblock;
+  D.gpos_c = q.gpos_c;
+  D.gpos_b = q.gpos_b;
+  D.gxw_c = q.gxw_c;
+  D.gxw_b = q.gxw_b;
+  D.accc = q.accc;
+  D.accb = q.accb;
   D.G = p.G;
   const int64_t P = p.P;
   // query shard: a contiguous range of chunks (points in p1 rank order)
@@ -1310,8 +1356,9 @@ int self_dom2d(const double *x, WPtr w, int64_t n, int nw, int kde, const double
     FCG_LAUNCH_CHECK();
   }
   FCG_PROF("pts_finish", st);
-  self_finish_kernel<<<g, 256, 0, st>>>(n, nw, q.accq, q.gc.acc, q.gc.inv, q.gb.acc, q.gb.inv, w,
-                                       add_w, mult, div, out, p.r[1].pos, D.c_lo, D.c_hi);
+  self_finish_kernel<<<g, 256, 0, st>>>(n, nw, q.accq, q.accc, q.accb, w,
+                                       add_w, mult, div, out, p.r[0].pos, p.r[1].pos, D.c_lo,
+                                       D.c_hi);
   FCG_LAUNCH_CHECK();
   return FCG_OK;
 }
