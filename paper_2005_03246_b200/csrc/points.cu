@@ -549,10 +549,7 @@ __global__ void adjacent_equal_kernel(const uint64_t *__restrict__ keys, int64_t
 // coordinates and weights, L2-resident after a CTA's first code), and the level-2 results land
 // in point order, so the finish is a streaming pass.
 
-// per point (input order): both dimension positions; coordinates and weights in one sector
-struct PtPos {
-  int32_t p0, p1;
-};
+// per point (input order): coordinates and weights in one sector
 struct __align__(16) PtXW {
   double x0, x1, w0, w1;
 };
@@ -566,26 +563,97 @@ inline WPtr wptr(const double *w, int nw, int64_t n) {  // the [nw][n] matrix la
   return WPtr{{w, (w && nw > 1) ? w + n : nullptr}};
 }
 
-// group order k <- point list[k]: (slot, rank) positions and the coordinate / weight sector,
-// both coalesced for the level-2 CTAs (chunk grouping: slot = p1, rank = p0; block: swapped)
-__global__ void group_gather_kernel(const int32_t *__restrict__ list, const PtPos *__restrict__ pos,
-                                    const PtXW *__restrict__ xw, int chunk, int64_t n,
-                                    int2 *__restrict__ gpos, PtXW *__restrict__ gxw) {
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t i = list[k];
-    const PtPos pp = pos[i];
-    gpos[k] = chunk ? make_int2(pp.p1, pp.p0) : make_int2(pp.p0, pp.p1);
-    gxw[k] = xw[i];
+// Self-path grouping without a global sort.  Group g of the slot dimension (chunk: points with
+// p1 in [g S, g S + Sg), i.e. order1[g S ...], slot = p1; block: order0, slot = p0) is ordered
+// by its rank-dimension position r (p0 for chunks, p1 for blocks): a shared-memory counting pass
+// over the level-1 cells r >> LS of the other dimension (about S / P points per cell) gives every
+// point its cell's start, and a count of the smaller keys inside the cell its index k.  Writes
+// the (slot, rank) positions and the coordinate / weight sector in group order, for the coarse
+// rows and the level-2 CTAs.  Same order as sorting by (slot >> LS, rank).
+constexpr int kGroupThreads = 1024;
+constexpr int kGroupPer = S / kGroupThreads;
+
+__global__ void __launch_bounds__(kGroupThreads) group_self_kernel(
+    const int32_t *__restrict__ order_slot, const int32_t *__restrict__ pos_rank,
+    const PtXW *__restrict__ xw, int64_t n, int64_t P, int shift, int2 *__restrict__ gpos,
+    PtXW *__restrict__ gxw) {
+  // P here: the number of cells key >> shift (the level-1 cells, or coarser ones for very large n)
+  extern __shared__ int32_t gs_smem[];
+  int32_t *s_cnt = gs_smem;                // [P + 1]: cell counts -> exclusive starts
+  int32_t *s_key = gs_smem + P + 1;        // [S]: keys by cell position
+  int32_t *s_wsum = s_key + S;             // [32]
+  const int64_t lo = (int64_t)blockIdx.x * S;
+  const int Sg = (int)(lo + S < n ? S : n - lo);
+  for (int64_t i = threadIdx.x; i <= P; i += kGroupThreads) s_cnt[i] = 0;
+  __syncthreads();
+  int32_t id[kGroupPer], key[kGroupPer], sl[kGroupPer];
+#pragma unroll
+  for (int j = 0; j < kGroupPer; ++j) {
+    const int i = threadIdx.x + j * kGroupThreads;
+    id[j] = i < Sg ? order_slot[lo + i] : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < kGroupPer; ++j) {
+    const int i = threadIdx.x + j * kGroupThreads;
+    key[j] = i < Sg ? pos_rank[id[j]] : 0;
+    sl[j] = i < Sg ? atomicAdd(&s_cnt[key[j] >> shift], 1) : 0;
+  }
+  __syncthreads();
+  {  // exclusive scan of the P + 1 counts in place (thread t: a contiguous run of cells)
+    const int64_t per = (P + 1 + kGroupThreads - 1) / kGroupThreads;
+    const int64_t a = threadIdx.x * per, b = a + per < P + 1 ? a + per : P + 1;
+    int32_t tot = 0;
+    for (int64_t i = a; i < b; ++i) tot += s_cnt[i];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t x = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[warp] = x;
+    __syncthreads();
+    int32_t run = x - tot;
+    for (int w = 0; w < warp; ++w) run += s_wsum[w];
+    for (int64_t i = a; i < b; ++i) {
+      const int32_t c = s_cnt[i];
+      s_cnt[i] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kGroupPer; ++j) {
+    const int i = threadIdx.x + j * kGroupThreads;
+    if (i < Sg) s_key[s_cnt[key[j] >> shift] + sl[j]] = key[j];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kGroupPer; ++j) {
+    const int i = threadIdx.x + j * kGroupThreads;
+    if (i >= Sg) continue;
+    const int64_t c = key[j] >> shift;
+    const int a = s_cnt[c], b = s_cnt[c + 1];
+    int k = a;
+    for (int m = a; m < b; ++m) k += s_key[m] < key[j];
+    gpos[lo + k] = make_int2((int32_t)(lo + i), key[j]);
+    gxw[lo + k] = xw[id[j]];
   }
 }
 
-__global__ void pack_points_kernel(const int32_t *__restrict__ pos0, const int32_t *__restrict__ pos1,
-                                   const double *__restrict__ x, WPtr w, int nw, int64_t n,
-                                   PtPos *__restrict__ pos, PtXW *__restrict__ xw) {
+constexpr int64_t kGroupMaxCells = 16384;  // shared-memory counters per group CTA
+inline int group_self_shift(int64_t n) {
+  int sh = LS;
+  while ((((n - 1) >> sh) + 1) > kGroupMaxCells) ++sh;
+  return sh;
+}
+inline int64_t group_self_cells(int64_t n) { return ((n - 1) >> group_self_shift(n)) + 1; }
+size_t group_self_smem(int64_t n) { return (size_t)(group_self_cells(n) + 1 + S + 32) * 4; }
+
+__global__ void pack_points_kernel(const double *__restrict__ x, WPtr w, int nw, int64_t n,
+                                   PtXW *__restrict__ xw) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    pos[i] = PtPos{pos0[i], pos1[i]};
     PtXW r;
     r.x0 = x[2 * i];
     r.x1 = x[2 * i + 1];
@@ -599,7 +667,6 @@ struct Dom2S {
   int64_t n, P, npad;
   int64_t c_lo, c_hi;  // query shard: points whose (unflipped) chunk p1 >> LS is in [c_lo, c_hi)
   int nch, f0, f1, kde;
-  const int32_t *bychunk, *byblock;  // the two groupings (point ids)
   const int2 *gpos_c, *gpos_b;  // (slot, rank) positions in group order
   const PtXW *gxw_c, *gxw_b;    // coordinates and weights in group order
   double *accc, *accb;          // level-2 results [n][nch] in p1 (chunks) / p0 (blocks) order
@@ -735,9 +802,7 @@ __global__ void __launch_bounds__(kSolverThreads) level2_codes(Dom2S D, Codes K)
   int16_t *s_slot = s_qy + S;                                     // [S] unflipped slot by k
   const PT *s_p = reinterpret_cast<const PT *>(s_psi);
 
-  const int32_t *list = CHUNK ? D.bychunk : D.byblock;
   double *out = CHUNK ? D.accc : D.accb;
-  (void)list;
   const int64_t g = blockIdx.x + (CHUNK ? D.c_lo : 0);  // unflipped chunk / block
   const int64_t lo = g * S;
   const int Sg = (int)(lo + S < D.n ? S : D.n - lo);
@@ -1207,12 +1272,6 @@ int rank_all(const double *x, int64_t n, int d, PtsWs &p, cudaStream_t st, bool 
   return FCG_OK;
 }
 
-int prep2d(const double *x, int64_t n, PtsWs &p, cudaStream_t st) {
-  FCG_TRY(rank_all(x, n, 2, p, st, false));
-  FCG_TRY(group_by(p.r[0].order, p.r[1].pos, n, p.P, p.bychunk, p, st));
-  FCG_TRY(group_by(p.r[1].order, p.r[0].pos, n, p.P, p.byblock, p, st));
-  return FCG_OK;
-}
 
 // d == 1 dominance: dst[i] = sum over sorted positions before (rev: after) i of vals, as the
 // reference computes it (inclusive cumsum minus self).  lat: 2n doubles of scratch.
@@ -1235,7 +1294,6 @@ int sorted_exclusive(const double *vals, const int32_t *order, int64_t n, bool r
 }
 
 struct SelfWs {
-  PtPos *pos;
   PtXW *xw;
   int2 *gpos_c, *gpos_b;
   PtXW *gxw_c, *gxw_b;
@@ -1244,7 +1302,6 @@ struct SelfWs {
 };
 
 void carve_self(Workspace &W, SelfWs &q, int64_t n, int nw) {
-  q.pos = W.take<PtPos>(n);
   q.xw = W.take<PtXW>(n);
   q.gpos_c = W.take<int2>(n);
   q.gpos_b = W.take<int2>(n);
@@ -1262,13 +1319,20 @@ int self_dom2d(const double *x, WPtr w, int64_t n, int nw, int kde, const double
                const double *centre, int add_w, double mult, double div, PtsWs &p, SelfWs &q,
                double *out, cudaStream_t st, const unsigned *smask = nullptr, int shard = 0,
                int nshards = 1) {
-  FCG_TRY(prep2d(x, n, p, st));
+  FCG_TRY(rank_all(x, n, 2, p, st, false));
   const int g = grid_for(n, 256);
   {
-    FCG_PROF("pts_pack", st);
-    pack_points_kernel<<<g, 256, 0, st>>>(p.r[0].pos, p.r[1].pos, x, w, nw, n, q.pos, q.xw);
-    group_gather_kernel<<<g, 256, 0, st>>>(p.bychunk, q.pos, q.xw, 1, n, q.gpos_c, q.gxw_c);
-    group_gather_kernel<<<g, 256, 0, st>>>(p.byblock, q.pos, q.xw, 0, n, q.gpos_b, q.gxw_b);
+    FCG_PROF("pts_group", st);
+    pack_points_kernel<<<g, 256, 0, st>>>(x, w, nw, n, q.xw);
+    const size_t gsm = group_self_smem(n);
+    const int64_t cells = group_self_cells(n);
+    const int sh = group_self_shift(n);
+    FCG_CUDA_TRY(cudaFuncSetAttribute(group_self_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)gsm));
+    group_self_kernel<<<(unsigned)p.P, kGroupThreads, gsm, st>>>(p.r[1].order, p.r[0].pos, q.xw, n,
+                                                                  cells, sh, q.gpos_c, q.gxw_c);
+    group_self_kernel<<<(unsigned)p.P, kGroupThreads, gsm, st>>>(p.r[0].order, p.r[1].pos, q.xw, n,
+                                                                  cells, sh, q.gpos_b, q.gxw_b);
     FCG_LAUNCH_CHECK();
   }
   Dom2S D{};
@@ -1277,8 +1341,6 @@ int self_dom2d(const double *x, WPtr w, int64_t n, int nw, int kde, const double
   D.npad = p.npad;
   D.nch = nw;
   D.kde = kde;
-  D.bychunk = p.bychunk;
-  D.byblock = p.byblock;
   D.gpos_c = q.gpos_c;
   D.gpos_b = q.gpos_b;
   D.gxw_c = q.gxw_c;
