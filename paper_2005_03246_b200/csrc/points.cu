@@ -24,6 +24,7 @@
 #include "common.cuh"
 #include "scan.cuh"
 #include "sort.cuh"
+#include "tma.cuh"
 
 namespace fcg {
 
@@ -1432,6 +1433,8 @@ int make_q(const int32_t *a, int64_t n, int kind, int64_t npad, int32_t *out, cu
   return FCG_OK;
 }
 
+#include "points_nd.cuh"
+
 int check_pts(int64_t n, int32_t d) {
   if (d < 1 || d > FCG_MAX_DIM) return fail(FCG_EUNSUPPORTED, "dimension out of range");
   if (n < 0) return fail(FCG_EINVAL, "n must be >= 0");
@@ -1511,6 +1514,8 @@ int ecdf_points_multi(const double *x, int64_t n, int d, const double *w, int sc
   Workspace W(ws);
   PtsWs p;
   carve(W, p, n, d, 1, dom_ok, false, d == 1 ? n : budget);
+  NdWs nq{};
+  if (nd_route(n, d)) carve_nd(W, nq, n, d, 1, 1, false);
   if (ws == nullptr) {
     *ws_bytes = W.bytes();
     return FCG_OK;
@@ -1633,7 +1638,23 @@ int ecdf_points_multi(const double *x, int64_t n, int d, const double *w, int sc
   }
 
   if (d == 2) return dom_too_large(n);
-  // brute force (d >= 3 without a feasible rank lattice)
+  if (nd_route(n, d)) {  // coarse grid + slab remainder in rank space
+    for (int q = 0; q < nreq; ++q) {
+      int rev[FCG_MAX_DIM], qoff[FCG_MAX_DIM];
+      const int32_t *thr[FCG_MAX_DIM];
+      for (int k = 0; k < d; ++k) {
+        rev[k] = req[q].survival ? 1 : 0;  // [x_i > x_t] <=> p_i >= upper_t
+        qoff[k] = 0;
+        thr[k] = (req[q].survival || req[q].delta[k] > 0) ? p.r[k].upper : p.r[k].lower;
+      }
+      FCG_TRY(dom_nd(p, nq, n, d, 1, NdW{{w, nullptr}, 1}, rev, qoff, thr, req[q].out, 0, 1, st));
+      FCG_PROF("pts_finish", st);
+      finish_ecdf_kernel<<<grid_for(n, 256), 256, 0, st>>>(req[q].out, n, w, 0, div);
+      FCG_LAUNCH_CHECK();
+    }
+    return FCG_OK;
+  }
+  // direct tiles (d >= 7, or too few points for the rank-space route to pay)
   for (int q = 0; q < nreq; ++q) {
     Brute B;
     B.n = n;
@@ -1679,9 +1700,12 @@ extern "C" int fcg_dnc_ecdf(const double *x, int64_t n, int32_t d, const double 
   const bool dom_ok = d == 2;
   Workspace W(ws);
   PtsWs p;
-  carve(W, p, n, d < 2 ? d : 2, 1, dom_ok, false, d == 1 ? 2 * n : 0);
+  const bool nd = nd_route(n, d);
+  carve(W, p, n, nd ? d : (d < 2 ? d : 2), 1, dom_ok, false, d == 1 ? 2 * n : 0);
   SelfWs q{};
   if (dom_ok) carve_self(W, q, n, 1);
+  NdWs nq{};
+  if (nd) carve_nd(W, nq, n, d, 1, 1, false);
   if (ws == nullptr) {
     *ws_bytes = W.bytes();
     return FCG_OK;
@@ -1695,6 +1719,12 @@ extern "C" int fcg_dnc_ecdf(const double *x, int64_t n, int32_t d, const double 
   } else if (dom_ok) {
     return self_dom2d(x, wptr(w, 1, n), n, 1, 0, nullptr, nullptr, include_self, 0.0, div, p, q,
                       out, st);
+  } else if (nd) {  // strict dominance in rank space: p_m(s) < p_m(t) for every m
+    FCG_TRY(rank_all(x, n, d, p, st, false));
+    int rev[FCG_MAX_DIM] = {0}, qoff[FCG_MAX_DIM] = {0};
+    const int32_t *thr[FCG_MAX_DIM];
+    for (int k = 0; k < d; ++k) thr[k] = p.r[k].pos;
+    FCG_TRY(dom_nd(p, nq, n, d, 1, NdW{{w, nullptr}, 1}, rev, qoff, thr, out, 0, 1, st));
   } else {
     Brute B;
     B.n = n;
@@ -1723,9 +1753,12 @@ extern "C" int fcg_kde_points_laplacian(const double *x, int64_t n, int32_t d, c
   const bool dom_ok = d == 2;
   Workspace W(ws);
   PtsWs p;
-  carve(W, p, n, d < 2 ? d : 2, nw, dom_ok, true, d == 1 ? n * 2 : 0);
+  const bool nd = nd_route(n, d);
+  carve(W, p, n, nd ? d : (d < 2 ? d : 2), nw, dom_ok, true, d == 1 ? n * 2 : 0);
   SelfWs q{};
   if (dom_ok) carve_self(W, q, n, nw);
+  NdWs nq{};
+  if (nd) carve_nd(W, nq, n, d, nw, 1 << d, true);
   double *psi1 = nullptr, *F1 = nullptr;
   if (d == 1) {
     psi1 = W.take<double>((size_t)n * nw);
@@ -1743,6 +1776,14 @@ extern "C" int fcg_kde_points_laplacian(const double *x, int64_t n, int32_t d, c
   for (int k = 0; k < d; ++k) prod_h *= h[k];
   const double scale = 1.0 / (std::ldexp(1.0, d) * (double)n * prod_h);
 
+  if (nd) {  // far field per sign code on a coarse rank grid + direct near-field pairs
+    FCG_TRY(rank_all(x, n, d, p, st, false));
+    FCG_TRY(kde_nd(p, nq, x, n, d, w, nw, h, centre, out, st));
+    FCG_PROF("pts_finish", st);
+    kde_finish_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, nw, w, scale, out);
+    FCG_LAUNCH_CHECK();
+    return FCG_OK;
+  }
   if (d >= 3 || !(d == 1 || dom_ok)) {
     Brute B;
     B.n = n;
@@ -2067,12 +2108,35 @@ extern "C" int fcg_dominance_terms(const double *x, int64_t n, int32_t d, const 
                                    double *table, void *ws, size_t *ws_bytes, void *stream) {
   FCG_TRY(check_pts(n, d));
   if (d > 6) return fail(FCG_EUNSUPPORTED, "dominance tables support d <= 6 (2^d columns)");
+  const bool nd = nd_route(n, d);
+  Workspace W(ws);
+  PtsWs p;
+  NdWs nq{};
+  if (nd) {
+    carve(W, p, n, d, 1, false, false, 0);
+    carve_nd(W, nq, n, d, 1, 1, false);
+  }
   if (ws == nullptr) {
-    *ws_bytes = 256;
+    *ws_bytes = W.bytes();
     return FCG_OK;
   }
   if (n == 0) return FCG_OK;
   const int nc = 1 << d;
+  if (nd) {  // one rank-space dominance sum per sign code (bit k: x_ik > x_jk)
+    cudaStream_t st = as_stream(stream);
+    FCG_TRY(rank_all(x, n, d, p, st, false));
+    for (int b = 0; b < nc; ++b) {
+      int rev[FCG_MAX_DIM], qoff[FCG_MAX_DIM];
+      const int32_t *thr[FCG_MAX_DIM];
+      for (int k = 0; k < d; ++k) {
+        rev[k] = qoff[k] = (b >> k) & 1;  // p_k(i) >= p_k(j) + 1
+        thr[k] = p.r[k].pos;
+      }
+      FCG_TRY(dom_nd(p, nq, n, d, 1, NdW{{psi + b, nullptr}, nc}, rev, qoff, thr, table + b, 0,
+                     nc, st));
+    }
+    return FCG_OK;
+  }
   const size_t smem = ((size_t)kTermQ * (nc + 1) + (size_t)kTermS * FCG_MAX_DIM +
                        (size_t)kTermS * nc) * sizeof(double);
   cudaStream_t st = as_stream(stream);

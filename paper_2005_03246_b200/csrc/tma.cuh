@@ -51,6 +51,16 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// global -> shared copy of a contiguous block (16-byte aligned, a multiple of 16 bytes) by the
+// TMA unit, completion counted on `bar`
+__device__ __forceinline__ void bulk_load_1d(void *dst, const void *src, uint32_t bytes,
+                                             uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 // generic-proxy shared-memory accesses before this are ordered before later async-proxy (TMA)
 // accesses of the same shared memory
 __device__ __forceinline__ void fence_proxy_async_smem() {

@@ -1,7 +1,7 @@
 """Generate golden fixtures by running the REFERENCE package itself (build container only).
 
     NUMBA_CACHE_DIR=/tmp/numba_golden PYTHONPATH=/root/reference/pkg/src \
-        python -B tests/golden/make_golden.py [--small] [--csv] [--configs cfg1,cfg2,...]
+        python -B tests/golden/make_golden.py [--small] [--nd] [--csv] [--configs cfg1,cfg2,...]
 
 Writes small .npz fixtures next to this file; they are committed and travel to the GPU box
 (the reference itself does not).  Inputs are stored with the outputs wherever they are small,
@@ -371,12 +371,43 @@ def csv_golden():
     print("wrote csv.npz", flush=True)
 
 
+def nd_golden():
+    """At-points dominance sums for d >= 3 at sizes that take the rank-space coarse-grid route
+    (n >= 8192): the reference's MergeND recursion (dnc.py:65-135, 307-410) is the oracle."""
+    bag = Bag()
+    rng = np.random.default_rng(20240521)
+    for d, n in [(3, 10_000), (4, 9_000), (5, 8_500)]:
+        x = rng.standard_normal((n, d))
+        w = rng.uniform(0.5, 2.0, n)
+        h = rng.uniform(0.4, 0.8, d)
+        key = f"nd{d}"
+        bag.put(key + ".x", x)
+        bag.put(key + ".w", w)
+        bag.put(key + ".h", h)
+        s = fc.validate_sample(x, w)
+        su = fc.validate_sample(x)
+        bag.put(key + ".ecdf_w", fc.ecdf_dnc(s, scaled=False).values)
+        bag.put(key + ".ecdf_unit_self", fc.ecdf_dnc(su, include_self=True, scaled=False).values)
+        bag.put(key + ".ecdf_scaled", fc.ecdf_dnc(su).values)
+        bag.put(key + ".kde_w", fc.kde_dnc(s, fc.laplacian(), fc.Bandwidth.diag(h)).values)
+        bag.put(key + ".kde_unit", fc.kde_dnc(su, fc.laplacian(), fc.Bandwidth.diag(h)).values)
+        if d <= 4:
+            tt = fc.kde_terms_dnc(s, fc.Bandwidth.diag(h), (0, d - 1, 1, 1))
+            rows = rng.integers(0, n, 400)
+            bag.put(key + ".terms_rows", rows)
+            bag.put(key + ".terms", tt.table[rows])
+    bag.save("nd.npz")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
+    ap.add_argument("--nd", action="store_true")
     ap.add_argument("--small", action="store_true")
     ap.add_argument("--csv", action="store_true")
     ap.add_argument("--configs", default="")
     a = ap.parse_args()
+    if a.nd:
+        nd_golden()
     if a.small:
         small()
     if a.csv:

@@ -141,3 +141,21 @@ def test_multilinear_interp(small_golden, oracle):
         out, cc = oracle.multilinear_interp(g.knots(key), g[key + ".vals"], g[key + ".q"])
         np.testing.assert_array_equal(out, g[key + ".out"])
         assert cc == int(g[key + ".clamp"])
+
+
+def test_nd_direct_sums_vs_reference_recursion(oracle):
+    """The oracle's direct at-points sums (naive.py:187-248 restated) against the reference's
+    MergeND recursion for d = 3..5 (nd.npz, dnc.py:65-135, 307-410, 531-690): pins the checker
+    that the d >= 3 device route is compared with on larger inputs."""
+    from conftest import GOLDEN, Golden
+
+    g = Golden(GOLDEN / "nd.npz")
+    for d in (3, 4, 5):
+        key = f"nd{d}"
+        x, w, h = g[key + ".x"], g[key + ".w"], g[key + ".h"]
+        got = oracle.ecdf_naive(x, w, x, (-1,) * d, scaled=False)
+        np.testing.assert_allclose(got, g[key + ".ecdf_w"], rtol=1e-12, atol=1e-9)
+        got = oracle.ecdf_naive(x, None, x, (-1,) * d, scaled=False) + 1.0
+        np.testing.assert_array_equal(got, g[key + ".ecdf_unit_self"])
+        got = oracle.kde_naive_laplacian(x, w, x, h)
+        np.testing.assert_allclose(got, g[key + ".kde_w"], rtol=1e-10, atol=0)
