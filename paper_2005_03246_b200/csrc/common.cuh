@@ -23,7 +23,9 @@ int fail(int code, const std::string &msg);
   do {                                                                                      \
     cudaError_t _e = cudaGetLastError();                                                    \
     if (_e != cudaSuccess)                                                                  \
-      return ::fcg::fail(FCG_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+      return ::fcg::fail(FCG_ECUDA, std::string("kernel launch (") + __FILE__ + ":" +         \
+                                        std::to_string(__LINE__) + "): " +                  \
+                                        cudaGetErrorString(_e));                            \
   } while (0)
 
 #define FCG_TRY(expr)                                                                       \

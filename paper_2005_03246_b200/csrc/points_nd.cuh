@@ -53,7 +53,7 @@ inline NdPlan nd_plan(int64_t n, int d, int nch, int ncodes, bool kde) {
     double cells = 1.0;
     for (int k = 0; k < d; ++k) cells *= (double)G;
     if (cells * 8.0 * nch > (double)kNdMaxCoarseBytes) continue;
-    const double near = (double)d * (double)n * (double)(int64_t(1) << ls) / (kde ? 6e11 : 4e12);
+    const double near = (double)d * (double)n * (double)(int64_t(1) << ls) / (kde ? 6.5e11 : 2.5e12);
     const double far = (double)ncodes * nch * (cells * 8.0 * (2 * d + 2) / 4e12 + (d + 3) * 4e-6);
     const double cost = near + far;
     if (best_cost < 0.0 || cost < best_cost) {

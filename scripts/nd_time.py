@@ -22,7 +22,8 @@ for d, n in cases:
     x = torch.randn((n, d), dtype=torch.float64, device="cuda", generator=g)
     w = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) + 0.5
     dist = (True,) * d  # skip the distinct-coordinates pass (continuous data)
-    s = fcb.Sample(x, w, distinct_by_dim=dist); su = fcb.Sample(x, None, distinct_by_dim=dist)
+    s = fcb.Sample(x, w, distinct_by_dim=dist, unit_weights=False)
+    su = fcb.Sample(x, torch.ones_like(w), distinct_by_dim=dist, unit_weights=True)
     bw = fcb.Bandwidth.diag([0.3] * d)
     t_u = timeit(lambda: fcb.ecdf_dnc(su, scaled=False))
     t_w = timeit(lambda: fcb.ecdf_dnc(s, scaled=False))
