@@ -30,12 +30,12 @@ namespace fcg {
 
 namespace {
 
-constexpr int LS = 12;
+constexpr int LS = 11;
 constexpr int S = 1 << LS;    // level-1 block / chunk size
-constexpr int SUBL = 6;
+constexpr int SUBL = 5;
 constexpr int SUB = 1 << SUBL;  // level-2 sub-block size
 constexpr int NSUB = S / SUB;   // 64
-constexpr int kSolverThreads = 1024;
+constexpr int kSolverThreads = 512;
 // The d = 2 dominance route keeps a (n/S)^2 x channels fp64 coarse grid: up to 48 GB of the
 // 180 GB HBM (n ~ 2.5e8 with two channels); larger n is refused up front with a clear error.
 constexpr int64_t kMaxCoarseBytes = int64_t(48) << 30;
@@ -687,62 +687,117 @@ __device__ __forceinline__ double code_s(const KdeP &kp, double x0, double x1) {
   return (x0 - kp.c[0]) * kp.a[0] + (x1 - kp.c[1]) * kp.a[1];
 }
 
-// Coarse rows of every code in one pass over the chunk-grouped points: CTA per (unflipped chunk
-// g, segment of TB unflipped blocks); a point adds its code-c psi to row (f1 ? P-1-g : g) at
-// block (f0 ? P-1-b : b) of grid c (every code's grid is stored in its own flipped frame).
-__global__ void __launch_bounds__(512) coarse_rows_codes(Dom2S D, Codes K, int64_t TB) {
-  extern __shared__ double s_row[];  // [ncodes][TB][nch]
-  const int64_t g = blockIdx.x, P = D.P;
-  const int64_t b0 = (int64_t)blockIdx.y * TB, nb = (b0 + TB < P ? TB : P - b0);
-  const int nch = D.nch;
-  for (int64_t i = threadIdx.x; i < K.n * nb * nch; i += blockDim.x) s_row[i] = 0.0;
-  __syncthreads();
-  const int64_t lo = g * S, hi = (g + 1) * S < D.n ? (g + 1) * S : D.n;
-  for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) {
-    const int64_t bl = (D.gpos_c[k].y >> LS) - b0;
-    if (bl < 0 || bl >= nb) continue;
-    const PtXW r = D.gxw_c[k];
-    for (int c = 0; c < K.n; ++c) {
-      const double e = K.kde ? exp(code_s(K.kp[c], r.x0, r.x1)) : 1.0;
-      for (int v = 0; v < nch; ++v)
-        atomicAdd(&s_row[(c * nb + bl) * nch + v],
-                  (v ? r.w1 : r.w0) * e * (K.kde ? chan_sign(K.kp[c], v) : 1.0));
-    }
-  }
-  __syncthreads();
-  for (int c = 0; c < K.n; ++c) {
-    const int f0 = c & 1, f1 = (c >> 1) & 1;
-    const int64_t row = f1 ? P - 1 - g : g;
-    double *grid = D.G + ((int64_t)c * P + row) * P * nch;
-    for (int64_t i = threadIdx.x; i < nb * nch; i += blockDim.x) {
-      const int64_t bl = i / nch, v = i - bl * nch;
-      const int64_t b = f0 ? P - 1 - (b0 + bl) : b0 + bl;
-      grid[b * nch + v] = s_row[(c * nb + bl) * nch + v];
-    }
-  }
-}
+// Coarse rows of every code, prefixed along the block axis: CTA per unflipped chunk g.  The
+// chunk's points arrive in p0 order, so their blocks are nondecreasing and the inclusive prefix
+// at block b is a running sum over the points evaluated at the last point of block <= b: one
+// CTA-wide scan per (code, channel) and plain run stores, no atomics.  Codes with f0 = 1 store
+// their grid flipped along the block axis: suffix sums, written at P-1-b.  Row f1 ? P-1-g : g.
+constexpr int kCoarseThreads = 512;
+constexpr int kCoarsePer = S / kCoarseThreads;  // consecutive points per thread
 
-// acc_q[ch][t] = sum_codes z_code(t) * G_code[chunk(t) - 1][block(t) - 1] (flipped frames),
-// codes summed in order (the shard's queries only; the others stay untouched)
-__global__ void coarse_query_codes(Dom2S D, Codes K, const int32_t *__restrict__ pos0,
-                                   const int32_t *__restrict__ pos1, const double *__restrict__ x,
-                                   double *__restrict__ accq) {
-  const int64_t P = D.P;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < D.n;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t cu = pos1[t] >> LS, bu = pos0[t] >> LS;
-    if (cu < D.c_lo || cu >= D.c_hi) continue;  // another shard's query
-    const double x0 = x[2 * t], x1 = x[2 * t + 1];
-    double acc[2] = {0.0, 0.0};
-    for (int c = 0; c < K.n; ++c) {
-      const int f0 = c & 1, f1 = (c >> 1) & 1;
-      const int64_t cc = f1 ? P - 1 - cu : cu, bb = f0 ? P - 1 - bu : bu;
-      if (cc == 0 || bb == 0) continue;
-      const double z = K.kde ? exp(-code_s(K.kp[c], x0, x1)) : 1.0;
-      const double *gv = D.G + (((int64_t)c * P + cc - 1) * P + bb - 1) * D.nch;
-      for (int v = 0; v < D.nch; ++v) acc[v] += z * gv[v];
+template <int NCH>
+__global__ void __launch_bounds__(kCoarseThreads) coarse_rows_codes(Dom2S D, Codes K) {
+  constexpr int NQ = 4 * NCH, NW = kCoarseThreads / 32;
+  __shared__ double s_wtot[NQ][NW];
+  __shared__ int32_t s_first[kCoarseThreads + 1], s_last[kCoarseThreads + 1];
+  const int64_t g = blockIdx.x, P = D.P, lo = g * S;
+  const int Sg = (int)(lo + S < D.n ? S : D.n - lo);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nq = K.n * NCH;
+  int32_t blk[kCoarsePer];
+  double val[kCoarsePer][NQ];
+#pragma unroll
+  for (int j = 0; j < kCoarsePer; ++j) {
+    const int k = tid * kCoarsePer + j;
+    const bool live = k < Sg;
+    blk[j] = live ? (D.gpos_c[lo + k].y >> LS) : (int32_t)P;
+    PtXW r = live ? D.gxw_c[lo + k] : PtXW{0.0, 0.0, 0.0, 0.0};
+    if (!live) r.w0 = r.w1 = 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (c >= K.n) break;
+      const double e = K.kde ? exp(code_s(K.kp[c], r.x0, r.x1)) : 1.0;
+#pragma unroll
+      for (int v = 0; v < NCH; ++v)
+        val[j][c * NCH + v] = (v ? r.w1 : r.w0) * e * (K.kde ? chan_sign(K.kp[c], v) : 1.0);
     }
-    for (int v = 0; v < D.nch; ++v) accq[v * D.n + t] = acc[v];
+  }
+  s_first[tid] = blk[0];
+  s_last[tid + 1] = blk[kCoarsePer - 1];
+  if (tid == 0) {
+    s_last[0] = -1;
+    s_first[kCoarseThreads] = (int32_t)P;
+  }
+  // inclusive scans over the points: ascending for f0 = 0 codes, descending for f0 = 1
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    if (q >= nq) break;
+    const bool rev = (q / NCH) & 1;
+    double run = 0.0;
+    if (!rev) {
+#pragma unroll
+      for (int j = 0; j < kCoarsePer; ++j) val[j][q] = run = run + val[j][q];
+    } else {
+#pragma unroll
+      for (int j = kCoarsePer - 1; j >= 0; --j) val[j][q] = run = run + val[j][q];
+    }
+    double x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = rev ? __shfl_down_sync(0xffffffffu, x, o) : __shfl_up_sync(0xffffffffu, x, o);
+      if (rev ? lane + o < 32 : lane >= o) x += y;
+    }
+    if (lane == (rev ? 0 : 31)) s_wtot[q][warp] = x;
+    double excl = rev ? __shfl_down_sync(0xffffffffu, x, 1) : __shfl_up_sync(0xffffffffu, x, 1);
+    if (lane == (rev ? 31 : 0)) excl = 0.0;  // the lanes before (after) this one
+#pragma unroll
+    for (int j = 0; j < kCoarsePer; ++j) val[j][q] += excl;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    if (q >= nq) break;
+    const bool rev = (q / NCH) & 1;
+    double carry = 0.0;
+    if (!rev) {
+      for (int w = 0; w < warp; ++w) carry += s_wtot[q][w];
+    } else {
+      for (int w = NW - 1; w > warp; --w) carry += s_wtot[q][w];
+    }
+#pragma unroll
+    for (int j = 0; j < kCoarsePer; ++j) val[j][q] += carry;
+  }
+  // run stores
+  const int32_t nxt = s_first[tid + 1], prv = s_last[tid];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (c >= K.n) break;
+    const int f0 = c & 1, f1 = (c >> 1) & 1;
+    double *row = D.G + ((int64_t)c * P + (f1 ? P - 1 - g : g)) * P * NCH;
+#pragma unroll
+    for (int j = 0; j < kCoarsePer; ++j) {
+      const int k = tid * kCoarsePer + j;
+      if (k >= Sg) break;
+      if (!f0) {  // blocks [blk(k), blk(k + 1)) hold the prefix through point k
+        const int32_t bnext = j + 1 < kCoarsePer ? blk[j + 1] : nxt;
+        for (int32_t bb = blk[j]; bb < bnext; ++bb)
+#pragma unroll
+          for (int v = 0; v < NCH; ++v) row[(int64_t)bb * NCH + v] = val[j][c * NCH + v];
+        if (k == 0)
+          for (int32_t bb = 0; bb < blk[0]; ++bb)
+#pragma unroll
+            for (int v = 0; v < NCH; ++v) row[(int64_t)bb * NCH + v] = 0.0;
+      } else {    // blocks (blk(k - 1), blk(k)] hold the suffix from point k, stored flipped
+        const int32_t bprev = j > 0 ? blk[j - 1] : prv;
+        for (int32_t bb = bprev + 1; bb <= blk[j]; ++bb)
+#pragma unroll
+          for (int v = 0; v < NCH; ++v) row[(P - 1 - bb) * NCH + v] = val[j][c * NCH + v];
+        if (k == Sg - 1)
+          for (int32_t bb = blk[j] + 1; bb < (int32_t)P; ++bb)
+#pragma unroll
+            for (int v = 0; v < NCH; ++v) row[(P - 1 - bb) * NCH + v] = 0.0;
+      }
+    }
   }
 }
 
@@ -860,15 +915,27 @@ __global__ void __launch_bounds__(kSolverThreads) level2_codes(Dom2S D, Codes K)
       s_kofx[x] = (int16_t)k;
       s_key[y] = flipp(key_u[j], frank, D.npad);
       const PtXW r = gxw[lo + k];
-      double e = 1.0;
+      double e = 1.0, z = 1.0;
       if (K.kde) {
         const double sv = code_s(kp, r.x0, r.x1);
         e = exp(sv);
-        s_z[k] = exp(-sv);
+        z = exp(-sv);
+        s_z[k] = z;
       }
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch)
         s_psi[x * NCH + ch] = (ch ? r.w1 : r.w0) * e * (K.kde ? chan_sign(kp, ch) : 1.0);
+      if (CHUNK) {
+        // level 1: the code's coarse cell below the query's chunk and block (flipped frame).
+        // The chunk's points run in p0 order, so a warp's reads walk one grid row in order.
+        const int64_t P = D.P, bu = key_u[j] >> LS;
+        const int64_t cc = f1 ? P - 1 - g : g, bb = f0 ? P - 1 - bu : bu;
+        if (cc > 0 && bb > 0) {
+          const double *gv = D.G + (((int64_t)code * P + cc - 1) * P + bb - 1) * NCH;
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) accB[j][ch] += z * gv[ch];
+        }
+      }
     }
     __syncthreads();
     // sub-grid rows: warp per sub-row u, lane l owns column cells l and l + 32; the inclusive
@@ -1038,9 +1105,9 @@ size_t level2_self_smem(int nch) {
          (size_t)S * 8 + (size_t)S * 4 + (size_t)S * 2 * 5;
 }
 
-// out[v][t] = (acc_q[v][t] + acc_c[p1(t)][v] + acc_b[p0(t)][v] + (add_w ? w[v][t] : 0))
-//             * mult / div      (mult == 0: none, div == 0: none)
-__global__ void self_finish_kernel(int64_t n, int nw, const double *__restrict__ accq,
+// out[v][t] = (acc_c[p1(t)][v] + acc_b[p0(t)][v] + (add_w ? w[v][t] : 0)) * mult / div
+// (mult == 0: none, div == 0: none); acc_c carries the level-1 term
+__global__ void self_finish_kernel(int64_t n, int nw,
                                    const double *__restrict__ accc, const double *__restrict__ accb,
                                    WPtr w, int add_w, double mult, double div,
                                    double *__restrict__ out, const int32_t *__restrict__ pos0,
@@ -1054,7 +1121,7 @@ __global__ void self_finish_kernel(int64_t n, int nw, const double *__restrict__
     }
     const int64_t kc = pos1[t], kb = pos0[t];
     for (int v = 0; v < nw; ++v) {
-      double r = accq[v * n + t] + accc[kc * nw + v] + accb[kb * nw + v];
+      double r = accc[kc * nw + v] + accb[kb * nw + v];
       if (add_w) r = r + w.at(v, t);
       if (mult != 0.0) r = r * mult;
       if (div != 0.0) r = r / div;
@@ -1298,7 +1365,6 @@ struct SelfWs {
   PtXW *xw;
   int2 *gpos_c, *gpos_b;
   PtXW *gxw_c, *gxw_b;
-  double *accq;        // [nw][n]
   double *accc, *accb;  // [n][nw]
 };
 
@@ -1308,7 +1374,6 @@ void carve_self(Workspace &W, SelfWs &q, int64_t n, int nw) {
   q.gpos_b = W.take<int2>(n);
   q.gxw_c = W.take<PtXW>(n);
   q.gxw_b = W.take<PtXW>(n);
-  q.accq = W.take<double>((size_t)n * nw);
   q.accc = W.take<double>((size_t)n * nw);
   q.accb = W.take<double>((size_t)n * nw);
 }
@@ -1380,14 +1445,11 @@ int self_dom2d(const double *x, WPtr w, int64_t n, int nw, int kde, const double
   }
   {
     FCG_PROF("pts_coarse_hist", st);
-    const int64_t TB = kCoarseRowBytes / (8 * (int64_t)nw * K.n), nseg = ceil_div(P, TB);
-    const size_t row_smem = (size_t)K.n * (TB < P ? TB : P) * nw * sizeof(double);
-    FCG_CUDA_TRY(cudaFuncSetAttribute(coarse_rows_codes, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kCoarseRowBytes));
-    coarse_rows_codes<<<dim3((unsigned)P, (unsigned)nseg), 512, row_smem, st>>>(D, K, TB);
+    if (nw == 1) coarse_rows_codes<1><<<(unsigned)P, kCoarseThreads, 0, st>>>(D, K);
+    else coarse_rows_codes<2><<<(unsigned)P, kCoarseThreads, 0, st>>>(D, K);
     FCG_LAUNCH_CHECK();
   }
-  {
+  {  // the block axis is prefixed by the row kernel; the chunk axis in one scan pass
     LatShape gs;
     gs.d = 4;
     gs.dims[0] = K.n;
@@ -1395,13 +1457,7 @@ int self_dom2d(const double *x, WPtr w, int64_t n, int nw, int kde, const double
     gs.dims[2] = P;
     gs.dims[3] = nw;
     Epi inplace;
-    FCG_TRY(scan_axis<double>(p.G, gs, 2, false, inplace, p.scratch, st));
     FCG_TRY(scan_axis<double>(p.G, gs, 1, false, inplace, p.scratch, st));
-  }
-  {
-    FCG_PROF("pts_coarse_query", st);
-    coarse_query_codes<<<g, 256, 0, st>>>(D, K, p.r[0].pos, p.r[1].pos, x, q.accq);
-    FCG_LAUNCH_CHECK();
   }
   // level 2: every code of a chunk / block in one CTA (the chunk solvers for the shard's chunks)
   {
@@ -1419,7 +1475,7 @@ int self_dom2d(const double *x, WPtr w, int64_t n, int nw, int kde, const double
     FCG_LAUNCH_CHECK();
   }
   FCG_PROF("pts_finish", st);
-  self_finish_kernel<<<g, 256, 0, st>>>(n, nw, q.accq, q.accc, q.accb, w,
+  self_finish_kernel<<<g, 256, 0, st>>>(n, nw, q.accc, q.accb, w,
                                        add_w, mult, div, out, p.r[0].pos, p.r[1].pos, D.c_lo,
                                        D.c_hi);
   FCG_LAUNCH_CHECK();

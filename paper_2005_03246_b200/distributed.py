@@ -319,11 +319,15 @@ def kde_fastsum_slab(sample: Sample, grid: RectilinearGrid, kernel, bandwidth: B
 # At-points queries, sharded (SURVEY 8e: "sample-point queries are sharded with the ranked data
 # replicated").  Every rank holds the whole sample; the device call ranks and groups all n
 # sources (replicated, no communication) and evaluates only the rank's queries: the points
-# whose dimension-1 rank falls in a contiguous 1/G slice of the 4096-point chunks.  Other
+# whose dimension-1 rank falls in a contiguous 1/G slice of the POINTS_CHUNK-point chunks.  Other
 # entries come back as exact zeros, so the optional final gather is one SUM all-reduce of the
 # owned values (computed by the single-GPU arithmetic).  The hot loop has no collective.
 
-def query_shard_chunks(n: int, shard: int, nshards: int, chunk: int = 4096) -> tuple[int, int]:
+POINTS_CHUNK = 2048  # points per rank chunk of the d = 2 dominance route (csrc/points.cu: S)
+
+
+def query_shard_chunks(n: int, shard: int, nshards: int,
+                       chunk: int = POINTS_CHUNK) -> tuple[int, int]:
     """[c_lo, c_hi): the dimension-1 rank chunks whose points shard `shard` evaluates."""
     P = -(-n // chunk)
     return P * shard // nshards, P * (shard + 1) // nshards

@@ -97,9 +97,10 @@ class OracleEngine:
 
     # ---- at-points query shards: the oracle's full answer, zeros outside the shard's chunks
     @staticmethod
-    def _owned(x, shard, nshards, chunk=4096):
-        from paper_2005_03246_b200.distributed import query_shard_chunks
+    def _owned(x, shard, nshards, chunk=None):
+        from paper_2005_03246_b200.distributed import POINTS_CHUNK, query_shard_chunks
 
+        chunk = chunk or POINTS_CHUNK
         n = x.shape[0]
         pos1 = np.empty(n, dtype=np.int64)
         pos1[np.argsort(x[:, 1], kind="stable")] = np.arange(n)

@@ -121,7 +121,7 @@ def _points_worker(rank, world, port, q):
 
         eng = OracleEngine()
         rng = np.random.default_rng(5)
-        n = 9000  # 3 chunks of 4096: shards own 0..3 chunks each
+        n = 9000  # a few rank chunks: shards own 0..3 chunks each
         x = rng.standard_normal((n, 2))
         y = np.sin(3 * x[:, 0]) + rng.normal(0, 0.1, n)
         s = fcb.validate_sample(x)
@@ -172,8 +172,8 @@ def test_points_query_shards_match_single(world):
 
 
 def test_query_shard_chunks_partition():
-    for n in (1, 4095, 4096, 9000, 10_000_000):
+    for n in (1, 2047, 2048, 4095, 4096, 9000, 10_000_000):
         for G in (1, 2, 3, 8):
             spans = [fdist.query_shard_chunks(n, s, G) for s in range(G)]
-            assert spans[0][0] == 0 and spans[-1][1] == -(-n // 4096)
+            assert spans[0][0] == 0 and spans[-1][1] == -(-n // fdist.POINTS_CHUNK)
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
