@@ -35,7 +35,7 @@ constexpr int S = 1 << LS;    // level-1 block / chunk size
 constexpr int SUBL = 5;
 constexpr int SUB = 1 << SUBL;  // level-2 sub-block size
 constexpr int NSUB = S / SUB;   // 64
-constexpr int kSolverThreads = 512;
+constexpr int kSolverThreads = 1024;
 // The d = 2 dominance route keeps a (n/S)^2 x channels fp64 coarse grid: up to 48 GB of the
 // 180 GB HBM (n ~ 2.5e8 with two channels); larger n is refused up front with a clear error.
 constexpr int64_t kMaxCoarseBytes = int64_t(48) << 30;
