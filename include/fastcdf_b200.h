@@ -219,7 +219,10 @@ int fcg_copy_d2h(void *dst_host, const void *src_dev, size_t bytes, void *stream
  * implements it (i == j included): out[j] = sum_i w_i prod_k [x_ik <= x_jk] (delta=+1) or
  * [x_ik < x_jk] (delta=-1); survival == 1 gives Eq. (2), sum_i w_i prod_k [x_ik > x_jk].
  * Divided by n when scaled.  Syncs (reads the distinct-level counts to pick the rank lattice
- * or the dominance kernel). */
+ * or the dominance kernel).  Routes: rank lattice when the grid of distinct levels is small;
+ * rank-space dominance otherwise (d = 2: coarse grid + per-chunk solvers; 3 <= d <= 6 and
+ * n >= 8192: coarse G^d grid + per-dimension slab phases, csrc/points_nd.cuh; direct tiles
+ * only for d >= 7 or fewer points). */
 int fcg_ecdf_points(const double *x, int64_t n, int32_t d, const double *w,
                     const int32_t *delta, int32_t survival, int32_t scaled, double *out,
                     void *ws, size_t *ws_bytes, void *stream);
@@ -233,7 +236,9 @@ int fcg_ecdf_esf_points(const double *x, int64_t n, int32_t d, const double *w,
 
 /* Strict-dominance ECDF at the sample points (requires pairwise-distinct coordinates per
  * dimension, checked by the caller): out[j] = sum_{i != j, x_i < x_j in every dim} w_i,
- * + w_j when include_self, / n when scaled.  Replaces dnc.py:531-561 ecdf_dnc. */
+ * + w_j when include_self, / n when scaled.  Replaces dnc.py:531-561 ecdf_dnc (and, for
+ * d >= 3, the MergeND recursion dnc.py:65-135, 307-410 behind it: the rank-space coarse grid +
+ * slab phases of csrc/points_nd.cuh for 3 <= d <= 6). */
 int fcg_dnc_ecdf(const double *x, int64_t n, int32_t d, const double *w,
                  int32_t include_self, int32_t scaled, double *out,
                  void *ws, size_t *ws_bytes, void *stream);
@@ -242,7 +247,9 @@ int fcg_dnc_ecdf(const double *x, int64_t n, int32_t d, const double *w,
  * (dnc.py:635-690 kde_dnc, _run_all_delta dnc.py:564-585).  Requires distinct coordinates.
  * h, centre: host (d,).  nw weight vectors w[v*n + i] (v < nw) are evaluated in one pass;
  * out[v*n + j] receives the density numerator of weight vector v (self term and
- * 1/(2^d n prod h) included, exactly the reference's kde_dnc output). */
+ * 1/(2^d n prod h) included, exactly the reference's kde_dnc output).  3 <= d <= 6: every
+ * sign code's far field from a coarse rank grid, pairs sharing a rank chunk summed directly
+ * (csrc/points_nd.cuh). */
 int fcg_kde_points_laplacian(const double *x, int64_t n, int32_t d, const double *w,
                              int32_t nw, const double *h, const double *centre, double *out,
                              void *ws, size_t *ws_bytes, void *stream);
@@ -250,11 +257,10 @@ int fcg_kde_points_laplacian(const double *x, int64_t n, int32_t d, const double
 /* Query-sharded forms for one process per GPU ("sample-point queries are sharded
  * with the ranked data replicated"); d = 2 (the dominance route).  Every shard ranks and
  * groups all n sources (replicated) but evaluates only its own queries: the points whose
- * rank along dimension 1 falls in chunks [P s / G, P (s+1) / G) of the P = ceil(n / 4096)
+ * rank along dimension 1 falls in chunks [P s / G, P (s+1) / G) of the P = ceil(n / 2048)
  * chunks (a contiguous 1/G slice of the queries in rank order).  Other entries of out are
  * set to exactly 0, so a SUM all-reduce over the G shards gathers the result (the owned values
- * are computed by exactly the unsharded arithmetic; the coarse histogram's shared-memory
- * atomics make repeated calls agree to rounding).  Same arguments as the unsharded calls plus
+ * are computed by exactly the unsharded arithmetic).  Same arguments as the unsharded calls plus
  * shard s in [0, G) and G. */
 int fcg_kde_points_laplacian_shard(const double *x, int64_t n, int32_t d, const double *w,
                                    int32_t nw, const double *h, const double *centre,
@@ -275,7 +281,8 @@ int fcg_kde_points_laplacian_w2(const double *x, int64_t n, int32_t d, const dou
 /* All-delta strict-dominance tables (dnc.py:608-632 kde_terms_dnc, _run_all_delta): psi and
  * table are (n, 2^d) row-major; table[j][b] = sum of psi[i][b] over the points i != j with
  * x_ik < x_jk where bit k of b is 0 and x_ik > x_jk where it is 1.  Requires distinct
- * coordinates per dimension; d <= 6.  Direct tiled pairs, O(n^2). */
+ * coordinates per dimension; d <= 6.  One rank-space dominance sum per code (3 <= d <= 6,
+ * n >= 8192: csrc/points_nd.cuh), direct tiled pairs otherwise. */
 int fcg_dominance_terms(const double *x, int64_t n, int32_t d, const double *psi, double *table,
                         void *ws, size_t *ws_bytes, void *stream);
 

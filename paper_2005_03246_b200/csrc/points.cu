@@ -10,15 +10,16 @@
 //  * rank-space dominance, d = 2 (continuous data — config 4): after ranking, the points are a
 //    permutation in [0,n)^2.  A 3-level decomposition answers every lower-left query
 //    F(t) = sum_i psi_i [p0_i < Q0_t][p1_i < Q1_t]:
-//      level 1: chunks of S = 4096 consecutive p1 positions x blocks of S p0 positions form a
+//      level 1: chunks of S = 2048 consecutive p1 positions x blocks of S p0 positions form a
 //               coarse (n/S)^2 grid; a 2-D inclusive prefix gives all fully-dominated cells;
 //      level 2: the query's own chunk and own block are solved inside one CTA each: the
-//               <= 4096 sources are laid out in shared memory by local slot / local rank, a
-//               64x64 sub-grid prefix covers full sub-cells, and <= 2 x 63 direct checks finish.
+//               <= 2048 sources are laid out in shared memory by local slot / local rank, a
+//               64x64 sub-grid prefix covers full sub-cells, and <= 2 x 31 direct checks finish.
 //    The four sign codes of the KDE (dnc.py:459-468) are the four orientations of the same
 //    problem (flip p0 and/or p1), sharing one ranking and one chunk/block grouping.
-//  * brute force O(n^2) tiles (d >= 3 without a feasible rank lattice; SURVEY §8f #3 widens
-//    this later).
+//  * rank-space dominance, 3 <= d <= 6 (points_nd.cuh): a coarse G^d grid of rank chunks for the
+//    far field and one slab phase per dimension for the sources sharing a chunk with the query.
+//  * direct O(n^2) tiles (d >= 7, or fewer than 8192 points).
 #include <string>
 
 #include "common.cuh"

@@ -4,7 +4,8 @@ functions ``ecdf_dnc`` (dnc.py:531-561) and ``kde_dnc`` (dnc.py:635-690).
 The reference computes them with an O(N log N) divide-and-conquer recursion; here the same sums
 come from the rank-space dominance kernel of ``fcg_dnc_ecdf`` / ``fcg_kde_points_laplacian``
 (device radix ranking + a 3-level coarse-grid / shared-memory decomposition, d = 2; sort + scan
-for d = 1; tiled direct sums for d >= 3).  Semantics, guards and exceptions follow the
+for d = 1; a coarse G^d rank grid + per-dimension slab phases for 3 <= d <= 6 in place of the
+MergeND recursion dnc.py:65-135, 307-410; direct tiles for tiny inputs and d >= 7).  Semantics, guards and exceptions follow the
 reference: distinct coordinates are required (TieError), strict comparisons on raw coordinates,
 exponentials on midrange-centred coordinates, the self term w_j added before the shared
 1/(2^d N prod h) normalisation.
@@ -166,7 +167,7 @@ def kde_terms_dnc(sample: Sample, bandwidth: Bandwidth,
     """All-delta dominance tables for exponential kernel compositions (dnc.py:608-632):
     psi(x_i, delta) = w_i x_{l,i}^p x_{m,i}^q exp(sum_k delta_k x_{k,i} / h_k), formed exactly
     as the reference does (numpy, host inputs) and summed over the dominating points on the
-    device (``fcg_dominance_terms``, tiled direct pairs)."""
+    device (``fcg_dominance_terms``: one rank-space dominance sum per code)."""
     import torch
 
     sample = as_sample(sample)
