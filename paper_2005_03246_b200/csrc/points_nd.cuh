@@ -14,8 +14,10 @@
 //               dimension; phase k takes the sources of chunk(Tf_k) along dimension k whose
 //               chunks are strictly below along the dimensions m < k, and compares positions
 //               directly for m >= k (each dominated source is met in exactly one phase).
-//               Queries are bucketed by chunk(Tf_k); a CTA stages the chunk's sources (already
-//               gathered in dimension-k order) through shared memory with TMA bulk copies.
+//               Thresholds are nondecreasing along the dimension's rank order, so the queries of
+//               chunk(Tf_k) are a contiguous run of that order; a CTA takes 256 of them and stages
+//               the chunk's sources below its largest threshold (already gathered in dimension-k
+//               order) through shared memory with TMA bulk copies.
 // Cost: d n 2^ls pair tests + (2d + 1) G^d lattice cell visits instead of n^2 pairs.
 //
 // The Laplacian KDE (kde_dnc, dnc.py:635-690) uses the same split over its 2^d sign codes: the
@@ -82,7 +84,7 @@ struct DomN {
   int64_t out_vs, out_ts;
   int32_t *rec;  // [NP][DP] flipped positions of the sources in dimension-k order
   double *wrec;  // [nch][NP]
-  int32_t *qkey, *qlist, *qstart, *tstart;
+  int32_t *qkey, *qstart, *tstart;
 };
 
 __device__ __forceinline__ int32_t nd_thr(const DomN &D, int m, int64_t t) {
@@ -161,6 +163,7 @@ __global__ void __launch_bounds__(kNdThreads) nd_near_kernel(DomN A) {
   __shared__ __align__(128) double s_w[2][UNIT ? 2 : NCH * kNdTile];
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ int s_j;
+  __shared__ int32_t s_tmax[kNdThreads / 32];
   const int tid = threadIdx.x;
   if (tid == 0) {  // the bucket this tile belongs to: tstart[j] <= tile < tstart[j + 1]
     const int32_t tile = (int32_t)blockIdx.x;
@@ -185,36 +188,49 @@ __global__ void __launch_bounds__(kNdThreads) nd_near_kernel(DomN A) {
   const int k = A.k, ls = A.ls;
   const int64_t qbeg = A.qstart[j] + (int64_t)((int32_t)blockIdx.x - A.tstart[j]) * kNdQ;
   const int64_t qend = A.qstart[j + 1];
+  // The queries of a bucket run in the dimension's (flipped) rank order, so their thresholds
+  // along k are nondecreasing: the tile only needs the chunk's sources below its largest one.
   int32_t T[kNdQPT][DD];
   int64_t tq[kNdQPT];
+  int32_t tkmax = 0;
 #pragma unroll
   for (int r = 0; r < kNdQPT; ++r) {
     const int64_t qi = qbeg + tid + r * kNdThreads;
-    tq[r] = qi < qend ? (int64_t)A.qlist[qi] : -1;
+    tq[r] = qi < qend ? (int64_t)A.order[k][A.rev[k] ? A.n - 1 - qi : qi] : -1;
 #pragma unroll
     for (int m = 0; m < DD; ++m) {
       int32_t tf = 0;  // dead lanes: nothing is below 0
       if (tq[r] >= 0) {
         tf = nd_thr(A, m, tq[r]);
         if (m < k) tf = (tf >> ls) << ls;
+        if (m == k) tkmax = max(tkmax, tf);
       }
       T[r][m] = tf;
     }
   }
-  const int64_t base = (A.rev[k] ? A.G - 1 - j : (int64_t)j) << ls;
-  const int ntile = (1 << ls) / kNdTile;
+  tkmax = __reduce_max_sync(0xffffffffu, tkmax);
+  if ((tid & 31) == 0) s_tmax[tid >> 5] = tkmax;
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < kNdThreads / 32; ++w) tkmax = max(tkmax, s_tmax[w]);
+  const bool revk = A.rev[k] != 0;
+  const int64_t base = (revk ? A.G - 1 - j : (int64_t)j) << ls;
+  const int ctiles = (1 << ls) / kNdTile;
+  int ntile = (int)((tkmax - ((int64_t)j << ls) + kNdTile - 1) / kNdTile);  // flipped offsets
+  ntile = ntile < 0 ? 0 : (ntile > ctiles ? ctiles : ntile);
   const int32_t *rec = A.rec + base * DP;
   auto issue = [&](int i) {
     const int sg = i & 1;
+    const int64_t u = revk ? ctiles - 1 - i : i;  // flipped order runs down the stored chunk
     fence_proxy_async_smem();
     mbar_expect_tx(&s_bar[sg], kRecBytes + (UNIT ? 0u : (uint32_t)NCH * kWBytes));
-    bulk_load_1d(s_rec[sg], rec + (int64_t)i * kNdTile * DP, kRecBytes, &s_bar[sg]);
+    bulk_load_1d(s_rec[sg], rec + u * kNdTile * DP, kRecBytes, &s_bar[sg]);
     if (!UNIT)
       for (int v = 0; v < NCH; ++v)
-        bulk_load_1d(&s_w[sg][v * kNdTile], A.wrec + (size_t)v * A.NP + base + (int64_t)i * kNdTile,
+        bulk_load_1d(&s_w[sg][v * kNdTile], A.wrec + (size_t)v * A.NP + base + u * kNdTile,
                      kWBytes, &s_bar[sg]);
   };
-  if (tid == 0) issue(0);
+  if (tid == 0 && ntile > 0) issue(0);
   int32_t cnt[kNdQPT] = {0};
   double acc[kNdQPT][NCH] = {{0.0}};
   for (int i = 0; i < ntile; ++i) {
@@ -260,7 +276,7 @@ __global__ void __launch_bounds__(kNdThreads) nd_near_kernel(DomN A) {
 }
 
 struct NdWs {
-  int32_t *rec, *qkey, *qlist, *qstart, *cursor, *tstart, *crec;
+  int32_t *rec, *qkey, *qstart, *tstart, *crec;
   double *wrec, *H, *EE, *IE, *erec;
 };
 
@@ -274,9 +290,7 @@ void carve_nd(Workspace &W, NdWs &q, int64_t n, int d, int nch, int ncodes, bool
     q.rec = W.take<int32_t>((size_t)pl.NP * DP);
     q.wrec = W.take<double>((size_t)pl.NP * nch);
     q.qkey = W.take<int32_t>(n);
-    q.qlist = W.take<int32_t>(n);
     q.qstart = W.take<int32_t>(pl.G + 3);
-    q.cursor = W.take<int32_t>(pl.G + 3);
     q.tstart = W.take<int32_t>(pl.G + 3);
   } else {
     q.EE = W.take<double>((size_t)n * d);
@@ -295,7 +309,8 @@ int nd_near_launch(const DomN &D, bool unit, unsigned grid, cudaStream_t st) {
 }
 
 // out[v][t] = sum_s w_v(s) prod_m [rev_m ? p_m(s) >= thr_m(t) + qoff_m : p_m(s) < thr_m(t) + qoff_m]
-// The ranking (p.r[m].pos / order for every m < d) must be in place.
+// The ranking (p.r[m].pos / order for every m < d) must be in place, and thr_m nondecreasing
+// along dimension m's rank order (positions, lower / upper tie ranks).
 int dom_nd(PtsWs &p, NdWs &q, int64_t n, int d, int nch, NdW w, const int *rev, const int *qoff,
            const int32_t *const *thr, double *out, int64_t out_vs, int64_t out_ts,
            cudaStream_t st) {
@@ -327,7 +342,6 @@ int dom_nd(PtsWs &p, NdWs &q, int64_t n, int d, int nch, NdW w, const int *rev, 
   D.rec = q.rec;
   D.wrec = unit ? nullptr : q.wrec;
   D.qkey = q.qkey;
-  D.qlist = q.qlist;
   D.qstart = q.qstart;
   D.tstart = q.tstart;
   // far field
@@ -361,7 +375,14 @@ int dom_nd(PtsWs &p, NdWs &q, int64_t n, int d, int nch, NdW w, const int *rev, 
       nd_qkey_kernel<<<grid_for(n, 256), 256, 0, st>>>(D);
       FCG_LAUNCH_CHECK();
     }
-    FCG_TRY(bucket(q.qkey, n, pl.G + 1, q.qlist, q.qstart, q.cursor, p, st));
+    // bucket starts only: a bucket's queries are a contiguous run of the dimension's rank order
+    FCG_CUDA_TRY(cudaMemsetAsync(q.qstart, 0, (size_t)(pl.G + 2) * 4, st));
+    {
+      FCG_PROF("pts_bucket", st);
+      bucket_count<<<grid_for(n, 256), 256, 0, st>>>(q.qkey, n, q.qstart);
+      FCG_LAUNCH_CHECK();
+    }
+    FCG_TRY(scan_i32(q.qstart, q.qstart, pl.G + 2, false, p.rw.partial, st));
     {
       FCG_PROF("pts_nd_keys", st);
       nd_tiles_kernel<<<grid_for(pl.G + 2, 256), 256, 0, st>>>(D);

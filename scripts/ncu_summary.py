@@ -25,8 +25,8 @@ SCOPES = [(r"^ecdf_final2d", "scan_lines_final"), (r"^final2d", "kde_final_group
           (r"^radix_scatter_kernel<.*SegMap, [1-9]", "kde_materialize"),
           (r"^radix_scatter", "radix_scatter"), (r"^radix_hist", "radix_hist"),
           (r"^part_bin", "part_bin"), (r"^plane_count", "plane_count"),
-          (r"^bin_scatter_kernel", "bin_scatter_count"), (r"^level2_self<0", "pts_level2_block"),
-          (r"^level2_self<1", "pts_level2_chunk"), (r"^group_gather", "pts_group_gather"),
+          (r"^bin_scatter_kernel", "bin_scatter_count"), (r"^level2_(self|codes)<0", "pts_level2_block"),
+          (r"^level2_(self|codes)<1", "pts_level2_chunk"), (r"^group_gather", "pts_group_gather"),
           (r"^group_psi", "pts_psi"), (r"^scan_(lookback|single)", "scan_i32"),
           (r"^minmax", "minmax")]
 
