@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(kNdThreads) nd_near_kernel(DomN A) {
 
 struct NdWs {
   int32_t *rec, *qkey, *qstart, *tstart, *crec;
-  double *wrec, *H, *EE, *IE, *erec;
+  double *wrec, *H, *EE, *IE, *erec, *trec, *wq;
 };
 
 inline int nd_rd(int d, int nw) { return (2 * d + nw + 1) & ~1; }  // doubles per KDE record
@@ -295,7 +295,12 @@ void carve_nd(Workspace &W, NdWs &q, int64_t n, int d, int nch, int ncodes, bool
   } else {
     q.EE = W.take<double>((size_t)n * d);
     q.IE = W.take<double>((size_t)n * d);
-    q.erec = W.take<double>((size_t)pl.NP * nd_rd(d, nch));
+    if (d <= 4) {  // table form of the near field
+      q.trec = W.take<double>((size_t)pl.NP << d);
+      q.wq = W.take<double>((size_t)pl.NP * 2);
+    } else {
+      q.erec = W.take<double>((size_t)pl.NP * nd_rd(d, nch));
+    }
     q.crec = W.take<int32_t>((size_t)pl.NP * DP);
   }
 }
@@ -418,8 +423,10 @@ struct KdeN {
   const double *w;  // [nw][n] or NULL
   double *EE, *IE;  // [d][n]: exp(+u), exp(-u), u = (x - c) / h
   double *H, *out;  // [nw][cells], [nw][n]
-  double *erec;     // [NP][RD]: E_0.., I_0.., w_0..
-  int32_t *crec;    // [NP][DP]: chunk of every dimension
+  double *erec;     // [NP][RD]: E_0.., I_0.., w_0..                      (d >= 5)
+  double *trec;     // [NP][2^d]: prod_m (bit m of the code ? I_m : E_m)  (d <= 4)
+  double *wq;       // [NP][2]: the weights                               (d <= 4)
+  int32_t *crec;    // [NP][DP]: position along every dimension (padding: -1)
 };
 
 __global__ void nd_kde_exp_kernel(KdeN K) {
@@ -587,6 +594,151 @@ void nd_kde_near_launch(const KdeN &K, unsigned grid, cudaStream_t st) {
   else nd_kde_near_kernel<DD, 2><<<grid, kNdThreads, 0, st>>>(K);
 }
 
+// ---- near field in table form (d = 3, 4) ----------------------------------------------------
+// Every point carries the 2^d products P[c] = prod_m (bit m of c ? exp(-u_m) : exp(+u_m)).  For a
+// pair the code c has bit m set where the source lies above the query, and the kernel value is
+// P_s[c] * P_t[~c]: one table read per side and one multiply instead of per-dimension factors.
+template <int DD>
+__global__ void nd_kde_tab_gather_kernel(KdeN K) {
+  constexpr int NC = 1 << DD;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < K.NP;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool live = i < K.n;
+    const int32_t s = live ? K.order[K.k][i] : 0;
+    double E[DD], I[DD];
+    int32_t c[4] = {-1, -1, -1, -1};
+#pragma unroll
+    for (int m = 0; m < DD; ++m) {
+      E[m] = live ? K.EE[(size_t)m * K.n + s] : 0.0;
+      I[m] = live ? K.IE[(size_t)m * K.n + s] : 0.0;
+      if (live) c[m] = K.pos[m][s];
+    }
+    double *tb = K.trec + i * NC;
+#pragma unroll
+    for (int code = 0; code < NC; ++code) {
+      double pr = (code & 1) ? I[0] : E[0];
+#pragma unroll
+      for (int m = 1; m < DD; ++m) pr *= ((code >> m) & 1) ? I[m] : E[m];
+      tb[code] = pr;
+    }
+    K.wq[2 * i] = live ? (K.w ? K.w[s] : 1.0) : 0.0;
+    K.wq[2 * i + 1] = (live && K.nw > 1) ? (K.w ? K.w[(size_t)K.n + s] : 1.0) : 0.0;
+    *reinterpret_cast<int4 *>(K.crec + i * 4) = make_int4(c[0], c[1], c[2], c[3]);
+  }
+}
+
+constexpr int kNdTabQPT = 2;
+inline size_t nd_kde_tab_smem(int d) {
+  const size_t NC = size_t(1) << d, NQ = kNdThreads * kNdTabQPT;
+  return (2 * kNdTileK * NC + 2 * kNdTileK * 2 + NC * NQ) * 8 + 2 * kNdTileK * 16 + 32;
+}
+
+// KK: the phase's dimension (pairs sharing a chunk along an earlier dimension are left to that
+// phase; phase 0 skips the query itself)
+template <int DD, int NW, int KK>
+__global__ void __launch_bounds__(kNdThreads) nd_kde_tab_kernel(KdeN K) {
+  constexpr int NC = 1 << DD, QPT = kNdTabQPT, NQ = kNdThreads * QPT, TS = kNdTileK;
+  constexpr uint32_t kTBytes = TS * NC * 8, kWBytes = TS * 16, kCBytes = TS * 16;
+  extern __shared__ __align__(128) unsigned char nd_smem[];
+  double *s_tab = reinterpret_cast<double *>(nd_smem);            // [2][TS][NC]
+  double *s_w = s_tab + 2 * TS * NC;                              // [2][TS][2]
+  double *s_q = s_w + 2 * TS * 2;                                 // [NC][NQ], complemented codes
+  int32_t *s_c = reinterpret_cast<int32_t *>(s_q + NC * NQ);      // [2][TS][4]
+  uint64_t *s_bar = reinterpret_cast<uint64_t *>(s_c + 2 * TS * 4);
+  const int tid = threadIdx.x;
+  const int ls = K.ls;
+  const int64_t q0 = (int64_t)blockIdx.x * NQ;  // dimension-k sorted index
+  const int64_t base = (q0 >> ls) << ls;        // uniform over the CTA
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  int32_t pt[QPT][DD], self[QPT];
+#pragma unroll
+  for (int r = 0; r < QPT; ++r) {
+    const int64_t qi = q0 + tid + r * kNdThreads;
+    const int4 c = *reinterpret_cast<const int4 *>(K.crec + qi * 4);
+    const int32_t cc[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int m = 0; m < DD; ++m) pt[r][m] = cc[m];
+#pragma unroll
+    for (int code = 0; code < NC; ++code)
+      s_q[(code ^ (NC - 1)) * NQ + r * kNdThreads + tid] = K.trec[qi * NC + code];
+    self[r] = (int32_t)(qi - base);
+  }
+  const int ntile = (1 << ls) / TS;
+  auto issue = [&](int i) {
+    const int sg = i & 1;
+    const int64_t off = base + (int64_t)i * TS;
+    fence_proxy_async_smem();
+    mbar_expect_tx(&s_bar[sg], kTBytes + kWBytes + kCBytes);
+    bulk_load_1d(s_tab + sg * TS * NC, K.trec + off * NC, kTBytes, &s_bar[sg]);
+    bulk_load_1d(s_w + sg * TS * 2, K.wq + off * 2, kWBytes, &s_bar[sg]);
+    bulk_load_1d(s_c + sg * TS * 4, K.crec + off * 4, kCBytes, &s_bar[sg]);
+  };
+  if (tid == 0) issue(0);
+  double acc[QPT][NW] = {{0.0}};
+  for (int i = 0; i < ntile; ++i) {
+    const int sg = i & 1;
+    if (tid == 0 && i + 1 < ntile) issue(i + 1);
+    mbar_wait(&s_bar[sg], (uint32_t)(i >> 1) & 1u);
+    const double *tb = s_tab + sg * TS * NC;
+    const double2 *w2 = reinterpret_cast<const double2 *>(s_w + sg * TS * 2);
+    const int4 *c4 = reinterpret_cast<const int4 *>(s_c + sg * TS * 4);
+#pragma unroll 2
+    for (int jj = 0; jj < TS; ++jj) {
+      const int4 c = c4[jj];
+      const int32_t ps[4] = {c.x, c.y, c.z, c.w};
+      const double2 wv = w2[jj];
+      const int32_t sj = i * TS + jj;
+#pragma unroll
+      for (int r = 0; r < QPT; ++r) {
+        unsigned code = 0;  // bit m: the source lies above the query along m
+#pragma unroll
+        for (int m = DD - 1; m >= 0; --m)
+          code = __funnelshift_l((unsigned)(pt[r][m] - ps[m]), code, 1);
+        double kv = tb[jj * NC + code] * s_q[code * NQ + r * kNdThreads + tid];
+        bool ok = KK > 0 || sj != self[r];
+#pragma unroll
+        for (int m = 0; m < KK; ++m) ok = ok && ((unsigned)(ps[m] ^ pt[r][m]) >> ls) != 0u;
+        kv = ok ? kv : 0.0;
+        acc[r][0] = fma(wv.x, kv, acc[r][0]);
+        if (NW > 1) acc[r][NW - 1] = fma(wv.y, kv, acc[r][NW - 1]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < QPT; ++r) {
+    const int64_t qi = q0 + tid + r * kNdThreads;
+    if (qi >= K.n) continue;
+    const int32_t t = K.order[KK][qi];
+#pragma unroll
+    for (int v = 0; v < NW; ++v) K.out[(size_t)v * K.n + t] += acc[r][v];
+  }
+}
+
+template <int DD, int NW, int KK>
+int nd_kde_tab_launch1(const KdeN &K, cudaStream_t st) {
+  const size_t sm = nd_kde_tab_smem(DD);
+  FCG_CUDA_TRY(cudaFuncSetAttribute(nd_kde_tab_kernel<DD, NW, KK>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  nd_kde_tab_kernel<DD, NW, KK>
+      <<<(unsigned)(K.NP / (kNdThreads * kNdTabQPT)), kNdThreads, sm, st>>>(K);
+  return FCG_OK;
+}
+template <int DD, int NW>
+int nd_kde_tab_launch(const KdeN &K, cudaStream_t st) {
+  switch (K.k) {
+    case 0: return nd_kde_tab_launch1<DD, NW, 0>(K, st);
+    case 1: return nd_kde_tab_launch1<DD, NW, 1>(K, st);
+    case 2: return nd_kde_tab_launch1<DD, NW, 2>(K, st);
+    default: return nd_kde_tab_launch1 < DD, NW, DD == 4 ? 3 : 2 > (K, st);
+  }
+}
+
 // out[v][t] = sum_{s != t} w_v(s) exp(-sum_m |x_sm - x_tm| / h_m)   (before the self term and
 // the normalisation, which kde_finish_kernel adds); the ranking must be in place
 int kde_nd(PtsWs &p, NdWs &q, const double *x, int64_t n, int d, const double *w, int nw,
@@ -617,6 +769,8 @@ int kde_nd(PtsWs &p, NdWs &q, const double *x, int64_t n, int d, const double *w
   K.H = q.H;
   K.out = out;
   K.erec = q.erec;
+  K.trec = q.trec;
+  K.wq = q.wq;
   K.crec = q.crec;
   {
     FCG_PROF("pts_psi", st);
@@ -648,19 +802,27 @@ int kde_nd(PtsWs &p, NdWs &q, const double *x, int64_t n, int d, const double *w
   const unsigned grid = (unsigned)(pl.NP / kNdThreads);
   for (int k = 0; k < d; ++k) {
     K.k = k;
+    if (d <= 4) {
+      {
+        FCG_PROF("pts_nd_gather", st);
+        if (d == 3) nd_kde_tab_gather_kernel<3><<<grid_for(pl.NP, 256), 256, 0, st>>>(K);
+        else nd_kde_tab_gather_kernel<4><<<grid_for(pl.NP, 256), 256, 0, st>>>(K);
+        FCG_LAUNCH_CHECK();
+      }
+      FCG_PROF("pts_nd_kde_near", st);
+      if (d == 3) FCG_TRY(nw == 1 ? (nd_kde_tab_launch<3, 1>(K, st)) : (nd_kde_tab_launch<3, 2>(K, st)));
+      else FCG_TRY(nw == 1 ? (nd_kde_tab_launch<4, 1>(K, st)) : (nd_kde_tab_launch<4, 2>(K, st)));
+      FCG_LAUNCH_CHECK();
+      continue;
+    }
     {
       FCG_PROF("pts_nd_gather", st);
-      if (d <= 4) nd_kde_gather_kernel<4><<<grid_for(pl.NP, 256), 256, 0, st>>>(K, RD);
-      else nd_kde_gather_kernel<8><<<grid_for(pl.NP, 256), 256, 0, st>>>(K, RD);
+      nd_kde_gather_kernel<8><<<grid_for(pl.NP, 256), 256, 0, st>>>(K, RD);
       FCG_LAUNCH_CHECK();
     }
     FCG_PROF("pts_nd_kde_near", st);
-    switch (d) {
-      case 3: nd_kde_near_launch<3>(K, grid, st); break;
-      case 4: nd_kde_near_launch<4>(K, grid, st); break;
-      case 5: nd_kde_near_launch<5>(K, grid, st); break;
-      default: nd_kde_near_launch<6>(K, grid, st); break;
-    }
+    if (d == 5) nd_kde_near_launch<5>(K, grid, st);
+    else nd_kde_near_launch<6>(K, grid, st);
     FCG_LAUNCH_CHECK();
   }
   return FCG_OK;
