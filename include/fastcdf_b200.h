@@ -290,7 +290,11 @@ int fcg_dominance_terms(const double *x, int64_t n, int32_t d, const double *psi
  * the d + 1 channels of dnc.py:661-669 are run as 2d + 1 Laplacian dominance channels whose
  * weights only change sign with the term (A = w e, B_k = s_k w e, C_l = s_l w xc_l e / h_l),
  * combined as A + sum_k (xc_k / h_k) B_k - sum_l C_l, + w, * 1 / (2^d n prod h (1 + d)).
- * One weight vector (or NULL); requires distinct coordinates; h, centre host (d,). */
+ * One weight vector (or NULL); requires distinct coordinates; h, centre host (d,).
+ * d = 3, 4 (n >= 8192): per sign code the two far-field channels sum w psi and sum w U psi
+ * (U = sum_k s_k u_k) on the coarse rank grid, pairs sharing a rank chunk summed directly as
+ * (1 + U_s - U_t) psi_s / psi_t from per-point tables (csrc/points_nd.cuh); d >= 5: direct
+ * tiles. */
 int fcg_kde_points_matern32(const double *x, int64_t n, int32_t d, const double *w,
                             const double *h, const double *centre, double *out,
                             void *ws, size_t *ws_bytes, void *stream);

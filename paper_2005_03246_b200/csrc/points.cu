@@ -1946,9 +1946,12 @@ extern "C" int fcg_kde_points_matern32(const double *x, int64_t n, int32_t d, co
   const int nchan = 2 * d + 1;
   Workspace W(ws);
   PtsWs p;
-  carve(W, p, n, d < 2 ? d : 2, 2, dom_ok, true, d == 1 ? n * 2 : 0);
+  const bool nd = nd_route(n, d) && d <= 4;  // table-form near field: d = 3, 4
+  carve(W, p, n, nd ? d : (d < 2 ? d : 2), 2, dom_ok, true, d == 1 ? n * 2 : 0);
   SelfWs q{};
   if (dom_ok) carve_self(W, q, n, 2);
+  NdWs nq{};
+  if (nd) carve_nd(W, nq, n, d, 2, 1 << d, true, true);
   double *wv = W.take<double>((size_t)n * nchan);
   double *acc = W.take<double>((size_t)n * nchan);
   double *psi1 = nullptr, *F1 = nullptr;
@@ -1970,6 +1973,14 @@ extern "C" int fcg_kde_points_matern32(const double *x, int64_t n, int32_t d, co
   double scale = 1.0 / (std::ldexp(1.0, d) * (double)n * prod_h);
   scale /= 1.0 + d;  // dnc.py:683-685
 
+  if (nd) {  // far field per sign code (two channels) + table-form near field
+    FCG_TRY(rank_all(x, n, d, p, st, false));
+    FCG_TRY(kde_nd(p, nq, x, n, d, w, 1, h, centre, out, st, true));
+    FCG_PROF("pts_finish", st);
+    kde_finish_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, 1, w, scale, out);
+    FCG_LAUNCH_CHECK();
+    return FCG_OK;
+  }
   if (d >= 3 || !(d == 1 || dom_ok)) {  // direct pairs with the matern32-additive kernel
     Brute B;
     B.n = n;

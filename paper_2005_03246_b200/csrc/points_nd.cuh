@@ -24,7 +24,9 @@
 // far field of every code is a coarse-grid dominance sum of psi_code = w prod_m E_m^{+-1}
 // (E_m = exp((x_m - c_m) / h_m)); pairs that share a chunk in some dimension are summed directly,
 // the kernel value formed as prod_m min(E_sm / E_tm, E_tm / E_sm) (no sign codes, no
-// cancellation); phase k takes the pairs whose first shared chunk is along dimension k.
+// cancellation); phase k takes the pairs whose first shared chunk is along dimension k.  For
+// d = 3, 4 every point carries the table of its 2^d signed products instead, so a pair costs one
+// table read per side and one multiply.
 
 constexpr int kNdThreads = 128;
 constexpr int kNdQPT = 2;                        // queries per thread (ECDF)
@@ -55,7 +57,7 @@ inline NdPlan nd_plan(int64_t n, int d, int nch, int ncodes, bool kde) {
     double cells = 1.0;
     for (int k = 0; k < d; ++k) cells *= (double)G;
     if (cells * 8.0 * nch > (double)kNdMaxCoarseBytes) continue;
-    const double near = (double)d * (double)n * (double)(int64_t(1) << ls) / (kde ? 6.5e11 : 2.5e12);
+    const double near = (double)d * (double)n * (double)(int64_t(1) << ls) / (kde ? (d <= 4 ? 1.25e12 : 6.5e11) : 5e12);
     const double far = (double)ncodes * nch * (cells * 8.0 * (2 * d + 2) / 4e12 + (d + 3) * 4e-6);
     const double cost = near + far;
     if (best_cost < 0.0 || cost < best_cost) {
@@ -277,12 +279,13 @@ __global__ void __launch_bounds__(kNdThreads) nd_near_kernel(DomN A) {
 
 struct NdWs {
   int32_t *rec, *qkey, *qstart, *tstart, *crec;
-  double *wrec, *H, *EE, *IE, *erec, *trec, *wq;
+  double *wrec, *H, *EE, *IE, *erec, *trec, *wq, *UU, *utab;
 };
 
 inline int nd_rd(int d, int nw) { return (2 * d + nw + 1) & ~1; }  // doubles per KDE record
 
-void carve_nd(Workspace &W, NdWs &q, int64_t n, int d, int nch, int ncodes, bool kde) {
+void carve_nd(Workspace &W, NdWs &q, int64_t n, int d, int nch, int ncodes, bool kde,
+              bool matern = false) {
   const NdPlan pl = nd_plan(n, d, nch, ncodes, kde);
   const int DP = d <= 4 ? 4 : 8;
   q.H = W.take<double>((size_t)pl.cells * nch);
@@ -295,6 +298,10 @@ void carve_nd(Workspace &W, NdWs &q, int64_t n, int d, int nch, int ncodes, bool
   } else {
     q.EE = W.take<double>((size_t)n * d);
     q.IE = W.take<double>((size_t)n * d);
+    if (matern) {
+      q.UU = W.take<double>((size_t)n * d);
+      q.utab = W.take<double>((size_t)pl.NP << d);
+    }
     if (d <= 4) {  // table form of the near field
       q.trec = W.take<double>((size_t)pl.NP << d);
       q.wq = W.take<double>((size_t)pl.NP * 2);
@@ -416,12 +423,15 @@ int dom_nd(PtsWs &p, NdWs &q, int64_t n, int d, int nch, NdW w, const int *rev, 
 struct KdeN {
   int64_t n, G, NP, cells;
   int d, ls, nw, k, code, first;
+  int matern;  // matern32-additive (dnc.py:659-685): kernel (1 + e) exp(-e), e = sum_m |du_m|
   const int32_t *pos[FCG_MAX_DIM], *order[FCG_MAX_DIM];
   int64_t stride[FCG_MAX_DIM];
   double c[FCG_MAX_DIM], h[FCG_MAX_DIM];
   const double *x;
   const double *w;  // [nw][n] or NULL
   double *EE, *IE;  // [d][n]: exp(+u), exp(-u), u = (x - c) / h
+  double *UU;       // [d][n]: u (matern)
+  double *utab;     // [NP][2^d]: U[c] = sum_m (bit m of c ? +u_m : -u_m) (matern, d <= 4)
   double *H, *out;  // [nw][cells], [nw][n]
   double *erec;     // [NP][RD]: E_0.., I_0.., w_0..                      (d >= 5)
   double *trec;     // [NP][2^d]: prod_m (bit m of the code ? I_m : E_m)  (d <= 4)
@@ -436,6 +446,7 @@ __global__ void nd_kde_exp_kernel(KdeN K) {
       const double u = (K.x[s * K.d + m] - K.c[m]) / K.h[m];
       K.EE[(size_t)m * K.n + s] = exp(u);
       K.IE[(size_t)m * K.n + s] = exp(-u);
+      if (K.matern) K.UU[(size_t)m * K.n + s] = u;
     }
 }
 
@@ -445,10 +456,18 @@ __global__ void nd_kde_scatter_kernel(KdeN K) {
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < K.n;
        s += (int64_t)gridDim.x * blockDim.x) {
     int64_t flat = 0;
-    double f = 1.0;
+    double f = 1.0, U = 0.0;
     for (int m = 0; m < K.d; ++m) {
+      const bool up = (K.code >> m) & 1;
       flat += (int64_t)(K.pos[m][s] >> K.ls) * K.stride[m];
-      f *= ((K.code >> m) & 1) ? K.IE[(size_t)m * K.n + s] : K.EE[(size_t)m * K.n + s];
+      f *= up ? K.IE[(size_t)m * K.n + s] : K.EE[(size_t)m * K.n + s];
+      if (K.matern) U += up ? K.UU[(size_t)m * K.n + s] : -K.UU[(size_t)m * K.n + s];
+    }
+    if (K.matern) {  // channels sum w psi and sum w U psi (one weight vector)
+      const double wf = (K.w ? K.w[s] : 1.0) * f;
+      atomicAdd(K.H + flat, wf);
+      atomicAdd(K.H + K.cells + flat, wf * U);
+      continue;
     }
     for (int v = 0; v < K.nw; ++v)
       atomicAdd(K.H + (size_t)v * K.cells + flat, (K.w ? K.w[(size_t)v * K.n + s] : 1.0) * f);
@@ -460,7 +479,7 @@ __global__ void nd_kde_query_kernel(KdeN K) {
        t += (int64_t)gridDim.x * blockDim.x) {
     int64_t flat = 0;
     bool live = true;
-    double z = 1.0;
+    double z = 1.0, U = 0.0;
     for (int m = 0; m < K.d; ++m) {
       const int64_t c = K.pos[m][t] >> K.ls;
       const bool up = (K.code >> m) & 1;
@@ -468,6 +487,13 @@ __global__ void nd_kde_query_kernel(KdeN K) {
       live = live && idx >= 0 && idx < K.G;
       flat += idx * K.stride[m];
       z *= up ? K.EE[(size_t)m * K.n + t] : K.IE[(size_t)m * K.n + t];
+      if (K.matern) U += up ? K.UU[(size_t)m * K.n + t] : -K.UU[(size_t)m * K.n + t];
+    }
+    if (K.matern) {  // sum_s w (1 + U_s - U_t) psi_s z_t
+      const double r = live ? z * ((1.0 - U) * K.H[flat] + K.H[K.cells + flat]) : 0.0;
+      double *o = K.out + t;
+      *o = K.first ? r : *o + r;
+      continue;
     }
     for (int v = 0; v < K.nw; ++v) {
       const double r = live ? z * K.H[(size_t)v * K.cells + flat] : 0.0;
@@ -621,6 +647,18 @@ __global__ void nd_kde_tab_gather_kernel(KdeN K) {
       for (int m = 1; m < DD; ++m) pr *= ((code >> m) & 1) ? I[m] : E[m];
       tb[code] = pr;
     }
+    if (K.matern) {
+      double u[DD];
+#pragma unroll
+      for (int m = 0; m < DD; ++m) u[m] = live ? K.UU[(size_t)m * K.n + s] : 0.0;
+#pragma unroll
+      for (int code = 0; code < NC; ++code) {
+        double U = 0.0;
+#pragma unroll
+        for (int m = 0; m < DD; ++m) U += ((code >> m) & 1) ? u[m] : -u[m];
+        K.utab[i * NC + code] = U;
+      }
+    }
     K.wq[2 * i] = live ? (K.w ? K.w[s] : 1.0) : 0.0;
     K.wq[2 * i + 1] = (live && K.nw > 1) ? (K.w ? K.w[(size_t)K.n + s] : 1.0) : 0.0;
     *reinterpret_cast<int4 *>(K.crec + i * 4) = make_int4(c[0], c[1], c[2], c[3]);
@@ -628,14 +666,15 @@ __global__ void nd_kde_tab_gather_kernel(KdeN K) {
 }
 
 constexpr int kNdTabQPT = 2;
-inline size_t nd_kde_tab_smem(int d) {
+inline size_t nd_kde_tab_smem(int d, bool matern) {
   const size_t NC = size_t(1) << d, NQ = kNdThreads * kNdTabQPT;
-  return (2 * kNdTileK * NC + 2 * kNdTileK * 2 + NC * NQ) * 8 + 2 * kNdTileK * 16 + 32;
+  return (2 * kNdTileK * NC + 2 * kNdTileK * 2 + NC * NQ) * 8 * (matern ? 2 : 1) +
+         2 * kNdTileK * 16 + 32;
 }
 
 // KK: the phase's dimension (pairs sharing a chunk along an earlier dimension are left to that
 // phase; phase 0 skips the query itself)
-template <int DD, int NW, int KK>
+template <int DD, int NW, int KK, bool MAT>
 __global__ void __launch_bounds__(kNdThreads) nd_kde_tab_kernel(KdeN K) {
   constexpr int NC = 1 << DD, QPT = kNdTabQPT, NQ = kNdThreads * QPT, TS = kNdTileK;
   constexpr uint32_t kTBytes = TS * NC * 8, kWBytes = TS * 16, kCBytes = TS * 16;
@@ -643,7 +682,10 @@ __global__ void __launch_bounds__(kNdThreads) nd_kde_tab_kernel(KdeN K) {
   double *s_tab = reinterpret_cast<double *>(nd_smem);            // [2][TS][NC]
   double *s_w = s_tab + 2 * TS * NC;                              // [2][TS][2]
   double *s_q = s_w + 2 * TS * 2;                                 // [NC][NQ], complemented codes
-  int32_t *s_c = reinterpret_cast<int32_t *>(s_q + NC * NQ);      // [2][TS][4]
+  double *s_ut = s_q + NC * NQ;                                   // [2][TS][NC]     (matern)
+  double *s_qu = s_ut + (MAT ? 2 * TS * NC : 0);                  // [NC][NQ]        (matern)
+  int32_t *s_c = reinterpret_cast<int32_t *>(
+      s_qu + (MAT ? NC * NQ + 2 * TS * 2 : 0));                   // [2][TS][4]
   uint64_t *s_bar = reinterpret_cast<uint64_t *>(s_c + 2 * TS * 4);
   const int tid = threadIdx.x;
   const int ls = K.ls;
@@ -664,8 +706,10 @@ __global__ void __launch_bounds__(kNdThreads) nd_kde_tab_kernel(KdeN K) {
 #pragma unroll
     for (int m = 0; m < DD; ++m) pt[r][m] = cc[m];
 #pragma unroll
-    for (int code = 0; code < NC; ++code)
+    for (int code = 0; code < NC; ++code) {
       s_q[(code ^ (NC - 1)) * NQ + r * kNdThreads + tid] = K.trec[qi * NC + code];
+      if (MAT) s_qu[code * NQ + r * kNdThreads + tid] = K.utab[qi * NC + code];
+    }
     self[r] = (int32_t)(qi - base);
   }
   const int ntile = (1 << ls) / TS;
@@ -673,7 +717,8 @@ __global__ void __launch_bounds__(kNdThreads) nd_kde_tab_kernel(KdeN K) {
     const int sg = i & 1;
     const int64_t off = base + (int64_t)i * TS;
     fence_proxy_async_smem();
-    mbar_expect_tx(&s_bar[sg], kTBytes + kWBytes + kCBytes);
+    mbar_expect_tx(&s_bar[sg], (MAT ? 2 : 1) * kTBytes + kWBytes + kCBytes);
+    if (MAT) bulk_load_1d(s_ut + sg * TS * NC, K.utab + off * NC, kTBytes, &s_bar[sg]);
     bulk_load_1d(s_tab + sg * TS * NC, K.trec + off * NC, kTBytes, &s_bar[sg]);
     bulk_load_1d(s_w + sg * TS * 2, K.wq + off * 2, kWBytes, &s_bar[sg]);
     bulk_load_1d(s_c + sg * TS * 4, K.crec + off * 4, kCBytes, &s_bar[sg]);
@@ -685,6 +730,7 @@ __global__ void __launch_bounds__(kNdThreads) nd_kde_tab_kernel(KdeN K) {
     if (tid == 0 && i + 1 < ntile) issue(i + 1);
     mbar_wait(&s_bar[sg], (uint32_t)(i >> 1) & 1u);
     const double *tb = s_tab + sg * TS * NC;
+    const double *ub = s_ut + sg * TS * NC;
     const double2 *w2 = reinterpret_cast<const double2 *>(s_w + sg * TS * 2);
     const int4 *c4 = reinterpret_cast<const int4 *>(s_c + sg * TS * 4);
 #pragma unroll 2
@@ -700,6 +746,7 @@ __global__ void __launch_bounds__(kNdThreads) nd_kde_tab_kernel(KdeN K) {
         for (int m = DD - 1; m >= 0; --m)
           code = __funnelshift_l((unsigned)(pt[r][m] - ps[m]), code, 1);
         double kv = tb[jj * NC + code] * s_q[code * NQ + r * kNdThreads + tid];
+        if (MAT) kv *= 1.0 + (ub[jj * NC + code] - s_qu[code * NQ + r * kNdThreads + tid]);
         bool ok = KK > 0 || sj != self[r];
 #pragma unroll
         for (int m = 0; m < KK; ++m) ok = ok && ((unsigned)(ps[m] ^ pt[r][m]) >> ls) != 0u;
@@ -720,31 +767,36 @@ __global__ void __launch_bounds__(kNdThreads) nd_kde_tab_kernel(KdeN K) {
   }
 }
 
-template <int DD, int NW, int KK>
+template <int DD, int NW, int KK, bool MAT>
 int nd_kde_tab_launch1(const KdeN &K, cudaStream_t st) {
-  const size_t sm = nd_kde_tab_smem(DD);
-  FCG_CUDA_TRY(cudaFuncSetAttribute(nd_kde_tab_kernel<DD, NW, KK>,
+  const size_t sm = nd_kde_tab_smem(DD, MAT);
+  FCG_CUDA_TRY(cudaFuncSetAttribute(nd_kde_tab_kernel<DD, NW, KK, MAT>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  nd_kde_tab_kernel<DD, NW, KK>
+  nd_kde_tab_kernel<DD, NW, KK, MAT>
       <<<(unsigned)(K.NP / (kNdThreads * kNdTabQPT)), kNdThreads, sm, st>>>(K);
   return FCG_OK;
 }
-template <int DD, int NW>
+template <int DD, int NW, bool MAT>
 int nd_kde_tab_launch(const KdeN &K, cudaStream_t st) {
+  constexpr int KL = DD - 1;
   switch (K.k) {
-    case 0: return nd_kde_tab_launch1<DD, NW, 0>(K, st);
-    case 1: return nd_kde_tab_launch1<DD, NW, 1>(K, st);
-    case 2: return nd_kde_tab_launch1<DD, NW, 2>(K, st);
-    default: return nd_kde_tab_launch1 < DD, NW, DD == 4 ? 3 : 2 > (K, st);
+    case 0: return nd_kde_tab_launch1<DD, NW, 0, MAT>(K, st);
+    case 1: return nd_kde_tab_launch1<DD, NW, 1, MAT>(K, st);
+    case 2: return nd_kde_tab_launch1<DD, NW, 2, MAT>(K, st);
+    default: return nd_kde_tab_launch1<DD, NW, KL, MAT>(K, st);
   }
 }
 
 // out[v][t] = sum_{s != t} w_v(s) exp(-sum_m |x_sm - x_tm| / h_m)   (before the self term and
 // the normalisation, which kde_finish_kernel adds); the ranking must be in place
+// matern (d <= 4, nw == 1): the matern32-additive kernel (1 + e) exp(-e) instead; its far field
+// needs the two channels sum w psi and sum w U psi per code (workspace carved with nch = 2)
 int kde_nd(PtsWs &p, NdWs &q, const double *x, int64_t n, int d, const double *w, int nw,
-           const double *h, const double *centre, double *out, cudaStream_t st) {
+           const double *h, const double *centre, double *out, cudaStream_t st,
+           bool matern = false) {
   const int ncodes = 1 << d;
-  const NdPlan pl = nd_plan(n, d, nw, ncodes, true);
+  const int nchan = matern ? 2 : nw;
+  const NdPlan pl = nd_plan(n, d, nchan, ncodes, true);
   KdeN K{};
   K.n = n;
   K.G = pl.G;
@@ -764,8 +816,11 @@ int kde_nd(PtsWs &p, NdWs &q, const double *x, int64_t n, int d, const double *w
   }
   K.x = x;
   K.w = w;
+  K.matern = matern ? 1 : 0;
   K.EE = q.EE;
   K.IE = q.IE;
+  K.UU = q.UU;
+  K.utab = q.utab;
   K.H = q.H;
   K.out = out;
   K.erec = q.erec;
@@ -786,13 +841,13 @@ int kde_nd(PtsWs &p, NdWs &q, const double *x, int64_t n, int d, const double *w
     K.first = code == 0;
     bool brev[FCG_MAX_DIM];
     for (int m = 0; m < d; ++m) brev[m] = (code >> m) & 1;
-    FCG_CUDA_TRY(cudaMemsetAsync(q.H, 0, (size_t)pl.cells * nw * 8, st));
+    FCG_CUDA_TRY(cudaMemsetAsync(q.H, 0, (size_t)pl.cells * nchan * 8, st));
     {
       FCG_PROF("pts_nd_scatter", st);
       nd_kde_scatter_kernel<<<grid_for(n, 256), 256, 0, st>>>(K);
       FCG_LAUNCH_CHECK();
     }
-    for (int v = 0; v < nw; ++v)
+    for (int v = 0; v < nchan; ++v)
       FCG_TRY(scan_lattice<double>(q.H + (size_t)v * pl.cells, gs, brev, inplace, p.scratch, st));
     FCG_PROF("pts_nd_far", st);
     nd_kde_query_kernel<<<grid_for(n, 256), 256, 0, st>>>(K);
@@ -810,8 +865,13 @@ int kde_nd(PtsWs &p, NdWs &q, const double *x, int64_t n, int d, const double *w
         FCG_LAUNCH_CHECK();
       }
       FCG_PROF("pts_nd_kde_near", st);
-      if (d == 3) FCG_TRY(nw == 1 ? (nd_kde_tab_launch<3, 1>(K, st)) : (nd_kde_tab_launch<3, 2>(K, st)));
-      else FCG_TRY(nw == 1 ? (nd_kde_tab_launch<4, 1>(K, st)) : (nd_kde_tab_launch<4, 2>(K, st)));
+      if (matern) {
+        FCG_TRY(d == 3 ? (nd_kde_tab_launch<3, 1, true>(K, st)) : (nd_kde_tab_launch<4, 1, true>(K, st)));
+      } else if (d == 3) {
+        FCG_TRY(nw == 1 ? (nd_kde_tab_launch<3, 1, false>(K, st)) : (nd_kde_tab_launch<3, 2, false>(K, st)));
+      } else {
+        FCG_TRY(nw == 1 ? (nd_kde_tab_launch<4, 1, false>(K, st)) : (nd_kde_tab_launch<4, 2, false>(K, st)));
+      }
       FCG_LAUNCH_CHECK();
       continue;
     }

@@ -33,3 +33,5 @@ for d, n in cases:
     fcb.ecdf_dnc(su, scaled=False); fcb.kde_dnc(s, fcb.laplacian(), bw); torch.cuda.synchronize()
     rep = _lib.profile_report(); _lib.profile_enable(False)
     print("   ", {k: (v[0], round(v[1], 3)) for k, v in rep.items() if v[1] > 0.05}, flush=True)
+    t_m = timeit(lambda: fcb.kde_dnc(s, fcb.matern32_additive(), bw)) if d <= 4 else float("nan")
+    print(f"    matern32-additive kde_dnc {t_m:.2f} ms", flush=True)

@@ -391,6 +391,7 @@ def nd_golden():
         bag.put(key + ".ecdf_scaled", fc.ecdf_dnc(su).values)
         bag.put(key + ".kde_w", fc.kde_dnc(s, fc.laplacian(), fc.Bandwidth.diag(h)).values)
         bag.put(key + ".kde_unit", fc.kde_dnc(su, fc.laplacian(), fc.Bandwidth.diag(h)).values)
+        bag.put(key + ".mat_w", fc.kde_dnc(s, fc.matern32_additive(), fc.Bandwidth.diag(h)).values)
         if d <= 4:
             tt = fc.kde_terms_dnc(s, fc.Bandwidth.diag(h), (0, d - 1, 1, 1))
             rows = rng.integers(0, n, 400)

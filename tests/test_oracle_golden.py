@@ -159,3 +159,6 @@ def test_nd_direct_sums_vs_reference_recursion(oracle):
         np.testing.assert_array_equal(got, g[key + ".ecdf_unit_self"])
         got = oracle.kde_naive_laplacian(x, w, x, h)
         np.testing.assert_allclose(got, g[key + ".kde_w"], rtol=1e-10, atol=0)
+        sub = np.arange(0, x.shape[0], 37)
+        got = oracle.kde_naive_matern32(x, w, x[sub], h)
+        np.testing.assert_allclose(got, g[key + ".mat_w"][sub], rtol=1e-10, atol=0)

@@ -38,6 +38,7 @@ def test_nd_reference_golden(d, nd_golden):
     bw = fcb.Bandwidth.diag(h)
     assert rel_err(fcb.kde_dnc(s, fcb.laplacian(), bw).values, g[key + ".kde_w"]) <= 1e-9
     assert rel_err(fcb.kde_dnc(su, fcb.laplacian(), bw).values, g[key + ".kde_unit"]) <= 1e-9
+    assert rel_err(fcb.kde_dnc(s, fcb.matern32_additive(), bw).values, g[key + ".mat_w"]) <= 1e-9
     if d <= 4:
         tt = fcb.kde_terms_dnc(s, bw, (0, d - 1, 1, 1))
         rows, ref = g[key + ".terms_rows"], g[key + ".terms"]
@@ -134,3 +135,19 @@ def test_nd_terms_vs_direct(oracle):
         for a, j in enumerate(q):
             exp_q[a, code] = tt.psi[np.all(sp < sp[j], axis=1), code].sum()
     assert np.max(np.abs(tt.table[q] - exp_q)) <= 1e-11 * np.max(np.abs(exp_q))
+
+
+@pytest.mark.parametrize("d,n", [(3, 120_000), (4, 30_000)])
+def test_nd_kde_dnc_matern32_vs_oracle(d, n, oracle):
+    """matern32-additive at the points for d = 3, 4 (dnc.py:659-685): two far-field channels per
+    sign code + the table-form near field, against the direct sum on a query subset."""
+    rng = np.random.default_rng(900 + d)
+    x = rng.standard_normal((n, d))
+    x[: n // 4] = x[: n // 4] * 0.03 - 0.5
+    w = rng.standard_normal(n)  # signed weights
+    h = rng.uniform(0.2, 0.7, d)
+    q = rng.integers(0, n, 300)
+    got = fcb.kde_dnc(fcb.validate_sample(x, w), fcb.matern32_additive(), fcb.Bandwidth.diag(h)).values
+    ref = oracle.kde_naive_matern32(x, w, x[q], h)
+    scale = oracle.kde_naive_matern32(x, np.abs(w), x[q], h)
+    assert rel_err(got[q], ref, scale) <= 1e-9
