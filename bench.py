@@ -3,7 +3,7 @@
 "ECDF/Laplacian-KDE points/sec at 1/2/4/8 B200; % of HBM roofline").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload cfg5|cfg5a|cfg5b|cfg3|cfg1|cfg2|cfg4]
+                    [--workload cfg5|cfg5a|cfg5b|cfg3|cfg1|cfg2|cfg4|nd3]
 
 Default workload: BASELINE config 5 (the largest configuration that fits one GPU): N = 1e8
 points iid U[0,1]^4 on a 128^4 grid; one step = the 4-D grid ECDF (y == 1) followed by the
@@ -538,12 +538,15 @@ class PointsWorkload:
 
         self.fcb = fcb
         self.name = name
-        self.w = wl.cfg2() if name == "cfg2" else wl.cfg4()
+        self.w = wl.cfg2() if name == "cfg2" else (wl.nd3() if name == "nd3" else wl.cfg4())
         self.n, self.d = self.w.n, self.w.d
 
     def describe(self):
         if self.name == "cfg2":
             what = "2-D ECDF at the points, ties (1024 levels), y~U(0,1), delta=(1,-1) + ESF"
+        elif self.name == "nd3":
+            what = ("3-D Laplacian KDE density + kernel-regression numerators at the points, "
+                    "h=0.2 (not a BASELINE config: the SURVEY 8f #3 widening)")
         else:
             what = "2-D Laplacian KDE density + kernel-regression numerators at the points, h=0.1"
         return {"workload": self.name, "what": what, "n_points": self.n, "dims": self.d,
@@ -559,7 +562,7 @@ class PointsWorkload:
         fcb = self.fcb
         if self.name == "cfg2":
             return fcb.Sample(x, y, None, False)
-        return fcb.Sample(x, None, (True, True), True)
+        return fcb.Sample(x, None, (True,) * self.d, True)
 
     def to_device(self):
         import torch
@@ -586,7 +589,7 @@ class PointsWorkload:
         if self.name == "cfg2":  # both outputs from one ranking of the points
             a, b = fcb.ecdf_esf_at_points(s, fcb.DeltaVector(self.w.delta))
             return a.values, b.values
-        if self.world > 1:
+        if self.world > 1 and self.name == "cfg4":
             from paper_2005_03246_b200 import distributed as fdist
 
             num = fdist.kde_numerators_sharded(s, [None, y], fcb.Bandwidth.diag(self.w.h))
@@ -632,6 +635,8 @@ class PointsWorkload:
         b = radix_bytes(n)
         if self.name == "cfg2":
             b.update({"pts_rank_scatter": (8 + 8 + 8) * n, "pts_gather": (8 + 8 + 8) * n})
+        elif self.name == "nd3":
+            pass  # pair-test kernels: issue-bound, no byte model
         else:
             # level-2 solvers: per source (id + 2 positions + 2 psi) and per query (threshold
             # pair + list entry + 2-channel output read-modify-write)
@@ -666,7 +671,7 @@ class PointsWorkload:
                 fc.esf_fastsum(s, g).values[flat]
             return self.n, ("full configuration; fastcdf.ecdf_fastsum + esf_fastsum on the "
                             "1024-level lattice, gathered at the points"), call
-        m = 1_000_000
+        m = 200_000 if self.name == "nd3" else 1_000_000
         s1 = fc.validate_sample(x[:m])
         s2 = fc.validate_sample(x[:m], self.w.extra["y"][:m])
         bw = fc.Bandwidth.diag(self.w.h)
@@ -686,8 +691,10 @@ class PointsWorkload:
             fc.ecdf_fastsum(s, g, fc.DeltaVector((1, -1)))
             fc.esf_fastsum(s, g)
         else:
+            if self.name == "nd3":
+                x = rng.random((256, 3))
             fc.kde_dnc(fc.validate_sample(x, rng.random(256)), fc.laplacian(),
-                       fc.Bandwidth.diag(np.array([0.1, 0.1])))
+                       fc.Bandwidth.diag(np.full(x.shape[1], 0.1)))
 
     def cpu_sample(self, threads):
         import oracle
@@ -699,6 +706,15 @@ class PointsWorkload:
             oracle.esf_at_points(self.w.points, self.w.weights)
             dt = time.perf_counter() - t0
             return self.n / dt, used, "full config (ECDF + ESF via the exact rank lattice)", dt
+        if self.name == "nd3":  # the oracle has direct sums only for d = 3: a query subset
+            m, nq = 200_000, 2_000
+            used = oracle.set_threads(threads)
+            t0 = time.perf_counter()
+            oracle.kde_naive_laplacian(self.w.points[:m], None, self.w.points[:nq], self.w.h)
+            oracle.kde_naive_laplacian(self.w.points[:m], self.w.extra["y"][:m],
+                                       self.w.points[:nq], self.w.h)
+            dt = time.perf_counter() - t0
+            return nq / dt, used, f"direct sums of {nq} queries over the first {m} points", dt
         m = 1_000_000
         t0 = time.perf_counter()
         oracle.kde_dnc_laplacian(self.w.points[:m], None, self.w.h)
@@ -710,7 +726,7 @@ class PointsWorkload:
 def make_workload(name):
     if name in ("cfg1", "cfg3", "cfg5", "cfg5a", "cfg5b"):
         return GridWorkload(name)
-    if name in ("cfg2", "cfg4"):
+    if name in ("cfg2", "cfg4", "nd3"):
         return PointsWorkload(name)
     raise SystemExit(f"unknown workload {name!r}")
 

@@ -95,6 +95,17 @@ def cfg4(n: int = 10_000_000) -> Workload:
     return Workload("cfg4", x, None, None, None, np.array([0.1, 0.1]), {"y": y})
 
 
+def nd3(n: int = 1_000_000) -> Workload:
+    """Not a BASELINE config (SURVEY §8f #3 widening): config 4's problem in three dimensions --
+    Laplacian KDE + kernel regression at the points, 8-component Gaussian mixture, h = 0.2."""
+    rng = np.random.default_rng(43)
+    comp = rng.integers(0, 8, n)
+    means = np.array([[a, b, c] for a in (-1.5, 1.5) for b in (-1.5, 1.5) for c in (-1.5, 1.5)])
+    x = means[comp] + 0.5 * rng.standard_normal((n, 3))
+    y = np.sin(3.0 * x[:, 0]) + np.cos(2.0 * x[:, 1]) + x[:, 2] + 0.1 * rng.standard_normal(n)
+    return Workload("nd3", x, None, None, None, np.array([0.2, 0.2, 0.2]), {"y": y})
+
+
 def cfg5(n: int = 100_000_000, m: int = 128, dtype_chunk: int = 0) -> Workload:
     """4-D grid ECDF (y == 1) + Laplacian KDE (y ~ Exp(1), h = 0.05): Uniform[0,1]^4,
     128^4 grid on [0, 1]^4."""
