@@ -1204,6 +1204,14 @@ void carve(Workspace &W, PtsWs &p, int64_t n, int d, int nch, bool need_dom, boo
 // mask: the dimension's digit mask (radix_digit_masks_f64), or ~0u to compute it here (syncs).
 int rank_dim(const double *x, int64_t n, int d, int k, PtsWs &p, cudaStream_t st, bool ties = true,
              uint32_t mask = ~0u) {
+  if (!ties && mask != ~0u && __builtin_popcount(mask & 0xFu) >= 2) {
+    // continuous data, positions only: sort the keys' top halves, order the short runs of
+    // equal top halves by the low halves (falls through when a run is too long)
+    bool done = false;
+    FCG_TRY(rank_order_split_f64(x + k, n, d, mask, reinterpret_cast<uint32_t *>(p.k), p.v, p.rw,
+                                 p.ndist + k, p.r[k].order, &done, st));
+    if (done) return pos_from_order(p.r[k].order, n, p.r[k].pos, st);
+  }
   FCG_TRY(radix_init_f64(x + k, n, d, p.k, p.v, st));
   if (mask == ~0u) FCG_TRY(radix_sort_pairs_pruned(p.k, p.v, n, p.rw, st));
   else FCG_TRY(radix_sort_pairs_mask(p.k, p.v, n, mask, p.rw, st));

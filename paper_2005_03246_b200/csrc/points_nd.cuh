@@ -52,7 +52,7 @@ struct NdPlan {
 inline NdPlan nd_plan(int64_t n, int d, int nch, int ncodes, bool kde) {
   NdPlan best{};
   double best_cost = -1.0;
-  for (int ls = kNdMinLs; ls <= 24; ++ls) {
+  for (int ls = kNdMinLs; ls <= 31; ++ls) {  // ends at G == 1 (one cell, always admissible)
     const int64_t G = ceil_div(n, int64_t(1) << ls);
     double cells = 1.0;
     for (int k = 0; k < d; ++k) cells *= (double)G;

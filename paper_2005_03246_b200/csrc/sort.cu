@@ -618,6 +618,102 @@ int radix_digit_masks_f64(const double *x, int64_t n, int d, unsigned long long 
   return FCG_OK;
 }
 
+// ---- positions-only ranking through the keys' top halves ---------------------------------
+constexpr int kTieRun = 48;  // longest run of equal top halves ordered in place
+
+__global__ void radix_init_hi32_kernel(const double *__restrict__ x, int64_t n, int64_t stride,
+                                       uint32_t *__restrict__ keys, int32_t *__restrict__ vals) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = (uint32_t)(f64_key(x[i * stride]) >> 32);
+    vals[i] = (int32_t)i;
+  }
+}
+
+// Runs of equal top halves (sorted; members in index order: the LSD passes are stable) are put
+// in (low half, index) order.  First the low halves of the run members are gathered next to
+// their keys; then every member counts the members of its run that precede it and writes its
+// index to that slot of `order` (singletons copy).  Runs longer than kTieRun raise *flag.
+__global__ void tie_low_kernel(const double *__restrict__ x, int64_t stride,
+                               const uint32_t *__restrict__ keys, const int32_t *__restrict__ vals,
+                               int64_t n, uint32_t *__restrict__ low) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = keys[p];
+    const bool in_run = (p > 0 && keys[p - 1] == k) || (p + 1 < n && keys[p + 1] == k);
+    if (in_run) low[p] = (uint32_t)f64_key(x[(int64_t)vals[p] * stride]);
+  }
+}
+
+__global__ void tie_rank_kernel(const uint32_t *__restrict__ keys, const uint32_t *__restrict__ low,
+                                const int32_t *__restrict__ vals, int64_t n,
+                                int32_t *__restrict__ order, int32_t *__restrict__ flag) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = keys[p];
+    const int32_t me = vals[p];
+    int before = 0, back = 0;  // members ahead of this one in (low, position) order
+    if (p > 0 && keys[p - 1] == k) {
+      const uint32_t l = low[p];
+      while (back < kTieRun && p - 1 - back >= 0 && keys[p - 1 - back] == k) {
+        before += low[p - 1 - back] <= l ? 1 : 0;  // earlier position wins ties
+        ++back;
+      }
+      if (back == kTieRun) *flag = 1;
+    }
+    int fwd = 0;
+    if (p + 1 < n && keys[p + 1] == k) {
+      const uint32_t l = low[p];
+      while (fwd < kTieRun && p + 1 + fwd < n && keys[p + 1 + fwd] == k) {
+        before += low[p + 1 + fwd] < l ? 1 : 0;
+        ++fwd;
+      }
+      if (fwd == kTieRun) *flag = 1;
+    }
+    order[p - back + before] = me;
+  }
+}
+
+__global__ void pos_from_order_kernel(const int32_t *__restrict__ order, int64_t n,
+                                      int32_t *__restrict__ pos) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    pos[order[p]] = (int32_t)p;
+}
+
+int rank_order_split_f64(const double *x, int64_t n, int64_t stride, uint32_t mask,
+                         uint32_t *keys32, int32_t *vals, const RadixWs &ws, int32_t *flag_dev,
+                         int32_t *order, bool *done, cudaStream_t st) {
+  *done = false;
+  if (n <= 1) return FCG_OK;
+  {
+    FCG_PROF("radix_init", st);
+    FCG_CUDA_TRY(cudaMemsetAsync(flag_dev, 0, 4, st));
+    radix_init_hi32_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(x, n, stride, keys32, vals);
+    FCG_LAUNCH_CHECK();
+  }
+  FCG_TRY(radix_sort_digits<uint32_t>(keys32, vals, n, (mask >> 4) & 0xFu, ws, st));
+  {
+    FCG_PROF("rank_tie_fix", st);
+    uint32_t *low = reinterpret_cast<uint32_t *>(ws.keys_alt);  // free after the in-place sort
+    tie_low_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(x, stride, keys32, vals, n, low);
+    tie_rank_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(keys32, low, vals, n, order, flag_dev);
+    FCG_LAUNCH_CHECK();
+  }
+  int32_t h = 0;
+  FCG_TRY(read_small(&h, flag_dev, 4, st));
+  *done = h == 0;
+  return FCG_OK;
+}
+
+int pos_from_order(const int32_t *order, int64_t n, int32_t *pos, cudaStream_t st) {
+  if (n <= 0) return FCG_OK;
+  FCG_PROF("rank_heads", st);
+  pos_from_order_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(order, n, pos);
+  FCG_LAUNCH_CHECK();
+  return FCG_OK;
+}
+
 int radix_sort_pairs_mask(uint64_t *keys, int32_t *vals, int64_t n, uint32_t mask,
                           const RadixWs &ws, cudaStream_t st) {
   return radix_sort_digits<uint64_t>(keys, vals, n, mask, ws, st);

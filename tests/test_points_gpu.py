@@ -442,3 +442,24 @@ def test_rank_tiebreak_matches_stable_argsort():
     np.testing.assert_array_equal(fcb.rank_tiebreak(pts), ref)
     # ranks restore distinct coordinates: the strict ECDF then counts index-ordered ties
     assert fcb.validate_sample(fcb.rank_tiebreak(pts)).distinct
+
+
+@pytest.mark.parametrize("case", ["one_top_half", "short_runs", "mixed"])
+def test_split_key_ranking_paths(case, oracle):
+    """The positions-only ranking sorts the keys' top 32 bits and orders runs of equal top halves
+    by the low halves; coordinates that share their top halves by the thousand must fall back to
+    the full-key sort.  Checked through ecdf_dnc (bit-exact counts) on d = 2."""
+    rng = np.random.default_rng(5)
+    n = 60_000
+    if case == "one_top_half":   # every coordinate in [1, 1 + 2^-21): one run of n members
+        x = 1.0 + rng.permutation(n)[:, None] * 2.0 ** -50 + np.array([[0.0, 2.0 ** -51]])
+        x = np.stack([x[:, 0], 1.0 + rng.permutation(n) * 2.0 ** -50], axis=1)
+    elif case == "short_runs":   # runs of ~8 members sharing 32 top bits
+        base = rng.standard_normal((n // 8, 2)).astype(np.float32).astype(np.float64)
+        x = np.repeat(base, 8, axis=0) * (1.0 + rng.permutation(n)[:, None] * 2.0 ** -45)
+    else:
+        x = rng.standard_normal((n, 2))
+        x[: n // 2, 0] = 3.0 + rng.permutation(n // 2) * 2.0 ** -48
+    s = fcb.validate_sample(x)
+    got = fcb.ecdf_dnc(s, scaled=False).values
+    np.testing.assert_array_equal(got, oracle.ecdf_dnc(x, None, scaled=False))
