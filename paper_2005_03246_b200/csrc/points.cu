@@ -691,114 +691,115 @@ __device__ __forceinline__ double code_s(const KdeP &kp, double x0, double x1) {
 // Coarse rows of every code, prefixed along the block axis: CTA per unflipped chunk g.  The
 // chunk's points arrive in p0 order, so their blocks are nondecreasing and the inclusive prefix
 // at block b is a running sum over the points evaluated at the last point of block <= b: one
-// CTA-wide scan per (code, channel) and plain run stores, no atomics.  Codes with f0 = 1 store
-// their grid flipped along the block axis: suffix sums, written at P-1-b.  Row f1 ? P-1-g : g.
+// CTA-wide scan per (code, channel), parked in shared memory, and an output-ordered pass where
+// every thread finds its block's point by binary search and stores coalesced.  Codes with
+// f0 = 1 store their grid flipped along the block axis: suffix sums (second sweep), written at
+// P-1-b.  Row f1 ? P-1-g : g.  No atomics.
 constexpr int kCoarseThreads = 512;
 constexpr int kCoarsePer = S / kCoarseThreads;  // consecutive points per thread
 
 template <int NCH>
-__global__ void __launch_bounds__(kCoarseThreads) coarse_rows_codes(Dom2S D, Codes K) {
-  constexpr int NQ = 4 * NCH, NW = kCoarseThreads / 32;
-  __shared__ double s_wtot[NQ][NW];
-  __shared__ int32_t s_first[kCoarseThreads + 1], s_last[kCoarseThreads + 1];
+__global__ void __launch_bounds__(kCoarseThreads, 2) coarse_rows_codes(Dom2S D, Codes K) {
+  constexpr int NV = 2 * NCH, NW = kCoarseThreads / 32;  // channels per sweep (2 codes)
+  extern __shared__ __align__(16) double s_scan[];        // [S][NV] scan values by point
+  int32_t *s_blk = reinterpret_cast<int32_t *>(s_scan + S * NV);  // [S] blocks by point
+  __shared__ double s_wtot[NV][NW];
   const int64_t g = blockIdx.x, P = D.P, lo = g * S;
   const int Sg = (int)(lo + S < D.n ? S : D.n - lo);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nq = K.n * NCH;
-  int32_t blk[kCoarsePer];
-  double val[kCoarsePer][NQ];
+  const int nc = K.n > 1 ? 2 : 1, nq = nc * NCH;
 #pragma unroll
   for (int j = 0; j < kCoarsePer; ++j) {
     const int k = tid * kCoarsePer + j;
-    const bool live = k < Sg;
-    blk[j] = live ? (D.gpos_c[lo + k].y >> LS) : (int32_t)P;
-    PtXW r = live ? D.gxw_c[lo + k] : PtXW{0.0, 0.0, 0.0, 0.0};
-    if (!live) r.w0 = r.w1 = 0.0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      if (c >= K.n) break;
-      const double e = K.kde ? exp(code_s(K.kp[c], r.x0, r.x1)) : 1.0;
-#pragma unroll
-      for (int v = 0; v < NCH; ++v)
-        val[j][c * NCH + v] = (v ? r.w1 : r.w0) * e * (K.kde ? chan_sign(K.kp[c], v) : 1.0);
-    }
+    s_blk[k] = k < Sg ? (D.gpos_c[lo + k].y >> LS) : (int32_t)P;
   }
-  s_first[tid] = blk[0];
-  s_last[tid + 1] = blk[kCoarsePer - 1];
-  if (tid == 0) {
-    s_last[0] = -1;
-    s_first[kCoarseThreads] = (int32_t)P;
-  }
-  // inclusive scans over the points: ascending for f0 = 0 codes, descending for f0 = 1
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    if (q >= nq) break;
-    const bool rev = (q / NCH) & 1;
-    double run = 0.0;
-    if (!rev) {
-#pragma unroll
-      for (int j = 0; j < kCoarsePer; ++j) val[j][q] = run = run + val[j][q];
-    } else {
-#pragma unroll
-      for (int j = kCoarsePer - 1; j >= 0; --j) val[j][q] = run = run + val[j][q];
-    }
-    double x = run;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double y = rev ? __shfl_down_sync(0xffffffffu, x, o) : __shfl_up_sync(0xffffffffu, x, o);
-      if (rev ? lane + o < 32 : lane >= o) x += y;
-    }
-    if (lane == (rev ? 0 : 31)) s_wtot[q][warp] = x;
-    double excl = rev ? __shfl_down_sync(0xffffffffu, x, 1) : __shfl_up_sync(0xffffffffu, x, 1);
-    if (lane == (rev ? 31 : 0)) excl = 0.0;  // the lanes before (after) this one
-#pragma unroll
-    for (int j = 0; j < kCoarsePer; ++j) val[j][q] += excl;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    if (q >= nq) break;
-    const bool rev = (q / NCH) & 1;
-    double carry = 0.0;
-    if (!rev) {
-      for (int w = 0; w < warp; ++w) carry += s_wtot[q][w];
-    } else {
-      for (int w = NW - 1; w > warp; --w) carry += s_wtot[q][w];
-    }
-#pragma unroll
-    for (int j = 0; j < kCoarsePer; ++j) val[j][q] += carry;
-  }
-  // run stores
-  const int32_t nxt = s_first[tid + 1], prv = s_last[tid];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    if (c >= K.n) break;
-    const int f0 = c & 1, f1 = (c >> 1) & 1;
-    double *row = D.G + ((int64_t)c * P + (f1 ? P - 1 - g : g)) * P * NCH;
+  for (int sweep = 0; sweep < (K.n > 1 ? 2 : 1); ++sweep) {
+    const bool rev = sweep != 0;
+    double val[kCoarsePer][NV];
 #pragma unroll
     for (int j = 0; j < kCoarsePer; ++j) {
       const int k = tid * kCoarsePer + j;
-      if (k >= Sg) break;
-      if (!f0) {  // blocks [blk(k), blk(k + 1)) hold the prefix through point k
-        const int32_t bnext = j + 1 < kCoarsePer ? blk[j + 1] : nxt;
-        for (int32_t bb = blk[j]; bb < bnext; ++bb)
+      const bool live = k < Sg;
+      PtXW r = live ? D.gxw_c[lo + k] : PtXW{0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-          for (int v = 0; v < NCH; ++v) row[(int64_t)bb * NCH + v] = val[j][c * NCH + v];
-        if (k == 0)
-          for (int32_t bb = 0; bb < blk[0]; ++bb)
+      for (int ci = 0; ci < 2; ++ci) {
+        if (ci >= nc) break;
+        const int c = sweep + 2 * ci;
+        const double e = (K.kde && live) ? exp(code_s(K.kp[c], r.x0, r.x1)) : (live ? 1.0 : 0.0);
 #pragma unroll
-            for (int v = 0; v < NCH; ++v) row[(int64_t)bb * NCH + v] = 0.0;
-      } else {    // blocks (blk(k - 1), blk(k)] hold the suffix from point k, stored flipped
-        const int32_t bprev = j > 0 ? blk[j - 1] : prv;
-        for (int32_t bb = bprev + 1; bb <= blk[j]; ++bb)
-#pragma unroll
-          for (int v = 0; v < NCH; ++v) row[(P - 1 - bb) * NCH + v] = val[j][c * NCH + v];
-        if (k == Sg - 1)
-          for (int32_t bb = blk[j] + 1; bb < (int32_t)P; ++bb)
-#pragma unroll
-            for (int v = 0; v < NCH; ++v) row[(P - 1 - bb) * NCH + v] = 0.0;
+        for (int v = 0; v < NCH; ++v)
+          val[j][ci * NCH + v] = (v ? r.w1 : r.w0) * e * (K.kde ? chan_sign(K.kp[c], v) : 1.0);
       }
     }
+    // inclusive scans over the points: ascending (sweep 0) or descending (sweep 1)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      if (q >= nq) break;
+      double run = 0.0;
+      if (!rev) {
+#pragma unroll
+        for (int j = 0; j < kCoarsePer; ++j) val[j][q] = run = run + val[j][q];
+      } else {
+#pragma unroll
+        for (int j = kCoarsePer - 1; j >= 0; --j) val[j][q] = run = run + val[j][q];
+      }
+      double x = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = rev ? __shfl_down_sync(0xffffffffu, x, o) : __shfl_up_sync(0xffffffffu, x, o);
+        if (rev ? lane + o < 32 : lane >= o) x += y;
+      }
+      if (lane == (rev ? 0 : 31)) s_wtot[q][warp] = x;
+      double excl = rev ? __shfl_down_sync(0xffffffffu, x, 1) : __shfl_up_sync(0xffffffffu, x, 1);
+      if (lane == (rev ? 31 : 0)) excl = 0.0;  // the lanes before (after) this one
+#pragma unroll
+      for (int j = 0; j < kCoarsePer; ++j) val[j][q] += excl;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      if (q >= nq) break;
+      double carry = 0.0;
+      if (!rev) {
+        for (int w = 0; w < warp; ++w) carry += s_wtot[q][w];
+      } else {
+        for (int w = NW - 1; w > warp; --w) carry += s_wtot[q][w];
+      }
+#pragma unroll
+      for (int j = 0; j < kCoarsePer; ++j)
+        s_scan[(tid * kCoarsePer + j) * NV + q] = val[j][q] + carry;
+    }
+    __syncthreads();
+    // output pass: block b takes the prefix through its last point (the suffix from its first)
+    double *rows[2];
+#pragma unroll
+    for (int ci = 0; ci < 2; ++ci) {
+      const int c = sweep + 2 * ci;
+      const int f1 = (c >> 1) & 1;
+      rows[ci] = D.G + ((int64_t)c * P + (f1 ? P - 1 - g : g)) * P * NCH;
+    }
+    const int32_t Pi = (int32_t)P;
+    for (int32_t b = tid; b < Pi; b += kCoarseThreads) {
+      // number of points with block < thr (dead points hold block P): sweep 0 counts blocks
+      // <= b, sweep 1 blocks < b; a fixed-step search over the S entries
+      const int32_t thr = rev ? b : b + 1;
+      int a = 0;
+#pragma unroll
+      for (int step = S / 2; step > 0; step >>= 1)
+        if (s_blk[a + step - 1] < thr) a += step;
+      if (s_blk[a] < thr) ++a;  // a in [0, S]; entries past Sg never count (thr <= P)
+      const int idx = rev ? a : a - 1;
+      const bool has = rev ? idx < Sg : idx >= 0;
+      const int64_t bq = rev ? P - 1 - b : b;
+#pragma unroll
+      for (int ci = 0; ci < 2; ++ci) {
+        if (ci >= nc) break;
+#pragma unroll
+        for (int v = 0; v < NCH; ++v)
+          rows[ci][bq * NCH + v] = has ? s_scan[idx * NV + ci * NCH + v] : 0.0;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -1454,8 +1455,14 @@ int self_dom2d(const double *x, WPtr w, int64_t n, int nw, int kde, const double
   }
   {
     FCG_PROF("pts_coarse_hist", st);
-    if (nw == 1) coarse_rows_codes<1><<<(unsigned)P, kCoarseThreads, 0, st>>>(D, K);
-    else coarse_rows_codes<2><<<(unsigned)P, kCoarseThreads, 0, st>>>(D, K);
+    const size_t csm = (size_t)S * 2 * nw * sizeof(double) + (size_t)S * sizeof(int32_t);
+    if (nw == 1) {
+      FCG_CUDA_TRY(cudaFuncSetAttribute(coarse_rows_codes<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+      coarse_rows_codes<1><<<(unsigned)P, kCoarseThreads, csm, st>>>(D, K);
+    } else {
+      FCG_CUDA_TRY(cudaFuncSetAttribute(coarse_rows_codes<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+      coarse_rows_codes<2><<<(unsigned)P, kCoarseThreads, csm, st>>>(D, K);
+    }
     FCG_LAUNCH_CHECK();
   }
   {  // the block axis is prefixed by the row kernel; the chunk axis in one scan pass
