@@ -1031,14 +1031,16 @@ __global__ void __launch_bounds__(kSolverThreads) level2_codes(Dom2S D, Codes K)
         acc[ch] = (occ && u > 0 && v > 0) ? s_sub[(ch * NSUB + (u - 1)) * NSUB + (v - 1)] : 0.0;
       const int xe = occ ? x : 0;  // candidates c < xe
       const int cend = (int)__reduce_max_sync(0xffffffffu, (unsigned)xe);
+      const int xe_t[4] = {xe, xe - 1, xe - 2, xe - 3};  // c0 + t < xe  <=>  c0 < xe - t
       for (int c0 = u << SUBL; c0 < cend; c0 += 4) {
-        const short4 y4 = *reinterpret_cast<const short4 *>(s_yofx + c0);
-        const int yc[4] = {y4.x, y4.y, y4.z, y4.w};
+        const uint2 y4 = *reinterpret_cast<const uint2 *>(s_yofx + c0);  // 4 ranks (< 2^15)
+        const int yc[4] = {(int)(y4.x & 0xffffu), (int)(y4.x >> 16), (int)(y4.y & 0xffffu),
+                           (int)(y4.y >> 16)};
         PT pc[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) pc[t] = s_p[c0 + t];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) PsiT<NCH>::add(acc, pc[t], c0 + t < xe && yc[t] < qy);
+        for (int t = 0; t < 4; ++t) PsiT<NCH>::add(acc, pc[t], c0 < xe_t[t] && yc[t] < qy);
       }
       if (occ) {
         const double z = K.kde ? s_z[k] : 1.0;
@@ -1062,15 +1064,20 @@ __global__ void __launch_bounds__(kSolverThreads) level2_codes(Dom2S D, Codes K)
       double acc[NCH];
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) acc[ch] = 0.0;
+      // cbeg <= c0 + t < qy as one unsigned compare of c0 against per-t bounds:
+      // (unsigned)(c0 - (cbeg - t)) < (unsigned)(qy - cbeg)   (idle lanes: cbeg = S, qy = 0)
+      const int lo_t[4] = {cbeg, cbeg - 1, cbeg - 2, cbeg - 3};
+      const unsigned span = (unsigned)(qy - cbeg);
       for (int c0 = cstart; c0 < cend; c0 += 4) {
-        const short4 x4 = *reinterpret_cast<const short4 *>(s_xofy + c0);
-        const int xc[4] = {x4.x, x4.y, x4.z, x4.w};
+        const uint2 x4 = *reinterpret_cast<const uint2 *>(s_xofy + c0);  // 4 slots (< 2^15)
+        const int xc[4] = {(int)(x4.x & 0xffffu), (int)(x4.x >> 16), (int)(x4.y & 0xffffu),
+                           (int)(x4.y >> 16)};
         PT pc[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) pc[t] = s_p[xc[t]];
 #pragma unroll
         for (int t = 0; t < 4; ++t)
-          PsiT<NCH>::add(acc, pc[t], c0 + t >= cbeg && c0 + t < qy && xc[t] < xfull);
+          PsiT<NCH>::add(acc, pc[t], (unsigned)(c0 - lo_t[t]) < span && xc[t] < xfull);
       }
       if (ok) {
         const double z = K.kde ? s_z[k] : 1.0;
