@@ -20,6 +20,7 @@
 //  * rank-space dominance, 3 <= d <= 6 (points_nd.cuh): a coarse G^d grid of rank chunks for the
 //    far field and one slab phase per dimension for the sources sharing a chunk with the query.
 //  * direct O(n^2) tiles (d >= 7, or fewer than 8192 points).
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -1109,6 +1110,338 @@ __global__ void __launch_bounds__(kSolverThreads) level2_codes(Dom2S D, Codes K)
   }
 }
 
+// ---- level 2, direct form ----------------------------------------------------------------
+// The same chunk / block problem in one unflipped frame.  Sources sit in shared memory by slot
+// (the slot dimension's local position) with their rank (order along the other dimension), the
+// table T[c] = exp(s_c(x)) of the four sign codes and their weights.  A query with slot x and
+// rank thresholds (qlo, qhi) -- dominated below: ranks < qlo, above: ranks >= qhi; its own rank
+// (chunks) or the ranks outside its own chunk (blocks) -- splits every code's sum into
+//   mid field: the 64 x 64 grid of (32 slots) x (32 ranks) cells, cell sums of psi_code
+//              scattered with shared atomics, prefixed along each axis in the code's direction,
+//              one lookup at the cell diagonal to the query's (slot cell, threshold rank cell);
+//   near field: the sources of the query's slot cell (pass A) and of the threshold's rank cell
+//              outside that slot cell (pass B), visited ONCE for all codes: the pair's quadrant
+//              picks the code c, and z_c(t) psi_c(s) = w_s T_s[c] T_t[3 - c] is formed directly
+//              (T[3 - c] = exp(-s_c): the opposite code), so nothing is masked out four times.
+// The plain ECDF (one code, psi = w) keeps only the pairs of quadrant 0.
+template <bool CHUNK, int NCH>
+__global__ void __launch_bounds__(kSolverThreads) level2_direct(Dom2S D, Codes K) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int RST = NSUB + 1;  // padded row: lookups of one slot cell spread over the banks
+  double *s_sub = reinterpret_cast<double *>(smem);               // [NCH][NSUB][RST]
+  double *s_tab = s_sub + NCH * NSUB * RST;                       // [S][4] by slot (16-byte aligned)
+  double *s_w = s_tab + S * 4;                                    // [S][NCH] by slot
+  double *s_tot = s_w + S * NCH;                                  // [kSolverThreads]
+  double *s_sgn = s_tot + kSolverThreads;                         // [4][2] channel signs by code
+  int32_t *s_key = reinterpret_cast<int32_t *>(s_sgn + 8);        // [S] rank-dimension key by rank
+  int16_t *s_yofx = reinterpret_cast<int16_t *>(s_key + S);       // [S] rank by slot
+  int16_t *s_xofy = s_yofx + S;                                   // [S] slot by rank
+  int16_t *s_qlo = s_xofy + S;                                    // [S] thresholds by slot
+  int16_t *s_qhi = s_qlo + S;
+  double *out = CHUNK ? D.accc : D.accb;
+  const int64_t g = blockIdx.x + (CHUNK ? D.c_lo : 0);  // unflipped chunk / block
+  const int64_t lo = g * S;
+  const int Sg = (int)(lo + S < D.n ? S : D.n - lo);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool kde = K.kde != 0;
+  const bool all_owned = CHUNK || (D.c_lo == 0 && D.c_hi == D.P);
+  const int2 *gpos = CHUNK ? D.gpos_c : D.gpos_b;
+  const PtXW *gxw = CHUNK ? D.gxw_c : D.gxw_b;
+  bool has_sign = false;
+  for (int v = 0; v < NCH; ++v) has_sign = has_sign || K.kp[0].smask[v] != 0u;
+  // empty slots / ranks: no rank, zero weight and table, key past every threshold
+  for (int i = tid; i < S / 2; i += kSolverThreads)
+    reinterpret_cast<uint32_t *>(s_yofx)[i] = (uint32_t)(uint16_t)kEmptyY * 0x10001u;
+  if (Sg < S) {
+    for (int i = tid; i < S * 4; i += kSolverThreads) s_tab[i] = 0.0;
+    for (int i = tid; i < S * NCH; i += kSolverThreads) s_w[i] = 0.0;
+    for (int i = Sg + tid; i < S; i += kSolverThreads) {
+      s_xofy[i] = 0;
+      s_key[i] = 0x7fffffff;
+    }
+  }
+  if (tid < 8) s_sgn[tid] = (K.kde && (tid & 1) < NCH) ? chan_sign(K.kp[tid >> 1], tid & 1) : 1.0;
+  __syncthreads();
+  int32_t key_u[kL2Per];
+  int slot[kL2Per];
+  double accA[kL2Per][NCH], accB[kL2Per][NCH];
+#pragma unroll
+  for (int j = 0; j < kL2Per; ++j) {
+    const int k = tid + j * kSolverThreads;
+    const bool live = k < Sg;
+    const int2 pp = live ? gpos[lo + k] : make_int2((int32_t)lo, 0);
+    key_u[j] = pp.y;
+    slot[j] = pp.x - (int32_t)lo;
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) accA[j][ch] = accB[j][ch] = 0.0;
+    if (!live) continue;
+    const PtXW r = gxw[lo + k];
+    double4 t4 = make_double4(1.0, 1.0, 1.0, 1.0);
+    if (kde) {
+      t4.x = exp(code_s(K.kp[0], r.x0, r.x1));
+      t4.y = exp(code_s(K.kp[1], r.x0, r.x1));
+      t4.z = exp(code_s(K.kp[2], r.x0, r.x1));
+      t4.w = exp(code_s(K.kp[3], r.x0, r.x1));
+    }
+    s_xofy[k] = (int16_t)slot[j];
+    s_yofx[slot[j]] = (int16_t)k;
+    s_key[k] = pp.y;
+    reinterpret_cast<double4 *>(s_tab)[slot[j]] = t4;
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) s_w[slot[j] * NCH + ch] = ch ? r.w1 : r.w0;
+  }
+  __syncthreads();
+  // thresholds of this thread's slots (pass A / lookup order)
+  int qloA[kL2Per], qhiA[kL2Per];
+  bool occA[kL2Per];
+#pragma unroll
+  for (int j = 0; j < kL2Per; ++j) {
+    const int x = tid + j * kSolverThreads;
+    const int y = s_yofx[x];
+    occA[j] = y != kEmptyY;
+    qloA[j] = qhiA[j] = 0;
+    if (!occA[j]) continue;
+    if (CHUNK) {
+      qloA[j] = y;
+      qhiA[j] = y + 1;
+    } else {
+      const int32_t key = s_key[y];
+      const int64_t c = key >> LS;
+      occA[j] = all_owned || (c >= D.c_lo && c < D.c_hi);
+      const int64_t t_lo = c * S, t_hi = (c + 1) * S;  // ranks with key < t: fixed-step search
+      int a = 0, b = 0;
+#pragma unroll
+      for (int step = S / 2; step > 0; step >>= 1) {
+        if ((int64_t)s_key[a + step - 1] < t_lo) a += step;
+        if ((int64_t)s_key[b + step - 1] < t_hi) b += step;
+      }
+      if ((int64_t)s_key[a] < t_lo) ++a;
+      if ((int64_t)s_key[b] < t_hi) ++b;
+      qloA[j] = a;
+      qhiA[j] = b;
+      s_qlo[x] = (int16_t)a;
+      s_qhi[x] = (int16_t)b;
+    }
+  }
+  // ---- mid field, one code at a time ----
+  for (int code = 0; code < K.n; ++code) {
+    const int f0 = code & 1, f1 = (code >> 1) & 1;
+    const int fslot = CHUNK ? f1 : f0, frank = CHUNK ? f0 : f1;
+    __syncthreads();  // the previous code's lookups are done
+    for (int i = tid; i < NCH * NSUB * RST; i += kSolverThreads) s_sub[i] = 0.0;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kL2Per; ++j) {
+      const int k = tid + j * kSolverThreads;
+      if (k >= Sg) continue;
+      const int u = slot[j] >> SUBL, v = k >> SUBL;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch)
+        atomicAdd(&s_sub[(ch * NSUB + v) * RST + u],  // a warp's sources share the rank cell
+                  s_w[slot[j] * NCH + ch] * s_tab[slot[j] * 4 + code] * s_sgn[code * 2 + ch]);
+      if (CHUNK) {
+        // level 1: the code's coarse cell below the query's chunk and block (flipped frame).
+        // The chunk's points run in p0 order, so a warp's reads walk one grid row in order.
+        const int64_t P = D.P, bu = key_u[j] >> LS;
+        const int64_t cc = f1 ? P - 1 - g : g, bb = f0 ? P - 1 - bu : bu;
+        if (cc > 0 && bb > 0) {
+          const double *gv = D.G + (((int64_t)code * P + cc - 1) * P + bb - 1) * NCH;
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) accB[j][ch] += s_tab[slot[j] * 4 + 3 - code] * gv[ch];
+        }
+      }
+    }
+    __syncthreads();
+    // cells are stored [channel][rank cell][slot cell].  Prefix along the slot cells (ascending,
+    // or descending for a reversed slot frame): a warp per (channel, rank cell) row, lanes on
+    // cells l and l + 32
+    for (int row = warp; row < NCH * NSUB; row += kSolverThreads / 32) {
+      double *rp = s_sub + row * RST;
+      double a = rp[lane], b = rp[lane + 32];
+      if (!fslot) {
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double ya = __shfl_up_sync(0xffffffffu, a, o), yb = __shfl_up_sync(0xffffffffu, b, o);
+          if (lane >= o) {
+            a += ya;
+            b += yb;
+          }
+        }
+        b += __shfl_sync(0xffffffffu, a, 31);
+      } else {
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double ya = __shfl_down_sync(0xffffffffu, a, o), yb = __shfl_down_sync(0xffffffffu, b, o);
+          if (lane + o < 32) {
+            a += ya;
+            b += yb;
+          }
+        }
+        a += __shfl_sync(0xffffffffu, b, 0);
+      }
+      rp[lane] = a;
+      rp[lane + 32] = b;
+    }
+    __syncthreads();
+    // prefix along the rank cells: thread (segment sg, column cc), segment totals meet in s_tot
+    {
+      constexpr int NCC = NCH * NSUB, SEGS = kSolverThreads / NCC, RPS = NSUB / SEGS;
+      const int cc = tid % NCC, sg = tid / NCC;
+      const int ch = cc / NSUB, v = cc % NSUB;
+      double *col = s_sub + (ch * NSUB + sg * RPS) * RST + v;
+      double vals[RPS];
+      double run = 0.0;
+#pragma unroll
+      for (int r = 0; r < RPS; ++r) vals[r] = col[r * RST];
+      if (!frank) {
+#pragma unroll
+        for (int r = 0; r < RPS; ++r) vals[r] = run = run + vals[r];
+      } else {
+#pragma unroll
+        for (int r = RPS - 1; r >= 0; --r) vals[r] = run = run + vals[r];
+      }
+      s_tot[sg * NCC + cc] = run;
+      __syncthreads();
+      double carry = 0.0;
+      if (!frank) {
+        for (int t = 0; t < sg; ++t) carry += s_tot[t * NCC + cc];
+      } else {
+        for (int t = SEGS - 1; t > sg; --t) carry += s_tot[t * NCC + cc];
+      }
+#pragma unroll
+      for (int r = 0; r < RPS; ++r) col[r * RST] = vals[r] + carry;
+    }
+    __syncthreads();
+    // lookup by slot
+#pragma unroll
+    for (int j = 0; j < kL2Per; ++j) {
+      if (!occA[j]) continue;
+      const int x = tid + j * kSolverThreads;
+      const int ui = fslot ? (x >> SUBL) + 1 : (x >> SUBL) - 1;
+      const int vi = frank ? (qhiA[j] >> SUBL) + 1 : (qloA[j] >> SUBL) - 1;
+      if (ui < 0 || ui >= NSUB || vi < 0 || vi >= NSUB) continue;
+      const double z = s_tab[x * 4 + (3 - code)];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) accA[j][ch] += z * s_sub[(ch * NSUB + vi) * RST + ui];
+    }
+  }
+  // ---- near field, all codes at once ----
+  // quadrant code of a pair: bit of dimension 0 / 1 set when the source lies above the query
+  auto pair_value = [&](int code2, int xs, const double4 &tq) -> double {
+    if (!kde) return code2 == 0 ? 1.0 : 0.0;
+    // the query's factor is its table entry of the opposite code
+    const double tt = (code2 & 2) ? ((code2 & 1) ? tq.x : tq.y) : ((code2 & 1) ? tq.z : tq.w);
+    return s_tab[xs * 4 + code2] * tt;
+  };
+  // pass A: this thread's slots, the 32 slots of their cell (a warp's slots share the cell)
+#pragma unroll
+  for (int j = 0; j < kL2Per; ++j) {
+    const int x = tid + j * kSolverThreads;
+    const int c0 = (x >> SUBL) << SUBL;
+    const int qlo = qloA[j], qhi = occA[j] ? qhiA[j] : 0x7ffe;  // idle lanes: nothing passes
+    const int qlo_e = occA[j] ? qlo : 0;
+    const double4 tq = reinterpret_cast<const double4 *>(s_tab)[x];
+    double acc[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) acc[ch] = 0.0;
+#pragma unroll 2
+    for (int c = c0; c < c0 + SUB; c += 4) {
+      const uint2 y4 = *reinterpret_cast<const uint2 *>(s_yofx + c);
+      const int yc[4] = {(int)(y4.x & 0xffffu), (int)(y4.x >> 16), (int)(y4.y & 0xffffu),
+                         (int)(y4.y >> 16)};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const bool below = yc[t] < qlo_e, above = yc[t] >= qhi && yc[t] != kEmptyY;
+        const int sb = c + t > x ? 1 : 0, rb = above ? 1 : 0;
+        const int code2 = CHUNK ? (rb | (sb << 1)) : (sb | (rb << 1));
+        double kv = pair_value(code2, c + t, tq);
+        kv = (below || above) ? kv : 0.0;
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+          double wv = s_w[(c + t) * NCH + ch];
+          if (has_sign) wv *= s_sgn[code2 * 2 + ch];
+          acc[ch] = fma(wv, kv, acc[ch]);
+        }
+      }
+    }
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) accA[j][ch] += acc[ch];
+  }
+  // pass B: this thread's ranks (its own sources), the threshold cells' ranks outside the
+  // query's slot cell
+#pragma unroll
+  for (int j = 0; j < kL2Per; ++j) {
+    const int k = tid + j * kSolverThreads;
+    const int x = slot[j];
+    bool ok = k < Sg;
+    int qlo = k, qhi = k + 1;
+    if (!CHUNK && ok) {
+      const int64_t cu = key_u[j] >> LS;
+      ok = all_owned || (cu >= D.c_lo && cu < D.c_hi);
+      qlo = s_qlo[x];
+      qhi = s_qhi[x];
+    }
+    const int lo_s = (qlo >> SUBL) << SUBL;
+    int hi_e = ((qhi >> SUBL) << SUBL) + SUB;
+    hi_e = hi_e > Sg ? Sg : hi_e;
+    const unsigned span_lo = ok ? (unsigned)(qlo - lo_s) : 0u;
+    const unsigned span_hi = (ok && hi_e > qhi) ? (unsigned)(hi_e - qhi) : 0u;
+    const int wmin = (int)__reduce_min_sync(0xffffffffu, ok ? (unsigned)lo_s : (unsigned)S);
+    const int wmax = (int)__reduce_max_sync(0xffffffffu, ok ? (unsigned)hi_e : 0u);
+    const int xcell = x >> SUBL;
+    const double4 tq = reinterpret_cast<const double4 *>(s_tab)[x];
+    double acc[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) acc[ch] = 0.0;
+    for (int r0 = wmin; r0 < wmax; r0 += 4) {
+      const uint2 x4 = *reinterpret_cast<const uint2 *>(s_xofy + r0);
+      const int xr[4] = {(int)(x4.x & 0xffffu), (int)(x4.x >> 16), (int)(x4.y & 0xffffu),
+                         (int)(x4.y >> 16)};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const bool below = (unsigned)(r0 + t - lo_s) < span_lo;
+        const bool above = (unsigned)(r0 + t - qhi) < span_hi;
+        const bool take = (below || above) && (xr[t] >> SUBL) != xcell;
+        const int sb = xr[t] > x ? 1 : 0, rb = above ? 1 : 0;
+        const int code2 = CHUNK ? (rb | (sb << 1)) : (sb | (rb << 1));
+        double kv = pair_value(code2, xr[t], tq);
+        kv = take ? kv : 0.0;
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+          double wv = s_w[xr[t] * NCH + ch];
+          if (has_sign) wv *= s_sgn[code2 * 2 + ch];
+          acc[ch] = fma(wv, kv, acc[ch]);
+        }
+      }
+    }
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) accB[j][ch] += acc[ch];
+  }
+  // the two halves of every query meet in shared memory by slot; coalesced store in slot order
+  __syncthreads();
+  double *s_acc = s_sub;  // [S][NCH] by slot
+#pragma unroll
+  for (int j = 0; j < kL2Per; ++j) {
+    const int k = tid + j * kSolverThreads;
+    if (k >= Sg) continue;
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) s_acc[slot[j] * NCH + ch] = accB[j][ch];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kL2Per; ++j) {
+    const int uu = tid + j * kSolverThreads;
+    if (uu >= Sg) continue;
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) out[(lo + uu) * NCH + ch] = accA[j][ch] + s_acc[uu * NCH + ch];
+  }
+}
+
+size_t level2_direct_smem(int nch) {
+  return (size_t)nch * NSUB * (NSUB + 1) * 8 + (size_t)S * 32 + (size_t)nch * S * 8 +
+         (size_t)kSolverThreads * 8 + 64 + (size_t)S * 4 + (size_t)S * 2 * 4;
+}
+
 size_t level2_self_smem(int nch) {
   return (size_t)nch * NSUB * NSUB * 8 + (size_t)nch * S * 8 + (size_t)kSolverThreads * 8 +
          (size_t)S * 8 + (size_t)S * 4 + (size_t)S * 2 * 5;
@@ -1436,8 +1769,20 @@ int self_dom2d(const double *x, WPtr w, int64_t n, int nw, int kde, const double
   D.c_lo = P * shard / nshards;
   D.c_hi = P * (shard + 1) / nshards;
   const unsigned nchunk = (unsigned)(D.c_hi - D.c_lo);
-  const size_t sm = level2_self_smem(nw);
-  if (nw == 1) {
+  static const bool direct = [] {  // FCG_LEVEL2=codes: the per-code masked passes (A/B runs)
+    const char *e = getenv("FCG_LEVEL2");
+    return !(e && std::string(e) == "codes");
+  }();
+  const size_t sm = direct ? level2_direct_smem(nw) : level2_self_smem(nw);
+  if (direct) {
+    if (nw == 1) {
+      FCG_CUDA_TRY(cudaFuncSetAttribute(level2_direct<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      FCG_CUDA_TRY(cudaFuncSetAttribute(level2_direct<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    } else {
+      FCG_CUDA_TRY(cudaFuncSetAttribute(level2_direct<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      FCG_CUDA_TRY(cudaFuncSetAttribute(level2_direct<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    }
+  } else if (nw == 1) {
     FCG_CUDA_TRY(cudaFuncSetAttribute(level2_codes<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     FCG_CUDA_TRY(cudaFuncSetAttribute(level2_codes<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   } else {
@@ -1486,15 +1831,27 @@ int self_dom2d(const double *x, WPtr w, int64_t n, int nw, int kde, const double
   {
     FCG_PROF("pts_level2_chunk", st);
     if (nchunk > 0) {
-      if (nw == 1) level2_codes<true, 1><<<nchunk, kSolverThreads, sm, st>>>(D, K);
-      else level2_codes<true, 2><<<nchunk, kSolverThreads, sm, st>>>(D, K);
+      if (direct) {
+        if (nw == 1) level2_direct<true, 1><<<nchunk, kSolverThreads, sm, st>>>(D, K);
+        else level2_direct<true, 2><<<nchunk, kSolverThreads, sm, st>>>(D, K);
+      } else if (nw == 1) {
+        level2_codes<true, 1><<<nchunk, kSolverThreads, sm, st>>>(D, K);
+      } else {
+        level2_codes<true, 2><<<nchunk, kSolverThreads, sm, st>>>(D, K);
+      }
     }
     FCG_LAUNCH_CHECK();
   }
   {
     FCG_PROF("pts_level2_block", st);
-    if (nw == 1) level2_codes<false, 1><<<(unsigned)P, kSolverThreads, sm, st>>>(D, K);
-    else level2_codes<false, 2><<<(unsigned)P, kSolverThreads, sm, st>>>(D, K);
+    if (direct) {
+      if (nw == 1) level2_direct<false, 1><<<(unsigned)P, kSolverThreads, sm, st>>>(D, K);
+      else level2_direct<false, 2><<<(unsigned)P, kSolverThreads, sm, st>>>(D, K);
+    } else if (nw == 1) {
+      level2_codes<false, 1><<<(unsigned)P, kSolverThreads, sm, st>>>(D, K);
+    } else {
+      level2_codes<false, 2><<<(unsigned)P, kSolverThreads, sm, st>>>(D, K);
+    }
     FCG_LAUNCH_CHECK();
   }
   FCG_PROF("pts_finish", st);
