@@ -1119,8 +1119,9 @@ __global__ void __launch_bounds__(kSolverThreads) level2_codes(Dom2S D, Codes K)
 //   mid field: the 64 x 64 grid of (32 slots) x (32 ranks) cells, cell sums of psi_code
 //              scattered with shared atomics, prefixed along each axis in the code's direction,
 //              one lookup at the cell diagonal to the query's (slot cell, threshold rank cell);
-//   near field: the sources of the query's slot cell (pass A) and of the threshold's rank cell
-//              outside that slot cell (pass B), visited ONCE for all codes: the pair's quadrant
+//   near field: the sources of the query's slot cell (pass A) and of the thresholds' rank cells
+//              (below: the cell of qlo; above: the rest of the cell of qhi - 1) outside that slot
+//              cell (pass B), visited ONCE for all codes: the pair's quadrant
 //              picks the code c, and z_c(t) psi_c(s) = w_s T_s[c] T_t[3 - c] is formed directly
 //              (T[3 - c] = exp(-s_c): the opposite code), so nothing is masked out four times.
 // The plain ECDF (one code, psi = w) keeps only the pairs of quadrant 0.
@@ -1208,15 +1209,18 @@ __global__ void __launch_bounds__(kSolverThreads) level2_direct(Dom2S D, Codes K
       const int32_t key = s_key[y];
       const int64_t c = key >> LS;
       occA[j] = all_owned || (c >= D.c_lo && c < D.c_hi);
-      const int64_t t_lo = c * S, t_hi = (c + 1) * S;  // ranks with key < t: fixed-step search
+      // ranks with key < t: fixed-step searches (keys < 2^31 - 1, so a clamped bound still
+      // counts every live key of the last chunk; empty ranks hold 2^31 - 1)
+      const int32_t t_lo = (int32_t)(c * S);
+      const int32_t t_hi = (c + 1) * S > 0x7fffffff ? 0x7fffffff : (int32_t)((c + 1) * S);
       int a = 0, b = 0;
 #pragma unroll
       for (int step = S / 2; step > 0; step >>= 1) {
-        if ((int64_t)s_key[a + step - 1] < t_lo) a += step;
-        if ((int64_t)s_key[b + step - 1] < t_hi) b += step;
+        if (s_key[a + step - 1] < t_lo) a += step;
+        if (s_key[b + step - 1] < t_hi) b += step;
       }
-      if ((int64_t)s_key[a] < t_lo) ++a;
-      if ((int64_t)s_key[b] < t_hi) ++b;
+      if (s_key[a] < t_lo) ++a;
+      if (s_key[b] < t_hi) ++b;
       qloA[j] = a;
       qhiA[j] = b;
       s_qlo[x] = (int16_t)a;
@@ -1318,7 +1322,8 @@ __global__ void __launch_bounds__(kSolverThreads) level2_direct(Dom2S D, Codes K
       if (!occA[j]) continue;
       const int x = tid + j * kSolverThreads;
       const int ui = fslot ? (x >> SUBL) + 1 : (x >> SUBL) - 1;
-      const int vi = frank ? (qhiA[j] >> SUBL) + 1 : (qloA[j] >> SUBL) - 1;
+      // above: the cells past the one holding the last excluded rank qhi - 1
+      const int vi = frank ? ((qhiA[j] - 1) >> SUBL) + 1 : (qloA[j] >> SUBL) - 1;
       if (ui < 0 || ui >= NSUB || vi < 0 || vi >= NSUB) continue;
       const double z = s_tab[x * 4 + (3 - code)];
 #pragma unroll
@@ -1382,7 +1387,7 @@ __global__ void __launch_bounds__(kSolverThreads) level2_direct(Dom2S D, Codes K
       qhi = s_qhi[x];
     }
     const int lo_s = (qlo >> SUBL) << SUBL;
-    int hi_e = ((qhi >> SUBL) << SUBL) + SUB;
+    int hi_e = (((qhi - 1) >> SUBL) << SUBL) + SUB;  // end of the cell holding rank qhi - 1
     hi_e = hi_e > Sg ? Sg : hi_e;
     const unsigned span_lo = ok ? (unsigned)(qlo - lo_s) : 0u;
     const unsigned span_hi = (ok && hi_e > qhi) ? (unsigned)(hi_e - qhi) : 0u;
