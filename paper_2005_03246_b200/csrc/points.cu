@@ -1192,6 +1192,36 @@ __global__ void __launch_bounds__(kSolverThreads) level2_direct(Dom2S D, Codes K
     for (int ch = 0; ch < NCH; ++ch) s_w[slot[j] * NCH + ch] = ch ? r.w1 : r.w0;
   }
   __syncthreads();
+  if (!CHUNK) {
+    // block thresholds by rank: the ranks of the query's own chunk [qlo, qhi) are a run around
+    // it (a block holds ~S / P points of a chunk), found by walking the neighbours; a long run
+    // (clustered data) falls back to fixed-step searches.  Keys < 2^31 - 1, so a clamped bound
+    // still counts every live key of the last chunk; empty ranks hold 2^31 - 1.
+#pragma unroll
+    for (int j = 0; j < kL2Per; ++j) {
+      const int y = tid + j * kSolverThreads;
+      if (y >= Sg) continue;
+      const int64_t c = key_u[j] >> LS;
+      const int32_t t_lo = (int32_t)(c * S);
+      const int32_t t_hi = (c + 1) * S > 0x7fffffff ? 0x7fffffff : (int32_t)((c + 1) * S);
+      int a = y, b = y + 1, steps = 0;
+      while (a > 0 && s_key[a - 1] >= t_lo && steps < 8) --a, ++steps;
+      while (b < Sg && s_key[b] < t_hi && steps < 16) ++b, ++steps;
+      if (steps >= 8) {
+        a = b = 0;
+#pragma unroll
+        for (int step = S / 2; step > 0; step >>= 1) {
+          if (s_key[a + step - 1] < t_lo) a += step;
+          if (s_key[b + step - 1] < t_hi) b += step;
+        }
+        if (s_key[a] < t_lo) ++a;
+        if (s_key[b] < t_hi) ++b;
+      }
+      s_qlo[slot[j]] = (int16_t)a;
+      s_qhi[slot[j]] = (int16_t)b;
+    }
+    __syncthreads();
+  }
   // thresholds of this thread's slots (pass A / lookup order)
   int qloA[kL2Per], qhiA[kL2Per];
   bool occA[kL2Per];
@@ -1206,26 +1236,22 @@ __global__ void __launch_bounds__(kSolverThreads) level2_direct(Dom2S D, Codes K
       qloA[j] = y;
       qhiA[j] = y + 1;
     } else {
-      const int32_t key = s_key[y];
-      const int64_t c = key >> LS;
+      const int64_t c = s_key[y] >> LS;
       occA[j] = all_owned || (c >= D.c_lo && c < D.c_hi);
-      // ranks with key < t: fixed-step searches (keys < 2^31 - 1, so a clamped bound still
-      // counts every live key of the last chunk; empty ranks hold 2^31 - 1)
-      const int32_t t_lo = (int32_t)(c * S);
-      const int32_t t_hi = (c + 1) * S > 0x7fffffff ? 0x7fffffff : (int32_t)((c + 1) * S);
-      int a = 0, b = 0;
-#pragma unroll
-      for (int step = S / 2; step > 0; step >>= 1) {
-        if (s_key[a + step - 1] < t_lo) a += step;
-        if (s_key[b + step - 1] < t_hi) b += step;
-      }
-      if (s_key[a] < t_lo) ++a;
-      if (s_key[b] < t_hi) ++b;
-      qloA[j] = a;
-      qhiA[j] = b;
-      s_qlo[x] = (int16_t)a;
-      s_qhi[x] = (int16_t)b;
+      qloA[j] = s_qlo[x];
+      qhiA[j] = s_qhi[x];
     }
+  }
+  // cell sums without atomics: a warp's 32 sources are one rank cell, so the cell row is the
+  // warp's alone; lanes whose sources share a slot cell are grouped once (match.any), the
+  // group's lowest lane stores the group's sum
+  unsigned grp[kL2Per];
+  int gmax[kL2Per];
+#pragma unroll
+  for (int j = 0; j < kL2Per; ++j) {
+    const int k = tid + j * kSolverThreads;
+    grp[j] = __match_any_sync(0xffffffffu, k < Sg ? (slot[j] >> SUBL) : NSUB + lane);
+    gmax[j] = (int)__reduce_max_sync(0xffffffffu, (unsigned)__popc(grp[j]));
   }
   // ---- mid field, one code at a time ----
   for (int code = 0; code < K.n; ++code) {
@@ -1237,12 +1263,32 @@ __global__ void __launch_bounds__(kSolverThreads) level2_direct(Dom2S D, Codes K
 #pragma unroll
     for (int j = 0; j < kL2Per; ++j) {
       const int k = tid + j * kSolverThreads;
-      if (k >= Sg) continue;
+      const bool live = k < Sg;
       const int u = slot[j] >> SUBL, v = k >> SUBL;
+      double psi[NCH];
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch)
-        atomicAdd(&s_sub[(ch * NSUB + v) * RST + u],  // a warp's sources share the rank cell
-                  s_w[slot[j] * NCH + ch] * s_tab[slot[j] * 4 + code] * s_sgn[code * 2 + ch]);
+        psi[ch] = live ? s_w[slot[j] * NCH + ch] * s_tab[slot[j] * 4 + code] * s_sgn[code * 2 + ch]
+                       : 0.0;
+      double tot[NCH];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) tot[ch] = psi[ch];
+      unsigned rem = grp[j] & ~(1u << lane);
+      for (int it = 1; it < gmax[j]; ++it) {  // warp-uniform trip count
+        const int src = rem ? __ffs(rem) - 1 : lane;
+        rem &= rem - 1;
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+          const double o = __shfl_sync(0xffffffffu, psi[ch], src);
+          // partners are added in lane order by every member; only the sum's owner stores it
+          if (src != lane) tot[ch] += o;
+        }
+      }
+      if (!live) continue;
+      if (lane == __ffs(grp[j]) - 1) {
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) s_sub[(ch * NSUB + v) * RST + u] = tot[ch];
+      }
       if (CHUNK) {
         // level 1: the code's coarse cell below the query's chunk and block (flipped frame).
         // The chunk's points run in p0 order, so a warp's reads walk one grid row in order.
