@@ -1258,13 +1258,18 @@ __global__ void __launch_bounds__(kSolverThreads) level2_direct(Dom2S D, Codes K
     const int f0 = code & 1, f1 = (code >> 1) & 1;
     const int fslot = CHUNK ? f1 : f0, frank = CHUNK ? f0 : f1;
     __syncthreads();  // the previous code's lookups are done
-    for (int i = tid; i < NCH * NSUB * RST; i += kSolverThreads) s_sub[i] = 0.0;
-    __syncthreads();
 #pragma unroll
     for (int j = 0; j < kL2Per; ++j) {
       const int k = tid + j * kSolverThreads;
       const bool live = k < Sg;
       const int u = slot[j] >> SUBL, v = k >> SUBL;
+      // the warp's rank-cell row starts from zero (every rank cell has its warp, live or not)
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        s_sub[(ch * NSUB + v) * RST + lane] = 0.0;
+        s_sub[(ch * NSUB + v) * RST + lane + 32] = 0.0;
+      }
+      __syncwarp();
       double psi[NCH];
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch)
