@@ -14,9 +14,10 @@
 //               coarse (n/S)^2 grid; a 2-D inclusive prefix gives all fully-dominated cells;
 //      level 2: the query's own chunk and own block are solved inside one CTA each: the
 //               <= 2048 sources are laid out in shared memory by local slot / local rank, a
-//               64x64 sub-grid prefix covers full sub-cells, and <= 2 x 31 direct checks finish.
+//               64x64 grid of cell sums (prefixed per code direction) covers full cells, and the
+//               <= 2 x 32 sources of the query's slot cell and threshold rank cells finish.
 //    The four sign codes of the KDE (dnc.py:459-468) are the four orientations of the same
-//    problem (flip p0 and/or p1), sharing one ranking and one chunk/block grouping.
+//    problem, sharing one ranking, one chunk/block grouping and (self path) one near-field pass.
 //  * rank-space dominance, 3 <= d <= 6 (points_nd.cuh): a coarse G^d grid of rank chunks for the
 //    far field and one slab phase per dimension for the sources sharing a chunk with the query.
 //  * direct O(n^2) tiles (d >= 7, or fewer than 8192 points).
