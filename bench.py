@@ -530,8 +530,8 @@ class PointsWorkload:
             return (f"query shards x{world}: sources ranked on every GPU (replicated), queries "
                     f"split by dimension-1 rank chunks, one NCCL SUM all-reduce gathers the "
                     f"numerators")
-        return (f"replicas x{world}: the rank-lattice route is not sharded, every GPU computes "
-                f"the whole problem (counted once)")
+        return (f"replicas x{world}: this route (rank lattice / d >= 3 rank grid) is not sharded, "
+                f"every GPU computes the whole problem (counted once)")
 
     def __init__(self, name):
         import paper_2005_03246_b200 as fcb
