@@ -151,3 +151,20 @@ def test_nd_kde_dnc_matern32_vs_oracle(d, n, oracle):
     ref = oracle.kde_naive_matern32(x, w, x[q], h)
     scale = oracle.kde_naive_matern32(x, np.abs(w), x[q], h)
     assert rel_err(got[q], ref, scale) <= 1e-9
+
+
+@pytest.mark.slow
+def test_nd_large_chunks(oracle):
+    """d = 3 at 1.5e6 points: the cost model picks 2048- / 4096-rank chunks (several source
+    tiles per chunk, triangular tile ranges); counts bit-exact, KDE to 1e-9, on a query subset."""
+    rng = np.random.default_rng(77)
+    n, d = 1_500_000, 3
+    x = rng.standard_normal((n, d))
+    q = rng.integers(0, n, 300)
+    got = fcb.ecdf_dnc(fcb.validate_sample(x), scaled=False).values
+    np.testing.assert_array_equal(got[q], oracle.ecdf_naive(x, None, x[q], (-1,) * d, scaled=False))
+    w = rng.uniform(0.5, 2.0, n)
+    h = [0.2, 0.25, 0.3]
+    got = fcb.kde_dnc(fcb.validate_sample(x, w), fcb.laplacian(), fcb.Bandwidth.diag(h)).values
+    ref = oracle.kde_naive_laplacian(x, w, x[q], h)
+    assert rel_err(got[q], ref) <= 1e-9
