@@ -957,13 +957,34 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
   // full-space leading indices of this CTA's plane, and each group's output plane
   constexpr int NL = NG == 4 ? 2 : 1;  // leading axes (t.nlead = log2 NG)
   int64_t fidx[NL];
-  {
-    int64_t rem = blockIdx.x;
-#pragma unroll
-    for (int k = NL - 1; k >= 0; --k) {
-      fidx[k] = rem % (t.lead_m[k] + 1);
-      rem /= t.lead_m[k] + 1;
+  // Launch order: interior planes first, the boundary planes (first / last index along a leading
+  // axis: fewer valid groups, the last layer holds no records) at the end, so the kernel's tail
+  // is made of its cheapest CTAs.
+  if (NL == 2) {
+    const int64_t n0 = t.lead_m[0] + 1, n1 = t.lead_m[1] + 1;
+    const int64_t ni = (n0 - 2) * (n1 - 2);
+    int64_t e = blockIdx.x;
+    if (n0 < 3 || n1 < 3) {
+      fidx[0] = e / n1;
+      fidx[NL - 1] = e % n1;
+    } else if (e < ni) {
+      fidx[0] = 1 + e / (n1 - 2);
+      fidx[NL - 1] = 1 + e % (n1 - 2);
+    } else {
+      e -= ni;
+      if (e < 2 * n1) {  // the first and the last row
+        fidx[0] = e < n1 ? 0 : n0 - 1;
+        fidx[NL - 1] = e % n1;
+      } else {           // the first and the last column of the rows between
+        e -= 2 * n1;
+        fidx[0] = 1 + e / 2;
+        fidx[NL - 1] = (e & 1) ? n1 - 1 : 0;
+      }
     }
+  } else {
+    const int64_t n0 = t.lead_m[0] + 1;
+    const int64_t e = blockIdx.x;
+    fidx[0] = n0 < 3 ? e : (e < n0 - 2 ? 1 + e : (e == n0 - 2 ? 0 : n0 - 1));
   }
   unsigned vmask = 0;
   int64_t oplane[NG];
@@ -981,7 +1002,9 @@ __global__ void __launch_bounds__(kAllThreads, 4) plane_kde_all_kernel(
     if (ok) vmask |= 1u << g;
   }
   if (vmask == 0) return;  // uniform
-  const int64_t fplane = blockIdx.x;
+  int64_t fplane = 0;
+#pragma unroll
+  for (int k = 0; k < NL; ++k) fplane = fplane * (t.lead_m[k] + 1) + fidx[k];
   tile_zero<double>(tiles, 2 * NG * TS);
   const uint32_t cmask = (1u << t.col_bits) - 1u, rmask = (1u << (t.cell_bits - t.col_bits)) - 1u;
   // walk ownership: lane l holds the column pairs (2 l, 2 l + 1) + 64 j, j < C, so a warp's
