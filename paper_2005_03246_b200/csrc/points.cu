@@ -1607,8 +1607,8 @@ int rank_dim(const double *x, int64_t n, int d, int k, PtsWs &p, cudaStream_t st
     // equal top halves by the low halves (falls through when a run is too long)
     bool done = false;
     FCG_TRY(rank_order_split_f64(x + k, n, d, mask, reinterpret_cast<uint32_t *>(p.k), p.v, p.rw,
-                                 p.ndist + k, p.r[k].order, &done, st));
-    if (done) return pos_from_order(p.r[k].order, n, p.r[k].pos, st);
+                                 p.ndist + k, p.r[k].order, p.r[k].pos, &done, st));
+    if (done) return FCG_OK;
   }
   FCG_TRY(radix_init_f64(x + k, n, d, p.k, p.v, st));
   if (mask == ~0u) FCG_TRY(radix_sort_pairs_pruned(p.k, p.v, n, p.rw, st));

@@ -647,7 +647,8 @@ __global__ void tie_low_kernel(const double *__restrict__ x, int64_t stride,
 
 __global__ void tie_rank_kernel(const uint32_t *__restrict__ keys, const uint32_t *__restrict__ low,
                                 const int32_t *__restrict__ vals, int64_t n,
-                                int32_t *__restrict__ order, int32_t *__restrict__ flag) {
+                                int32_t *__restrict__ order, int32_t *__restrict__ pos,
+                                int32_t *__restrict__ flag) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t k = keys[p];
@@ -671,6 +672,7 @@ __global__ void tie_rank_kernel(const uint32_t *__restrict__ keys, const uint32_
       if (fwd == kTieRun) *flag = 1;
     }
     order[p - back + before] = me;
+    if (pos) pos[me] = (int32_t)(p - back + before);
   }
 }
 
@@ -683,7 +685,7 @@ __global__ void pos_from_order_kernel(const int32_t *__restrict__ order, int64_t
 
 int rank_order_split_f64(const double *x, int64_t n, int64_t stride, uint32_t mask,
                          uint32_t *keys32, int32_t *vals, const RadixWs &ws, int32_t *flag_dev,
-                         int32_t *order, bool *done, cudaStream_t st) {
+                         int32_t *order, int32_t *pos, bool *done, cudaStream_t st) {
   *done = false;
   if (n <= 1) return FCG_OK;
   {
@@ -697,7 +699,8 @@ int rank_order_split_f64(const double *x, int64_t n, int64_t stride, uint32_t ma
     FCG_PROF("rank_tie_fix", st);
     uint32_t *low = reinterpret_cast<uint32_t *>(ws.keys_alt);  // free after the in-place sort
     tie_low_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(x, stride, keys32, vals, n, low);
-    tie_rank_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(keys32, low, vals, n, order, flag_dev);
+    tie_rank_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(keys32, low, vals, n, order, pos,
+                                                         flag_dev);
     FCG_LAUNCH_CHECK();
   }
   int32_t h = 0;
