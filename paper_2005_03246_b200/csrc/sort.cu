@@ -676,13 +676,6 @@ __global__ void tie_rank_kernel(const uint32_t *__restrict__ keys, const uint32_
   }
 }
 
-__global__ void pos_from_order_kernel(const int32_t *__restrict__ order, int64_t n,
-                                      int32_t *__restrict__ pos) {
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
-       p += (int64_t)gridDim.x * blockDim.x)
-    pos[order[p]] = (int32_t)p;
-}
-
 int rank_order_split_f64(const double *x, int64_t n, int64_t stride, uint32_t mask,
                          uint32_t *keys32, int32_t *vals, const RadixWs &ws, int32_t *flag_dev,
                          int32_t *order, int32_t *pos, bool *done, cudaStream_t st) {
@@ -706,14 +699,6 @@ int rank_order_split_f64(const double *x, int64_t n, int64_t stride, uint32_t ma
   int32_t h = 0;
   FCG_TRY(read_small(&h, flag_dev, 4, st));
   *done = h == 0;
-  return FCG_OK;
-}
-
-int pos_from_order(const int32_t *order, int64_t n, int32_t *pos, cudaStream_t st) {
-  if (n <= 0) return FCG_OK;
-  FCG_PROF("rank_heads", st);
-  pos_from_order_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(order, n, pos);
-  FCG_LAUNCH_CHECK();
   return FCG_OK;
 }
 

@@ -79,8 +79,6 @@ int radix_sort_pairs_pruned(uint64_t *keys, int32_t *vals, int64_t n, const Radi
 int rank_order_split_f64(const double *x, int64_t n, int64_t stride, uint32_t mask,
                          uint32_t *keys32, int32_t *vals, const RadixWs &ws, int32_t *flag_dev,
                          int32_t *order, int32_t *pos, bool *done, cudaStream_t st);
-// pos[order[p]] = p
-int pos_from_order(const int32_t *order, int64_t n, int32_t *pos, cudaStream_t st);
 
 // Exclusive (or inclusive) prefix sum of int32 (in and out may alias). partial: scan ws.
 int scan_i32(const int32_t *in, int32_t *out, int64_t n, bool inclusive, int32_t *partial,
