@@ -72,7 +72,12 @@ inline NdPlan nd_plan(int64_t n, int d, int nch, int ncodes, bool kde) {
   return best;
 }
 
-inline bool nd_route(int64_t n, int d) { return d >= 3 && d <= 6 && n >= kNdMinN; }
+// FCG_ND=off sends every d >= 3 request to the direct tiles (cross-checks in the tests)
+inline bool nd_route(int64_t n, int d) {
+  const char *e = getenv("FCG_ND");
+  if (e && std::string(e) == "off") return false;
+  return d >= 3 && d <= 6 && n >= kNdMinN;
+}
 
 struct DomN {
   int64_t n, G, NP, cells;

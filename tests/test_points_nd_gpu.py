@@ -168,3 +168,45 @@ def test_nd_large_chunks(oracle):
     got = fcb.kde_dnc(fcb.validate_sample(x, w), fcb.laplacian(), fcb.Bandwidth.diag(h)).values
     ref = oracle.kde_naive_laplacian(x, w, x[q], h)
     assert rel_err(got[q], ref) <= 1e-9
+
+
+def test_nd_route_vs_direct_tiles_random_shapes(monkeypatch):
+    """Random shapes, tie patterns, deltas and weights: the rank-space route against the direct
+    O(n^2) tiles of the same library (FCG_ND=off), on the device for every query."""
+    from paper_2005_03246_b200 import _lib
+
+    rng = np.random.default_rng(2024)
+    for trial in range(14):
+        d = int(rng.integers(3, 7))
+        n = int(rng.integers(8192, 30_000))
+        x = rng.standard_normal((n, d))
+        mode = trial % 4
+        if mode == 1:    # heavy ties in one dimension, light ties in another
+            x[:, 0] = rng.integers(0, 5, n)
+            x[:, d - 1] = np.round(x[:, d - 1], 1)
+        elif mode == 2:  # lattice-valued but too many levels for the rank lattice
+            x = np.floor(rng.random((n, d)) * 200) / 200
+        elif mode == 3:  # a tight cluster plus outliers
+            x[: n // 2] = 1e-3 * x[: n // 2]
+        w = rng.integers(1, 9, n).astype(float)
+        delta = tuple(int(v) for v in rng.choice([-1, 1], d))
+        s = fcb.validate_sample(x, w)
+        monkeypatch.delenv("FCG_ND", raising=False)
+        _lib.profile_enable(True)
+        e1, f1 = fcb.ecdf_esf_at_points(s, fcb.DeltaVector(delta), scaled=False)
+        assert "pts_nd_near" in _lib.profile_report()
+        monkeypatch.setenv("FCG_ND", "off")
+        e0, f0 = fcb.ecdf_esf_at_points(s, fcb.DeltaVector(delta), scaled=False)
+        rep = _lib.profile_report()
+        _lib.profile_enable(False)
+        assert "pts_brute" in rep and "pts_nd_near" not in rep
+        np.testing.assert_array_equal(e1.values, e0.values, err_msg=f"trial {trial} d={d} n={n}")
+        np.testing.assert_array_equal(f1.values, f0.values, err_msg=f"trial {trial} d={d} n={n}")
+        if mode in (0, 3):  # distinct coordinates: the KDE at the points as well
+            h = rng.uniform(0.3, 0.9, d)
+            monkeypatch.delenv("FCG_ND", raising=False)
+            k1 = fcb.kde_dnc(s, fcb.laplacian(), fcb.Bandwidth.diag(h)).values
+            monkeypatch.setenv("FCG_ND", "off")
+            k0 = fcb.kde_dnc(s, fcb.laplacian(), fcb.Bandwidth.diag(h)).values
+            assert rel_err(k1, k0) <= 1e-10, (trial, d, n)
+    monkeypatch.delenv("FCG_ND", raising=False)
