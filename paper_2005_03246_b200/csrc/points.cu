@@ -1826,7 +1826,7 @@ int self_dom2d(const double *x, WPtr w, int64_t n, int nw, int kde, const double
   D.c_lo = P * shard / nshards;
   D.c_hi = P * (shard + 1) / nshards;
   const unsigned nchunk = (unsigned)(D.c_hi - D.c_lo);
-  static const bool direct = [] {  // FCG_LEVEL2=codes: the per-code masked passes (A/B runs)
+  const bool direct = [] {  // FCG_LEVEL2=codes: the per-code masked passes (A/B runs, tests)
     const char *e = getenv("FCG_LEVEL2");
     return !(e && std::string(e) == "codes");
   }();

@@ -490,3 +490,43 @@ def test_level2_correlated_layouts(case, oracle):
     ref = oracle.kde_naive_laplacian(x, ws, x[q], h)
     scale = oracle.kde_naive_laplacian(x, np.abs(ws), x[q], h)
     assert rel_err(got[q], ref, scale) <= 1e-9
+
+
+def test_level2_direct_vs_masked_passes_random(monkeypatch):
+    """The direct level-2 kernels against the per-code masked passes they replaced
+    (FCG_LEVEL2=codes) on random sizes (ragged last groups), layouts and weights: counts
+    bit-exact, KDE numerators (one and two weight vectors, signed) to 1e-11 of the |w| scale."""
+    from paper_2005_03246_b200 import points as pts
+
+    rng = np.random.default_rng(99)
+    for trial in range(12):
+        n = int(rng.integers(1, 60_000)) if trial else 2049
+        x = rng.standard_normal((n, 2))
+        if trial % 3 == 1:
+            x[: n // 2] = 0.5 + 1e-5 * x[: n // 2]
+        elif trial % 3 == 2:
+            x[:, 1] = x[:, 0] * (1.0 if trial % 2 else -1.0) + 1e-6 * x[:, 1]
+        w = rng.integers(1, 9, n).astype(float)
+        y = rng.standard_normal(n)
+        h = rng.uniform(0.05, 0.5, 2)
+        s = fcb.validate_sample(x, w)
+        out = {}
+        for mode in ("direct", "codes"):
+            if mode == "codes":
+                monkeypatch.setenv("FCG_LEVEL2", "codes")
+            else:
+                monkeypatch.delenv("FCG_LEVEL2", raising=False)
+            out[mode] = (fcb.ecdf_dnc(s, scaled=False).values,
+                         fcb.kde_dnc(fcb.validate_sample(x, y), fcb.laplacian(),
+                                     fcb.Bandwidth.diag(h)).values,
+                         [np.asarray(v) for v in pts.kde_numerators(
+                             fcb.validate_sample(x), [None, y], fcb.Bandwidth.diag(h))],
+                         fcb.kde_dnc(fcb.validate_sample(x, np.abs(y)), fcb.laplacian(),
+                                     fcb.Bandwidth.diag(h)).values)
+        monkeypatch.delenv("FCG_LEVEL2", raising=False)
+        a, b = out["direct"], out["codes"]
+        np.testing.assert_array_equal(a[0], b[0], err_msg=f"trial {trial} n={n}")
+        scale = np.maximum(b[3], np.finfo(float).tiny)
+        assert np.max(np.abs(a[1] - b[1]) / scale) <= 1e-11, (trial, n)
+        assert rel_err(a[2][0], b[2][0]) <= 1e-11, (trial, n)
+        assert np.max(np.abs(a[2][1] - b[2][1]) / scale) <= 1e-11, (trial, n)
