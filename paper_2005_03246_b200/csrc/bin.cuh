@@ -30,12 +30,20 @@ struct PsiParams {  // psi_i = w_i * exp(sum_k (x_ik - c_k) * a_k), a_k = delta_
 // The mesh guess (exact for uniform grids except right at knots) is verified against the
 // uploaded knot values and nudged once; anything farther off falls back to binary search, so
 // the result is the exact count for any rectilinear grid.
+//
+// mesh_ok: the knots were checked to lie within kMeshTol mesh steps of z0 + j dz (mesh_uniform
+// below).  Then a point whose mesh coordinate t is farther than kMeshSafe from every integer is
+// on the same side of the nearest knots as of the mesh lines (t itself is off by < 1e-13 for
+// m <= 2^20), so the guess is the exact count and the knot loads and compares are skipped.
+constexpr double kMeshTol = 1e-9, kMeshSafe = 1e-6;
+
 __device__ __forceinline__ int knot_count(double x, const double *kn, int m, int le, double z0,
-                                          double inv_dz) {
+                                          double inv_dz, bool mesh_ok = false) {
   const double t = (x - z0) * inv_dz;
   // floor(t) + 1 (le) or ceil(t), clamped to [0, m]: the conversions saturate (NaN -> 0)
   const int f = le ? __double2int_rd(t) : __double2int_ru(t - 1.0);
   const int g = min(max(f, -1), m - 1) + 1;
+  if (mesh_ok && fabs(t - rint(t)) > kMeshSafe) return g;  // NaN: falls through
   // pred(k) := knot k counts (kn[k] < x, or <= x when le); valid iff pred(g-1) && !pred(g)
   const double a = kn[g > 0 ? g - 1 : 0], b = kn[g < m ? g : m - 1];
   const bool lo_ok = (g == 0) || a < x || (le && a == x);
@@ -53,6 +61,22 @@ __device__ __forceinline__ int knot_count(double x, const double *kn, int m, int
     else hi = mid;
   }
   return lo;
+}
+
+// Bit k set when dimension k's knots follow the mesh z0 + j dz to kMeshTol steps.  Call from
+// every thread of the CTA after stage_knots' barrier (contains barriers).
+__device__ __forceinline__ unsigned mesh_uniform(const BinGrid &g, const double *kb,
+                                                 const double *s_z0, const double *s_idz) {
+  unsigned mask = 0;
+  for (int k = 0; k < g.d; ++k) {
+    const double *kn = kb + g.koff[k];
+    bool ok = true;
+    for (int64_t j = threadIdx.x; j < g.m[k]; j += blockDim.x)
+      ok = ok && fabs((kn[j] - s_z0[k]) * s_idz[k] - (double)j) <= kMeshTol;
+    if (g.m[k] > (int64_t(1) << 20)) ok = false;
+    if (__syncthreads_and(ok)) mask |= 1u << k;
+  }
+  return mask;
 }
 
 inline BinGrid make_bin_grid(int d, const int64_t *m, const int *le, const int64_t *shift,

@@ -50,7 +50,7 @@ template <int D, int LEU = 2>
 __device__ __forceinline__ void part_key(const double *xi, int d, const double *kb, const BinGrid &g,
                                          const double *s_z0, const double *s_idz,
                                          const PartGeo &p, int64_t i, uint32_t &key,
-                                         int32_t &val) {
+                                         int32_t &val, unsigned mesh = 0u) {
   uint32_t plane = 0;
   int row = 0, col = 0;
   bool live = true;
@@ -58,7 +58,7 @@ __device__ __forceinline__ void part_key(const double *xi, int d, const double *
   for (int k = 0; k < (D > 0 ? D : FCG_MAX_DIM); ++k) {
     if (k < d) {
       const int c = knot_count(xi[k], kb + g.koff[k], (int)g.m[k], LEU == 2 ? g.le[k] : LEU,
-                               s_z0[k], s_idz[k]) -
+                               s_z0[k], s_idz[k], (mesh >> k) & 1u) -
                     (int)p.shift[k];
       live = live && c >= 0 && c < (int)p.E[k];
       if (k < d - 2) plane = plane * (uint32_t)p.E[k] + (uint32_t)c;
@@ -1892,6 +1892,8 @@ __global__ void __launch_bounds__(256, D == 3 || D == 4 ? 4 : 1) part_bin_tile_k
   for (int i = threadIdx.x & 31; i < 256; i += 32) s_hist[warp][i] = 0;
   const double *kb = stage_knots(g, knots, s_knots, s_z0, s_idz);
   __syncthreads();
+  // uniform axes: points away from the mesh lines skip the knot verification
+  const unsigned mesh = g.total_knots <= kSmemKnots ? mesh_uniform(g, kb, s_z0, s_idz) : 0u;
   constexpr int DD = D > 0 ? D : FCG_MAX_DIM;
   const int64_t tile0 = (int64_t)blockIdx.x * tile;
   constexpr int U = 2;  // points in flight per thread
@@ -1924,7 +1926,7 @@ __global__ void __launch_bounds__(256, D == 3 || D == 4 ? 4 : 1) part_bin_tile_k
       if (i >= n) continue;
       uint32_t key;
       int32_t val;
-      part_key<D, LEU>(xi[u], d, kb, g, s_z0, s_idz, p, i, key, val);
+      part_key<D, LEU>(xi[u], d, kb, g, s_z0, s_idz, p, i, key, val, mesh);
       keys[i] = key;
       if (vals) vals[i] = val;
       atomicAdd(&s_hist[warp][(key >> hshift) & 0xFFu], 1);
