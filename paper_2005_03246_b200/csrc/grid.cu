@@ -54,6 +54,8 @@ __global__ void __launch_bounds__(256, 4) bin_scatter_kernel(const double *__res
   }
   __syncthreads();
   const double *kb = use_smem ? s_knots : knots;
+  // uniform axes: points away from the mesh lines skip the knot verification (bin.cuh)
+  const unsigned mesh = use_smem ? mesh_uniform(g, kb, s_z0, s_idz) : 0u;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double xi[D > 0 ? D : FCG_MAX_DIM];
@@ -75,7 +77,8 @@ __global__ void __launch_bounds__(256, 4) bin_scatter_kernel(const double *__res
 #pragma unroll
     for (int k = 0; k < (D > 0 ? D : FCG_MAX_DIM); ++k) {
       if (k < d) {
-        const int64_t b = knot_count(xi[k], kb + g.koff[k], (int)g.m[k], g.le[k], s_z0[k], s_idz[k]);
+        const int64_t b = knot_count(xi[k], kb + g.koff[k], (int)g.m[k], g.le[k], s_z0[k], s_idz[k],
+                                     (mesh >> k) & 1u);
         const int64_t cell = b - g.shift[k];
         live = live && (cell >= 0) && (cell < g.dims[k]);
         flat += cell * g.stride[k];
