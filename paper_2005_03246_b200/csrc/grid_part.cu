@@ -54,12 +54,35 @@ __device__ __forceinline__ void part_key(const double *xi, int d, const double *
   uint32_t plane = 0;
   int row = 0, col = 0;
   bool live = true;
+  constexpr int DD = D > 0 ? D : FCG_MAX_DIM;
+  int cnt[DD];
+  bool counted = false;
+  if (D > 0 && mesh == (1u << D) - 1u) {
+    // every axis follows its mesh (CTA-uniform): the mesh counts of all axes first, ONE test
+    // whether the point is clear of every mesh line (bin.cuh: then they are the exact counts);
+    // the rare point near a line takes the verified counts below
+    bool safe = true;
 #pragma unroll
-  for (int k = 0; k < (D > 0 ? D : FCG_MAX_DIM); ++k) {
+    for (int k = 0; k < DD; ++k) {
+      const int le = LEU == 2 ? g.le[k] : LEU;
+      const double t = (xi[k] - s_z0[k]) * s_idz[k];
+      const int f = le ? __double2int_rd(t) : __double2int_ru(t - 1.0);
+      cnt[k] = min(max(f, -1), (int)g.m[k] - 1) + 1;
+      safe = safe && fabs(t - rint(t)) > kMeshSafe;  // NaN: not safe
+    }
+    counted = safe;
+  }
+  if (!counted) {
+#pragma unroll
+    for (int k = 0; k < DD; ++k)
+      if (k < d)
+        cnt[k] = knot_count(xi[k], kb + g.koff[k], (int)g.m[k], LEU == 2 ? g.le[k] : LEU,
+                            s_z0[k], s_idz[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < DD; ++k) {
     if (k < d) {
-      const int c = knot_count(xi[k], kb + g.koff[k], (int)g.m[k], LEU == 2 ? g.le[k] : LEU,
-                               s_z0[k], s_idz[k], (mesh >> k) & 1u) -
-                    (int)p.shift[k];
+      const int c = cnt[k] - (int)p.shift[k];
       live = live && c >= 0 && c < (int)p.E[k];
       if (k < d - 2) plane = plane * (uint32_t)p.E[k] + (uint32_t)c;
       else if (k == d - 2) row = c;
