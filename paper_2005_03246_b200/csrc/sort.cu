@@ -622,10 +622,13 @@ int radix_digit_masks_f64(const double *x, int64_t n, int d, unsigned long long 
 constexpr int kTieRun = 48;  // longest run of equal top halves ordered in place
 
 __global__ void radix_init_hi32_kernel(const double *__restrict__ x, int64_t n, int64_t stride,
-                                       uint32_t *__restrict__ keys, int32_t *__restrict__ vals) {
+                                       uint32_t *__restrict__ keys, uint32_t *__restrict__ lows,
+                                       int32_t *__restrict__ vals) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    keys[i] = (uint32_t)(f64_key(x[i * stride]) >> 32);
+    const uint64_t k = f64_key(x[i * stride]);
+    keys[i] = (uint32_t)(k >> 32);
+    lows[i] = (uint32_t)k;  // by item: 4 n bytes, L2-resident for the tie pass's gathers
     vals[i] = (int32_t)i;
   }
 }
@@ -634,14 +637,14 @@ __global__ void radix_init_hi32_kernel(const double *__restrict__ x, int64_t n, 
 // in (low half, index) order.  First the low halves of the run members are gathered next to
 // their keys; then every member counts the members of its run that precede it and writes its
 // index to that slot of `order` (singletons copy).  Runs longer than kTieRun raise *flag.
-__global__ void tie_low_kernel(const double *__restrict__ x, int64_t stride,
+__global__ void tie_low_kernel(const uint32_t *__restrict__ lows,
                                const uint32_t *__restrict__ keys, const int32_t *__restrict__ vals,
                                int64_t n, uint32_t *__restrict__ low) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t k = keys[p];
     const bool in_run = (p > 0 && keys[p - 1] == k) || (p + 1 < n && keys[p + 1] == k);
-    if (in_run) low[p] = (uint32_t)f64_key(x[(int64_t)vals[p] * stride]);
+    if (in_run) low[p] = lows[vals[p]];
   }
 }
 
@@ -684,14 +687,15 @@ int rank_order_split_f64(const double *x, int64_t n, int64_t stride, uint32_t ma
   {
     FCG_PROF("radix_init", st);
     FCG_CUDA_TRY(cudaMemsetAsync(flag_dev, 0, 4, st));
-    radix_init_hi32_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(x, n, stride, keys32, vals);
+    radix_init_hi32_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(x, n, stride, keys32, keys32 + n,
+                                                                vals);
     FCG_LAUNCH_CHECK();
   }
   FCG_TRY(radix_sort_digits<uint32_t>(keys32, vals, n, (mask >> 4) & 0xFu, ws, st));
   {
     FCG_PROF("rank_tie_fix", st);
     uint32_t *low = reinterpret_cast<uint32_t *>(ws.keys_alt);  // free after the in-place sort
-    tie_low_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(x, stride, keys32, vals, n, low);
+    tie_low_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(keys32 + n, keys32, vals, n, low);
     tie_rank_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(keys32, low, vals, n, order, pos,
                                                          flag_dev);
     FCG_LAUNCH_CHECK();

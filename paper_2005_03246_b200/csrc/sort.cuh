@@ -73,9 +73,10 @@ int radix_sort_pairs_pruned(uint64_t *keys, int32_t *vals, int64_t n, const Radi
 // order keys (at most 4 passes over 8-byte items instead of 8 over 12-byte ones), then every
 // member of a run of equal top halves takes its (low half, index) place inside the run.  `order`
 // receives the stable order (and pos, when given, its inverse); *done = false when a run is
-// longer than the limit (near-duplicates by the million): the caller then sorts the full keys.  keys32: n words (may alias the 64-bit
-// key buffer); vals: n words of scratch; flag_dev: one device word.  mask from
-// radix_digit_masks_f64.  Synchronises `st`.
+// longer than the limit (near-duplicates by the million): the caller then sorts the full keys.
+// keys32: 2 n words (the 64-bit key buffer: top halves, then the low halves by item); vals: n
+// words of scratch; flag_dev: one device word.  mask from radix_digit_masks_f64.  Synchronises
+// `st`.
 int rank_order_split_f64(const double *x, int64_t n, int64_t stride, uint32_t mask,
                          uint32_t *keys32, int32_t *vals, const RadixWs &ws, int32_t *flag_dev,
                          int32_t *order, int32_t *pos, bool *done, cudaStream_t st);
